@@ -1,0 +1,174 @@
+/*
+ * helmdef_b200.h -- C-ABI drop-in for the reference's hot path
+ *
+ *   SolverSetup compose(const DiscreteSystem&, const PrecondSpec&)   inc/precond.hpp:149
+ *   GmresResult gmres(op, rhs, start, monitor, const GmresOptions&)   inc/linalg.hpp:41-42
+ *
+ * called as a pair from run_cell (src/harness.cpp:222-224).  The pair is
+ * replaced as one unit: the reference's LinearOp/ResidualFn closures map host
+ * Eigen vectors to host Eigen vectors (inc/linalg.hpp:17, 22), so replacing
+ * only the closure would force two host<->device copies per operator call.
+ * hd_create() does what compose() does at setup (Galerkin multigrid
+ * hierarchy, deflation matrix E = Z^T A Z and its exact solver, device
+ * buffers); hd_solve() runs the transformed right-hand side, start vector,
+ * unrestarted left-preconditioned GMRES with the true-residual monitor and
+ * returns the reference's GmresResult fields plus OperationCounts.
+ *
+ * Plain C: pointers and sizes only, no CUDA or torch types.  Complex vectors
+ * are interleaved (re, im) doubles, the layout of Eigen::VectorXcd; 2D index
+ * iy*per_dim + ix (x fastest), the reference's kron(outer=y, inner=x) layout
+ * (inc/assembly.hpp:37, src/assembly.cpp:255).
+ *
+ * Errors: a non-zero hd_status; hd_last_error() returns the thread-local
+ * message.  This replaces the reference's std::runtime_error on LU failure or
+ * zero smoother diagonal (src/linalg.cpp:98-99, src/precond.cpp:98-99, 128);
+ * non-convergence is not an error (converged = 0), as in the reference.
+ *
+ * Threading: one hd_ctx is used by one host thread at a time; distinct
+ * contexts may run concurrently (each owns its stream), mirroring the
+ * reference's per-cell ownership in the sweep pool (src/harness.cpp:281-307).
+ */
+#ifndef HELMDEF_B200_H
+#define HELMDEF_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HD_OK = 0,
+  HD_ERR_INVALID = 1,     /* bad argument / unsupported combination        */
+  HD_ERR_CUDA = 2,        /* CUDA runtime / cuBLAS / cuSOLVER failure       */
+  HD_ERR_FACTOR = 3,      /* singular coarse operator or zero diagonal      */
+  HD_ERR_NO_DEVICE = 4    /* no CUDA device: there is no CPU fallback       */
+} hd_status;
+
+/* Wave-number field kinds (WaveField, inc/problems.hpp:18-29). */
+enum { HD_FIELD_CONSTANT = 0, HD_FIELD_LAYERED = 1 };
+
+/* Model problem (helmdef::Problem, inc/problems.hpp:50-60) restricted to the
+ * iteration-study problems: point_source_1d / point_source_2d /
+ * layered_medium_2d (src/problems.cpp:45-74). */
+typedef struct {
+  int dim;              /* 1 or 2                                             */
+  int order;            /* B-spline degree p                                  */
+  int elements;         /* elements per direction                            */
+  double k;             /* base wave number                                  */
+  int field_kind;       /* HD_FIELD_*                                         */
+  double multipliers[16]; /* layered: block(bx,by) = multipliers[4*by+bx]     */
+} hd_problem;
+
+/* Discrete system as the device consumes it (DiscreteSystem,
+ * inc/assembly.hpp:43-52, in factored form).  For dim = 2,
+ *   A      = kron(M1, S1) + kron(S1, M1) - K2,
+ *   K2     = k^2 kron(M1, M1)                          (constant field)
+ *          = sum_{by,bx} (k m_{by,bx})^2 kron(B_by, B_bx) (layered field),
+ * for dim = 1, A = S1 - k^2 M1 (+ corner at (n-1, n-1)).  Bands are reduced
+ * (Dirichlet rows dropped), per_dim x (2*order+1), row-major,
+ * band[i*(2p+1) + (j-i+p)] = X(i, j). */
+typedef struct {
+  int dim;
+  int order;
+  int elements;
+  int per_dim;
+  int field_kind;
+  double k;
+  double multipliers[16];
+  const double* stiffness_band;   /* S1                                    */
+  const double* mass_band;        /* M1                                    */
+  const double* interval_mass;    /* layered: 4 bands B_0..B_3 (else NULL)  */
+  double corner_re, corner_im;    /* 1D only: added to A(n-1,n-1)          */
+} hd_system;
+
+/* PrecondSpec (inc/precond.hpp:122-130) plus MultigridOptions::coarsest
+ * (inc/precond.hpp:57-61). */
+typedef struct {
+  int deflate;
+  double drop;
+  int shift;
+  double beta2;
+  int cycles;          /* >= 1: multigrid V-cycles; 0: exact shifted inverse (unsupported here) */
+  int smooth_steps;
+  double omega;
+  int coarsest;        /* per-dimension size solved directly (reference: 32) */
+} hd_precond;
+
+/* GmresOptions (inc/linalg.hpp:24-27). */
+typedef struct {
+  int max_iterations;
+  double tolerance;
+} hd_gmres;
+
+/* GmresResult scalars (inc/linalg.hpp:29-34) + OperationCounts
+ * (inc/precond.hpp:114-119) + timings. */
+typedef struct {
+  int iterations;
+  int converged;
+  long matvecs;
+  long coarse_solves;
+  long shift_solves;
+  long vcycles;
+  double t_setup_s;    /* hd_create: device hierarchy + factorisations        */
+  double t_solve_s;    /* hd_solve: CUDA-event time of the whole solve          */
+  int kernel_launches; /* device kernels launched by the last hd_solve          */
+} hd_report;
+
+typedef struct hd_ctx hd_ctx;
+
+/* ---- host assembly (mirrors src/assembly.cpp; not accelerated) ---------- */
+
+/* Retained basis functions per direction (src/assembly.cpp:174-184). */
+int hd_problem_per_dim(const hd_problem* pb);
+
+/* Assemble the reduced 1D factors and the point-source load vector
+ * (src/assembly.cpp:163-258).  stiffness_band / mass_band: per_dim*(2p+1);
+ * interval_mass: 4*per_dim*(2p+1) for layered fields (may be NULL otherwise);
+ * rhs: 2*per_dim^dim doubles (interleaved complex). */
+hd_status hd_assemble(const hd_problem* pb, double* stiffness_band, double* mass_band,
+                      double* interval_mass, double* rhs);
+
+/* ---- the drop-in solver ------------------------------------------------ */
+
+/* compose(): build the preconditioner on device(s).  devices/n_devices: the
+ * CUDA devices to use (NULL/0 = current device); n_devices > 1 is reserved
+ * for the row-slab decomposition and is rejected in this build. */
+hd_status hd_create(const hd_system* sys, const hd_precond* spec, const int* devices,
+                    int n_devices, hd_ctx** out);
+
+/* gmres(compose(...)): host buffers.  rhs: 2N doubles; x_out: 2N doubles;
+ * residuals_out: max_iterations (+1) doubles (may be NULL).  Includes the
+ * host->device copy of rhs and the device->host copy of x. */
+hd_status hd_solve(hd_ctx* ctx, const hd_gmres* opt, const double* rhs, double* x_out,
+                   double* residuals_out, hd_report* report);
+
+/* Same solve with rhs / x already resident in device memory (device
+ * pointers of 2N doubles on the context's device). */
+hd_status hd_solve_device(hd_ctx* ctx, const hd_gmres* opt, const double* d_rhs,
+                          double* d_x, double* residuals_out, hd_report* report);
+
+/* Vector length N (= per_dim^dim) and multigrid level count of a context. */
+long hd_size(const hd_ctx* ctx);
+int hd_levels(const hd_ctx* ctx);
+
+/* Test hooks (device pointers): y = A x (the unshifted operator) and
+ * y = MG^-1 x (c V-cycles of the shifted operator) and y = op(x) (the full
+ * composed left-preconditioned operator, src/precond.cpp:236-245). */
+hd_status hd_apply(hd_ctx* ctx, int which, const double* d_x, double* d_y);
+enum { HD_APPLY_A = 0, HD_APPLY_SHIFTED = 1, HD_APPLY_MG = 2, HD_APPLY_PROJECT = 3, HD_APPLY_OP = 4,
+       HD_APPLY_Q = 5 };
+
+/* Test hook on multigrid level `level` (device pointers, level sizes):
+ *   0: y = M_l x            1: y = omega D_l^-1 x       2: y = x + omega D_l^-1 (x - M_l x)
+ *   3: y = x - M_l x        4: y = Z_l^T x (l -> l+1)   5: y += Z_l x (l+1 -> l)
+ *   6: y = M_L^-1 x (coarsest level exact solve)                                      */
+hd_status hd_debug_level(hd_ctx* ctx, int which, int level, const double* d_x, double* d_y);
+int hd_level_size(const hd_ctx* ctx, int level);
+
+void hd_destroy(hd_ctx* ctx);
+const char* hd_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HELMDEF_B200_H */

@@ -1,0 +1,72 @@
+"""Builds the in-tree sm_100a shared library ``libhelmdef_b200.so``.
+
+nvcc cross-compiles for ``-gencode arch=compute_100a,code=sm_100a`` without a
+GPU, so this runs in the CPU container as the driver's "does it build" check;
+the resulting .so travels to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OUT = PKG / "libhelmdef_b200.so"
+BUILD = PKG / "_build"
+
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include")]
+
+CU_SOURCES = ["solver.cu"]
+CPP_SOURCES = ["host/banded.cpp", "host/assembly.cpp"]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError(f"build failed: {cmd[0]} exited {r.returncode}")
+    return r
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    headers = list(CSRC.rglob("*.cuh")) + list(CSRC.rglob("*.hpp")) + list((ROOT / "include").glob("*.h"))
+    objs = []
+    for src in CU_SOURCES:
+        s = CSRC / src
+        o = BUILD / (Path(src).stem + ".o")
+        if _stale(o, [s] + headers):
+            cmd = [NVCC, *ARCH, *COMMON, "-lineinfo", "-c", str(s), "-o", str(o)]
+            if ptxas_info:
+                cmd.insert(1, "-Xptxas=-v")
+            r = _run(cmd)
+            if verbose or ptxas_info:
+                sys.stderr.write(r.stderr)
+        objs.append(o)
+    for src in CPP_SOURCES:
+        s = CSRC / src
+        o = BUILD / (Path(src).stem + ".cpp.o")
+        if _stale(o, [s] + headers):
+            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)])
+        objs.append(o)
+    if _stale(OUT, objs):
+        _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *map(str, objs), "-o", str(OUT),
+              "-lcublas", "-lcusolver", "-lcudart"])
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(verbose=True, ptxas_info="-v" in sys.argv))

@@ -1,0 +1,557 @@
+// sm_100a kernels of the deflated multigrid-CSLP GMRES path, FP64 complex.
+//
+//   operator apply  k_op2d / k_op1d   A x, b - M x, damped Jacobi, ||f - A x||
+//                                      (reference: every `(*A) * v` / `m * x` of
+//                                      src/precond.cpp:107,140,147,238,262)
+//   transfers       k_restrict* / k_prolong*   Z^T r, x += Z e, w - Z e
+//                                      (linear MG stencil src/precond.cpp:57-76,
+//                                       Bezier deflation stencil :34-55)
+//   Krylov vectors  k_dot / k_axpy_dot / k_axpy_norm / k_iterate / k_givens
+//                                      (src/linalg.cpp:40-90)
+//   exact solvers   k_fd_small / k_fd_scale / k_bandlu_solve
+//                                      (coarsest MG level src/precond.cpp:133,145
+//                                       and deflation E solve :95-104)
+//
+// 2D operators are Kronecker sums of banded 1D factors,
+//   L = My (x) Sx + Sy (x) Mx - c My (x) Mx,
+// applied sum-factorised (x pass, then y pass) from 1D band tables -- the 2D
+// matrix (125 M nonzeros at C5) is never stored or streamed.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace hd {
+
+struct LevelDev {
+  const double* S;  // n x (2b+1) band rows
+  const double* M;
+  int n;
+  int b;
+  double2 c;        // L = ... - c My(x)Mx   (2D)  or  S - c M  (1D)
+  double2 corner;   // 1D only: added to L(n-1, n-1)
+};
+
+struct RedOut {
+  double2* partials;
+  unsigned* counter;
+  double* dst;       // final scalar written by the last block
+  double scale;      // dst = sqrt(sum |.|^2) * scale
+};
+
+enum OpMode { OP_APPLY = 0, OP_RESID = 1, OP_JACOBI = 2, OP_RESNORM = 3 };
+
+constexpr int kTX = 128;  // threads (columns) per stencil CTA
+constexpr int kNS = 8;    // cp.async ring depth (rows in flight per CTA)
+
+// ---------------------------------------------------------------------------
+// 2D stencil: one thread per column, the CTA streams a strip of rows through a
+// cp.async ring in shared memory; the x pass produces P = Sx x - c Mx x and
+// Q = Mx x per row into register queues of depth 2B+1; the y pass combines
+// y = sum_d My(iy,d) P(iy+d) + Sy(iy,d) Q(iy+d).
+// ---------------------------------------------------------------------------
+template <int B, int MODE>
+__global__ void __launch_bounds__(kTX) k_op2d(LevelDev L, const double2* __restrict__ x,
+                                              const double2* __restrict__ bv, double2* __restrict__ out,
+                                              double omega, int RY, RedOut red) {
+  constexpr int NB = 2 * B + 1;
+  constexpr int W = kTX + 2 * B;
+  constexpr bool NEED_B = (MODE != OP_APPLY);
+  __shared__ __align__(16) double2 xs[kNS][W];
+  __shared__ __align__(16) double2 bs[NEED_B ? kNS : 1][kTX];
+  __shared__ double cy[2][64][NB];  // (My, Sy) rows of this strip (RY <= 64)
+  __shared__ double2 scratch[32];
+
+  const int n = L.n;
+  const int t = threadIdx.x;
+  const int x0 = blockIdx.x * kTX;
+  const int y0 = blockIdx.y * RY;
+  const int yend = min(y0 + RY, n);
+  const int nout = yend - y0;
+  const int nin = nout + 2 * B;
+  const int ix = x0 + t;
+  const bool colv = ix < n;
+
+  for (int e = t; e < nout * NB; e += kTX) {
+    const int r = e / NB, d = e % NB;
+    cy[0][r][d] = L.M[(size_t)(y0 + r) * NB + d];
+    cy[1][r][d] = L.S[(size_t)(y0 + r) * NB + d];
+  }
+  double sx[NB], mx[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    sx[j] = colv ? L.S[(size_t)ix * NB + j] : 0.0;
+    mx[j] = colv ? L.M[(size_t)ix * NB + j] : 0.0;
+  }
+
+  auto load = [&](int k) {
+    const int r = y0 - B + k;
+    const int s = k % kNS;
+    const bool rv = (r >= 0) && (r < n);
+    const double2* rowp = x + (size_t)(rv ? r : 0) * n;
+    int col = x0 - B + t;
+    bool v = rv && col >= 0 && col < n;
+    cp_async16(&xs[s][t], rowp + (v ? col : 0), v);
+    if (t < 2 * B) {
+      col = x0 - B + kTX + t;
+      v = rv && col >= 0 && col < n;
+      cp_async16(&xs[s][kTX + t], rowp + (v ? col : 0), v);
+    }
+    if (NEED_B) {
+      const int rb = r - B;  // output row consumed at the same step
+      v = (rb >= y0) && (rb < yend) && colv;
+      cp_async16(&bs[s][t], bv + (v ? (size_t)rb * n + ix : 0), v);
+    }
+  };
+
+#pragma unroll
+  for (int k = 0; k < kNS - 1; ++k) {
+    if (k < nin) load(k);
+    cp_async_commit();
+  }
+  double2 P[NB], Q[NB];
+  double2 XC[B + 1];  // this column's x on the last B+1 input rows (Jacobi centre)
+#pragma unroll
+  for (int j = 0; j < NB; ++j) P[j] = Q[j] = cmk(0.0, 0.0);
+#pragma unroll
+  for (int j = 0; j <= B; ++j) XC[j] = cmk(0.0, 0.0);
+  double acc = 0.0;
+  const double2 c = L.c;
+
+  for (int k = 0; k < nin; ++k) {
+    cp_async_wait<kNS - 2>();
+    __syncthreads();
+    if (k + kNS - 1 < nin) load(k + kNS - 1);
+    cp_async_commit();
+    const int s = k % kNS;
+    double2 u = cmk(0.0, 0.0), v = cmk(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const double2 xv = xs[s][t + j];
+      u = cfma_r(sx[j], xv, u);
+      v = cfma_r(mx[j], xv, v);
+    }
+#pragma unroll
+    for (int j = 0; j < NB - 1; ++j) {
+      P[j] = P[j + 1];
+      Q[j] = Q[j + 1];
+    }
+    P[NB - 1] = csub(u, cmul(c, v));
+    Q[NB - 1] = v;
+    if (MODE == OP_JACOBI) {
+#pragma unroll
+      for (int j = 0; j < B; ++j) XC[j] = XC[j + 1];
+      XC[B] = xs[s][t + B];
+    }
+    if (k >= 2 * B) {
+      const int ro = k - 2 * B;  // output row offset within the strip
+      const int iy = y0 + ro;
+      double2 y = cmk(0.0, 0.0);
+#pragma unroll
+      for (int d = 0; d < NB; ++d) {
+        y = cfma_r(cy[0][ro][d], P[d], y);
+        y = cfma_r(cy[1][ro][d], Q[d], y);
+      }
+      if (colv) {
+        const size_t gi = (size_t)iy * n + ix;
+        if (MODE == OP_APPLY) {
+          out[gi] = y;
+        } else if (MODE == OP_RESID) {
+          out[gi] = csub(bs[s][t], y);
+        } else if (MODE == OP_RESNORM) {
+          acc += cnorm2(csub(bs[s][t], y));
+        } else {  // damped Jacobi: x + omega D^-1 (b - L x)
+          const double myc = cy[0][ro][B], syc = cy[1][ro][B];
+          const double2 D = csub(cmk(myc * sx[B] + syc * mx[B], 0.0), cscale(myc * mx[B], c));
+          const double2 xc = XC[0];
+          const double2 r = csub(bs[s][t], y);
+          out[gi] = cadd(xc, cscale(omega, cmul(cinv(D), r)));
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (MODE == OP_RESNORM) {
+    double2 total;
+    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) * red.scale;
+  }
+}
+
+// x = omega D^-1 b: the first Jacobi sweep from a zero iterate
+// (src/precond.cpp:140 with x = 0, src/precond.cpp:150,160).
+__global__ void k_jacobi0_2d(LevelDev L, const double2* __restrict__ b, double2* __restrict__ out, double omega) {
+  const int n = L.n, NB = 2 * L.b + 1;
+  const size_t N = (size_t)n * n;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
+    const int iy = (int)(g / n), ix = (int)(g % n);
+    const double my = L.M[(size_t)iy * NB + L.b], sy = L.S[(size_t)iy * NB + L.b];
+    const double mxx = L.M[(size_t)ix * NB + L.b], sxx = L.S[(size_t)ix * NB + L.b];
+    const double2 D = csub(cmk(my * sxx + sy * mxx, 0.0), cscale(my * mxx, L.c));
+    out[g] = cscale(omega, cmul(cinv(D), b[g]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 1D banded operator L = S - c M (+ corner), one thread per row.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void k_op1d(LevelDev L, const double2* __restrict__ x, const double2* __restrict__ bv,
+                       double2* __restrict__ out, double omega, RedOut red) {
+  __shared__ double2 scratch[32];
+  const int n = L.n, b = L.b, NB = 2 * b + 1;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double2 sxv = cmk(0.0, 0.0), mxv = cmk(0.0, 0.0);
+    for (int d = -b; d <= b; ++d) {
+      const int j = i + d;
+      if (j < 0 || j >= n) continue;
+      const double2 xv = x[j];
+      sxv = cfma_r(L.S[(size_t)i * NB + d + b], xv, sxv);
+      mxv = cfma_r(L.M[(size_t)i * NB + d + b], xv, mxv);
+    }
+    double2 y = csub(sxv, cmul(L.c, mxv));
+    if (i == n - 1) y = cfma(L.corner, x[i], y);
+    if (MODE == OP_APPLY) {
+      out[i] = y;
+    } else if (MODE == OP_RESID) {
+      out[i] = csub(bv[i], y);
+    } else if (MODE == OP_RESNORM) {
+      acc += cnorm2(csub(bv[i], y));
+    } else {
+      double2 D = csub(cmk(L.S[(size_t)i * NB + b], 0.0), cscale(L.M[(size_t)i * NB + b], L.c));
+      if (i == n - 1) D = cadd(D, L.corner);
+      out[i] = cadd(x[i], cscale(omega, cmul(cinv(D), csub(bv[i], y))));
+    }
+  }
+  if (MODE == OP_RESNORM) {
+    double2 total;
+    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) * red.scale;
+  }
+}
+
+__global__ void k_jacobi0_1d(LevelDev L, const double2* __restrict__ b, double2* __restrict__ out, double omega) {
+  const int n = L.n, NB = 2 * L.b + 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double2 D = csub(cmk(L.S[(size_t)i * NB + L.b], 0.0), cscale(L.M[(size_t)i * NB + L.b], L.c));
+    if (i == n - 1) D = cadd(D, L.corner);
+    out[i] = cscale(omega, cmul(cinv(D), b[i]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Transfers.  kind 0: linear MG stencil, kind 1: Bezier deflation stencil.
+// Restriction (Z^T r)[q] = sum_o w_o r[2q+o] over in-range fine rows:
+//   linear  o = 0..2   w = (1/2, 1, 1/2)
+//   Bezier  o = -1..3  w = (1/8, 1/2, (6-drop)/8, 1/2, 1/8)
+// Prolongation (Z e)[i]: odd i (0-based) -> linear: e[(i-1)/2];
+//   Bezier: 1/8 e[(i-3)/2] + (6-drop)/8 e[(i-1)/2] + 1/8 e[(i+1)/2];
+//   even i -> 1/2 (e[i/2-1] + e[i/2]); out-of-range coarse entries dropped.
+// ---------------------------------------------------------------------------
+struct Stencil {
+  int kind;
+  double drop;
+};
+
+__device__ __forceinline__ int rweights(const Stencil& z, double* w) {  // returns o_lo
+  if (z.kind == 0) {
+    w[0] = 0.5; w[1] = 1.0; w[2] = 0.5; w[3] = 0.0; w[4] = 0.0;
+    return 0;
+  }
+  w[0] = 0.125; w[1] = 0.5; w[2] = (6.0 - z.drop) / 8.0; w[3] = 0.5; w[4] = 0.125;
+  return -1;
+}
+
+// fine index i -> up to 3 (coarse index, weight) pairs
+__device__ __forceinline__ int pweights(const Stencil& z, int i, int nc, int* q, double* w) {
+  int m = 0;
+  auto push = [&](int qq, double ww) {
+    if (qq >= 0 && qq < nc) { q[m] = qq; w[m] = ww; ++m; }
+  };
+  if (i & 1) {
+    if (z.kind == 0) {
+      push((i - 1) / 2, 1.0);
+    } else {
+      push((i - 3) / 2, 0.125);
+      push((i - 1) / 2, (6.0 - z.drop) / 8.0);
+      push((i + 1) / 2, 0.125);
+    }
+  } else {
+    push(i / 2 - 1, 0.5);
+    push(i / 2, 0.5);
+  }
+  return m;
+}
+
+// out: interleaved (planar == 0) or planar re/im planes of nc^dim (planar == 1)
+template <int DIM>
+__global__ void k_restrict(Stencil z, const double2* __restrict__ r, int nf, int nc, double2* __restrict__ outc,
+                           double* __restrict__ outp) {
+  double w[5];
+  const int olo = rweights(z, w);
+  const int nw = z.kind == 0 ? 3 : 5;
+  const size_t NC = DIM == 2 ? (size_t)nc * nc : (size_t)nc;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < NC; g += (size_t)gridDim.x * blockDim.x) {
+    double2 acc = cmk(0.0, 0.0);
+    if (DIM == 1) {
+      const int q = (int)g;
+      for (int o = 0; o < nw; ++o) {
+        const int i = 2 * q + olo + o;
+        if (i >= 0 && i < nf) acc = cfma_r(w[o], r[i], acc);
+      }
+    } else {
+      const int qy = (int)(g / nc), qx = (int)(g % nc);
+      for (int oy = 0; oy < nw; ++oy) {
+        const int iy = 2 * qy + olo + oy;
+        if (iy < 0 || iy >= nf) continue;
+        for (int ox = 0; ox < nw; ++ox) {
+          const int ixx = 2 * qx + olo + ox;
+          if (ixx < 0 || ixx >= nf) continue;
+          acc = cfma_r(w[oy] * w[ox], r[(size_t)iy * nf + ixx], acc);
+        }
+      }
+    }
+    if (outp) {
+      outp[g] = acc.x;
+      outp[g + NC] = acc.y;
+    } else {
+      outc[g] = acc;
+    }
+  }
+}
+
+// mode 0: x += Z e (interleaved e);  mode 1: out = s - Z e (planar e);
+// mode 2: out = Z e (planar e)
+template <int DIM, int PMODE>
+__global__ void k_prolong(Stencil z, const double2* __restrict__ ec, const double* __restrict__ ep, int nf, int nc,
+                          const double2* __restrict__ s, double2* __restrict__ out) {
+  const size_t NF = DIM == 2 ? (size_t)nf * nf : (size_t)nf;
+  const size_t NC = DIM == 2 ? (size_t)nc * nc : (size_t)nc;
+  auto ce = [&](size_t qi) -> double2 { return PMODE == 0 ? ec[qi] : cmk(ep[qi], ep[qi + NC]); };
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < NF; g += (size_t)gridDim.x * blockDim.x) {
+    double2 acc = cmk(0.0, 0.0);
+    if (DIM == 1) {
+      int q[3]; double w[3];
+      const int m = pweights(z, (int)g, nc, q, w);
+      for (int a = 0; a < m; ++a) acc = cfma_r(w[a], ce(q[a]), acc);
+    } else {
+      const int iy = (int)(g / nf), ixx = (int)(g % nf);
+      int qy[3], qx[3]; double wy[3], wx[3];
+      const int my = pweights(z, iy, nc, qy, wy);
+      const int mx = pweights(z, ixx, nc, qx, wx);
+      for (int a = 0; a < my; ++a)
+        for (int bb = 0; bb < mx; ++bb) acc = cfma_r(wy[a] * wx[bb], ce((size_t)qy[a] * nc + qx[bb]), acc);
+    }
+    if (PMODE == 0) out[g] = cadd(out[g], acc);
+    else if (PMODE == 1) out[g] = csub(s[g], acc);
+    else out[g] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Krylov vector kernels (MGS Arnoldi, src/linalg.cpp:41-47, 78-80, 89)
+// ---------------------------------------------------------------------------
+// dst = conj(a) . b
+__global__ void k_dot(const double2* __restrict__ a, const double2* __restrict__ b, size_t N, RedOut red,
+                      double2* dst) {
+  __shared__ double2 scratch[32];
+  double2 acc = cmk(0.0, 0.0);
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
+    acc = cadd(acc, cconjmul(a[g], b[g]));
+  double2 total;
+  if (grid_sum2(acc, red.partials, red.counter, scratch, &total)) *dst = total;
+}
+
+// w -= h * vi ; dst = conj(vn) . w      (one fused MGS step)
+__global__ void k_axpy_dot(double2* __restrict__ w, const double2* __restrict__ vi, const double2* __restrict__ h,
+                           const double2* __restrict__ vn, size_t N, RedOut red, double2* dst) {
+  __shared__ double2 scratch[32];
+  const double2 hh = *h;
+  double2 acc = cmk(0.0, 0.0);
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
+    const double2 nw = csub(w[g], cmul(hh, vi[g]));
+    w[g] = nw;
+    acc = cadd(acc, cconjmul(vn[g], nw));
+  }
+  double2 total;
+  if (grid_sum2(acc, red.partials, red.counter, scratch, &total)) *dst = total;
+}
+
+// w -= h * vi ; hnew = ||w||  -> dst (as complex (hnew, 0)) and *dnorm
+__global__ void k_axpy_norm(double2* __restrict__ w, const double2* __restrict__ vi, const double2* __restrict__ h,
+                            size_t N, RedOut red, double2* dst) {
+  __shared__ double2 scratch[32];
+  const double2 hh = h ? *h : cmk(0.0, 0.0);
+  double acc = 0.0;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
+    double2 nw = w[g];
+    if (vi) {
+      nw = csub(nw, cmul(hh, vi[g]));
+      w[g] = nw;
+    }
+    acc += cnorm2(nw);
+  }
+  double2 total;
+  if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) {
+    const double nrm = sqrt(total.x);
+    *dst = cmk(nrm, 0.0);
+    if (red.dst) *red.dst = nrm;
+  }
+}
+
+// out = a - b
+__global__ void k_sub(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ out,
+                      size_t N) {
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
+    out[g] = csub(a[g], b[g]);
+}
+
+// dst = src / h (h real, read from device; the reference's `w / hnew`)
+__global__ void k_scale_inv(double2* __restrict__ dst, const double2* __restrict__ src, const double* __restrict__ h,
+                            size_t N) {
+  const double s = *h;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = src[g];
+    dst[g] = cmk(v.x / s, v.y / s);
+  }
+}
+
+// x = x0 + sum_{i<m} y_i V_i   (basis vectors contiguous, stride N)
+__global__ void k_iterate(double2* __restrict__ x, const double2* __restrict__ x0, const double2* __restrict__ V,
+                          const double2* __restrict__ y, int m, size_t N) {
+  __shared__ double2 ys[128];
+  for (int i = threadIdx.x; i < m && i < 128; i += blockDim.x) ys[i] = y[i];
+  __syncthreads();
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
+    double2 acc = x0[g];
+    for (int i = 0; i < m; ++i) acc = cfma(ys[i], V[(size_t)i * N + g], acc);
+    x[g] = acc;
+  }
+}
+
+// Givens update of column j + back substitution (src/linalg.cpp:49-77).
+// H column-major with leading dimension ldh = maxit+1.
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) { return cmul(a, cinv(b)); }
+__device__ __forceinline__ double2 cconj(double2 a) { return cmk(a.x, -a.y); }
+
+__global__ void k_givens(double2* H, int ldh, double2* g, double2* cs, double2* sn, double2* y, int j) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double2* col = H + (size_t)j * ldh;
+  for (int i = 0; i < j; ++i) {
+    const double2 a = col[i], b = col[i + 1];
+    const double2 t = cadd(cmul(cs[i], a), cmul(sn[i], b));
+    col[i + 1] = cadd(cmul(cmk(-sn[i].x, sn[i].y), a), cmul(cconj(cs[i]), b));
+    col[i] = t;
+  }
+  const double2 hjj = col[j], hj1 = col[j + 1];
+  const double denom = sqrt(cnorm2(hjj) + cnorm2(hj1));
+  if (denom == 0.0) {
+    cs[j] = cmk(1.0, 0.0);
+    sn[j] = cmk(0.0, 0.0);
+  } else {
+    cs[j] = cmk(hjj.x / denom, -hjj.y / denom);
+    sn[j] = cmk(hj1.x / denom, -hj1.y / denom);
+  }
+  col[j] = cadd(cmul(cs[j], hjj), cmul(sn[j], hj1));
+  col[j + 1] = cmk(0.0, 0.0);
+  const double2 gj = g[j];
+  g[j + 1] = cmul(cmk(-sn[j].x, sn[j].y), gj);
+  g[j] = cmul(cs[j], gj);
+  const int m = j + 1;
+  for (int i = m - 1; i >= 0; --i) {
+    double2 s = g[i];
+    for (int l = i + 1; l < m; ++l) s = csub(s, cmul(H[(size_t)l * ldh + i], y[l]));
+    y[i] = cdiv(s, H[(size_t)i * ldh + i]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exact solvers
+// ---------------------------------------------------------------------------
+// Fast diagonalisation for a small Kronecker-sum operator (n <= 32), one CTA:
+// X (n x n, interleaved, [qy][qx]) -> (V (x) V) diag(Dinv) (V (x) V)^T X.
+// V column-major (V[i + k n] = v_k(i)), Dinv[ky*n + kx].
+__global__ void k_fd_small(const double* __restrict__ V, const double2* __restrict__ Dinv, int n,
+                           const double2* __restrict__ X, double2* __restrict__ Y) {
+  __shared__ double2 A[32 * 32], Bm[32 * 32];
+  __shared__ double Vs[32 * 32];
+  const int nn = n * n;
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    A[e] = X[e];
+    Vs[e] = V[e];
+  }
+  __syncthreads();
+  // B[ky][qx] = sum_qy V(qy,ky) A[qy][qx]
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int ky = e / n, qx = e % n;
+    double2 s = cmk(0.0, 0.0);
+    for (int qy = 0; qy < n; ++qy) s = cfma_r(Vs[qy + ky * n], A[qy * n + qx], s);
+    Bm[e] = s;
+  }
+  __syncthreads();
+  // A[ky][kx] = Dinv * sum_qx V(qx,kx) B[ky][qx]
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int ky = e / n, kx = e % n;
+    double2 s = cmk(0.0, 0.0);
+    for (int qx = 0; qx < n; ++qx) s = cfma_r(Vs[qx + kx * n], Bm[ky * n + qx], s);
+    A[e] = cmul(Dinv[e], s);
+  }
+  __syncthreads();
+  // B[ky][qx] = sum_kx V(qx,kx) A[ky][kx]
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int ky = e / n, qx = e % n;
+    double2 s = cmk(0.0, 0.0);
+    for (int kx = 0; kx < n; ++kx) s = cfma_r(Vs[qx + kx * n], A[ky * n + kx], s);
+    Bm[e] = s;
+  }
+  __syncthreads();
+  // Y[qy][qx] = sum_ky V(qy,ky) B[ky][qx]
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int qy = e / n, qx = e % n;
+    double2 s = cmk(0.0, 0.0);
+    for (int ky = 0; ky < n; ++ky) s = cfma_r(Vs[qy + ky * n], Bm[ky * n + qx], s);
+    Y[e] = s;
+  }
+}
+
+// planar complex T (re plane, im plane; n*n each) *= Dinv (complex, n*n)
+__global__ void k_fd_scale(double* __restrict__ T, const double2* __restrict__ Dinv, size_t NN) {
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < NN; g += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = cmul(cmk(T[g], T[g + NN]), Dinv[g]);
+    T[g] = v.x;
+    T[g + NN] = v.y;
+  }
+}
+
+// Banded LU solve with the host-computed factors (one thread; 1D only).
+// in/out interleaved (planar == nullptr) or planar (n re, n im).
+__global__ void k_bandlu_solve(const double2* __restrict__ Lf, const double2* __restrict__ Uf,
+                               const int* __restrict__ piv, int n, int kl, int ku, const double2* __restrict__ b,
+                               const double* __restrict__ bp, double2* __restrict__ work, double2* __restrict__ x,
+                               double* __restrict__ xp) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = 0; i < n; ++i) work[i] = bp ? cmk(bp[i], bp[i + n]) : b[i];
+  for (int k = 0; k < n; ++k) {
+    const int p = piv[k];
+    if (p != k) {
+      const double2 tmp = work[k];
+      work[k] = work[p];
+      work[p] = tmp;
+    }
+    const double2 wk = work[k];
+    for (int r = 1; r <= kl && k + r < n; ++r) work[k + r] = csub(work[k + r], cmul(Lf[(size_t)k * kl + r - 1], wk));
+  }
+  for (int k = n - 1; k >= 0; --k) {
+    double2 s = work[k];
+    for (int d = 1; d <= ku && k + d < n; ++d) s = csub(s, cmul(Uf[(size_t)k * (ku + 1) + d], work[k + d]));
+    work[k] = cdiv(s, Uf[(size_t)k * (ku + 1)]);
+  }
+  for (int i = 0; i < n; ++i) {
+    if (xp) {
+      xp[i] = work[i].x;
+      xp[i + n] = work[i].y;
+    } else {
+      x[i] = work[i];
+    }
+  }
+}
+
+}  // namespace hd

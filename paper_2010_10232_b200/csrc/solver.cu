@@ -1,0 +1,967 @@
+// Host driver of the device solve behind the C-ABI of include/helmdef_b200.h.
+//
+// hd_create  == compose()  (src/precond.cpp:196-265): Galerkin multigrid
+//               hierarchy of the shifted operator (as 1D factors, see
+//               host/banded.hpp), inverse-diagonal Jacobi, coarsest exact
+//               solve, Bezier deflation E = Z^T A Z and its exact solve.
+// hd_solve   == gmres(setup.op, setup.rhs, setup.start, setup.monitor, opt)
+//               (src/linalg.cpp:10-92) with every vector resident on the
+//               device; one 2-scalar device->host read per iteration decides
+//               convergence.
+// SPDX-License-Identifier: Apache-2.0
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/helmdef_b200.h"
+#include "host/assembly.hpp"
+#include "host/banded.hpp"
+#include "kernels.cuh"
+
+namespace hd {
+
+static thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+  hd_status code;
+  Error(hd_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess)                                                                        \
+      throw Error(HD_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + \
+                                   ":" + std::to_string(__LINE__));                               \
+  } while (0)
+#define CKB(x)                                                                                    \
+  do {                                                                                            \
+    cublasStatus_t e_ = (x);                                                                      \
+    if (e_ != CUBLAS_STATUS_SUCCESS) throw Error(HD_ERR_CUDA, std::string(#x) + " failed: " + std::to_string(e_)); \
+  } while (0)
+#define CKS(x)                                                                                    \
+  do {                                                                                            \
+    cusolverStatus_t e_ = (x);                                                                    \
+    if (e_ != CUSOLVER_STATUS_SUCCESS) throw Error(HD_ERR_CUDA, std::string(#x) + " failed: " + std::to_string(e_)); \
+  } while (0)
+
+template <class T>
+static T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+struct DevBand {
+  double* S = nullptr;
+  double* M = nullptr;
+  int n = 0, b = 0;
+};
+
+// Exact solver of one Kronecker-sum (2D) or banded (1D) operator.
+struct ExactSolver {
+  int dim = 0, n = 0;
+  // 2D fast diagonalisation
+  double* V = nullptr;       // n x n column-major eigenvectors, V^T M V = I
+  double2* Dinv = nullptr;   // n x n, 1 / (lam_y + lam_x - c)
+  double* T1 = nullptr;      // planar work, 2 n^2
+  double* T2 = nullptr;
+  // 1D banded LU
+  int kl = 0, ku = 0;
+  double2* L = nullptr;
+  double2* U = nullptr;
+  int* piv = nullptr;
+  double2* work = nullptr;
+};
+
+}  // namespace hd
+
+using namespace hd;
+
+struct hd_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  cublasHandle_t cb = nullptr;
+  int dim = 1, p = 1, n = 0;
+  size_t N = 0;
+  double k = 0.0;
+  hd_precond spec{};
+  double2 corner = cmk(0.0, 0.0);
+  // operators
+  DevBand fine;                 // reduced S1, M1 (b = p)
+  double2 cA = cmk(0.0, 0.0);   // A = ... - k^2 M(x)M
+  double2 cM = cmk(0.0, 0.0);   // shifted: - k^2 (1 - i beta2) M(x)M
+  std::vector<DevBand> lev;     // multigrid levels (lev[0] = fine)
+  ExactSolver coarsest;
+  std::vector<double2*> mg_b, mg_x, mg_y, mg_r;
+  // deflation
+  int nc = 0;
+  ExactSolver E;
+  double* ep = nullptr;         // planar coarse buffers (2 nc^dim)
+  double* ep2 = nullptr;
+  // vectors
+  double2 *f = nullptr, *rhsp = nullptr, *x0 = nullptr, *x = nullptr, *w = nullptr, *t1 = nullptr,
+          *t2 = nullptr, *t3 = nullptr;
+  double2* V = nullptr;
+  int v_cap = 0;
+  // GMRES scalars
+  int maxit_cap = 0;
+  double2 *H = nullptr, *g = nullptr, *cs = nullptr, *sn = nullptr, *y = nullptr;
+  double2* scal = nullptr;      // [0] hnew, [1] beta, [2] scratch dot
+  double* dres = nullptr;       // [0] rr, [1] hnew, [2] beta, [3] fnorm
+  double* hres = nullptr;       // pinned mirror
+  double2* partials = nullptr;
+  unsigned* counter = nullptr;
+  int red_blocks = 0;
+  // counters
+  long matvecs = 0, coarse_solves = 0, shift_solves = 0, vcycles = 0;
+  int launches = 0;
+  double t_setup = 0.0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace hd {
+
+static DevBand upload_band(const Band& B) {
+  DevBand d;
+  d.n = B.n;
+  d.b = B.b;
+  d.S = dalloc<double>(B.a.size());
+  CK(cudaMemcpy(d.S, B.a.data(), B.a.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return d;
+}
+
+static DevBand upload_pair(const Band& S, const Band& M) {
+  const int b = std::max(S.b, M.b);
+  Band s2(S.n, b), m2(M.n, b);
+  for (int i = 0; i < S.n; ++i)
+    for (int d = -b; d <= b; ++d) {
+      const int j = i + d;
+      if (j < 0 || j >= S.n) continue;
+      s2.ref(i, j) = S.at(i, j);
+      m2.ref(i, j) = M.at(i, j);
+    }
+  DevBand d;
+  d.n = S.n;
+  d.b = b;
+  d.S = dalloc<double>(s2.a.size());
+  d.M = dalloc<double>(m2.a.size());
+  CK(cudaMemcpy(d.S, s2.a.data(), s2.a.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d.M, m2.a.data(), m2.a.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return d;
+}
+
+static Band band_from_host(const double* a, int n, int b) {
+  Band B(n, b);
+  std::memcpy(B.a.data(), a, B.a.size() * sizeof(double));
+  return B;
+}
+
+static LevelDev level_dev(const DevBand& d, double2 c, double2 corner) {
+  LevelDev L;
+  L.S = d.S;
+  L.M = d.M;
+  L.n = d.n;
+  L.b = d.b;
+  L.c = c;
+  L.corner = corner;
+  return L;
+}
+
+static std::vector<double> dense_of(const Band& B) {
+  std::vector<double> D(static_cast<size_t>(B.n) * B.n, 0.0);
+  for (int i = 0; i < B.n; ++i)
+    for (int j = std::max(0, i - B.b); j <= std::min(B.n - 1, i + B.b); ++j) D[i + static_cast<size_t>(j) * B.n] = B.at(i, j);
+  return D;
+}
+
+// Fast diagonalisation of W = M(x)S + S(x)M - c M(x)M: S V = M V diag(lam),
+// V^T M V = I (cuSOLVER sygvd at setup), Dinv = 1/(lam_i + lam_j - c).
+static ExactSolver make_fd(cudaStream_t st, const Band& S, const Band& M, double2 c) {
+  ExactSolver X;
+  X.dim = 2;
+  X.n = S.n;
+  const int n = S.n;
+  std::vector<double> As = dense_of(S), Bm = dense_of(M);
+  double *dA = dalloc<double>(As.size()), *dB = dalloc<double>(Bm.size()), *dW = dalloc<double>(n);
+  int* dinfo = dalloc<int>(1);
+  CK(cudaMemcpy(dA, As.data(), As.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, Bm.data(), Bm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  cusolverDnHandle_t h;
+  CKS(cusolverDnCreate(&h));
+  CKS(cusolverDnSetStream(h, st));
+  int lwork = 0;
+  CKS(cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dA, n,
+                                  dB, n, dW, &lwork));
+  double* dwork = dalloc<double>(std::max(lwork, 1));
+  CKS(cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dA, n, dB, n, dW,
+                       dwork, lwork, dinfo));
+  int info = 0;
+  CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cusolverDnDestroy(h);
+  if (info != 0) throw Error(HD_ERR_FACTOR, "coarse operator factorization failed (sygvd info " + std::to_string(info) + ")");
+  std::vector<double> lam(n);
+  CK(cudaMemcpy(lam.data(), dW, n * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<double2> Dinv(static_cast<size_t>(n) * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const std::complex<double> d(lam[i] + lam[j] - c.x, -c.y);
+      if (d == std::complex<double>(0.0, 0.0)) throw Error(HD_ERR_FACTOR, "coarse operator factorization failed (singular)");
+      const std::complex<double> r = 1.0 / d;
+      Dinv[static_cast<size_t>(i) * n + j] = cmk(r.real(), r.imag());
+    }
+  X.V = dA;
+  X.Dinv = dalloc<double2>(Dinv.size());
+  CK(cudaMemcpy(X.Dinv, Dinv.data(), Dinv.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  X.T1 = dalloc<double>(2 * static_cast<size_t>(n) * n);
+  X.T2 = dalloc<double>(2 * static_cast<size_t>(n) * n);
+  cudaFree(dB);
+  cudaFree(dW);
+  cudaFree(dinfo);
+  cudaFree(dwork);
+  return X;
+}
+
+static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 corner) {
+  BandLU f = band_lu(S, M, cplx(c.x, c.y), cplx(corner.x, corner.y));
+  ExactSolver X;
+  X.dim = 1;
+  X.n = f.n;
+  X.kl = f.kl;
+  X.ku = f.ku;
+  X.L = dalloc<double2>(f.L.size());
+  X.U = dalloc<double2>(f.U.size());
+  X.piv = dalloc<int>(f.piv.size());
+  X.work = dalloc<double2>(f.n);
+  CK(cudaMemcpy(X.L, f.L.data(), f.L.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(X.U, f.U.data(), f.U.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(X.piv, f.piv.data(), f.piv.size() * sizeof(int), cudaMemcpyHostToDevice));
+  return X;
+}
+
+static void free_exact(ExactSolver& X) {
+  cudaFree(X.V); cudaFree(X.Dinv); cudaFree(X.T1); cudaFree(X.T2);
+  cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work);
+  X = ExactSolver{};
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+static int grid_for(size_t N, int threads = 256, int cap = 148 * 8) {
+  const size_t g = (N + threads - 1) / threads;
+  return static_cast<int>(std::max<size_t>(1, std::min<size_t>(g, cap)));
+}
+
+static int strip_rows(int n) {
+  // rows per CTA: keep >= ~4 CTAs per SM in flight on the big levels
+  const int cols = (n + kTX - 1) / kTX;
+  int ry = 32;
+  while (ry > 8 && static_cast<long>(cols) * ((n + ry - 1) / ry) < 148 * 4) ry /= 2;
+  return ry;
+}
+
+template <int MODE>
+static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
+                             double omega, RedOut red) {
+  const int ry = strip_rows(L.n);
+  dim3 grid((L.n + kTX - 1) / kTX, (L.n + ry - 1) / ry);
+  switch (L.b) {
+#define HD_CASE(BB) \
+  case BB: k_op2d<BB, MODE><<<grid, kTX, 0, c->st>>>(L, x, b, out, omega, ry, red); break;
+    HD_CASE(1) HD_CASE(2) HD_CASE(3) HD_CASE(4) HD_CASE(5) HD_CASE(6)
+#undef HD_CASE
+    default: throw Error(HD_ERR_INVALID, "band half-width " + std::to_string(L.b) + " unsupported");
+  }
+  CK(cudaGetLastError());
+  ++c->launches;
+}
+
+static RedOut red_of(hd_ctx* c, double* dst = nullptr, double scale = 1.0) {
+  RedOut r;
+  r.partials = c->partials;
+  r.counter = c->counter;
+  r.dst = dst;
+  r.scale = scale;
+  return r;
+}
+
+// out = L x | b - L x | x + w D^-1 (b - L x) | ||b - L x|| * scale -> dst
+static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, const double2* b, double2* out,
+                     double omega = 0.0, double* dst = nullptr, double scale = 1.0) {
+  RedOut red = red_of(c, dst, scale);
+  if (c->dim == 2) {
+    switch (mode) {
+      case OP_APPLY: launch_op2d_mode<OP_APPLY>(c, L, x, b, out, omega, red); break;
+      case OP_RESID: launch_op2d_mode<OP_RESID>(c, L, x, b, out, omega, red); break;
+      case OP_JACOBI: launch_op2d_mode<OP_JACOBI>(c, L, x, b, out, omega, red); break;
+      default: launch_op2d_mode<OP_RESNORM>(c, L, x, b, out, omega, red); break;
+    }
+  } else {
+    const int grid = mode == OP_RESNORM ? std::min(grid_for(L.n), c->red_blocks) : grid_for(L.n);
+    switch (mode) {
+      case OP_APPLY: k_op1d<OP_APPLY><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
+      case OP_RESID: k_op1d<OP_RESID><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
+      case OP_JACOBI: k_op1d<OP_JACOBI><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
+      default: k_op1d<OP_RESNORM><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
+    }
+    CK(cudaGetLastError());
+    ++c->launches;
+  }
+}
+
+static void jacobi0(hd_ctx* c, const LevelDev& L, const double2* b, double2* out, double omega) {
+  const size_t NN = c->dim == 2 ? static_cast<size_t>(L.n) * L.n : L.n;
+  if (c->dim == 2) k_jacobi0_2d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega);
+  else k_jacobi0_1d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega);
+  CK(cudaGetLastError());
+  ++c->launches;
+}
+
+static void restrict_(hd_ctx* c, Stencil z, const double2* r, int nf, int nc, double2* outc, double* outp) {
+  const size_t NC = c->dim == 2 ? static_cast<size_t>(nc) * nc : nc;
+  if (c->dim == 2) k_restrict<2><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp);
+  else k_restrict<1><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp);
+  CK(cudaGetLastError());
+  ++c->launches;
+}
+
+template <int PMODE>
+static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, int nf, int nc, const double2* s,
+                     double2* out) {
+  const size_t NF = c->dim == 2 ? static_cast<size_t>(nf) * nf : nf;
+  if (c->dim == 2) k_prolong<2, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out);
+  else k_prolong<1, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out);
+  CK(cudaGetLastError());
+  ++c->launches;
+}
+
+// Exact solve: in/out planar (2D FD) or via the banded LU (1D).
+static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
+  if (X.dim == 2) {
+    const int n = X.n;
+    const long nn = static_cast<long>(n) * n;
+    const double one = 1.0, zero = 0.0;
+    // T1 = V^T [Xre | Xim]
+    CKB(cublasDgemm(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, inout, n, &zero, X.T1, n));
+    // T2_plane = T1_plane V
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, X.T1, n, nn, X.V, n, 0, &zero,
+                                  X.T2, n, nn, 2));
+    k_fd_scale<<<grid_for(nn), 256, 0, c->st>>>(X.T2, X.Dinv, nn);
+    CK(cudaGetLastError());
+    // T1 = V [T2re | T2im]
+    CKB(cublasDgemm(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, X.T2, n, &zero, X.T1, n));
+    // out_plane = T1_plane V^T
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, n, n, n, &one, X.T1, n, nn, X.V, n, 0, &zero,
+                                  inout, n, nn, 2));
+    c->launches += 5;
+  } else {
+    k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, nullptr, inout, X.work, nullptr, inout);
+    CK(cudaGetLastError());
+    ++c->launches;
+  }
+}
+
+// coarsest multigrid level: interleaved in/out
+static void coarsest_solve(hd_ctx* c, const double2* b, double2* out) {
+  ExactSolver& X = c->coarsest;
+  if (X.dim == 2) {
+    k_fd_small<<<1, 1024, 0, c->st>>>(X.V, X.Dinv, X.n, b, out);
+  } else {
+    k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, b, nullptr, X.work, out, nullptr);
+  }
+  CK(cudaGetLastError());
+  ++c->launches;
+}
+
+static size_t lsize(const hd_ctx* c, int n) { return c->dim == 2 ? static_cast<size_t>(n) * n : n; }
+
+// x_out = (damped Jacobi)^steps from x (x_zero: x == 0), ping-pong through tmp
+static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2* xb, bool x_zero, int steps) {
+  const LevelDev L = level_dev(c->lev[l], c->cM, l == 0 ? c->corner : cmk(0.0, 0.0));
+  double2* cur = xa;
+  double2* oth = xb;
+  int s = 0;
+  if (x_zero) {
+    if (steps == 0) {
+      CK(cudaMemsetAsync(cur, 0, lsize(c, L.n) * sizeof(double2), c->st));
+      return cur;
+    }
+    jacobi0(c, L, b, cur, c->spec.omega);
+    s = 1;
+  }
+  for (; s < steps; ++s) {
+    op_apply(c, OP_JACOBI, L, cur, b, oth, c->spec.omega);
+    std::swap(cur, oth);
+  }
+  return cur;
+}
+
+// One V-cycle at level l (src/precond.cpp:144-153); returns the buffer holding x.
+static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero) {
+  const int last = static_cast<int>(c->lev.size()) - 1;
+  if (l == last) {
+    coarsest_solve(c, b, c->mg_x[l]);
+    return c->mg_x[l];
+  }
+  const LevelDev L = level_dev(c->lev[l], c->cM, l == 0 ? c->corner : cmk(0.0, 0.0));
+  double2* xcur = smooth(c, l, b, c->mg_x[l], c->mg_y[l], x_zero, c->spec.smooth_steps);
+  double2* xoth = xcur == c->mg_x[l] ? c->mg_y[l] : c->mg_x[l];
+  op_apply(c, OP_RESID, L, xcur, b, c->mg_r[l]);
+  const int nf = c->lev[l].n, ncl = c->lev[l + 1].n;
+  restrict_(c, Stencil{0, 0.0}, c->mg_r[l], nf, ncl, c->mg_b[l + 1], nullptr);
+  double2* ec = cycle_at(c, l + 1, c->mg_b[l + 1], true);
+  prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, nf, ncl, nullptr, xcur);
+  double2* res = smooth(c, l, b, xcur, xoth, false, c->spec.smooth_steps);
+  return res;
+}
+
+// out = MG^-1 b  with `cycles` V-cycles from zero (src/precond.cpp:159-163)
+static void mg_solve(hd_ctx* c, const double2* b, double2* out) {
+  const size_t N = c->N;
+  bool zero = true;
+  double2* xb = nullptr;
+  for (int cy = 0; cy < c->spec.cycles; ++cy) {
+    if (!zero) {
+      // level-0 iterate must live in mg_x[0] for the next cycle
+      if (xb != c->mg_x[0]) CK(cudaMemcpyAsync(c->mg_x[0], xb, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    }
+    if (c->lev.size() == 1) {
+      coarsest_solve(c, b, c->mg_x[0]);
+      xb = c->mg_x[0];
+    } else if (zero) {
+      xb = cycle_at(c, 0, b, true);
+    } else {
+      // general cycle from a non-zero iterate held in mg_x[0]
+      const LevelDev L = level_dev(c->lev[0], c->cM, c->corner);
+      double2* xcur = smooth(c, 0, b, c->mg_x[0], c->mg_y[0], false, c->spec.smooth_steps);
+      double2* xoth = xcur == c->mg_x[0] ? c->mg_y[0] : c->mg_x[0];
+      op_apply(c, OP_RESID, L, xcur, b, c->mg_r[0]);
+      restrict_(c, Stencil{0, 0.0}, c->mg_r[0], c->lev[0].n, c->lev[1].n, c->mg_b[1], nullptr);
+      double2* ec = cycle_at(c, 1, c->mg_b[1], true);
+      prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, c->lev[0].n, c->lev[1].n, nullptr, xcur);
+      xb = smooth(c, 0, b, xcur, xoth, false, c->spec.smooth_steps);
+    }
+    zero = false;
+  }
+  if (c->spec.cycles <= 0) {
+    CK(cudaMemsetAsync(out, 0, N * sizeof(double2), c->st));
+    return;
+  }
+  CK(cudaMemcpyAsync(out, xb, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+}
+
+static LevelDev opA(hd_ctx* c) { return level_dev(c->fine, c->cA, c->corner); }
+
+// out = Q v = Z E^-1 Z^T v  (Deflation::apply_Q, src/precond.cpp:102-104)
+static void apply_Q(hd_ctx* c, const double2* v, double2* out) {
+  const Stencil z{1, c->spec.drop};
+  restrict_(c, z, v, c->n, c->nc, nullptr, c->ep);
+  exact_solve_planar(c, c->E, c->ep);
+  prolong_<2>(c, z, nullptr, c->ep, c->n, c->nc, nullptr, out);
+}
+
+// out = w - Q (A w)  (Deflation::project, src/precond.cpp:106-108)
+static void project(hd_ctx* c, const double2* w, double2* out) {
+  const Stencil z{1, c->spec.drop};
+  op_apply(c, OP_APPLY, opA(c), w, nullptr, c->t3);
+  restrict_(c, z, c->t3, c->n, c->nc, nullptr, c->ep);
+  exact_solve_planar(c, c->E, c->ep);
+  prolong_<1>(c, z, nullptr, c->ep, c->n, c->nc, w, out);
+}
+
+// out = op(v) = P MG^-1 A v  (src/precond.cpp:236-245); v, out distinct from t1, t2, t3
+static void compose_op(hd_ctx* c, const double2* v, double2* out) {
+  ++c->matvecs;
+  op_apply(c, OP_APPLY, opA(c), v, nullptr, c->t1);
+  const double2* cur = c->t1;
+  if (c->spec.shift) {
+    ++c->shift_solves;
+    c->vcycles += c->spec.cycles;
+    mg_solve(c, c->t1, c->t2);
+    cur = c->t2;
+  }
+  if (c->spec.deflate) {
+    ++c->coarse_solves;
+    project(c, cur, out);
+  } else {
+    CK(cudaMemcpyAsync(out, cur, c->N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+  }
+}
+
+static void ensure_gmres(hd_ctx* c, int maxit) {
+  if (maxit + 1 > c->v_cap) {
+    cudaFree(c->V);
+    c->V = dalloc<double2>(static_cast<size_t>(maxit + 1) * c->N);
+    c->v_cap = maxit + 1;
+  }
+  if (maxit > c->maxit_cap) {
+    cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
+    c->H = dalloc<double2>(static_cast<size_t>(maxit + 1) * maxit);
+    c->g = dalloc<double2>(maxit + 1);
+    c->cs = dalloc<double2>(maxit);
+    c->sn = dalloc<double2>(maxit);
+    c->y = dalloc<double2>(maxit);
+    c->maxit_cap = maxit;
+  }
+}
+
+static void read_scalars(hd_ctx* c) {
+  CK(cudaMemcpyAsync(c->hres, c->dres, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+}
+
+struct SolveOut {
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> residuals;
+};
+
+// gmres(setup.op, setup.rhs, setup.start, setup.monitor, opt) after the
+// compose() right-hand side / start transforms; f already in c->f.
+static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
+  const size_t N = c->N;
+  const int maxit = opt.max_iterations;
+  ensure_gmres(c, std::max(maxit, 1));
+  c->matvecs = c->coarse_solves = c->shift_solves = c->vcycles = 0;
+  c->launches = 0;
+  const int nb = c->red_blocks;
+  // ||f|| (monitor scale, src/precond.cpp:258)
+  k_axpy_norm<<<nb, 256, 0, c->st>>>(c->f, nullptr, nullptr, N, red_of(c, c->dres + 3), c->scal + 2);
+  ++c->launches;
+  // rhs' = P MG^-1 f   (src/precond.cpp:247-253)
+  const double2* b = c->f;
+  if (c->spec.shift) {
+    ++c->shift_solves;
+    c->vcycles += c->spec.cycles;
+    mg_solve(c, c->f, c->t2);
+    b = c->t2;
+  }
+  if (c->spec.deflate) {
+    ++c->coarse_solves;
+    project(c, b, c->rhsp);
+  } else {
+    CK(cudaMemcpyAsync(c->rhsp, b, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+  }
+  // start = Q f (src/precond.cpp:255-256)
+  if (c->spec.deflate) {
+    apply_Q(c, c->f, c->x0);
+    ++c->coarse_solves;
+  } else {
+    CK(cudaMemsetAsync(c->x0, 0, N * sizeof(double2), c->st));
+  }
+  read_scalars(c);
+  const double fnorm = c->hres[3];
+  const double scale = fnorm > 0.0 ? 1.0 / fnorm : 1.0;
+
+  SolveOut res;
+  auto monitor = [&](const double2* xv) {
+    op_apply(c, OP_RESNORM, opA(c), xv, c->f, nullptr, 0.0, c->dres + 0, scale);
+  };
+  monitor(c->x0);
+  read_scalars(c);
+  const double r0 = c->hres[0];
+  if (r0 <= opt.tolerance) {  // src/linalg.cpp:17-22
+    res.converged = true;
+    res.residuals.push_back(r0);
+    CK(cudaMemcpyAsync(xout, c->x0, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    return res;
+  }
+  // r = rhs' - op(x0); beta = ||r||; V0 = r / beta  (src/linalg.cpp:24-33)
+  compose_op(c, c->x0, c->w);
+  k_sub<<<grid_for(N), 256, 0, c->st>>>(c->rhsp, c->w, c->w, N);
+  k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, nullptr, nullptr, N, red_of(c, c->dres + 2), c->g);
+  c->launches += 2;
+  read_scalars(c);
+  const double beta = c->hres[2];
+  if (beta == 0.0) {
+    monitor(c->x0);
+    read_scalars(c);
+    res.converged = c->hres[0] <= opt.tolerance;
+    CK(cudaMemcpyAsync(xout, c->x0, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    return res;
+  }
+  CK(cudaMemsetAsync(c->H, 0, sizeof(double2) * (maxit + 1) * maxit, c->st));
+  CK(cudaMemsetAsync(c->g + 1, 0, sizeof(double2) * maxit, c->st));
+  k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V, c->w, c->dres + 2, N);
+  ++c->launches;
+  const int ldh = maxit + 1;
+  for (int j = 0; j < maxit; ++j) {
+    double2* Vj = c->V + static_cast<size_t>(j) * N;
+    compose_op(c, Vj, c->w);
+    double2* Hj = c->H + static_cast<size_t>(j) * ldh;
+    // modified Gram-Schmidt (src/linalg.cpp:42-47)
+    k_dot<<<nb, 256, 0, c->st>>>(c->V, c->w, N, red_of(c), Hj + 0);
+    for (int i = 0; i < j; ++i)
+      k_axpy_dot<<<nb, 256, 0, c->st>>>(c->w, c->V + static_cast<size_t>(i) * N, Hj + i,
+                                        c->V + static_cast<size_t>(i + 1) * N, N, red_of(c), Hj + i + 1);
+    k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, Vj, Hj + j, N, red_of(c, c->dres + 1), Hj + j + 1);
+    k_givens<<<1, 32, 0, c->st>>>(c->H, ldh, c->g, c->cs, c->sn, c->y, j);
+    k_iterate<<<grid_for(N), 256, 0, c->st>>>(xout, c->x0, c->V, c->y, j + 1, N);
+    c->launches += j + 4;
+    CK(cudaGetLastError());
+    res.iterations = j + 1;
+    monitor(xout);
+    read_scalars(c);
+    const double rr = c->hres[0];
+    const double hnew = c->hres[1];
+    res.residuals.push_back(rr);
+    if (rr <= opt.tolerance) {
+      res.converged = true;
+      break;
+    }
+    if (hnew < 1e-300) break;
+    if (j + 1 < maxit) {
+      k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V + static_cast<size_t>(j + 1) * N, c->w, c->dres + 1, N);
+      ++c->launches;
+    }
+  }
+  return res;
+}
+
+static void destroy_ctx(hd_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  auto fb = [](DevBand& d) { cudaFree(d.S); cudaFree(d.M); };
+  fb(c->fine);
+  for (size_t l = 1; l < c->lev.size(); ++l) fb(c->lev[l]);
+  free_exact(c->coarsest);
+  free_exact(c->E);
+  for (auto* p : c->mg_b) cudaFree(p);
+  for (auto* p : c->mg_x) cudaFree(p);
+  for (auto* p : c->mg_y) cudaFree(p);
+  for (auto* p : c->mg_r) cudaFree(p);
+  cudaFree(c->ep); cudaFree(c->ep2);
+  cudaFree(c->f); cudaFree(c->rhsp); cudaFree(c->x0); cudaFree(c->x); cudaFree(c->w);
+  cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->t3); cudaFree(c->V);
+  cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
+  cudaFree(c->scal); cudaFree(c->dres); cudaFree(c->partials); cudaFree(c->counter);
+  if (c->hres) cudaFreeHost(c->hres);
+  if (c->cb) cublasDestroy(c->cb);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* devices, int n_devices, hd_ctx** out) {
+  if (!sys || !spec || !out) throw Error(HD_ERR_INVALID, "null argument");
+  if (n_devices > 1) throw Error(HD_ERR_INVALID, "multi-device row slabs are not available in this build");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(HD_ERR_NO_DEVICE, "no CUDA device: the helmdef_b200 path has no CPU fallback");
+  if (sys->dim != 1 && sys->dim != 2) throw Error(HD_ERR_INVALID, "dim must be 1 or 2");
+  if (sys->field_kind != HD_FIELD_CONSTANT) throw Error(HD_ERR_INVALID, "only constant wave-number fields are supported");
+  if (spec->shift && spec->cycles <= 0) throw Error(HD_ERR_INVALID, "exact shifted inverse (cycles = 0, C_ex) is not on the device path");
+  if (sys->per_dim < 2) throw Error(HD_ERR_INVALID, "per_dim must be >= 2");
+  const auto t0 = std::chrono::steady_clock::now();
+  std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
+  c->device = (devices && n_devices == 1) ? devices[0] : 0;
+  if (!devices || n_devices == 0) CK(cudaGetDevice(&c->device));
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  CKB(cublasCreate(&c->cb));
+  CKB(cublasSetStream(c->cb, c->st));
+  CKB(cublasSetMathMode(c->cb, CUBLAS_DEFAULT_MATH));
+  CK(cudaEventCreate(&c->ev0));
+  CK(cudaEventCreate(&c->ev1));
+  c->dim = sys->dim;
+  c->p = sys->order;
+  c->n = sys->per_dim;
+  c->N = c->dim == 2 ? static_cast<size_t>(c->n) * c->n : c->n;
+  c->k = sys->k;
+  c->spec = *spec;
+  if (c->spec.coarsest <= 0) c->spec.coarsest = 32;
+  c->corner = c->dim == 1 ? cmk(sys->corner_re, sys->corner_im) : cmk(0.0, 0.0);
+  const double k2 = c->k * c->k;
+  c->cA = cmk(k2, 0.0);
+  // shifted operator A + i beta2 K2 = ... - k^2 (1 - i beta2) M(x)M  (src/precond.cpp:165-167)
+  c->cM = cmk(k2, -k2 * c->spec.beta2);
+  const Band S1 = band_from_host(sys->stiffness_band, c->n, sys->order);
+  const Band M1 = band_from_host(sys->mass_band, c->n, sys->order);
+  c->fine = upload_pair(S1, M1);
+  // multigrid hierarchy of the shifted operator (src/precond.cpp:110-134)
+  if (c->spec.shift) {
+    std::vector<Band> Ss{S1}, Ms{M1};
+    int nl = c->n;
+    while (nl > c->spec.coarsest) {
+      const Transfer z = linear_stencil(nl);
+      Ss.push_back(galerkin(Ss.back(), z));
+      Ms.push_back(galerkin(Ms.back(), z));
+      nl = z.coarse;
+    }
+    c->lev.push_back(c->fine);
+    for (size_t l = 1; l < Ss.size(); ++l) c->lev.push_back(upload_pair(Ss[l], Ms[l]));
+    // zero-diagonal check of every level (src/precond.cpp:125-132)
+    for (size_t l = 0; l < Ss.size(); ++l)
+      for (int i = 0; i < Ss[l].n; ++i)
+        for (int j = 0; j < (c->dim == 2 ? Ss[l].n : 1); ++j) {
+          const int jj = c->dim == 2 ? j : i;
+          std::complex<double> d = c->dim == 2
+                                       ? std::complex<double>(Ms[l].at(i, i) * Ss[l].at(jj, jj) + Ss[l].at(i, i) * Ms[l].at(jj, jj), 0.0) -
+                                             std::complex<double>(c->cM.x, c->cM.y) * (Ms[l].at(i, i) * Ms[l].at(jj, jj))
+                                       : std::complex<double>(Ss[l].at(i, i), 0.0) - std::complex<double>(c->cM.x, c->cM.y) * Ms[l].at(i, i);
+          if (l == 0 && c->dim == 1 && i == c->n - 1) d += std::complex<double>(c->corner.x, c->corner.y);
+          if (d == std::complex<double>(0.0, 0.0)) throw Error(HD_ERR_FACTOR, "zero diagonal in smoother");
+        }
+    const Band& SL = Ss.back();
+    const Band& ML = Ms.back();
+    if (c->dim == 2) c->coarsest = make_fd(c->st, SL, ML, c->cM);
+    else c->coarsest = make_bandlu(SL, ML, c->cM, Ss.size() == 1 ? c->corner : cmk(0.0, 0.0));
+    for (size_t l = 0; l < c->lev.size(); ++l) {
+      const size_t NL = lsize(c.get(), c->lev[l].n);
+      c->mg_b.push_back(l == 0 ? nullptr : dalloc<double2>(NL));
+      c->mg_x.push_back(dalloc<double2>(NL));
+      c->mg_y.push_back(dalloc<double2>(NL));
+      c->mg_r.push_back(dalloc<double2>(NL));
+    }
+  }
+  // deflation: E = Z^T A Z with the Bezier stencil (src/precond.cpp:93-100, 228-232)
+  if (c->spec.deflate) {
+    const Transfer z = halving_stencil(c->n, c->spec.drop);
+    c->nc = z.coarse;
+    if (c->nc < 1) throw Error(HD_ERR_INVALID, "deflation needs per_dim >= 2");
+    const Band ES = galerkin(S1, z), EM = galerkin(M1, z);
+    if (c->dim == 2) {
+      c->E = make_fd(c->st, ES, EM, c->cA);
+    } else {
+      // corner term of A restricted: Z^T (corner e_n e_n^T) Z
+      double2 corner_c = cmk(0.0, 0.0);
+      if (c->corner.x != 0.0 || c->corner.y != 0.0) {
+        // the last fine row maps onto the last coarse column(s); E's (nc-1, nc-1) gets w^2 * corner
+        double wl = 0.0;
+        for (size_t t = 0; t < z.w.size(); ++t)
+          if (z.row[t] == c->n - 1 && z.col[t] == c->nc - 1) wl = z.w[t];
+        if (wl != 0.0) corner_c = cmk(c->corner.x * wl * wl, c->corner.y * wl * wl);
+      }
+      c->E = make_bandlu(ES, EM, c->cA, corner_c);
+    }
+    const size_t NC = lsize(c.get(), c->nc);
+    c->ep = dalloc<double>(2 * NC);
+    c->ep2 = dalloc<double>(2 * NC);
+  }
+  const size_t N = c->N;
+  c->f = dalloc<double2>(N);
+  c->rhsp = dalloc<double2>(N);
+  c->x0 = dalloc<double2>(N);
+  c->x = dalloc<double2>(N);
+  c->w = dalloc<double2>(N);
+  c->t1 = dalloc<double2>(N);
+  c->t2 = dalloc<double2>(N);
+  c->t3 = dalloc<double2>(N);
+  c->scal = dalloc<double2>(8);
+  c->dres = dalloc<double>(8);
+  CK(cudaMallocHost(&c->hres, 8 * sizeof(double)));
+  c->red_blocks = 148 * 4;
+  const int max_stencil_blocks = 148 * 64;
+  c->partials = dalloc<double2>(std::max(c->red_blocks, max_stencil_blocks) + 16);
+  c->counter = dalloc<unsigned>(4);
+  CK(cudaMemset(c->counter, 0, 4 * sizeof(unsigned)));
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaDeviceSynchronize());
+  c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = c.release();
+}
+
+}  // namespace hd
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* hd_last_error(void) { return g_last_error.c_str(); }
+
+#define HD_GUARD_BEGIN try {
+#define HD_GUARD_END                          \
+  }                                           \
+  catch (const hd::Error& e) {                \
+    g_last_error = e.what();                  \
+    return e.code;                            \
+  }                                           \
+  catch (const std::exception& e) {           \
+    g_last_error = e.what();                  \
+    return HD_ERR_INVALID;                    \
+  }                                           \
+  return HD_OK;
+
+int hd_problem_per_dim(const hd_problem* pb) {
+  if (!pb) return -1;
+  return pb->elements + pb->order - 2;  // both ends (all faces) Dirichlet
+}
+
+hd_status hd_assemble(const hd_problem* pb, double* stiffness_band, double* mass_band, double* interval_mass,
+                      double* rhs) {
+  HD_GUARD_BEGIN
+  if (!pb || !stiffness_band || !mass_band || !rhs) throw Error(HD_ERR_INVALID, "null argument");
+  if (pb->dim != 1 && pb->dim != 2) throw Error(HD_ERR_INVALID, "dim must be 1 or 2");
+  if (pb->order < 1 || pb->order > 6 || pb->elements < 1) throw Error(HD_ERR_INVALID, "bad order/elements");
+  const Forms1d f = assemble_forms_1d(pb->elements, pb->order);
+  const int nb = f.kv.basis_count();
+  std::vector<int> kept;
+  for (int j = 1; j < nb - 1; ++j) kept.push_back(j);  // Dirichlet at both ends / all faces
+  const int n = static_cast<int>(kept.size());
+  const Band S1 = reduce(f.stiffness, kept), M1 = reduce(f.mass, kept);
+  std::memcpy(stiffness_band, S1.a.data(), S1.a.size() * sizeof(double));
+  std::memcpy(mass_band, M1.a.data(), M1.a.size() * sizeof(double));
+  if (interval_mass) {
+    for (int b = 0; b < 4; ++b) {
+      const Band Bb = reduce(mass_on_interval(f.kv, 0.25 * b, 0.25 * (b + 1)), kept);
+      std::memcpy(interval_mass + static_cast<size_t>(b) * Bb.a.size(), Bb.a.data(), Bb.a.size() * sizeof(double));
+    }
+  }
+  std::vector<double> phi(n);
+  for (int i = 0; i < n; ++i) phi[i] = bspline_value(f.kv, f.kv.degree, kept[i], 0.5);
+  if (pb->dim == 1) {
+    for (int i = 0; i < n; ++i) {
+      rhs[2 * i] = phi[i];
+      rhs[2 * i + 1] = 0.0;
+    }
+  } else {
+    for (int iy = 0; iy < n; ++iy)
+      for (int ix = 0; ix < n; ++ix) {
+        const size_t g = static_cast<size_t>(iy) * n + ix;
+        rhs[2 * g] = phi[iy] * phi[ix];
+        rhs[2 * g + 1] = 0.0;
+      }
+  }
+  HD_GUARD_END
+}
+
+hd_status hd_create(const hd_system* sys, const hd_precond* spec, const int* devices, int n_devices, hd_ctx** out) {
+  HD_GUARD_BEGIN
+  create_ctx(sys, spec, devices, n_devices, out);
+  HD_GUARD_END
+}
+
+static hd_status solve_impl(hd_ctx* c, const hd_gmres* opt, const double* rhs, bool rhs_dev, double* x_out,
+                            bool x_dev, double* residuals_out, hd_report* report) {
+  HD_GUARD_BEGIN
+  if (!c || !opt || !rhs || !x_out) throw Error(HD_ERR_INVALID, "null argument");
+  if (opt->max_iterations < 0) throw Error(HD_ERR_INVALID, "max_iterations < 0");
+  CK(cudaSetDevice(c->device));
+  const size_t N = c->N;
+  CK(cudaEventRecord(c->ev0, c->st));
+  CK(cudaMemcpyAsync(c->f, rhs, N * sizeof(double2), rhs_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     c->st));
+  double2* xd = x_dev ? reinterpret_cast<double2*>(x_out) : c->x;
+  hd_gmres o = *opt;
+  SolveOut r;
+  if (o.max_iterations == 0) {
+    // degenerate budget: only the start vector and its monitor
+    o.max_iterations = 1;
+    ensure_gmres(c, 1);
+  }
+  r = run_solve(c, *opt, xd);
+  if (!x_dev) CK(cudaMemcpyAsync(x_out, xd, N * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaEventRecord(c->ev1, c->st));
+  CK(cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  if (residuals_out)
+    for (size_t i = 0; i < r.residuals.size(); ++i) residuals_out[i] = r.residuals[i];
+  if (report) {
+    report->iterations = r.iterations;
+    report->converged = r.converged ? 1 : 0;
+    report->matvecs = c->matvecs;
+    report->coarse_solves = c->coarse_solves;
+    report->shift_solves = c->shift_solves;
+    report->vcycles = c->vcycles;
+    report->t_setup_s = c->t_setup;
+    report->t_solve_s = ms * 1e-3;
+    report->kernel_launches = c->launches;
+  }
+  HD_GUARD_END
+}
+
+hd_status hd_solve(hd_ctx* c, const hd_gmres* opt, const double* rhs, double* x_out, double* residuals_out,
+                   hd_report* report) {
+  return solve_impl(c, opt, rhs, false, x_out, false, residuals_out, report);
+}
+
+hd_status hd_solve_device(hd_ctx* c, const hd_gmres* opt, const double* d_rhs, double* d_x, double* residuals_out,
+                          hd_report* report) {
+  return solve_impl(c, opt, d_rhs, true, d_x, true, residuals_out, report);
+}
+
+long hd_size(const hd_ctx* c) { return c ? static_cast<long>(c->N) : -1; }
+int hd_levels(const hd_ctx* c) { return c ? static_cast<int>(c->lev.size()) : -1; }
+
+hd_status hd_apply(hd_ctx* c, int which, const double* d_x, double* d_y) {
+  HD_GUARD_BEGIN
+  if (!c || !d_x || !d_y) throw Error(HD_ERR_INVALID, "null argument");
+  CK(cudaSetDevice(c->device));
+  const double2* x = reinterpret_cast<const double2*>(d_x);
+  double2* yv = reinterpret_cast<double2*>(d_y);
+  switch (which) {
+    case HD_APPLY_A: op_apply(c, OP_APPLY, opA(c), x, nullptr, yv); break;
+    case HD_APPLY_SHIFTED: op_apply(c, OP_APPLY, level_dev(c->fine, c->cM, c->corner), x, nullptr, yv); break;
+    case HD_APPLY_MG:
+      if (!c->spec.shift) throw Error(HD_ERR_INVALID, "no multigrid in this context");
+      mg_solve(c, x, yv);
+      break;
+    case HD_APPLY_PROJECT:
+      if (!c->spec.deflate) throw Error(HD_ERR_INVALID, "no deflation in this context");
+      project(c, x, yv);
+      break;
+    case HD_APPLY_Q:
+      if (!c->spec.deflate) throw Error(HD_ERR_INVALID, "no deflation in this context");
+      apply_Q(c, x, yv);
+      break;
+    case HD_APPLY_OP: compose_op(c, x, yv); break;
+    default: throw Error(HD_ERR_INVALID, "unknown apply selector");
+  }
+  CK(cudaStreamSynchronize(c->st));
+  HD_GUARD_END
+}
+
+int hd_level_size(const hd_ctx* c, int level) {
+  if (!c || level < 0 || level >= static_cast<int>(c->lev.size())) return -1;
+  return c->lev[level].n;
+}
+
+hd_status hd_debug_level(hd_ctx* c, int which, int level, const double* d_x, double* d_y) {
+  HD_GUARD_BEGIN
+  if (!c || !d_x || !d_y) throw Error(HD_ERR_INVALID, "null argument");
+  if (level < 0 || level >= static_cast<int>(c->lev.size())) throw Error(HD_ERR_INVALID, "bad level");
+  CK(cudaSetDevice(c->device));
+  const double2* x = reinterpret_cast<const double2*>(d_x);
+  double2* yv = reinterpret_cast<double2*>(d_y);
+  const LevelDev L = level_dev(c->lev[level], c->cM, level == 0 ? c->corner : cmk(0.0, 0.0));
+  const bool has_next = level + 1 < static_cast<int>(c->lev.size());
+  switch (which) {
+    case 0: op_apply(c, OP_APPLY, L, x, nullptr, yv); break;
+    case 1: jacobi0(c, L, x, yv, c->spec.omega); break;
+    case 2: op_apply(c, OP_JACOBI, L, x, x, yv, c->spec.omega); break;
+    case 3: op_apply(c, OP_RESID, L, x, x, yv); break;
+    case 4:
+      if (!has_next) throw Error(HD_ERR_INVALID, "no coarser level");
+      restrict_(c, Stencil{0, 0.0}, x, L.n, c->lev[level + 1].n, yv, nullptr);
+      break;
+    case 5:
+      if (!has_next) throw Error(HD_ERR_INVALID, "no coarser level");
+      prolong_<0>(c, Stencil{0, 0.0}, x, nullptr, L.n, c->lev[level + 1].n, nullptr, yv);
+      break;
+    case 6: coarsest_solve(c, x, yv); break;
+    default: throw Error(HD_ERR_INVALID, "unknown debug selector");
+  }
+  CK(cudaStreamSynchronize(c->st));
+  HD_GUARD_END
+}
+
+void hd_destroy(hd_ctx* c) { destroy_ctx(c); }
+
+}  // extern "C"
