@@ -1,0 +1,343 @@
+#!/usr/bin/env python3
+"""Benchmark of the deflated multigrid-CSLP GMRES solve (BASELINE.json metric:
+preconditioned GMRES iterations/s & time-to-solution; achieved HBM GB/s).
+
+One "step" = one complete solve (hd_solve_device: transformed rhs, start
+vector, GMRES to tol 1e-7) of the workload on every rank.  Default workload:
+C5 = 2D point source, k = 1000, p = 3, 1600 x 1600 elements (N = 2,563,201
+complex doubles), DC_MG^1 with beta2 = 0.5, omega = 2/3, nu = 1 -- the largest
+BASELINE config and the one its roofline target names.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5]
+  python bench.py --impl reference ...   # the reference algorithm on the host CPU
+
+N > 1 (torchrun): every rank solves its own replica (weak scaling, no
+data-path collective).  Timing: CUDA events on the
+library's stream (set to torch's current stream), barrier + synchronize on
+both sides, max over ranks; the L2 is flushed (256 MiB write) between steps
+outside the timed events.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (dim, p, elements, k, extra)   -- BASELINE.json configs[]
+    "C1": (1, 2, 80, 50.0),
+    "C2": (1, 4, 31623, 1000.0),
+    "C3": (2, 2, 320, 200.0),
+    "C5": (2, 3, 1600, 1000.0),
+}
+SPEC = dict(tag="DC_MG", beta2="0.5", cycles=1, smoothing=1, omega=2.0 / 3.0)
+TOL, MAXIT = 1e-7, 100
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_name(cfg):
+    dim, p, ne, k = CONFIGS[cfg]
+    return f"{cfg}: {dim}D IgA Helmholtz point source, k={k:g}, p={p}, {ne}^{dim} elements, DC_MG^1 (beta2=0.5, omega=2/3, nu=1), GMRES tol 1e-7"
+
+
+# ---------------------------------------------------------------------------
+# CPU legs: the oracle restatement of the reference (test infrastructure)
+# ---------------------------------------------------------------------------
+def oracle_sample(cfg, iters, warm=0):
+    """Time `iters` GMRES iterations (after `warm` untimed ones) of the oracle
+    on the host; returns (iterations/s, seconds, note)."""
+    from oracle import helmdef_oracle as O
+    dim, p, ne, k = CONFIGS[cfg]
+    pb = O.point_source_2d(ne, p, k) if dim == 2 else O.point_source_1d(ne, p, k)
+    spec = O.to_spec(SPEC["tag"], p, k, beta2=SPEC["beta2"], cycles=SPEC["cycles"],
+                     smoothing=SPEC["smoothing"], omega=SPEC["omega"])
+    t0 = time.perf_counter()
+    s = O.assemble(pb)
+    big = dim == 2 and s.A.shape[0] > 300_000
+    setup = O.compose(s, spec, galerkin="kron" if dim == 2 else "sparse", e_solver="fd" if big else "splu")
+    t_setup = time.perf_counter() - t0
+    gen = O.gmres_steps(setup.op, setup.rhs, setup.start, setup.monitor, O.GmresOptions(MAXIT, TOL))
+    done = 0
+    t_start = None
+    res = None
+    tic = time.perf_counter()
+    for res in gen:
+        done += 1
+        if done == warm:
+            tic = time.perf_counter()
+        if done >= warm + iters or res.converged:
+            break
+    el = time.perf_counter() - tic
+    n = max(done - warm, 1)
+    note = (f"oracle port (scipy CSR SpMV + SuperLU/FD), first {warm}+{n} GMRES iterations of {cfg} "
+            f"after {t_setup:.1f}s untimed setup; E solve by {'fast diagonalisation' if big else 'SuperLU'}")
+    return n / el, el, note, t_setup
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    rate, el, note, t_setup = oracle_sample(args.config, args.steps, warm=args.warmup)
+    cores = cpu_threads()
+    line = {"metric": "preconditioned GMRES iterations/s", "value": rate, "unit": "iterations/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * el / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128 (f64 complex)", "data": "synthetic (deterministic point source)",
+            "config": {"workload": workload_name(args.config), "step": "one GMRES iteration (CPU sample)"},
+            "impl": "reference",
+            "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": cores, "kind": "port",
+                             "sample": note + "; SpMV single-threaded, BLAS threads=%d" % cores},
+            "e2e": {"value": rate, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """Samples SM clocks and throttle reasons through NVML during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, k): k for k in dir(nv) if k.startswith("nvmlClocksThrottleReason") and
+                 isinstance(getattr(nv, k), int)}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in names.items():
+                    if bit and (r & bit) == bit and name not in ("nvmlClocksThrottleReasonNone",
+                                                                  "nvmlClocksThrottleReasonAll",
+                                                                  "nvmlClocksThrottleReasonGpuIdle",
+                                                                  "nvmlClocksThrottleReasonApplicationsClocksSetting"):
+                        self.reasons.add(name.replace("nvmlClocksThrottleReason", ""))
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons)}
+
+
+def run_gpu(args):
+    import torch
+    import paper_2010_10232_b200 as hd
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    dim, p, ne, k = CONFIGS[args.config]
+    pb = hd.point_source_2d(ne, p, k) if dim == 2 else hd.point_source_1d(ne, p, k)
+    sys_ = hd.assemble(pb)
+    spec = hd.to_spec(SPEC["tag"], p, k, beta2=SPEC["beta2"], cycles=SPEC["cycles"], smoothing=SPEC["smoothing"],
+                      omega=SPEC["omega"])
+    opt = hd.GmresOptions(MAXIT, TOL)
+    N = sys_.size
+    solver = hd.Solver(sys_, spec, devices=[local])
+    stream = torch.cuda.current_stream(dev)
+    solver.set_stream(stream.cuda_stream)
+    rhs_d = torch.from_numpy(sys_.rhs.view(np.float64)).to(dev)
+    x_d = torch.zeros(2 * N, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        return solver.solve_device(rhs_d.data_ptr(), x_d.data_ptr(), opt)
+
+    for _ in range(args.warmup):
+        r = step()
+    torch.cuda.synchronize()
+    # --- timed region: K steps, per-step CUDA events, L2 flushed between steps
+    solver.profile(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    iters = 0
+    launches = 0
+    libcalls = 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            r = step()
+            evs[i][1].record(stream)
+            iters += r.iterations
+            launches += r.kernel_launches
+            libcalls += r.library_calls
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    times = [a.elapsed_time(b) for a, b in evs]
+    t_ms = float(sum(times))
+    prof = solver.profile_read()
+    solver.profile(False)
+    if dist:
+        tt = torch.tensor([t_ms, float(iters)], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tt.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        t_max, iters_all = float(mx[0]), float(sm[1])
+    else:
+        t_max, iters_all = t_ms, float(iters)
+    value = iters_all / (t_max * 1e-3)
+
+    # --- end to end through the public host-buffer API (pinned host memory)
+    rhs_h = torch.from_numpy(sys_.rhs.view(np.float64).copy()).pin_memory()
+    x_h = torch.zeros(2 * N, dtype=torch.float64).pin_memory()
+    import ctypes as C
+    from paper_2010_10232_b200 import HdGmres, HdReport, _check
+    res_h = np.zeros(MAXIT + 1)
+    e_iters = 0
+    e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    lib = hd.load_library()
+    o = HdGmres(opt.max_iterations, opt.tolerance)
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        rep = HdReport()
+        e_evs[i][0].record(stream)
+        _check(lib.hd_solve(solver._ctx, C.byref(o), C.cast(C.c_void_p(rhs_h.data_ptr()), C.POINTER(C.c_double)),
+                            C.cast(C.c_void_p(x_h.data_ptr()), C.POINTER(C.c_double)),
+                            res_h.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep)))
+        e_evs[i][1].record(stream)
+        e_iters += rep.iterations
+    torch.cuda.synchronize()
+    e_ms = float(sum(a.elapsed_time(b) for a, b in e_evs))
+    if dist:
+        tt = torch.tensor([e_ms, float(e_iters)], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tt.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        e_ms, e_iters = float(mx[0]), float(sm[1])
+    e2e = {"value": e_iters / (e_ms * 1e-3), "unit": "iterations/s", "h2d_bytes_per_step": 16 * N,
+           "d2h_bytes_per_step": 16 * N + 8 * (r.iterations), "ms_per_step": e_ms / args.steps}
+
+    # --- roofline of the dominant kernel kind (live CUDA events, algorithmic bytes)
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    roof = None
+    breakdown = {}
+    tot_prof_ms = sum(v[1] for v in prof.values()) or 1.0
+    for name, (n, ms, b) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        breakdown[name] = {"launches": n, "ms": round(ms, 3), "share": round(ms / tot_prof_ms, 4),
+                           "GBps": round(b / (ms * 1e-3) / 1e9, 1) if ms > 0 and b > 0 else None}
+    if dom:
+        name, (n, ms, b) = dom
+        ach = b / (ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "launches": n,
+                "bytes_per_launch": b / n, "us_per_launch": 1e3 * ms / n, "peak_source": peak_src}
+    # whole-solve effective bandwidth on the algorithmic bytes of all own kernels
+    all_b = sum(v[2] for k_, v in prof.items() if k_ != "lib_gemm")
+
+    line = {"metric": "preconditioned GMRES iterations/s", "value": value, "unit": "iterations/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64 complex)",
+            "data": "synthetic (deterministic point source, as the reference)",
+            "config": {"workload": workload_name(args.config), "N": N, "iterations_per_solve": r.iterations,
+                       "step": "one full solve (hd_solve_device)",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "l2": "flushed (256 MiB write) between steps, outside the timed events"},
+            "time_to_solution_ms": t_max / args.steps, "t_setup_s": r.t_setup,
+            "e2e": e2e, "gpu_launches": launches, "library_calls": libcalls,
+            "roofline": roof, "kernel_breakdown": breakdown,
+            "solve_effective_GBps": round(all_b / (tot_prof_ms * 1e-3) / 1e9, 1) if prof else None,
+            "clocks": clk.summary()}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rate, el, note, _ = oracle_sample(args.config, args.cpu_iters)
+        line["cpu_baseline"] = {"value": rate, "unit": "iterations/s", "cores": cpu_threads(), "kind": "port",
+                                "sample": note}
+    solver.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C5")
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -110,7 +110,8 @@ typedef struct {
   long vcycles;
   double t_setup_s;    /* hd_create: device hierarchy + factorisations        */
   double t_solve_s;    /* hd_solve: CUDA-event time of the whole solve          */
-  int kernel_launches; /* device kernels launched by the last hd_solve          */
+  int kernel_launches; /* own device kernels launched by the last hd_solve      */
+  int library_calls;   /* cuBLAS calls (coarse fast-diagonalisation GEMMs)     */
 } hd_report;
 
 typedef struct hd_ctx hd_ctx;
@@ -163,6 +164,19 @@ enum { HD_APPLY_A = 0, HD_APPLY_SHIFTED = 1, HD_APPLY_MG = 2, HD_APPLY_PROJECT =
  *   6: y = M_L^-1 x (coarsest level exact solve)                                      */
 hd_status hd_debug_level(hd_ctx* ctx, int which, int level, const double* d_x, double* d_y);
 int hd_level_size(const hd_ctx* ctx, int level);
+
+/* Run subsequent work of this context on an external CUDA stream
+ * (cudaStream_t passed as void*; NULL restores the context's own stream). */
+hd_status hd_set_stream(hd_ctx* ctx, void* stream);
+
+/* Per-launch profiling: when enabled, every device launch of the next solves
+ * is bracketed by CUDA events on the launch stream and tagged with its kind
+ * and algorithmic bytes (compulsory HBM traffic of that launch).  hd_profile
+ * (enable) also clears previous records; hd_profile_read sums one kind. */
+enum { HD_K_OP_FINE = 0, HD_K_OP_COARSE = 1, HD_K_JACOBI0 = 2, HD_K_TRANSFER = 3, HD_K_EXACT = 4,
+       HD_K_MGS = 5, HD_K_ITERATE = 6, HD_K_VEC = 7, HD_K_GIVENS = 8, HD_K_LIBGEMM = 9, HD_K_COUNT = 10 };
+hd_status hd_profile(hd_ctx* ctx, int enable);
+hd_status hd_profile_read(hd_ctx* ctx, int kind, long* launches, double* ms, double* bytes);
 
 void hd_destroy(hd_ctx* ctx);
 const char* hd_last_error(void);

@@ -38,7 +38,10 @@ HD_APPLY_A, HD_APPLY_SHIFTED, HD_APPLY_MG, HD_APPLY_PROJECT, HD_APPLY_OP, HD_APP
 
 # Every symbol include/helmdef_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = ["hd_problem_per_dim", "hd_assemble", "hd_create", "hd_solve", "hd_solve_device", "hd_size",
-           "hd_levels", "hd_apply", "hd_debug_level", "hd_level_size", "hd_destroy", "hd_last_error"]
+           "hd_levels", "hd_apply", "hd_debug_level", "hd_level_size", "hd_set_stream", "hd_profile",
+           "hd_profile_read", "hd_destroy", "hd_last_error"]
+KERNEL_KINDS = ["op_fine", "op_coarse", "jacobi0", "transfer", "exact", "mgs", "iterate", "vec", "givens",
+                "lib_gemm"]
 
 
 class HdProblem(C.Structure):
@@ -65,7 +68,8 @@ class HdGmres(C.Structure):
 class HdReport(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("matvecs", C.c_long),
                 ("coarse_solves", C.c_long), ("shift_solves", C.c_long), ("vcycles", C.c_long),
-                ("t_setup_s", C.c_double), ("t_solve_s", C.c_double), ("kernel_launches", C.c_int)]
+                ("t_setup_s", C.c_double), ("t_solve_s", C.c_double), ("kernel_launches", C.c_int),
+                ("library_calls", C.c_int)]
 
 
 _lib = None
@@ -103,6 +107,13 @@ def load_library() -> C.CDLL:
     lib.hd_debug_level.restype = C.c_int
     lib.hd_level_size.argtypes = [C.c_void_p, C.c_int]
     lib.hd_level_size.restype = C.c_int
+    lib.hd_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+    lib.hd_set_stream.restype = C.c_int
+    lib.hd_profile.argtypes = [C.c_void_p, C.c_int]
+    lib.hd_profile.restype = C.c_int
+    lib.hd_profile_read.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_long), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]
+    lib.hd_profile_read.restype = C.c_int
     lib.hd_destroy.argtypes = [C.c_void_p]
     lib.hd_destroy.restype = None
     lib.hd_last_error.argtypes = []
@@ -251,6 +262,7 @@ class GmresResult:
     t_setup: float = 0.0
     t_solve: float = 0.0
     kernel_launches: int = 0
+    library_calls: int = 0
 
 
 def resolve_beta2(expr, k):  # src/harness.cpp:143-147
@@ -347,7 +359,7 @@ class Solver:
         return GmresResult(x, rep.iterations, bool(rep.converged), list(res[:max(rep.iterations, 1)])
                            if rep.iterations or rep.converged else [],
                            OperationCounts(rep.matvecs, rep.coarse_solves, rep.shift_solves, rep.vcycles),
-                           rep.t_setup_s, rep.t_solve_s, rep.kernel_launches)
+                           rep.t_setup_s, rep.t_solve_s, rep.kernel_launches, rep.library_calls)
 
     def solve(self, opt: GmresOptions = GmresOptions(), rhs: Optional[np.ndarray] = None) -> GmresResult:
         """Host buffers in/out (hd_solve)."""
@@ -368,6 +380,24 @@ class Solver:
         _check(self._lib.hd_solve_device(self._ctx, C.byref(o), C.c_void_p(d_rhs_ptr), C.c_void_p(d_x_ptr),
                                          _dp(res), C.byref(rep)))
         return self._result(rep, None, res)
+
+    def set_stream(self, stream_handle: int):
+        """Run on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); 0 = own stream."""
+        _check(self._lib.hd_set_stream(self._ctx, C.c_void_p(stream_handle or None)))
+
+    def profile(self, enable: bool = True):
+        """Enable per-launch CUDA-event timing of subsequent solves (clears old records)."""
+        _check(self._lib.hd_profile(self._ctx, int(enable)))
+
+    def profile_read(self) -> dict:
+        """{kind: (launches, ms, algorithmic_bytes)} of the profiled solves."""
+        out = {}
+        for i, name in enumerate(KERNEL_KINDS):
+            n, ms, b = C.c_long(), C.c_double(), C.c_double()
+            _check(self._lib.hd_profile_read(self._ctx, i, C.byref(n), C.byref(ms), C.byref(b)))
+            if n.value:
+                out[name] = (n.value, ms.value, b.value)
+        return out
 
     def debug_level(self, which: int, level: int, d_x_ptr: int, d_y_ptr: int):
         """Test hook on one multigrid level (see hd_debug_level in include/helmdef_b200.h)."""

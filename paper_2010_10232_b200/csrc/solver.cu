@@ -126,9 +126,17 @@ struct hd_ctx {
   int red_blocks = 0;
   // counters
   long matvecs = 0, coarse_solves = 0, shift_solves = 0, vcycles = 0;
-  int launches = 0;
+  int launches = 0;             // own kernels launched in the last solve
+  int lib_calls = 0;            // cuBLAS calls in the last solve
   double t_setup = 0.0;
+  // per-launch event timing (hd_profile)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_ev;
+  size_t prof_used = 0;
+  struct ProfRec { int kind; size_t ev; double bytes; };
+  std::vector<ProfRec> prof_recs;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t own_st = nullptr;  // the context's own stream while an external one is set
 };
 
 namespace hd {
@@ -258,8 +266,38 @@ static void free_exact(ExactSolver& X) {
 }
 
 // ---------------------------------------------------------------------------
-// launch helpers
+// launch helpers + per-launch profiling (CUDA events on the launch stream)
 // ---------------------------------------------------------------------------
+static size_t prof_mark(hd_ctx* c) {
+  if (!c->prof_on) return static_cast<size_t>(-1);
+  if (c->prof_used >= c->prof_ev.size()) {
+    const size_t grow = std::max<size_t>(1024, c->prof_ev.size());
+    for (size_t i = 0; i < grow; ++i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->prof_ev.push_back(e);
+    }
+  }
+  CK(cudaEventRecord(c->prof_ev[c->prof_used], c->st));
+  return c->prof_used++;
+}
+
+// called right after a launch: error check, launch count, profile record
+static void launched(hd_ctx* c, int kind, size_t mark, double bytes, bool library = false) {
+  CK(cudaGetLastError());
+  if (library) ++c->lib_calls;
+  else ++c->launches;
+  if (mark == static_cast<size_t>(-1)) return;
+  prof_mark(c);
+  c->prof_recs.push_back({kind, mark, bytes});
+}
+
+#define HD_LAUNCH(kind, bytes, ...)        \
+  do {                                     \
+    const size_t mk_ = prof_mark(c);       \
+    __VA_ARGS__;                           \
+    launched(c, (kind), mk_, (bytes));     \
+  } while (0)
 static int grid_for(size_t N, int threads = 256, int cap = 148 * 8) {
   const size_t g = (N + threads - 1) / threads;
   return static_cast<int>(std::max<size_t>(1, std::min<size_t>(g, cap)));
@@ -273,11 +311,22 @@ static int strip_rows(int n) {
   return ry;
 }
 
+// algorithmic bytes of one operator launch: x read + output (+ b read)
+static double op_bytes(int mode, size_t NL) {
+  const double P = 16.0 * static_cast<double>(NL);
+  switch (mode) {
+    case OP_APPLY: return 2 * P;
+    case OP_RESNORM: return 2 * P;
+    default: return 3 * P;
+  }
+}
+
 template <int MODE>
 static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
-                             double omega, RedOut red) {
+                             double omega, RedOut red, int kind) {
   const int ry = strip_rows(L.n);
   dim3 grid((L.n + kTX - 1) / kTX, (L.n + ry - 1) / ry);
+  const size_t mk = prof_mark(c);
   switch (L.b) {
 #define HD_CASE(BB) \
   case BB: k_op2d<BB, MODE><<<grid, kTX, 0, c->st>>>(L, x, b, out, omega, ry, red); break;
@@ -285,8 +334,7 @@ static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, con
 #undef HD_CASE
     default: throw Error(HD_ERR_INVALID, "band half-width " + std::to_string(L.b) + " unsupported");
   }
-  CK(cudaGetLastError());
-  ++c->launches;
+  launched(c, kind, mk, op_bytes(MODE, static_cast<size_t>(L.n) * L.n));
 }
 
 static RedOut red_of(hd_ctx* c, double* dst = nullptr, double scale = 1.0) {
@@ -302,50 +350,50 @@ static RedOut red_of(hd_ctx* c, double* dst = nullptr, double scale = 1.0) {
 static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, const double2* b, double2* out,
                      double omega = 0.0, double* dst = nullptr, double scale = 1.0) {
   RedOut red = red_of(c, dst, scale);
+  const int kind = L.n == c->n ? HD_K_OP_FINE : HD_K_OP_COARSE;
   if (c->dim == 2) {
     switch (mode) {
-      case OP_APPLY: launch_op2d_mode<OP_APPLY>(c, L, x, b, out, omega, red); break;
-      case OP_RESID: launch_op2d_mode<OP_RESID>(c, L, x, b, out, omega, red); break;
-      case OP_JACOBI: launch_op2d_mode<OP_JACOBI>(c, L, x, b, out, omega, red); break;
-      default: launch_op2d_mode<OP_RESNORM>(c, L, x, b, out, omega, red); break;
+      case OP_APPLY: launch_op2d_mode<OP_APPLY>(c, L, x, b, out, omega, red, kind); break;
+      case OP_RESID: launch_op2d_mode<OP_RESID>(c, L, x, b, out, omega, red, kind); break;
+      case OP_JACOBI: launch_op2d_mode<OP_JACOBI>(c, L, x, b, out, omega, red, kind); break;
+      default: launch_op2d_mode<OP_RESNORM>(c, L, x, b, out, omega, red, kind); break;
     }
   } else {
     const int grid = mode == OP_RESNORM ? std::min(grid_for(L.n), c->red_blocks) : grid_for(L.n);
+    const size_t mk = prof_mark(c);
     switch (mode) {
       case OP_APPLY: k_op1d<OP_APPLY><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
       case OP_RESID: k_op1d<OP_RESID><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
       case OP_JACOBI: k_op1d<OP_JACOBI><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
       default: k_op1d<OP_RESNORM><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
     }
-    CK(cudaGetLastError());
-    ++c->launches;
+    launched(c, kind, mk, op_bytes(mode, L.n));
   }
 }
 
 static void jacobi0(hd_ctx* c, const LevelDev& L, const double2* b, double2* out, double omega) {
   const size_t NN = c->dim == 2 ? static_cast<size_t>(L.n) * L.n : L.n;
-  if (c->dim == 2) k_jacobi0_2d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega);
-  else k_jacobi0_1d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega);
-  CK(cudaGetLastError());
-  ++c->launches;
+  HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,
+            if (c->dim == 2) k_jacobi0_2d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega);
+            else k_jacobi0_1d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega));
 }
 
 static void restrict_(hd_ctx* c, Stencil z, const double2* r, int nf, int nc, double2* outc, double* outp) {
   const size_t NC = c->dim == 2 ? static_cast<size_t>(nc) * nc : nc;
-  if (c->dim == 2) k_restrict<2><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp);
-  else k_restrict<1><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp);
-  CK(cudaGetLastError());
-  ++c->launches;
+  const double NF = c->dim == 2 ? static_cast<double>(nf) * nf : nf;
+  HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NF + NC),
+            if (c->dim == 2) k_restrict<2><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp);
+            else k_restrict<1><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp));
 }
 
 template <int PMODE>
 static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, int nf, int nc, const double2* s,
                      double2* out) {
   const size_t NF = c->dim == 2 ? static_cast<size_t>(nf) * nf : nf;
-  if (c->dim == 2) k_prolong<2, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out);
-  else k_prolong<1, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out);
-  CK(cudaGetLastError());
-  ++c->launches;
+  const double NC = c->dim == 2 ? static_cast<double>(nc) * nc : nc;
+  HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NC + (PMODE == 2 ? 1.0 : 2.0) * NF),
+            if (c->dim == 2) k_prolong<2, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out);
+            else k_prolong<1, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out));
 }
 
 // Exact solve: in/out planar (2D FD) or via the banded LU (1D).
@@ -354,36 +402,41 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
     const int n = X.n;
     const long nn = static_cast<long>(n) * n;
     const double one = 1.0, zero = 0.0;
+    const double gb = 16.0 * nn * 2 + 8.0 * nn;  // planar in/out + V  (bytes of one GEMM)
+    size_t mk = prof_mark(c);
     // T1 = V^T [Xre | Xim]
     CKB(cublasDgemm(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, inout, n, &zero, X.T1, n));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    mk = prof_mark(c);
     // T2_plane = T1_plane V
     CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, X.T1, n, nn, X.V, n, 0, &zero,
                                   X.T2, n, nn, 2));
-    k_fd_scale<<<grid_for(nn), 256, 0, c->st>>>(X.T2, X.Dinv, nn);
-    CK(cudaGetLastError());
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    HD_LAUNCH(HD_K_EXACT, 48.0 * nn, k_fd_scale<<<grid_for(nn), 256, 0, c->st>>>(X.T2, X.Dinv, nn));
+    mk = prof_mark(c);
     // T1 = V [T2re | T2im]
     CKB(cublasDgemm(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, X.T2, n, &zero, X.T1, n));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    mk = prof_mark(c);
     // out_plane = T1_plane V^T
     CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, n, n, n, &one, X.T1, n, nn, X.V, n, 0, &zero,
                                   inout, n, nn, 2));
-    c->launches += 5;
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
   } else {
-    k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, nullptr, inout, X.work, nullptr, inout);
-    CK(cudaGetLastError());
-    ++c->launches;
+    HD_LAUNCH(HD_K_EXACT, 32.0 * X.n,
+              k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, nullptr, inout, X.work, nullptr,
+                                                  inout));
   }
 }
 
 // coarsest multigrid level: interleaved in/out
 static void coarsest_solve(hd_ctx* c, const double2* b, double2* out) {
   ExactSolver& X = c->coarsest;
-  if (X.dim == 2) {
-    k_fd_small<<<1, 1024, 0, c->st>>>(X.V, X.Dinv, X.n, b, out);
-  } else {
-    k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, b, nullptr, X.work, out, nullptr);
-  }
-  CK(cudaGetLastError());
-  ++c->launches;
+  const double NL = X.dim == 2 ? static_cast<double>(X.n) * X.n : X.n;
+  HD_LAUNCH(HD_K_EXACT, 32.0 * NL,
+            if (X.dim == 2) k_fd_small<<<1, 1024, 0, c->st>>>(X.V, X.Dinv, X.n, b, out);
+            else k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, b, nullptr, X.work, out,
+                                                     nullptr));
 }
 
 static size_t lsize(const hd_ctx* c, int n) { return c->dim == 2 ? static_cast<size_t>(n) * n : n; }
@@ -536,11 +589,11 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   const int maxit = opt.max_iterations;
   ensure_gmres(c, std::max(maxit, 1));
   c->matvecs = c->coarse_solves = c->shift_solves = c->vcycles = 0;
-  c->launches = 0;
+  c->launches = c->lib_calls = 0;
   const int nb = c->red_blocks;
+  const double P = 16.0 * static_cast<double>(N);
   // ||f|| (monitor scale, src/precond.cpp:258)
-  k_axpy_norm<<<nb, 256, 0, c->st>>>(c->f, nullptr, nullptr, N, red_of(c, c->dres + 3), c->scal + 2);
-  ++c->launches;
+  HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->f, nullptr, nullptr, N, red_of(c, c->dres + 3), c->scal + 2));
   // rhs' = P MG^-1 f   (src/precond.cpp:247-253)
   const double2* b = c->f;
   if (c->spec.shift) {
@@ -581,9 +634,8 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   }
   // r = rhs' - op(x0); beta = ||r||; V0 = r / beta  (src/linalg.cpp:24-33)
   compose_op(c, c->x0, c->w);
-  k_sub<<<grid_for(N), 256, 0, c->st>>>(c->rhsp, c->w, c->w, N);
-  k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, nullptr, nullptr, N, red_of(c, c->dres + 2), c->g);
-  c->launches += 2;
+  HD_LAUNCH(HD_K_VEC, 3 * P, k_sub<<<grid_for(N), 256, 0, c->st>>>(c->rhsp, c->w, c->w, N));
+  HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, nullptr, nullptr, N, red_of(c, c->dres + 2), c->g));
   read_scalars(c);
   const double beta = c->hres[2];
   if (beta == 0.0) {
@@ -595,23 +647,23 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   }
   CK(cudaMemsetAsync(c->H, 0, sizeof(double2) * (maxit + 1) * maxit, c->st));
   CK(cudaMemsetAsync(c->g + 1, 0, sizeof(double2) * maxit, c->st));
-  k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V, c->w, c->dres + 2, N);
-  ++c->launches;
+  HD_LAUNCH(HD_K_VEC, 2 * P, k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V, c->w, c->dres + 2, N));
   const int ldh = maxit + 1;
   for (int j = 0; j < maxit; ++j) {
     double2* Vj = c->V + static_cast<size_t>(j) * N;
     compose_op(c, Vj, c->w);
     double2* Hj = c->H + static_cast<size_t>(j) * ldh;
     // modified Gram-Schmidt (src/linalg.cpp:42-47)
-    k_dot<<<nb, 256, 0, c->st>>>(c->V, c->w, N, red_of(c), Hj + 0);
+    HD_LAUNCH(HD_K_MGS, 2 * P, k_dot<<<nb, 256, 0, c->st>>>(c->V, c->w, N, red_of(c), Hj + 0));
     for (int i = 0; i < j; ++i)
-      k_axpy_dot<<<nb, 256, 0, c->st>>>(c->w, c->V + static_cast<size_t>(i) * N, Hj + i,
-                                        c->V + static_cast<size_t>(i + 1) * N, N, red_of(c), Hj + i + 1);
-    k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, Vj, Hj + j, N, red_of(c, c->dres + 1), Hj + j + 1);
-    k_givens<<<1, 32, 0, c->st>>>(c->H, ldh, c->g, c->cs, c->sn, c->y, j);
-    k_iterate<<<grid_for(N), 256, 0, c->st>>>(xout, c->x0, c->V, c->y, j + 1, N);
-    c->launches += j + 4;
-    CK(cudaGetLastError());
+      HD_LAUNCH(HD_K_MGS, 4 * P,
+                k_axpy_dot<<<nb, 256, 0, c->st>>>(c->w, c->V + static_cast<size_t>(i) * N, Hj + i,
+                                                  c->V + static_cast<size_t>(i + 1) * N, N, red_of(c), Hj + i + 1));
+    HD_LAUNCH(HD_K_MGS, 3 * P,
+              k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, Vj, Hj + j, N, red_of(c, c->dres + 1), Hj + j + 1));
+    HD_LAUNCH(HD_K_GIVENS, 0.0, k_givens<<<1, 32, 0, c->st>>>(c->H, ldh, c->g, c->cs, c->sn, c->y, j));
+    HD_LAUNCH(HD_K_ITERATE, (j + 3) * P,
+              k_iterate<<<grid_for(N), 256, 0, c->st>>>(xout, c->x0, c->V, c->y, j + 1, N));
     res.iterations = j + 1;
     monitor(xout);
     read_scalars(c);
@@ -624,8 +676,9 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
     }
     if (hnew < 1e-300) break;
     if (j + 1 < maxit) {
-      k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V + static_cast<size_t>(j + 1) * N, c->w, c->dres + 1, N);
-      ++c->launches;
+      HD_LAUNCH(HD_K_VEC, 2 * P,
+                k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V + static_cast<size_t>(j + 1) * N, c->w, c->dres + 1,
+                                                            N));
     }
   }
   return res;
@@ -653,7 +706,9 @@ static void destroy_ctx(hd_ctx* c) {
   if (c->cb) cublasDestroy(c->cb);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
-  if (c->st) cudaStreamDestroy(c->st);
+  for (auto e : c->prof_ev) cudaEventDestroy(e);
+  cudaStream_t mine = c->own_st ? c->own_st : c->st;
+  if (mine) cudaStreamDestroy(mine);
   delete c;
 }
 
@@ -883,6 +938,7 @@ static hd_status solve_impl(hd_ctx* c, const hd_gmres* opt, const double* rhs, b
     report->t_setup_s = c->t_setup;
     report->t_solve_s = ms * 1e-3;
     report->kernel_launches = c->launches;
+    report->library_calls = c->lib_calls;
   }
   HD_GUARD_END
 }
@@ -925,6 +981,47 @@ hd_status hd_apply(hd_ctx* c, int which, const double* d_x, double* d_y) {
     default: throw Error(HD_ERR_INVALID, "unknown apply selector");
   }
   CK(cudaStreamSynchronize(c->st));
+  HD_GUARD_END
+}
+
+hd_status hd_set_stream(hd_ctx* c, void* stream) {
+  HD_GUARD_BEGIN
+  if (!c) throw Error(HD_ERR_INVALID, "null context");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->st));
+  if (!c->own_st) c->own_st = c->st;
+  c->st = stream ? static_cast<cudaStream_t>(stream) : c->own_st;
+  CKB(cublasSetStream(c->cb, c->st));
+  HD_GUARD_END
+}
+
+hd_status hd_profile(hd_ctx* c, int enable) {
+  HD_GUARD_BEGIN
+  if (!c) throw Error(HD_ERR_INVALID, "null context");
+  CK(cudaStreamSynchronize(c->st));
+  c->prof_on = enable != 0;
+  c->prof_used = 0;
+  c->prof_recs.clear();
+  HD_GUARD_END
+}
+
+hd_status hd_profile_read(hd_ctx* c, int kind, long* launches, double* ms, double* bytes) {
+  HD_GUARD_BEGIN
+  if (!c || !launches || !ms || !bytes) throw Error(HD_ERR_INVALID, "null argument");
+  CK(cudaStreamSynchronize(c->st));
+  long n = 0;
+  double t = 0.0, b = 0.0;
+  for (const auto& r : c->prof_recs) {
+    if (r.kind != kind) continue;
+    float e = 0.f;
+    CK(cudaEventElapsedTime(&e, c->prof_ev[r.ev], c->prof_ev[r.ev + 1]));
+    ++n;
+    t += e;
+    b += r.bytes;
+  }
+  *launches = n;
+  *ms = t;
+  *bytes = b;
   HD_GUARD_END
 }
 
