@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -27,6 +28,8 @@
 #include "host/assembly.hpp"
 #include "host/banded.hpp"
 #include "kernels.cuh"
+#include "arnoldi.cuh"
+#include "arnoldi_lowsync.cuh"
 
 namespace hd {
 
@@ -124,6 +127,25 @@ struct hd_ctx {
   double2* partials = nullptr;
   unsigned* counter = nullptr;
   int red_blocks = 0;
+  // persistent Arnoldi tail (arnoldi.cuh)
+  bool use_arnoldi = false;
+  int arn_G = 0, arn_K = 0;
+  size_t arn_chunk = 0, arn_smem = 0;
+  int* dj = nullptr;
+  double2* arn_partials = nullptr;
+  int arn_maxit = -1;
+  unsigned* arn_bar = nullptr;
+  unsigned long long* arn_trace = nullptr;  // HD_TRACE: phase timestamps of the last launch
+  double arn_phase_ns[4] = {0, 0, 0, 0};
+  // Arnoldi engine: 2 = one-reduction ICWY-MGS streaming passes (default),
+  // 1 = persistent exact-order MGS chain, 0 = one kernel per MGS step.
+  int arn_mode = 2;
+  // one-reduction engine state (arnoldi_lowsync.cuh)
+  double* lsa_sig = nullptr;
+  double2 *lsa_L = nullptr, *lsa_ch = nullptr, *lsa_cx = nullptr, *lsa_partials = nullptr;
+  unsigned* lsa_counter = nullptr;
+  int lsa_G = 0, lsa_maxit = -1;
+  size_t lsa_givens_smem = 0;
   // counters
   long matvecs = 0, coarse_solves = 0, shift_solves = 0, vcycles = 0;
   int launches = 0;             // own kernels launched in the last solve
@@ -554,6 +576,74 @@ static void compose_op(hd_ctx* c, const double2* v, double2* out) {
   }
 }
 
+// Chooses the persistent Arnoldi geometry: G CTAs of kArnBD threads (<= one
+// per SM), each owning `chunk` elements, K per thread; shared memory holds the
+// non-register part of w and, in block 0, the packed R of the back substitution.
+static void setup_arnoldi(hd_ctx* c, int maxit) {
+  int dev_sms = 0, smem_optin = 0;
+  CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
+  CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  const size_t N = c->N;
+  const size_t per_thread_target = 4;
+  int G = static_cast<int>(std::min<size_t>(dev_sms, std::max<size_t>(1, (N + kArnBD * per_thread_target - 1) /
+                                                                             (kArnBD * per_thread_target))));
+  const size_t chunk = (N + G - 1) / G;
+  const int K = static_cast<int>((chunk + kArnBD - 1) / kArnBD);
+  const size_t w_smem = static_cast<size_t>(std::max(0, K - kArnRW)) * kArnBD * sizeof(double2);
+  const size_t r_smem = (static_cast<size_t>(maxit + 1) * (maxit + 2) / 2 + 4 * (maxit + 2) + 8) * sizeof(double2);
+  const size_t smem = std::max(w_smem, r_smem);
+  c->use_arnoldi = false;
+  if (maxit > 127) return;  // y staged in 128 shared slots
+  if (smem + 4096 > static_cast<size_t>(smem_optin)) return;  // w does not fit on chip: per-step kernels
+  CK(cudaFuncSetAttribute(k_arnoldi<kArnRW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi<kArnRW>, kArnBD, smem));
+  if (per_sm < 1) return;
+  c->arn_G = G;
+  c->arn_K = K;
+  c->arn_chunk = chunk;
+  c->arn_smem = smem;
+  if (!c->dj) c->dj = dalloc<int>(4);
+  if (!c->arn_partials) c->arn_partials = dalloc<double2>(2 * static_cast<size_t>(dev_sms) + 8);
+  if (!c->arn_bar) c->arn_bar = dalloc<unsigned>(4);
+  if (!c->arn_trace && std::getenv("HD_TRACE")) {
+    CK(cudaMallocHost(&c->arn_trace, 8 * sizeof(unsigned long long)));
+  }
+  c->use_arnoldi = true;
+}
+
+static void launch_arnoldi(hd_ctx* c, double2* xout, int maxit, const int* done, double bytes) {
+  ArnoldiArgs a;
+  a.V = c->V;
+  a.Vw = c->V;
+  a.w = c->w;
+  a.x0 = c->x0;
+  a.x = xout;
+  a.N = c->N;
+  a.dj = c->dj;
+  a.done = done;
+  a.H = c->H;
+  a.ldh = maxit + 1;
+  a.g = c->g;
+  a.cs = c->cs;
+  a.sn = c->sn;
+  a.y = c->y;
+  a.hnew_out = c->dres + 1;
+  a.partials = c->arn_partials;
+  a.bar = c->arn_bar;
+  a.K = c->arn_K;
+  a.chunk = c->arn_chunk;
+  a.trace = c->arn_trace;
+  CK(cudaMemsetAsync(c->arn_bar, 0, sizeof(unsigned), c->st));
+  void* args[] = {&a};
+  const double P = 16.0 * static_cast<double>(c->N);
+  (void)P;
+  const size_t mk = prof_mark(c);
+  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_arnoldi<kArnRW>), dim3(c->arn_G), dim3(kArnBD), args,
+                                 c->arn_smem, c->st));
+  launched(c, HD_K_MGS, mk, bytes);
+}
+
 static void ensure_gmres(hd_ctx* c, int maxit) {
   if (maxit + 1 > c->v_cap) {
     cudaFree(c->V);
@@ -569,7 +659,65 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
     c->y = dalloc<double2>(maxit);
     c->maxit_cap = maxit;
   }
+  if (maxit != c->arn_maxit) {
+    setup_arnoldi(c, maxit);
+    c->arn_maxit = maxit;
+  }
+  if (maxit != c->lsa_maxit && maxit + 1 <= kLsaMaxJ) {
+    int sms = 0, per = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lsa_dots, kLsaBD, 0));
+    int per2 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_lsa_update, kLsaBD, 0));
+    per = std::max(1, std::min(per, per2));
+    const size_t tiles = (c->N + static_cast<size_t>(kLsaBD) * kLsaTE - 1) / (static_cast<size_t>(kLsaBD) * kLsaTE);
+    c->lsa_G = static_cast<int>(std::max<size_t>(1, std::min<size_t>(tiles, static_cast<size_t>(sms) * per)));
+    cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
+    c->lsa_sig = dalloc<double>(maxit + 2);
+    c->lsa_L = dalloc<double2>(static_cast<size_t>(maxit + 1) * (maxit + 1));
+    c->lsa_ch = dalloc<double2>(maxit + 2);
+    c->lsa_cx = dalloc<double2>(maxit + 2);
+    c->lsa_partials = dalloc<double2>(static_cast<size_t>(c->lsa_G) * (2 * kLsaMaxJ + 2) + 8);
+    if (!c->lsa_counter) {
+      c->lsa_counter = dalloc<unsigned>(4);
+      CK(cudaMemset(c->lsa_counter, 0, 4 * sizeof(unsigned)));
+    }
+    const int m = maxit + 1;
+    c->lsa_givens_smem = (static_cast<size_t>(m) * (m + 1) / 2 + 4 * (m + 2) + 8) * sizeof(double2);
+    CK(cudaFuncSetAttribute(k_lsa_givens, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(c->lsa_givens_smem)));
+    c->lsa_maxit = maxit;
+  }
 }
+
+static LsaArgs lsa_args(hd_ctx* c, double2* xout, int j, int mode, int maxit) {
+  LsaArgs a;
+  a.U = c->V;
+  a.Uw = c->V;
+  a.w = c->w;
+  a.x0 = c->x0;
+  a.x = xout;
+  a.N = c->N;
+  a.j = j;
+  a.mode = mode;
+  a.sig = c->lsa_sig;
+  a.L = c->lsa_L;
+  a.ldl = maxit + 1;
+  a.H = c->H;
+  a.ldh = maxit + 1;
+  a.g = c->g;
+  a.cs = c->cs;
+  a.sn = c->sn;
+  a.ch = c->lsa_ch;
+  a.cx = c->lsa_cx;
+  a.hnew_out = c->dres + 1;
+  a.partials = c->lsa_partials;
+  a.counter = c->lsa_counter;
+  a.done = nullptr;
+  return a;
+}
+
+__global__ void k_inv_scalar(double* dst, const double* src) { *dst = *src > 0.0 ? 1.0 / *src : 0.0; }
 
 static void read_scalars(hd_ctx* c) {
   CK(cudaMemcpyAsync(c->hres, c->dres, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -649,7 +797,91 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   CK(cudaMemsetAsync(c->g + 1, 0, sizeof(double2) * maxit, c->st));
   HD_LAUNCH(HD_K_VEC, 2 * P, k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V, c->w, c->dres + 2, N));
   const int ldh = maxit + 1;
-  for (int j = 0; j < maxit; ++j) {
+  if (c->arn_mode == 2 && maxit + 1 <= kLsaMaxJ) {
+    // u_0 = r (unnormalised), sigma_0 = 1 / beta
+    CK(cudaMemcpyAsync(c->V, c->w, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    HD_LAUNCH(HD_K_VEC, 0.0, k_inv_scalar<<<1, 1, 0, c->st>>>(c->lsa_sig, c->dres + 2));
+    const int G = c->lsa_G;
+    bool stop = false;
+    double hnew_prev = 1.0;
+    for (int j = 0; j < maxit && !stop; ++j) {
+      // the op of iteration j is speculative until x_{j-1} is known not to
+      // have converged; its counts are rolled back if GMRES stops at j-1
+      const long snap[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
+      auto rollback = [&]() {
+        c->matvecs = snap[0];
+        c->coarse_solves = snap[1];
+        c->shift_solves = snap[2];
+        c->vcycles = snap[3];
+      };
+      compose_op(c, c->V + static_cast<size_t>(j) * N, c->w);
+      LsaArgs a = lsa_args(c, xout, j, 0, maxit);
+      HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 4.0 : 2.0) * P, k_lsa_dots<<<G, kLsaBD, 0, c->st>>>(a));
+      if (j >= 1) {  // x_{j-1} is ready: monitor it (the reference's iteration j-1)
+        monitor(xout);
+        read_scalars(c);
+        const double rr = c->hres[0];
+        res.iterations = j;
+        res.residuals.push_back(rr);
+        if (rr <= opt.tolerance) {
+          res.converged = true;
+          stop = true;
+          rollback();
+          break;
+        }
+        if (hnew_prev < 1e-300) {
+          stop = true;
+          rollback();
+          break;
+        }
+      }
+      HD_LAUNCH(HD_K_MGS, (j + 3.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a));
+      HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a, G));
+      CK(cudaMemcpyAsync(c->hres + 1, c->dres + 1, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      // hnew of this iteration is needed one iteration later (read with the next sync)
+      if (j + 1 == maxit) {
+        // budget exhausted: x_{maxit-1} by an iterate-only pass, then its monitor
+        LsaArgs b = lsa_args(c, xout, j, 1, maxit);
+        HD_LAUNCH(HD_K_ITERATE, (j + 3.0) * P, k_lsa_dots<<<G, kLsaBD, 0, c->st>>>(b));
+        monitor(xout);
+        read_scalars(c);
+        const double rr = c->hres[0];
+        res.iterations = j + 1;
+        res.residuals.push_back(rr);
+        res.converged = rr <= opt.tolerance;
+        stop = true;
+      }
+      CK(cudaStreamSynchronize(c->st));
+      hnew_prev = c->hres[1];
+    }
+    return res;
+  }
+  const bool persistent = c->use_arnoldi && c->arn_mode == 1;
+  if (persistent) CK(cudaMemsetAsync(c->dj, 0, sizeof(int), c->st));
+  for (int j = 0; j < maxit && persistent; ++j) {
+    compose_op(c, c->V + static_cast<size_t>(j) * N, c->w);
+    // w in, V_0..V_j (MGS), V_{j+1} out, x0 + V_0..V_j in + x out (iterate)
+    launch_arnoldi(c, xout, maxit, nullptr, (2.0 * j + 6.0) * P);
+    res.iterations = j + 1;
+    monitor(xout);
+    read_scalars(c);
+    if (c->arn_trace) {
+      const unsigned long long* q = c->arn_trace;
+      c->arn_phase_ns[0] += static_cast<double>(q[1] - q[0]);  // MGS chain
+      c->arn_phase_ns[1] += static_cast<double>(q[2] - q[1]);  // V_{j+1} + Givens
+      c->arn_phase_ns[2] += static_cast<double>(q[3] - q[2]);  // barrier
+      c->arn_phase_ns[3] += static_cast<double>(q[4] - q[3]);  // iterate
+    }
+    const double rr = c->hres[0];
+    const double hnew = c->hres[1];
+    res.residuals.push_back(rr);
+    if (rr <= opt.tolerance) {
+      res.converged = true;
+      break;
+    }
+    if (hnew < 1e-300) break;
+  }
+  for (int j = 0; j < maxit && !persistent; ++j) {
     double2* Vj = c->V + static_cast<size_t>(j) * N;
     compose_op(c, Vj, c->w);
     double2* Hj = c->H + static_cast<size_t>(j) * ldh;
@@ -681,6 +913,12 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
                                                             N));
     }
   }
+  if (c->arn_trace) {
+    std::fprintf(stderr, "[hd trace] arnoldi phases over %d its (ms): mgs %.3f givens %.3f barrier %.3f iterate %.3f\n",
+                 res.iterations, c->arn_phase_ns[0] * 1e-6, c->arn_phase_ns[1] * 1e-6, c->arn_phase_ns[2] * 1e-6,
+                 c->arn_phase_ns[3] * 1e-6);
+    for (double& v : c->arn_phase_ns) v = 0.0;
+  }
   return res;
 }
 
@@ -702,6 +940,10 @@ static void destroy_ctx(hd_ctx* c) {
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->t3); cudaFree(c->V);
   cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
   cudaFree(c->scal); cudaFree(c->dres); cudaFree(c->partials); cudaFree(c->counter);
+  cudaFree(c->dj); cudaFree(c->arn_partials); cudaFree(c->arn_bar);
+  cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
+  cudaFree(c->lsa_counter);
+  if (c->arn_trace) cudaFreeHost(c->arn_trace);
   if (c->hres) cudaFreeHost(c->hres);
   if (c->cb) cublasDestroy(c->cb);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -827,6 +1069,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   CK(cudaMemset(c->counter, 0, 4 * sizeof(unsigned)));
   CK(cudaStreamSynchronize(c->st));
   CK(cudaDeviceSynchronize());
+  if (const char* e = std::getenv("HD_ARNOLDI")) c->arn_mode = std::atoi(e);
   c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = c.release();
 }
