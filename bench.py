@@ -208,7 +208,8 @@ def run_gpu(args):
         r = step()
     torch.cuda.synchronize()
     # --- timed region: K steps, per-step CUDA events, L2 flushed between steps
-    solver.profile(True)
+    #     (graph-resident GMRES loop; the per-kernel roofline comes from one
+    #      extra profiled solve after the timed region)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     iters = 0
     launches = 0
@@ -230,6 +231,11 @@ def run_gpu(args):
         dist.barrier()
     times = [a.elapsed_time(b) for a, b in evs]
     t_ms = float(sum(times))
+    # one profiled solve: every launch bracketed by CUDA events on the library stream
+    solver.profile(True)
+    flush.zero_()
+    step()
+    torch.cuda.synchronize()
     prof = solver.profile_read()
     solver.profile(False)
     if dist:
@@ -310,6 +316,8 @@ def run_gpu(args):
             "time_to_solution_ms": t_max / args.steps, "t_setup_s": r.t_setup,
             "e2e": e2e, "gpu_launches": launches, "library_calls": libcalls,
             "roofline": roof, "kernel_breakdown": breakdown,
+            "roofline_note": "per-kernel CUDA events of one extra profiled solve (host-driven launch loop) "
+                             "after the timed region; achieved = algorithmic bytes / event time",
             "solve_effective_GBps": round(all_b / (tot_prof_ms * 1e-3) / 1e9, 1) if prof else None,
             "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

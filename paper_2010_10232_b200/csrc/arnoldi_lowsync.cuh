@@ -49,6 +49,7 @@ struct LsaArgs {
   double2* partials;  // gridDim.x * (2 kLsaMaxJ + 2)
   unsigned* counter;  // last-block ticket, zero between launches
   const int* done;    // early exit (speculative graph iterations); may be null
+  const int* dj;      // device-side iteration index (graph mode); overrides j when set
 };
 
 __device__ __forceinline__ double2 lsa_warp_sum(double2 v) {
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   __shared__ double2 sh_s[kLsaMaxJ + 1];
   __shared__ double2 sh_lj[kLsaMaxJ];
   if (a.done && *((volatile const int*)a.done)) return;
-  const int j = a.j;
+  const int j = a.dj ? *a.dj : a.j;
   const bool dots = a.mode == 0;
   const bool iter = j >= 1 || a.mode == 1;     // x_{j-1} (mode 1: x_j, iterate-only)
   const int mi = a.mode == 1 ? j + 1 : j;      // iterate terms
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
   __shared__ double2 sh_c[kLsaMaxJ + 1];
   __shared__ double red[NW];
   if (a.done && *((volatile const int*)a.done)) return;
-  const int j = a.j;
+  const int j = a.dj ? *a.dj : a.j;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int q = threadIdx.x; q <= j; q += kLsaBD) sh_c[q] = __ldcg(&a.ch[q]);
   __syncthreads();
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_givens(LsaArgs a, int nparts) {
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double s_hnew;
   if (a.done && *((volatile const int*)a.done)) return;
-  const int j = a.j;
+  const int j = a.dj ? *a.dj : a.j;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp == 0) {
     double s = 0.0;
@@ -364,6 +365,52 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_givens(LsaArgs a, int nparts) {
       __syncwarp();
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Device-side loop control for the graph-resident GMRES loop (WHILE node).
+// ---------------------------------------------------------------------------
+struct LoopState {
+  int j;          // current iteration
+  int done;       // loop finished (all remaining body kernels exit early)
+  int iters;      // GmresResult::iterations when done
+  int conv;       // converged flag
+  int need_tail;  // budget exhausted: the host forms x_{maxit-1} and its monitor
+};
+
+// After the monitor of x_{j-1} (src/linalg.cpp:82-88): record the residual,
+// stop on tolerance or Krylov breakdown of the previous step.
+__global__ void k_loop_check(LoopState* s, const double* dres, double* res_hist, double tol,
+                             cudaGraphConditionalHandle h) {
+  if (s->done) return;
+  const int j = s->j;
+  if (j < 1) return;
+  const double rr = dres[0];
+  res_hist[j - 1] = rr;
+  if (rr <= tol) {
+    s->conv = 1;
+    s->done = 1;
+    s->iters = j;
+    cudaGraphSetConditional(h, 0);
+    return;
+  }
+  if (dres[1] < 1e-300) {  // hnew of iteration j-1
+    s->done = 1;
+    s->iters = j;
+    cudaGraphSetConditional(h, 0);
+  }
+}
+
+__global__ void k_loop_next(LoopState* s, int maxit, cudaGraphConditionalHandle h) {
+  if (s->done) return;
+  if (s->j + 1 >= maxit) {
+    s->done = 1;
+    s->need_tail = 1;
+    s->iters = maxit;
+    cudaGraphSetConditional(h, 0);
+    return;
+  }
+  s->j += 1;
 }
 
 }  // namespace hd

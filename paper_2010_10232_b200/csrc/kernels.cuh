@@ -35,7 +35,7 @@ struct RedOut {
   double2* partials;
   unsigned* counter;
   double* dst;       // final scalar written by the last block
-  double scale;      // dst = sqrt(sum |.|^2) * scale
+  double scale;      // dst = sqrt(sum |.|^2) / scale   (monitor: ||f|| or 1, src/precond.cpp:261-262)
 };
 
 enum OpMode { OP_APPLY = 0, OP_RESID = 1, OP_JACOBI = 2, OP_RESNORM = 3 };
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kTX) k_op2d(LevelDev L, const double2* __restr
   cp_async_wait<0>();
   if (MODE == OP_RESNORM) {
     double2 total;
-    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) * red.scale;
+    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) / red.scale;
   }
 }
 
@@ -195,8 +195,9 @@ __global__ void k_jacobi0_2d(LevelDev L, const double2* __restrict__ b, double2*
 // ---------------------------------------------------------------------------
 template <int MODE>
 __global__ void k_op1d(LevelDev L, const double2* __restrict__ x, const double2* __restrict__ bv,
-                       double2* __restrict__ out, double omega, RedOut red) {
+                       double2* __restrict__ out, double omega, RedOut red, const int* xidx, size_t xstride) {
   __shared__ double2 scratch[32];
+  if (xidx) x += (size_t)(*xidx) * xstride;
   const int n = L.n, b = L.b, NB = 2 * b + 1;
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -224,7 +225,7 @@ __global__ void k_op1d(LevelDev L, const double2* __restrict__ x, const double2*
   }
   if (MODE == OP_RESNORM) {
     double2 total;
-    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) * red.scale;
+    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) / red.scale;
   }
 }
 

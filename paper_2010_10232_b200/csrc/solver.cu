@@ -28,6 +28,8 @@
 #include "host/assembly.hpp"
 #include "host/banded.hpp"
 #include "kernels.cuh"
+#include "stencil.cuh"
+#include "transfer.cuh"
 #include "arnoldi.cuh"
 #include "arnoldi_lowsync.cuh"
 
@@ -146,6 +148,18 @@ struct hd_ctx {
   unsigned* lsa_counter = nullptr;
   int lsa_G = 0, lsa_maxit = -1;
   size_t lsa_givens_smem = 0;
+  // graph-resident GMRES loop (WHILE conditional node), rebuilt when (maxit, tol) change
+  cudaGraph_t loop_graph = nullptr;
+  cudaGraphExec_t loop_exec = nullptr;
+  int loop_maxit = -1;
+  double loop_tol = -1.0;
+  LoopState* loop_state = nullptr;
+  LoopState* loop_host = nullptr;   // pinned
+  double* res_hist = nullptr;       // device, maxit
+  double* res_host = nullptr;       // pinned
+  void* cublas_ws = nullptr;
+  bool graph_enabled = true;        // HD_GRAPH=0: host-driven loop
+  int graph_body_kernels = 0;       // own kernels per body execution
   // counters
   long matvecs = 0, coarse_solves = 0, shift_solves = 0, vcycles = 0;
   int launches = 0;             // own kernels launched in the last solve
@@ -343,15 +357,24 @@ static double op_bytes(int mode, size_t NL) {
   }
 }
 
+static int stencil_rows(int n) {
+  // rows per strip: keep >= ~6 warps per SM on the big levels
+  const int wcols = (n + kSW * kSWarps - 1) / (kSW * kSWarps);
+  int ry = kSRows;
+  while (ry > 8 && static_cast<long>(wcols) * ((n + ry - 1) / ry) * kSWarps < 148L * 12) ry /= 2;
+  return ry;
+}
+
 template <int MODE>
 static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
-                             double omega, RedOut red, int kind) {
-  const int ry = strip_rows(L.n);
-  dim3 grid((L.n + kTX - 1) / kTX, (L.n + ry - 1) / ry);
+                             double omega, RedOut red, int kind, const int* xidx, size_t xstride) {
+  const int ry = stencil_rows(L.n);
+  dim3 grid((L.n + kSW * kSWarps - 1) / (kSW * kSWarps), (L.n + ry - 1) / ry);
   const size_t mk = prof_mark(c);
   switch (L.b) {
 #define HD_CASE(BB) \
-  case BB: k_op2d<BB, MODE><<<grid, kTX, 0, c->st>>>(L, x, b, out, omega, ry, red); break;
+  case BB: k_stencil2d<BB, MODE><<<grid, kSW * kSWarps, 0, c->st>>>(L, x, b, out, omega, ry, red, xidx, xstride); \
+    break;
     HD_CASE(1) HD_CASE(2) HD_CASE(3) HD_CASE(4) HD_CASE(5) HD_CASE(6)
 #undef HD_CASE
     default: throw Error(HD_ERR_INVALID, "band half-width " + std::to_string(L.b) + " unsupported");
@@ -370,24 +393,25 @@ static RedOut red_of(hd_ctx* c, double* dst = nullptr, double scale = 1.0) {
 
 // out = L x | b - L x | x + w D^-1 (b - L x) | ||b - L x|| * scale -> dst
 static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, const double2* b, double2* out,
-                     double omega = 0.0, double* dst = nullptr, double scale = 1.0) {
+                     double omega = 0.0, double* dst = nullptr, double scale = 1.0, const int* xidx = nullptr,
+                     size_t xstride = 0) {
   RedOut red = red_of(c, dst, scale);
   const int kind = L.n == c->n ? HD_K_OP_FINE : HD_K_OP_COARSE;
   if (c->dim == 2) {
     switch (mode) {
-      case OP_APPLY: launch_op2d_mode<OP_APPLY>(c, L, x, b, out, omega, red, kind); break;
-      case OP_RESID: launch_op2d_mode<OP_RESID>(c, L, x, b, out, omega, red, kind); break;
-      case OP_JACOBI: launch_op2d_mode<OP_JACOBI>(c, L, x, b, out, omega, red, kind); break;
-      default: launch_op2d_mode<OP_RESNORM>(c, L, x, b, out, omega, red, kind); break;
+      case OP_APPLY: launch_op2d_mode<OP_APPLY>(c, L, x, b, out, omega, red, kind, xidx, xstride); break;
+      case OP_RESID: launch_op2d_mode<OP_RESID>(c, L, x, b, out, omega, red, kind, xidx, xstride); break;
+      case OP_JACOBI: launch_op2d_mode<OP_JACOBI>(c, L, x, b, out, omega, red, kind, xidx, xstride); break;
+      default: launch_op2d_mode<OP_RESNORM>(c, L, x, b, out, omega, red, kind, xidx, xstride); break;
     }
   } else {
     const int grid = mode == OP_RESNORM ? std::min(grid_for(L.n), c->red_blocks) : grid_for(L.n);
     const size_t mk = prof_mark(c);
     switch (mode) {
-      case OP_APPLY: k_op1d<OP_APPLY><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
-      case OP_RESID: k_op1d<OP_RESID><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
-      case OP_JACOBI: k_op1d<OP_JACOBI><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
-      default: k_op1d<OP_RESNORM><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red); break;
+      case OP_APPLY: k_op1d<OP_APPLY><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red, xidx, xstride); break;
+      case OP_RESID: k_op1d<OP_RESID><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red, xidx, xstride); break;
+      case OP_JACOBI: k_op1d<OP_JACOBI><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red, xidx, xstride); break;
+      default: k_op1d<OP_RESNORM><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red, xidx, xstride); break;
     }
     launched(c, kind, mk, op_bytes(mode, L.n));
   }
@@ -396,16 +420,25 @@ static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, c
 static void jacobi0(hd_ctx* c, const LevelDev& L, const double2* b, double2* out, double omega) {
   const size_t NN = c->dim == 2 ? static_cast<size_t>(L.n) * L.n : L.n;
   HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,
-            if (c->dim == 2) k_jacobi0_2d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega);
+            if (c->dim == 2) k_jacobi0_2d_t<<<dim3((L.n + 63) / 64, (L.n + 15) / 16), 256, 0, c->st>>>(L, b, out,
+                                                                                                        omega);
             else k_jacobi0_1d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega));
 }
 
 static void restrict_(hd_ctx* c, Stencil z, const double2* r, int nf, int nc, double2* outc, double* outp) {
   const size_t NC = c->dim == 2 ? static_cast<size_t>(nc) * nc : nc;
   const double NF = c->dim == 2 ? static_cast<double>(nf) * nf : nf;
+  if (c->dim == 2) {
+    dim3 grid((nc + kRQX - 1) / kRQX, (nc + kRQY - 1) / kRQY);
+    HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NF + NC),
+              if (z.kind == 0 && !outp) k_restrict2d<0, 0><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp);
+              else if (z.kind == 0) k_restrict2d<0, 1><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp);
+              else if (!outp) k_restrict2d<1, 0><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp);
+              else k_restrict2d<1, 1><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp));
+    return;
+  }
   HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NF + NC),
-            if (c->dim == 2) k_restrict<2><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp);
-            else k_restrict<1><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp));
+            k_restrict<1><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp));
 }
 
 template <int PMODE>
@@ -413,9 +446,15 @@ static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, 
                      double2* out) {
   const size_t NF = c->dim == 2 ? static_cast<size_t>(nf) * nf : nf;
   const double NC = c->dim == 2 ? static_cast<double>(nc) * nc : nc;
+  if (c->dim == 2) {
+    dim3 grid((nf + kPFX - 1) / kPFX, (nf + kPFY - 1) / kPFY);
+    HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NC + (PMODE == 2 ? 1.0 : 2.0) * NF),
+              if (z.kind == 0) k_prolong2d<0, PMODE><<<grid, 256, 0, c->st>>>(z.drop, ec, ep, nf, nc, s, out);
+              else k_prolong2d<1, PMODE><<<grid, 256, 0, c->st>>>(z.drop, ec, ep, nf, nc, s, out));
+    return;
+  }
   HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NC + (PMODE == 2 ? 1.0 : 2.0) * NF),
-            if (c->dim == 2) k_prolong<2, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out);
-            else k_prolong<1, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out));
+            k_prolong<1, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out));
 }
 
 // Exact solve: in/out planar (2D FD) or via the banded LU (1D).
@@ -558,9 +597,9 @@ static void project(hd_ctx* c, const double2* w, double2* out) {
 }
 
 // out = op(v) = P MG^-1 A v  (src/precond.cpp:236-245); v, out distinct from t1, t2, t3
-static void compose_op(hd_ctx* c, const double2* v, double2* out) {
+static void compose_op(hd_ctx* c, const double2* v, double2* out, const int* vidx = nullptr) {
   ++c->matvecs;
-  op_apply(c, OP_APPLY, opA(c), v, nullptr, c->t1);
+  op_apply(c, OP_APPLY, opA(c), v, nullptr, c->t1, 0.0, nullptr, 1.0, vidx, c->N);
   const double2* cur = c->t1;
   if (c->spec.shift) {
     ++c->shift_solves;
@@ -714,6 +753,7 @@ static LsaArgs lsa_args(hd_ctx* c, double2* xout, int j, int mode, int maxit) {
   a.partials = c->lsa_partials;
   a.counter = c->lsa_counter;
   a.done = nullptr;
+  a.dj = nullptr;
   return a;
 }
 
@@ -722,6 +762,87 @@ __global__ void k_inv_scalar(double* dst, const double* src) { *dst = *src > 0.0
 static void read_scalars(hd_ctx* c) {
   CK(cudaMemcpyAsync(c->hres, c->dres, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+}
+
+__global__ void k_loop_init(LoopState* s) {
+  s->j = 0;
+  s->done = 0;
+  s->iters = 0;
+  s->conv = 0;
+  s->need_tail = 0;
+}
+
+__global__ void k_scale_monitor(double* dres) {  // graph monitor: raw norm / (||f|| or 1)
+  const double f = dres[3];
+  dres[0] = dres[0] / (f > 0.0 ? f : 1.0);
+}
+
+static void monitor_raw(hd_ctx* c, const double2* x) {
+  op_apply(c, OP_RESNORM, level_dev(c->fine, c->cA, c->corner), x, c->f, nullptr, 0.0, c->dres + 0, 1.0);
+}
+
+// Captures the GMRES iteration body (device-side j) into the body of a WHILE
+// conditional node: op(u_j) -> pass 1 (dots, x_{j-1}) -> monitor x_{j-1} ->
+// convergence check -> pass 2 (u_{j+1}) -> Givens -> j++.
+static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
+  if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
+  if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
+  c->loop_exec = nullptr;
+  c->loop_graph = nullptr;
+  if (!c->loop_state) {
+    c->loop_state = dalloc<LoopState>(1);
+    CK(cudaMallocHost(&c->loop_host, sizeof(LoopState)));
+  }
+  cudaFree(c->res_hist);
+  if (c->res_host) cudaFreeHost(c->res_host);
+  c->res_hist = dalloc<double>(maxit + 1);
+  CK(cudaMallocHost(&c->res_host, (maxit + 1) * sizeof(double)));
+  const long saved[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
+  const int saved_l = c->launches, saved_b = c->lib_calls;
+  const bool prof = c->prof_on;
+  c->prof_on = false;
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  const int G = c->lsa_G;
+  int* dj = &c->loop_state->j;
+  compose_op(c, c->V, c->w, dj);
+  LsaArgs a = lsa_args(c, c->x, 0, 0, maxit);
+  a.dj = dj;
+  a.done = &c->loop_state->done;
+  k_lsa_dots<<<G, kLsaBD, 0, c->st>>>(a);
+  monitor_raw(c, c->x);
+  k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres);
+  k_loop_check<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, c->res_hist, tol, h);
+  k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a);
+  k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a, G);
+  k_loop_next<<<1, 1, 0, c->st>>>(c->loop_state, maxit, h);
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(c->st, &captured);
+  c->prof_on = prof;
+  c->graph_body_kernels = c->launches - saved_l + 6;  // op + monitor kernels + dots/scale/check/update/givens/next
+  c->matvecs = saved[0];
+  c->coarse_solves = saved[1];
+  c->shift_solves = saved[2];
+  c->vcycles = saved[3];
+  c->launches = saved_l;
+  c->lib_calls = saved_b;
+  CK(ec);
+  CK(cudaGetLastError());
+  CK(cudaGraphInstantiate(&c->loop_exec, g, 0));
+  c->loop_graph = g;
+  c->loop_maxit = maxit;
+  c->loop_tol = tol;
 }
 
 struct SolveOut {
@@ -765,7 +886,7 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   }
   read_scalars(c);
   const double fnorm = c->hres[3];
-  const double scale = fnorm > 0.0 ? 1.0 / fnorm : 1.0;
+  const double scale = fnorm > 0.0 ? fnorm : 1.0;
 
   SolveOut res;
   auto monitor = [&](const double2* xv) {
@@ -802,6 +923,37 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
     CK(cudaMemcpyAsync(c->V, c->w, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
     HD_LAUNCH(HD_K_VEC, 0.0, k_inv_scalar<<<1, 1, 0, c->st>>>(c->lsa_sig, c->dres + 2));
     const int G = c->lsa_G;
+    if (c->graph_enabled && !c->prof_on) {
+      if (c->loop_maxit != maxit || c->loop_tol != opt.tolerance) build_loop_graph(c, maxit, opt.tolerance);
+      k_loop_init<<<1, 1, 0, c->st>>>(c->loop_state);
+      CK(cudaGraphLaunch(c->loop_exec, c->st));
+      CK(cudaMemcpyAsync(c->loop_host, c->loop_state, sizeof(LoopState), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(c->res_host, c->res_hist, maxit * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      const LoopState ls = *c->loop_host;
+      // per-iteration launches of the body (op + 7) for the report
+      int it = ls.iters;
+      res.iterations = it;
+      res.converged = ls.conv != 0;
+      for (int q = 0; q < (ls.need_tail ? maxit - 1 : it); ++q) res.residuals.push_back(c->res_host[q]);
+      if (ls.need_tail) {  // x_{maxit-1}: iterate-only pass + monitor
+        LsaArgs b = lsa_args(c, c->x, maxit - 1, 1, maxit);
+        HD_LAUNCH(HD_K_ITERATE, (maxit + 2.0) * P, k_lsa_dots<<<G, kLsaBD, 0, c->st>>>(b));
+        monitor(c->x);
+        read_scalars(c);
+        res.residuals.push_back(c->hres[0]);
+        res.converged = c->hres[0] <= opt.tolerance;
+      }
+      c->matvecs += it;
+      if (c->spec.shift) {
+        c->shift_solves += it;
+        c->vcycles += static_cast<long>(it) * c->spec.cycles;
+      }
+      if (c->spec.deflate) c->coarse_solves += it;
+      c->launches += (it + 1) * (c->graph_body_kernels);
+      if (xout != c->x) CK(cudaMemcpyAsync(xout, c->x, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+      return res;
+    }
     bool stop = false;
     double hnew_prev = 1.0;
     for (int j = 0; j < maxit && !stop; ++j) {
@@ -943,6 +1095,11 @@ static void destroy_ctx(hd_ctx* c) {
   cudaFree(c->dj); cudaFree(c->arn_partials); cudaFree(c->arn_bar);
   cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
   cudaFree(c->lsa_counter);
+  if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
+  if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
+  cudaFree(c->loop_state); cudaFree(c->res_hist); cudaFree(c->cublas_ws);
+  if (c->loop_host) cudaFreeHost(c->loop_host);
+  if (c->res_host) cudaFreeHost(c->res_host);
   if (c->arn_trace) cudaFreeHost(c->arn_trace);
   if (c->hres) cudaFreeHost(c->hres);
   if (c->cb) cublasDestroy(c->cb);
@@ -1070,6 +1227,9 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   CK(cudaStreamSynchronize(c->st));
   CK(cudaDeviceSynchronize());
   if (const char* e = std::getenv("HD_ARNOLDI")) c->arn_mode = std::atoi(e);
+  if (const char* e = std::getenv("HD_GRAPH")) c->graph_enabled = std::atoi(e) != 0;
+  c->cublas_ws = dalloc<char>(32u << 20);
+  CKB(cublasSetWorkspace(c->cb, c->cublas_ws, 32u << 20));
   c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = c.release();
 }

@@ -1,0 +1,162 @@
+// Shared-memory tiled 2D transfers (separable Kronecker-square stencils).
+//
+// Restriction rc = (z (x) z)^T r: a CTA stages the fine region that feeds an
+// 8 x 32 tile of coarse points (coalesced, zero-filled outside), contracts x
+// then y in shared memory, and writes the tile (interleaved or planar).
+// Prolongation out = base +- (z (x) z) e: a CTA stages the coarse region of a
+// 16 x 64 fine tile and produces 4 fine points per thread.
+// linear z  (src/precond.cpp:57-76):  even j inject, odd j average;
+// Bezier z  (src/precond.cpp:34-55):  even j 1/8 (1, 6-drop, 1), odd j 1/2 (1, 1).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace hd {
+
+constexpr int kRQY = 8, kRQX = 32;   // coarse tile of the restriction
+constexpr int kPFY = 16, kPFX = 64;  // fine tile of the prolongation
+
+template <int KIND>
+struct ZW {
+  static constexpr int lo = KIND == 0 ? 0 : -1;
+  static constexpr int nw = KIND == 0 ? 3 : 5;
+  __device__ static double w(int o, double drop) {  // restriction weight at offset lo + o
+    if (KIND == 0) return o == 1 ? 1.0 : 0.5;
+    return o == 0 || o == 4 ? 0.125 : (o == 2 ? (6.0 - drop) / 8.0 : 0.5);
+  }
+};
+
+// PLANAR: 0 interleaved output (outc), 1 planar (outp: re plane then im plane)
+template <int KIND, int PLANAR>
+__global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* __restrict__ r, int nf, int nc,
+                                                    double2* __restrict__ outc, double* __restrict__ outp) {
+  constexpr int lo = ZW<KIND>::lo, nw = ZW<KIND>::nw;
+  constexpr int RR = 2 * kRQY + nw - 1;  // fine rows of the region
+  constexpr int RC = 2 * kRQX + nw - 1;  // fine cols
+  __shared__ double2 f[RR][RC + 1];
+  __shared__ double2 tx[RR][kRQX];
+  const int qx0 = blockIdx.x * kRQX, qy0 = blockIdx.y * kRQY;
+  const int fx0 = 2 * qx0 + lo, fy0 = 2 * qy0 + lo;
+  for (int e = threadIdx.x; e < RR * RC; e += blockDim.x) {
+    const int rr = e / RC, cc = e % RC;
+    const int fy = fy0 + rr, fx = fx0 + cc;
+    f[rr][cc] = (fy >= 0 && fy < nf && fx >= 0 && fx < nf) ? r[(size_t)fy * nf + fx] : cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  double w[nw];
+#pragma unroll
+  for (int o = 0; o < nw; ++o) w[o] = ZW<KIND>::w(o, drop);
+  for (int e = threadIdx.x; e < RR * kRQX; e += blockDim.x) {
+    const int rr = e / kRQX, qx = e % kRQX;
+    double2 s = cmk(0.0, 0.0);
+#pragma unroll
+    for (int o = 0; o < nw; ++o) s = cfma_r(w[o], f[rr][2 * qx + o], s);
+    tx[rr][qx] = s;
+  }
+  __syncthreads();
+  const size_t NC = (size_t)nc * nc;
+  for (int e = threadIdx.x; e < kRQY * kRQX; e += blockDim.x) {
+    const int qy = e / kRQX, qx = e % kRQX;
+    const int gy = qy0 + qy, gx = qx0 + qx;
+    if (gy >= nc || gx >= nc) continue;
+    double2 s = cmk(0.0, 0.0);
+#pragma unroll
+    for (int o = 0; o < nw; ++o) s = cfma_r(w[o], tx[2 * qy + o][qx], s);
+    const size_t gi = (size_t)gy * nc + gx;
+    if (PLANAR) {
+      outp[gi] = s.x;
+      outp[gi + NC] = s.y;
+    } else {
+      outc[gi] = s;
+    }
+  }
+}
+
+// fine index i -> coarse neighbours as offsets into a staged region starting at
+// coarse index qbase; returns count.  Same stencil as pweights() in kernels.cuh.
+template <int KIND>
+__device__ __forceinline__ int pw2(int i, int nc, double drop, int* q, double* w) {
+  int m = 0;
+  auto push = [&](int qq, double ww) {
+    if (qq >= 0 && qq < nc) {
+      q[m] = qq;
+      w[m] = ww;
+      ++m;
+    }
+  };
+  if (i & 1) {
+    if (KIND == 0) {
+      push((i - 1) / 2, 1.0);
+    } else {
+      push((i - 3) / 2, 0.125);
+      push((i - 1) / 2, (6.0 - drop) / 8.0);
+      push((i + 1) / 2, 0.125);
+    }
+  } else {
+    push(i / 2 - 1, 0.5);
+    push(i / 2, 0.5);
+  }
+  return m;
+}
+
+// PMODE 0: out += Z e (interleaved e);  1: out = s - Z e (planar e);  2: out = Z e (planar e)
+template <int KIND, int PMODE>
+__global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* __restrict__ ec,
+                                                   const double* __restrict__ ep, int nf, int nc,
+                                                   const double2* __restrict__ s, double2* __restrict__ out) {
+  constexpr int CR = kPFY / 2 + 3, CC = kPFX / 2 + 3;
+  __shared__ double2 cs[CR][CC];
+  const int fx0 = blockIdx.x * kPFX, fy0 = blockIdx.y * kPFY;
+  const int qx0 = fx0 / 2 - 1, qy0 = fy0 / 2 - 1;  // region origin (may be -1)
+  const size_t NC = (size_t)nc * nc;
+  for (int e = threadIdx.x; e < CR * CC; e += blockDim.x) {
+    const int rr = e / CC, cc = e % CC;
+    const int qy = qy0 + rr, qx = qx0 + cc;
+    double2 v = cmk(0.0, 0.0);
+    if (qy >= 0 && qy < nc && qx >= 0 && qx < nc) {
+      const size_t qi = (size_t)qy * nc + qx;
+      v = PMODE == 0 ? ec[qi] : cmk(ep[qi], ep[qi + NC]);
+    }
+    cs[rr][cc] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kPFY * kPFX; e += blockDim.x) {
+    const int fy = fy0 + e / kPFX, fx = fx0 + e % kPFX;
+    if (fy >= nf || fx >= nf) continue;
+    int qy[3], qx[3];
+    double wy[3], wx[3];
+    const int my = pw2<KIND>(fy, nc, drop, qy, wy);
+    const int mx = pw2<KIND>(fx, nc, drop, qx, wx);
+    double2 acc = cmk(0.0, 0.0);
+    for (int a = 0; a < my; ++a) {
+      double2 t = cmk(0.0, 0.0);
+      for (int b = 0; b < mx; ++b) t = cfma_r(wx[b], cs[qy[a] - qy0][qx[b] - qx0], t);
+      acc = cfma_r(wy[a], t, acc);
+    }
+    const size_t gi = (size_t)fy * nf + fx;
+    if (PMODE == 0) out[gi] = cadd(out[gi], acc);
+    else if (PMODE == 1) out[gi] = csub(s[gi], acc);
+    else out[gi] = acc;
+  }
+}
+
+// x = omega D^-1 b on a 2D level, 2D grid (no 64-bit div/mod per element)
+__global__ void __launch_bounds__(256) k_jacobi0_2d_t(LevelDev L, const double2* __restrict__ b,
+                                                      double2* __restrict__ out, double omega) {
+  const int n = L.n, NB = 2 * L.b + 1;
+  const int ix = blockIdx.x * 64 + (threadIdx.x & 63);
+  const int iy0 = blockIdx.y * 16 + (threadIdx.x >> 6) * 4;
+  if (ix >= n) return;
+  const double mxx = L.M[(size_t)ix * NB + L.b], sxx = L.S[(size_t)ix * NB + L.b];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int iy = iy0 + r;
+    if (iy >= n) break;
+    const double my = L.M[(size_t)iy * NB + L.b], sy = L.S[(size_t)iy * NB + L.b];
+    const double2 D = csub(cmk(my * sxx + sy * mxx, 0.0), cscale(my * mxx, L.c));
+    const size_t g = (size_t)iy * n + ix;
+    out[g] = cscale(omega, cmul(cinv(D), ld_stream(b + g)));
+  }
+}
+
+}  // namespace hd
