@@ -160,6 +160,7 @@ struct hd_ctx {
   void* cublas_ws = nullptr;
   bool graph_enabled = true;        // HD_GRAPH=0: host-driven loop
   int graph_body_kernels = 0;       // own kernels per body execution
+  int n_sms = 148;
   // counters
   long matvecs = 0, coarse_solves = 0, shift_solves = 0, vcycles = 0;
   int launches = 0;             // own kernels launched in the last solve
@@ -339,14 +340,6 @@ static int grid_for(size_t N, int threads = 256, int cap = 148 * 8) {
   return static_cast<int>(std::max<size_t>(1, std::min<size_t>(g, cap)));
 }
 
-static int strip_rows(int n) {
-  // rows per CTA: keep >= ~4 CTAs per SM in flight on the big levels
-  const int cols = (n + kTX - 1) / kTX;
-  int ry = 32;
-  while (ry > 8 && static_cast<long>(cols) * ((n + ry - 1) / ry) < 148 * 4) ry /= 2;
-  return ry;
-}
-
 // algorithmic bytes of one operator launch: x read + output (+ b read)
 static double op_bytes(int mode, size_t NL) {
   const double P = 16.0 * static_cast<double>(NL);
@@ -357,24 +350,58 @@ static double op_bytes(int mode, size_t NL) {
   }
 }
 
-static int stencil_rows(int n) {
-  // rows per strip: keep >= ~6 warps per SM on the big levels
-  const int wcols = (n + kSW * kSWarps - 1) / (kSW * kSWarps);
-  int ry = kSRows;
-  while (ry > 8 && static_cast<long>(wcols) * ((n + ry - 1) / ry) * kSWarps < 148L * 12) ry /= 2;
-  return ry;
+// Per instantiation: opt in to the dynamic shared memory of the tallest strip
+// and query how many CTAs are resident per SM.
+template <int B, int MODE>
+static int stencil_occupancy() {
+  static int per = 0;
+  if (!per) {
+    constexpr size_t sm = stencil_smem<B, MODE>(kSRowsMax);
+    CK(cudaFuncSetAttribute(k_stencil2d<B, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stencil2d<B, MODE>, kSW * kSWarps, sm));
+    per = std::max(per, 1);
+  }
+  return per;
+}
+
+// Strip height: fill whole waves of resident CTAs, discounted by the 2B halo
+// rows each strip re-reads.
+static int pick_rows(int n, int slots, int B) {
+  const int colblocks = (n + kSW * kSWarps - 1) / (kSW * kSWarps);
+  static const int cand[] = {8, 12, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 112, 128};
+  int best = 32;
+  double best_score = -1.0;
+  for (int ry : cand) {
+    if (ry > kSRowsMax) break;
+    const long tiles = static_cast<long>(colblocks) * ((n + ry - 1) / ry);
+    const long waves = (tiles + slots - 1) / slots;
+    const double util = static_cast<double>(tiles) / (static_cast<double>(waves) * slots);
+    const double score = util * ry / (ry + 2.0 * B);
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = ry;
+    }
+  }
+  return best;
+}
+
+template <int B, int MODE>
+static void launch_stencil(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
+                           double omega, RedOut red, const int* xidx, size_t xstride) {
+  const int per = stencil_occupancy<B, MODE>();
+  const int ry = pick_rows(L.n, per * c->n_sms, B);
+  dim3 grid((L.n + kSW * kSWarps - 1) / (kSW * kSWarps), (L.n + ry - 1) / ry);
+  k_stencil2d<B, MODE><<<grid, kSW * kSWarps, stencil_smem<B, MODE>(ry), c->st>>>(L, x, b, out, omega, ry, red,
+                                                                               xidx, xstride);
 }
 
 template <int MODE>
 static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
                              double omega, RedOut red, int kind, const int* xidx, size_t xstride) {
-  const int ry = stencil_rows(L.n);
-  dim3 grid((L.n + kSW * kSWarps - 1) / (kSW * kSWarps), (L.n + ry - 1) / ry);
   const size_t mk = prof_mark(c);
   switch (L.b) {
 #define HD_CASE(BB) \
-  case BB: k_stencil2d<BB, MODE><<<grid, kSW * kSWarps, 0, c->st>>>(L, x, b, out, omega, ry, red, xidx, xstride); \
-    break;
+  case BB: launch_stencil<BB, MODE>(c, L, x, b, out, omega, red, xidx, xstride); break;
     HD_CASE(1) HD_CASE(2) HD_CASE(3) HD_CASE(4) HD_CASE(5) HD_CASE(6)
 #undef HD_CASE
     default: throw Error(HD_ERR_INVALID, "band half-width " + std::to_string(L.b) + " unsupported");
@@ -1228,6 +1255,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   CK(cudaDeviceSynchronize());
   if (const char* e = std::getenv("HD_ARNOLDI")) c->arn_mode = std::atoi(e);
   if (const char* e = std::getenv("HD_GRAPH")) c->graph_enabled = std::atoi(e) != 0;
+  CK(cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, c->device));
   c->cublas_ws = dalloc<char>(32u << 20);
   CKB(cublasSetWorkspace(c->cb, c->cublas_ws, 32u << 20));
   c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

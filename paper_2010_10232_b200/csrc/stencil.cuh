@@ -9,8 +9,11 @@
 // in the row loop.  The x pass forms P = Sx x - c Mx x and Q = Mx x for the
 // newest row; the y pass reads the last 2B+1 (P, Q) from register queues that
 // are rotated statically (the row loop is unrolled by 2B+1), so no register
-// moves are executed.  x-direction coefficients live in registers, the y
-// coefficients of the strip in shared memory as (My, Sy) pairs.
+// moves are executed.  Every sum is split into two independent FMA chains
+// (even / odd taps) to keep the FP64 pipe fed at low occupancy.
+// x-direction coefficients live in registers, the y coefficients of the strip
+// in shared memory as (My, Sy) pairs.  The strip height RY is chosen by the
+// host so that the tile count fills whole waves of resident CTAs.
 //
 // Modes: APPLY y; RESID b - y; JACOBI x + omega D^-1 (b - y); RESNORM
 // ||b - y||^2 (deterministic grid reduction, no write).
@@ -23,20 +26,27 @@ namespace hd {
 constexpr int kSW = 32;      // columns per warp
 constexpr int kSWarps = 4;   // warps per CTA
 constexpr int kSRing = 8;    // ring depth (rows in flight per warp)
-constexpr int kSRows = 32;   // rows per strip (max)
+constexpr int kSRowsMax = 128;
+
+template <int B, int MODE>
+constexpr size_t stencil_smem(int ry) {
+  return sizeof(double2) * ((size_t)kSWarps * kSRing * ((kSW + 2 * B) + (MODE != OP_APPLY ? kSW : 0)) +
+                            (size_t)(ry + 4 * B + 1) * (2 * B + 1));
+}
 
 template <int B, int MODE>
 __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const double2* __restrict__ x,
                                                             const double2* __restrict__ bv,
                                                             double2* __restrict__ out, double omega, int RY,
                                                             RedOut red, const int* xidx, size_t xstride) {
-  if (xidx) x += (size_t)(*xidx) * xstride;  // graph mode: x = V + j N
   constexpr int NB = 2 * B + 1;
   constexpr int W = kSW + 2 * B;
   constexpr bool NEED_B = MODE != OP_APPLY;
-  __shared__ __align__(16) double2 ring[kSWarps][kSRing][W];
-  __shared__ __align__(16) double2 bring[NEED_B ? kSWarps : 1][NEED_B ? kSRing : 1][kSW];
-  __shared__ __align__(16) double2 cy[kSRows + 1][NB];  // (My, Sy) per strip row
+  if (xidx) x += (size_t)(*xidx) * xstride;  // graph mode: x = V + j N
+  extern __shared__ __align__(16) double2 dsm[];
+  double2(*ring)[kSRing][W] = reinterpret_cast<double2(*)[kSRing][W]>(dsm);
+  double2(*bring)[kSRing][kSW] = reinterpret_cast<double2(*)[kSRing][kSW]>(dsm + kSWarps * kSRing * W);
+  double2* cy = dsm + kSWarps * kSRing * (W + (NEED_B ? kSW : 0));  // (My, Sy) per strip row, NB each
   __shared__ double2 scratch[32];
 
   const int n = L.n;
@@ -49,9 +59,12 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
   const int ix = x0 + lane;
   const bool colv = ix < n;
 
-  for (int e = threadIdx.x; e < nout * NB; e += blockDim.x) {
-    const int r = e / NB, d = e % NB;
-    cy[r][d] = cmk(L.M[(size_t)(y0 + r) * NB + d], L.S[(size_t)(y0 + r) * NB + d]);
+  // (My, Sy) band rows of output rows o = -2B .. nout+2B-1 of the strip,
+  // zero outside [0, nout): accumulation into out-of-strip rows is a no-op
+  for (int e = threadIdx.x; e < (nout + 4 * B) * NB; e += blockDim.x) {
+    const int r = e / NB - 2 * B, d = e % NB;
+    cy[e] = (r >= 0 && r < nout) ? cmk(L.M[(size_t)(y0 + r) * NB + d], L.S[(size_t)(y0 + r) * NB + d])
+                                 : cmk(0.0, 0.0);
   }
   double sx[NB], mx[NB];
 #pragma unroll
@@ -59,42 +72,52 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
     sx[j] = colv ? L.S[(size_t)ix * NB + j] : 0.0;
     mx[j] = colv ? L.M[(size_t)ix * NB + j] : 0.0;
   }
-  __syncthreads();  // cy staged (the only block barrier in the row loop's scope)
+  __syncthreads();  // cy staged (the only block barrier before the final reduction)
   if (x0 >= n && MODE != OP_RESNORM) return;
   double acc = 0.0;
   if (x0 < n) {
     double2(*rg)[W] = ring[warp];
-    // per-lane load descriptors: main column and (lanes < 2B) one halo column
+    // per-lane load descriptors, advanced by one row per step
     const int colA = x0 - B + lane;
     const int colB = x0 - B + kSW + lane;
+    const bool okA = colA >= 0 && colA < n;
     const bool hasB = lane < 2 * B;
-    auto load = [&](int k) {
-      const int r = y0 - B + k;
-      const int s = k % kSRing;
-      const bool rv = (r >= 0) && (r < n);
-      const double2* rowp = x + (size_t)(rv ? r : 0) * n;
-      bool v = rv && colA >= 0 && colA < n;
-      cp_async16(&rg[s][lane], rowp + (v ? colA : 0), v);
-      if (hasB) {
-        v = rv && colB < n;
-        cp_async16(&rg[s][kSW + lane], rowp + (v ? colB : 0), v);
-      }
+    const bool okB = hasB && colB < n;
+    const double2* pA = x + (ptrdiff_t)(y0 - B) * n + (okA ? colA : 0);
+    const double2* pB = x + (ptrdiff_t)(y0 - B) * n + (okB ? colB : 0);
+    const double2* pb = bv + (ptrdiff_t)(y0 - 2 * B) * n + (colv ? ix : 0);
+    int rl = y0 - B;  // global row of the next load
+    int sl = 0;       // its ring slot
+    auto load = [&]() {
+      const bool rv = (rl >= 0) && (rl < n);
+      cp_async16(&rg[sl][lane], rv && okA ? pA : x, rv && okA);
+      if (hasB) cp_async16(&rg[sl][kSW + lane], rv && okB ? pB : x, rv && okB);
       if (NEED_B) {
-        const int rb = r - B;
-        v = (rb >= y0) && (rb < yend) && colv;
-        cp_async16(&bring[warp][s][lane], bv + (v ? (size_t)rb * n + ix : 0), v);
+        const int rb = rl - B;
+        const bool v = (rb >= y0) && (rb < yend) && colv;
+        cp_async16(&bring[warp][sl][lane], v ? pb : bv, v);
+        pb += n;
       }
+      pA += n;
+      pB += n;
+      ++rl;
+      sl = (sl + 1) & (kSRing - 1);
     };
 #pragma unroll
     for (int k = 0; k < kSRing - 1; ++k) {
-      if (k < nin) load(k);
+      if (k < nin) load();
       cp_async_commit();
     }
-    double2 P[NB], Q[NB], XC[NB];
+    // scatter form: row k contributes to the 2B+1 pending output rows
+    // o = k-2B .. k; output o lives in accumulator slot o % NB == (t+1+d) % NB
+    // for d = o - (k-2B), and is complete (stored) after row k = o + 2B.
+    double2 Y[NB], XC[NB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) P[j] = Q[j] = XC[j] = cmk(0.0, 0.0);
+    for (int j = 0; j < NB; ++j) Y[j] = XC[j] = cmk(0.0, 0.0);
     const double2 c = L.c;
-    // rows k = kb + t, t = 0..NB-1; slot of row k in the queues is k % NB == t
+    double2* outp = out + (size_t)y0 * n + ix;
+    const double2* cyk = cy;  // band row of output o = k - 2B (padded index o + 2B == k)
+    int s = 0;                // ring slot of row k
     for (int kb = 0; kb < nin; kb += NB) {
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
@@ -102,45 +125,51 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
         if (k < nin) {
           cp_async_wait<kSRing - 2>();
           __syncwarp();
-          if (k + kSRing - 1 < nin) load(k + kSRing - 1);
+          if (k + kSRing - 1 < nin) load();
           cp_async_commit();
-          const int s = k % kSRing;
-          double2 u = cmk(0.0, 0.0), v = cmk(0.0, 0.0);
+          double2 u0 = cmk(0.0, 0.0), u1 = cmk(0.0, 0.0), v0 = cmk(0.0, 0.0), v1 = cmk(0.0, 0.0);
 #pragma unroll
           for (int j = 0; j < NB; ++j) {
             const double2 xv = rg[s][lane + j];
-            u = cfma_r(sx[j], xv, u);
-            v = cfma_r(mx[j], xv, v);
-          }
-          P[t] = csub(u, cmul(c, v));
-          Q[t] = v;
-          if (MODE == OP_JACOBI) XC[t] = rg[s][lane + B];
-          if (k >= 2 * B) {
-            const int ro = k - 2 * B;  // output row offset; row iy+d sits in slot (t + 1 + d) % NB
-            double2 y = cmk(0.0, 0.0);
-#pragma unroll
-            for (int d = 0; d < NB; ++d) {
-              const int q = (t + 1 + d) % NB;
-              const double2 cyd = cy[ro][d];
-              y = cfma_r(cyd.x, P[q], y);
-              y = cfma_r(cyd.y, Q[q], y);
+            if (j & 1) {
+              u1 = cfma_r(sx[j], xv, u1);
+              v1 = cfma_r(mx[j], xv, v1);
+            } else {
+              u0 = cfma_r(sx[j], xv, u0);
+              v0 = cfma_r(mx[j], xv, v0);
             }
+          }
+          const double2 v = cadd(v0, v1);
+          const double2 Pk = csub(cadd(u0, u1), cmul(c, v));
+          if (MODE == OP_JACOBI) XC[(t + 1 + B) % NB] = rg[s][lane + B];  // centre of output k - B
+#pragma unroll
+          for (int d = 0; d < NB; ++d) {
+            // output o = k - 2B + d takes row k with its band offset 2B - d
+            const double2 cyd = cyk[d * NB + (2 * B - d)];
+            double2& yo = Y[(t + 1 + d) % NB];
+            yo = cfma_r(cyd.x, Pk, cfma_r(cyd.y, v, yo));
+          }
+          if (k >= 2 * B) {  // output o = k - 2B is complete
+            double2& yo = Y[(t + 1) % NB];
             if (colv) {
-              const size_t gi = (size_t)(y0 + ro) * n + ix;
               if (MODE == OP_APPLY) {
-                out[gi] = y;
+                *outp = yo;
               } else if (MODE == OP_RESID) {
-                out[gi] = csub(bring[warp][s][lane], y);
+                *outp = csub(bring[warp][s][lane], yo);
               } else if (MODE == OP_RESNORM) {
-                acc += cnorm2(csub(bring[warp][s][lane], y));
+                acc += cnorm2(csub(bring[warp][s][lane], yo));
               } else {
-                const double2 cyc = cy[ro][B];
+                const double2 cyc = cyk[B];
                 const double2 D = csub(cmk(cyc.x * sx[B] + cyc.y * mx[B], 0.0), cscale(cyc.x * mx[B], c));
-                const double2 r = csub(bring[warp][s][lane], y);
-                out[gi] = cadd(XC[(t + 1 + B) % NB], cscale(omega, cmul(cinv(D), r)));
+                const double2 r = csub(bring[warp][s][lane], yo);
+                *outp = cadd(XC[(t + 1) % NB], cscale(omega, cmul(cinv(D), r)));
               }
             }
+            yo = cmk(0.0, 0.0);
+            outp += n;
           }
+          cyk += NB;
+          s = (s + 1) & (kSRing - 1);
         }
       }
     }

@@ -99,6 +99,23 @@ __device__ __forceinline__ int pw2(int i, int nc, double drop, int* q, double* w
   return m;
 }
 
+// Separable prolongation weights of fine index i into the zero-padded coarse
+// region (local index l = q - q0, q0 = f0/2 - 1 for an even tile origin f0):
+// the three taps cover local indices li-1, li, li+1 with li = i/2 - q0 for odd
+// i (linear: 0, 1, 0; Bezier: 1/8, (6-drop)/8, 1/8 on (i-3)/2, (i-1)/2, (i+1)/2)
+// and li-1, li for even i (1/2, 1/2 on i/2 - 1, i/2).  Coarse indices outside
+// [0, nc) are zero in the region, which drops those entries exactly as the
+// reference's stencil does (no renormalisation).
+template <int KIND>
+__device__ __forceinline__ void ptaps(int i, double drop, double& w0, double& w1, double& w2) {
+  if (i & 1) {
+    if (KIND == 0) { w0 = 0.0; w1 = 1.0; w2 = 0.0; }
+    else { w0 = 0.125; w1 = (6.0 - drop) / 8.0; w2 = 0.125; }
+  } else {
+    w0 = 0.5; w1 = 0.5; w2 = 0.0;
+  }
+}
+
 // PMODE 0: out += Z e (interleaved e);  1: out = s - Z e (planar e);  2: out = Z e (planar e)
 template <int KIND, int PMODE>
 __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* __restrict__ ec,
@@ -106,6 +123,7 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
                                                    const double2* __restrict__ s, double2* __restrict__ out) {
   constexpr int CR = kPFY / 2 + 3, CC = kPFX / 2 + 3;
   __shared__ double2 cs[CR][CC];
+  __shared__ double2 ty[kPFY][CC];  // y-interpolated coarse columns for every fine row of the tile
   const int fx0 = blockIdx.x * kPFX, fy0 = blockIdx.y * kPFY;
   const int qx0 = fx0 / 2 - 1, qy0 = fy0 / 2 - 1;  // region origin (may be -1)
   const size_t NC = (size_t)nc * nc;
@@ -120,22 +138,33 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
     cs[rr][cc] = v;
   }
   __syncthreads();
+  // y pass: fine row fy (local r) from coarse rows li-1..li+1, li = fy/2 - qy0
+  for (int e = threadIdx.x; e < kPFY * CC; e += blockDim.x) {
+    const int r = e / CC, cc = e % CC;
+    const int fy = fy0 + r;
+    const int li = fy / 2 - qy0;  // >= 1
+    double w0, w1, w2;
+    ptaps<KIND>(fy, drop, w0, w1, w2);
+    double2 t;
+    if (fy & 1) t = cfma_r(w0, cs[li - 1][cc], cfma_r(w1, cs[li][cc], cscale(w2, cs[li + 1][cc])));
+    else t = cfma_r(w0, cs[li - 1][cc], cscale(w1, cs[li][cc]));
+    ty[r][cc] = t;
+  }
+  __syncthreads();
+  // x pass + combine with the fine vector, 4 points per thread (coalesced rows)
   for (int e = threadIdx.x; e < kPFY * kPFX; e += blockDim.x) {
-    const int fy = fy0 + e / kPFX, fx = fx0 + e % kPFX;
+    const int r = e / kPFX, cx = e % kPFX;
+    const int fy = fy0 + r, fx = fx0 + cx;
     if (fy >= nf || fx >= nf) continue;
-    int qy[3], qx[3];
-    double wy[3], wx[3];
-    const int my = pw2<KIND>(fy, nc, drop, qy, wy);
-    const int mx = pw2<KIND>(fx, nc, drop, qx, wx);
-    double2 acc = cmk(0.0, 0.0);
-    for (int a = 0; a < my; ++a) {
-      double2 t = cmk(0.0, 0.0);
-      for (int b = 0; b < mx; ++b) t = cfma_r(wx[b], cs[qy[a] - qy0][qx[b] - qx0], t);
-      acc = cfma_r(wy[a], t, acc);
-    }
+    const int li = fx / 2 - qx0;
+    double w0, w1, w2;
+    ptaps<KIND>(fx, drop, w0, w1, w2);
+    double2 acc;
+    if (fx & 1) acc = cfma_r(w0, ty[r][li - 1], cfma_r(w1, ty[r][li], cscale(w2, ty[r][li + 1])));
+    else acc = cfma_r(w0, ty[r][li - 1], cscale(w1, ty[r][li]));
     const size_t gi = (size_t)fy * nf + fx;
     if (PMODE == 0) out[gi] = cadd(out[gi], acc);
-    else if (PMODE == 1) out[gi] = csub(s[gi], acc);
+    else if (PMODE == 1) out[gi] = csub(ld_stream(s + gi), acc);
     else out[gi] = acc;
   }
 }
