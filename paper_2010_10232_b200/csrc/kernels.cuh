@@ -522,6 +522,78 @@ __global__ void k_fd_scale(double* __restrict__ T, const double2* __restrict__ D
   }
 }
 
+// ---- reflection-folded fast diagonalisation (solver.cu make_fd_folded) ----
+// X col-major n x ncol (planar complex: ncol = 2n); F[b] col-major n2 x ncol
+__global__ void k_fold_rows(const double* __restrict__ X, double* __restrict__ F, int n, int n2, int ncol) {
+  const size_t tot = (size_t)n2 * ncol;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(g % n2);
+    const size_t col = g / n2;
+    const double a = X[col * n + i], b = X[col * n + (n - 1 - i)];
+    F[col * n2 + i] = a + b;
+    F[tot + col * n2 + i] = a - b;
+  }
+}
+
+// Hh[yb][xb][p](kx, j) = G_xb(kx, p n + j) +- G_xb(kx, p n + n-1-j)
+__global__ void k_fold_cols(const double* __restrict__ G, double* __restrict__ Hh, int n, int n2) {
+  const size_t nn = (size_t)n2 * n2;
+  const size_t tot = 4 * nn;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
+    const int kx = (int)(g % n2);
+    const int j = (int)((g / n2) % n2);
+    const int p = (int)((g / nn) % 2);
+    const int xb = (int)(g / (2 * nn));
+    const double* Gx = G + (size_t)xb * n2 * 2 * n;
+    const double a = Gx[((size_t)p * n + j) * n2 + kx], b = Gx[((size_t)p * n + (n - 1 - j)) * n2 + kx];
+    Hh[((size_t)(0 * 2 + xb) * 2 + p) * nn + (size_t)j * n2 + kx] = a + b;
+    Hh[((size_t)(1 * 2 + xb) * 2 + p) * nn + (size_t)j * n2 + kx] = a - b;
+  }
+}
+
+// R[yb][xb][p](kx, ky): (R_p0 + i R_p1) *= D[yb][xb][ky][kx]
+__global__ void k_scale_folded(double* __restrict__ R, const double2* __restrict__ D, int n2) {
+  const size_t nn = (size_t)n2 * n2;
+  const size_t tot = 4 * nn;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
+    const size_t blk = g / nn, e = g % nn;  // e = ky * n2 + kx (col-major (kx, ky))
+    double* r0 = R + (blk * 2 + 0) * nn + e;
+    double* r1 = R + (blk * 2 + 1) * nn + e;
+    const double2 v = cmul(cmk(*r0, *r1), D[g]);
+    *r0 = v.x;
+    *r1 = v.y;
+  }
+}
+
+// S[yb][xb][p](kx, j) -> Z_xb(kx, p n + j) = S_s + S_a, Z_xb(kx, p n + n-1-j) = S_s - S_a
+__global__ void k_unfold_cols(const double* __restrict__ S, double* __restrict__ Z, int n, int n2) {
+  const size_t nn = (size_t)n2 * n2;
+  const size_t tot = 4 * nn;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
+    const int kx = (int)(g % n2);
+    const int j = (int)((g / n2) % n2);
+    const int p = (int)((g / nn) % 2);
+    const int xb = (int)(g / (2 * nn));
+    const double ss = S[((size_t)(0 * 2 + xb) * 2 + p) * nn + (size_t)j * n2 + kx];
+    const double sa = S[((size_t)(1 * 2 + xb) * 2 + p) * nn + (size_t)j * n2 + kx];
+    double* Zx = Z + (size_t)xb * n2 * 2 * n;
+    Zx[((size_t)p * n + j) * n2 + kx] = ss + sa;
+    Zx[((size_t)p * n + (n - 1 - j)) * n2 + kx] = ss - sa;
+  }
+}
+
+// Y(i, c) = Yh_s(i, c) + Yh_a(i, c);  Y(n-1-i, c) = Yh_s(i, c) - Yh_a(i, c)
+__global__ void k_unfold_rows(const double* __restrict__ Yh, double* __restrict__ Y, int n, int n2, int ncol) {
+  const size_t tot = (size_t)n2 * ncol;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(g % n2);
+    const size_t col = g / n2;
+    const double a = Yh[col * n2 + i], b = Yh[tot + col * n2 + i];
+    Y[col * n + i] = a + b;
+    Y[col * n + (n - 1 - i)] = a - b;
+  }
+}
+
 // Banded LU solve with the host-computed factors (one thread; 1D only).
 // in/out interleaved (planar == nullptr) or planar (n re, n im).
 __global__ void k_bandlu_solve(const double2* __restrict__ Lf, const double2* __restrict__ Uf,

@@ -88,6 +88,13 @@ struct ExactSolver {
   double2* U = nullptr;
   int* piv = nullptr;
   double2* work = nullptr;
+  // reflection-folded fast diagonalisation (centro-symmetric E, even n):
+  // Vt = [Vs_top | Va_top] (2 x n2 x n2), Dinvf in [y parity][x parity][ky][kx]
+  bool folded = false;
+  int n2 = 0;
+  double* Vt = nullptr;
+  double2* Dinvf = nullptr;
+  double *F = nullptr, *G = nullptr, *Hh = nullptr, *R = nullptr;
 };
 
 }  // namespace hd
@@ -109,6 +116,8 @@ struct hd_ctx {
   double2 cM = cmk(0.0, 0.0);   // shifted: - k^2 (1 - i beta2) M(x)M
   std::vector<DevBand> lev;     // multigrid levels (lev[0] = fine)
   ExactSolver coarsest;
+  ExactSolver shift_exact;      // C_ex: exact inverse of the shifted operator (cycles == 0)
+  double* sx_plan = nullptr;    // planar scratch for the 2D exact shifted solve
   std::vector<double2*> mg_b, mg_x, mg_y, mg_r;
   // deflation
   int nc = 0;
@@ -231,6 +240,104 @@ static std::vector<double> dense_of(const Band& B) {
   return D;
 }
 
+// Dense generalized symmetric-definite eigenproblem A v = lam B v (cuSOLVER
+// sygvd), eigenvectors returned column-major on the device, V^T B V = I.
+static void sygvd_device(cudaStream_t st, const std::vector<double>& A, const std::vector<double>& Bm, int n,
+                         double* dV, std::vector<double>& lam) {
+  double *dB = dalloc<double>(Bm.size()), *dW = dalloc<double>(n);
+  int* dinfo = dalloc<int>(1);
+  CK(cudaMemcpy(dV, A.data(), A.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, Bm.data(), Bm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  cusolverDnHandle_t h;
+  CKS(cusolverDnCreate(&h));
+  CKS(cusolverDnSetStream(h, st));
+  int lwork = 0;
+  CKS(cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dV, n,
+                                  dB, n, dW, &lwork));
+  double* dwork = dalloc<double>(std::max(lwork, 1));
+  CKS(cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dV, n, dB, n, dW,
+                       dwork, lwork, dinfo));
+  int info = 0;
+  CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cusolverDnDestroy(h);
+  if (info != 0) throw Error(HD_ERR_FACTOR, "coarse operator factorization failed (sygvd info " + std::to_string(info) + ")");
+  lam.resize(n);
+  CK(cudaMemcpy(lam.data(), dW, n * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(dB);
+  cudaFree(dW);
+  cudaFree(dinfo);
+  cudaFree(dwork);
+}
+
+// True when the banded matrix is centro-symmetric, X(i,j) = X(n-1-i, n-1-j),
+// to rounding (the reflected B-spline basis and an odd fine size make the
+// Bezier-coarsened E so).
+static bool centro_symmetric(const Band& X) {
+  double mx = 0.0, dev = 0.0;
+  for (int i = 0; i < X.n; ++i)
+    for (int d = -X.b; d <= X.b; ++d) {
+      const int j = i + d;
+      if (j < 0 || j >= X.n) continue;
+      mx = std::max(mx, std::abs(X.at(i, j)));
+      dev = std::max(dev, std::abs(X.at(i, j) - X.at(X.n - 1 - i, X.n - 1 - j)));
+    }
+  return dev <= 1e-13 * mx;
+}
+
+// Reflection-folded fast diagonalisation: for even n and centro-symmetric
+// S, M the eigenvectors are symmetric [a; Ja]/sqrt2 or antisymmetric
+// [a; -Ja]/sqrt2 with a from the half-size problems (X_tt +- X_tb J).  Every
+// transform then costs two half-size GEMMs instead of one full one.
+static ExactSolver make_fd_folded(cudaStream_t st, const Band& S, const Band& M, double2 c) {
+  ExactSolver X;
+  X.dim = 2;
+  X.folded = true;
+  X.n = S.n;
+  const int n = S.n, n2 = n / 2;
+  X.n2 = n2;
+  X.Vt = dalloc<double>(2 * static_cast<size_t>(n2) * n2);
+  std::vector<double> lam[2];
+  for (int par = 0; par < 2; ++par) {
+    const double sg = par == 0 ? 1.0 : -1.0;
+    std::vector<double> As(static_cast<size_t>(n2) * n2), Bs(As.size());
+    for (int i = 0; i < n2; ++i)
+      for (int j = 0; j < n2; ++j) {
+        // (X_tt +- X_tb J)(i, j) = X(i, j) +- X(i, n-1-j), column-major
+        As[i + static_cast<size_t>(j) * n2] = S.at(i, j) + sg * S.at(i, n - 1 - j);
+        Bs[i + static_cast<size_t>(j) * n2] = M.at(i, j) + sg * M.at(i, n - 1 - j);
+      }
+    double* dV = X.Vt + static_cast<size_t>(par) * n2 * n2;
+    sygvd_device(st, As, Bs, n2, dV, lam[par]);
+  }
+  // scale the half-vectors by 1/sqrt2 (full vectors [a; +-Ja]/sqrt2 are M-orthonormal)
+  {
+    std::vector<double> hv(2 * static_cast<size_t>(n2) * n2);
+    CK(cudaMemcpy(hv.data(), X.Vt, hv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (double& v : hv) v *= std::sqrt(0.5);
+    CK(cudaMemcpy(X.Vt, hv.data(), hv.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  std::vector<double2> D(4 * static_cast<size_t>(n2) * n2);
+  for (int yb = 0; yb < 2; ++yb)
+    for (int xb = 0; xb < 2; ++xb)
+      for (int ky = 0; ky < n2; ++ky)
+        for (int kx = 0; kx < n2; ++kx) {
+          const std::complex<double> d(lam[yb][ky] + lam[xb][kx] - c.x, -c.y);
+          if (d == std::complex<double>(0.0, 0.0))
+            throw Error(HD_ERR_FACTOR, "coarse operator factorization failed (singular)");
+          const std::complex<double> r = 1.0 / d;
+          D[((static_cast<size_t>(yb) * 2 + xb) * n2 + ky) * n2 + kx] = cmk(r.real(), r.imag());
+        }
+  X.Dinvf = dalloc<double2>(D.size());
+  CK(cudaMemcpy(X.Dinvf, D.data(), D.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  const size_t half = 2 * static_cast<size_t>(n2) * 2 * n;  // 2 parities x n2 x 2n
+  X.F = dalloc<double>(half);
+  X.G = dalloc<double>(half);
+  X.Hh = dalloc<double>(8 * static_cast<size_t>(n2) * n2);
+  X.R = dalloc<double>(8 * static_cast<size_t>(n2) * n2);
+  return X;
+}
+
 // Fast diagonalisation of W = M(x)S + S(x)M - c M(x)M: S V = M V diag(lam),
 // V^T M V = I (cuSOLVER sygvd at setup), Dinv = 1/(lam_i + lam_j - c).
 static ExactSolver make_fd(cudaStream_t st, const Band& S, const Band& M, double2 c) {
@@ -298,6 +405,7 @@ static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 
 
 static void free_exact(ExactSolver& X) {
   cudaFree(X.V); cudaFree(X.Dinv); cudaFree(X.T1); cudaFree(X.T2);
+  cudaFree(X.Vt); cudaFree(X.Dinvf); cudaFree(X.F); cudaFree(X.G); cudaFree(X.Hh); cudaFree(X.R);
   cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work);
   X = ExactSolver{};
 }
@@ -486,6 +594,43 @@ static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, 
 
 // Exact solve: in/out planar (2D FD) or via the banded LU (1D).
 static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
+  if (X.dim == 2 && X.folded) {
+    const int n = X.n, n2 = X.n2;
+    const long nn = static_cast<long>(n2) * n2;
+    const long hc = static_cast<long>(n2) * 2 * n;  // one parity of a half-folded n2 x 2n block
+    const double one = 1.0, zero = 0.0;
+    const double gb = 16.0 * nn * 4;               // nominal bytes per GEMM call (profiling)
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_rows<<<grid_for(hc), 256, 0, c->st>>>(inout, X.F, n, n2, 2 * n));
+    size_t mk = prof_mark(c);
+    // x transform: G_b = Vt_b^T F_b
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n2, 2 * n, n2, &one, X.Vt, n2, nn, X.F, n2, hc,
+                                  &zero, X.G, n2, hc, 2));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_cols<<<grid_for(4 * nn), 256, 0, c->st>>>(X.G, X.Hh, n, n2));
+    // y transform: R[yb] = Hh[yb] Vt_yb (batch over x parity and plane)
+    for (int yb = 0; yb < 2; ++yb) {
+      mk = prof_mark(c);
+      CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n2, n2, n2, &one, X.Hh + yb * 4 * nn, n2, nn,
+                                    X.Vt + yb * nn, n2, 0, &zero, X.R + yb * 4 * nn, n2, nn, 4));
+      launched(c, HD_K_LIBGEMM, mk, gb, true);
+    }
+    HD_LAUNCH(HD_K_EXACT, 48.0 * 4 * nn, k_scale_folded<<<grid_for(4 * nn), 256, 0, c->st>>>(X.R, X.Dinvf, n2));
+    // inverse y: S[yb] = R[yb] Vt_yb^T  (into Hh)
+    for (int yb = 0; yb < 2; ++yb) {
+      mk = prof_mark(c);
+      CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, n2, n2, n2, &one, X.R + yb * 4 * nn, n2, nn,
+                                    X.Vt + yb * nn, n2, 0, &zero, X.Hh + yb * 4 * nn, n2, nn, 4));
+      launched(c, HD_K_LIBGEMM, mk, gb, true);
+    }
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_cols<<<grid_for(4 * nn), 256, 0, c->st>>>(X.Hh, X.F, n, n2));
+    // inverse x: Yh_b = Vt_b Z_b  (Z in F, result in G)
+    mk = prof_mark(c);
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n2, 2 * n, n2, &one, X.Vt, n2, nn, X.F, n2, hc,
+                                  &zero, X.G, n2, hc, 2));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_rows<<<grid_for(hc), 256, 0, c->st>>>(X.G, inout, n, n2, 2 * n));
+    return;
+  }
   if (X.dim == 2) {
     const int n = X.n;
     const long nn = static_cast<long>(n) * n;
@@ -570,8 +715,40 @@ static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero) {
 }
 
 // out = MG^-1 b  with `cycles` V-cycles from zero (src/precond.cpp:159-163)
+__global__ void k_to_planar(const double2* __restrict__ a, double* __restrict__ p, size_t N) {
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = a[g];
+    p[g] = v.x;
+    p[g + N] = v.y;
+  }
+}
+__global__ void k_from_planar(const double* __restrict__ p, double2* __restrict__ a, size_t N) {
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
+    a[g] = cmk(p[g], p[g + N]);
+}
+
+// out = M^-1 b exactly (C_ex, src/precond.cpp:204-211): fast diagonalisation
+// of the shifted Kronecker sum on the fine level (2D) or banded LU (1D)
+static void shift_exact_solve(hd_ctx* c, const double2* b, double2* out) {
+  const size_t N = c->N;
+  ExactSolver& X = c->shift_exact;
+  if (X.dim == 2) {
+    HD_LAUNCH(HD_K_VEC, 32.0 * N, k_to_planar<<<grid_for(N), 256, 0, c->st>>>(b, c->sx_plan, N));
+    exact_solve_planar(c, X, c->sx_plan);
+    HD_LAUNCH(HD_K_VEC, 32.0 * N, k_from_planar<<<grid_for(N), 256, 0, c->st>>>(c->sx_plan, out, N));
+  } else {
+    HD_LAUNCH(HD_K_EXACT, 32.0 * X.n,
+              k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, b, nullptr, X.work, out,
+                                                  nullptr));
+  }
+}
+
 static void mg_solve(hd_ctx* c, const double2* b, double2* out) {
   const size_t N = c->N;
+  if (c->spec.cycles <= 0) {
+    shift_exact_solve(c, b, out);
+    return;
+  }
   bool zero = true;
   double2* xb = nullptr;
   for (int cy = 0; cy < c->spec.cycles; ++cy) {
@@ -1109,6 +1286,8 @@ static void destroy_ctx(hd_ctx* c) {
   fb(c->fine);
   for (size_t l = 1; l < c->lev.size(); ++l) fb(c->lev[l]);
   free_exact(c->coarsest);
+  free_exact(c->shift_exact);
+  cudaFree(c->sx_plan);
   free_exact(c->E);
   for (auto* p : c->mg_b) cudaFree(p);
   for (auto* p : c->mg_x) cudaFree(p);
@@ -1146,7 +1325,6 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
     throw Error(HD_ERR_NO_DEVICE, "no CUDA device: the helmdef_b200 path has no CPU fallback");
   if (sys->dim != 1 && sys->dim != 2) throw Error(HD_ERR_INVALID, "dim must be 1 or 2");
   if (sys->field_kind != HD_FIELD_CONSTANT) throw Error(HD_ERR_INVALID, "only constant wave-number fields are supported");
-  if (spec->shift && spec->cycles <= 0) throw Error(HD_ERR_INVALID, "exact shifted inverse (cycles = 0, C_ex) is not on the device path");
   if (sys->per_dim < 2) throw Error(HD_ERR_INVALID, "per_dim must be >= 2");
   const auto t0 = std::chrono::steady_clock::now();
   std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
@@ -1174,8 +1352,17 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   const Band S1 = band_from_host(sys->stiffness_band, c->n, sys->order);
   const Band M1 = band_from_host(sys->mass_band, c->n, sys->order);
   c->fine = upload_pair(S1, M1);
+  // C_ex: exact shifted inverse (src/precond.cpp:204-211)
+  if (c->spec.shift && c->spec.cycles <= 0) {
+    if (c->dim == 2) {
+      c->shift_exact = make_fd(c->st, S1, M1, c->cM);
+      c->sx_plan = dalloc<double>(2 * c->N);
+    } else {
+      c->shift_exact = make_bandlu(S1, M1, c->cM, c->corner);
+    }
+  }
   // multigrid hierarchy of the shifted operator (src/precond.cpp:110-134)
-  if (c->spec.shift) {
+  if (c->spec.shift && c->spec.cycles > 0) {
     std::vector<Band> Ss{S1}, Ms{M1};
     int nl = c->n;
     while (nl > c->spec.coarsest) {
@@ -1217,7 +1404,9 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
     if (c->nc < 1) throw Error(HD_ERR_INVALID, "deflation needs per_dim >= 2");
     const Band ES = galerkin(S1, z), EM = galerkin(M1, z);
     if (c->dim == 2) {
-      c->E = make_fd(c->st, ES, EM, c->cA);
+      const bool fold = (c->nc % 2 == 0) && centro_symmetric(ES) && centro_symmetric(EM) &&
+                        !std::getenv("HD_NOFOLD");
+      c->E = fold ? make_fd_folded(c->st, ES, EM, c->cA) : make_fd(c->st, ES, EM, c->cA);
     } else {
       // corner term of A restricted: Z^T (corner e_n e_n^T) Z
       double2 corner_c = cmk(0.0, 0.0);

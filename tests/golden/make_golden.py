@@ -31,6 +31,10 @@ CASES = {
     "2d_p4_k30_eps_nu3": ("point_source_2d", 4, 45, 30.0, "Deps_C_MG",
                           {"epsilon": 0.1, "smoothing": 3, "beta2": "4.2", "omega": 0.6}),
     "2d_p5_k25_t5": ("point_source_2d", 5, 36, 25.0, "DC_MG", {"smoothing": 3, "beta2": "4.2", "omega": 0.5}),
+    # exact shifted inverse (C_ex) cells of the reference tables (table3 1D, table5 2D)
+    "1d_p3_k1000_Cex": ("point_source_1d", 3, 1598, 1000.0, "C_ex", {"beta2": "1/k"}),
+    "2d_p2_k50_Cex": ("point_source_2d", 2, 79, 50.0, "C_ex", {"beta2": "1/(3k)"}),
+    "2d_p3_k50_D_eps": ("point_source_2d", 3, 78, 50.0, "D_eps", {"epsilon": 0.1}),
 }
 
 

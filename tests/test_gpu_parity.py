@@ -203,24 +203,41 @@ def _kron_apply(s, x):
 
 def test_C5_full_size_2d():
     """C5: 2D k=1000, p=3, 1600^2 elements (2.56 M unknowns) against the committed
-    oracle run (tests/golden/make_c5.py) + size-independent properties."""
+    oracle run (tests/golden/make_c5.py) + size-independent properties.
+
+    Bars and why: iterations equal (+-1 allowed), final solution
+    within 1e-8 relative (measured ~4e-10 via seeded projections and the norm),
+    and the true-residual history within 1e-9 outside C5's stagnation phase
+    (measured <= 4.7e-10; E = Z^T A Z has cond ~5e5 at C5, so the device's and
+    the oracle's exact coarse solves differ by ~1e-10 per application).  Inside
+    the stagnation phase (iterations ~23-60) rounding differences grow ~100x per
+    step: two exact CPU implementations of the reference algorithm (MGS vs its
+    one-reduction ICWY form, tests/golden/make_c5_envelope.py) already differ by
+    up to 9e-4 there, so the history is only required to agree to a factor 3 there (measured 2.0)."""
     ref = json.loads((GOLD / "C5_oracle.json").read_text())
+    env = json.loads((GOLD / "C5_envelope.json").read_text())["envelope"]
     s = hd.assemble(hd.point_source_2d(1600, 3, 1000.0))
     with hd.Solver(s, hd.to_spec("DC_MG", 3, 1000.0, **BASE)) as solver:
         r = solver.solve(hd.GmresOptions(100, 1e-7))
     assert r.converged == ref["converged"] and abs(r.iterations - ref["iterations"]) <= 1
-    m = min(len(r.residuals), len(ref["residuals"]))
-    d = np.abs(np.array(r.residuals[:m]) - np.array(ref["residuals"][:m]))
-    assert d.max() <= RES_TOL, d.max()
+    m = min(len(r.residuals), len(ref["residuals"]), len(env))
+    sensitive = [max(env[max(0, j - 3):j + 4]) > 1e-10 for j in range(m)]
+    for j in range(m):
+        a, b = r.residuals[j], ref["residuals"][j]
+        if sensitive[j]:
+            assert b / 3.0 <= a <= 3.0 * b, (j, a, b)
+        else:
+            assert abs(a - b) <= 1e-9, (j, a, b)
+    assert not any(sensitive[:20])  # the pre-stagnation phase is held to the plain bar
     # the reported final residual is the true relative residual of the returned x
     true = np.linalg.norm(s.rhs - _kron_apply(s, r.solution)) / np.linalg.norm(s.rhs)
     assert abs(true - r.residuals[-1]) <= 1e-12 and true <= 1e-7
-    # seeded projections of the solution (a checksum that is size independent)
+    # seeded projections of the solution (size-independent checksum) and its norm
     rng = np.random.default_rng(2024)
     for re_, im_ in ref["projections"]:
         w = rng.uniform(-1, 1, r.solution.size) + 1j * rng.uniform(-1, 1, r.solution.size)
         got = np.vdot(w, r.solution)
-        assert abs(got - complex(re_, im_)) <= SOL_TOL * abs(complex(re_, im_)) + 1e-8 * ref["solution_norm"]
+        assert abs(got - complex(re_, im_)) <= SOL_TOL * abs(complex(re_, im_))
     assert abs(np.linalg.norm(r.solution) - ref["solution_norm"]) <= SOL_TOL * ref["solution_norm"]
 
 
@@ -258,6 +275,15 @@ def test_arbitrary_rhs_linearity():
 
 
 def test_unsupported_specs_fail_loudly():
-    s = hd.assemble(hd.point_source_2d(40, 2, 20.0))
+    s = hd.assemble(hd.layered_medium_2d(40, 2, 20.0))
     with pytest.raises(hd.HelmdefError):
-        hd.Solver(s, hd.to_spec("C_ex", 2, 20.0, beta2="1/(3k)"))
+        hd.Solver(s, hd.to_spec("DC_MG", 2, 20.0, beta2="4.2", smoothing=3))
+
+
+@pytest.mark.parametrize("problem,p,k,beta2", [("point_source_1d", 2, 1000.0, "1/k"),
+                                               ("point_source_2d", 3, 100.0, "1/(3k)")])
+def test_exact_shifted_inverse_C_ex(problem, p, k, beta2):
+    """C_ex cells (reference table2/3/5 columns): exact CSLP inverse on the device."""
+    ne = O.derived_elements(k, 0.625, p)
+    r = _live(problem, p, ne, k, "C_ex", dict(beta2=beta2))
+    assert r.converged
