@@ -299,8 +299,15 @@ def run_gpu(args):
     if dom:
         name, (n, ms, b) = dom
         ach = b / (ms * 1e-3) / 1e9
+        traffic, traffic_src = None, None
+        try:  # per-launch DRAM bytes of the same kernels from the committed ncu capture
+            tr = json.loads((ROOT / "profiles" / "r1_traffic.json").read_text())
+            if tr.get("kernel_kind") == name and args.config == "C5":
+                traffic, traffic_src = tr["dram_bytes_per_launch"], tr["source"]
+        except Exception:
+            pass
         roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": None, "launches": n,
+                "frac": round(ach / peak, 4), "traffic": traffic, "traffic_source": traffic_src, "launches": n,
                 "bytes_per_launch": b / n, "us_per_launch": 1e3 * ms / n, "peak_source": peak_src}
     # whole-solve effective bandwidth on the algorithmic bytes of all own kernels
     all_b = sum(v[2] for k_, v in prof.items() if k_ != "lib_gemm")
