@@ -594,6 +594,167 @@ __global__ void k_unfold_rows(const double* __restrict__ Yh, double* __restrict_
   }
 }
 
+// Banded LU solve, sequential in one thread, with the factors streamed into
+// shared memory by the rest of the CTA one chunk ahead (double-buffered), so
+// the dependent elimination chain only ever waits on shared memory.  The
+// elimination window lives in registers (KL = lower bandwidth of L, the
+// factor's upper bandwidth is 2 KL).  in/out interleaved or planar.
+template <int KL>
+__global__ void __launch_bounds__(256) k_bandlu_staged(const double2* __restrict__ Lf, const double2* __restrict__ Uf,
+                                                       const double2* __restrict__ Uinv, const int* __restrict__ piv,
+                                                       int n, const double2* __restrict__ b,
+                                                       const double* __restrict__ bp, double2* __restrict__ work,
+                                                       double2* __restrict__ x, double* __restrict__ xp) {
+  constexpr int KU = 2 * KL;
+  constexpr int CH = 256;
+  extern __shared__ __align__(16) double2 sm[];
+  // forward buffers: [2][CH*KL] L, [2][CH+KL] b (rows r0 .. r0+CH+KL-1: the
+  // window refill never reads the next chunk), [2][CH] pivot offsets;
+  // backward: [2][CH*KU] U, [2][CH] Uinv, [2][CH] y
+  constexpr int CB = CH + KL;
+  double2* fL = sm;
+  double2* fB = fL + 2 * CH * KL;
+  int* fP = reinterpret_cast<int*>(fB + 2 * CB);
+  const int nch = (n + CH - 1) / CH;
+  auto stage_fwd = [&](int c, int buf, int t0, int nt) {
+    const int r0 = c * CH, rn = min(CH, n - r0), rb = min(CB, n - r0);
+    for (int e = t0; e < rn * KL; e += nt) fL[buf * CH * KL + e] = Lf[(size_t)r0 * KL + e];
+    for (int e = t0; e < rb; e += nt) fB[buf * CB + e] = bp ? cmk(bp[r0 + e], bp[r0 + e + n]) : b[r0 + e];
+    for (int e = t0; e < rn; e += nt) fP[buf * CH + e] = piv[r0 + e] - (r0 + e);
+  };
+  stage_fwd(0, 0, threadIdx.x, blockDim.x);
+  __syncthreads();
+  // window w[0..KL] = rows k..k+KL of the (permuted, partially eliminated) rhs
+  double2 w[KL + 1];
+#pragma unroll
+  for (int r = 0; r <= KL; ++r) w[r] = cmk(0.0, 0.0);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int r = 0; r < KL; ++r) w[r + 1] = r < n ? fB[r] : cmk(0.0, 0.0);
+  }
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (threadIdx.x >= 32) {  // warps 1.. stage; warp 0 holds only the sequential lane
+      if (c + 1 < nch) stage_fwd(c + 1, buf ^ 1, threadIdx.x - 32, blockDim.x - 32);
+    } else if (threadIdx.x == 0) {
+      const int r0 = c * CH, rn = min(CH, n - r0);
+      const double2* bb = fB + buf * CB;
+      const double2* lb = fL + buf * CH * KL;
+      const int* pb = fP + buf * CH;
+      // operands of step i are loaded during step i-1 (software pipeline)
+      double2 ln[KL];
+      int dpn = pb[0];
+      double2 bn = (r0 + KL < n) ? bb[KL] : cmk(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < KL; ++r) ln[r] = lb[r];
+      for (int i = 0; i < rn; ++i) {
+        const int k = r0 + i;
+        const int dp = dpn;
+        double2 l[KL];
+#pragma unroll
+        for (int r = 0; r < KL; ++r) l[r] = ln[r];
+        const double2 bin = bn;
+        if (i + 1 < rn) {
+          dpn = pb[i + 1];
+#pragma unroll
+          for (int r = 0; r < KL; ++r) ln[r] = lb[(i + 1) * KL + r];
+          bn = (k + 1 + KL < n) ? bb[i + 1 + KL] : cmk(0.0, 0.0);
+        }
+        // window <- rows k .. k+KL: shift, and bring in row k+KL untouched so far
+#pragma unroll
+        for (int r = 0; r < KL; ++r) w[r] = w[r + 1];
+        w[KL] = bin;
+#pragma unroll
+        for (int r = 1; r <= KL; ++r)
+          if (dp == r) {
+            const double2 t = w[0];
+            w[0] = w[r];
+            w[r] = t;
+          }
+#pragma unroll
+        for (int r = 1; r <= KL; ++r) w[r] = csub(w[r], cmul(l[r - 1], w[0]));
+        work[k] = w[0];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- backward: x_k = (y_k - sum_d U(k,k+d) x_{k+d}) / U(k,k), chunks in reverse
+  double2* bU = sm;
+  double2* bI = bU + 2 * CH * KU;
+  double2* bY = bI + 2 * CH;
+  auto stage_bwd = [&](int c, int buf, int t0, int nt) {
+    const int r0 = c * CH, rn = min(CH, n - r0);
+    for (int e = t0; e < rn * (KU + 1); e += nt) {
+      const int i = e / (KU + 1), d = e % (KU + 1);
+      if (d > 0) bU[buf * CH * KU + i * KU + (d - 1)] = Uf[(size_t)(r0 + i) * (KU + 1) + d];
+    }
+    for (int e = t0; e < rn; e += nt) {
+      bI[buf * CH + e] = Uinv[r0 + e];
+      bY[buf * CH + e] = __ldcg(&work[r0 + e]);
+    }
+  };
+  __threadfence_block();
+  stage_bwd(nch - 1, (nch - 1) & 1, threadIdx.x, blockDim.x);
+  __syncthreads();
+  double2 xv[KU];  // x_{k+1} .. x_{k+KU}
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int d = 0; d < KU; ++d) xv[d] = cmk(0.0, 0.0);
+  }
+  for (int c = nch - 1; c >= 0; --c) {
+    const int buf = c & 1;
+    if (threadIdx.x >= 32) {
+      if (c > 0) stage_bwd(c - 1, buf ^ 1, threadIdx.x - 32, blockDim.x - 32);
+    } else if (threadIdx.x == 0) {
+      const int r0 = c * CH, rn = min(CH, n - r0);
+      const double2* ub = bU + buf * CH * KU;
+      double2 un[KU];
+      double2 yn = bY[buf * CH + rn - 1], in_ = bI[buf * CH + rn - 1];
+#pragma unroll
+      for (int d = 0; d < KU; ++d) un[d] = ub[(rn - 1) * KU + d];
+      for (int i = rn - 1; i >= 0; --i) {
+        const int k = r0 + i;
+        double2 u[KU];
+#pragma unroll
+        for (int d = 0; d < KU; ++d) u[d] = un[d];
+        const double2 yk = yn, ik = in_;
+        if (i > 0) {
+#pragma unroll
+          for (int d = 0; d < KU; ++d) un[d] = ub[(i - 1) * KU + d];
+          yn = bY[buf * CH + i - 1];
+          in_ = bI[buf * CH + i - 1];
+        }
+        // only the d = 1 term depends on the previous step: sum the rest first
+        double2 s0 = yk, s1 = cmk(0.0, 0.0);
+#pragma unroll
+        for (int d = KU; d >= 2; --d) {
+          if (d & 1) s0 = csub(s0, cmul(u[d - 1], xv[d - 1]));
+          else s1 = csub(s1, cmul(u[d - 1], xv[d - 1]));
+        }
+        const double2 xk = cmul(csub(cadd(s0, s1), cmul(u[0], xv[0])), ik);
+#pragma unroll
+        for (int d = KU - 1; d > 0; --d) xv[d] = xv[d - 1];
+        xv[0] = xk;
+        if (xp) {
+          xp[k] = xk.x;
+          xp[k + n] = xk.y;
+        } else {
+          x[k] = xk;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int KL>
+constexpr size_t bandlu_smem() {
+  constexpr int CH = 256;
+  const size_t f = sizeof(double2) * (2 * CH * KL + 2 * (CH + KL)) + sizeof(int) * 2 * CH;
+  const size_t b = sizeof(double2) * (2 * CH * 2 * KL + 4 * CH);
+  return f > b ? f : b;
+}
+
 // Banded LU solve with the host-computed factors (one thread; 1D only).
 // in/out interleaved (planar == nullptr) or planar (n re, n im).
 __global__ void k_bandlu_solve(const double2* __restrict__ Lf, const double2* __restrict__ Uf,

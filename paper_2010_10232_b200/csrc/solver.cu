@@ -88,6 +88,7 @@ struct ExactSolver {
   double2* U = nullptr;
   int* piv = nullptr;
   double2* work = nullptr;
+  double2* Uinv = nullptr;   // 1 / U(k, k)
   // reflection-folded fast diagonalisation (centro-symmetric E, even n):
   // Vt = [Vs_top | Va_top] (2 x n2 x n2), Dinvf in [y parity][x parity][ky][kx]
   bool folded = false;
@@ -397,6 +398,10 @@ static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 
   X.U = dalloc<double2>(f.U.size());
   X.piv = dalloc<int>(f.piv.size());
   X.work = dalloc<double2>(f.n);
+  std::vector<cplx> uinv(f.n);
+  for (int k = 0; k < f.n; ++k) uinv[k] = 1.0 / f.U[static_cast<size_t>(k) * (f.ku + 1)];
+  X.Uinv = dalloc<double2>(f.n);
+  CK(cudaMemcpy(X.Uinv, uinv.data(), uinv.size() * sizeof(double2), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(X.L, f.L.data(), f.L.size() * sizeof(double2), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(X.U, f.U.data(), f.U.size() * sizeof(double2), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(X.piv, f.piv.data(), f.piv.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -406,8 +411,35 @@ static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 
 static void free_exact(ExactSolver& X) {
   cudaFree(X.V); cudaFree(X.Dinv); cudaFree(X.T1); cudaFree(X.T2);
   cudaFree(X.Vt); cudaFree(X.Dinvf); cudaFree(X.F); cudaFree(X.G); cudaFree(X.Hh); cudaFree(X.R);
-  cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work);
+  cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work); cudaFree(X.Uinv);
   X = ExactSolver{};
+}
+
+template <int KL>
+static void bandlu_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b, const double* bp, double2* x,
+                            double* xp) {
+  static bool attr = false;
+  constexpr size_t sm = bandlu_smem<KL>();
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_bandlu_staged<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    attr = true;
+  }
+  k_bandlu_staged<KL><<<1, 256, sm, st>>>(X.L, X.U, X.Uinv, X.piv, X.n, b, bp, X.work, x, xp);
+}
+
+// 1D exact solve with the staged banded-LU kernel (kl = 1..6), in/out interleaved or planar
+static void bandlu_launch(cudaStream_t st, const ExactSolver& X, const double2* b, const double* bp, double2* x,
+                          double* xp) {
+  if (X.ku != 2 * X.kl) throw Error(HD_ERR_INVALID, "banded LU layout mismatch");
+  switch (X.kl) {
+    case 1: bandlu_launch_t<1>(st, X, b, bp, x, xp); break;
+    case 2: bandlu_launch_t<2>(st, X, b, bp, x, xp); break;
+    case 3: bandlu_launch_t<3>(st, X, b, bp, x, xp); break;
+    case 4: bandlu_launch_t<4>(st, X, b, bp, x, xp); break;
+    case 5: bandlu_launch_t<5>(st, X, b, bp, x, xp); break;
+    case 6: bandlu_launch_t<6>(st, X, b, bp, x, xp); break;
+    default: throw Error(HD_ERR_INVALID, "banded LU bandwidth " + std::to_string(X.kl) + " unsupported");
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -657,8 +689,7 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
     launched(c, HD_K_LIBGEMM, mk, gb, true);
   } else {
     HD_LAUNCH(HD_K_EXACT, 32.0 * X.n,
-              k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, nullptr, inout, X.work, nullptr,
-                                                  inout));
+              bandlu_launch(c->st, X, nullptr, inout, nullptr, inout));
   }
 }
 
@@ -668,8 +699,7 @@ static void coarsest_solve(hd_ctx* c, const double2* b, double2* out) {
   const double NL = X.dim == 2 ? static_cast<double>(X.n) * X.n : X.n;
   HD_LAUNCH(HD_K_EXACT, 32.0 * NL,
             if (X.dim == 2) k_fd_small<<<1, 1024, 0, c->st>>>(X.V, X.Dinv, X.n, b, out);
-            else k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, b, nullptr, X.work, out,
-                                                     nullptr));
+            else bandlu_launch(c->st, X, b, nullptr, out, nullptr));
 }
 
 static size_t lsize(const hd_ctx* c, int n) { return c->dim == 2 ? static_cast<size_t>(n) * n : n; }
@@ -738,8 +768,7 @@ static void shift_exact_solve(hd_ctx* c, const double2* b, double2* out) {
     HD_LAUNCH(HD_K_VEC, 32.0 * N, k_from_planar<<<grid_for(N), 256, 0, c->st>>>(c->sx_plan, out, N));
   } else {
     HD_LAUNCH(HD_K_EXACT, 32.0 * X.n,
-              k_bandlu_solve<<<1, 32, 0, c->st>>>(X.L, X.U, X.piv, X.n, X.kl, X.ku, b, nullptr, X.work, out,
-                                                  nullptr));
+              bandlu_launch(c->st, X, b, nullptr, out, nullptr));
   }
 }
 
