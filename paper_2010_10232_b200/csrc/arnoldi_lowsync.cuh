@@ -84,92 +84,70 @@ __device__ __forceinline__ double2 lsa_collect(const double2* partials, int nslo
 }
 
 // ---------------------------------------------------------------------------
-// pass 1: dots against w and u_j, lagged iterate
+// pass 1: dots against w and u_j as a chunked GEMV-T.  Each CTA stages a chunk
+// of w and u_j in shared memory; its warps stream whole basis vectors over the
+// chunk (coalesced, 8 loads in flight per lane) and reduce once per chunk and
+// vector into per-CTA shared accumulators (one warp owns each vector slot).
 // ---------------------------------------------------------------------------
+constexpr int kLsaCE = 2048;  // chunk elements
+
+constexpr size_t lsa_dots_smem() { return sizeof(double2) * (2 * kLsaCE + 2 * (kLsaMaxJ + 1)); }
+
 __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   constexpr int NW = kLsaBD / 32;
-  __shared__ double2 acc[NW][2 * kLsaMaxJ + 2];  // per-warp partials of s_i and G_jl
-  __shared__ double2 sh_cx[kLsaMaxJ];
+  constexpr int PER = kLsaCE / 32;  // elements per lane per chunk
+  extern __shared__ __align__(16) double2 dsm[];
+  double2* ws = dsm;                    // w chunk
+  double2* us = dsm + kLsaCE;           // u_j chunk
+  double2* acc = dsm + 2 * kLsaCE;      // [0..j]: s_i ; [kLsaMaxJ+1 ..]: G_ji
   __shared__ double2 sh_s[kLsaMaxJ + 1];
   __shared__ double2 sh_lj[kLsaMaxJ];
+  __shared__ double2 hsm[kLsaMaxJ + 1];
   if (a.done && *((volatile const int*)a.done)) return;
   const int j = a.dj ? *a.dj : a.j;
-  const bool dots = a.mode == 0;
-  const bool iter = j >= 1 || a.mode == 1;     // x_{j-1} (mode 1: x_j, iterate-only)
-  const int mi = a.mode == 1 ? j + 1 : j;      // iterate terms
-  const int nd = dots ? j + 1 : 0;             // vectors entering the dots
-  const int nv = max(nd, iter ? mi : 0);       // vectors streamed
+  const int nd = j + 1;
   const int nslot = 2 * kLsaMaxJ + 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int q = threadIdx.x; q < NW * nslot; q += kLsaBD) (&acc[0][0])[q] = cmk(0.0, 0.0);
-  for (int q = threadIdx.x; q < mi; q += kLsaBD) sh_cx[q] = a.cx[q];
-  __syncthreads();
+  for (int q = threadIdx.x; q < nslot; q += kLsaBD) acc[q] = cmk(0.0, 0.0);
   const size_t N = a.N;
-  const size_t tile = (size_t)kLsaBD * kLsaTE;
   const double2* uj = a.U + (size_t)j * N;
-  for (size_t t0 = (size_t)blockIdx.x * tile; t0 < N; t0 += (size_t)gridDim.x * tile) {
-    double2 wv[kLsaTE], ujv[kLsaTE], xv[kLsaTE];
-#pragma unroll
-    for (int u = 0; u < kLsaTE; ++u) {
-      const size_t e = t0 + (size_t)u * kLsaBD + threadIdx.x;
-      const bool ok = e < N;
-      wv[u] = (dots && ok) ? ld_stream(a.w + e) : cmk(0.0, 0.0);
-      ujv[u] = (dots && ok && j > 0) ? uj[e] : cmk(0.0, 0.0);
-      xv[u] = (iter && ok) ? ld_stream(a.x0 + e) : cmk(0.0, 0.0);
+  const size_t nchunks = (N + kLsaCE - 1) / kLsaCE;
+  for (size_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const size_t c0 = ch * kLsaCE;
+    const int len = (int)min((size_t)kLsaCE, N - c0);
+    __syncthreads();  // previous chunk fully consumed
+    for (int e = threadIdx.x; e < kLsaCE; e += kLsaBD) {
+      ws[e] = e < len ? ld_stream(a.w + c0 + e) : cmk(0.0, 0.0);
+      us[e] = (e < len && j > 0) ? uj[c0 + e] : cmk(0.0, 0.0);
     }
-    // software pipeline: the loads of vector i+1 are in flight while vector i
-    // is reduced (8 outstanding 16-B loads per thread)
-    double2 vc[kLsaTE], vnx[kLsaTE];
-    auto load_vec = [&](int i, double2* dst) {
-      const double2* ui = a.U + (size_t)i * N;
-#pragma unroll
-      for (int u = 0; u < kLsaTE; ++u) {
-        const size_t e = t0 + (size_t)u * kLsaBD + threadIdx.x;
-        dst[u] = (i < nv && e < N) ? __ldg(ui + e) : cmk(0.0, 0.0);
-      }
-    };
-    load_vec(0, vc);
-    for (int i = 0; i < nv; ++i) {
-      load_vec(i + 1, vnx);
-      if (i < nd) {
-        double2 s = cmk(0.0, 0.0), gl = cmk(0.0, 0.0);
-#pragma unroll
-        for (int u = 0; u < kLsaTE; ++u) {
-          s = cadd(s, cconjmul(vc[u], wv[u]));
-          gl = cadd(gl, cconjmul(ujv[u], vc[u]));
-        }
-        s = lsa_warp_sum(s);
-        if (i < j) gl = lsa_warp_sum(gl);
-        if (lane == 0) {
-          acc[warp][i] = cadd(acc[warp][i], s);
-          if (i < j) acc[warp][kLsaMaxJ + 1 + i] = cadd(acc[warp][kLsaMaxJ + 1 + i], gl);
+    __syncthreads();
+    for (int i = warp; i < nd; i += NW) {
+      const double2* ui = a.U + (size_t)i * N + c0;
+      double2 sa = cmk(0.0, 0.0), sb = cmk(0.0, 0.0), ga = cmk(0.0, 0.0), gb = cmk(0.0, 0.0);
+#pragma unroll 8
+      for (int q = 0; q < PER; ++q) {
+        const int e = q * 32 + lane;
+        const double2 v = e < len ? __ldg(ui + e) : cmk(0.0, 0.0);
+        if (q & 1) {
+          sb = cadd(sb, cconjmul(v, ws[e]));
+          gb = cadd(gb, cconjmul(us[e], v));
+        } else {
+          sa = cadd(sa, cconjmul(v, ws[e]));
+          ga = cadd(ga, cconjmul(us[e], v));
         }
       }
-      if (iter && i < mi) {
-        const double2 c = sh_cx[i];
-#pragma unroll
-        for (int u = 0; u < kLsaTE; ++u) xv[u] = cfma(c, vc[u], xv[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < kLsaTE; ++u) vc[u] = vnx[u];
-    }
-    if (iter) {
-#pragma unroll
-      for (int u = 0; u < kLsaTE; ++u) {
-        const size_t e = t0 + (size_t)u * kLsaBD + threadIdx.x;
-        if (e < N) a.x[e] = xv[u];
+      double2 s_ = lsa_warp_sum(cadd(sa, sb));
+      double2 g_ = (i < j) ? lsa_warp_sum(cadd(ga, gb)) : cmk(0.0, 0.0);
+      if (lane == 0) {
+        acc[i] = cadd(acc[i], s_);
+        if (i < j) acc[kLsaMaxJ + 1 + i] = cadd(acc[kLsaMaxJ + 1 + i], g_);
       }
     }
   }
-  if (!dots) return;
   __syncthreads();
-  // CTA partials: fixed-order sum over warps
   for (int q = threadIdx.x; q < nslot; q += kLsaBD) {
     const bool used = q < nd || (q >= kLsaMaxJ + 1 && q < kLsaMaxJ + 1 + j);
-    if (!used) continue;
-    double2 s = cmk(0.0, 0.0);
-    for (int wv2 = 0; wv2 < NW; ++wv2) s = cadd(s, acc[wv2][q]);
-    a.partials[(size_t)blockIdx.x * nslot + q] = s;
+    if (used) a.partials[(size_t)blockIdx.x * nslot + q] = acc[q];
   }
   if (!lsa_last_block(a.counter)) return;
   // ---- last CTA: totals, Gram row j, triangular solve (I + L) h = s --------
@@ -192,7 +170,7 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   // sequential in i, parallel over l with a fixed-order reduction
   if (warp == 0) {
     double2* Hj = a.H + (size_t)j * a.ldh;
-    double2* hs = &acc[0][0];  // reuse: h_0..h_j
+    double2* hs = hsm;
     for (int i = 0; i <= j; ++i) {
       double2 t = cmk(0.0, 0.0);
       for (int l = lane; l < i; l += 32)
@@ -215,30 +193,42 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double2 lsa_cdiv(double2 a, double2 b) { return cmul(a, cinv(b)); }
 
+// mode 0: u_{j+1} = sigma_j w - sum_{i<=j} c_i u_i (+ norm) and, for j >= 1, the
+// lagged iterate x_{j-1} = x0 + sum_{i<j} c'_i u_i (src/linalg.cpp:78-80);
+// mode 1 (budget exhausted): only x_j = x0 + sum_{i<=j} c'_i u_i.
 __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
   constexpr int NW = kLsaBD / 32;
   __shared__ double2 sh_c[kLsaMaxJ + 1];
+  __shared__ double2 sh_x[kLsaMaxJ + 1];
   __shared__ double red[NW];
   if (a.done && *((volatile const int*)a.done)) return;
   const int j = a.dj ? *a.dj : a.j;
+  const bool upd = a.mode == 0;
+  const bool iter = a.mode == 1 || j >= 1;
+  const int mi = a.mode == 1 ? j + 1 : j;      // iterate terms
+  const int nv = upd ? j + 1 : mi;             // vectors streamed
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int q = threadIdx.x; q <= j; q += kLsaBD) sh_c[q] = __ldcg(&a.ch[q]);
+  for (int q = threadIdx.x; q <= j; q += kLsaBD) {
+    sh_c[q] = upd ? __ldcg(&a.ch[q]) : cmk(0.0, 0.0);
+    sh_x[q] = (iter && q < mi) ? __ldcg(&a.cx[q]) : cmk(0.0, 0.0);
+  }
   __syncthreads();
-  const double sj = a.sig[j];
+  const double sj = upd ? a.sig[j] : 0.0;
   const size_t N = a.N;
   const size_t tile = (size_t)kLsaBD * kLsaTE;
   double2* un = a.Uw + (size_t)(j + 1) * N;
   double nrm = 0.0;
   for (size_t t0 = (size_t)blockIdx.x * tile; t0 < N; t0 += (size_t)gridDim.x * tile) {
-    double2 wv[kLsaTE];
+    double2 wv[kLsaTE], xv[kLsaTE];
 #pragma unroll
     for (int u = 0; u < kLsaTE; ++u) {
       const size_t e = t0 + (size_t)u * kLsaBD + threadIdx.x;
-      wv[u] = e < N ? cscale(sj, ld_stream(a.w + e)) : cmk(0.0, 0.0);
+      wv[u] = (upd && e < N) ? cscale(sj, ld_stream(a.w + e)) : cmk(0.0, 0.0);
+      xv[u] = (iter && e < N) ? ld_stream(a.x0 + e) : cmk(0.0, 0.0);
     }
     // two vectors per step: 8 outstanding 16-B loads per thread
-    for (int i = 0; i <= j; i += 2) {
-      const bool two = i + 1 <= j;
+    for (int i = 0; i < nv; i += 2) {
+      const bool two = i + 1 < nv;
       const double2* u0 = a.U + (size_t)i * N;
       const double2* u1 = a.U + (size_t)(i + 1) * N;
       double2 v0[kLsaTE], v1[kLsaTE];
@@ -249,21 +239,32 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
         v1[u] = (two && e < N) ? __ldg(u1 + e) : cmk(0.0, 0.0);
       }
       const double2 c0 = sh_c[i], c1 = two ? sh_c[i + 1] : cmk(0.0, 0.0);
+      const double2 d0 = sh_x[i], d1 = two ? sh_x[i + 1] : cmk(0.0, 0.0);
 #pragma unroll
       for (int u = 0; u < kLsaTE; ++u) {
-        wv[u] = csub(wv[u], cmul(c0, v0[u]));
-        if (two) wv[u] = csub(wv[u], cmul(c1, v1[u]));
+        if (upd) {
+          wv[u] = csub(wv[u], cmul(c0, v0[u]));
+          if (two) wv[u] = csub(wv[u], cmul(c1, v1[u]));
+        }
+        if (iter) {
+          xv[u] = cfma(d0, v0[u], xv[u]);
+          if (two) xv[u] = cfma(d1, v1[u], xv[u]);
+        }
       }
     }
 #pragma unroll
     for (int u = 0; u < kLsaTE; ++u) {
       const size_t e = t0 + (size_t)u * kLsaBD + threadIdx.x;
       if (e < N) {
-        un[e] = wv[u];
-        nrm += cnorm2(wv[u]);
+        if (upd) {
+          un[e] = wv[u];
+          nrm += cnorm2(wv[u]);
+        }
+        if (iter) a.x[e] = xv[u];
       }
     }
   }
+  if (!upd) return;
   // CTA partial of ||u_{j+1}||^2
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nrm += __shfl_down_sync(0xffffffffu, nrm, o);

@@ -938,7 +938,9 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
   if (maxit != c->lsa_maxit && maxit + 1 <= kLsaMaxJ) {
     int sms = 0, per = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lsa_dots, kLsaBD, 0));
+    CK(cudaFuncSetAttribute(k_lsa_dots, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(lsa_dots_smem())));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lsa_dots, kLsaBD, lsa_dots_smem()));
     int per2 = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_lsa_update, kLsaBD, 0));
     per = std::max(1, std::min(per, per2));
@@ -1053,11 +1055,11 @@ static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
   LsaArgs a = lsa_args(c, c->x, 0, 0, maxit);
   a.dj = dj;
   a.done = &c->loop_state->done;
-  k_lsa_dots<<<G, kLsaBD, 0, c->st>>>(a);
+  k_lsa_dots<<<G, kLsaBD, lsa_dots_smem(), c->st>>>(a);
+  k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a);  // u_{j+1} and the lagged x_{j-1}
   monitor_raw(c, c->x);
   k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres);
   k_loop_check<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, c->res_hist, tol, h);
-  k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a);
   k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a, G);
   k_loop_next<<<1, 1, 0, c->st>>>(c->loop_state, maxit, h);
   cudaGraph_t captured = nullptr;
@@ -1171,7 +1173,7 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
       for (int q = 0; q < (ls.need_tail ? maxit - 1 : it); ++q) res.residuals.push_back(c->res_host[q]);
       if (ls.need_tail) {  // x_{maxit-1}: iterate-only pass + monitor
         LsaArgs b = lsa_args(c, c->x, maxit - 1, 1, maxit);
-        HD_LAUNCH(HD_K_ITERATE, (maxit + 2.0) * P, k_lsa_dots<<<G, kLsaBD, 0, c->st>>>(b));
+        HD_LAUNCH(HD_K_ITERATE, (maxit + 2.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(b));
         monitor(c->x);
         read_scalars(c);
         res.residuals.push_back(c->hres[0]);
@@ -1201,7 +1203,9 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
       };
       compose_op(c, c->V + static_cast<size_t>(j) * N, c->w);
       LsaArgs a = lsa_args(c, xout, j, 0, maxit);
-      HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 4.0 : 2.0) * P, k_lsa_dots<<<G, kLsaBD, 0, c->st>>>(a));
+      // pass 1 reads w, u_j, u_0..u_j; pass 2 reads w, u_0..u_j (+ x0 for j >= 1), writes u_{j+1} (+ x)
+      HD_LAUNCH(HD_K_MGS, (j + 3.0) * P, k_lsa_dots<<<G, kLsaBD, lsa_dots_smem(), c->st>>>(a));
+      HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 5.0 : 3.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a));
       if (j >= 1) {  // x_{j-1} is ready: monitor it (the reference's iteration j-1)
         monitor(xout);
         read_scalars(c);
@@ -1220,14 +1224,13 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
           break;
         }
       }
-      HD_LAUNCH(HD_K_MGS, (j + 3.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a));
       HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a, G));
       CK(cudaMemcpyAsync(c->hres + 1, c->dres + 1, sizeof(double), cudaMemcpyDeviceToHost, c->st));
       // hnew of this iteration is needed one iteration later (read with the next sync)
       if (j + 1 == maxit) {
         // budget exhausted: x_{maxit-1} by an iterate-only pass, then its monitor
         LsaArgs b = lsa_args(c, xout, j, 1, maxit);
-        HD_LAUNCH(HD_K_ITERATE, (j + 3.0) * P, k_lsa_dots<<<G, kLsaBD, 0, c->st>>>(b));
+        HD_LAUNCH(HD_K_ITERATE, (j + 3.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(b));
         monitor(xout);
         read_scalars(c);
         const double rr = c->hres[0];
