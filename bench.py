@@ -50,6 +50,21 @@ def dist_env():
     return ws, rank, local
 
 
+def rank_reduce(dist, t_ms, work, device="cpu"):
+    """Whole-job timing over ranks: the MAX of the per-rank timed regions and
+    the SUM of the work units (bench contract).  Any backend (nccl on the GPU
+    box, gloo in tests/test_multirank.py)."""
+    if dist is None:
+        return float(t_ms), float(work)
+    import torch
+    tt = torch.tensor([float(t_ms), float(work)], dtype=torch.float64, device=device)
+    mx = tt.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = tt.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return float(mx[0]), float(sm[1])
+
+
 def workload_name(cfg):
     dim, p, ne, k = CONFIGS[cfg]
     return f"{cfg}: {dim}D IgA Helmholtz point source, k={k:g}, p={p}, {ne}^{dim} elements, DC_MG^1 (beta2=0.5, omega=2/3, nu=1), GMRES tol 1e-7"
@@ -238,15 +253,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     prof = solver.profile_read()
     solver.profile(False)
-    if dist:
-        tt = torch.tensor([t_ms, float(iters)], dtype=torch.float64, device=dev)
-        mx = tt.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = tt.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        t_max, iters_all = float(mx[0]), float(sm[1])
-    else:
-        t_max, iters_all = t_ms, float(iters)
+    t_max, iters_all = rank_reduce(dist, t_ms, iters, dev)
     value = iters_all / (t_max * 1e-3)
 
     # --- end to end through the public host-buffer API (pinned host memory)
@@ -271,13 +278,7 @@ def run_gpu(args):
         e_iters += rep.iterations
     torch.cuda.synchronize()
     e_ms = float(sum(a.elapsed_time(b) for a, b in e_evs))
-    if dist:
-        tt = torch.tensor([e_ms, float(e_iters)], dtype=torch.float64, device=dev)
-        mx = tt.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = tt.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        e_ms, e_iters = float(mx[0]), float(sm[1])
+    e_ms, e_iters = rank_reduce(dist, e_ms, e_iters, dev)
     e2e = {"value": e_iters / (e_ms * 1e-3), "unit": "iterations/s", "h2d_bytes_per_step": 16 * N,
            "d2h_bytes_per_step": 16 * N + 8 * (r.iterations), "ms_per_step": e_ms / args.steps}
 
