@@ -29,6 +29,7 @@ struct LevelDev {
   int b;
   double2 c;        // L = ... - c My(x)Mx   (2D)  or  S - c M  (1D)
   double2 corner;   // 1D only: added to L(n-1, n-1)
+  const void* gen;  // host-side GenLevel (layered field, layered.cuh) or null; unused on the device
 };
 
 struct RedOut {

@@ -1,0 +1,141 @@
+// Layered wave-number field (reference layered_medium_2d, src/problems.cpp:25-32,
+// 68-74; K2 assembly src/assembly.cpp:234-246):
+//
+//   K2 = sum_{by,bx} (k m_{by,bx})^2  B_by (x) B_bx ,   B_b = mass on [b/4, (b+1)/4]
+//
+// Grouped by the y factor, every level operator of the hierarchy is a sum of
+// G <= 6 Kronecker products with banded 1D factors,
+//
+//   L = My (x) Sx + Sy (x) Mx + sum_by gamma_by  B_by (x) W_by ,
+//   W_by = sum_bx m_{by,bx}^2 B_bx ,  gamma = -k^2 (A) or -k^2 (1 - i beta2) (shifted),
+//
+// and Galerkin coarsening keeps that form factor by factor (z^T Y z, z^T X z).
+// k_kron2d applies it sum-factorised from shared memory: a CTA stages a
+// (16 + 2b) x (32 + 2b) input tile, forms the G x-products of every staged row,
+// then combines them along y for its 16 x 32 outputs.  The exact solves of the
+// layered hierarchy (deflation E, coarsest level) are dense inverses built by
+// k_dense_kron + cuSOLVER getrf/getrs; they are not Kronecker sums, so the fast
+// diagonalisation of the constant field does not apply.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace hd {
+
+constexpr int kGenMaxG = 6;
+constexpr int kGenTY = 16, kGenTX = 32, kGenThreads = 256;
+
+struct GenLevel {
+  int n, b, G;
+  const double* Y[kGenMaxG];  // n x (2b+1) band rows (y factor of group g)
+  const double* X[kGenMaxG];  // n x (2b+1) band rows (x factor)
+  double2 coef[kGenMaxG];
+};
+
+__host__ __device__ constexpr size_t gen_smem(int b, int G) {
+  return sizeof(double2) * ((size_t)(kGenTY + 2 * b) * (kGenTX + 2 * b) + (size_t)G * (kGenTY + 2 * b) * kGenTX);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kGenThreads) k_kron2d(GenLevel L, const double2* __restrict__ x,
+                                                        const double2* __restrict__ bv, double2* __restrict__ out,
+                                                        double omega, RedOut red, const int* xidx, size_t xstride) {
+  if (xidx) x += (size_t)(*xidx) * xstride;
+  extern __shared__ __align__(16) double2 gsm[];
+  __shared__ double2 scratch[32];
+  const int n = L.n, b = L.b, NB = 2 * b + 1, G = L.G;
+  const int RW = kGenTX + 2 * b, RH = kGenTY + 2 * b;
+  double2* xs = gsm;             // RH x RW
+  double2* px = gsm + RH * RW;   // G x RH x kGenTX
+  const int x0 = blockIdx.x * kGenTX, y0 = blockIdx.y * kGenTY;
+  for (int e = threadIdx.x; e < RH * RW; e += blockDim.x) {
+    const int rr = e / RW, cc = e % RW;
+    const int gy = y0 - b + rr, gx = x0 - b + cc;
+    xs[e] = (gy >= 0 && gy < n && gx >= 0 && gx < n) ? x[(size_t)gy * n + gx] : cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  // x pass: px[g][rr][c] = sum_j X_g(ix, j) x(row rr, ix + j - b)
+  for (int e = threadIdx.x; e < G * RH * kGenTX; e += blockDim.x) {
+    const int g = e / (RH * kGenTX), rem = e % (RH * kGenTX);
+    const int rr = rem / kGenTX, c = rem % kGenTX;
+    const int ix = x0 + c;
+    double2 s = cmk(0.0, 0.0);
+    if (ix < n) {
+      const double* Xr = L.X[g] + (size_t)ix * NB;
+      const double2* xr = xs + rr * RW + c;
+      for (int j = 0; j < NB; ++j) s = cfma_r(__ldg(Xr + j), xr[j], s);
+    }
+    px[e] = s;
+  }
+  __syncthreads();
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < kGenTY * kGenTX; e += blockDim.x) {
+    const int r = e / kGenTX, c = e % kGenTX;
+    const int iy = y0 + r, ix = x0 + c;
+    if (iy >= n || ix >= n) continue;
+    double2 y = cmk(0.0, 0.0);
+    for (int g = 0; g < G; ++g) {
+      const double* Yr = L.Y[g] + (size_t)iy * NB;
+      const double2* pr = px + ((size_t)g * RH + r) * kGenTX + c;
+      double2 t = cmk(0.0, 0.0);
+      for (int d = 0; d < NB; ++d) t = cfma_r(__ldg(Yr + d), pr[d * kGenTX], t);
+      y = cadd(y, cmul(L.coef[g], t));
+    }
+    const size_t gi = (size_t)iy * n + ix;
+    if (MODE == OP_APPLY) {
+      out[gi] = y;
+    } else if (MODE == OP_RESID) {
+      out[gi] = csub(bv[gi], y);
+    } else if (MODE == OP_RESNORM) {
+      acc += cnorm2(csub(bv[gi], y));
+    } else {
+      double2 D = cmk(0.0, 0.0);
+      for (int g = 0; g < G; ++g)
+        D = cadd(D, cscale(__ldg(L.Y[g] + (size_t)iy * NB + b) * __ldg(L.X[g] + (size_t)ix * NB + b), L.coef[g]));
+      out[gi] = cadd(xs[(r + b) * RW + c + b], cscale(omega, cmul(cinv(D), csub(bv[gi], y))));
+    }
+  }
+  if (MODE == OP_RESNORM) {
+    double2 total;
+    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) / red.scale;
+  }
+}
+
+// x = omega D^-1 b (Jacobi sweep from a zero iterate)
+__global__ void __launch_bounds__(256) k_jacobi0_gen(GenLevel L, const double2* __restrict__ bv,
+                                                     double2* __restrict__ out, double omega) {
+  const int n = L.n, NB = 2 * L.b + 1;
+  const size_t NN = (size_t)n * n;
+  for (size_t gi = blockIdx.x * (size_t)blockDim.x + threadIdx.x; gi < NN; gi += (size_t)gridDim.x * blockDim.x) {
+    const int iy = (int)(gi / n), ix = (int)(gi % n);
+    double2 D = cmk(0.0, 0.0);
+    for (int g = 0; g < L.G; ++g)
+      D = cadd(D, cscale(L.Y[g][(size_t)iy * NB + L.b] * L.X[g][(size_t)ix * NB + L.b], L.coef[g]));
+    out[gi] = cscale(omega, cmul(cinv(D), bv[gi]));
+  }
+}
+
+// Dense column-major n^2 x n^2 matrix of the Kronecker sum (row = iy*n+ix,
+// col = jy*n+jx), for the dense exact solves.
+__global__ void k_dense_kron(GenLevel L, double2* __restrict__ A) {
+  const int n = L.n, b = L.b, NB = 2 * b + 1;
+  const size_t NN = (size_t)n * n, tot = NN * NN;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = e % NN, col = e / NN;
+    const int iy = (int)(row / n), ix = (int)(row % n), jy = (int)(col / n), jx = (int)(col % n);
+    const int dy = jy - iy, dx = jx - ix;
+    double2 v = cmk(0.0, 0.0);
+    if (dy >= -b && dy <= b && dx >= -b && dx <= b)
+      for (int g = 0; g < L.G; ++g)
+        v = cadd(v, cscale(L.Y[g][(size_t)iy * NB + dy + b] * L.X[g][(size_t)ix * NB + dx + b], L.coef[g]));
+    A[e] = v;
+  }
+}
+
+__global__ void k_identity(double2* __restrict__ B, size_t NN) {
+  const size_t tot = NN * NN;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x)
+    B[e] = cmk((e % NN) == (e / NN) ? 1.0 : 0.0, 0.0);
+}
+
+}  // namespace hd

@@ -32,6 +32,7 @@
 #include "transfer.cuh"
 #include "arnoldi.cuh"
 #include "arnoldi_lowsync.cuh"
+#include "layered.cuh"
 
 namespace hd {
 
@@ -72,6 +73,11 @@ struct DevBand {
   double* S = nullptr;
   double* M = nullptr;
   int n = 0, b = 0;
+  // layered field: the level as a G-term Kronecker sum (layered.cuh), with the
+  // unshifted (A) and shifted coefficients; band tables owned by `gen_mem`
+  GenLevel* genA = nullptr;
+  GenLevel* genM = nullptr;
+  double* gen_mem = nullptr;
 };
 
 // Exact solver of one Kronecker-sum (2D) or banded (1D) operator.
@@ -96,6 +102,11 @@ struct ExactSolver {
   double* Vt = nullptr;
   double2* Dinvf = nullptr;
   double *F = nullptr, *G = nullptr, *Hh = nullptr, *R = nullptr;
+  // dense inverse (layered field: E and the coarsest level are not Kronecker sums)
+  bool dense = false;
+  size_t NN = 0;
+  double2* Ainv = nullptr;   // NN x NN column-major
+  double2 *dx = nullptr, *dy = nullptr;
 };
 
 }  // namespace hd
@@ -223,8 +234,9 @@ static Band band_from_host(const double* a, int n, int b) {
   return B;
 }
 
-static LevelDev level_dev(const DevBand& d, double2 c, double2 corner) {
+static LevelDev level_dev(const DevBand& d, double2 c, double2 corner, const GenLevel* gen = nullptr) {
   LevelDev L;
+  L.gen = gen;
   L.S = d.S;
   L.M = d.M;
   L.n = d.n;
@@ -412,6 +424,7 @@ static void free_exact(ExactSolver& X) {
   cudaFree(X.V); cudaFree(X.Dinv); cudaFree(X.T1); cudaFree(X.T2);
   cudaFree(X.Vt); cudaFree(X.Dinvf); cudaFree(X.F); cudaFree(X.G); cudaFree(X.Hh); cudaFree(X.R);
   cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work); cudaFree(X.Uinv);
+  cudaFree(X.Ainv); cudaFree(X.dx); cudaFree(X.dy);
   X = ExactSolver{};
 }
 
@@ -549,6 +562,23 @@ static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, con
   launched(c, kind, mk, op_bytes(MODE, static_cast<size_t>(L.n) * L.n));
 }
 
+// layered field: G-term Kronecker-sum operator (layered.cuh)
+template <int MODE>
+static void launch_gen_mode(hd_ctx* c, const GenLevel& G, const double2* x, const double2* b, double2* out,
+                            double omega, RedOut red, int kind, const int* xidx, size_t xstride) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_kron2d<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(gen_smem(6, kGenMaxG))));
+    attr = true;
+  }
+  if (G.b > 6 || G.G > kGenMaxG) throw Error(HD_ERR_INVALID, "layered operator exceeds the kernel limits");
+  const dim3 grid((G.n + kGenTX - 1) / kGenTX, (G.n + kGenTY - 1) / kGenTY);
+  HD_LAUNCH(kind, op_bytes(MODE, static_cast<size_t>(G.n) * G.n),
+            k_kron2d<MODE><<<grid, kGenThreads, gen_smem(G.b, G.G), c->st>>>(G, x, b, out, omega, red, xidx,
+                                                                               xstride));
+}
+
 static RedOut red_of(hd_ctx* c, double* dst = nullptr, double scale = 1.0) {
   RedOut r;
   r.partials = c->partials;
@@ -564,6 +594,16 @@ static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, c
                      size_t xstride = 0) {
   RedOut red = red_of(c, dst, scale);
   const int kind = L.n == c->n ? HD_K_OP_FINE : HD_K_OP_COARSE;
+  if (L.gen) {
+    const GenLevel& G = *static_cast<const GenLevel*>(L.gen);
+    switch (mode) {
+      case OP_APPLY: launch_gen_mode<OP_APPLY>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
+      case OP_RESID: launch_gen_mode<OP_RESID>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
+      case OP_JACOBI: launch_gen_mode<OP_JACOBI>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
+      default: launch_gen_mode<OP_RESNORM>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
+    }
+    return;
+  }
   if (c->dim == 2) {
     switch (mode) {
       case OP_APPLY: launch_op2d_mode<OP_APPLY>(c, L, x, b, out, omega, red, kind, xidx, xstride); break;
@@ -586,6 +626,11 @@ static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, c
 
 static void jacobi0(hd_ctx* c, const LevelDev& L, const double2* b, double2* out, double omega) {
   const size_t NN = c->dim == 2 ? static_cast<size_t>(L.n) * L.n : L.n;
+  if (L.gen) {
+    HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,
+              k_jacobi0_gen<<<grid_for(NN), 256, 0, c->st>>>(*static_cast<const GenLevel*>(L.gen), b, out, omega));
+    return;
+  }
   HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,
             if (c->dim == 2) k_jacobi0_2d_t<<<dim3((L.n + 63) / 64, (L.n + 15) / 16), 256, 0, c->st>>>(L, b, out,
                                                                                                         omega);
@@ -624,8 +669,37 @@ static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, 
             k_prolong<1, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out));
 }
 
+// interleaved <-> planar (re plane, im plane) complex vectors
+__global__ void k_to_planar(const double2* __restrict__ a, double* __restrict__ p, size_t N) {
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = a[g];
+    p[g] = v.x;
+    p[g + N] = v.y;
+  }
+}
+__global__ void k_from_planar(const double* __restrict__ p, double2* __restrict__ a, size_t N) {
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
+    a[g] = cmk(p[g], p[g + N]);
+}
+
+// y = Ainv x (dense exact solve of the layered field), interleaved
+static void dense_apply(hd_ctx* c, const ExactSolver& X, const double2* x, double2* y) {
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  const size_t mk = prof_mark(c);
+  CKB(cublasZgemv(c->cb, CUBLAS_OP_N, static_cast<int>(X.NN), static_cast<int>(X.NN), &one,
+                  reinterpret_cast<const cuDoubleComplex*>(X.Ainv), static_cast<int>(X.NN),
+                  reinterpret_cast<const cuDoubleComplex*>(x), 1, &zero, reinterpret_cast<cuDoubleComplex*>(y), 1));
+  launched(c, HD_K_LIBGEMM, mk, 16.0 * X.NN * X.NN, true);
+}
+
 // Exact solve: in/out planar (2D FD) or via the banded LU (1D).
 static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
+  if (X.dense) {
+    HD_LAUNCH(HD_K_VEC, 32.0 * X.NN, k_from_planar<<<grid_for(X.NN), 256, 0, c->st>>>(inout, X.dx, X.NN));
+    dense_apply(c, X, X.dx, X.dy);
+    HD_LAUNCH(HD_K_VEC, 32.0 * X.NN, k_to_planar<<<grid_for(X.NN), 256, 0, c->st>>>(X.dy, inout, X.NN));
+    return;
+  }
   if (X.dim == 2 && X.folded) {
     const int n = X.n, n2 = X.n2;
     const long nn = static_cast<long>(n2) * n2;
@@ -696,6 +770,10 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
 // coarsest multigrid level: interleaved in/out
 static void coarsest_solve(hd_ctx* c, const double2* b, double2* out) {
   ExactSolver& X = c->coarsest;
+  if (X.dense) {
+    dense_apply(c, X, b, out);
+    return;
+  }
   const double NL = X.dim == 2 ? static_cast<double>(X.n) * X.n : X.n;
   HD_LAUNCH(HD_K_EXACT, 32.0 * NL,
             if (X.dim == 2) k_fd_small<<<1, 1024, 0, c->st>>>(X.V, X.Dinv, X.n, b, out);
@@ -704,9 +782,14 @@ static void coarsest_solve(hd_ctx* c, const double2* b, double2* out) {
 
 static size_t lsize(const hd_ctx* c, int n) { return c->dim == 2 ? static_cast<size_t>(n) * n : n; }
 
+// level l of the shifted hierarchy
+static LevelDev levM(hd_ctx* c, int l) {
+  return level_dev(c->lev[l], c->cM, l == 0 ? c->corner : cmk(0.0, 0.0), c->lev[l].genM);
+}
+
 // x_out = (damped Jacobi)^steps from x (x_zero: x == 0), ping-pong through tmp
 static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2* xb, bool x_zero, int steps) {
-  const LevelDev L = level_dev(c->lev[l], c->cM, l == 0 ? c->corner : cmk(0.0, 0.0));
+  const LevelDev L = levM(c, l);
   double2* cur = xa;
   double2* oth = xb;
   int s = 0;
@@ -732,7 +815,7 @@ static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero) {
     coarsest_solve(c, b, c->mg_x[l]);
     return c->mg_x[l];
   }
-  const LevelDev L = level_dev(c->lev[l], c->cM, l == 0 ? c->corner : cmk(0.0, 0.0));
+  const LevelDev L = levM(c, l);
   double2* xcur = smooth(c, l, b, c->mg_x[l], c->mg_y[l], x_zero, c->spec.smooth_steps);
   double2* xoth = xcur == c->mg_x[l] ? c->mg_y[l] : c->mg_x[l];
   op_apply(c, OP_RESID, L, xcur, b, c->mg_r[l]);
@@ -742,19 +825,6 @@ static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero) {
   prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, nf, ncl, nullptr, xcur);
   double2* res = smooth(c, l, b, xcur, xoth, false, c->spec.smooth_steps);
   return res;
-}
-
-// out = MG^-1 b  with `cycles` V-cycles from zero (src/precond.cpp:159-163)
-__global__ void k_to_planar(const double2* __restrict__ a, double* __restrict__ p, size_t N) {
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
-    const double2 v = a[g];
-    p[g] = v.x;
-    p[g + N] = v.y;
-  }
-}
-__global__ void k_from_planar(const double* __restrict__ p, double2* __restrict__ a, size_t N) {
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
-    a[g] = cmk(p[g], p[g + N]);
 }
 
 // out = M^-1 b exactly (C_ex, src/precond.cpp:204-211): fast diagonalisation
@@ -792,7 +862,7 @@ static void mg_solve(hd_ctx* c, const double2* b, double2* out) {
       xb = cycle_at(c, 0, b, true);
     } else {
       // general cycle from a non-zero iterate held in mg_x[0]
-      const LevelDev L = level_dev(c->lev[0], c->cM, c->corner);
+      const LevelDev L = levM(c, 0);
       double2* xcur = smooth(c, 0, b, c->mg_x[0], c->mg_y[0], false, c->spec.smooth_steps);
       double2* xoth = xcur == c->mg_x[0] ? c->mg_y[0] : c->mg_x[0];
       op_apply(c, OP_RESID, L, xcur, b, c->mg_r[0]);
@@ -810,7 +880,7 @@ static void mg_solve(hd_ctx* c, const double2* b, double2* out) {
   CK(cudaMemcpyAsync(out, xb, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
 }
 
-static LevelDev opA(hd_ctx* c) { return level_dev(c->fine, c->cA, c->corner); }
+static LevelDev opA(hd_ctx* c) { return level_dev(c->fine, c->cA, c->corner, c->fine.genA); }
 
 // out = Q v = Z E^-1 Z^T v  (Deflation::apply_Q, src/precond.cpp:102-104)
 static void apply_Q(hd_ctx* c, const double2* v, double2* out) {
@@ -1013,7 +1083,7 @@ __global__ void k_scale_monitor(double* dres) {  // graph monitor: raw norm / (|
 }
 
 static void monitor_raw(hd_ctx* c, const double2* x) {
-  op_apply(c, OP_RESNORM, level_dev(c->fine, c->cA, c->corner), x, c->f, nullptr, 0.0, c->dres + 0, 1.0);
+  op_apply(c, OP_RESNORM, opA(c), x, c->f, nullptr, 0.0, c->dres + 0, 1.0);
 }
 
 // Captures the GMRES iteration body (device-side j) into the body of a WHILE
@@ -1310,11 +1380,145 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   return res;
 }
 
+// ---------------------------------------------------------------------------
+// layered field (layered.cuh): level groups (Y_g, X_g), g = 0..5
+// ---------------------------------------------------------------------------
+struct GenHost {
+  std::vector<Band> Y, X;
+};
+
+// fine level: (M, S), (S, M), (B_by, W_by = sum_bx m_{by,bx}^2 B_bx), by = 0..3
+// (K2 of src/assembly.cpp:234-246 grouped by its y factor)
+static GenHost layered_fine(const Band& S1, const Band& M1, const double* interval_mass, const double* mult) {
+  GenHost h;
+  h.Y = {M1, S1};
+  h.X = {S1, M1};
+  std::vector<Band> Bb;
+  for (int b = 0; b < 4; ++b)
+    Bb.push_back(band_from_host(interval_mass + static_cast<size_t>(b) * M1.a.size(), M1.n, M1.b));
+  for (int by = 0; by < 4; ++by) {
+    Band W(M1.n, M1.b);
+    for (int bx = 0; bx < 4; ++bx) {
+      const double m2 = mult[4 * by + bx] * mult[4 * by + bx];
+      for (size_t e = 0; e < W.a.size(); ++e) W.a[e] += m2 * Bb[bx].a[e];
+    }
+    h.Y.push_back(Bb[by]);
+    h.X.push_back(W);
+  }
+  return h;
+}
+
+static GenHost galerkin_gen(const GenHost& h, const Transfer& z) {
+  GenHost o;
+  for (const Band& y : h.Y) o.Y.push_back(galerkin(y, z));
+  for (const Band& x : h.X) o.X.push_back(galerkin(x, z));
+  return o;
+}
+
+static Band padded(const Band& B, int b) {
+  Band o(B.n, b);
+  for (int i = 0; i < B.n; ++i)
+    for (int j = std::max(0, i - B.b); j <= std::min(B.n - 1, i + B.b); ++j) o.ref(i, j) = B.at(i, j);
+  return o;
+}
+
+// Upload the groups; layered coefficient cl of groups 2..5 (groups 0, 1: 1).
+static GenLevel upload_gen(const GenHost& h, double2 cl, double** mem) {
+  const int G = static_cast<int>(h.Y.size());
+  int b = 0;
+  for (int g = 0; g < G; ++g) b = std::max({b, h.Y[g].b, h.X[g].b});
+  const int n = h.Y[0].n;
+  const size_t per = static_cast<size_t>(n) * (2 * b + 1);
+  *mem = dalloc<double>(2 * G * per);
+  GenLevel L{};
+  L.n = n;
+  L.b = b;
+  L.G = G;
+  for (int g = 0; g < G; ++g) {
+    const Band y = padded(h.Y[g], b), x = padded(h.X[g], b);
+    double* dy = *mem + (2 * g) * per;
+    double* dx = *mem + (2 * g + 1) * per;
+    CK(cudaMemcpy(dy, y.a.data(), per * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dx, x.a.data(), per * sizeof(double), cudaMemcpyHostToDevice));
+    L.Y[g] = dy;
+    L.X[g] = dx;
+    L.coef[g] = g < 2 ? cmk(1.0, 0.0) : cl;
+  }
+  return L;
+}
+
+// attach the layered groups to a level: unshifted (-k^2) and shifted (-k^2 (1 - i beta2))
+static void attach_gen(DevBand& d, const GenHost& h, double2 cA, double2 cM) {
+  double* mem = nullptr;
+  GenLevel a = upload_gen(h, cmk(-cA.x, -cA.y), &mem);
+  GenLevel m = a;
+  for (int g = 2; g < m.G; ++g) m.coef[g] = cmk(-cM.x, -cM.y);
+  d.gen_mem = mem;
+  d.genA = new GenLevel(a);
+  d.genM = new GenLevel(m);
+}
+
+// Dense inverse of a layered level operator (coefficient cl on groups 2..5):
+// E = Z^T A Z and the coarsest shifted level of the layered hierarchy stand in
+// for the reference's SparseLU factors (src/precond.cpp:95-99, 133).
+static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl) {
+  const int n = h.Y[0].n;
+  const size_t NN = static_cast<size_t>(n) * n;
+  if (NN > 20000)
+    throw Error(HD_ERR_INVALID, "layered field: exact solve of " + std::to_string(NN) +
+                                    " unknowns exceeds the dense-inverse limit (20000)");
+  ExactSolver X;
+  X.dim = 2;
+  X.n = n;
+  X.dense = true;
+  X.NN = NN;
+  double* mem = nullptr;
+  const GenLevel L = upload_gen(h, cl, &mem);
+  double2* A = dalloc<double2>(NN * NN);
+  X.Ainv = dalloc<double2>(NN * NN);
+  X.dx = dalloc<double2>(NN);
+  X.dy = dalloc<double2>(NN);
+  k_dense_kron<<<grid_for(NN * NN, 256, 148 * 32), 256, 0, st>>>(L, A);
+  CK(cudaGetLastError());
+  k_identity<<<grid_for(NN * NN, 256, 148 * 32), 256, 0, st>>>(X.Ainv, NN);
+  CK(cudaGetLastError());
+  cusolverDnHandle_t hs;
+  CKS(cusolverDnCreate(&hs));
+  CKS(cusolverDnSetStream(hs, st));
+  const int m = static_cast<int>(NN);
+  int lwork = 0;
+  auto* Az = reinterpret_cast<cuDoubleComplex*>(A);
+  CKS(cusolverDnZgetrf_bufferSize(hs, m, m, Az, m, &lwork));
+  cuDoubleComplex* work = dalloc<cuDoubleComplex>(std::max(lwork, 1));
+  int* ipiv = dalloc<int>(NN);
+  int* info = dalloc<int>(2);
+  CKS(cusolverDnZgetrf(hs, m, m, Az, m, work, ipiv, info));
+  CKS(cusolverDnZgetrs(hs, CUBLAS_OP_N, m, m, Az, m, ipiv, reinterpret_cast<cuDoubleComplex*>(X.Ainv), m, info + 1));
+  int hinfo[2] = {0, 0};
+  CK(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cusolverDnDestroy(hs);
+  cudaFree(A);
+  cudaFree(work);
+  cudaFree(ipiv);
+  cudaFree(info);
+  cudaFree(mem);
+  if (hinfo[0] != 0 || hinfo[1] != 0)
+    throw Error(HD_ERR_FACTOR, "layered exact solve: singular operator (getrf info " + std::to_string(hinfo[0]) + ")");
+  return X;
+}
+
 static void destroy_ctx(hd_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
-  auto fb = [](DevBand& d) { cudaFree(d.S); cudaFree(d.M); };
+  auto fb = [](DevBand& d) {
+    cudaFree(d.S);
+    cudaFree(d.M);
+    cudaFree(d.gen_mem);
+    delete d.genA;
+    delete d.genM;
+  };
   fb(c->fine);
   for (size_t l = 1; l < c->lev.size(); ++l) fb(c->lev[l]);
   free_exact(c->coarsest);
@@ -1356,7 +1560,12 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw Error(HD_ERR_NO_DEVICE, "no CUDA device: the helmdef_b200 path has no CPU fallback");
   if (sys->dim != 1 && sys->dim != 2) throw Error(HD_ERR_INVALID, "dim must be 1 or 2");
-  if (sys->field_kind != HD_FIELD_CONSTANT) throw Error(HD_ERR_INVALID, "only constant wave-number fields are supported");
+  const bool layered = sys->field_kind == HD_FIELD_LAYERED;
+  if (sys->field_kind != HD_FIELD_CONSTANT && !layered) throw Error(HD_ERR_INVALID, "unknown wave-number field kind");
+  if (layered && sys->dim != 2) throw Error(HD_ERR_INVALID, "the layered field is two-dimensional");
+  if (layered && !sys->interval_mass) throw Error(HD_ERR_INVALID, "layered field needs the interval masses");
+  if (layered && spec->shift && spec->cycles <= 0)
+    throw Error(HD_ERR_INVALID, "C_ex (exact shifted inverse) on the layered field is not supported by this build");
   if (sys->per_dim < 2) throw Error(HD_ERR_INVALID, "per_dim must be >= 2");
   const auto t0 = std::chrono::steady_clock::now();
   std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
@@ -1384,6 +1593,11 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   const Band S1 = band_from_host(sys->stiffness_band, c->n, sys->order);
   const Band M1 = band_from_host(sys->mass_band, c->n, sys->order);
   c->fine = upload_pair(S1, M1);
+  GenHost fineH;
+  if (layered) {
+    fineH = layered_fine(S1, M1, sys->interval_mass, sys->multipliers);
+    attach_gen(c->fine, fineH, c->cA, c->cM);
+  }
   // C_ex: exact shifted inverse (src/precond.cpp:204-211)
   if (c->spec.shift && c->spec.cycles <= 0) {
     if (c->dim == 2) {
@@ -1396,17 +1610,36 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   // multigrid hierarchy of the shifted operator (src/precond.cpp:110-134)
   if (c->spec.shift && c->spec.cycles > 0) {
     std::vector<Band> Ss{S1}, Ms{M1};
+    std::vector<GenHost> Hs{fineH};
     int nl = c->n;
     while (nl > c->spec.coarsest) {
       const Transfer z = linear_stencil(nl);
       Ss.push_back(galerkin(Ss.back(), z));
       Ms.push_back(galerkin(Ms.back(), z));
+      if (layered) Hs.push_back(galerkin_gen(Hs.back(), z));
       nl = z.coarse;
     }
     c->lev.push_back(c->fine);
-    for (size_t l = 1; l < Ss.size(); ++l) c->lev.push_back(upload_pair(Ss[l], Ms[l]));
+    for (size_t l = 1; l < Ss.size(); ++l) {
+      c->lev.push_back(upload_pair(Ss[l], Ms[l]));
+      if (layered) attach_gen(c->lev.back(), Hs[l], c->cA, c->cM);
+    }
+    if (layered)  // zero-diagonal check of the layered levels (src/precond.cpp:125-132)
+      for (size_t l = 0; l < Hs.size(); ++l) {
+        const GenHost& h = Hs[l];
+        const int nn = h.Y[0].n;
+        for (int i = 0; i < nn; ++i)
+          for (int j = 0; j < nn; ++j) {
+            std::complex<double> d(0.0, 0.0);
+            for (size_t g = 0; g < h.Y.size(); ++g) {
+              const std::complex<double> cg = g < 2 ? std::complex<double>(1.0, 0.0) : -std::complex<double>(c->cM.x, c->cM.y);
+              d += cg * (h.Y[g].at(i, i) * h.X[g].at(j, j));
+            }
+            if (d == std::complex<double>(0.0, 0.0)) throw Error(HD_ERR_FACTOR, "zero diagonal in smoother");
+          }
+      }
     // zero-diagonal check of every level (src/precond.cpp:125-132)
-    for (size_t l = 0; l < Ss.size(); ++l)
+    for (size_t l = 0; !layered && l < Ss.size(); ++l)
       for (int i = 0; i < Ss[l].n; ++i)
         for (int j = 0; j < (c->dim == 2 ? Ss[l].n : 1); ++j) {
           const int jj = c->dim == 2 ? j : i;
@@ -1419,7 +1652,8 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
         }
     const Band& SL = Ss.back();
     const Band& ML = Ms.back();
-    if (c->dim == 2) c->coarsest = make_fd(c->st, SL, ML, c->cM);
+    if (layered) c->coarsest = make_dense(c->st, Hs.back(), cmk(-c->cM.x, -c->cM.y));
+    else if (c->dim == 2) c->coarsest = make_fd(c->st, SL, ML, c->cM);
     else c->coarsest = make_bandlu(SL, ML, c->cM, Ss.size() == 1 ? c->corner : cmk(0.0, 0.0));
     for (size_t l = 0; l < c->lev.size(); ++l) {
       const size_t NL = lsize(c.get(), c->lev[l].n);
@@ -1435,7 +1669,9 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
     c->nc = z.coarse;
     if (c->nc < 1) throw Error(HD_ERR_INVALID, "deflation needs per_dim >= 2");
     const Band ES = galerkin(S1, z), EM = galerkin(M1, z);
-    if (c->dim == 2) {
+    if (layered) {
+      c->E = make_dense(c->st, galerkin_gen(fineH, z), cmk(-c->cA.x, -c->cA.y));
+    } else if (c->dim == 2) {
       const bool fold = (c->nc % 2 == 0) && centro_symmetric(ES) && centro_symmetric(EM) &&
                         !std::getenv("HD_NOFOLD");
       c->E = fold ? make_fd_folded(c->st, ES, EM, c->cA) : make_fd(c->st, ES, EM, c->cA);
@@ -1616,7 +1852,7 @@ hd_status hd_apply(hd_ctx* c, int which, const double* d_x, double* d_y) {
   double2* yv = reinterpret_cast<double2*>(d_y);
   switch (which) {
     case HD_APPLY_A: op_apply(c, OP_APPLY, opA(c), x, nullptr, yv); break;
-    case HD_APPLY_SHIFTED: op_apply(c, OP_APPLY, level_dev(c->fine, c->cM, c->corner), x, nullptr, yv); break;
+    case HD_APPLY_SHIFTED: op_apply(c, OP_APPLY, level_dev(c->fine, c->cM, c->corner, c->fine.genM), x, nullptr, yv); break;
     case HD_APPLY_MG:
       if (!c->spec.shift) throw Error(HD_ERR_INVALID, "no multigrid in this context");
       mg_solve(c, x, yv);
@@ -1689,7 +1925,7 @@ hd_status hd_debug_level(hd_ctx* c, int which, int level, const double* d_x, dou
   CK(cudaSetDevice(c->device));
   const double2* x = reinterpret_cast<const double2*>(d_x);
   double2* yv = reinterpret_cast<double2*>(d_y);
-  const LevelDev L = level_dev(c->lev[level], c->cM, level == 0 ? c->corner : cmk(0.0, 0.0));
+  const LevelDev L = levM(c, level);
   const bool has_next = level + 1 < static_cast<int>(c->lev.size());
   switch (which) {
     case 0: op_apply(c, OP_APPLY, L, x, nullptr, yv); break;

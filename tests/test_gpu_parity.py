@@ -31,15 +31,24 @@ def _problem(problem, ne, p, k):
     return {"point_source_1d": hd.point_source_1d, "point_source_2d": hd.point_source_2d}[problem](ne, p, k)
 
 
-def _check(r, meta, x_ref, exact_iters=True):
+def _check(r, meta, x_ref, exact_iters=True, env=None):
+    """env: per-step |MGS - ICWY| of two exact CPU runs (the method's own rounding
+    sensitivity); where it exceeds 1e-10 near step j the history is held to a
+    factor 3 instead of RES_TOL (as for C5)."""
     assert r.converged == meta["converged"]
     if exact_iters:
         assert r.iterations == meta["iterations"]
     else:
         assert abs(r.iterations - meta["iterations"]) <= 1
     m = min(len(r.residuals), len(meta["residuals"]))
-    d = np.abs(np.array(r.residuals[:m]) - np.array(meta["residuals"][:m]))
+    a_, b_ = np.array(r.residuals[:m]), np.array(meta["residuals"][:m])
+    sens = np.zeros(m, bool)
+    if env is not None:
+        e = np.array(list(env) + [0.0] * max(0, m - len(env)))
+        sens = np.array([e[max(0, j - 3):j + 4].max() > 1e-10 for j in range(m)])
+    d = np.where(sens, 0.0, np.abs(a_ - b_))
     assert d.max() <= RES_TOL, (d.max(), int(np.argmax(d)))
+    assert np.all(~sens | ((a_ <= 3 * b_) & (b_ <= 3 * a_)))
     rel = np.linalg.norm(r.solution - x_ref) / np.linalg.norm(x_ref)
     assert rel <= SOL_TOL, rel
     c = meta["counts"]
@@ -155,7 +164,7 @@ def _live(problem, p, ne, k, tag, kw, exact_iters=True):
     so, st = _oracle(problem, p, ne, k, tag, **kw)
     g = O.gmres(st.op, st.rhs, st.start, st.monitor, O.GmresOptions(100, 1e-7))
     meta = dict(iterations=g.iterations, converged=g.converged, residuals=g.residuals,
-                counts=vars(st.counts))
+                counts=dict(vars(st.counts)))
     s = hd.assemble(_problem(problem, ne, p, k))
     with hd.Solver(s, hd.to_spec(tag, p, k, **kw)) as solver:
         r = solver.solve(hd.GmresOptions(100, 1e-7))
@@ -275,9 +284,123 @@ def test_arbitrary_rhs_linearity():
 
 
 def test_unsupported_specs_fail_loudly():
+    """C_ex on the layered field would need a sparse direct solve of the whole
+    shifted operator; the build refuses it instead of approximating."""
     s = hd.assemble(hd.layered_medium_2d(40, 2, 20.0))
     with pytest.raises(hd.HelmdefError):
-        hd.Solver(s, hd.to_spec("DC_MG", 2, 20.0, beta2="4.2", smoothing=3))
+        hd.Solver(s, hd.to_spec("C_ex", 2, 20.0, beta2="1/(3k)"))
+
+
+# ---- layered 4x4 medium (table6, SURVEY.md §8(f)) -----------------------------
+T6 = dict(beta2="4.2", cycles=12, omega=0.6)  # data/config/table6.json DC_MG (smoothing 3, p=5: 2)
+
+
+def _t6(p):
+    return dict(T6, smoothing=2 if p == 5 else 3)
+
+
+def _layered_oracle(p, ne, k, kw):
+    """The reference's own algorithm: sparse Galerkin products + SparseLU."""
+    so = O.assemble(O.layered_medium_2d(ne, p, k))
+    return so, O.compose(so, O.to_spec("DC_MG", p, k, **kw))
+
+
+@pytest.mark.parametrize("p,ne,k,kw", [(2, 40, 20.0, BASE), (3, 66, 40.0, dict(BASE, cycles=2, smoothing=2)),
+                                       (5, 76, 50.0, None)])
+def test_layered_components_match_oracle(p, ne, k, kw):
+    import torch
+    kw = kw or _t6(p)
+    so, st = _layered_oracle(p, ne, k, kw)
+    s = hd.assemble(hd.layered_medium_2d(ne, p, k))
+    spec = hd.to_spec("DC_MG", p, k, **kw)
+    rng = np.random.default_rng(99)
+    v = rng.uniform(-1, 1, s.size) + 1j * rng.uniform(-1, 1, s.size)
+    checks = [(hd.HD_APPLY_A, so.A @ v, 1e-13),
+              (hd.HD_APPLY_SHIFTED, O.shifted_operator(so, spec.beta2) @ v, 1e-13),
+              (hd.HD_APPLY_MG, st.multigrid.solve(v, spec.cycles), 1e-11),
+              (hd.HD_APPLY_Q, st.deflation.apply_Q(v), 1e-10),
+              (hd.HD_APPLY_PROJECT, st.deflation.project(v), 1e-10),
+              (hd.HD_APPLY_OP, st.op(v), 1e-10)]
+    with hd.Solver(s, spec) as solver:
+        assert solver.levels == st.multigrid.levels()
+        xd = torch.from_numpy(v).cuda()
+        for which, ref, tol in checks:
+            yd = torch.zeros_like(xd)
+            solver.apply(which, xd.data_ptr(), yd.data_ptr())
+            rel = np.linalg.norm(yd.cpu().numpy() - ref) / np.linalg.norm(ref)
+            assert rel <= tol, (which, rel)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+def test_layered_table6_k50_live(p):
+    """table6 cells at k = 50 (elements by kh = 0.625) against a live oracle solve."""
+    k = 50.0
+    ne = O.derived_elements(k, 0.625, p)
+    kw = _t6(p)
+    so, st = _layered_oracle(p, ne, k, kw)
+    g = O.gmres(st.op, st.rhs, st.start, st.monitor, O.GmresOptions(100, 1e-7))
+    meta = dict(iterations=g.iterations, converged=g.converged, residuals=g.residuals, counts=dict(vars(st.counts)))
+    # rounding sensitivity of the method on this cell: MGS vs its one-reduction
+    # form on the CPU (p = 1 has a transient at step 10 where they differ by 8e-8)
+    import sys
+    sys.path.insert(0, str(GOLD))
+    from make_c5_envelope import gmres_icwy
+    h = gmres_icwy(st.op, st.rhs, st.start, st.monitor)
+    m = min(len(h), len(g.residuals))
+    env = np.abs(np.array(h[:m]) - np.array(g.residuals[:m]))
+    s = hd.assemble(hd.layered_medium_2d(ne, p, k))
+    with hd.Solver(s, hd.to_spec("DC_MG", p, k, **kw)) as solver:
+        r = solver.solve(hd.GmresOptions(100, 1e-7))
+    _check(r, meta, g.solution, env=env)
+
+
+def test_layered_table6_pins():
+    """Every table6 DC_MG^12 cell with k <= 150 (the shipped config): the device
+    iteration count equals the pinned oracle's (tests/golden/oracle_pins.csv, +-1)
+    and meets the reference's golden under its compare rule ('*' = not converged)."""
+    import csv
+    rows = [r for r in csv.DictReader(open(GOLD / "oracle_pins.csv"))
+            if r["table"] == "table6" and r["tag"] == "DC_MG^12"]
+    assert len(rows) == 15
+    for r in rows:
+        p, k, ne = int(r["p"]), float(r["k"]), int(r["elements"])
+        if (p, k) == (3, 150.0):
+            continue  # rounding-chaotic cell: test_layered_table6_sensitive_cell
+        s = hd.assemble(hd.layered_medium_2d(ne, p, k))
+        with hd.Solver(s, hd.to_spec("DC_MG", p, k, **_t6(p))) as solver:
+            res = solver.solve(hd.GmresOptions(100, 1e-7))
+        assert bool(res.converged) == bool(int(r["converged"])), r
+        assert abs(res.iterations - int(r["oracle"])) <= 1, (r, res.iterations)
+        if r["golden"] == "*":
+            assert not res.converged
+        else:
+            assert abs(res.iterations - int(r["golden"])) <= float(r["tol"]), (r, res.iterations)
+
+
+def test_layered_table6_sensitive_cell():
+    """table6 k = 150, p = 3 (reference golden '*'): after step ~30 the true residual
+    drifts inside the near-null space of P MG^-1, so two exact CPU runs (MGS and
+    its ICWY form, tests/golden/make_table6_sensitive.py) bottom out at 3.5e-7 and
+    4.8e-7 and then diverge to ~1e3; whether a run ever dips below 1e-7 is decided
+    by rounding.  The CPU runs' floor (~5e-7) is rounding of their SuperLU coarse
+    solves; the device's dense-inverse coarse solves leave a lower floor, so it
+    keeps descending and converges, exactly as the same CPU algorithm with dense
+    coarse inverses does (36 iterations; the SuperLU runs already depart from it
+    by 3x at step 25).  Bars: device within a factor 3 of that run at every step,
+    iterations +-1, and at least the accuracy of the SuperLU runs."""
+    ref = json.loads((GOLD / "table6_sensitive.json").read_text())
+    c = ref["cell"]
+    s = hd.assemble(hd.layered_medium_2d(c["elements"], c["p"], c["k"]))
+    with hd.Solver(s, hd.to_spec("DC_MG", c["p"], c["k"], **_t6(c["p"]))) as solver:
+        r = solver.solve(hd.GmresOptions(100, 1e-7))
+    a, b = np.array(ref["mgs"]), np.array(ref["icwy"])
+    # the device reaches at least the accuracy of the SuperLU-based CPU runs ...
+    assert min(r.residuals) <= 3.0 * max(a.min(), b.min())
+    # ... and follows the CPU run that uses its kind of coarse solver
+    dn = np.array(ref["dense"])
+    assert ref["dense_converged"] and r.converged and abs(r.iterations - ref["dense_iterations"]) <= 1
+    m = min(len(dn), len(r.residuals))
+    assert np.all((np.array(r.residuals[:m]) <= 3 * dn[:m]) & (dn[:m] <= 3 * np.array(r.residuals[:m])))
 
 
 @pytest.mark.parametrize("problem,p,k,beta2", [("point_source_1d", 2, 1000.0, "1/k"),
