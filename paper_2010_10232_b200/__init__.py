@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -30,7 +31,8 @@ from typing import List, Optional
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libhelmdef_b200.so"
+# HD_LIBRARY: alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ["HD_LIBRARY"]) if os.environ.get("HD_LIBRARY") else _PKG / "libhelmdef_b200.so"
 
 HD_FIELD_CONSTANT = 0
 HD_FIELD_LAYERED = 1
