@@ -50,6 +50,8 @@ struct LsaArgs {
   unsigned* counter;  // last-block ticket, zero between launches
   const int* done;    // early exit (speculative graph iterations); may be null
   const int* dj;      // device-side iteration index (graph mode); overrides j when set
+  int jlag;           // Givens only: work on iteration (j - jlag) (graph mode: the previous
+                      // iteration's Givens overlaps this iteration's operator)
 };
 
 __device__ __forceinline__ double2 lsa_warp_sum(double2 v) {
@@ -286,7 +288,8 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_givens(LsaArgs a, int nparts) {
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double s_hnew;
   if (a.done && *((volatile const int*)a.done)) return;
-  const int j = a.dj ? *a.dj : a.j;
+  const int j = (a.dj ? *a.dj : a.j) - a.jlag;
+  if (j < 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp == 0) {
     double s = 0.0;

@@ -195,6 +195,8 @@ struct hd_ctx {
   std::vector<ProfRec> prof_recs;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t own_st = nullptr;  // the context's own stream while an external one is set
+  cudaStream_t st2 = nullptr;     // side branch of the graph body (Givens of the previous iteration)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace hd {
@@ -1036,6 +1038,7 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
 
 static LsaArgs lsa_args(hd_ctx* c, double2* xout, int j, int mode, int maxit) {
   LsaArgs a;
+  a.jlag = 0;
   a.U = c->V;
   a.Uw = c->V;
   a.w = c->w;
@@ -1121,16 +1124,29 @@ static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
   CK(cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   const int G = c->lsa_G;
   int* dj = &c->loop_state->j;
-  compose_op(c, c->V, c->w, dj);
   LsaArgs a = lsa_args(c, c->x, 0, 0, maxit);
   a.dj = dj;
   a.done = &c->loop_state->done;
+  // side branch: the Givens rotation + back substitution of iteration j-1
+  // (needed first by pass 2 of iteration j) overlaps the operator of iteration j
+  if (!c->st2) {
+    CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(c->ev_fork, c->st));
+  CK(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+  LsaArgs ag = a;
+  ag.jlag = 1;
+  k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st2>>>(ag, G);
+  CK(cudaEventRecord(c->ev_join, c->st2));
+  compose_op(c, c->V, c->w, dj);
+  CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
   k_lsa_dots<<<G, kLsaBD, lsa_dots_smem(), c->st>>>(a);
   k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a);  // u_{j+1} and the lagged x_{j-1}
   monitor_raw(c, c->x);
   k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres);
   k_loop_check<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, c->res_hist, tol, h);
-  k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a, G);
   k_loop_next<<<1, 1, 0, c->st>>>(c->loop_state, maxit, h);
   cudaGraph_t captured = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(c->st, &captured);
@@ -1241,8 +1257,9 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
       res.iterations = it;
       res.converged = ls.conv != 0;
       for (int q = 0; q < (ls.need_tail ? maxit - 1 : it); ++q) res.residuals.push_back(c->res_host[q]);
-      if (ls.need_tail) {  // x_{maxit-1}: iterate-only pass + monitor
+      if (ls.need_tail) {  // x_{maxit-1}: its Givens, an iterate-only pass + monitor
         LsaArgs b = lsa_args(c, c->x, maxit - 1, 1, maxit);
+        HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(b, G));
         HD_LAUNCH(HD_K_ITERATE, (maxit + 2.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(b));
         monitor(c->x);
         read_scalars(c);
@@ -1550,6 +1567,9 @@ static void destroy_ctx(hd_ctx* c) {
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   cudaStream_t mine = c->own_st ? c->own_st : c->st;
   if (mine) cudaStreamDestroy(mine);
+  if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
 }
 
