@@ -33,6 +33,7 @@
 #include "arnoldi.cuh"
 #include "arnoldi_lowsync.cuh"
 #include "layered.cuh"
+#include "segsolve.cuh"
 
 namespace hd {
 
@@ -95,6 +96,8 @@ struct ExactSolver {
   int* piv = nullptr;
   double2* work = nullptr;
   double2* Uinv = nullptr;   // 1 / U(k, k)
+  // segmented sweeps (segsolve.cuh); seg.P == 0: single-lane staged kernel
+  SegArgs seg{};
   // reflection-folded fast diagonalisation (centro-symmetric E, even n):
   // Vt = [Vs_top | Va_top] (2 x n2 x n2), Dinvf in [y parity][x parity][ky][kx]
   bool folded = false;
@@ -401,6 +404,67 @@ static ExactSolver make_fd(cudaStream_t st, const Band& S, const Band& M, double
   return X;
 }
 
+// Influence rows and window transfers of the segmented sweeps (segsolve.cuh),
+// by running each segment's recurrences on unit boundary values.
+static void make_segments(ExactSolver& X, const BandLU& f) {
+  const int n = f.n, kl = f.kl, ku = f.ku, W = kl + 1;
+  const int Ls = 32;
+  const int P = n / Ls;
+  if (P < 2 || ku != 2 * kl || Ls < ku) return;
+  std::vector<cplx> hf(static_cast<size_t>(n) * W), Ff(static_cast<size_t>(P) * W * W), hb(static_cast<size_t>(n) * ku);
+  for (int i = 0; i < P; ++i) {
+    const int s = i * Ls, e = i + 1 == P ? n : (i + 1) * Ls;
+    for (int q = 0; q < W; ++q) {  // forward from window e_q, no rhs
+      std::vector<cplx> w(W, cplx(0.0, 0.0));
+      w[q] = 1.0;
+      for (int k = s; k < e; ++k) {
+        const int p = f.piv[k] - k;
+        if (p != 0) std::swap(w[0], w[p]);
+        const cplx yk = w[0];
+        hf[static_cast<size_t>(k) * W + q] = yk;
+        for (int r = 1; r <= kl; ++r) w[r] -= f.L[static_cast<size_t>(k) * kl + r - 1] * yk;
+        for (int r = 0; r < kl; ++r) w[r] = w[r + 1];
+        w[kl] = 0.0;
+      }
+      for (int r = 0; r < W; ++r) Ff[(static_cast<size_t>(i) * W + r) * W + q] = w[r];
+    }
+    for (int r = 0; r < ku; ++r) {  // backward from future x_{e+r} = 1, no rhs
+      std::vector<cplx> xw(ku, cplx(0.0, 0.0));  // x_{k+1} .. x_{k+ku}
+      xw[r] = 1.0;
+      for (int k = e - 1; k >= s; --k) {
+        cplx acc(0.0, 0.0);
+        for (int d = ku; d >= 1; --d) acc -= f.U[static_cast<size_t>(k) * (ku + 1) + d] * xw[d - 1];
+        const cplx xk = acc / f.U[static_cast<size_t>(k) * (ku + 1)];
+        for (int d = ku - 1; d >= 1; --d) xw[d] = xw[d - 1];
+        xw[0] = xk;
+        hb[static_cast<size_t>(k) * ku + r] = xk;
+      }
+    }
+  }
+  auto up = [](const std::vector<cplx>& v) {
+    double2* d = dalloc<double2>(v.size());
+    CK(cudaMemcpy(d, v.data(), v.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    return d;
+  };
+  SegArgs& a = X.seg;
+  a.n = n;
+  a.P = P;
+  a.Ls = Ls;
+  a.L = X.L;
+  a.U = X.U;
+  a.Uinv = X.Uinv;
+  a.piv = X.piv;
+  a.hf = up(hf);
+  a.Ff = up(Ff);
+  a.hb = up(hb);
+  a.y = dalloc<double2>(n);
+  a.x0 = dalloc<double2>(n);
+  a.D = dalloc<double2>(static_cast<size_t>(P) * W);
+  a.Dl = dalloc<double2>(static_cast<size_t>(P) * W);
+  a.X0 = dalloc<double2>(static_cast<size_t>(P) * ku);
+  a.Xb = dalloc<double2>(static_cast<size_t>(P + 1) * ku);
+}
+
 static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 corner) {
   BandLU f = band_lu(S, M, cplx(c.x, c.y), cplx(corner.x, corner.y));
   ExactSolver X;
@@ -419,6 +483,8 @@ static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 
   CK(cudaMemcpy(X.L, f.L.data(), f.L.size() * sizeof(double2), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(X.U, f.U.data(), f.U.size() * sizeof(double2), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(X.piv, f.piv.data(), f.piv.size() * sizeof(int), cudaMemcpyHostToDevice));
+  const char* e = std::getenv("HD_SEG");
+  if (!(e && std::atoi(e) == 0) && f.kl >= 1 && f.kl <= 6) make_segments(X, f);
   return X;
 }
 
@@ -426,6 +492,11 @@ static void free_exact(ExactSolver& X) {
   cudaFree(X.V); cudaFree(X.Dinv); cudaFree(X.T1); cudaFree(X.T2);
   cudaFree(X.Vt); cudaFree(X.Dinvf); cudaFree(X.F); cudaFree(X.G); cudaFree(X.Hh); cudaFree(X.R);
   cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work); cudaFree(X.Uinv);
+  if (X.seg.P) {
+    cudaFree(const_cast<double2*>(X.seg.hf)); cudaFree(const_cast<double2*>(X.seg.Ff));
+    cudaFree(const_cast<double2*>(X.seg.hb)); cudaFree(X.seg.y); cudaFree(X.seg.x0); cudaFree(X.seg.D);
+    cudaFree(X.seg.Dl); cudaFree(X.seg.X0); cudaFree(X.seg.Xb);
+  }
   cudaFree(X.Ainv); cudaFree(X.dx); cudaFree(X.dy);
   X = ExactSolver{};
 }
@@ -442,10 +513,34 @@ static void bandlu_launch_t(cudaStream_t st, const ExactSolver& X, const double2
   k_bandlu_staged<KL><<<1, 256, sm, st>>>(X.L, X.U, X.Uinv, X.piv, X.n, b, bp, X.work, x, xp);
 }
 
-// 1D exact solve with the staged banded-LU kernel (kl = 1..6), in/out interleaved or planar
+template <int KL>
+static void seg_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b, const double* bp, double2* x,
+                         double* xp) {
+  const SegArgs& a = X.seg;
+  const int blocks = (a.P + 31) / 32;
+  k_seg_fwd<KL><<<blocks, 32, 0, st>>>(a, b, bp);
+  k_seg_scan_fwd<KL><<<1, 32, 0, st>>>(a);
+  k_seg_bwd<KL><<<blocks, 32, 0, st>>>(a);
+  k_seg_scan_bwd<KL><<<1, 32, 0, st>>>(a);
+  k_seg_out<KL><<<std::min((a.n + 255) / 256, 148 * 4), 256, 0, st>>>(a, x, xp);
+}
+
+// 1D exact solve (kl = 1..6), in/out interleaved or planar: segmented sweeps,
+// or the single-lane staged kernel for short systems
 static void bandlu_launch(cudaStream_t st, const ExactSolver& X, const double2* b, const double* bp, double2* x,
                           double* xp) {
   if (X.ku != 2 * X.kl) throw Error(HD_ERR_INVALID, "banded LU layout mismatch");
+  if (X.seg.P) {
+    switch (X.kl) {
+      case 1: seg_launch_t<1>(st, X, b, bp, x, xp); break;
+      case 2: seg_launch_t<2>(st, X, b, bp, x, xp); break;
+      case 3: seg_launch_t<3>(st, X, b, bp, x, xp); break;
+      case 4: seg_launch_t<4>(st, X, b, bp, x, xp); break;
+      case 5: seg_launch_t<5>(st, X, b, bp, x, xp); break;
+      default: seg_launch_t<6>(st, X, b, bp, x, xp); break;
+    }
+    return;
+  }
   switch (X.kl) {
     case 1: bandlu_launch_t<1>(st, X, b, bp, x, xp); break;
     case 2: bandlu_launch_t<2>(st, X, b, bp, x, xp); break;
@@ -766,6 +861,7 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
   } else {
     HD_LAUNCH(HD_K_EXACT, 32.0 * X.n,
               bandlu_launch(c->st, X, nullptr, inout, nullptr, inout));
+    if (X.seg.P) c->launches += 4;  // segmented sweeps: 5 kernels
   }
 }
 
@@ -780,6 +876,7 @@ static void coarsest_solve(hd_ctx* c, const double2* b, double2* out) {
   HD_LAUNCH(HD_K_EXACT, 32.0 * NL,
             if (X.dim == 2) k_fd_small<<<1, 1024, 0, c->st>>>(X.V, X.Dinv, X.n, b, out);
             else bandlu_launch(c->st, X, b, nullptr, out, nullptr));
+  if (X.dim != 2 && X.seg.P) c->launches += 4;
 }
 
 static size_t lsize(const hd_ctx* c, int n) { return c->dim == 2 ? static_cast<size_t>(n) * n : n; }
@@ -841,6 +938,7 @@ static void shift_exact_solve(hd_ctx* c, const double2* b, double2* out) {
   } else {
     HD_LAUNCH(HD_K_EXACT, 32.0 * X.n,
               bandlu_launch(c->st, X, b, nullptr, out, nullptr));
+    if (X.seg.P) c->launches += 4;
   }
 }
 
