@@ -405,24 +405,38 @@ static ExactSolver make_fd(cudaStream_t st, const Band& S, const Band& M, double
 }
 
 // Influence rows and window transfers of the segmented sweeps (segsolve.cuh),
-// by running each segment's recurrences on unit boundary values.
+// by running each segment's recurrences on unit boundary values; all per-row
+// tables in the [row-in-segment][field][segment] layout, rows past n = identity.
 static void make_segments(ExactSolver& X, const BandLU& f) {
-  const int n = f.n, kl = f.kl, ku = f.ku, W = kl + 1;
-  const int Ls = 32;
-  const int P = n / Ls;
-  if (P < 2 || ku != 2 * kl || Ls < ku) return;
-  std::vector<cplx> hf(static_cast<size_t>(n) * W), Ff(static_cast<size_t>(P) * W * W), hb(static_cast<size_t>(n) * ku);
+  const int n = f.n, kl = f.kl, ku = f.ku, W = kl + 1, Ls = kSegL;
+  const int P = (n + Ls - 1) / Ls;
+  if (P < 4 || ku != 2 * kl) return;
+  const int NP = P * Ls;
+  // padded row access
+  auto Lm = [&](int k, int q) { return k < n ? f.L[static_cast<size_t>(k) * kl + q] : cplx(0.0, 0.0); };
+  auto Uu = [&](int k, int d) { return k < n ? f.U[static_cast<size_t>(k) * (ku + 1) + d] : (d == 0 ? cplx(1.0, 0.0) : cplx(0.0, 0.0)); };
+  auto pv = [&](int k) { return k < n ? f.piv[k] - k : 0; };
+  auto at = [&](int k, int fld, int nf) { return (static_cast<size_t>(k % Ls) * nf + fld) * P + k / Ls; };
+  std::vector<cplx> Lt(static_cast<size_t>(NP) * kl), hf(static_cast<size_t>(NP) * W), Ut(static_cast<size_t>(NP) * ku),
+      Ui(NP), hb(static_cast<size_t>(NP) * ku), Ff(static_cast<size_t>(P) * W * W), Hb(static_cast<size_t>(P) * ku * ku);
+  std::vector<int> pt(NP);
+  for (int k = 0; k < NP; ++k) {
+    for (int q = 0; q < kl; ++q) Lt[at(k, q, kl)] = Lm(k, q);
+    pt[at(k, 0, 1)] = pv(k);
+    for (int d = 1; d <= ku; ++d) Ut[at(k, d - 1, ku)] = Uu(k, d);
+    Ui[at(k, 0, 1)] = 1.0 / Uu(k, 0);
+  }
   for (int i = 0; i < P; ++i) {
-    const int s = i * Ls, e = i + 1 == P ? n : (i + 1) * Ls;
+    const int s = i * Ls, e = s + Ls;
     for (int q = 0; q < W; ++q) {  // forward from window e_q, no rhs
       std::vector<cplx> w(W, cplx(0.0, 0.0));
       w[q] = 1.0;
       for (int k = s; k < e; ++k) {
-        const int p = f.piv[k] - k;
+        const int p = pv(k);
         if (p != 0) std::swap(w[0], w[p]);
         const cplx yk = w[0];
-        hf[static_cast<size_t>(k) * W + q] = yk;
-        for (int r = 1; r <= kl; ++r) w[r] -= f.L[static_cast<size_t>(k) * kl + r - 1] * yk;
+        hf[at(k, q, W)] = yk;
+        for (int r = 1; r <= kl; ++r) w[r] -= Lm(k, r - 1) * yk;
         for (int r = 0; r < kl; ++r) w[r] = w[r + 1];
         w[kl] = 0.0;
       }
@@ -433,32 +447,34 @@ static void make_segments(ExactSolver& X, const BandLU& f) {
       xw[r] = 1.0;
       for (int k = e - 1; k >= s; --k) {
         cplx acc(0.0, 0.0);
-        for (int d = ku; d >= 1; --d) acc -= f.U[static_cast<size_t>(k) * (ku + 1) + d] * xw[d - 1];
-        const cplx xk = acc / f.U[static_cast<size_t>(k) * (ku + 1)];
+        for (int d = ku; d >= 1; --d) acc -= Uu(k, d) * xw[d - 1];
+        const cplx xk = acc / Uu(k, 0);
         for (int d = ku - 1; d >= 1; --d) xw[d] = xw[d - 1];
         xw[0] = xk;
-        hb[static_cast<size_t>(k) * ku + r] = xk;
+        hb[at(k, r, ku)] = xk;
+        if (k - s < ku) Hb[(static_cast<size_t>(i) * ku + (k - s)) * ku + r] = xk;
       }
     }
   }
-  auto up = [](const std::vector<cplx>& v) {
-    double2* d = dalloc<double2>(v.size());
-    CK(cudaMemcpy(d, v.data(), v.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  auto up = [](const auto& v) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    T* d = dalloc<T>(v.size());
+    CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
     return d;
   };
   SegArgs& a = X.seg;
   a.n = n;
   a.P = P;
-  a.Ls = Ls;
-  a.L = X.L;
-  a.U = X.U;
-  a.Uinv = X.Uinv;
-  a.piv = X.piv;
-  a.hf = up(hf);
-  a.Ff = up(Ff);
-  a.hb = up(hb);
-  a.y = dalloc<double2>(n);
-  a.x0 = dalloc<double2>(n);
+  a.L = reinterpret_cast<const double2*>(up(Lt));
+  a.pv = up(pt);
+  a.hf = reinterpret_cast<const double2*>(up(hf));
+  a.U = reinterpret_cast<const double2*>(up(Ut));
+  a.Ui = reinterpret_cast<const double2*>(up(Ui));
+  a.hb = reinterpret_cast<const double2*>(up(hb));
+  a.Ff = reinterpret_cast<const double2*>(up(Ff));
+  a.Hb = reinterpret_cast<const double2*>(up(Hb));
+  a.y = dalloc<double2>(NP);
+  a.x0 = dalloc<double2>(NP);
   a.D = dalloc<double2>(static_cast<size_t>(P) * W);
   a.Dl = dalloc<double2>(static_cast<size_t>(P) * W);
   a.X0 = dalloc<double2>(static_cast<size_t>(P) * ku);
@@ -493,8 +509,12 @@ static void free_exact(ExactSolver& X) {
   cudaFree(X.Vt); cudaFree(X.Dinvf); cudaFree(X.F); cudaFree(X.G); cudaFree(X.Hh); cudaFree(X.R);
   cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work); cudaFree(X.Uinv);
   if (X.seg.P) {
-    cudaFree(const_cast<double2*>(X.seg.hf)); cudaFree(const_cast<double2*>(X.seg.Ff));
-    cudaFree(const_cast<double2*>(X.seg.hb)); cudaFree(X.seg.y); cudaFree(X.seg.x0); cudaFree(X.seg.D);
+    for (const void* p : {static_cast<const void*>(X.seg.L), static_cast<const void*>(X.seg.pv),
+                          static_cast<const void*>(X.seg.hf), static_cast<const void*>(X.seg.U),
+                          static_cast<const void*>(X.seg.Ui), static_cast<const void*>(X.seg.hb),
+                          static_cast<const void*>(X.seg.Ff), static_cast<const void*>(X.seg.Hb)})
+      cudaFree(const_cast<void*>(p));
+    cudaFree(X.seg.y); cudaFree(X.seg.x0); cudaFree(X.seg.D);
     cudaFree(X.seg.Dl); cudaFree(X.seg.X0); cudaFree(X.seg.Xb);
   }
   cudaFree(X.Ainv); cudaFree(X.dx); cudaFree(X.dy);
