@@ -25,12 +25,19 @@ namespace hd {
 
 constexpr int kSW = 32;      // columns per warp
 constexpr int kSWarps = 4;   // warps per CTA
-constexpr int kSRing = 8;    // ring depth (rows in flight per warp)
 constexpr int kSRowsMax = 128;
 
+// ring depth (rows in flight per warp): the band height 2B+1 if that is >= 7,
+// else its smallest multiple >= 8, so that the row loop unrolled over one ring period addresses
+// both the ring slots and the rotating accumulators statically
+template <int B>
+__host__ __device__ constexpr int stencil_ring() {
+  return 2 * B + 1 >= 7 ? 2 * B + 1 : (2 * B + 1) * ((8 + 2 * B) / (2 * B + 1));
+}
+
 template <int B, int MODE>
-constexpr size_t stencil_smem(int ry) {
-  return sizeof(double2) * ((size_t)kSWarps * kSRing * ((kSW + 2 * B) + (MODE != OP_APPLY ? kSW : 0)) +
+__host__ __device__ constexpr size_t stencil_smem(int ry) {
+  return sizeof(double2) * ((size_t)kSWarps * stencil_ring<B>() * ((kSW + 2 * B) + (MODE != OP_APPLY ? kSW : 0)) +
                             (size_t)(ry + 4 * B + 1) * (2 * B + 1));
 }
 
@@ -41,6 +48,7 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
                                                             RedOut red, const int* xidx, size_t xstride) {
   constexpr int NB = 2 * B + 1;
   constexpr int W = kSW + 2 * B;
+  constexpr int kSRing = stencil_ring<B>();
   constexpr bool NEED_B = MODE != OP_APPLY;
   if (xidx) x += (size_t)(*xidx) * xstride;  // graph mode: x = V + j N
   extern __shared__ __align__(16) double2 dsm[];
@@ -87,8 +95,7 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
     const double2* pB = x + (ptrdiff_t)(y0 - B) * n + (okB ? colB : 0);
     const double2* pb = bv + (ptrdiff_t)(y0 - 2 * B) * n + (colv ? ix : 0);
     int rl = y0 - B;  // global row of the next load
-    int sl = 0;       // its ring slot
-    auto load = [&]() {
+    auto load = [&](int sl) {  // sl: its ring slot (static at every call site)
       const bool rv = (rl >= 0) && (rl < n);
       cp_async16(&rg[sl][lane], rv && okA ? pA : x, rv && okA);
       if (hasB) cp_async16(&rg[sl][kSW + lane], rv && okB ? pB : x, rv && okB);
@@ -101,11 +108,10 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
       pA += n;
       pB += n;
       ++rl;
-      sl = (sl + 1) & (kSRing - 1);
     };
 #pragma unroll
     for (int k = 0; k < kSRing - 1; ++k) {
-      if (k < nin) load();
+      if (k < nin) load(k);
       cp_async_commit();
     }
     // scatter form: row k contributes to the 2B+1 pending output rows
@@ -117,15 +123,15 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
     const double2 c = L.c;
     double2* outp = out + (size_t)y0 * n + ix;
     const double2* cyk = cy;  // band row of output o = k - 2B (padded index o + 2B == k)
-    int s = 0;                // ring slot of row k
-    for (int kb = 0; kb < nin; kb += NB) {
+    for (int kb = 0; kb < nin; kb += kSRing) {
 #pragma unroll
-      for (int t = 0; t < NB; ++t) {
+      for (int t = 0; t < kSRing; ++t) {
         const int k = kb + t;
+        const int s = t;  // ring slot of row k (kb is a multiple of the ring depth)
         if (k < nin) {
           cp_async_wait<kSRing - 2>();
           __syncwarp();
-          if (k + kSRing - 1 < nin) load();
+          if (k + kSRing - 1 < nin) load((t + kSRing - 1) % kSRing);
           cp_async_commit();
           double2 u0 = cmk(0.0, 0.0), u1 = cmk(0.0, 0.0), v0 = cmk(0.0, 0.0), v1 = cmk(0.0, 0.0);
 #pragma unroll
@@ -169,7 +175,6 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
             outp += n;
           }
           cyk += NB;
-          s = (s + 1) & (kSRing - 1);
         }
       }
     }
