@@ -22,6 +22,8 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include")]
 
+TOOL_SRC = ROOT / "tools" / "hd_cell.cpp"
+TOOL = ROOT / "tools" / "hd_cell"
 CU_SOURCES = ["solver.cu"]
 CPP_SOURCES = ["host/banded.cpp", "host/assembly.cpp"]
 
@@ -65,6 +67,11 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
     if _stale(OUT, objs):
         _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *map(str, objs), "-o", str(OUT),
               "-lcublas", "-lcusolver", "-lcudart"])
+    # the C++ host mirror's cell tool (include/helmdef_b200.hpp), linked against
+    # the in-tree library with a relative rpath so the built tree can move
+    if TOOL_SRC.exists() and _stale(TOOL, [TOOL_SRC, OUT, ROOT / "include" / "helmdef_b200.hpp"]):
+        _run(["g++", "-O2", "-std=c++17", "-Wall", "-I", str(ROOT / "include"), str(TOOL_SRC), "-o", str(TOOL),
+              "-L", str(PKG), "-lhelmdef_b200", "-Wl,-rpath,$ORIGIN/../paper_2010_10232_b200"])
     return OUT
 
 
