@@ -312,6 +312,20 @@ def run_gpu(args):
                 "bytes_per_launch": b / n, "us_per_launch": 1e3 * ms / n, "peak_source": peak_src}
     # whole-solve effective bandwidth on the algorithmic bytes of all own kernels
     all_b = sum(v[2] for k_, v in prof.items() if k_ != "lib_gemm")
+    # SURVEY.md 8(d) path roofline: compulsory bytes B_min(j) of the reference's
+    # formulation (MGS + per-step iterate), summed over this solve's iterations
+    L = solver.levels
+    if L > 1:
+        nl = [solver.level_size(l) ** dim for l in range(L)]
+        mg = sum((6 * SPEC["smoothing"] + 2) * nl[l] / N + 2 * nl[l + 1] / N for l in range(L - 1))
+    else:
+        mg = 0.0
+    base = (18.0 if dim == 2 else 19.0) + SPEC["cycles"] * mg
+    bmin = sum(16.0 * N * (base + 5 * j) for j in range(r.iterations))
+    path_bmin = {"bytes_per_solve": bmin, "GBps": round(bmin / (t_max / args.steps * 1e-3) / 1e9, 1),
+                 "frac": round(bmin / (t_max / args.steps * 1e-3) / 1e9 / peak, 4),
+                 "note": "SURVEY.md 8(d) B_min(j) = 16N[18 + 5j + c*MG] (2D): the reference's MGS formulation; "
+                         "this path's one-reduction Arnoldi streams ~2j vector passes per iteration, not 5j"}
 
     line = {"metric": "preconditioned GMRES iterations/s", "value": value, "unit": "iterations/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
@@ -327,6 +341,7 @@ def run_gpu(args):
             "roofline_note": "per-kernel CUDA events of one extra profiled solve (host-driven launch loop) "
                              "after the timed region; achieved = algorithmic bytes / event time",
             "solve_effective_GBps": round(all_b / (tot_prof_ms * 1e-3) / 1e9, 1) if prof else None,
+            "path_roofline_Bmin": path_bmin,
             "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, el, note, _ = oracle_sample(args.config, args.cpu_iters)
