@@ -91,7 +91,7 @@ __device__ __forceinline__ double2 lsa_collect(const double2* partials, int nslo
 // chunk (coalesced, 8 loads in flight per lane) and reduce once per chunk and
 // vector into per-CTA shared accumulators (one warp owns each vector slot).
 // ---------------------------------------------------------------------------
-constexpr int kLsaCE = 2048;  // chunk elements
+constexpr int kLsaCE = 1024;  // chunk elements
 
 constexpr size_t lsa_dots_smem() { return sizeof(double2) * (2 * kLsaCE + 2 * (kLsaMaxJ + 1)); }
 
