@@ -136,6 +136,19 @@ hd_status hd_assemble(const hd_problem* pb, double* stiffness_band, double* mass
 hd_status hd_create(const hd_system* sys, const hd_precond* spec, const int* devices,
                     int n_devices, hd_ctx** out);
 
+/* compose() on a row-slab decomposition of the 2D grid:
+ * nslabs bands of iy rows with halo rows, halo exchange before every apply
+ * and transfer, the gather level and the deflation coarse vector assembled
+ * whole, reductions combined in slab order -- the multi-GPU program, run here
+ * with all slabs on one device (copies for the exchanges).  hd_solve /
+ * hd_solve_device / hd_apply then use the slabs.  Constant field, shift with
+ * cycles >= 1 (the DC_MG family). */
+hd_status hd_create_slabs(const hd_system* sys, const hd_precond* spec, int nslabs, hd_ctx** out);
+
+/* Slab count of a context (0: single domain); gather_level and the nslabs+1
+ * fine row bounds are written when non-NULL. */
+int hd_slab_info(const hd_ctx* ctx, int* gather_level, int* bounds);
+
 /* gmres(compose(...)): host buffers.  rhs: 2N doubles; x_out: 2N doubles;
  * residuals_out: max_iterations (+1) doubles (may be NULL).  Includes the
  * host->device copy of rhs and the device->host copy of x. */

@@ -41,7 +41,7 @@ HD_APPLY_A, HD_APPLY_SHIFTED, HD_APPLY_MG, HD_APPLY_PROJECT, HD_APPLY_OP, HD_APP
 # Every symbol include/helmdef_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = ["hd_problem_per_dim", "hd_assemble", "hd_create", "hd_solve", "hd_solve_device", "hd_size",
            "hd_levels", "hd_apply", "hd_debug_level", "hd_level_size", "hd_set_stream", "hd_profile",
-           "hd_profile_read", "hd_destroy", "hd_last_error"]
+           "hd_profile_read", "hd_destroy", "hd_last_error", "hd_create_slabs", "hd_slab_info"]
 KERNEL_KINDS = ["op_fine", "op_coarse", "jacobi0", "transfer", "exact", "mgs", "iterate", "vec", "givens",
                 "lib_gemm"]
 
@@ -94,6 +94,10 @@ def load_library() -> C.CDLL:
     lib.hd_create.argtypes = [C.POINTER(HdSystem), C.POINTER(HdPrecond), C.POINTER(C.c_int), C.c_int,
                               C.POINTER(C.c_void_p)]
     lib.hd_create.restype = C.c_int
+    lib.hd_create_slabs.argtypes = [C.POINTER(HdSystem), C.POINTER(HdPrecond), C.c_int, C.POINTER(C.c_void_p)]
+    lib.hd_create_slabs.restype = C.c_int
+    lib.hd_slab_info.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    lib.hd_slab_info.restype = C.c_int
     lib.hd_solve.argtypes = [C.c_void_p, C.POINTER(HdGmres), dp, dp, dp, C.POINTER(HdReport)]
     lib.hd_solve.restype = C.c_int
     lib.hd_solve_device.argtypes = [C.c_void_p, C.POINTER(HdGmres), C.c_void_p, C.c_void_p, dp,
@@ -309,7 +313,8 @@ def to_spec(tag, order, k, epsilon=0.1, beta2="1", cycles=1, smoothing=1, omega=
 class Solver:
     """compose(sys, spec) on the device; .solve() is gmres(op, rhs, start, monitor)."""
 
-    def __init__(self, sys_: DiscreteSystem, spec: PrecondSpec, devices=None):
+    def __init__(self, sys_: DiscreteSystem, spec: PrecondSpec, devices=None, slabs: int = 0):
+        """slabs > 0: the row-slab decomposition (hd_create_slabs)."""
         lib = load_library()
         self._lib = lib
         self.sys = sys_
@@ -334,11 +339,18 @@ class Solver:
         if devices:
             arr = (C.c_int * len(devices))(*devices)
             _check(lib.hd_create(C.byref(h), C.byref(p), arr, len(devices), C.byref(ctx)))
+        elif slabs:
+            _check(lib.hd_create_slabs(C.byref(h), C.byref(p), int(slabs), C.byref(ctx)))
         else:
             _check(lib.hd_create(C.byref(h), C.byref(p), None, 0, C.byref(ctx)))
         self._ctx = ctx
         self.size = lib.hd_size(ctx)
         self.levels = lib.hd_levels(ctx)
+        gl = C.c_int(0)
+        bnd = (C.c_int * 65)()
+        self.slabs = lib.hd_slab_info(ctx, C.byref(gl), bnd) if slabs else 0
+        self.slab_gather_level = gl.value if self.slabs else None
+        self.slab_bounds = [bnd[i] for i in range(self.slabs + 1)] if self.slabs else None
 
     def close(self):
         if getattr(self, "_ctx", None):

@@ -52,6 +52,9 @@ struct LsaArgs {
   const int* dj;      // device-side iteration index (graph mode); overrides j when set
   int jlag;           // Givens only: work on iteration (j - jlag) (graph mode: the previous
                       // iteration's Givens overlaps this iteration's operator)
+  int part_offset;    // row slabs: this slab's first CTA slot in `partials` (0: single domain)
+  int partial_only;   // row slabs: pass 1 writes its CTA partials and stops (k_lsa_dots_finish
+                      // combines the slabs' partials in slab order)
 };
 
 __device__ __forceinline__ double2 lsa_warp_sum(double2 v) {
@@ -77,10 +80,10 @@ __device__ __forceinline__ bool lsa_last_block(unsigned* counter) {
 }
 
 // Sum slot q of the per-CTA partials (fixed order) -- one warp per slot.
-__device__ __forceinline__ double2 lsa_collect(const double2* partials, int nslot, int q) {
+__device__ __forceinline__ double2 lsa_collect(const double2* partials, int nslot, int q, int nparts) {
   double2 s = cmk(0.0, 0.0);
   const int lane = threadIdx.x & 31;
-  for (unsigned b = lane; b < gridDim.x; b += 32) s = cadd(s, __ldcg(&partials[(size_t)b * nslot + q]));
+  for (int b = lane; b < nparts; b += 32) s = cadd(s, __ldcg(&partials[(size_t)b * nslot + q]));
   s = lsa_warp_sum(s);
   return cmk(__shfl_sync(0xffffffffu, s.x, 0), __shfl_sync(0xffffffffu, s.y, 0));
 }
@@ -92,6 +95,9 @@ __device__ __forceinline__ double2 lsa_collect(const double2* partials, int nslo
 // vector into per-CTA shared accumulators (one warp owns each vector slot).
 // ---------------------------------------------------------------------------
 constexpr int kLsaCE = 1024;  // chunk elements
+
+struct LsaArgs;
+__device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh_s, double2* sh_lj, double2* hsm);
 
 constexpr size_t lsa_dots_smem() { return sizeof(double2) * (2 * kLsaCE + 2 * (kLsaMaxJ + 1)); }
 
@@ -149,17 +155,27 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   __syncthreads();
   for (int q = threadIdx.x; q < nslot; q += kLsaBD) {
     const bool used = q < nd || (q >= kLsaMaxJ + 1 && q < kLsaMaxJ + 1 + j);
-    if (used) a.partials[(size_t)blockIdx.x * nslot + q] = acc[q];
+    if (used) a.partials[(size_t)(a.part_offset + blockIdx.x) * nslot + q] = acc[q];
   }
+  if (a.partial_only) return;
   if (!lsa_last_block(a.counter)) return;
-  // ---- last CTA: totals, Gram row j, triangular solve (I + L) h = s --------
+  lsa_dots_finish(a, j, gridDim.x, sh_s, sh_lj, hsm);
+  if (threadIdx.x == 0) *a.counter = 0u;
+}
+
+// ---- totals, Gram row j, triangular solve (I + L) h = s (one CTA) ----------
+__device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh_s, double2* sh_lj, double2* hsm) {
+  constexpr int NW = kLsaBD / 32;
+  const int nd = j + 1;
+  const int nslot = 2 * kLsaMaxJ + 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double sj = a.sig[j];
   for (int q = warp; q < nd; q += NW) {
-    const double2 s = lsa_collect(a.partials, nslot, q);
+    const double2 s = lsa_collect(a.partials, nslot, q, nparts);
     if (lane == 0) sh_s[q] = cscale(a.sig[q] * sj, s);
   }
   for (int q = warp; q < j; q += NW) {
-    const double2 gsum = lsa_collect(a.partials, nslot, kLsaMaxJ + 1 + q);
+    const double2 gsum = lsa_collect(a.partials, nslot, kLsaMaxJ + 1 + q, nparts);
     if (lane == 0) {
       const double2 lq = cscale(sj * a.sig[q], gsum);  // v_j^H v_q
       a.L[(size_t)j * a.ldl + q] = lq;
@@ -187,7 +203,15 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
       __syncwarp();
     }
   }
-  if (threadIdx.x == 0) *a.counter = 0u;
+}
+
+// row slabs: combine the partials of all slabs (nparts CTA slots, slab order)
+__global__ void __launch_bounds__(kLsaBD) k_lsa_dots_finish(LsaArgs a, int nparts) {
+  __shared__ double2 sh_s[kLsaMaxJ + 1];
+  __shared__ double2 sh_lj[kLsaMaxJ];
+  __shared__ double2 hsm[kLsaMaxJ + 1];
+  const int j = a.dj ? *a.dj : a.j;
+  lsa_dots_finish(a, j, nparts, sh_s, sh_lj, hsm);
 }
 
 // ---------------------------------------------------------------------------
@@ -275,7 +299,7 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int q = 0; q < NW; ++q) s += red[q];
-    a.partials[blockIdx.x] = cmk(s, 0.0);
+    a.partials[a.part_offset + blockIdx.x] = cmk(s, 0.0);
   }
 }
 

@@ -37,6 +37,7 @@ struct RedOut {
   unsigned* counter;
   double* dst;       // final scalar written by the last block
   double scale;      // dst = sqrt(sum |.|^2) / scale   (monitor: ||f|| or 1, src/precond.cpp:261-262)
+  int raw;           // 1: dst = sum |.|^2 (a row slab's share; slabs are summed before the sqrt)
 };
 
 enum OpMode { OP_APPLY = 0, OP_RESID = 1, OP_JACOBI = 2, OP_RESNORM = 3 };

@@ -204,6 +204,7 @@ struct hd_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t own_st = nullptr;  // the context's own stream while an external one is set
   cudaStream_t st2 = nullptr;     // side branch of the graph body (Givens of the previous iteration)
+  void* slabs = nullptr;          // row-slab state (hd_create_slabs), or null
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
@@ -747,14 +748,14 @@ static int stencil_occupancy() {
 
 // Strip height: fill whole waves of resident CTAs, discounted by the 2B halo
 // rows each strip re-reads.
-static int pick_rows(int n, int slots, int B) {
+static int pick_rows(int n, int rows, int slots, int B) {
   const int colblocks = (n + kSW * kSWarps - 1) / (kSW * kSWarps);
   static const int cand[] = {8, 12, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 112, 128};
   int best = 32;
   double best_score = -1.0;
   for (int ry : cand) {
     if (ry > kSRowsMax) break;
-    const long tiles = static_cast<long>(colblocks) * ((n + ry - 1) / ry);
+    const long tiles = static_cast<long>(colblocks) * ((rows + ry - 1) / ry);
     const long waves = (tiles + slots - 1) / slots;
     const double util = static_cast<double>(tiles) / (static_cast<double>(waves) * slots);
     const double score = util * ry / (ry + 2.0 * B);
@@ -768,26 +769,28 @@ static int pick_rows(int n, int slots, int B) {
 
 template <int B, int MODE>
 static void launch_stencil(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
-                           double omega, RedOut red, const int* xidx, size_t xstride) {
+                           double omega, RedOut red, const int* xidx, size_t xstride, int rb, int re) {
   const int per = stencil_occupancy<B, MODE>();
-  const int ry = pick_rows(L.n, per * c->n_sms, B);
-  dim3 grid((L.n + kSW * kSWarps - 1) / (kSW * kSWarps), (L.n + ry - 1) / ry);
+  const int ry = pick_rows(L.n, re - rb, per * c->n_sms, B);
+  dim3 grid((L.n + kSW * kSWarps - 1) / (kSW * kSWarps), (re - rb + ry - 1) / ry);
   k_stencil2d<B, MODE><<<grid, kSW * kSWarps, stencil_smem<B, MODE>(ry), c->st>>>(L, x, b, out, omega, ry, red,
-                                                                               xidx, xstride);
+                                                                               xidx, xstride, rb, re);
 }
 
 template <int MODE>
 static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
-                             double omega, RedOut red, int kind, const int* xidx, size_t xstride) {
+                             double omega, RedOut red, int kind, const int* xidx, size_t xstride, int rb = 0,
+                             int re = -1) {
+  if (re < 0) re = L.n;
   const size_t mk = prof_mark(c);
   switch (L.b) {
 #define HD_CASE(BB) \
-  case BB: launch_stencil<BB, MODE>(c, L, x, b, out, omega, red, xidx, xstride); break;
+  case BB: launch_stencil<BB, MODE>(c, L, x, b, out, omega, red, xidx, xstride, rb, re); break;
     HD_CASE(1) HD_CASE(2) HD_CASE(3) HD_CASE(4) HD_CASE(5) HD_CASE(6)
 #undef HD_CASE
     default: throw Error(HD_ERR_INVALID, "band half-width " + std::to_string(L.b) + " unsupported");
   }
-  launched(c, kind, mk, op_bytes(MODE, static_cast<size_t>(L.n) * L.n));
+  launched(c, kind, mk, op_bytes(MODE, static_cast<size_t>(L.n) * (re - rb)));
 }
 
 // layered field: G-term Kronecker-sum operator (layered.cuh)
@@ -809,6 +812,7 @@ static void launch_gen_mode(hd_ctx* c, const GenLevel& G, const double2* x, cons
 
 static RedOut red_of(hd_ctx* c, double* dst = nullptr, double scale = 1.0) {
   RedOut r;
+  r.raw = 0;
   r.partials = c->partials;
   r.counter = c->counter;
   r.dst = dst;
@@ -819,8 +823,9 @@ static RedOut red_of(hd_ctx* c, double* dst = nullptr, double scale = 1.0) {
 // out = L x | b - L x | x + w D^-1 (b - L x) | ||b - L x|| * scale -> dst
 static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, const double2* b, double2* out,
                      double omega = 0.0, double* dst = nullptr, double scale = 1.0, const int* xidx = nullptr,
-                     size_t xstride = 0) {
+                     size_t xstride = 0, int rb = 0, int re = -1, int raw = 0) {
   RedOut red = red_of(c, dst, scale);
+  red.raw = raw;
   const int kind = L.n == c->n ? HD_K_OP_FINE : HD_K_OP_COARSE;
   if (L.gen) {
     const GenLevel& G = *static_cast<const GenLevel*>(L.gen);
@@ -834,10 +839,10 @@ static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, c
   }
   if (c->dim == 2) {
     switch (mode) {
-      case OP_APPLY: launch_op2d_mode<OP_APPLY>(c, L, x, b, out, omega, red, kind, xidx, xstride); break;
-      case OP_RESID: launch_op2d_mode<OP_RESID>(c, L, x, b, out, omega, red, kind, xidx, xstride); break;
-      case OP_JACOBI: launch_op2d_mode<OP_JACOBI>(c, L, x, b, out, omega, red, kind, xidx, xstride); break;
-      default: launch_op2d_mode<OP_RESNORM>(c, L, x, b, out, omega, red, kind, xidx, xstride); break;
+      case OP_APPLY: launch_op2d_mode<OP_APPLY>(c, L, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+      case OP_RESID: launch_op2d_mode<OP_RESID>(c, L, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+      case OP_JACOBI: launch_op2d_mode<OP_JACOBI>(c, L, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+      default: launch_op2d_mode<OP_RESNORM>(c, L, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
     }
   } else {
     const int grid = mode == OP_RESNORM ? std::min(grid_for(L.n), c->red_blocks) : grid_for(L.n);
@@ -852,7 +857,9 @@ static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, c
   }
 }
 
-static void jacobi0(hd_ctx* c, const LevelDev& L, const double2* b, double2* out, double omega) {
+static void jacobi0(hd_ctx* c, const LevelDev& L, const double2* b, double2* out, double omega, int rb = 0,
+                    int re = -1) {
+  if (re < 0) re = L.n;
   const size_t NN = c->dim == 2 ? static_cast<size_t>(L.n) * L.n : L.n;
   if (L.gen) {
     HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,
@@ -860,21 +867,23 @@ static void jacobi0(hd_ctx* c, const LevelDev& L, const double2* b, double2* out
     return;
   }
   HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,
-            if (c->dim == 2) k_jacobi0_2d_t<<<dim3((L.n + 63) / 64, (L.n + 15) / 16), 256, 0, c->st>>>(L, b, out,
-                                                                                                        omega);
+            if (c->dim == 2) k_jacobi0_2d_t<<<dim3((L.n + 63) / 64, (re - rb + 15) / 16), 256, 0, c->st>>>(
+                L, b, out, omega, rb, re);
             else k_jacobi0_1d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega));
 }
 
-static void restrict_(hd_ctx* c, Stencil z, const double2* r, int nf, int nc, double2* outc, double* outp) {
+static void restrict_(hd_ctx* c, Stencil z, const double2* r, int nf, int nc, double2* outc, double* outp,
+                      int qb = 0, int qe = -1) {
+  if (qe < 0) qe = nc;
   const size_t NC = c->dim == 2 ? static_cast<size_t>(nc) * nc : nc;
   const double NF = c->dim == 2 ? static_cast<double>(nf) * nf : nf;
   if (c->dim == 2) {
-    dim3 grid((nc + kRQX - 1) / kRQX, (nc + kRQY - 1) / kRQY);
+    dim3 grid((nc + kRQX - 1) / kRQX, (qe - qb + kRQY - 1) / kRQY);
     HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NF + NC),
-              if (z.kind == 0 && !outp) k_restrict2d<0, 0><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp);
-              else if (z.kind == 0) k_restrict2d<0, 1><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp);
-              else if (!outp) k_restrict2d<1, 0><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp);
-              else k_restrict2d<1, 1><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp));
+              if (z.kind == 0 && !outp) k_restrict2d<0, 0><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp, qb, qe);
+              else if (z.kind == 0) k_restrict2d<0, 1><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp, qb, qe);
+              else if (!outp) k_restrict2d<1, 0><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp, qb, qe);
+              else k_restrict2d<1, 1><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp, qb, qe));
     return;
   }
   HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NF + NC),
@@ -883,14 +892,15 @@ static void restrict_(hd_ctx* c, Stencil z, const double2* r, int nf, int nc, do
 
 template <int PMODE>
 static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, int nf, int nc, const double2* s,
-                     double2* out) {
+                     double2* out, int fb = 0, int fe = -1) {
+  if (fe < 0) fe = nf;
   const size_t NF = c->dim == 2 ? static_cast<size_t>(nf) * nf : nf;
   const double NC = c->dim == 2 ? static_cast<double>(nc) * nc : nc;
   if (c->dim == 2) {
-    dim3 grid((nf + kPFX - 1) / kPFX, (nf + kPFY - 1) / kPFY);
+    dim3 grid((nf + kPFX - 1) / kPFX, (fe - fb + kPFY - 1) / kPFY);
     HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NC + (PMODE == 2 ? 1.0 : 2.0) * NF),
-              if (z.kind == 0) k_prolong2d<0, PMODE><<<grid, 256, 0, c->st>>>(z.drop, ec, ep, nf, nc, s, out);
-              else k_prolong2d<1, PMODE><<<grid, 256, 0, c->st>>>(z.drop, ec, ep, nf, nc, s, out));
+              if (z.kind == 0) k_prolong2d<0, PMODE><<<grid, 256, 0, c->st>>>(z.drop, ec, ep, nf, nc, s, out, fb, fe);
+              else k_prolong2d<1, PMODE><<<grid, 256, 0, c->st>>>(z.drop, ec, ep, nf, nc, s, out, fb, fe));
     return;
   }
   HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NC + (PMODE == 2 ? 1.0 : 2.0) * NF),
@@ -1308,6 +1318,8 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
 static LsaArgs lsa_args(hd_ctx* c, double2* xout, int j, int mode, int maxit) {
   LsaArgs a;
   a.jlag = 0;
+  a.part_offset = 0;
+  a.partial_only = 0;
   a.U = c->V;
   a.Uw = c->V;
   a.w = c->w;
@@ -1794,8 +1806,11 @@ static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl) {
   return X;
 }
 
+static void destroy_slabs(hd_ctx* c);
+
 static void destroy_ctx(hd_ctx* c) {
   if (!c) return;
+  if (c->slabs) destroy_slabs(c);
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   auto fb = [](DevBand& d) {
@@ -2015,6 +2030,547 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   *out = c.release();
 }
 
+// ===========================================================================
+// Row-slab decomposition (plan: paper_2010_10232_b200/slabs.py)
+//
+// The 2D grid is cut into S bands of iy rows.  Every distributed level vector
+// is held per slab with H halo rows above and below ([r0-H, r1+H) of the
+// global rows); kernels address it through a "virtual" pointer shifted by the
+// slab origin, so they index global rows and read the halo rows where a
+// stencil or transfer crosses the slab edge.  Communication happens exactly
+// where the multi-GPU program communicates:
+//   * halo exchange before every apply / transfer on a distributed level
+//     (here: device copies between the slabs' buffers; multi-GPU: neighbour
+//     send/recv of H rows);
+//   * the gather level's restricted rhs and the deflation coarse vector are
+//     written into one global buffer (multi-GPU: allgather), the levels below
+//     the gather level and the E solve run once (multi-GPU: redundantly);
+//   * reductions: each slab writes its partial sums (norms: a raw sum of
+//     squares; Arnoldi: its CTAs' partials at its own offset) and one kernel
+//     combines them in slab order (multi-GPU: allreduce).
+// On one GPU the slabs run in sequence on one stream (no kernel waits on
+// another); the result is the single-domain solve up to the association of
+// the sums, which tests/test_gpu_parity.py checks.
+// ===========================================================================
+struct SlabLevel {
+  int n = 0, b = 0, H = 0;
+  bool dist = false;
+  std::vector<int> bounds;  // S+1 row boundaries (distributed levels)
+};
+
+struct hd_slabs {
+  int S = 0, g = 0, Gs = 0;
+  std::vector<SlabLevel> lv;                    // MG levels
+  std::vector<std::vector<double2*>> X, Y, B, R;  // [level][slab], levels < g
+  std::vector<int> cur;                         // ping-pong state of X/Y per level
+  // fine-level vectors, per slab, halo'd with H = lv[0].H
+  std::vector<double2*> f, w, t1, t2, t3, x, x0, rhsp, vin;
+  std::vector<double2*> V;                      // per slab: basis u_0..u_maxit (own rows, flat)
+  int maxit = -1;
+  double* slots = nullptr;                      // per-slab raw sums
+  double2* parts = nullptr;                     // S x Gs Arnoldi partials
+};
+
+__global__ void k_slab_sumsq(const double2* __restrict__ x, size_t N, RedOut red) {
+  __shared__ double2 scratch[32];
+  double acc = 0.0;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
+    acc += cnorm2(x[g]);
+  double2 total;
+  if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = total.x;
+}
+
+// norm = sqrt(sum of the slabs' raw sums, slab order) / scale -> dst (and cdst = (norm, 0))
+__global__ void k_slab_norm(const double* slots, int S, const double* scale_src, double* dst, double2* cdst) {
+  double s = 0.0;
+  for (int i = 0; i < S; ++i) s += slots[i];
+  double sc = 1.0;
+  if (scale_src) sc = *scale_src > 0.0 ? *scale_src : 1.0;
+  const double nrm = sqrt(s) / sc;
+  *dst = nrm;
+  if (cdst) *cdst = cmk(nrm, 0.0);
+}
+
+static hd_slabs* slabs_of(hd_ctx* c) { return reinterpret_cast<hd_slabs*>(c->slabs); }
+
+// virtual pointer of a halo'd slab buffer: global row r of the slab lives at v + r*n
+static inline double2* vptr(double2* buf, int r0, int H, int n) {
+  return buf - static_cast<ptrdiff_t>(r0 - H) * n;
+}
+static inline int own(const SlabLevel& L, int s) { return L.bounds[s + 1] - L.bounds[s]; }
+
+// halo exchange of one distributed level vector (slab s <- neighbours' own rows)
+static void slab_exchange(hd_ctx* c, const SlabLevel& L, const std::vector<double2*>& v) {
+  hd_slabs* sl = slabs_of(c);
+  const size_t row = static_cast<size_t>(L.n) * sizeof(double2);
+  for (int s = 0; s < sl->S; ++s) {
+    if (s > 0)  // top halo: the last H own rows of slab s-1
+      CK(cudaMemcpyAsync(v[s], v[s - 1] + static_cast<size_t>(own(L, s - 1)) * L.n, L.H * row,
+                         cudaMemcpyDeviceToDevice, c->st));
+    if (s + 1 < sl->S)  // bottom halo: the first H own rows of slab s+1
+      CK(cudaMemcpyAsync(v[s] + static_cast<size_t>(L.H + own(L, s)) * L.n, v[s + 1] + static_cast<size_t>(L.H) * L.n,
+                         L.H * row, cudaMemcpyDeviceToDevice, c->st));
+  }
+}
+
+static std::vector<double2*> slab_alloc(const SlabLevel& L, int S) {
+  std::vector<double2*> v(S);
+  for (int s = 0; s < S; ++s) {
+    const size_t rows = static_cast<size_t>(own(L, s) + 2 * L.H);
+    v[s] = dalloc<double2>(rows * L.n);
+    CK(cudaMemset(v[s], 0, rows * L.n * sizeof(double2)));
+  }
+  return v;
+}
+
+// ---- level operators on slabs ------------------------------------------------
+static void s_apply(hd_ctx* c, int mode, const LevelDev& L, const SlabLevel& G, std::vector<double2*>& x,
+                    const std::vector<double2*>* b, std::vector<double2*>* out, double omega) {
+  hd_slabs* sl = slabs_of(c);
+  slab_exchange(c, G, x);
+  for (int s = 0; s < sl->S; ++s) {
+    const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
+    op_apply(c, mode, L, vptr(x[s], r0, G.H, G.n), b ? vptr((*b)[s], r0, G.H, G.n) : nullptr,
+             out ? vptr((*out)[s], r0, G.H, G.n) : nullptr, omega, mode == OP_RESNORM ? sl->slots + s : nullptr, 1.0,
+             nullptr, 0, r0, r1, mode == OP_RESNORM ? 1 : 0);
+  }
+}
+
+static void s_jacobi0(hd_ctx* c, const LevelDev& L, const SlabLevel& G, const std::vector<double2*>& b,
+                      std::vector<double2*>& out) {
+  hd_slabs* sl = slabs_of(c);
+  for (int s = 0; s < sl->S; ++s) {
+    const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
+    jacobi0(c, L, vptr(b[s], r0, G.H, G.n), vptr(out[s], r0, G.H, G.n), c->spec.omega, r0, r1);
+  }
+}
+
+static std::vector<double2*>& sX(hd_slabs* sl, int l) { return sl->cur[l] ? sl->Y[l] : sl->X[l]; }
+static std::vector<double2*>& sY(hd_slabs* sl, int l) { return sl->cur[l] ? sl->X[l] : sl->Y[l]; }
+
+// one V-cycle at distributed level l (src/precond.cpp:144-153); rhs per slab;
+// the result is in sX(l)
+static void s_cycle(hd_ctx* c, int l, std::vector<double2*>& b, bool x_zero) {
+  hd_slabs* sl = slabs_of(c);
+  const SlabLevel& G = sl->lv[l];
+  const LevelDev L = levM(c, l);
+  const int nu = c->spec.smooth_steps;
+  int st = 0;
+  if (x_zero) {
+    if (nu == 0) {
+      for (int s = 0; s < sl->S; ++s)
+        CK(cudaMemsetAsync(sX(sl, l)[s], 0, static_cast<size_t>(own(G, s) + 2 * G.H) * G.n * sizeof(double2), c->st));
+    } else {
+      s_jacobi0(c, L, G, b, sX(sl, l));
+      st = 1;
+    }
+  }
+  for (; st < nu; ++st) {
+    s_apply(c, OP_JACOBI, L, G, sX(sl, l), &b, &sY(sl, l), c->spec.omega);
+    sl->cur[l] ^= 1;
+  }
+  s_apply(c, OP_RESID, L, G, sX(sl, l), &b, &sl->R[l], 0.0);
+  // restriction into level l+1: its slabs, or the global buffer at the gather level
+  const SlabLevel& Gc = sl->lv[l + 1];
+  slab_exchange(c, G, sl->R[l]);
+  const bool coarse_dist = l + 1 < sl->g;
+  for (int s = 0; s < sl->S; ++s) {
+    const int q0 = Gc.bounds[s], q1 = Gc.bounds[s + 1];
+    double2* out = coarse_dist ? vptr(sl->B[l + 1][s], q0, Gc.H, Gc.n) : c->mg_b[l + 1];
+    restrict_(c, Stencil{0, 0.0}, vptr(sl->R[l][s], G.bounds[s], G.H, G.n), G.n, Gc.n, out, nullptr, q0, q1);
+  }
+  const double2* eglob = nullptr;
+  if (coarse_dist) {
+    s_cycle(c, l + 1, sl->B[l + 1], true);
+    slab_exchange(c, Gc, sX(sl, l + 1));
+  } else {
+    eglob = cycle_at(c, l + 1, c->mg_b[l + 1], true);  // the small levels, once (multi-GPU: on every rank)
+  }
+  for (int s = 0; s < sl->S; ++s) {
+    const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
+    const double2* ec = coarse_dist ? vptr(sX(sl, l + 1)[s], Gc.bounds[s], Gc.H, Gc.n) : eglob;
+    prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, G.n, Gc.n, nullptr, vptr(sX(sl, l)[s], r0, G.H, G.n), r0, r1);
+  }
+  for (int k = 0; k < nu; ++k) {
+    s_apply(c, OP_JACOBI, L, G, sX(sl, l), &b, &sY(sl, l), c->spec.omega);
+    sl->cur[l] ^= 1;
+  }
+}
+
+// out = MG^-1 b on the slabs (src/precond.cpp:159-163)
+static void s_mg_solve(hd_ctx* c, std::vector<double2*>& b, std::vector<double2*>& out) {
+  hd_slabs* sl = slabs_of(c);
+  const SlabLevel& G = sl->lv[0];
+  const LevelDev L = levM(c, 0);
+  for (int cy = 0; cy < c->spec.cycles; ++cy) {
+    if (cy == 0) {
+      s_cycle(c, 0, b, true);
+    } else {  // later cycles from the current iterate
+      for (int k = 0; k < c->spec.smooth_steps; ++k) {
+        s_apply(c, OP_JACOBI, L, G, sX(sl, 0), &b, &sY(sl, 0), c->spec.omega);
+        sl->cur[0] ^= 1;
+      }
+      // residual, restriction, coarse cycle, correction, post-smoothing: as s_cycle from a nonzero start
+      s_apply(c, OP_RESID, L, G, sX(sl, 0), &b, &sl->R[0], 0.0);
+      const SlabLevel& Gc = sl->lv[1];
+      slab_exchange(c, G, sl->R[0]);
+      const bool coarse_dist = 1 < sl->g;
+      for (int s = 0; s < sl->S; ++s) {
+        double2* o = coarse_dist ? vptr(sl->B[1][s], Gc.bounds[s], Gc.H, Gc.n) : c->mg_b[1];
+        restrict_(c, Stencil{0, 0.0}, vptr(sl->R[0][s], G.bounds[s], G.H, G.n), G.n, Gc.n, o, nullptr, Gc.bounds[s],
+                  Gc.bounds[s + 1]);
+      }
+      const double2* eglob = nullptr;
+      if (coarse_dist) {
+        s_cycle(c, 1, sl->B[1], true);
+        slab_exchange(c, Gc, sX(sl, 1));
+      } else {
+        eglob = cycle_at(c, 1, c->mg_b[1], true);
+      }
+      for (int s = 0; s < sl->S; ++s) {
+        const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
+        const double2* ec = coarse_dist ? vptr(sX(sl, 1)[s], Gc.bounds[s], Gc.H, Gc.n) : eglob;
+        prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, G.n, Gc.n, nullptr, vptr(sX(sl, 0)[s], r0, G.H, G.n), r0, r1);
+      }
+      for (int k = 0; k < c->spec.smooth_steps; ++k) {
+        s_apply(c, OP_JACOBI, L, G, sX(sl, 0), &b, &sY(sl, 0), c->spec.omega);
+        sl->cur[0] ^= 1;
+      }
+    }
+  }
+  const size_t row = static_cast<size_t>(G.n) * sizeof(double2);
+  for (int s = 0; s < sl->S; ++s)
+    CK(cudaMemcpyAsync(out[s] + static_cast<size_t>(G.H) * G.n, sX(sl, 0)[s] + static_cast<size_t>(G.H) * G.n,
+                       own(G, s) * row, cudaMemcpyDeviceToDevice, c->st));
+}
+
+// deflation on the slabs: out = v - Z E^-1 Z^T (A v) (project) or Z E^-1 Z^T v (Q)
+static void s_deflate(hd_ctx* c, std::vector<double2*>& v, std::vector<double2*>& out, bool project) {
+  hd_slabs* sl = slabs_of(c);
+  const SlabLevel& G = sl->lv[0];
+  const Stencil z{1, c->spec.drop};
+  std::vector<double2*>* src = &v;
+  if (project) {
+    s_apply(c, OP_APPLY, opA(c), G, v, nullptr, &sl->t3, 0.0);
+    src = &sl->t3;
+  }
+  slab_exchange(c, G, *src);
+  const SlabLevel& Gc = sl->lv[1];  // the deflation coarse grid (per_dim / 2) shares level 1's rows
+  for (int s = 0; s < sl->S; ++s)
+    restrict_(c, z, vptr((*src)[s], G.bounds[s], G.H, G.n), c->n, c->nc, nullptr, c->ep, Gc.bounds[s],
+              Gc.bounds[s + 1]);
+  exact_solve_planar(c, c->E, c->ep);  // once (multi-GPU: on every rank after the allgather)
+  for (int s = 0; s < sl->S; ++s) {
+    const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
+    if (project)
+      prolong_<1>(c, z, nullptr, c->ep, c->n, c->nc, vptr(v[s], r0, G.H, G.n), vptr(out[s], r0, G.H, G.n), r0, r1);
+    else
+      prolong_<2>(c, z, nullptr, c->ep, c->n, c->nc, nullptr, vptr(out[s], r0, G.H, G.n), r0, r1);
+  }
+}
+
+// op(v) = P MG^-1 A v on the slabs (src/precond.cpp:236-245)
+static void s_op(hd_ctx* c, std::vector<double2*>& v, std::vector<double2*>& out) {
+  hd_slabs* sl = slabs_of(c);
+  ++c->matvecs;
+  s_apply(c, OP_APPLY, opA(c), sl->lv[0], v, nullptr, &sl->t1, 0.0);
+  std::vector<double2*>* cur = &sl->t1;
+  if (c->spec.shift) {
+    ++c->shift_solves;
+    c->vcycles += c->spec.cycles;
+    s_mg_solve(c, sl->t1, sl->t2);
+    cur = &sl->t2;
+  }
+  if (c->spec.deflate) {
+    ++c->coarse_solves;
+    s_deflate(c, *cur, out, true);
+  } else {
+    const SlabLevel& G = sl->lv[0];
+    for (int s = 0; s < sl->S; ++s)
+      CK(cudaMemcpyAsync(out[s], (*cur)[s], static_cast<size_t>(own(G, s) + 2 * G.H) * G.n * sizeof(double2),
+                         cudaMemcpyDeviceToDevice, c->st));
+  }
+}
+
+// ||v|| over the slabs -> dst (raw sums in slab order; scale_src: divide by it)
+static void s_norm(hd_ctx* c, std::vector<double2*>& v, double* dst, double2* cdst = nullptr,
+                   const double* scale_src = nullptr) {
+  hd_slabs* sl = slabs_of(c);
+  const SlabLevel& G = sl->lv[0];
+  for (int s = 0; s < sl->S; ++s) {
+    RedOut r = red_of(c, sl->slots + s);
+    r.raw = 1;
+    const size_t N = static_cast<size_t>(own(G, s)) * G.n;
+    HD_LAUNCH(HD_K_VEC, 16.0 * N,
+              k_slab_sumsq<<<std::min(grid_for(N), c->red_blocks), 256, 0, c->st>>>(v[s] + static_cast<size_t>(G.H) * G.n, N, r));
+  }
+  HD_LAUNCH(HD_K_VEC, 0.0, k_slab_norm<<<1, 1, 0, c->st>>>(sl->slots, sl->S, scale_src, dst, cdst));
+}
+
+static void s_monitor(hd_ctx* c, std::vector<double2*>& x) {  // ||f - A x|| / ||f||
+  hd_slabs* sl = slabs_of(c);
+  s_apply(c, OP_RESNORM, opA(c), sl->lv[0], x, &sl->f, nullptr, 0.0);
+  HD_LAUNCH(HD_K_VEC, 0.0, k_slab_norm<<<1, 1, 0, c->st>>>(sl->slots, sl->S, c->dres + 3, c->dres + 0, nullptr));
+}
+
+// whole-grid vector <-> slabs (own rows)
+static void s_scatter(hd_ctx* c, const double2* full, std::vector<double2*>& v) {
+  hd_slabs* sl = slabs_of(c);
+  const SlabLevel& G = sl->lv[0];
+  for (int s = 0; s < sl->S; ++s)
+    CK(cudaMemcpyAsync(v[s] + static_cast<size_t>(G.H) * G.n, full + static_cast<size_t>(G.bounds[s]) * G.n,
+                       static_cast<size_t>(own(G, s)) * G.n * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+}
+static void s_gather(hd_ctx* c, const std::vector<double2*>& v, double2* full) {
+  hd_slabs* sl = slabs_of(c);
+  const SlabLevel& G = sl->lv[0];
+  for (int s = 0; s < sl->S; ++s)
+    CK(cudaMemcpyAsync(full + static_cast<size_t>(G.bounds[s]) * G.n, v[s] + static_cast<size_t>(G.H) * G.n,
+                       static_cast<size_t>(own(G, s)) * G.n * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+}
+
+// basis vector u_j of slab s <-> halo'd slab vectors
+static void s_basis_to(hd_ctx* c, int j, std::vector<double2*>& v) {
+  hd_slabs* sl = slabs_of(c);
+  const SlabLevel& G = sl->lv[0];
+  for (int s = 0; s < sl->S; ++s) {
+    const size_t Ns = static_cast<size_t>(own(G, s)) * G.n;
+    CK(cudaMemcpyAsync(v[s] + static_cast<size_t>(G.H) * G.n, sl->V[s] + static_cast<size_t>(j) * Ns,
+                       Ns * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+  }
+}
+
+static LsaArgs s_lsa(hd_ctx* c, int s, int j, int mode, int maxit) {
+  hd_slabs* sl = slabs_of(c);
+  const SlabLevel& G = sl->lv[0];
+  LsaArgs a = lsa_args(c, sl->x[s] + static_cast<size_t>(G.H) * G.n, j, mode, maxit);
+  a.U = a.Uw = sl->V[s];
+  a.w = sl->w[s] + static_cast<size_t>(G.H) * G.n;
+  a.x0 = sl->x0[s] + static_cast<size_t>(G.H) * G.n;
+  a.N = static_cast<size_t>(own(G, s)) * G.n;
+  a.partials = sl->parts;
+  a.part_offset = s * sl->Gs;
+  a.partial_only = 1;
+  return a;
+}
+
+static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f_full, double2* xout_full) {
+  hd_slabs* sl = slabs_of(c);
+  const int maxit = std::max(opt.max_iterations, 1);
+  if (maxit + 1 > kLsaMaxJ) throw Error(HD_ERR_INVALID, "row slabs: max_iterations above the Arnoldi limit");
+  ensure_gmres(c, maxit);
+  const SlabLevel& G = sl->lv[0];
+  if (sl->maxit < maxit) {
+    for (auto* p : sl->V) cudaFree(p);
+    for (int s = 0; s < sl->S; ++s) sl->V[s] = dalloc<double2>(static_cast<size_t>(maxit + 1) * own(G, s) * G.n);
+    sl->maxit = maxit;
+  }
+  c->matvecs = c->coarse_solves = c->shift_solves = c->vcycles = 0;
+  c->launches = c->lib_calls = 0;
+  s_scatter(c, f_full, sl->f);
+  s_norm(c, sl->f, c->dres + 3);
+  // rhs' = P MG^-1 f, start = Q f  (src/precond.cpp:247-256)
+  std::vector<double2*>* b = &sl->f;
+  if (c->spec.shift) {
+    ++c->shift_solves;
+    c->vcycles += c->spec.cycles;
+    s_mg_solve(c, sl->f, sl->t2);
+    b = &sl->t2;
+  }
+  if (c->spec.deflate) {
+    ++c->coarse_solves;
+    s_deflate(c, *b, sl->rhsp, true);
+    s_deflate(c, sl->f, sl->x0, false);
+    ++c->coarse_solves;
+  } else {
+    for (int s = 0; s < sl->S; ++s) {
+      CK(cudaMemcpyAsync(sl->rhsp[s], (*b)[s], static_cast<size_t>(own(G, s) + 2 * G.H) * G.n * sizeof(double2),
+                         cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemsetAsync(sl->x0[s], 0, static_cast<size_t>(own(G, s) + 2 * G.H) * G.n * sizeof(double2), c->st));
+    }
+  }
+  SolveOut res;
+  s_monitor(c, sl->x0);
+  read_scalars(c);
+  if (c->hres[0] <= opt.tolerance) {
+    res.converged = true;
+    res.residuals.push_back(c->hres[0]);
+    s_gather(c, sl->x0, xout_full);
+    return res;
+  }
+  // r = rhs' - op(x0), beta = ||r||, u_0 = r, sigma_0 = 1/beta
+  s_op(c, sl->x0, sl->w);
+  for (int s = 0; s < sl->S; ++s) {
+    const size_t o = static_cast<size_t>(G.H) * G.n, Ns = static_cast<size_t>(own(G, s)) * G.n;
+    HD_LAUNCH(HD_K_VEC, 48.0 * Ns, k_sub<<<grid_for(Ns), 256, 0, c->st>>>(sl->rhsp[s] + o, sl->w[s] + o, sl->w[s] + o, Ns));
+  }
+  s_norm(c, sl->w, c->dres + 2, c->g);
+  read_scalars(c);
+  if (c->hres[2] == 0.0) {
+    s_monitor(c, sl->x0);
+    read_scalars(c);
+    res.converged = c->hres[0] <= opt.tolerance;
+    s_gather(c, sl->x0, xout_full);
+    return res;
+  }
+  CK(cudaMemsetAsync(c->H, 0, sizeof(double2) * (maxit + 1) * maxit, c->st));
+  CK(cudaMemsetAsync(c->g + 1, 0, sizeof(double2) * maxit, c->st));
+  for (int s = 0; s < sl->S; ++s) {
+    const size_t Ns = static_cast<size_t>(own(G, s)) * G.n;
+    CK(cudaMemcpyAsync(sl->V[s], sl->w[s] + static_cast<size_t>(G.H) * G.n, Ns * sizeof(double2),
+                       cudaMemcpyDeviceToDevice, c->st));
+  }
+  HD_LAUNCH(HD_K_VEC, 0.0, k_inv_scalar<<<1, 1, 0, c->st>>>(c->lsa_sig, c->dres + 2));
+  const int nparts = sl->S * sl->Gs;
+  bool stop = false;
+  double hnew_prev = 1.0;
+  for (int j = 0; j < maxit && !stop; ++j) {
+    const long snap[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
+    auto rollback = [&]() {
+      c->matvecs = snap[0];
+      c->coarse_solves = snap[1];
+      c->shift_solves = snap[2];
+      c->vcycles = snap[3];
+    };
+    s_basis_to(c, j, sl->vin);
+    s_op(c, sl->vin, sl->w);
+    // pass 1 per slab (partials at the slab's offset), then the slab-order combination
+    for (int s = 0; s < sl->S; ++s) {
+      LsaArgs a = s_lsa(c, s, j, 0, maxit);
+      HD_LAUNCH(HD_K_MGS, (j + 3.0) * 16.0 * a.N, k_lsa_dots<<<sl->Gs, kLsaBD, lsa_dots_smem(), c->st>>>(a));
+    }
+    LsaArgs a0 = s_lsa(c, 0, j, 0, maxit);
+    HD_LAUNCH(HD_K_MGS, 0.0, k_lsa_dots_finish<<<1, kLsaBD, 0, c->st>>>(a0, nparts));
+    for (int s = 0; s < sl->S; ++s) {
+      LsaArgs a = s_lsa(c, s, j, 0, maxit);
+      HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 5.0 : 3.0) * 16.0 * a.N, k_lsa_update<<<sl->Gs, kLsaBD, 0, c->st>>>(a));
+    }
+    if (j >= 1) {  // x_{j-1} is ready
+      s_monitor(c, sl->x);
+      read_scalars(c);
+      const double rr = c->hres[0];
+      res.iterations = j;
+      res.residuals.push_back(rr);
+      if (rr <= opt.tolerance) {
+        res.converged = true;
+        stop = true;
+        rollback();
+        break;
+      }
+      if (hnew_prev < 1e-300) {
+        stop = true;
+        rollback();
+        break;
+      }
+    }
+    HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a0, nparts));
+    CK(cudaMemcpyAsync(c->hres + 1, c->dres + 1, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    if (j + 1 == maxit) {  // budget exhausted: x_{maxit-1}, then its monitor
+      for (int s = 0; s < sl->S; ++s) {
+        LsaArgs bq = s_lsa(c, s, j, 1, maxit);
+        HD_LAUNCH(HD_K_ITERATE, (j + 3.0) * 16.0 * bq.N, k_lsa_update<<<sl->Gs, kLsaBD, 0, c->st>>>(bq));
+      }
+      s_monitor(c, sl->x);
+      read_scalars(c);
+      const double rr = c->hres[0];
+      res.iterations = j + 1;
+      res.residuals.push_back(rr);
+      res.converged = rr <= opt.tolerance;
+      stop = true;
+    }
+    CK(cudaStreamSynchronize(c->st));
+    hnew_prev = c->hres[1];
+  }
+  s_gather(c, sl->x, xout_full);
+  return res;
+}
+
+// plan of slabs.py (gather level, doubled boundaries), built from the context's hierarchy
+static void create_slabs(hd_ctx* c, int S) {
+  if (c->dim != 2) throw Error(HD_ERR_INVALID, "row slabs: 2D only (1D configs run as replicas)");
+  if (c->lev.size() < 2 || !c->spec.shift || c->spec.cycles < 1)
+    throw Error(HD_ERR_INVALID, "row slabs: needs the multigrid-CSLP preconditioner (shift, cycles >= 1)");
+  if (c->fine.genA) throw Error(HD_ERR_INVALID, "row slabs: constant wave-number field only");
+  const int L = static_cast<int>(c->lev.size());
+  const char* e = std::getenv("HD_SLAB_AGGLOMERATE");
+  const int agg = e ? std::atoi(e) : 200;
+  auto split = [&](int n) {
+    std::vector<int> q(S + 1);
+    for (int r = 0; r <= S; ++r) q[r] = static_cast<int>((static_cast<long>(r) * n + S / 2) / S);
+    return q;
+  };
+  int g = 1;
+  while (g < L - 1 && c->lev[g].n > agg) ++g;
+  std::vector<std::vector<int>> bnd;
+  for (;; --g) {
+    const std::vector<int> q = split(c->lev[g].n);
+    bnd.assign(L, {});
+    bool ok = true;
+    for (int l = 0; l <= g; ++l) {
+      const int f = 1 << (g - l);
+      std::vector<int> b(S + 1);
+      for (int r = 0; r < S; ++r) b[r] = q[r] * f;
+      b[S] = c->lev[l].n;
+      bnd[l] = b;
+      if (l < g)
+        for (int r = 0; r < S; ++r)
+          if (b[r + 1] - b[r] < std::max(8, std::max(c->lev[l].b, 2) + 2)) ok = false;
+    }
+    if (ok) break;
+    if (g == 1) throw Error(HD_ERR_INVALID, "row slabs: grid too small for " + std::to_string(S) + " slabs");
+  }
+  auto* sl = new hd_slabs();
+  c->slabs = sl;
+  sl->S = S;
+  sl->g = g;
+  sl->lv.resize(L);
+  for (int l = 0; l < L; ++l) {
+    SlabLevel& G = sl->lv[l];
+    G.n = c->lev[l].n;
+    G.b = c->lev[l].b;
+    G.H = std::max({G.b, c->fine.b, 2});
+    G.dist = l < g;
+    G.bounds = bnd[l];
+  }
+  sl->X.resize(g);
+  sl->Y.resize(g);
+  sl->B.resize(g);
+  sl->R.resize(g);
+  sl->cur.assign(L, 0);
+  for (int l = 0; l < g; ++l) {
+    sl->X[l] = slab_alloc(sl->lv[l], S);
+    sl->Y[l] = slab_alloc(sl->lv[l], S);
+    if (l > 0) sl->B[l] = slab_alloc(sl->lv[l], S);
+    sl->R[l] = slab_alloc(sl->lv[l], S);
+  }
+  for (auto* v : {&sl->f, &sl->w, &sl->t1, &sl->t2, &sl->t3, &sl->x, &sl->x0, &sl->rhsp, &sl->vin})
+    *v = slab_alloc(sl->lv[0], S);
+  sl->V.assign(S, nullptr);
+  sl->slots = dalloc<double>(S);
+  // Arnoldi grid per slab and the partials of all slabs
+  const size_t Nmax = static_cast<size_t>(*std::max_element(bnd[0].begin() + 1, bnd[0].end())) * c->n;
+  sl->Gs = std::max(1, std::min(c->lsa_G > 0 ? c->lsa_G : 296, static_cast<int>((Nmax + 1023) / 1024)));
+  sl->parts = dalloc<double2>(static_cast<size_t>(S) * sl->Gs * (2 * kLsaMaxJ + 2) + 8);
+  CK(cudaDeviceSynchronize());
+}
+
+static void destroy_slabs(hd_ctx* c) {
+  hd_slabs* sl = slabs_of(c);
+  if (!sl) return;
+  auto fr = [](std::vector<double2*>& v) {
+    for (auto* p : v) cudaFree(p);
+  };
+  for (auto& v : sl->X) fr(v);
+  for (auto& v : sl->Y) fr(v);
+  for (auto& v : sl->B) fr(v);
+  for (auto& v : sl->R) fr(v);
+  for (auto* v : {&sl->f, &sl->w, &sl->t1, &sl->t2, &sl->t3, &sl->x, &sl->x0, &sl->rhsp, &sl->vin, &sl->V}) fr(*v);
+  cudaFree(sl->slots);
+  cudaFree(sl->parts);
+  delete sl;
+  c->slabs = nullptr;
+}
+
 }  // namespace hd
 
 // ===========================================================================
@@ -2086,6 +2642,30 @@ hd_status hd_create(const hd_system* sys, const hd_precond* spec, const int* dev
   HD_GUARD_END
 }
 
+hd_status hd_create_slabs(const hd_system* sys, const hd_precond* spec, int nslabs, hd_ctx** out) {
+  HD_GUARD_BEGIN
+  if (!out || nslabs < 1) throw Error(HD_ERR_INVALID, "nslabs must be >= 1");
+  hd_ctx* c = nullptr;
+  create_ctx(sys, spec, nullptr, 0, &c);
+  try {
+    create_slabs(c, nslabs);
+  } catch (...) {
+    destroy_ctx(c);
+    throw;
+  }
+  *out = c;
+  HD_GUARD_END
+}
+
+int hd_slab_info(const hd_ctx* c, int* gather_level, int* bounds) {
+  if (!c || !c->slabs) return 0;
+  const hd_slabs* sl = reinterpret_cast<const hd_slabs*>(c->slabs);
+  if (gather_level) *gather_level = sl->g;
+  if (bounds)
+    for (int s = 0; s <= sl->S; ++s) bounds[s] = sl->lv[0].bounds[s];
+  return sl->S;
+}
+
 static hd_status solve_impl(hd_ctx* c, const hd_gmres* opt, const double* rhs, bool rhs_dev, double* x_out,
                             bool x_dev, double* residuals_out, hd_report* report) {
   HD_GUARD_BEGIN
@@ -2104,7 +2684,7 @@ static hd_status solve_impl(hd_ctx* c, const hd_gmres* opt, const double* rhs, b
     o.max_iterations = 1;
     ensure_gmres(c, 1);
   }
-  r = run_solve(c, *opt, xd);
+  r = c->slabs ? run_solve_slabs(c, *opt, c->f, xd) : run_solve(c, *opt, xd);
   if (!x_dev) CK(cudaMemcpyAsync(x_out, xd, N * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
   CK(cudaEventRecord(c->ev1, c->st));
   CK(cudaEventSynchronize(c->ev1));
@@ -2146,6 +2726,24 @@ hd_status hd_apply(hd_ctx* c, int which, const double* d_x, double* d_y) {
   CK(cudaSetDevice(c->device));
   const double2* x = reinterpret_cast<const double2*>(d_x);
   double2* yv = reinterpret_cast<double2*>(d_y);
+  if (c->slabs) {  // the row-slab operators: scatter, apply on the slabs, gather
+    hd_slabs* sl = slabs_of(c);
+    s_scatter(c, x, sl->vin);
+    switch (which) {
+      case HD_APPLY_A: s_apply(c, OP_APPLY, opA(c), sl->lv[0], sl->vin, nullptr, &sl->t3, 0.0); s_gather(c, sl->t3, yv); break;
+      case HD_APPLY_MG: s_mg_solve(c, sl->vin, sl->t2); s_gather(c, sl->t2, yv); break;
+      case HD_APPLY_PROJECT:
+        if (!c->spec.deflate) throw Error(HD_ERR_INVALID, "no deflation in this context");
+        s_deflate(c, sl->vin, sl->rhsp, true); s_gather(c, sl->rhsp, yv); break;
+      case HD_APPLY_Q:
+        if (!c->spec.deflate) throw Error(HD_ERR_INVALID, "no deflation in this context");
+        s_deflate(c, sl->vin, sl->rhsp, false); s_gather(c, sl->rhsp, yv); break;
+      case HD_APPLY_OP: s_op(c, sl->vin, sl->w); s_gather(c, sl->w, yv); break;
+      default: throw Error(HD_ERR_INVALID, "apply selector not available on row slabs");
+    }
+    CK(cudaStreamSynchronize(c->st));
+    return HD_OK;
+  }
   switch (which) {
     case HD_APPLY_A: op_apply(c, OP_APPLY, opA(c), x, nullptr, yv); break;
     case HD_APPLY_SHIFTED: op_apply(c, OP_APPLY, level_dev(c->fine, c->cM, c->corner, c->fine.genM), x, nullptr, yv); break;

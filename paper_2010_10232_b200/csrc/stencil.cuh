@@ -45,7 +45,8 @@ template <int B, int MODE>
 __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const double2* __restrict__ x,
                                                             const double2* __restrict__ bv,
                                                             double2* __restrict__ out, double omega, int RY,
-                                                            RedOut red, const int* xidx, size_t xstride) {
+                                                            RedOut red, const int* xidx, size_t xstride, int rb,
+                                                            int re) {
   constexpr int NB = 2 * B + 1;
   constexpr int W = kSW + 2 * B;
   constexpr int kSRing = stencil_ring<B>();
@@ -60,8 +61,11 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
   const int n = L.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int x0 = (blockIdx.x * kSWarps + warp) * kSW;
-  const int y0 = blockIdx.y * RY;
-  const int yend = min(y0 + RY, n);
+  // output rows [rb, re) (a row slab; the whole grid: 0, n).  Pointers are
+  // addressed with global rows: rows of a slab's halo are read through them,
+  // rows outside [0, n) are zero.
+  const int y0 = rb + blockIdx.y * RY;
+  const int yend = min(y0 + RY, re);
   const int nout = max(0, yend - y0);
   const int nin = nout + 2 * B;
   const int ix = x0 + lane;
@@ -182,7 +186,8 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
   }
   if (MODE == OP_RESNORM) {  // every thread of the CTA reaches this reduction
     double2 total;
-    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) / red.scale;
+    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total))
+      *red.dst = red.raw ? total.x : sqrt(total.x) / red.scale;
   }
 }
 

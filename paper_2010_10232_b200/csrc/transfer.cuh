@@ -29,13 +29,15 @@ struct ZW {
 // PLANAR: 0 interleaved output (outc), 1 planar (outp: re plane then im plane)
 template <int KIND, int PLANAR>
 __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* __restrict__ r, int nf, int nc,
-                                                    double2* __restrict__ outc, double* __restrict__ outp) {
+                                                    double2* __restrict__ outc, double* __restrict__ outp, int qb,
+                                                    int qe) {
   constexpr int lo = ZW<KIND>::lo, nw = ZW<KIND>::nw;
   constexpr int RR = 2 * kRQY + nw - 1;  // fine rows of the region
   constexpr int RC = 2 * kRQX + nw - 1;  // fine cols
   __shared__ double2 f[RR][RC + 1];
   __shared__ double2 tx[RR][kRQX];
-  const int qx0 = blockIdx.x * kRQX, qy0 = blockIdx.y * kRQY;
+  // coarse rows [qb, qe) (a row slab; whole grid: 0, nc), global row addressing
+  const int qx0 = blockIdx.x * kRQX, qy0 = qb + blockIdx.y * kRQY;
   const int fx0 = 2 * qx0 + lo, fy0 = 2 * qy0 + lo;
   for (int e = threadIdx.x; e < RR * RC; e += blockDim.x) {
     const int rr = e / RC, cc = e % RC;
@@ -58,7 +60,7 @@ __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* 
   for (int e = threadIdx.x; e < kRQY * kRQX; e += blockDim.x) {
     const int qy = e / kRQX, qx = e % kRQX;
     const int gy = qy0 + qy, gx = qx0 + qx;
-    if (gy >= nc || gx >= nc) continue;
+    if (gy >= qe || gx >= nc) continue;
     double2 s = cmk(0.0, 0.0);
 #pragma unroll
     for (int o = 0; o < nw; ++o) s = cfma_r(w[o], tx[2 * qy + o][qx], s);
@@ -120,11 +122,13 @@ __device__ __forceinline__ void ptaps(int i, double drop, double& w0, double& w1
 template <int KIND, int PMODE>
 __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* __restrict__ ec,
                                                    const double* __restrict__ ep, int nf, int nc,
-                                                   const double2* __restrict__ s, double2* __restrict__ out) {
+                                                   const double2* __restrict__ s, double2* __restrict__ out, int fb,
+                                                   int fe) {
   constexpr int CR = kPFY / 2 + 3, CC = kPFX / 2 + 3;
   __shared__ double2 cs[CR][CC];
   __shared__ double2 ty[kPFY][CC];  // y-interpolated coarse columns for every fine row of the tile
-  const int fx0 = blockIdx.x * kPFX, fy0 = blockIdx.y * kPFY;
+  // fine rows [fb, fe) (a row slab, fb even; whole grid: 0, nf), global row addressing
+  const int fx0 = blockIdx.x * kPFX, fy0 = fb + blockIdx.y * kPFY;
   const int qx0 = fx0 / 2 - 1, qy0 = fy0 / 2 - 1;  // region origin (may be -1)
   const size_t NC = (size_t)nc * nc;
   for (int e = threadIdx.x; e < CR * CC; e += blockDim.x) {
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
   for (int e = threadIdx.x; e < kPFY * kPFX; e += blockDim.x) {
     const int r = e / kPFX, cx = e % kPFX;
     const int fy = fy0 + r, fx = fx0 + cx;
-    if (fy >= nf || fx >= nf) continue;
+    if (fy >= fe || fx >= nf) continue;
     const int li = fx / 2 - qx0;
     double w0, w1, w2;
     ptaps<KIND>(fx, drop, w0, w1, w2);
@@ -171,16 +175,16 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
 
 // x = omega D^-1 b on a 2D level, 2D grid (no 64-bit div/mod per element)
 __global__ void __launch_bounds__(256) k_jacobi0_2d_t(LevelDev L, const double2* __restrict__ b,
-                                                      double2* __restrict__ out, double omega) {
+                                                      double2* __restrict__ out, double omega, int rb, int re) {
   const int n = L.n, NB = 2 * L.b + 1;
   const int ix = blockIdx.x * 64 + (threadIdx.x & 63);
-  const int iy0 = blockIdx.y * 16 + (threadIdx.x >> 6) * 4;
+  const int iy0 = rb + blockIdx.y * 16 + (threadIdx.x >> 6) * 4;
   if (ix >= n) return;
   const double mxx = L.M[(size_t)ix * NB + L.b], sxx = L.S[(size_t)ix * NB + L.b];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int iy = iy0 + r;
-    if (iy >= n) break;
+    if (iy >= re) break;
     const double my = L.M[(size_t)iy * NB + L.b], sy = L.S[(size_t)iy * NB + L.b];
     const double2 D = csub(cmk(my * sxx + sy * mxx, 0.0), cscale(my * mxx, L.c));
     const size_t g = (size_t)iy * n + ix;

@@ -410,3 +410,45 @@ def test_exact_shifted_inverse_C_ex(problem, p, k, beta2):
     ne = O.derived_elements(k, 0.625, p)
     r = _live(problem, p, ne, k, "C_ex", dict(beta2=beta2))
     assert r.converged
+
+
+# ---- row slabs ---------------------------------------------
+@pytest.mark.parametrize("S,ne,p,k,agg", [(2, 130, 3, 60.0, 40), (3, 200, 2, 100.0, 60), (4, 320, 2, 200.0, 200),
+                                          (8, 256, 2, 120.0, 40)])
+def test_row_slabs_match_single_domain(S, ne, p, k, agg, monkeypatch):
+    """The slab program (halo'd slab buffers, halo copies, gathered coarse levels
+    and E, slab-order reductions) on one device against the single-domain solve:
+    components to 1e-10, equal iterations and counts, history 1e-10, solution 1e-8."""
+    import torch
+    monkeypatch.setenv("HD_SLAB_AGGLOMERATE", str(agg))
+    s = hd.assemble(hd.point_source_2d(ne, p, k))
+    spec = hd.to_spec("DC_MG", p, k, **BASE)
+    rng = np.random.default_rng(5)
+    v = rng.uniform(-1, 1, s.size) + 1j * rng.uniform(-1, 1, s.size)
+    xd = torch.from_numpy(v).cuda()
+    with hd.Solver(s, spec) as one, hd.Solver(s, spec, slabs=S) as sl:
+        assert sl.slabs == S and sl.slab_bounds[0] == 0 and sl.slab_bounds[-1] == s.per_dim
+        assert 1 <= sl.slab_gather_level < sl.levels
+        for which, tol in ((hd.HD_APPLY_A, 1e-14), (hd.HD_APPLY_MG, 1e-12), (hd.HD_APPLY_Q, 1e-10),
+                           (hd.HD_APPLY_PROJECT, 1e-10), (hd.HD_APPLY_OP, 1e-10)):
+            y1, y2 = torch.zeros_like(xd), torch.zeros_like(xd)
+            one.apply(which, xd.data_ptr(), y1.data_ptr())
+            sl.apply(which, xd.data_ptr(), y2.data_ptr())
+            a, b = y1.cpu().numpy(), y2.cpu().numpy()
+            assert np.linalg.norm(a - b) <= tol * np.linalg.norm(a), (which, np.linalg.norm(a - b) / np.linalg.norm(a))
+        r1 = one.solve(hd.GmresOptions(100, 1e-7))
+        r2 = sl.solve(hd.GmresOptions(100, 1e-7))
+    assert r2.converged == r1.converged and r2.iterations == r1.iterations
+    assert (r2.counts.matvecs, r2.counts.coarse_solves, r2.counts.shift_solves, r2.counts.vcycles) == \
+        (r1.counts.matvecs, r1.counts.coarse_solves, r1.counts.shift_solves, r1.counts.vcycles)
+    assert np.max(np.abs(np.array(r2.residuals) - np.array(r1.residuals))) <= 1e-10
+    assert np.linalg.norm(r2.solution - r1.solution) <= 1e-8 * np.linalg.norm(r1.solution)
+
+
+def test_row_slabs_reject_unsupported():
+    s = hd.assemble(hd.point_source_1d(80, 2, 50.0))
+    with pytest.raises(hd.HelmdefError):
+        hd.Solver(s, hd.to_spec("DC_MG", 2, 50.0, **BASE), slabs=2)
+    s2 = hd.assemble(hd.point_source_2d(40, 2, 20.0))
+    with pytest.raises(hd.HelmdefError):
+        hd.Solver(s2, hd.to_spec("DC_MG", 2, 20.0, **BASE), slabs=16)  # slabs thinner than the halo
