@@ -37,8 +37,17 @@ CONFIGS = {
     "C1": (1, 2, 80, 50.0),
     "C2": (1, 4, 31623, 1000.0),
     "C3": (2, 2, 320, 200.0),
+    "C4": (2, 3, 480, 150.0),   # three-layer wedge k0 = 150 (oracle extension)
     "C5": (2, 3, 1600, 1000.0),
 }
+
+
+def make_problem(mod, cfg):
+    """The config's problem from `mod` (the device package or the oracle)."""
+    dim, p, ne, k = CONFIGS[cfg]
+    if cfg == "C4":
+        return mod.wedge_2d(ne, p, k)
+    return mod.point_source_2d(ne, p, k) if dim == 2 else mod.point_source_1d(ne, p, k)
 SPEC = dict(tag="DC_MG", beta2="0.5", cycles=1, smoothing=1, omega=2.0 / 3.0)
 TOL, MAXIT = 1e-7, 100
 
@@ -67,6 +76,9 @@ def rank_reduce(dist, t_ms, work, device="cpu"):
 
 def workload_name(cfg):
     dim, p, ne, k = CONFIGS[cfg]
+    if cfg == "C4":
+        return (f"C4: 2D IgA Helmholtz, three-layer wedge k0={k:g} (1.2/1.5/1.0), source (0.5, 1-h), p={p}, "
+                f"{ne}^2 elements, DC_MG^1 (beta2=0.5, omega=2/3, nu=1), GMRES tol 1e-7")
     return f"{cfg}: {dim}D IgA Helmholtz point source, k={k:g}, p={p}, {ne}^{dim} elements, DC_MG^1 (beta2=0.5, omega=2/3, nu=1), GMRES tol 1e-7"
 
 
@@ -78,13 +90,14 @@ def oracle_sample(cfg, iters, warm=0):
     on the host; returns (iterations/s, seconds, note)."""
     from oracle import helmdef_oracle as O
     dim, p, ne, k = CONFIGS[cfg]
-    pb = O.point_source_2d(ne, p, k) if dim == 2 else O.point_source_1d(ne, p, k)
+    pb = make_problem(O, cfg)
     spec = O.to_spec(SPEC["tag"], p, k, beta2=SPEC["beta2"], cycles=SPEC["cycles"],
                      smoothing=SPEC["smoothing"], omega=SPEC["omega"])
     t0 = time.perf_counter()
     s = O.assemble(pb)
-    big = dim == 2 and s.A.shape[0] > 300_000
-    setup = O.compose(s, spec, galerkin="kron" if dim == 2 else "sparse", e_solver="fd" if big else "splu")
+    big = dim == 2 and s.A.shape[0] > 300_000 and s.separable
+    setup = O.compose(s, spec, galerkin="kron" if dim == 2 and s.separable else "sparse",
+                      e_solver="fd" if big else "splu")
     t_setup = time.perf_counter() - t0
     gen = O.gmres_steps(setup.op, setup.rhs, setup.start, setup.monitor, O.GmresOptions(MAXIT, TOL))
     done = 0
@@ -203,8 +216,7 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     dim, p, ne, k = CONFIGS[args.config]
-    pb = hd.point_source_2d(ne, p, k) if dim == 2 else hd.point_source_1d(ne, p, k)
-    sys_ = hd.assemble(pb)
+    sys_ = hd.assemble(make_problem(hd, args.config))
     spec = hd.to_spec(SPEC["tag"], p, k, beta2=SPEC["beta2"], cycles=SPEC["cycles"], smoothing=SPEC["smoothing"],
                       omega=SPEC["omega"])
     opt = hd.GmresOptions(MAXIT, TOL)

@@ -43,8 +43,12 @@ typedef enum {
   HD_ERR_NO_DEVICE = 4    /* no CUDA device: there is no CPU fallback       */
 } hd_status;
 
-/* Wave-number field kinds (WaveField, inc/problems.hpp:18-29). */
-enum { HD_FIELD_CONSTANT = 0, HD_FIELD_LAYERED = 1 };
+/* Wave-number field kinds (WaveField, inc/problems.hpp:18-29), plus the
+ * BASELINE config-4 wedge, which the reference's WaveField cannot express
+ * (SURVEY.md §0 C8): three layers split by two lines, K2 integrated with the
+ * reference's (p+1)-point Gauss rule per direction and k(x,y)^2 sampled at the
+ * Gauss points (oracle/helmdef_oracle.py wedge_2d freezes the same rule). */
+enum { HD_FIELD_CONSTANT = 0, HD_FIELD_LAYERED = 1, HD_FIELD_WEDGE = 2 };
 
 /* Model problem (helmdef::Problem, inc/problems.hpp:50-60) restricted to the
  * iteration-study problems: point_source_1d / point_source_2d /
@@ -55,7 +59,13 @@ typedef struct {
   int elements;         /* elements per direction                            */
   double k;             /* base wave number                                  */
   int field_kind;       /* HD_FIELD_*                                         */
-  double multipliers[16]; /* layered: block(bx,by) = multipliers[4*by+bx]     */
+  double multipliers[16]; /* layered: block(bx,by) = multipliers[4*by+bx];
+                             wedge: [0..2] = top, middle, bottom layer        */
+  double lines[4];      /* wedge: top iff y > lines[0] + lines[1] x, else middle
+                           iff y > lines[2] + lines[3] x, else bottom          */
+  int point_source;     /* 0: load at (1/2, 1/2) as the reference
+                           (src/assembly.cpp:251-256); 1: at source[]       */
+  double source[2];     /* (x_s, y_s) when point_source = 1                   */
 } hd_problem;
 
 /* Discrete system as the device consumes it (DiscreteSystem,
@@ -63,6 +73,7 @@ typedef struct {
  *   A      = kron(M1, S1) + kron(S1, M1) - K2,
  *   K2     = k^2 kron(M1, M1)                          (constant field)
  *          = sum_{by,bx} (k m_{by,bx})^2 kron(B_by, B_bx) (layered field),
+ *          = shift_mass_2d as a general 2D stencil           (wedge field),
  * for dim = 1, A = S1 - k^2 M1 (+ corner at (n-1, n-1)).  Bands are reduced
  * (Dirichlet rows dropped), per_dim x (2*order+1), row-major,
  * band[i*(2p+1) + (j-i+p)] = X(i, j). */
@@ -78,6 +89,10 @@ typedef struct {
   const double* mass_band;        /* M1                                    */
   const double* interval_mass;    /* layered: 4 bands B_0..B_3 (else NULL)  */
   double corner_re, corner_im;    /* 1D only: added to A(n-1,n-1)          */
+  /* wedge (any non-separable K2): K2 as a 2D stencil, N x (2p+1)^2 doubles,
+   * shift_mass_2d[(iy*n+ix)*(2p+1)^2 + (dy+p)*(2p+1) + (dx+p)]
+   *   = K2(iy*n+ix, (iy+dy)*n + ix+dx), zero where the neighbour is outside.  */
+  const double* shift_mass_2d;
 } hd_system;
 
 /* PrecondSpec (inc/precond.hpp:122-130) plus MultigridOptions::coarsest
@@ -127,6 +142,10 @@ int hd_problem_per_dim(const hd_problem* pb);
  * rhs: 2*per_dim^dim doubles (interleaved complex). */
 hd_status hd_assemble(const hd_problem* pb, double* stiffness_band, double* mass_band,
                       double* interval_mass, double* rhs);
+
+/* Non-separable K2 of a wedge problem as the 2D stencil hd_system.shift_mass_2d
+ * expects (N x (2p+1)^2 doubles, N = per_dim^2). */
+hd_status hd_assemble_field(const hd_problem* pb, double* shift_mass_2d);
 
 /* ---- the drop-in solver ------------------------------------------------ */
 

@@ -36,10 +36,11 @@ LIB_PATH = Path(os.environ["HD_LIBRARY"]) if os.environ.get("HD_LIBRARY") else _
 
 HD_FIELD_CONSTANT = 0
 HD_FIELD_LAYERED = 1
+HD_FIELD_WEDGE = 2
 HD_APPLY_A, HD_APPLY_SHIFTED, HD_APPLY_MG, HD_APPLY_PROJECT, HD_APPLY_OP, HD_APPLY_Q = range(6)
 
 # Every symbol include/helmdef_b200.h declares (checked by tests/test_capi.py).
-EXPORTS = ["hd_problem_per_dim", "hd_assemble", "hd_create", "hd_solve", "hd_solve_device", "hd_size",
+EXPORTS = ["hd_problem_per_dim", "hd_assemble", "hd_assemble_field", "hd_create", "hd_solve", "hd_solve_device", "hd_size",
            "hd_levels", "hd_apply", "hd_debug_level", "hd_level_size", "hd_set_stream", "hd_profile",
            "hd_profile_read", "hd_destroy", "hd_last_error", "hd_create_slabs", "hd_slab_info"]
 KERNEL_KINDS = ["op_fine", "op_coarse", "jacobi0", "transfer", "exact", "mgs", "iterate", "vec", "givens",
@@ -48,14 +49,16 @@ KERNEL_KINDS = ["op_fine", "op_coarse", "jacobi0", "transfer", "exact", "mgs", "
 
 class HdProblem(C.Structure):
     _fields_ = [("dim", C.c_int), ("order", C.c_int), ("elements", C.c_int), ("k", C.c_double),
-                ("field_kind", C.c_int), ("multipliers", C.c_double * 16)]
+                ("field_kind", C.c_int), ("multipliers", C.c_double * 16), ("lines", C.c_double * 4),
+                ("point_source", C.c_int), ("source", C.c_double * 2)]
 
 
 class HdSystem(C.Structure):
     _fields_ = [("dim", C.c_int), ("order", C.c_int), ("elements", C.c_int), ("per_dim", C.c_int),
                 ("field_kind", C.c_int), ("k", C.c_double), ("multipliers", C.c_double * 16),
                 ("stiffness_band", C.POINTER(C.c_double)), ("mass_band", C.POINTER(C.c_double)),
-                ("interval_mass", C.POINTER(C.c_double)), ("corner_re", C.c_double), ("corner_im", C.c_double)]
+                ("interval_mass", C.POINTER(C.c_double)), ("corner_re", C.c_double), ("corner_im", C.c_double),
+                ("shift_mass_2d", C.POINTER(C.c_double))]
 
 
 class HdPrecond(C.Structure):
@@ -91,6 +94,8 @@ def load_library() -> C.CDLL:
     lib.hd_problem_per_dim.restype = C.c_int
     lib.hd_assemble.argtypes = [C.POINTER(HdProblem), dp, dp, dp, dp]
     lib.hd_assemble.restype = C.c_int
+    lib.hd_assemble_field.argtypes = [C.POINTER(HdProblem), dp]
+    lib.hd_assemble_field.restype = C.c_int
     lib.hd_create.argtypes = [C.POINTER(HdSystem), C.POINTER(HdPrecond), C.POINTER(C.c_int), C.c_int,
                               C.POINTER(C.c_void_p)]
     lib.hd_create.restype = C.c_int
@@ -163,6 +168,15 @@ class Problem:
     k: float
     layered: bool = False
     multipliers: List[float] = field(default_factory=lambda: [1.0] * 16)
+    wedge: bool = False
+    wedge_lines: List[float] = field(default_factory=lambda: list(WEDGE_LINES))
+    source_xy: Optional[List[float]] = None   # None: (1/2, 1/2), the reference's load
+
+
+# BASELINE config 4 (an extension: the reference's WaveField cannot express it,
+# SURVEY.md §0 C8): top iff y > 0.6 - 0.2x, middle iff y > 0.3 + 0.1x, else bottom.
+WEDGE_LINES = [0.6, -0.2, 0.3, 0.1]
+WEDGE_MULTIPLIERS = [1.2, 1.5, 1.0]
 
 
 def point_source_1d(elements, order, k):
@@ -178,6 +192,14 @@ def layered_medium_2d(elements, order, k, multipliers=None):
                    list(multipliers or LAYERED_MULTIPLIERS))
 
 
+def wedge_2d(elements, order, k0, multipliers=None, lines=None, source_xy=None):
+    """BASELINE config 4: three-layer wedge k = k0 * (top, middle, bottom), point
+    source at (0.5, 1 - h) by default (oracle/helmdef_oracle.py wedge_2d)."""
+    src = list(source_xy) if source_xy is not None else [0.5, 1.0 - 1.0 / elements]
+    return Problem("wedge_2d", 2, order, elements, float(k0), False,
+                   list(multipliers or WEDGE_MULTIPLIERS) + [0.0] * 13, True, list(lines or WEDGE_LINES), src)
+
+
 @dataclass
 class DiscreteSystem:
     """DiscreteSystem (inc/assembly.hpp:43-52) in the factored form the device
@@ -189,6 +211,7 @@ class DiscreteSystem:
     mass_band: np.ndarray
     rhs: np.ndarray                # complex128, per_dim**dim
     interval_mass: Optional[np.ndarray] = None
+    shift_mass_2d: Optional[np.ndarray] = None   # wedge: K2 stencil, N x (2p+1)^2
 
     @property
     def dim(self):
@@ -202,9 +225,14 @@ class DiscreteSystem:
 def _hd_problem(pb: Problem) -> HdProblem:
     h = HdProblem()
     h.dim, h.order, h.elements, h.k = pb.dim, pb.order, pb.elements, pb.k
-    h.field_kind = HD_FIELD_LAYERED if pb.layered else HD_FIELD_CONSTANT
+    h.field_kind = HD_FIELD_WEDGE if pb.wedge else (HD_FIELD_LAYERED if pb.layered else HD_FIELD_CONSTANT)
     for i, m in enumerate(pb.multipliers):
         h.multipliers[i] = m
+    for i, v in enumerate(pb.wedge_lines):
+        h.lines[i] = v
+    if pb.source_xy is not None:
+        h.point_source = 1
+        h.source[0], h.source[1] = pb.source_xy
     return h
 
 
@@ -220,7 +248,11 @@ def assemble(pb: Problem) -> DiscreteSystem:
     rhs = np.zeros(n ** pb.dim, dtype=np.complex128)
     _check(lib.hd_assemble(C.byref(h), _dp(S), _dp(M), _dp(IM) if IM is not None else None,
                            rhs.view(np.float64).ctypes.data_as(C.POINTER(C.c_double))))
-    return DiscreteSystem(pb, n, S, M, rhs, IM)
+    K2 = None
+    if pb.wedge:
+        K2 = np.zeros((n * n, nb * nb))
+        _check(lib.hd_assemble_field(C.byref(h), _dp(K2)))
+    return DiscreteSystem(pb, n, S, M, rhs, IM, K2)
 
 
 # ---------------------------------------------------------------------------
@@ -322,7 +354,7 @@ class Solver:
         pb = sys_.problem
         h = HdSystem()
         h.dim, h.order, h.elements, h.per_dim = pb.dim, pb.order, pb.elements, sys_.per_dim
-        h.field_kind = HD_FIELD_LAYERED if pb.layered else HD_FIELD_CONSTANT
+        h.field_kind = HD_FIELD_WEDGE if pb.wedge else (HD_FIELD_LAYERED if pb.layered else HD_FIELD_CONSTANT)
         h.k = pb.k
         for i, m in enumerate(pb.multipliers):
             h.multipliers[i] = m
@@ -333,6 +365,9 @@ class Solver:
         if sys_.interval_mass is not None:
             self._IM = np.ascontiguousarray(sys_.interval_mass)
             h.interval_mass = _dp(self._IM)
+        if sys_.shift_mass_2d is not None:
+            self._K2 = np.ascontiguousarray(sys_.shift_mass_2d)
+            h.shift_mass_2d = _dp(self._K2)
         p = HdPrecond(int(spec.deflate), spec.drop, int(spec.shift), spec.beta2, spec.cycles,
                       spec.smooth_steps, spec.omega, spec.coarsest)
         ctx = C.c_void_p()

@@ -167,6 +167,79 @@ Band mass_on_interval(const Knots& kv, double x0, double x1) {
   return out;
 }
 
+double wedge_k2(double x, double y, double k0, const double* mult, const double* lines) {
+  const double m = y > lines[0] + lines[1] * x ? mult[0] : (y > lines[2] + lines[3] * x ? mult[1] : mult[2]);
+  const double kk = k0 * m;
+  return kk * kk;
+}
+
+std::vector<double> wedge_mass_stencil(const Knots& kv, double k0, const double* mult, const double* lines,
+                                       const std::vector<int>& kept) {
+  const int p = kv.degree, m = p + 1, ne = kv.elements, nb = kv.basis_count(), NB = 2 * p + 1;
+  std::vector<double> nodes, weights;
+  gauss_legendre(m, nodes, weights);
+  const double h = 1.0 / ne;
+  // Gauss points, weights and the p+1 nonzero basis values of every element
+  std::vector<double> X(static_cast<size_t>(ne) * m), W(X.size()), B(X.size() * m);
+  for (int e = 0; e < ne; ++e)
+    for (int q = 0; q < m; ++q) {
+      const double x = e * h + 0.5 * h * (nodes[q] + 1.0);
+      X[e * m + q] = x;
+      W[e * m + q] = 0.5 * h * weights[q];
+      for (int l = 0; l < m; ++l) B[(static_cast<size_t>(e) * m + q) * m + l] = bspline_value(kv, p, e + l, x);
+    }
+  // full-basis band table K[iy][dy][ix][dx]
+  const size_t rowsz = static_cast<size_t>(NB) * nb * NB;
+  std::vector<double> K(static_cast<size_t>(nb) * rowsz, 0.0);
+  std::vector<double> T(static_cast<size_t>(m) * m * m);  // T[qy][lx][mx] of one element
+  for (int ey = 0; ey < ne; ++ey)
+    for (int ex = 0; ex < ne; ++ex) {
+      // x stage: T[qy][lx][mx] = sum_qx w_qx k^2 B[ex,qx,lx] B[ex,qx,mx]
+      for (int qy = 0; qy < m; ++qy)
+        for (int lx = 0; lx < m; ++lx)
+          for (int mx = 0; mx < m; ++mx) {
+            double t = 0.0;
+            for (int qx = 0; qx < m; ++qx) {
+              const double kk = wedge_k2(X[ex * m + qx], X[ey * m + qy], k0, mult, lines);
+              t += kk * W[ex * m + qx] * B[(static_cast<size_t>(ex) * m + qx) * m + lx] *
+                   B[(static_cast<size_t>(ex) * m + qx) * m + mx];
+            }
+            T[(qy * m + lx) * m + mx] = t;
+          }
+      // y stage into the band table
+      for (int ly = 0; ly < m; ++ly)
+        for (int my = 0; my < m; ++my)
+          for (int lx = 0; lx < m; ++lx)
+            for (int mx = 0; mx < m; ++mx) {
+              double v = 0.0;
+              for (int qy = 0; qy < m; ++qy)
+                v += W[ey * m + qy] * B[(static_cast<size_t>(ey) * m + qy) * m + ly] *
+                     B[(static_cast<size_t>(ey) * m + qy) * m + my] * T[(qy * m + lx) * m + mx];
+              K[static_cast<size_t>(ey + ly) * rowsz + (static_cast<size_t>(my - ly + p) * nb + ex + lx) * NB +
+                (mx - lx + p)] += v;
+            }
+    }
+  // reduce to the kept basis (contiguous in this build: Dirichlet on all faces)
+  const int n = static_cast<int>(kept.size());
+  std::vector<double> out(static_cast<size_t>(n) * n * NB * NB, 0.0);
+  for (int iy = 0; iy < n; ++iy)
+    for (int dy = -p; dy <= p; ++dy) {
+      const int jy = iy + dy;
+      if (jy < 0 || jy >= n) continue;
+      for (int ix = 0; ix < n; ++ix)
+        for (int dx = -p; dx <= p; ++dx) {
+          const int jx = ix + dx;
+          if (jx < 0 || jx >= n) continue;
+          const int fy = kept[iy], fx = kept[ix];
+          const int gy = kept[jy] - fy, gx = kept[jx] - fx;
+          if (gy < -p || gy > p || gx < -p || gx > p) continue;
+          out[(static_cast<size_t>(iy) * n + ix) * NB * NB + (dy + p) * NB + (dx + p)] =
+              K[static_cast<size_t>(fy) * rowsz + (static_cast<size_t>(gy + p) * nb + fx) * NB + (gx + p)];
+        }
+    }
+  return out;
+}
+
 Band reduce(const Band& full, const std::vector<int>& kept) {
   const int n = static_cast<int>(kept.size());
   Band out(n, full.b);

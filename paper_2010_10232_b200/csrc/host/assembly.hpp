@@ -35,6 +35,18 @@ Forms1d assemble_forms_1d(int elements, int order);
 /// Mass restricted to [x0, x1] (own Gauss rule per element overlap).
 Band mass_on_interval(const Knots& kv, double x0, double x1);
 
+/// Wedge field (BASELINE config 4; an oracle extension, the reference's WaveField
+/// cannot express it): top iff y > l[0] + l[1] x, else middle iff y > l[2] + l[3] x,
+/// else bottom; k = k0 * mult[layer].
+double wedge_k2(double x, double y, double k0, const double* mult, const double* lines);
+
+/// K2 = sum_e sum_(qy,qx) w w k(x_q, y_q)^2 phi phi with the (p+1)-point Gauss rule
+/// per direction (src/assembly.cpp:23-43 applied pointwise), on the basis kept in
+/// both directions, as a 2D stencil out[(iy*n+ix)*NB*NB + (dy+p)*NB + (dx+p)],
+/// NB = 2p+1, n = kept.size().
+std::vector<double> wedge_mass_stencil(const Knots& kv, double k0, const double* mult, const double* lines,
+                                       const std::vector<int>& kept);
+
 /// Drop rows/cols not in `kept` (Dirichlet elimination).
 Band reduce(const Band& full, const std::vector<int>& kept);
 

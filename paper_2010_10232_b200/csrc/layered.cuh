@@ -16,6 +16,15 @@
 // layered hierarchy (deflation E, coarsest level) are dense inverses built by
 // k_dense_kron + cuSOLVER getrf/getrs; they are not Kronecker sums, so the fast
 // diagonalisation of the constant field does not apply.
+//
+// Wedge field (BASELINE config 4, non-separable K2): the level operator is the
+// Kronecker-sum part My (x) Sx + Sy (x) My (G = 2 groups) plus a stored 2D stencil
+//
+//   L += kc * K_l ,  K_l = (z (x) z)^T K_{l-1} (z (x) z)   (Galerkin, host),
+//
+// with kc = -1 (A) or -(1 - i beta2) (shifted).  K_l is held as (2b+1)^2 planes
+// of n^2 doubles (plane t = (dy+b)(2b+1) + dx+b), so a warp's loads of one tap are
+// coalesced; the kernel adds it from the same staged input tile.
 #pragma once
 
 #include "kernels.cuh"
@@ -30,7 +39,22 @@ struct GenLevel {
   const double* Y[kGenMaxG];  // n x (2b+1) band rows (y factor of group g)
   const double* X[kGenMaxG];  // n x (2b+1) band rows (x factor)
   double2 coef[kGenMaxG];
+  const double* K;  // stored stencil planes (wedge), or null
+  double2 kc;       // coefficient of the stored stencil
 };
+
+// Entry (r, s) of the level operator, r = iy*n+ix, s = (iy+dy)*n + ix+dx, |dy|,|dx| <= b.
+__device__ __forceinline__ double2 gen_entry(const GenLevel& L, int iy, int ix, int dy, int dx) {
+  const int NB = 2 * L.b + 1;
+  double2 v = cmk(0.0, 0.0);
+  for (int g = 0; g < L.G; ++g)
+    v = cadd(v, cscale(L.Y[g][(size_t)iy * NB + dy + L.b] * L.X[g][(size_t)ix * NB + dx + L.b], L.coef[g]));
+  if (L.K) {
+    const size_t NN = (size_t)L.n * L.n;
+    v = cadd(v, cscale(L.K[(size_t)((dy + L.b) * NB + dx + L.b) * NN + (size_t)iy * L.n + ix], L.kc));
+  }
+  return v;
+}
 
 __host__ __device__ constexpr size_t gen_smem(int b, int G) {
   return sizeof(double2) * ((size_t)(kGenTY + 2 * b) * (kGenTX + 2 * b) + (size_t)G * (kGenTY + 2 * b) * kGenTX);
@@ -82,6 +106,16 @@ __global__ void __launch_bounds__(kGenThreads) k_kron2d(GenLevel L, const double
       y = cadd(y, cmul(L.coef[g], t));
     }
     const size_t gi = (size_t)iy * n + ix;
+    if (L.K) {
+      const size_t NN = (size_t)n * n;
+      double2 t = cmk(0.0, 0.0);
+      const double* Kp = L.K + gi;
+      for (int dy = 0; dy < NB; ++dy) {
+        const double2* xr = xs + (r + dy) * RW + c;
+        for (int dx = 0; dx < NB; ++dx) t = cfma_r(__ldg(Kp + (size_t)(dy * NB + dx) * NN), xr[dx], t);
+      }
+      y = cadd(y, cmul(L.kc, t));
+    }
     if (MODE == OP_APPLY) {
       out[gi] = y;
     } else if (MODE == OP_RESID) {
@@ -92,6 +126,7 @@ __global__ void __launch_bounds__(kGenThreads) k_kron2d(GenLevel L, const double
       double2 D = cmk(0.0, 0.0);
       for (int g = 0; g < G; ++g)
         D = cadd(D, cscale(__ldg(L.Y[g] + (size_t)iy * NB + b) * __ldg(L.X[g] + (size_t)ix * NB + b), L.coef[g]));
+      if (L.K) D = cadd(D, cscale(__ldg(L.K + (size_t)(b * NB + b) * ((size_t)n * n) + gi), L.kc));
       out[gi] = cadd(xs[(r + b) * RW + c + b], cscale(omega, cmul(cinv(D), csub(bv[gi], y))));
     }
   }
@@ -108,9 +143,7 @@ __global__ void __launch_bounds__(256) k_jacobi0_gen(GenLevel L, const double2* 
   const size_t NN = (size_t)n * n;
   for (size_t gi = blockIdx.x * (size_t)blockDim.x + threadIdx.x; gi < NN; gi += (size_t)gridDim.x * blockDim.x) {
     const int iy = (int)(gi / n), ix = (int)(gi % n);
-    double2 D = cmk(0.0, 0.0);
-    for (int g = 0; g < L.G; ++g)
-      D = cadd(D, cscale(L.Y[g][(size_t)iy * NB + L.b] * L.X[g][(size_t)ix * NB + L.b], L.coef[g]));
+    const double2 D = gen_entry(L, iy, ix, 0, 0);
     out[gi] = cscale(omega, cmul(cinv(D), bv[gi]));
   }
 }
@@ -124,11 +157,7 @@ __global__ void k_dense_kron(GenLevel L, double2* __restrict__ A) {
     const size_t row = e % NN, col = e / NN;
     const int iy = (int)(row / n), ix = (int)(row % n), jy = (int)(col / n), jx = (int)(col % n);
     const int dy = jy - iy, dx = jx - ix;
-    double2 v = cmk(0.0, 0.0);
-    if (dy >= -b && dy <= b && dx >= -b && dx <= b)
-      for (int g = 0; g < L.G; ++g)
-        v = cadd(v, cscale(L.Y[g][(size_t)iy * NB + dy + b] * L.X[g][(size_t)ix * NB + dx + b], L.coef[g]));
-    A[e] = v;
+    A[e] = (dy >= -b && dy <= b && dx >= -b && dx <= b) ? gen_entry(L, iy, ix, dy, dx) : cmk(0.0, 0.0);
   }
 }
 

@@ -33,6 +33,7 @@
 #include "arnoldi.cuh"
 #include "arnoldi_lowsync.cuh"
 #include "layered.cuh"
+#include "btri.cuh"
 #include "segsolve.cuh"
 #include "ysolve.cuh"
 
@@ -115,6 +116,10 @@ struct ExactSolver {
   size_t NN = 0;
   double2* Ainv = nullptr;   // NN x NN column-major
   double2 *dx = nullptr, *dy = nullptr;
+  // block tridiagonal (btri.cuh): real non-Kronecker operators too large for a dense inverse
+  bool btri = false;
+  BtriArgs bt{};
+  int bt_kr = 0;
 };
 
 }  // namespace hd
@@ -630,6 +635,10 @@ static void free_exact(ExactSolver& X) {
     cudaFree(X.seg.Dl); cudaFree(X.seg.X0); cudaFree(X.seg.Xb);
   }
   cudaFree(X.Ainv); cudaFree(X.dx); cudaFree(X.dy);
+  if (X.btri) {
+    cudaFree(const_cast<double*>(X.bt.GT)); cudaFree(const_cast<double*>(X.bt.SinvT));
+    cudaFree(const_cast<double*>(X.bt.HT)); cudaFree(X.bt.y); cudaFree(X.bt.bar);
+  }
   X = ExactSolver{};
 }
 
@@ -930,6 +939,42 @@ static void dense_apply(hd_ctx* c, const ExactSolver& X, const double2* x, doubl
   launched(c, HD_K_LIBGEMM, mk, 16.0 * X.NN * X.NN, true);
 }
 
+// Block tridiagonal exact solve (btri.cuh), in/out planar.
+template <int KR>
+static void btri_launch_t(hd_ctx* c, ExactSolver& X) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_btri_solve<KR>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c->n_sms);
+  cfg.blockDim = dim3(btri_threads(KR));
+  cfg.stream = c->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_btri_solve<KR>, X.bt));
+}
+
+static void btri_solve(hd_ctx* c, ExactSolver& X, double* inout) {
+  X.bt.io = inout;
+  CK(cudaMemsetAsync(X.bt.bar, 0, sizeof(unsigned), c->st));
+  const double mm = static_cast<double>(X.bt.m) * X.bt.m;
+  HD_LAUNCH(HD_K_EXACT, 8.0 * mm * (3.0 * X.bt.nb - 2.0) + 32.0 * X.bt.NN,
+            switch (X.bt_kr) {
+              case 8: btri_launch_t<8>(c, X); break;
+              case 16: btri_launch_t<16>(c, X); break;
+              case 24: btri_launch_t<24>(c, X); break;
+              case 32: btri_launch_t<32>(c, X); break;
+              case 48: btri_launch_t<48>(c, X); break;
+              case 64: btri_launch_t<64>(c, X); break;
+              default: btri_launch_t<96>(c, X); break;
+            });
+}
+
 // Exact solve: in/out planar (2D FD) or via the banded LU (1D).
 template <int KL>
 static void ysolve_launch_t(hd_ctx* c, const YArgs& a) {
@@ -970,6 +1015,10 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
     // out = V [Yre | Yim]
     CKB(cublasDgemm(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, X.T1, np, &zero, inout, n));
     launched(c, HD_K_LIBGEMM, mk, gb, true);
+    return;
+  }
+  if (X.btri) {
+    btri_solve(c, X, inout);
     return;
   }
   if (X.dense) {
@@ -1683,7 +1732,61 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
 // ---------------------------------------------------------------------------
 struct GenHost {
   std::vector<Band> Y, X;
+  // wedge: stored 2D stencil K[(iy*n+ix)*(2kb+1)^2 + (dy+kb)*(2kb+1) + dx+kb] (kb < 0: none)
+  std::vector<double> K;
+  int kb = -1;
 };
+
+// Galerkin product (z (x) z)^T K (z (x) z) of a 2D stencil (the reference's
+// sparse triple product Z^T M Z, src/precond.cpp:119, in stencil form).
+static void galerkin_stencil2d(const std::vector<double>& K, int n, int b, const Transfer& z, std::vector<double>& Kc,
+                               int& bc) {
+  const int nc = z.coarse;
+  std::vector<std::vector<std::pair<int, double>>> par(n);
+  for (size_t t = 0; t < z.w.size(); ++t) par[z.row[t]].push_back({z.col[t], z.w[t]});
+  bc = 0;
+  for (int i = 0; i < n; ++i)
+    for (int d = -b; d <= b; ++d) {
+      const int j = i + d;
+      if (j < 0 || j >= n) continue;
+      for (const auto& I : par[i])
+        for (const auto& J : par[j]) bc = std::max(bc, std::abs(J.first - I.first));
+    }
+  const int NB = 2 * b + 1, NBc = 2 * bc + 1;
+  Kc.assign(static_cast<size_t>(nc) * nc * NBc * NBc, 0.0);
+  for (int iy = 0; iy < n; ++iy)
+    for (int ix = 0; ix < n; ++ix)
+      for (int dy = -b; dy <= b; ++dy) {
+        const int jy = iy + dy;
+        if (jy < 0 || jy >= n) continue;
+        for (int dx = -b; dx <= b; ++dx) {
+          const int jx = ix + dx;
+          if (jx < 0 || jx >= n) continue;
+          const double v = K[(static_cast<size_t>(iy) * n + ix) * NB * NB + (dy + b) * NB + (dx + b)];
+          if (v == 0.0) continue;
+          for (const auto& Iy : par[iy])
+            for (const auto& Jy : par[jy]) {
+              const double vy = Iy.second * v * Jy.second;
+              const int oy = Jy.first - Iy.first + bc;
+              for (const auto& Ix : par[ix])
+                for (const auto& Jx : par[jx])
+                  Kc[(static_cast<size_t>(Iy.first) * nc + Ix.first) * NBc * NBc + oy * NBc +
+                     (Jx.first - Ix.first + bc)] += vy * Ix.second * Jx.second;
+            }
+        }
+      }
+}
+
+// wedge fine level: (M, S), (S, M) and the stored K2 stencil
+static GenHost wedge_fine(const Band& S1, const Band& M1, const double* K2, int p) {
+  GenHost h;
+  h.Y = {M1, S1};
+  h.X = {S1, M1};
+  const size_t n = static_cast<size_t>(M1.n);
+  h.K.assign(K2, K2 + n * n * (2 * p + 1) * (2 * p + 1));
+  h.kb = p;
+  return h;
+}
 
 // fine level: (M, S), (S, M), (B_by, W_by = sum_bx m_{by,bx}^2 B_bx), by = 0..3
 // (K2 of src/assembly.cpp:234-246 grouped by its y factor)
@@ -1710,7 +1813,20 @@ static GenHost galerkin_gen(const GenHost& h, const Transfer& z) {
   GenHost o;
   for (const Band& y : h.Y) o.Y.push_back(galerkin(y, z));
   for (const Band& x : h.X) o.X.push_back(galerkin(x, z));
+  if (h.kb >= 0) galerkin_stencil2d(h.K, h.Y[0].n, h.kb, z, o.K, o.kb);
   return o;
+}
+
+// diagonal entry (iy, ix) of a level operator with group coefficients 1 (g < 2), cl (g >= 2) and kc = cl
+static std::complex<double> gen_diag_host(const GenHost& h, int iy, int ix, std::complex<double> cl) {
+  std::complex<double> d(0.0, 0.0);
+  for (size_t g = 0; g < h.Y.size(); ++g)
+    d += (g < 2 ? std::complex<double>(1.0, 0.0) : cl) * (h.Y[g].at(iy, iy) * h.X[g].at(ix, ix));
+  if (h.kb >= 0) {
+    const int n = h.Y[0].n, NB = 2 * h.kb + 1;
+    d += cl * h.K[(static_cast<size_t>(iy) * n + ix) * NB * NB + h.kb * NB + h.kb];
+  }
+  return d;
 }
 
 static Band padded(const Band& B, int b) {
@@ -1723,11 +1839,13 @@ static Band padded(const Band& B, int b) {
 // Upload the groups; layered coefficient cl of groups 2..5 (groups 0, 1: 1).
 static GenLevel upload_gen(const GenHost& h, double2 cl, double** mem) {
   const int G = static_cast<int>(h.Y.size());
-  int b = 0;
+  int b = std::max(h.kb, 0);
   for (int g = 0; g < G; ++g) b = std::max({b, h.Y[g].b, h.X[g].b});
   const int n = h.Y[0].n;
   const size_t per = static_cast<size_t>(n) * (2 * b + 1);
-  *mem = dalloc<double>(2 * G * per);
+  const int NB = 2 * b + 1;
+  const size_t NN = static_cast<size_t>(n) * n, kplanes = h.kb >= 0 ? static_cast<size_t>(NB) * NB * NN : 0;
+  *mem = dalloc<double>(2 * G * per + kplanes);
   GenLevel L{};
   L.n = n;
   L.b = b;
@@ -1742,6 +1860,20 @@ static GenLevel upload_gen(const GenHost& h, double2 cl, double** mem) {
     L.X[g] = dx;
     L.coef[g] = g < 2 ? cmk(1.0, 0.0) : cl;
   }
+  L.K = nullptr;
+  L.kc = cl;
+  if (h.kb >= 0) {
+    // tap-planar, padded to the level band b
+    const int kNB = 2 * h.kb + 1;
+    std::vector<double> planes(kplanes, 0.0);
+    for (size_t i = 0; i < NN; ++i)
+      for (int dy = -h.kb; dy <= h.kb; ++dy)
+        for (int dx = -h.kb; dx <= h.kb; ++dx)
+          planes[static_cast<size_t>((dy + b) * NB + dx + b) * NN + i] = h.K[i * kNB * kNB + (dy + h.kb) * kNB + dx + h.kb];
+    double* dk = *mem + 2 * G * per;
+    CK(cudaMemcpy(dk, planes.data(), kplanes * sizeof(double), cudaMemcpyHostToDevice));
+    L.K = dk;
+  }
   return L;
 }
 
@@ -1751,6 +1883,7 @@ static void attach_gen(DevBand& d, const GenHost& h, double2 cA, double2 cM) {
   GenLevel a = upload_gen(h, cmk(-cA.x, -cA.y), &mem);
   GenLevel m = a;
   for (int g = 2; g < m.G; ++g) m.coef[g] = cmk(-cM.x, -cM.y);
+  m.kc = cmk(-cM.x, -cM.y);
   d.gen_mem = mem;
   d.genA = new GenLevel(a);
   d.genM = new GenLevel(m);
@@ -1759,12 +1892,18 @@ static void attach_gen(DevBand& d, const GenHost& h, double2 cA, double2 cM) {
 // Dense inverse of a layered level operator (coefficient cl on groups 2..5):
 // E = Z^T A Z and the coarsest shifted level of the layered hierarchy stand in
 // for the reference's SparseLU factors (src/precond.cpp:95-99, 133).
-static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl) {
+static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int n_sms);
+
+static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl, int n_sms = 148) {
   const int n = h.Y[0].n;
   const size_t NN = static_cast<size_t>(n) * n;
+  // real operators (E) beyond the dense-inverse limit, or HD_BTRI=1: block tridiagonal LU
+  const char* fb = std::getenv("HD_BTRI");
+  if (cl.y == 0.0 && (NN > 20000 || (fb && std::atoi(fb) == 1) ) && !(fb && std::atoi(fb) == 0))
+    return make_btri(st, h, cl, n_sms);
   if (NN > 20000)
-    throw Error(HD_ERR_INVALID, "layered field: exact solve of " + std::to_string(NN) +
-                                    " unknowns exceeds the dense-inverse limit (20000)");
+    throw Error(HD_ERR_INVALID, "non-separable field: exact solve of " + std::to_string(NN) +
+                                    " complex unknowns exceeds the dense-inverse limit (20000)");
   ExactSolver X;
   X.dim = 2;
   X.n = n;
@@ -1803,6 +1942,92 @@ static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl) {
   cudaFree(mem);
   if (hinfo[0] != 0 || hinfo[1] != 0)
     throw Error(HD_ERR_FACTOR, "layered exact solve: singular operator (getrf info " + std::to_string(hinfo[0]) + ")");
+  return X;
+}
+
+// Block tridiagonal LU of a real level operator (btri.cuh): q = b grid rows per block.
+static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int n_sms) {
+  const int n = h.Y[0].n;
+  double* mem = nullptr;
+  const GenLevel L = upload_gen(h, cl, &mem);
+  for (int g = 0; g < L.G; ++g)
+    if (L.coef[g].y != 0.0) throw Error(HD_ERR_INVALID, "block tridiagonal solve needs a real operator");
+  const int q = std::max(L.b, 1), m = q * n, nb = (n + q - 1) / q;
+  const int kr_need = (m + 31) / 32;
+  int kr = 0;
+  for (int cand : {8, 16, 24, 32, 48, 64, 96})
+    if (cand >= kr_need) {
+      kr = cand;
+      break;
+    }
+  if (kr == 0) throw Error(HD_ERR_INVALID, "block tridiagonal solve: block size " + std::to_string(m) + " > 3072");
+  const size_t mm = static_cast<size_t>(m) * m, tot = static_cast<size_t>(nb) * mm;
+  ExactSolver X;
+  X.dim = 2;
+  X.n = n;
+  X.btri = true;
+  X.bt_kr = kr;
+  double *D = dalloc<double>(tot), *Bu = dalloc<double>(tot), *Cl = dalloc<double>(tot);
+  double *GT = dalloc<double>(tot), *SinvT = dalloc<double>(tot), *HT = dalloc<double>(tot);
+  CK(cudaMemsetAsync(GT, 0, mm * sizeof(double), st));
+  CK(cudaMemsetAsync(HT + (nb - 1) * mm, 0, mm * sizeof(double), st));
+  k_btri_blocks<<<grid_for(tot, 256, 148 * 32), 256, 0, st>>>(L, q, m, nb, D, Bu, Cl);
+  CK(cudaGetLastError());
+  cublasHandle_t cb;
+  CKB(cublasCreate(&cb));
+  CKB(cublasSetStream(cb, st));
+  cusolverDnHandle_t hs;
+  CKS(cusolverDnCreate(&hs));
+  CKS(cusolverDnSetStream(hs, st));
+  int lwork = 0;
+  CKS(cusolverDnDgetrf_bufferSize(hs, m, m, D, m, &lwork));
+  double* work = dalloc<double>(std::max(lwork, 1));
+  int* ipiv = dalloc<int>(m);
+  int* info = dalloc<int>(2 * nb);
+  CK(cudaMemsetAsync(info, 0, 2 * nb * sizeof(int), st));
+  std::vector<double> eye(mm, 0.0);
+  for (int i = 0; i < m; ++i) eye[i + static_cast<size_t>(i) * m] = 1.0;
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  for (int i = 0; i < nb; ++i) {
+    double* S = D + i * mm;  // S_i overwrites D_i
+    // S_i = D_i - G_i B_{i-1}   (G_i = (G_i^T)^T)
+    if (i > 0) CKB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, m, &mone, GT + i * mm, m, Bu + (i - 1) * mm, m, &one, S, m));
+    CKS(cusolverDnDgetrf(hs, m, m, S, m, work, ipiv, info + 2 * i));
+    // S_i^-T = solve(S_i^T X = I)
+    double* Si = SinvT + i * mm;
+    CK(cudaMemcpyAsync(Si, eye.data(), mm * sizeof(double), cudaMemcpyHostToDevice, st));
+    CKS(cusolverDnDgetrs(hs, CUBLAS_OP_T, m, m, S, m, ipiv, Si, m, info + 2 * i + 1));
+    if (i + 1 < nb) {
+      // G_{i+1}^T = S_i^-T C_{i+1}^T ;  H_i^T = B_i^T S_i^-T
+      CKB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, m, m, &one, Si, m, Cl + (i + 1) * mm, m, &zero, GT + (i + 1) * mm, m));
+      CKB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, m, &one, Bu + i * mm, m, Si, m, &zero, HT + i * mm, m));
+    }
+  }
+  std::vector<int> hinfo(2 * nb);
+  CK(cudaMemcpyAsync(hinfo.data(), info, hinfo.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cublasDestroy(cb);
+  cusolverDnDestroy(hs);
+  cudaFree(D); cudaFree(Bu); cudaFree(Cl); cudaFree(work); cudaFree(ipiv); cudaFree(info); cudaFree(mem);
+  for (int v : hinfo)
+    if (v != 0) {
+      cudaFree(GT); cudaFree(SinvT); cudaFree(HT);
+      throw Error(HD_ERR_FACTOR, "block tridiagonal exact solve: singular block (info " + std::to_string(v) + ")");
+    }
+  X.bt.n = n;
+  X.bt.q = q;
+  X.bt.m = m;
+  X.bt.nb = nb;
+  X.bt.NN = static_cast<size_t>(n) * n;
+  X.bt.GT = GT;
+  X.bt.SinvT = SinvT;
+  X.bt.HT = HT;
+  // y, w, x: one allocation
+  X.bt.y = dalloc<double>(6 * static_cast<size_t>(nb) * m);
+  X.bt.w = X.bt.y + 2 * static_cast<size_t>(nb) * m;
+  X.bt.x = X.bt.w + 2 * static_cast<size_t>(nb) * m;
+  X.bt.bar = dalloc<unsigned>(1);
+  (void)n_sms;
   return X;
 }
 
@@ -1865,11 +2090,14 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
     throw Error(HD_ERR_NO_DEVICE, "no CUDA device: the helmdef_b200 path has no CPU fallback");
   if (sys->dim != 1 && sys->dim != 2) throw Error(HD_ERR_INVALID, "dim must be 1 or 2");
   const bool layered = sys->field_kind == HD_FIELD_LAYERED;
-  if (sys->field_kind != HD_FIELD_CONSTANT && !layered) throw Error(HD_ERR_INVALID, "unknown wave-number field kind");
-  if (layered && sys->dim != 2) throw Error(HD_ERR_INVALID, "the layered field is two-dimensional");
+  const bool wedge = sys->field_kind == HD_FIELD_WEDGE;
+  const bool gen = layered || wedge;  // non-Kronecker-sum fields (layered.cuh)
+  if (sys->field_kind != HD_FIELD_CONSTANT && !gen) throw Error(HD_ERR_INVALID, "unknown wave-number field kind");
+  if (gen && sys->dim != 2) throw Error(HD_ERR_INVALID, "the layered and wedge fields are two-dimensional");
   if (layered && !sys->interval_mass) throw Error(HD_ERR_INVALID, "layered field needs the interval masses");
-  if (layered && spec->shift && spec->cycles <= 0)
-    throw Error(HD_ERR_INVALID, "C_ex (exact shifted inverse) on the layered field is not supported by this build");
+  if (wedge && !sys->shift_mass_2d) throw Error(HD_ERR_INVALID, "wedge field needs shift_mass_2d (hd_assemble_field)");
+  if (gen && spec->shift && spec->cycles <= 0)
+    throw Error(HD_ERR_INVALID, "C_ex (exact shifted inverse) on a non-separable field is not supported by this build");
   if (sys->per_dim < 2) throw Error(HD_ERR_INVALID, "per_dim must be >= 2");
   const auto t0 = std::chrono::steady_clock::now();
   std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
@@ -1890,7 +2118,8 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   c->spec = *spec;
   if (c->spec.coarsest <= 0) c->spec.coarsest = 32;
   c->corner = c->dim == 1 ? cmk(sys->corner_re, sys->corner_im) : cmk(0.0, 0.0);
-  const double k2 = c->k * c->k;
+  // wedge: K2 carries k(x,y)^2 itself, so its coefficients are 1 and 1 - i beta2
+  const double k2 = wedge ? 1.0 : c->k * c->k;
   c->cA = cmk(k2, 0.0);
   // shifted operator A + i beta2 K2 = ... - k^2 (1 - i beta2) M(x)M  (src/precond.cpp:165-167)
   c->cM = cmk(k2, -k2 * c->spec.beta2);
@@ -1898,8 +2127,9 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   const Band M1 = band_from_host(sys->mass_band, c->n, sys->order);
   c->fine = upload_pair(S1, M1);
   GenHost fineH;
-  if (layered) {
-    fineH = layered_fine(S1, M1, sys->interval_mass, sys->multipliers);
+  if (gen) {
+    fineH = layered ? layered_fine(S1, M1, sys->interval_mass, sys->multipliers)
+                    : wedge_fine(S1, M1, sys->shift_mass_2d, sys->order);
     attach_gen(c->fine, fineH, c->cA, c->cM);
   }
   // C_ex: exact shifted inverse (src/precond.cpp:204-211)
@@ -1920,30 +2150,25 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
       const Transfer z = linear_stencil(nl);
       Ss.push_back(galerkin(Ss.back(), z));
       Ms.push_back(galerkin(Ms.back(), z));
-      if (layered) Hs.push_back(galerkin_gen(Hs.back(), z));
+      if (gen) Hs.push_back(galerkin_gen(Hs.back(), z));
       nl = z.coarse;
     }
     c->lev.push_back(c->fine);
     for (size_t l = 1; l < Ss.size(); ++l) {
       c->lev.push_back(upload_pair(Ss[l], Ms[l]));
-      if (layered) attach_gen(c->lev.back(), Hs[l], c->cA, c->cM);
+      if (gen) attach_gen(c->lev.back(), Hs[l], c->cA, c->cM);
     }
-    if (layered)  // zero-diagonal check of the layered levels (src/precond.cpp:125-132)
+    if (gen)  // zero-diagonal check of the layered / wedge levels (src/precond.cpp:125-132)
       for (size_t l = 0; l < Hs.size(); ++l) {
         const GenHost& h = Hs[l];
         const int nn = h.Y[0].n;
         for (int i = 0; i < nn; ++i)
-          for (int j = 0; j < nn; ++j) {
-            std::complex<double> d(0.0, 0.0);
-            for (size_t g = 0; g < h.Y.size(); ++g) {
-              const std::complex<double> cg = g < 2 ? std::complex<double>(1.0, 0.0) : -std::complex<double>(c->cM.x, c->cM.y);
-              d += cg * (h.Y[g].at(i, i) * h.X[g].at(j, j));
-            }
-            if (d == std::complex<double>(0.0, 0.0)) throw Error(HD_ERR_FACTOR, "zero diagonal in smoother");
-          }
+          for (int j = 0; j < nn; ++j)
+            if (gen_diag_host(h, i, j, -std::complex<double>(c->cM.x, c->cM.y)) == std::complex<double>(0.0, 0.0))
+              throw Error(HD_ERR_FACTOR, "zero diagonal in smoother");
       }
     // zero-diagonal check of every level (src/precond.cpp:125-132)
-    for (size_t l = 0; !layered && l < Ss.size(); ++l)
+    for (size_t l = 0; !gen && l < Ss.size(); ++l)
       for (int i = 0; i < Ss[l].n; ++i)
         for (int j = 0; j < (c->dim == 2 ? Ss[l].n : 1); ++j) {
           const int jj = c->dim == 2 ? j : i;
@@ -1956,7 +2181,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
         }
     const Band& SL = Ss.back();
     const Band& ML = Ms.back();
-    if (layered) c->coarsest = make_dense(c->st, Hs.back(), cmk(-c->cM.x, -c->cM.y));
+    if (gen) c->coarsest = make_dense(c->st, Hs.back(), cmk(-c->cM.x, -c->cM.y));
     else if (c->dim == 2) c->coarsest = make_fd(c->st, SL, ML, c->cM);
     else c->coarsest = make_bandlu(SL, ML, c->cM, Ss.size() == 1 ? c->corner : cmk(0.0, 0.0));
     for (size_t l = 0; l < c->lev.size(); ++l) {
@@ -1973,8 +2198,10 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
     c->nc = z.coarse;
     if (c->nc < 1) throw Error(HD_ERR_INVALID, "deflation needs per_dim >= 2");
     const Band ES = galerkin(S1, z), EM = galerkin(M1, z);
-    if (layered) {
-      c->E = make_dense(c->st, galerkin_gen(fineH, z), cmk(-c->cA.x, -c->cA.y));
+    if (gen) {
+      int nsm = 148;
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+      c->E = make_dense(c->st, galerkin_gen(fineH, z), cmk(-c->cA.x, -c->cA.y), nsm);
     } else if (c->dim == 2) {
       const bool fold = (c->nc % 2 == 0) && centro_symmetric(ES) && centro_symmetric(EM) &&
                         !std::getenv("HD_NOFOLD");
@@ -2618,21 +2845,40 @@ hd_status hd_assemble(const hd_problem* pb, double* stiffness_band, double* mass
       std::memcpy(interval_mass + static_cast<size_t>(b) * Bb.a.size(), Bb.a.data(), Bb.a.size() * sizeof(double));
     }
   }
-  std::vector<double> phi(n);
-  for (int i = 0; i < n; ++i) phi[i] = bspline_value(f.kv, f.kv.degree, kept[i], 0.5);
+  // point load phi_i(x_s) phi_j(y_s) (src/assembly.cpp:251-256; (1/2, 1/2) unless set)
+  const double xs = pb->point_source ? pb->source[0] : 0.5, ys = pb->point_source ? pb->source[1] : 0.5;
+  std::vector<double> phix(n), phiy(n);
+  for (int i = 0; i < n; ++i) {
+    phix[i] = bspline_value(f.kv, f.kv.degree, kept[i], xs);
+    phiy[i] = bspline_value(f.kv, f.kv.degree, kept[i], ys);
+  }
   if (pb->dim == 1) {
     for (int i = 0; i < n; ++i) {
-      rhs[2 * i] = phi[i];
+      rhs[2 * i] = phix[i];
       rhs[2 * i + 1] = 0.0;
     }
   } else {
     for (int iy = 0; iy < n; ++iy)
       for (int ix = 0; ix < n; ++ix) {
         const size_t g = static_cast<size_t>(iy) * n + ix;
-        rhs[2 * g] = phi[iy] * phi[ix];
+        rhs[2 * g] = phiy[iy] * phix[ix];
         rhs[2 * g + 1] = 0.0;
       }
   }
+  HD_GUARD_END
+}
+
+hd_status hd_assemble_field(const hd_problem* pb, double* shift_mass_2d) {
+  HD_GUARD_BEGIN
+  if (!pb || !shift_mass_2d) throw Error(HD_ERR_INVALID, "null argument");
+  if (pb->field_kind != HD_FIELD_WEDGE || pb->dim != 2)
+    throw Error(HD_ERR_INVALID, "hd_assemble_field: only the 2D wedge field has a non-separable K2");
+  if (pb->order < 1 || pb->order > 6 || pb->elements < 1) throw Error(HD_ERR_INVALID, "bad order/elements");
+  const Knots kv = Knots::open_uniform(pb->elements, pb->order);
+  std::vector<int> kept;
+  for (int j = 1; j < kv.basis_count() - 1; ++j) kept.push_back(j);
+  const std::vector<double> K = wedge_mass_stencil(kv, pb->k, pb->multipliers, pb->lines, kept);
+  std::memcpy(shift_mass_2d, K.data(), K.size() * sizeof(double));
   HD_GUARD_END
 }
 

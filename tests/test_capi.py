@@ -88,3 +88,35 @@ def test_to_spec_mirrors_reference_mapping():
     assert hd.derived_elements(1000, 0.625, 3) == O.derived_elements(1000, 0.625, 3) == 1598
     with pytest.raises(ValueError):
         hd.to_spec("bogus", 1, 1.0)
+
+
+@pytest.mark.parametrize("ne,p,k0", [(16, 2, 30.0), (24, 3, 30.0), (40, 3, 60.0), (20, 4, 25.0)])
+def test_native_wedge_assembly_matches_oracle(ne, p, k0):
+    """BASELINE config-4 wedge (oracle extension): the native K2 stencil and the
+    off-centre point load equal the oracle's assembly."""
+    s = hd.assemble(hd.wedge_2d(ne, p, k0))
+    so = O.assemble(O.wedge_2d(ne, p, k0))
+    n, NB = s.per_dim, 2 * p + 1
+    K = s.shift_mass_2d.reshape(n, n, NB, NB).transpose(0, 2, 1, 3)
+    assert np.abs(K - so.K2_stencil).max() <= 1e-14 * np.abs(so.K2_stencil).max()
+    assert np.abs(s.rhs - so.rhs).max() == 0.0 and np.count_nonzero(s.rhs) > 0
+
+
+def test_wedge_with_equal_layers_is_the_constant_field():
+    """Pointwise Gauss sampling of a constant k reproduces k^2 M(x)M exactly
+    (the (p+1)-point rule integrates the degree-2p products exactly)."""
+    s = O.assemble(O.wedge_2d(24, 3, 17.0, multipliers=[1.0, 1.0, 1.0]))
+    c = O.assemble(O.point_source_2d(24, 3, 17.0))
+    assert abs(s.shift_mass - c.shift_mass).max() <= 1e-15 * abs(c.shift_mass).max() * 10
+    assert abs(s.A - c.A).max() <= 1e-13
+
+
+def test_wedge_layers():
+    """k^2 sampling: the three layers and the strict interfaces."""
+    m, ln = O.WEDGE_MULTIPLIERS, O.WEDGE_LINES
+    k2 = lambda x, y: float(O.wedge_k2(np.array(x), np.array(y), 10.0, m, ln))
+    assert k2(0.5, 0.9) == pytest.approx(144.0)     # top
+    assert k2(0.5, 0.45) == pytest.approx(225.0)    # middle (0.35 < y <= 0.5 at x = 0.5)
+    assert k2(0.5, 0.1) == pytest.approx(100.0)     # bottom
+    assert k2(0.0, 0.6) == pytest.approx(225.0)     # on the top interface: not top
+    assert k2(1.0, 0.41) == pytest.approx(144.0)    # right edge, the layers meet at y = 0.4
