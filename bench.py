@@ -12,7 +12,8 @@ BASELINE config and the one its roofline target names.
   python bench.py --impl reference ...   # the reference algorithm on the host CPU
 
 N > 1 (torchrun): every rank solves its own replica (weak scaling, no
-data-path collective).  Timing: CUDA events on the
+data-path collective); with --slabs the ranks share one
+solve as row slabs over NCCL (hd_create_dist, strong scaling).  Timing: CUDA events on the
 library's stream (set to torch's current stream), barrier + synchronize on
 both sides, max over ranks; the L2 is flushed (256 MiB write) between steps
 outside the timed events.
@@ -221,7 +222,14 @@ def run_gpu(args):
                       omega=SPEC["omega"])
     opt = hd.GmresOptions(MAXIT, TOL)
     N = sys_.size
-    solver = hd.Solver(sys_, spec, devices=[local])
+    if args.slabs:
+        # row slabs, one per process, NCCL transport (hd_create_dist): strong scaling of one solve
+        uid = [hd.nccl_unique_id() if rank == 0 else None]
+        if dist:
+            dist.broadcast_object_list(uid, src=0)
+        solver = hd.Solver(sys_, spec, dist=(rank, ws, uid[0], local))
+    else:
+        solver = hd.Solver(sys_, spec, devices=[local])
     stream = torch.cuda.current_stream(dev)
     solver.set_stream(stream.cuda_stream)
     rhs_d = torch.from_numpy(sys_.rhs.view(np.float64)).to(dev)
@@ -266,6 +274,8 @@ def run_gpu(args):
     prof = solver.profile_read()
     solver.profile(False)
     t_max, iters_all = rank_reduce(dist, t_ms, iters, dev)
+    if args.slabs:
+        iters_all /= ws  # one distributed solve: every rank reports the same iterations
     value = iters_all / (t_max * 1e-3)
 
     # --- end to end through the public host-buffer API (pinned host memory)
@@ -291,6 +301,8 @@ def run_gpu(args):
     torch.cuda.synchronize()
     e_ms = float(sum(a.elapsed_time(b) for a, b in e_evs))
     e_ms, e_iters = rank_reduce(dist, e_ms, e_iters, dev)
+    if args.slabs:
+        e_iters /= ws
     e2e = {"value": e_iters / (e_ms * 1e-3), "unit": "iterations/s", "h2d_bytes_per_step": 16 * N,
            "d2h_bytes_per_step": 16 * N + 8 * (r.iterations), "ms_per_step": e_ms / args.steps}
 
@@ -341,11 +353,13 @@ def run_gpu(args):
 
     line = {"metric": "preconditioned GMRES iterations/s", "value": value, "unit": "iterations/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64 complex)",
+            "higher_is_better": True, "scaling": "strong" if args.slabs else "weak", "vs_baseline": None,
+            "dtype": "c128 (f64 complex)",
             "data": "synthetic (deterministic point source, as the reference)",
             "config": {"workload": workload_name(args.config), "N": N, "iterations_per_solve": r.iterations,
                        "step": "one full solve (hd_solve_device)",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "parallelism": (f"row slabs x{ws} (NCCL)" if args.slabs else
+                                       (f"replicas x{ws}" if ws > 1 else "single GPU")),
                        "l2": "flushed (256 MiB write) between steps, outside the timed events"},
             "time_to_solution_ms": t_max / args.steps, "t_setup_s": r.t_setup,
             "e2e": e2e, "gpu_launches": launches, "library_calls": libcalls,
@@ -376,6 +390,9 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C5")
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slabs", action="store_true",
+                    help="N > 1: one row slab per rank over NCCL (hd_create_dist), strong scaling of one solve; "
+                         "default: N independent replicas")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -164,6 +164,20 @@ hd_status hd_create(const hd_system* sys, const hd_precond* spec, const int* dev
  * cycles >= 1 (the DC_MG family). */
 hd_status hd_create_slabs(const hd_system* sys, const hd_precond* spec, int nslabs, hd_ctx** out);
 
+/* The same slab program with one slab per process (one process per GPU,
+ * SURVEY.md §8(e)): this process owns slab `rank` of `nranks` on CUDA device
+ * `device`.  Halo rows travel by NCCL send/recv, the gather-level and
+ * deflation coarse vectors by NCCL broadcasts from their row owners, the
+ * reduction partials by NCCL allgathers combined in slab order (so every
+ * process computes the same scalars and takes the same branches).
+ * nccl_id: the 128-byte ncclUniqueId from hd_nccl_unique_id on rank 0, passed
+ * to every rank by the caller (e.g. a torch.distributed broadcast).  hd_solve
+ * takes the whole rhs on every rank and returns the whole x on every rank.
+ * NCCL is loaded at run time (dlopen "libnccl.so.2"). */
+hd_status hd_nccl_unique_id(unsigned char* nccl_id_out /* 128 bytes */);
+hd_status hd_create_dist(const hd_system* sys, const hd_precond* spec, int rank, int nranks,
+                         const unsigned char* nccl_id, int device, hd_ctx** out);
+
 /* Slab count of a context (0: single domain); gather_level and the nslabs+1
  * fine row bounds are written when non-NULL. */
 int hd_slab_info(const hd_ctx* ctx, int* gather_level, int* bounds);

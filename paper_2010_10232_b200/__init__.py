@@ -42,7 +42,8 @@ HD_APPLY_A, HD_APPLY_SHIFTED, HD_APPLY_MG, HD_APPLY_PROJECT, HD_APPLY_OP, HD_APP
 # Every symbol include/helmdef_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = ["hd_problem_per_dim", "hd_assemble", "hd_assemble_field", "hd_create", "hd_solve", "hd_solve_device", "hd_size",
            "hd_levels", "hd_apply", "hd_debug_level", "hd_level_size", "hd_set_stream", "hd_profile",
-           "hd_profile_read", "hd_destroy", "hd_last_error", "hd_create_slabs", "hd_slab_info"]
+           "hd_profile_read", "hd_destroy", "hd_last_error", "hd_create_slabs", "hd_slab_info",
+           "hd_nccl_unique_id", "hd_create_dist"]
 KERNEL_KINDS = ["op_fine", "op_coarse", "jacobi0", "transfer", "exact", "mgs", "iterate", "vec", "givens",
                 "lib_gemm"]
 
@@ -101,6 +102,11 @@ def load_library() -> C.CDLL:
     lib.hd_create.restype = C.c_int
     lib.hd_create_slabs.argtypes = [C.POINTER(HdSystem), C.POINTER(HdPrecond), C.c_int, C.POINTER(C.c_void_p)]
     lib.hd_create_slabs.restype = C.c_int
+    lib.hd_nccl_unique_id.argtypes = [C.c_char_p]
+    lib.hd_nccl_unique_id.restype = C.c_int
+    lib.hd_create_dist.argtypes = [C.POINTER(HdSystem), C.POINTER(HdPrecond), C.c_int, C.c_int, C.c_char_p, C.c_int,
+                                   C.POINTER(C.c_void_p)]
+    lib.hd_create_dist.restype = C.c_int
     lib.hd_slab_info.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.hd_slab_info.restype = C.c_int
     lib.hd_solve.argtypes = [C.c_void_p, C.POINTER(HdGmres), dp, dp, dp, C.POINTER(HdReport)]
@@ -342,11 +348,19 @@ def to_spec(tag, order, k, epsilon=0.1, beta2="1", cycles=1, smoothing=1, omega=
     return s
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for hd_create_dist (create on rank 0, broadcast to all)."""
+    buf = C.create_string_buffer(128)
+    _check(load_library().hd_nccl_unique_id(buf))
+    return buf.raw
+
+
 class Solver:
     """compose(sys, spec) on the device; .solve() is gmres(op, rhs, start, monitor)."""
 
-    def __init__(self, sys_: DiscreteSystem, spec: PrecondSpec, devices=None, slabs: int = 0):
-        """slabs > 0: the row-slab decomposition (hd_create_slabs)."""
+    def __init__(self, sys_: DiscreteSystem, spec: PrecondSpec, devices=None, slabs: int = 0, dist=None):
+        """slabs > 0: the row-slab decomposition on this GPU (hd_create_slabs, SURVEY.md 8(e));
+        dist = (rank, nranks, nccl_id, device): one slab per process over NCCL (hd_create_dist)."""
         lib = load_library()
         self._lib = lib
         self.sys = sys_
@@ -374,6 +388,11 @@ class Solver:
         if devices:
             arr = (C.c_int * len(devices))(*devices)
             _check(lib.hd_create(C.byref(h), C.byref(p), arr, len(devices), C.byref(ctx)))
+        elif dist is not None:
+            rank, nranks, uid, dev = dist
+            _check(lib.hd_create_dist(C.byref(h), C.byref(p), int(rank), int(nranks), bytes(uid), int(dev),
+                                      C.byref(ctx)))
+            slabs = int(nranks)
         elif slabs:
             _check(lib.hd_create_slabs(C.byref(h), C.byref(p), int(slabs), C.byref(ctx)))
         else:

@@ -66,7 +66,7 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
         objs.append(o)
     if _stale(OUT, objs):
         _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *map(str, objs), "-o", str(OUT),
-              "-lcublas", "-lcusolver", "-lcudart"])
+              "-lcublas", "-lcusolver", "-lcudart", "-ldl"])
     # the C++ host mirror's cell tool (include/helmdef_b200.hpp), linked against
     # the in-tree library with a relative rpath so the built tree can move
     if TOOL_SRC.exists() and _stale(TOOL, [TOOL_SRC, OUT, ROOT / "include" / "helmdef_b200.hpp"]):

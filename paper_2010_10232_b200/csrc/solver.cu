@@ -12,6 +12,8 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -2285,8 +2287,77 @@ struct SlabLevel {
   std::vector<int> bounds;  // S+1 row boundaries (distributed levels)
 };
 
+// NCCL, resolved at run time (dlopen) so the library loads without it; only
+// the multi-process slab program (hd_create_dist) needs it.
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  if (api.h) return api;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) throw Error(HD_ERR_INVALID, "multi-process row slabs need NCCL (libnccl.so.2 not found)");
+  auto sym = [&](const char* n) {
+    void* f = dlsym(h, n);
+    if (!f) throw Error(HD_ERR_INVALID, std::string("NCCL symbol missing: ") + n);
+    return f;
+  };
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+  api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+  api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  api.h = h;
+  return api;
+}
+
+#define CKN(x)                                                                                    \
+  do {                                                                                            \
+    ncclResult_t e_ = (x);                                                                        \
+    if (e_ != ncclSuccess) throw Error(HD_ERR_CUDA, std::string(#x) + ": " + nccl().GetErrorString(e_)); \
+  } while (0)
+
+// A point-to-point transfer of the slab program (halo rows).
+struct SlabPost {
+  const double2* src;
+  double2* dst;
+  size_t count;  // double2 elements
+  int peer;      // the other slab
+};
+
 struct hd_slabs {
   int S = 0, g = 0, Gs = 0;
+  // transport.  nranks == 1: every slab lives in this process (one GPU, the
+  // exchanges are device copies); nranks > 1: this process owns slab `rank`
+  // (one process per GPU) and the exchanges are NCCL send/recv, the shared
+  // coarse vectors NCCL broadcasts and the reduction partials NCCL allgathers.
+  // vranks (HD_SLAB_VRANKS=1, one process): every slab is its own virtual
+  // rank and halo rows go through the same posted send/recv records as the
+  // NCCL path, matched and copied at group end -- the offsets and sizes of
+  // the multi-process program exercised on one GPU.
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  bool vranks = false;
+  std::vector<int> mine;                        // slabs of this process
+  std::vector<SlabPost> sends, recvs;           // posted in the current group (vranks)
+  double2* red = nullptr;                       // S x nslot per-slab Arnoldi pass-1 sums
   std::vector<SlabLevel> lv;                    // MG levels
   std::vector<std::vector<double2*>> X, Y, B, R;  // [level][slab], levels < g
   std::vector<int> cur;                         // ping-pong state of X/Y per level
@@ -2318,7 +2389,21 @@ __global__ void k_slab_norm(const double* slots, int S, const double* scale_src,
   if (cdst) *cdst = cmk(nrm, 0.0);
 }
 
+// Arnoldi pass 1 of one slab: its Gs CTA partials summed per used slot in CTA
+// order (deterministic), so a process contributes one row of kLsaNslot sums
+constexpr int kLsaNslot = 2 * kLsaMaxJ + 2;
+__global__ void k_lsa_slab_reduce(const double2* __restrict__ parts, int Gs, int j, double2* __restrict__ out) {
+  for (int q = threadIdx.x; q < kLsaNslot; q += blockDim.x) {
+    const bool used = q < j + 1 || (q >= kLsaMaxJ + 1 && q < kLsaMaxJ + 1 + j);
+    double2 acc = cmk(0.0, 0.0);
+    if (used)
+      for (int b = 0; b < Gs; ++b) acc = cadd(acc, parts[(size_t)b * kLsaNslot + q]);
+    out[q] = acc;
+  }
+}
+
 static hd_slabs* slabs_of(hd_ctx* c) { return reinterpret_cast<hd_slabs*>(c->slabs); }
+static inline bool is_local(const hd_slabs* sl, int s) { return sl->nranks == 1 || s == sl->rank; }
 
 // virtual pointer of a halo'd slab buffer: global row r of the slab lives at v + r*n
 static inline double2* vptr(double2* buf, int r0, int H, int n) {
@@ -2326,23 +2411,129 @@ static inline double2* vptr(double2* buf, int r0, int H, int n) {
 }
 static inline int own(const SlabLevel& L, int s) { return L.bounds[s + 1] - L.bounds[s]; }
 
+// ---- transport -------------------------------------------------------------
+// halo rows: slab s receives from a neighbour t.  Local pairs are device copies;
+// remote pairs (other process, or a virtual rank) are posted send/recv.
+static void xp_send(hd_ctx* c, const double2* src, size_t count, int from, int to) {
+  hd_slabs* sl = slabs_of(c);
+  if (sl->vranks) {
+    sl->sends.push_back({src, nullptr, count, to});
+    (void)from;
+  } else {
+    CKN(nccl().Send(src, 2 * count, ncclDouble, to, sl->comm, c->st));
+  }
+}
+static void xp_recv(hd_ctx* c, double2* dst, size_t count, int from, int to) {
+  hd_slabs* sl = slabs_of(c);
+  if (sl->vranks) {
+    sl->recvs.push_back({nullptr, dst, count, from});
+    (void)to;
+  } else {
+    CKN(nccl().Recv(dst, 2 * count, ncclDouble, from, sl->comm, c->st));
+  }
+}
+static bool remote_pairs(const hd_slabs* sl) { return sl->nranks > 1 || sl->vranks; }
+static void xp_group_start(hd_ctx* c) {
+  hd_slabs* sl = slabs_of(c);
+  if (sl->nranks > 1) CKN(nccl().GroupStart());
+  sl->sends.clear();
+  sl->recvs.clear();
+}
+// vranks: the k-th send from slab a to slab b pairs with the k-th receive of b from a
+static void xp_group_end(hd_ctx* c, const std::vector<int>& send_from, const std::vector<int>& recv_to) {
+  hd_slabs* sl = slabs_of(c);
+  if (sl->nranks > 1) {
+    CKN(nccl().GroupEnd());
+    return;
+  }
+  if (!sl->vranks) return;
+  std::vector<bool> used(sl->sends.size(), false);
+  for (size_t r = 0; r < sl->recvs.size(); ++r) {
+    const SlabPost& rv = sl->recvs[r];
+    bool found = false;
+    for (size_t q = 0; q < sl->sends.size() && !found; ++q) {
+      if (used[q] || send_from[q] != rv.peer || sl->sends[q].peer != recv_to[r]) continue;
+      if (sl->sends[q].count != rv.count) throw Error(HD_ERR_INVALID, "slab transport: send/recv size mismatch");
+      CK(cudaMemcpyAsync(rv.dst, sl->sends[q].src, rv.count * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+      used[q] = found = true;
+    }
+    if (!found) throw Error(HD_ERR_INVALID, "slab transport: receive without a matching send");
+  }
+  for (bool u : used)
+    if (!u) throw Error(HD_ERR_INVALID, "slab transport: send without a matching receive");
+}
+
 // halo exchange of one distributed level vector (slab s <- neighbours' own rows)
 static void slab_exchange(hd_ctx* c, const SlabLevel& L, const std::vector<double2*>& v) {
   hd_slabs* sl = slabs_of(c);
-  const size_t row = static_cast<size_t>(L.n) * sizeof(double2);
-  for (int s = 0; s < sl->S; ++s) {
-    if (s > 0)  // top halo: the last H own rows of slab s-1
-      CK(cudaMemcpyAsync(v[s], v[s - 1] + static_cast<size_t>(own(L, s - 1)) * L.n, L.H * row,
-                         cudaMemcpyDeviceToDevice, c->st));
-    if (s + 1 < sl->S)  // bottom halo: the first H own rows of slab s+1
-      CK(cudaMemcpyAsync(v[s] + static_cast<size_t>(L.H + own(L, s)) * L.n, v[s + 1] + static_cast<size_t>(L.H) * L.n,
-                         L.H * row, cudaMemcpyDeviceToDevice, c->st));
+  const size_t row = static_cast<size_t>(L.n), hrows = static_cast<size_t>(L.H) * row;
+  const bool remote = remote_pairs(sl);
+  std::vector<int> send_from, recv_to;
+  if (remote) xp_group_start(c);
+  for (int s : sl->mine) {
+    const size_t ownr = static_cast<size_t>(own(L, s));
+    double2* top_halo = v[s];
+    double2* bot_halo = v[s] + (L.H + ownr) * row;
+    const double2* first_own = v[s] + hrows;
+    const double2* last_own = v[s] + ownr * row;  // rows own-H .. own-1 (after the H halo rows)
+    if (s > 0) {
+      if (!remote && is_local(sl, s - 1)) {
+        CK(cudaMemcpyAsync(top_halo, v[s - 1] + static_cast<size_t>(own(L, s - 1)) * row, hrows * sizeof(double2),
+                           cudaMemcpyDeviceToDevice, c->st));
+      } else {
+        xp_send(c, first_own, hrows, s, s - 1);
+        send_from.push_back(s);
+        xp_recv(c, top_halo, hrows, s - 1, s);
+        recv_to.push_back(s);
+      }
+    }
+    if (s + 1 < sl->S) {
+      if (!remote && is_local(sl, s + 1)) {
+        CK(cudaMemcpyAsync(bot_halo, v[s + 1] + hrows, hrows * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+      } else {
+        xp_send(c, last_own, hrows, s, s + 1);
+        send_from.push_back(s);
+        xp_recv(c, bot_halo, hrows, s + 1, s);
+        recv_to.push_back(s);
+      }
+    }
   }
+  if (remote) xp_group_end(c, send_from, recv_to);
 }
 
-static std::vector<double2*> slab_alloc(const SlabLevel& L, int S) {
-  std::vector<double2*> v(S);
+// rows [bounds[s], bounds[s+1]) of a whole-grid buffer (planes of `plane`
+// double2, or planar doubles when planar) written by their owners -> every
+// process (multi-process: one NCCL broadcast per owner and plane)
+static void slab_share_rows(hd_ctx* c, const SlabLevel& L, void* buf, bool planar) {
+  hd_slabs* sl = slabs_of(c);
+  if (sl->nranks == 1) return;  // one process: the buffer is already whole
+  const size_t NN = static_cast<size_t>(L.n) * L.n;
+  CKN(nccl().GroupStart());
+  for (int s = 0; s < sl->S; ++s) {
+    const size_t r0 = static_cast<size_t>(L.bounds[s]) * L.n, cnt = static_cast<size_t>(own(L, s)) * L.n;
+    if (planar) {
+      double* d = static_cast<double*>(buf);
+      for (int pl = 0; pl < 2; ++pl)
+        CKN(nccl().Broadcast(d + pl * NN + r0, d + pl * NN + r0, cnt, ncclDouble, s, sl->comm, c->st));
+    } else {
+      double2* d = static_cast<double2*>(buf);
+      CKN(nccl().Broadcast(d + r0, d + r0, 2 * cnt, ncclDouble, s, sl->comm, c->st));
+    }
+  }
+  CKN(nccl().GroupEnd());
+}
+
+// per-slab blocks of `per` doubles at slab offsets (slab s at s*per) -> every process
+static void slab_allgather(hd_ctx* c, double* buf, size_t per) {
+  hd_slabs* sl = slabs_of(c);
+  if (sl->nranks == 1) return;
+  CKN(nccl().AllGather(buf + static_cast<size_t>(sl->rank) * per, buf, per, ncclDouble, sl->comm, c->st));
+}
+
+static std::vector<double2*> slab_alloc(const SlabLevel& L, int S, const hd_slabs* sl) {
+  std::vector<double2*> v(S, nullptr);
   for (int s = 0; s < S; ++s) {
+    if (!is_local(sl, s)) continue;
     const size_t rows = static_cast<size_t>(own(L, s) + 2 * L.H);
     v[s] = dalloc<double2>(rows * L.n);
     CK(cudaMemset(v[s], 0, rows * L.n * sizeof(double2)));
@@ -2355,18 +2546,19 @@ static void s_apply(hd_ctx* c, int mode, const LevelDev& L, const SlabLevel& G, 
                     const std::vector<double2*>* b, std::vector<double2*>* out, double omega) {
   hd_slabs* sl = slabs_of(c);
   slab_exchange(c, G, x);
-  for (int s = 0; s < sl->S; ++s) {
+  for (int s : sl->mine) {
     const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
     op_apply(c, mode, L, vptr(x[s], r0, G.H, G.n), b ? vptr((*b)[s], r0, G.H, G.n) : nullptr,
              out ? vptr((*out)[s], r0, G.H, G.n) : nullptr, omega, mode == OP_RESNORM ? sl->slots + s : nullptr, 1.0,
              nullptr, 0, r0, r1, mode == OP_RESNORM ? 1 : 0);
   }
+  if (mode == OP_RESNORM) slab_allgather(c, sl->slots, 1);
 }
 
 static void s_jacobi0(hd_ctx* c, const LevelDev& L, const SlabLevel& G, const std::vector<double2*>& b,
                       std::vector<double2*>& out) {
   hd_slabs* sl = slabs_of(c);
-  for (int s = 0; s < sl->S; ++s) {
+  for (int s : sl->mine) {
     const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
     jacobi0(c, L, vptr(b[s], r0, G.H, G.n), vptr(out[s], r0, G.H, G.n), c->spec.omega, r0, r1);
   }
@@ -2385,7 +2577,7 @@ static void s_cycle(hd_ctx* c, int l, std::vector<double2*>& b, bool x_zero) {
   int st = 0;
   if (x_zero) {
     if (nu == 0) {
-      for (int s = 0; s < sl->S; ++s)
+      for (int s : sl->mine)
         CK(cudaMemsetAsync(sX(sl, l)[s], 0, static_cast<size_t>(own(G, s) + 2 * G.H) * G.n * sizeof(double2), c->st));
     } else {
       s_jacobi0(c, L, G, b, sX(sl, l));
@@ -2401,11 +2593,12 @@ static void s_cycle(hd_ctx* c, int l, std::vector<double2*>& b, bool x_zero) {
   const SlabLevel& Gc = sl->lv[l + 1];
   slab_exchange(c, G, sl->R[l]);
   const bool coarse_dist = l + 1 < sl->g;
-  for (int s = 0; s < sl->S; ++s) {
+  for (int s : sl->mine) {
     const int q0 = Gc.bounds[s], q1 = Gc.bounds[s + 1];
     double2* out = coarse_dist ? vptr(sl->B[l + 1][s], q0, Gc.H, Gc.n) : c->mg_b[l + 1];
     restrict_(c, Stencil{0, 0.0}, vptr(sl->R[l][s], G.bounds[s], G.H, G.n), G.n, Gc.n, out, nullptr, q0, q1);
   }
+  if (!coarse_dist) slab_share_rows(c, Gc, c->mg_b[l + 1], false);  // the gather level: allgather
   const double2* eglob = nullptr;
   if (coarse_dist) {
     s_cycle(c, l + 1, sl->B[l + 1], true);
@@ -2413,7 +2606,7 @@ static void s_cycle(hd_ctx* c, int l, std::vector<double2*>& b, bool x_zero) {
   } else {
     eglob = cycle_at(c, l + 1, c->mg_b[l + 1], true);  // the small levels, once (multi-GPU: on every rank)
   }
-  for (int s = 0; s < sl->S; ++s) {
+  for (int s : sl->mine) {
     const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
     const double2* ec = coarse_dist ? vptr(sX(sl, l + 1)[s], Gc.bounds[s], Gc.H, Gc.n) : eglob;
     prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, G.n, Gc.n, nullptr, vptr(sX(sl, l)[s], r0, G.H, G.n), r0, r1);
@@ -2442,11 +2635,12 @@ static void s_mg_solve(hd_ctx* c, std::vector<double2*>& b, std::vector<double2*
       const SlabLevel& Gc = sl->lv[1];
       slab_exchange(c, G, sl->R[0]);
       const bool coarse_dist = 1 < sl->g;
-      for (int s = 0; s < sl->S; ++s) {
+      for (int s : sl->mine) {
         double2* o = coarse_dist ? vptr(sl->B[1][s], Gc.bounds[s], Gc.H, Gc.n) : c->mg_b[1];
         restrict_(c, Stencil{0, 0.0}, vptr(sl->R[0][s], G.bounds[s], G.H, G.n), G.n, Gc.n, o, nullptr, Gc.bounds[s],
                   Gc.bounds[s + 1]);
       }
+      if (!coarse_dist) slab_share_rows(c, Gc, c->mg_b[1], false);
       const double2* eglob = nullptr;
       if (coarse_dist) {
         s_cycle(c, 1, sl->B[1], true);
@@ -2454,7 +2648,7 @@ static void s_mg_solve(hd_ctx* c, std::vector<double2*>& b, std::vector<double2*
       } else {
         eglob = cycle_at(c, 1, c->mg_b[1], true);
       }
-      for (int s = 0; s < sl->S; ++s) {
+      for (int s : sl->mine) {
         const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
         const double2* ec = coarse_dist ? vptr(sX(sl, 1)[s], Gc.bounds[s], Gc.H, Gc.n) : eglob;
         prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, G.n, Gc.n, nullptr, vptr(sX(sl, 0)[s], r0, G.H, G.n), r0, r1);
@@ -2466,7 +2660,7 @@ static void s_mg_solve(hd_ctx* c, std::vector<double2*>& b, std::vector<double2*
     }
   }
   const size_t row = static_cast<size_t>(G.n) * sizeof(double2);
-  for (int s = 0; s < sl->S; ++s)
+  for (int s : sl->mine)
     CK(cudaMemcpyAsync(out[s] + static_cast<size_t>(G.H) * G.n, sX(sl, 0)[s] + static_cast<size_t>(G.H) * G.n,
                        own(G, s) * row, cudaMemcpyDeviceToDevice, c->st));
 }
@@ -2483,11 +2677,12 @@ static void s_deflate(hd_ctx* c, std::vector<double2*>& v, std::vector<double2*>
   }
   slab_exchange(c, G, *src);
   const SlabLevel& Gc = sl->lv[1];  // the deflation coarse grid (per_dim / 2) shares level 1's rows
-  for (int s = 0; s < sl->S; ++s)
+  for (int s : sl->mine)
     restrict_(c, z, vptr((*src)[s], G.bounds[s], G.H, G.n), c->n, c->nc, nullptr, c->ep, Gc.bounds[s],
               Gc.bounds[s + 1]);
-  exact_solve_planar(c, c->E, c->ep);  // once (multi-GPU: on every rank after the allgather)
-  for (int s = 0; s < sl->S; ++s) {
+  slab_share_rows(c, Gc, c->ep, true);  // the deflation coarse vector: allgather (both planes)
+  exact_solve_planar(c, c->E, c->ep);    // redundantly on every process
+  for (int s : sl->mine) {
     const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
     if (project)
       prolong_<1>(c, z, nullptr, c->ep, c->n, c->nc, vptr(v[s], r0, G.H, G.n), vptr(out[s], r0, G.H, G.n), r0, r1);
@@ -2513,7 +2708,7 @@ static void s_op(hd_ctx* c, std::vector<double2*>& v, std::vector<double2*>& out
     s_deflate(c, *cur, out, true);
   } else {
     const SlabLevel& G = sl->lv[0];
-    for (int s = 0; s < sl->S; ++s)
+    for (int s : sl->mine)
       CK(cudaMemcpyAsync(out[s], (*cur)[s], static_cast<size_t>(own(G, s) + 2 * G.H) * G.n * sizeof(double2),
                          cudaMemcpyDeviceToDevice, c->st));
   }
@@ -2524,13 +2719,14 @@ static void s_norm(hd_ctx* c, std::vector<double2*>& v, double* dst, double2* cd
                    const double* scale_src = nullptr) {
   hd_slabs* sl = slabs_of(c);
   const SlabLevel& G = sl->lv[0];
-  for (int s = 0; s < sl->S; ++s) {
+  for (int s : sl->mine) {
     RedOut r = red_of(c, sl->slots + s);
     r.raw = 1;
     const size_t N = static_cast<size_t>(own(G, s)) * G.n;
     HD_LAUNCH(HD_K_VEC, 16.0 * N,
               k_slab_sumsq<<<std::min(grid_for(N), c->red_blocks), 256, 0, c->st>>>(v[s] + static_cast<size_t>(G.H) * G.n, N, r));
   }
+  slab_allgather(c, sl->slots, 1);
   HD_LAUNCH(HD_K_VEC, 0.0, k_slab_norm<<<1, 1, 0, c->st>>>(sl->slots, sl->S, scale_src, dst, cdst));
 }
 
@@ -2544,23 +2740,23 @@ static void s_monitor(hd_ctx* c, std::vector<double2*>& x) {  // ||f - A x|| / |
 static void s_scatter(hd_ctx* c, const double2* full, std::vector<double2*>& v) {
   hd_slabs* sl = slabs_of(c);
   const SlabLevel& G = sl->lv[0];
-  for (int s = 0; s < sl->S; ++s)
+  for (int s : sl->mine)
     CK(cudaMemcpyAsync(v[s] + static_cast<size_t>(G.H) * G.n, full + static_cast<size_t>(G.bounds[s]) * G.n,
                        static_cast<size_t>(own(G, s)) * G.n * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
 }
 static void s_gather(hd_ctx* c, const std::vector<double2*>& v, double2* full) {
   hd_slabs* sl = slabs_of(c);
   const SlabLevel& G = sl->lv[0];
-  for (int s = 0; s < sl->S; ++s)
+  for (int s : sl->mine)
     CK(cudaMemcpyAsync(full + static_cast<size_t>(G.bounds[s]) * G.n, v[s] + static_cast<size_t>(G.H) * G.n,
-                       static_cast<size_t>(own(G, s)) * G.n * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+                       static_cast<size_t>(own(G, s)) * G.n * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));  slab_share_rows(c, G, full, false);
 }
 
 // basis vector u_j of slab s <-> halo'd slab vectors
 static void s_basis_to(hd_ctx* c, int j, std::vector<double2*>& v) {
   hd_slabs* sl = slabs_of(c);
   const SlabLevel& G = sl->lv[0];
-  for (int s = 0; s < sl->S; ++s) {
+  for (int s : sl->mine) {
     const size_t Ns = static_cast<size_t>(own(G, s)) * G.n;
     CK(cudaMemcpyAsync(v[s] + static_cast<size_t>(G.H) * G.n, sl->V[s] + static_cast<size_t>(j) * Ns,
                        Ns * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
@@ -2589,7 +2785,7 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
   const SlabLevel& G = sl->lv[0];
   if (sl->maxit < maxit) {
     for (auto* p : sl->V) cudaFree(p);
-    for (int s = 0; s < sl->S; ++s) sl->V[s] = dalloc<double2>(static_cast<size_t>(maxit + 1) * own(G, s) * G.n);
+    for (int s : sl->mine) sl->V[s] = dalloc<double2>(static_cast<size_t>(maxit + 1) * own(G, s) * G.n);
     sl->maxit = maxit;
   }
   c->matvecs = c->coarse_solves = c->shift_solves = c->vcycles = 0;
@@ -2610,7 +2806,7 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
     s_deflate(c, sl->f, sl->x0, false);
     ++c->coarse_solves;
   } else {
-    for (int s = 0; s < sl->S; ++s) {
+    for (int s : sl->mine) {
       CK(cudaMemcpyAsync(sl->rhsp[s], (*b)[s], static_cast<size_t>(own(G, s) + 2 * G.H) * G.n * sizeof(double2),
                          cudaMemcpyDeviceToDevice, c->st));
       CK(cudaMemsetAsync(sl->x0[s], 0, static_cast<size_t>(own(G, s) + 2 * G.H) * G.n * sizeof(double2), c->st));
@@ -2627,7 +2823,7 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
   }
   // r = rhs' - op(x0), beta = ||r||, u_0 = r, sigma_0 = 1/beta
   s_op(c, sl->x0, sl->w);
-  for (int s = 0; s < sl->S; ++s) {
+  for (int s : sl->mine) {
     const size_t o = static_cast<size_t>(G.H) * G.n, Ns = static_cast<size_t>(own(G, s)) * G.n;
     HD_LAUNCH(HD_K_VEC, 48.0 * Ns, k_sub<<<grid_for(Ns), 256, 0, c->st>>>(sl->rhsp[s] + o, sl->w[s] + o, sl->w[s] + o, Ns));
   }
@@ -2642,13 +2838,13 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
   }
   CK(cudaMemsetAsync(c->H, 0, sizeof(double2) * (maxit + 1) * maxit, c->st));
   CK(cudaMemsetAsync(c->g + 1, 0, sizeof(double2) * maxit, c->st));
-  for (int s = 0; s < sl->S; ++s) {
+  for (int s : sl->mine) {
     const size_t Ns = static_cast<size_t>(own(G, s)) * G.n;
     CK(cudaMemcpyAsync(sl->V[s], sl->w[s] + static_cast<size_t>(G.H) * G.n, Ns * sizeof(double2),
                        cudaMemcpyDeviceToDevice, c->st));
   }
   HD_LAUNCH(HD_K_VEC, 0.0, k_inv_scalar<<<1, 1, 0, c->st>>>(c->lsa_sig, c->dres + 2));
-  const int nparts = sl->S * sl->Gs;
+  const int nparts = sl->S * sl->Gs;  // pass-2 partials (one per CTA of every slab)
   bool stop = false;
   double hnew_prev = 1.0;
   for (int j = 0; j < maxit && !stop; ++j) {
@@ -2662,16 +2858,24 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
     s_basis_to(c, j, sl->vin);
     s_op(c, sl->vin, sl->w);
     // pass 1 per slab (partials at the slab's offset), then the slab-order combination
-    for (int s = 0; s < sl->S; ++s) {
+    for (int s : sl->mine) {
       LsaArgs a = s_lsa(c, s, j, 0, maxit);
       HD_LAUNCH(HD_K_MGS, (j + 3.0) * 16.0 * a.N, k_lsa_dots<<<sl->Gs, kLsaBD, lsa_dots_smem(), c->st>>>(a));
     }
-    LsaArgs a0 = s_lsa(c, 0, j, 0, maxit);
-    HD_LAUNCH(HD_K_MGS, 0.0, k_lsa_dots_finish<<<1, kLsaBD, 0, c->st>>>(a0, nparts));
-    for (int s = 0; s < sl->S; ++s) {
+    // per-slab sums of the CTA partials (fixed order), gathered from every slab, combined in slab order
+    for (int s : sl->mine)
+      HD_LAUNCH(HD_K_MGS, 0.0, k_lsa_slab_reduce<<<1, kLsaBD, 0, c->st>>>(sl->parts + static_cast<size_t>(s) * sl->Gs * kLsaNslot,
+                                                                       sl->Gs, j, sl->red + static_cast<size_t>(s) * kLsaNslot));
+    slab_allgather(c, reinterpret_cast<double*>(sl->red), 2 * static_cast<size_t>(kLsaNslot));
+    LsaArgs a0 = s_lsa(c, sl->mine[0], j, 0, maxit);
+    LsaArgs af = a0;
+    af.partials = sl->red;
+    HD_LAUNCH(HD_K_MGS, 0.0, k_lsa_dots_finish<<<1, kLsaBD, 0, c->st>>>(af, sl->S));
+    for (int s : sl->mine) {
       LsaArgs a = s_lsa(c, s, j, 0, maxit);
       HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 5.0 : 3.0) * 16.0 * a.N, k_lsa_update<<<sl->Gs, kLsaBD, 0, c->st>>>(a));
     }
+    slab_allgather(c, reinterpret_cast<double*>(sl->parts), 2 * static_cast<size_t>(sl->Gs));
     if (j >= 1) {  // x_{j-1} is ready
       s_monitor(c, sl->x);
       read_scalars(c);
@@ -2693,7 +2897,7 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
     HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a0, nparts));
     CK(cudaMemcpyAsync(c->hres + 1, c->dres + 1, sizeof(double), cudaMemcpyDeviceToHost, c->st));
     if (j + 1 == maxit) {  // budget exhausted: x_{maxit-1}, then its monitor
-      for (int s = 0; s < sl->S; ++s) {
+      for (int s : sl->mine) {
         LsaArgs bq = s_lsa(c, s, j, 1, maxit);
         HD_LAUNCH(HD_K_ITERATE, (j + 3.0) * 16.0 * bq.N, k_lsa_update<<<sl->Gs, kLsaBD, 0, c->st>>>(bq));
       }
@@ -2713,7 +2917,7 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
 }
 
 // plan of slabs.py (gather level, doubled boundaries), built from the context's hierarchy
-static void create_slabs(hd_ctx* c, int S) {
+static void create_slabs(hd_ctx* c, int S, int rank = 0, int nranks = 1, ncclComm_t comm = nullptr) {
   if (c->dim != 2) throw Error(HD_ERR_INVALID, "row slabs: 2D only (1D configs run as replicas)");
   if (c->lev.size() < 2 || !c->spec.shift || c->spec.cycles < 1)
     throw Error(HD_ERR_INVALID, "row slabs: needs the multigrid-CSLP preconditioner (shift, cycles >= 1)");
@@ -2750,6 +2954,13 @@ static void create_slabs(hd_ctx* c, int S) {
   c->slabs = sl;
   sl->S = S;
   sl->g = g;
+  sl->rank = rank;
+  sl->nranks = nranks;
+  sl->comm = comm;
+  const char* vr = std::getenv("HD_SLAB_VRANKS");
+  sl->vranks = nranks == 1 && vr && std::atoi(vr) == 1;
+  for (int s = 0; s < S; ++s)
+    if (nranks == 1 || s == rank) sl->mine.push_back(s);
   sl->lv.resize(L);
   for (int l = 0; l < L; ++l) {
     SlabLevel& G = sl->lv[l];
@@ -2765,19 +2976,20 @@ static void create_slabs(hd_ctx* c, int S) {
   sl->R.resize(g);
   sl->cur.assign(L, 0);
   for (int l = 0; l < g; ++l) {
-    sl->X[l] = slab_alloc(sl->lv[l], S);
-    sl->Y[l] = slab_alloc(sl->lv[l], S);
-    if (l > 0) sl->B[l] = slab_alloc(sl->lv[l], S);
-    sl->R[l] = slab_alloc(sl->lv[l], S);
+    sl->X[l] = slab_alloc(sl->lv[l], S, sl);
+    sl->Y[l] = slab_alloc(sl->lv[l], S, sl);
+    if (l > 0) sl->B[l] = slab_alloc(sl->lv[l], S, sl);
+    sl->R[l] = slab_alloc(sl->lv[l], S, sl);
   }
   for (auto* v : {&sl->f, &sl->w, &sl->t1, &sl->t2, &sl->t3, &sl->x, &sl->x0, &sl->rhsp, &sl->vin})
-    *v = slab_alloc(sl->lv[0], S);
+    *v = slab_alloc(sl->lv[0], S, sl);
   sl->V.assign(S, nullptr);
   sl->slots = dalloc<double>(S);
   // Arnoldi grid per slab and the partials of all slabs
   const size_t Nmax = static_cast<size_t>(*std::max_element(bnd[0].begin() + 1, bnd[0].end())) * c->n;
   sl->Gs = std::max(1, std::min(c->lsa_G > 0 ? c->lsa_G : 296, static_cast<int>((Nmax + 1023) / 1024)));
   sl->parts = dalloc<double2>(static_cast<size_t>(S) * sl->Gs * (2 * kLsaMaxJ + 2) + 8);
+  sl->red = dalloc<double2>(static_cast<size_t>(S) * kLsaNslot);
   CK(cudaDeviceSynchronize());
 }
 
@@ -2794,6 +3006,8 @@ static void destroy_slabs(hd_ctx* c) {
   for (auto* v : {&sl->f, &sl->w, &sl->t1, &sl->t2, &sl->t3, &sl->x, &sl->x0, &sl->rhsp, &sl->vin, &sl->V}) fr(*v);
   cudaFree(sl->slots);
   cudaFree(sl->parts);
+  cudaFree(sl->red);
+  if (sl->comm) nccl().CommDestroy(sl->comm);
   delete sl;
   c->slabs = nullptr;
 }
@@ -2895,6 +3109,42 @@ hd_status hd_create_slabs(const hd_system* sys, const hd_precond* spec, int nsla
   create_ctx(sys, spec, nullptr, 0, &c);
   try {
     create_slabs(c, nslabs);
+  } catch (...) {
+    destroy_ctx(c);
+    throw;
+  }
+  *out = c;
+  HD_GUARD_END
+}
+
+hd_status hd_nccl_unique_id(unsigned char* out) {
+  HD_GUARD_BEGIN
+  if (!out) throw Error(HD_ERR_INVALID, "null argument");
+  ncclUniqueId id;
+  CKN(nccl().GetUniqueId(&id));
+  std::memcpy(out, id.internal, sizeof(id.internal));
+  HD_GUARD_END
+}
+
+hd_status hd_create_dist(const hd_system* sys, const hd_precond* spec, int rank, int nranks,
+                         const unsigned char* nccl_id, int device, hd_ctx** out) {
+  HD_GUARD_BEGIN
+  if (!out || !nccl_id || nranks < 1 || rank < 0 || rank >= nranks) throw Error(HD_ERR_INVALID, "bad rank / nranks");
+  hd_ctx* c = nullptr;
+  const int dev[1] = {device};
+  create_ctx(sys, spec, dev, 1, &c);
+  try {
+    ncclUniqueId id;
+    std::memcpy(id.internal, nccl_id, sizeof(id.internal));
+    ncclComm_t comm = nullptr;
+    CK(cudaSetDevice(device));
+    CKN(nccl().CommInitRank(&comm, nranks, id, rank));
+    try {
+      create_slabs(c, nranks, rank, nranks, comm);
+    } catch (...) {
+      nccl().CommDestroy(comm);
+      throw;
+    }
   } catch (...) {
     destroy_ctx(c);
     throw;

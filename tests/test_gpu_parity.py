@@ -413,14 +413,19 @@ def test_exact_shifted_inverse_C_ex(problem, p, k, beta2):
 
 
 # ---- row slabs ---------------------------------------------
+@pytest.mark.parametrize("vranks", [0, 1])
 @pytest.mark.parametrize("S,ne,p,k,agg", [(2, 130, 3, 60.0, 40), (3, 200, 2, 100.0, 60), (4, 320, 2, 200.0, 200),
                                           (8, 256, 2, 120.0, 40)])
-def test_row_slabs_match_single_domain(S, ne, p, k, agg, monkeypatch):
+def test_row_slabs_match_single_domain(S, ne, p, k, agg, vranks, monkeypatch):
     """The slab program (halo'd slab buffers, halo copies, gathered coarse levels
     and E, slab-order reductions) on one device against the single-domain solve:
-    components to 1e-10, equal iterations and counts, history 1e-10, solution 1e-8."""
+    components to 1e-10, equal iterations and counts, history 1e-10, solution 1e-8.
+    vranks = 1: every slab is its own virtual rank, so each halo transfer goes
+    through the posted send/recv records of the multi-process (NCCL) program,
+    matched by (sender, receiver, order) and checked for equal sizes."""
     import torch
     monkeypatch.setenv("HD_SLAB_AGGLOMERATE", str(agg))
+    monkeypatch.setenv("HD_SLAB_VRANKS", str(vranks))
     s = hd.assemble(hd.point_source_2d(ne, p, k))
     spec = hd.to_spec("DC_MG", p, k, **BASE)
     rng = np.random.default_rng(5)
@@ -441,6 +446,22 @@ def test_row_slabs_match_single_domain(S, ne, p, k, agg, monkeypatch):
     assert r2.converged == r1.converged and r2.iterations == r1.iterations
     assert (r2.counts.matvecs, r2.counts.coarse_solves, r2.counts.shift_solves, r2.counts.vcycles) == \
         (r1.counts.matvecs, r1.counts.coarse_solves, r1.counts.shift_solves, r1.counts.vcycles)
+    assert np.max(np.abs(np.array(r2.residuals) - np.array(r1.residuals))) <= 1e-10
+    assert np.linalg.norm(r2.solution - r1.solution) <= 1e-8 * np.linalg.norm(r1.solution)
+
+
+def test_dist_single_process_nccl():
+    """hd_create_dist at nranks = 1: NCCL loaded at run time, a one-rank
+    communicator, the one-slab program; equal to the single-domain solve."""
+    s = hd.assemble(hd.point_source_2d(130, 3, 60.0))
+    spec = hd.to_spec("DC_MG", 3, 60.0, **BASE)
+    uid = hd.nccl_unique_id()
+    assert len(uid) == 128
+    with hd.Solver(s, spec) as one, hd.Solver(s, spec, dist=(0, 1, uid, 0)) as d:
+        assert d.slabs == 1
+        r1 = one.solve(hd.GmresOptions(100, 1e-7))
+        r2 = d.solve(hd.GmresOptions(100, 1e-7))
+    assert r2.converged == r1.converged and r2.iterations == r1.iterations
     assert np.max(np.abs(np.array(r2.residuals) - np.array(r1.residuals))) <= 1e-10
     assert np.linalg.norm(r2.solution - r1.solution) <= 1e-8 * np.linalg.norm(r1.solution)
 
