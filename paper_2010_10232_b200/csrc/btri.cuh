@@ -1,7 +1,8 @@
-// Exact solve of a real 2D level operator that is not a Kronecker sum (the
-// deflation matrix E = Z^T A Z of the wedge and layered fields) as a block
-// tridiagonal system, standing in for the reference's Eigen::SparseLU of E
-// (src/precond.cpp:95-99, 103).
+// Exact solve of a 2D level operator that is not a Kronecker sum as a block
+// tridiagonal system, standing in for the reference's Eigen::SparseLU: the
+// deflation matrix E = Z^T A Z of the wedge and layered fields (real;
+// src/precond.cpp:95-99, 103) and the whole shifted operator of C_ex on those
+// fields (complex; src/precond.cpp:204-211).
 //
 // Ordering the unknowns lexicographically (x fastest) and grouping q = b grid
 // rows (b = the stencil's half-width in y) into one "super-row" of m = q*n
@@ -11,7 +12,8 @@
 //
 //   S_0 = D_0,  S_i = D_i - G_i B_{i-1},  G_i = C_i S_{i-1}^-1,  H_i = S_i^-1 B_i,
 //
-// and per solve (re and im planes are two real right-hand sides):
+// and per solve (real operator: the re and im planes are two real right-hand
+// sides; complex operator: one complex right-hand side, planar):
 //
 //   y_i = r_i - G_i y_{i-1}          (nb sequential steps)
 //   w_i = S_i^-1 y_i                 (all blocks in parallel)
@@ -31,15 +33,32 @@
 
 namespace hd {
 
-// warps per CTA by the registers a row needs per lane
-__host__ __device__ constexpr int btri_threads(int kr) { return kr <= 16 ? 512 : (kr <= 32 ? 384 : 256); }
+// scalar helpers over double (real operator) and double2 (complex operator)
+__device__ __forceinline__ double bt_zero(double) { return 0.0; }
+__device__ __forceinline__ double2 bt_zero(double2) { return cmk(0.0, 0.0); }
+__device__ __forceinline__ void bt_set(double& d, double2 v) { d = v.x; }
+__device__ __forceinline__ void bt_set(double2& d, double2 v) { d = v; }
+__device__ __forceinline__ double bt_one(double) { return 1.0; }
+__device__ __forceinline__ double2 bt_one(double2) { return cmk(1.0, 0.0); }
+// acc (re, im) += a * (vr + i vi)
+__device__ __forceinline__ void bt_fma(double a, double vr, double vi, double& sr, double& si) {
+  sr = fma(a, vr, sr);
+  si = fma(a, vi, si);
+}
+__device__ __forceinline__ void bt_fma(double2 a, double vr, double vi, double& sr, double& si) {
+  sr = fma(a.x, vr, fma(-a.y, vi, sr));
+  si = fma(a.x, vi, fma(a.y, vr, si));
+}
+
+// warps per CTA by the registers a row needs per lane (doubles per lane)
+__host__ __device__ constexpr int btri_threads(int regs) { return regs <= 16 ? 512 : (regs <= 32 ? 384 : 256); }
 
 struct BtriArgs {
   int n, q, m, nb;     // grid side, rows per block, block size m = q*n, blocks
   size_t NN;           // n^2 (unknowns); padded length nb*m
-  const double* GT;    // nb blocks, row-major: G_i (block 0 unused)
-  const double* SinvT; // nb blocks, row-major: S_i^-1
-  const double* HT;    // nb blocks, row-major: H_i (block nb-1 unused)
+  const void* GT;      // nb blocks, row-major: G_i (block 0 unused)      [double or double2]
+  const void* SinvT;   // nb blocks, row-major: S_i^-1
+  const void* HT;      // nb blocks, row-major: H_i (block nb-1 unused)
   double* y;           // 2 planes x nb*m
   double* w;           // 2 planes x nb*m
   double* x;           // 2 planes x nb*m
@@ -48,9 +67,10 @@ struct BtriArgs {
 };
 
 // Column-major m x m blocks D_i, B_i (= E[i, i+1]), C_i (= E[i, i-1]) of the
-// real part of the level operator (coefficients must be real).
-__global__ void k_btri_blocks(GenLevel L, int q, int m, int nb, double* __restrict__ D, double* __restrict__ Bu,
-                              double* __restrict__ Cl) {
+// level operator (T = double: its real part; the coefficients must be real).
+template <class T>
+__global__ void k_btri_blocks(GenLevel L, int q, int m, int nb, T* __restrict__ D, T* __restrict__ Bu,
+                              T* __restrict__ Cl) {
   const int n = L.n;
   const size_t mm = (size_t)m * m, tot = (size_t)nb * mm;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
@@ -58,18 +78,18 @@ __global__ void k_btri_blocks(GenLevel L, int q, int m, int nb, double* __restri
     const size_t rem = e % mm;
     const int a = (int)(rem % m), c = (int)(rem / m);  // column-major (row a, column c)
     const int iy = i * q + a / n, ix = a % n;
-    double d = 0.0, bu = 0.0, cl = 0.0;
+    T d = bt_zero(T()), bu = bt_zero(T()), cl = bt_zero(T());
     if (iy < n) {
       // diagonal block: column c is unknown (i*q + c/n, c%n)
       const int jy = i * q + c / n, jx = c % n;
       const int dy = jy - iy, dx = jx - ix;
-      if (jy < n && dy >= -L.b && dy <= L.b && dx >= -L.b && dx <= L.b) d = gen_entry(L, iy, ix, dy, dx).x;
+      if (jy < n && dy >= -L.b && dy <= L.b && dx >= -L.b && dx <= L.b) bt_set(d, gen_entry(L, iy, ix, dy, dx));
       const int jyu = (i + 1) * q + c / n, dyu = jyu - iy;
-      if (jyu < n && dyu <= L.b && dx >= -L.b && dx <= L.b) bu = gen_entry(L, iy, ix, dyu, dx).x;
+      if (jyu < n && dyu <= L.b && dx >= -L.b && dx <= L.b) bt_set(bu, gen_entry(L, iy, ix, dyu, dx));
       const int jyl = (i - 1) * q + c / n, dyl = jyl - iy;
-      if (i > 0 && dyl >= -L.b && dx >= -L.b && dx <= L.b) cl = gen_entry(L, iy, ix, dyl, dx).x;
+      if (i > 0 && dyl >= -L.b && dx >= -L.b && dx <= L.b) bt_set(cl, gen_entry(L, iy, ix, dyl, dx));
     } else if (a == c) {
-      d = 1.0;  // padding unknown
+      d = bt_one(T());  // padding unknown
     }
     D[e] = d;
     Bu[e] = bu;
@@ -77,14 +97,14 @@ __global__ void k_btri_blocks(GenLevel L, int q, int m, int nb, double* __restri
   }
 }
 
-// One matrix row (m doubles, lane-strided into KR registers).
-template <int KR>
-__device__ __forceinline__ void btri_row_load(const double* __restrict__ row, int m, double (&r)[KR]) {
+// One matrix row (m entries, lane-strided into KR registers).
+template <class T, int KR>
+__device__ __forceinline__ void btri_row_load(const T* __restrict__ row, int m, T (&r)[KR]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
     const int c = lane + 32 * k;
-    r[k] = c < m ? __ldcs(row + c) : 0.0;
+    r[k] = c < m ? __ldcs(row + c) : bt_zero(T());
   }
 }
 
@@ -107,9 +127,10 @@ __device__ __forceinline__ void btri_wait(unsigned* bar, unsigned target) {
   __syncthreads();
 }
 
-// Plain (barrier-ordered) row dot of both planes of a vector.
-template <int KR>
-__device__ __forceinline__ double2 btri_row_dot_b(const double (&r)[KR], const double* v, size_t plane, int m) {
+// Row dot with a planar vector (re plane at v, im plane at v + plane) that
+// other CTAs wrote before the last barrier (L2-coherent loads).
+template <class T, int KR>
+__device__ __forceinline__ double2 btri_row_dot(const T (&r)[KR], const double* v, size_t plane, int m) {
   const int lane = threadIdx.x & 31;
   double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
 #pragma unroll
@@ -117,13 +138,8 @@ __device__ __forceinline__ double2 btri_row_dot_b(const double (&r)[KR], const d
     const int c = lane + 32 * k;
     if (c < m) {
       const double vr = __ldcg(v + c), vi = __ldcg(v + plane + c);
-      if (k & 1) {
-        sr1 = fma(r[k], vr, sr1);
-        si1 = fma(r[k], vi, si1);
-      } else {
-        sr0 = fma(r[k], vr, sr0);
-        si0 = fma(r[k], vi, si0);
-      }
+      if (k & 1) bt_fma(r[k], vr, vi, sr1, si1);
+      else bt_fma(r[k], vr, vi, sr0, si0);
     }
   }
   double sr = sr0 + sr1, si = si0 + si1;
@@ -144,8 +160,8 @@ __device__ __forceinline__ double2 btri_row_dot_b(const double (&r)[KR], const d
 // into registers between arriving at and waiting on the barrier, so the HBM
 // fetch of the step matrices overlaps the barrier (as do its right-hand-side
 // reads); further tasks (2m > warps) load after the wait.
-template <int KR>
-__global__ void __launch_bounds__(btri_threads(KR), 1) k_btri_solve(BtriArgs a) {
+template <class T, int KR>
+__global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_btri_solve(BtriArgs a) {
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
@@ -153,10 +169,13 @@ __global__ void __launch_bounds__(btri_threads(KR), 1) k_btri_solve(BtriArgs a) 
   const int m = a.m, nb = a.nb;
   const size_t mm = (size_t)m * m, P = (size_t)nb * m;
   const unsigned G = gridDim.x;
+  const T* GT = static_cast<const T*>(a.GT);
+  const T* SinvT = static_cast<const T*>(a.SinvT);
+  const T* HT = static_cast<const T*>(a.HT);
   unsigned phase = 0;
-  double r[KR];
-  auto frow = [&](int i, int t) -> const double* {
-    return t < m ? a.GT + i * mm + (size_t)t * m : a.SinvT + (i - 1) * mm + (size_t)(t - m) * m;
+  T r[KR];
+  auto frow = [&](int i, int t) -> const T* {
+    return t < m ? GT + i * mm + (size_t)t * m : SinvT + (i - 1) * mm + (size_t)(t - m) * m;
   };
   // ---- forward ----
   for (int i = 0; i < nb; ++i) {
@@ -172,8 +191,8 @@ __global__ void __launch_bounds__(btri_threads(KR), 1) k_btri_solve(BtriArgs a) 
       }
       double2 acc = cmk(0.0, 0.0);
       if (i > 0) {
-        if (t != gw) btri_row_load<KR>(frow(i, t), m, r);
-        acc = btri_row_dot_b<KR>(r, a.y + (size_t)(i - 1) * m, P, m);
+        if (t != gw) btri_row_load<T, KR>(frow(i, t), m, r);
+        acc = btri_row_dot<T, KR>(r, a.y + (size_t)(i - 1) * m, P, m);
       }
       if (lane == 0) {
         double* dst = yrow ? a.y + gi : a.w + gi - m;
@@ -183,9 +202,9 @@ __global__ void __launch_bounds__(btri_threads(KR), 1) k_btri_solve(BtriArgs a) 
     }
     btri_arrive(a.bar);
     if (i + 1 < nb) {
-      if (gw < 2 * m) btri_row_load<KR>(frow(i + 1, gw), m, r);
+      if (gw < 2 * m) btri_row_load<T, KR>(frow(i + 1, gw), m, r);
     } else if (gw < m) {
-      btri_row_load<KR>(a.SinvT + (nb - 1) * mm + (size_t)gw * m, m, r);
+      btri_row_load<T, KR>(SinvT + (nb - 1) * mm + (size_t)gw * m, m, r);
     }
     btri_wait(a.bar, ++phase * G);
   }
@@ -195,14 +214,14 @@ __global__ void __launch_bounds__(btri_threads(KR), 1) k_btri_solve(BtriArgs a) 
       const size_t gi = (size_t)i * m + row;
       double xr, xi;
       if (i == nb - 1) {
-        if (row != gw) btri_row_load<KR>(a.SinvT + i * mm + (size_t)row * m, m, r);
-        const double2 acc = btri_row_dot_b<KR>(r, a.y + (size_t)i * m, P, m);
+        if (row != gw) btri_row_load<T, KR>(SinvT + i * mm + (size_t)row * m, m, r);
+        const double2 acc = btri_row_dot<T, KR>(r, a.y + (size_t)i * m, P, m);
         xr = acc.x;
         xi = acc.y;
       } else {
         const double wr = lane == 0 ? __ldcg(a.w + gi) : 0.0, wi = lane == 0 ? __ldcg(a.w + P + gi) : 0.0;
-        if (row != gw) btri_row_load<KR>(a.HT + i * mm + (size_t)row * m, m, r);
-        const double2 acc = btri_row_dot_b<KR>(r, a.x + (size_t)(i + 1) * m, P, m);
+        if (row != gw) btri_row_load<T, KR>(HT + i * mm + (size_t)row * m, m, r);
+        const double2 acc = btri_row_dot<T, KR>(r, a.x + (size_t)(i + 1) * m, P, m);
         xr = wr - acc.x;
         xi = wi - acc.y;
       }
@@ -217,7 +236,7 @@ __global__ void __launch_bounds__(btri_threads(KR), 1) k_btri_solve(BtriArgs a) 
     }
     if (i > 0) {
       btri_arrive(a.bar);
-      if (gw < m) btri_row_load<KR>(a.HT + (i - 1) * mm + (size_t)gw * m, m, r);
+      if (gw < m) btri_row_load<T, KR>(HT + (i - 1) * mm + (size_t)gw * m, m, r);
       btri_wait(a.bar, ++phase * G);
     }
   }

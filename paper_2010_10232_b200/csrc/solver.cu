@@ -120,6 +120,7 @@ struct ExactSolver {
   double2 *dx = nullptr, *dy = nullptr;
   // block tridiagonal (btri.cuh): real non-Kronecker operators too large for a dense inverse
   bool btri = false;
+  bool bt_cplx = false;  // complex operator (C_ex on a non-separable field)
   BtriArgs bt{};
   int bt_kr = 0;
 };
@@ -638,8 +639,8 @@ static void free_exact(ExactSolver& X) {
   }
   cudaFree(X.Ainv); cudaFree(X.dx); cudaFree(X.dy);
   if (X.btri) {
-    cudaFree(const_cast<double*>(X.bt.GT)); cudaFree(const_cast<double*>(X.bt.SinvT));
-    cudaFree(const_cast<double*>(X.bt.HT)); cudaFree(X.bt.y); cudaFree(X.bt.bar);
+    cudaFree(const_cast<void*>(X.bt.GT)); cudaFree(const_cast<void*>(X.bt.SinvT));
+    cudaFree(const_cast<void*>(X.bt.HT)); cudaFree(X.bt.y); cudaFree(X.bt.bar);
   }
   X = ExactSolver{};
 }
@@ -942,38 +943,44 @@ static void dense_apply(hd_ctx* c, const ExactSolver& X, const double2* x, doubl
 }
 
 // Block tridiagonal exact solve (btri.cuh), in/out planar.
-template <int KR>
+template <class T, int KR>
 static void btri_launch_t(hd_ctx* c, ExactSolver& X) {
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(k_btri_solve<KR>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CK(cudaFuncSetAttribute(k_btri_solve<T, KR>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c->n_sms);
-  cfg.blockDim = dim3(btri_threads(KR));
+  cfg.blockDim = dim3(btri_threads(KR * static_cast<int>(sizeof(T) / 8)));
   cfg.stream = c->st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeCooperative;
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k_btri_solve<KR>, X.bt));
+  CK(cudaLaunchKernelEx(&cfg, k_btri_solve<T, KR>, X.bt));
 }
 
 static void btri_solve(hd_ctx* c, ExactSolver& X, double* inout) {
   X.bt.io = inout;
   CK(cudaMemsetAsync(X.bt.bar, 0, sizeof(unsigned), c->st));
-  const double mm = static_cast<double>(X.bt.m) * X.bt.m;
+  const double mm = static_cast<double>(X.bt.m) * X.bt.m * (X.bt_cplx ? 2.0 : 1.0);
   HD_LAUNCH(HD_K_EXACT, 8.0 * mm * (3.0 * X.bt.nb - 2.0) + 32.0 * X.bt.NN,
-            switch (X.bt_kr) {
-              case 8: btri_launch_t<8>(c, X); break;
-              case 16: btri_launch_t<16>(c, X); break;
-              case 24: btri_launch_t<24>(c, X); break;
-              case 32: btri_launch_t<32>(c, X); break;
-              case 48: btri_launch_t<48>(c, X); break;
-              case 64: btri_launch_t<64>(c, X); break;
-              default: btri_launch_t<96>(c, X); break;
+            if (X.bt_cplx) switch (X.bt_kr) {
+              case 8: btri_launch_t<double2, 8>(c, X); break;
+              case 16: btri_launch_t<double2, 16>(c, X); break;
+              case 24: btri_launch_t<double2, 24>(c, X); break;
+              case 32: btri_launch_t<double2, 32>(c, X); break;
+              default: btri_launch_t<double2, 48>(c, X); break;
+            } else switch (X.bt_kr) {
+              case 8: btri_launch_t<double, 8>(c, X); break;
+              case 16: btri_launch_t<double, 16>(c, X); break;
+              case 24: btri_launch_t<double, 24>(c, X); break;
+              case 32: btri_launch_t<double, 32>(c, X); break;
+              case 48: btri_launch_t<double, 48>(c, X); break;
+              case 64: btri_launch_t<double, 64>(c, X); break;
+              default: btri_launch_t<double, 96>(c, X); break;
             });
 }
 
@@ -1899,10 +1906,9 @@ static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int 
 static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl, int n_sms = 148) {
   const int n = h.Y[0].n;
   const size_t NN = static_cast<size_t>(n) * n;
-  // real operators (E) beyond the dense-inverse limit, or HD_BTRI=1: block tridiagonal LU
+  // operators beyond the dense-inverse limit, or HD_BTRI=1: block tridiagonal LU
   const char* fb = std::getenv("HD_BTRI");
-  if (cl.y == 0.0 && (NN > 20000 || (fb && std::atoi(fb) == 1) ) && !(fb && std::atoi(fb) == 0))
-    return make_btri(st, h, cl, n_sms);
+  if ((NN > 20000 || (fb && std::atoi(fb) == 1)) && !(fb && std::atoi(fb) == 0)) return make_btri(st, h, cl, n_sms);
   if (NN > 20000)
     throw Error(HD_ERR_INVALID, "non-separable field: exact solve of " + std::to_string(NN) +
                                     " complex unknowns exceeds the dense-inverse limit (20000)");
@@ -1947,33 +1953,61 @@ static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl, int
   return X;
 }
 
-// Block tridiagonal LU of a real level operator (btri.cuh): q = b grid rows per block.
-static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int n_sms) {
-  const int n = h.Y[0].n;
-  double* mem = nullptr;
-  const GenLevel L = upload_gen(h, cl, &mem);
-  for (int g = 0; g < L.G; ++g)
-    if (L.coef[g].y != 0.0) throw Error(HD_ERR_INVALID, "block tridiagonal solve needs a real operator");
-  const int q = std::max(L.b, 1), m = q * n, nb = (n + q - 1) / q;
-  const int kr_need = (m + 31) / 32;
-  int kr = 0;
-  for (int cand : {8, 16, 24, 32, 48, 64, 96})
-    if (cand >= kr_need) {
-      kr = cand;
-      break;
-    }
-  if (kr == 0) throw Error(HD_ERR_INVALID, "block tridiagonal solve: block size " + std::to_string(m) + " > 3072");
+// Block tridiagonal LU of a level operator (btri.cuh): q = b grid rows per
+// block; real (T = double) when every coefficient is real, else complex.
+template <class T>
+struct BtriLib;
+template <>
+struct BtriLib<double> {
+  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, const double* al,
+                             const double* A, const double* B, const double* be, double* C) {
+    return cublasDgemm(h, ta, tb, m, m, m, al, A, m, B, m, be, C, m);
+  }
+  static cusolverStatus_t getrf_ws(cusolverDnHandle_t h, int m, double* A, int* lw) {
+    return cusolverDnDgetrf_bufferSize(h, m, m, A, m, lw);
+  }
+  static cusolverStatus_t getrf(cusolverDnHandle_t h, int m, double* A, double* w, int* piv, int* info) {
+    return cusolverDnDgetrf(h, m, m, A, m, w, piv, info);
+  }
+  static cusolverStatus_t getrs_t(cusolverDnHandle_t h, int m, const double* A, const int* piv, double* B, int* info) {
+    return cusolverDnDgetrs(h, CUBLAS_OP_T, m, m, A, m, piv, B, m, info);
+  }
+  static double one() { return 1.0; }
+  static double mone() { return -1.0; }
+  static double zero() { return 0.0; }
+};
+template <>
+struct BtriLib<double2> {
+  using Z = cuDoubleComplex;
+  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, const double2* al,
+                             const double2* A, const double2* B, const double2* be, double2* C) {
+    return cublasZgemm(h, ta, tb, m, m, m, reinterpret_cast<const Z*>(al), reinterpret_cast<const Z*>(A), m,
+                       reinterpret_cast<const Z*>(B), m, reinterpret_cast<const Z*>(be), reinterpret_cast<Z*>(C), m);
+  }
+  static cusolverStatus_t getrf_ws(cusolverDnHandle_t h, int m, double2* A, int* lw) {
+    return cusolverDnZgetrf_bufferSize(h, m, m, reinterpret_cast<Z*>(A), m, lw);
+  }
+  static cusolverStatus_t getrf(cusolverDnHandle_t h, int m, double2* A, double2* w, int* piv, int* info) {
+    return cusolverDnZgetrf(h, m, m, reinterpret_cast<Z*>(A), m, reinterpret_cast<Z*>(w), piv, info);
+  }
+  static cusolverStatus_t getrs_t(cusolverDnHandle_t h, int m, const double2* A, const int* piv, double2* B, int* info) {
+    // plain transpose (not conjugate): the stored factors are the row-major blocks
+    return cusolverDnZgetrs(h, CUBLAS_OP_T, m, m, reinterpret_cast<const Z*>(A), m, piv, reinterpret_cast<Z*>(B), m, info);
+  }
+  static double2 one() { return cmk(1.0, 0.0); }
+  static double2 mone() { return cmk(-1.0, 0.0); }
+  static double2 zero() { return cmk(0.0, 0.0); }
+};
+
+template <class T>
+static void btri_factor(cudaStream_t st, const GenLevel& L, int q, int m, int nb, ExactSolver& X) {
+  using Lb = BtriLib<T>;
   const size_t mm = static_cast<size_t>(m) * m, tot = static_cast<size_t>(nb) * mm;
-  ExactSolver X;
-  X.dim = 2;
-  X.n = n;
-  X.btri = true;
-  X.bt_kr = kr;
-  double *D = dalloc<double>(tot), *Bu = dalloc<double>(tot), *Cl = dalloc<double>(tot);
-  double *GT = dalloc<double>(tot), *SinvT = dalloc<double>(tot), *HT = dalloc<double>(tot);
-  CK(cudaMemsetAsync(GT, 0, mm * sizeof(double), st));
-  CK(cudaMemsetAsync(HT + (nb - 1) * mm, 0, mm * sizeof(double), st));
-  k_btri_blocks<<<grid_for(tot, 256, 148 * 32), 256, 0, st>>>(L, q, m, nb, D, Bu, Cl);
+  T *D = dalloc<T>(tot), *Bu = dalloc<T>(tot), *Cl = dalloc<T>(tot);
+  T *GT = dalloc<T>(tot), *SinvT = dalloc<T>(tot), *HT = dalloc<T>(tot);
+  CK(cudaMemsetAsync(GT, 0, mm * sizeof(T), st));
+  CK(cudaMemsetAsync(HT + (nb - 1) * mm, 0, mm * sizeof(T), st));
+  k_btri_blocks<T><<<grid_for(tot, 256, 148 * 32), 256, 0, st>>>(L, q, m, nb, D, Bu, Cl);
   CK(cudaGetLastError());
   cublasHandle_t cb;
   CKB(cublasCreate(&cb));
@@ -1982,27 +2016,27 @@ static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int 
   CKS(cusolverDnCreate(&hs));
   CKS(cusolverDnSetStream(hs, st));
   int lwork = 0;
-  CKS(cusolverDnDgetrf_bufferSize(hs, m, m, D, m, &lwork));
-  double* work = dalloc<double>(std::max(lwork, 1));
+  CKS(Lb::getrf_ws(hs, m, D, &lwork));
+  T* work = dalloc<T>(std::max(lwork, 1));
   int* ipiv = dalloc<int>(m);
   int* info = dalloc<int>(2 * nb);
   CK(cudaMemsetAsync(info, 0, 2 * nb * sizeof(int), st));
-  std::vector<double> eye(mm, 0.0);
-  for (int i = 0; i < m; ++i) eye[i + static_cast<size_t>(i) * m] = 1.0;
-  const double one = 1.0, mone = -1.0, zero = 0.0;
+  std::vector<T> eye(mm);
+  for (size_t e = 0; e < mm; ++e) eye[e] = (e % (m + 1) == 0) ? Lb::one() : Lb::zero();
+  const T one = Lb::one(), mone = Lb::mone(), zero = Lb::zero();
   for (int i = 0; i < nb; ++i) {
-    double* S = D + i * mm;  // S_i overwrites D_i
+    T* S = D + i * mm;  // S_i overwrites D_i
     // S_i = D_i - G_i B_{i-1}   (G_i = (G_i^T)^T)
-    if (i > 0) CKB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, m, &mone, GT + i * mm, m, Bu + (i - 1) * mm, m, &one, S, m));
-    CKS(cusolverDnDgetrf(hs, m, m, S, m, work, ipiv, info + 2 * i));
+    if (i > 0) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, GT + i * mm, Bu + (i - 1) * mm, &one, S));
+    CKS(Lb::getrf(hs, m, S, work, ipiv, info + 2 * i));
     // S_i^-T = solve(S_i^T X = I)
-    double* Si = SinvT + i * mm;
-    CK(cudaMemcpyAsync(Si, eye.data(), mm * sizeof(double), cudaMemcpyHostToDevice, st));
-    CKS(cusolverDnDgetrs(hs, CUBLAS_OP_T, m, m, S, m, ipiv, Si, m, info + 2 * i + 1));
+    T* Si = SinvT + i * mm;
+    CK(cudaMemcpyAsync(Si, eye.data(), mm * sizeof(T), cudaMemcpyHostToDevice, st));
+    CKS(Lb::getrs_t(hs, m, S, ipiv, Si, info + 2 * i + 1));
     if (i + 1 < nb) {
       // G_{i+1}^T = S_i^-T C_{i+1}^T ;  H_i^T = B_i^T S_i^-T
-      CKB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, m, m, &one, Si, m, Cl + (i + 1) * mm, m, &zero, GT + (i + 1) * mm, m));
-      CKB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, m, &one, Bu + i * mm, m, Si, m, &zero, HT + i * mm, m));
+      CKB(Lb::gemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, &one, Si, Cl + (i + 1) * mm, &zero, GT + (i + 1) * mm));
+      CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &one, Bu + i * mm, Si, &zero, HT + i * mm));
     }
   }
   std::vector<int> hinfo(2 * nb);
@@ -2010,20 +2044,52 @@ static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int 
   CK(cudaStreamSynchronize(st));
   cublasDestroy(cb);
   cusolverDnDestroy(hs);
-  cudaFree(D); cudaFree(Bu); cudaFree(Cl); cudaFree(work); cudaFree(ipiv); cudaFree(info); cudaFree(mem);
+  cudaFree(D); cudaFree(Bu); cudaFree(Cl); cudaFree(work); cudaFree(ipiv); cudaFree(info);
   for (int v : hinfo)
     if (v != 0) {
       cudaFree(GT); cudaFree(SinvT); cudaFree(HT);
       throw Error(HD_ERR_FACTOR, "block tridiagonal exact solve: singular block (info " + std::to_string(v) + ")");
     }
+  X.bt.GT = GT;
+  X.bt.SinvT = SinvT;
+  X.bt.HT = HT;
+}
+
+static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int n_sms) {
+  const int n = h.Y[0].n;
+  double* mem = nullptr;
+  const GenLevel L = upload_gen(h, cl, &mem);
+  bool cplx = L.K && L.kc.y != 0.0;
+  for (int g = 0; g < L.G; ++g) cplx = cplx || L.coef[g].y != 0.0;
+  const int q = std::max(L.b, 1), m = q * n, nb = (n + q - 1) / q;
+  const int kr_need = (m + 31) / 32;
+  int kr = 0;
+  for (int cand : {8, 16, 24, 32, 48, 64, 96})
+    if (cand >= kr_need && (!cplx || cand <= 48)) {
+      kr = cand;
+      break;
+    }
+  if (kr == 0)
+    throw Error(HD_ERR_INVALID, "block tridiagonal solve: block size " + std::to_string(m) + " above the kernel limit");
+  ExactSolver X;
+  X.dim = 2;
+  X.n = n;
+  X.btri = true;
+  X.bt_cplx = cplx;
+  X.bt_kr = kr;
+  try {
+    if (cplx) btri_factor<double2>(st, L, q, m, nb, X);
+    else btri_factor<double>(st, L, q, m, nb, X);
+  } catch (...) {
+    cudaFree(mem);
+    throw;
+  }
+  cudaFree(mem);
   X.bt.n = n;
   X.bt.q = q;
   X.bt.m = m;
   X.bt.nb = nb;
   X.bt.NN = static_cast<size_t>(n) * n;
-  X.bt.GT = GT;
-  X.bt.SinvT = SinvT;
-  X.bt.HT = HT;
   // y, w, x: one allocation
   X.bt.y = dalloc<double>(6 * static_cast<size_t>(nb) * m);
   X.bt.w = X.bt.y + 2 * static_cast<size_t>(nb) * m;
@@ -2098,8 +2164,6 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   if (gen && sys->dim != 2) throw Error(HD_ERR_INVALID, "the layered and wedge fields are two-dimensional");
   if (layered && !sys->interval_mass) throw Error(HD_ERR_INVALID, "layered field needs the interval masses");
   if (wedge && !sys->shift_mass_2d) throw Error(HD_ERR_INVALID, "wedge field needs shift_mass_2d (hd_assemble_field)");
-  if (gen && spec->shift && spec->cycles <= 0)
-    throw Error(HD_ERR_INVALID, "C_ex (exact shifted inverse) on a non-separable field is not supported by this build");
   if (sys->per_dim < 2) throw Error(HD_ERR_INVALID, "per_dim must be >= 2");
   const auto t0 = std::chrono::steady_clock::now();
   std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
@@ -2136,7 +2200,13 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   }
   // C_ex: exact shifted inverse (src/precond.cpp:204-211)
   if (c->spec.shift && c->spec.cycles <= 0) {
-    if (c->dim == 2) {
+    if (gen) {
+      // non-separable field: dense inverse (small) or complex block tridiagonal LU of the shifted operator
+      int nsm = 148;
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+      c->shift_exact = make_dense(c->st, fineH, cmk(-c->cM.x, -c->cM.y), nsm);
+      c->sx_plan = dalloc<double>(2 * c->N);
+    } else if (c->dim == 2) {
       c->shift_exact = make_fd(c->st, S1, M1, c->cM);
       c->sx_plan = dalloc<double>(2 * c->N);
     } else {

@@ -284,11 +284,11 @@ def test_arbitrary_rhs_linearity():
 
 
 def test_unsupported_specs_fail_loudly():
-    """C_ex on the layered field would need a sparse direct solve of the whole
-    shifted operator; the build refuses it instead of approximating."""
+    """Row slabs are built for the constant field only; the build refuses the
+    layered field there instead of approximating."""
     s = hd.assemble(hd.layered_medium_2d(40, 2, 20.0))
     with pytest.raises(hd.HelmdefError):
-        hd.Solver(s, hd.to_spec("C_ex", 2, 20.0, beta2="1/(3k)"))
+        hd.Solver(s, hd.to_spec("DC_MG", 2, 20.0, **BASE), slabs=2)
 
 
 # ---- layered 4x4 medium (table6, SURVEY.md §8(f)) -----------------------------
@@ -375,6 +375,56 @@ def test_layered_table6_pins():
             assert not res.converged
         else:
             assert abs(res.iterations - int(r["golden"])) <= float(r["tol"]), (r, res.iterations)
+
+
+T6CEX = dict(beta2="1/(3k)")  # data/config/table6.json C_ex
+
+
+@pytest.mark.parametrize("btri", [0, 1])
+@pytest.mark.parametrize("p", [1, 3, 5])
+def test_layered_cex_k50_live(p, btri, monkeypatch):
+    """C_ex (exact shifted inverse, src/precond.cpp:204-211) on the layered field:
+    table6 cells at k = 50 against a live oracle solve (SuperLU of the whole
+    shifted operator).  btri = 1 forces the complex block tridiagonal LU that
+    the larger cells use (dense inverse otherwise)."""
+    import torch
+    monkeypatch.setenv("HD_BTRI", str(btri))
+    k = 50.0
+    ne = O.derived_elements(k, 0.625, p)
+    so = O.assemble(O.layered_medium_2d(ne, p, k))
+    st = O.compose(so, O.to_spec("C_ex", p, k, **T6CEX))
+    g = O.gmres(st.op, st.rhs, st.start, st.monitor, O.GmresOptions(100, 1e-7))
+    s = hd.assemble(hd.layered_medium_2d(ne, p, k))
+    spec = hd.to_spec("C_ex", p, k, **T6CEX)
+    with hd.Solver(s, spec) as solver:
+        rng = np.random.default_rng(11)
+        v = rng.uniform(-1, 1, s.size) + 1j * rng.uniform(-1, 1, s.size)
+        xd = torch.from_numpy(v).cuda()
+        yd = torch.zeros_like(xd)
+        solver.apply(hd.HD_APPLY_MG, xd.data_ptr(), yd.data_ptr())  # cycles = 0: the exact shifted solve
+        ref = O.DirectSolver(O.shifted_operator(so, spec.beta2)).solve(v)
+        assert np.linalg.norm(yd.cpu().numpy() - ref) <= 1e-10 * np.linalg.norm(ref)
+        r = solver.solve(hd.GmresOptions(100, 1e-7))
+    meta = dict(iterations=g.iterations, converged=g.converged, residuals=g.residuals, counts=dict(vars(st.counts)))
+    _check(r, meta, g.solution)
+
+
+def test_layered_table6_cex_pins():
+    """Every table6 C_ex cell (k <= 150): the device iteration count equals the
+    pinned oracle's (+-1) and meets the reference's golden under its compare
+    rule.  k = 100, 150 (25k-57k unknowns) use the complex block tridiagonal LU."""
+    import csv
+    rows = [r for r in csv.DictReader(open(GOLD / "oracle_pins.csv"))
+            if r["table"] == "table6" and r["tag"] == "C_ex"]
+    assert len(rows) == 15
+    for r in rows:
+        p, k, ne = int(r["p"]), float(r["k"]), int(r["elements"])
+        s = hd.assemble(hd.layered_medium_2d(ne, p, k))
+        with hd.Solver(s, hd.to_spec("C_ex", p, k, **T6CEX)) as solver:
+            res = solver.solve(hd.GmresOptions(100, 1e-7))
+        assert bool(res.converged) == bool(int(r["converged"])), r
+        assert abs(res.iterations - int(r["oracle"])) <= 1, (r, res.iterations)
+        assert abs(res.iterations - int(r["golden"])) <= float(r["tol"]), (r, res.iterations)
 
 
 def test_layered_table6_sensitive_cell():

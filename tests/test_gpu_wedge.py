@@ -133,7 +133,18 @@ def test_C4_full_size_wedge():
     assert abs(np.linalg.norm(r.solution) - ref["solution_norm"]) <= 1e-8 * ref["solution_norm"]
 
 
-def test_wedge_rejects_cex():
-    s = hd.assemble(hd.wedge_2d(32, 2, 20.0))
-    with pytest.raises(hd.HelmdefError):
-        hd.Solver(s, hd.to_spec("C_ex", 2, 20.0, beta2="0.5"))
+@pytest.mark.parametrize("btri", [0, 1])
+def test_wedge_cex_live(btri, monkeypatch):
+    """C_ex on the wedge: the exact shifted inverse by the dense inverse or the
+    complex block tridiagonal LU, against the oracle (SuperLU)."""
+    monkeypatch.setenv("HD_BTRI", str(btri))
+    ne, p, k0 = 48, 3, 25.0
+    so = O.assemble(O.wedge_2d(ne, p, k0))
+    st = O.compose(so, O.to_spec("C_ex", p, k0, beta2="0.5"))
+    g = O.gmres(st.op, st.rhs, st.start, st.monitor, O.GmresOptions(100, 1e-7))
+    s = hd.assemble(hd.wedge_2d(ne, p, k0))
+    with hd.Solver(s, hd.to_spec("C_ex", p, k0, beta2="0.5")) as solver:
+        r = solver.solve(hd.GmresOptions(100, 1e-7))
+    assert r.converged == g.converged and r.iterations == g.iterations
+    assert np.max(np.abs(np.array(r.residuals) - np.array(g.residuals))) <= 1e-10
+    assert np.linalg.norm(r.solution - g.solution) <= 1e-8 * np.linalg.norm(g.solution)
