@@ -127,17 +127,27 @@ __device__ __forceinline__ void btri_wait(unsigned* bar, unsigned target) {
   __syncthreads();
 }
 
-// Row dot with a planar vector (re plane at v, im plane at v + plane) that
-// other CTAs wrote before the last barrier (L2-coherent loads).
+// The step's input vector (planar: re plane at v, im plane at v + plane),
+// written by other CTAs before the last barrier, staged once per CTA into
+// shared memory (vs: m re values, then m im values).
+__device__ __forceinline__ void btri_stage(const double* v, size_t plane, int m, double* vs) {
+  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+    vs[c] = __ldcg(v + c);
+    vs[m + c] = __ldcg(v + plane + c);
+  }
+  __syncthreads();
+}
+
+// Row dot with the staged vector.
 template <class T, int KR>
-__device__ __forceinline__ double2 btri_row_dot(const T (&r)[KR], const double* v, size_t plane, int m) {
+__device__ __forceinline__ double2 btri_row_dot(const T (&r)[KR], const double* vs, int m) {
   const int lane = threadIdx.x & 31;
   double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
     const int c = lane + 32 * k;
     if (c < m) {
-      const double vr = __ldcg(v + c), vi = __ldcg(v + plane + c);
+      const double vr = vs[c], vi = vs[m + c];
       if (k & 1) bt_fma(r[k], vr, vi, sr1, si1);
       else bt_fma(r[k], vr, vi, sr0, si0);
     }
@@ -174,12 +184,14 @@ __global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_
   const T* HT = static_cast<const T*>(a.HT);
   unsigned phase = 0;
   T r[KR];
+  extern __shared__ double vs[];  // 2m: the staged step vector
   auto frow = [&](int i, int t) -> const T* {
     return t < m ? GT + i * mm + (size_t)t * m : SinvT + (i - 1) * mm + (size_t)(t - m) * m;
   };
   // ---- forward ----
   for (int i = 0; i < nb; ++i) {
     const int ntask = i > 0 ? 2 * m : m;
+    if (i > 0 && blockIdx.x * wpb < ntask) btri_stage(a.y + (size_t)(i - 1) * m, P, m, vs);
     for (int t = gw; t < ntask; t += W) {
       const bool yrow = t < m;
       const int row = yrow ? t : t - m;
@@ -192,7 +204,7 @@ __global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_
       double2 acc = cmk(0.0, 0.0);
       if (i > 0) {
         if (t != gw) btri_row_load<T, KR>(frow(i, t), m, r);
-        acc = btri_row_dot<T, KR>(r, a.y + (size_t)(i - 1) * m, P, m);
+        acc = btri_row_dot<T, KR>(r, vs, m);
       }
       if (lane == 0) {
         double* dst = yrow ? a.y + gi : a.w + gi - m;
@@ -210,18 +222,19 @@ __global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_
   }
   // ---- backward (x in its own buffer) ----
   for (int i = nb - 1; i >= 0; --i) {
+    if (blockIdx.x * wpb < m) btri_stage(i == nb - 1 ? a.y + (size_t)i * m : a.x + (size_t)(i + 1) * m, P, m, vs);
     for (int row = gw; row < m; row += W) {
       const size_t gi = (size_t)i * m + row;
       double xr, xi;
       if (i == nb - 1) {
         if (row != gw) btri_row_load<T, KR>(SinvT + i * mm + (size_t)row * m, m, r);
-        const double2 acc = btri_row_dot<T, KR>(r, a.y + (size_t)i * m, P, m);
+        const double2 acc = btri_row_dot<T, KR>(r, vs, m);
         xr = acc.x;
         xi = acc.y;
       } else {
         const double wr = lane == 0 ? __ldcg(a.w + gi) : 0.0, wi = lane == 0 ? __ldcg(a.w + P + gi) : 0.0;
         if (row != gw) btri_row_load<T, KR>(HT + i * mm + (size_t)row * m, m, r);
-        const double2 acc = btri_row_dot<T, KR>(r, a.x + (size_t)(i + 1) * m, P, m);
+        const double2 acc = btri_row_dot<T, KR>(r, vs, m);
         xr = wr - acc.x;
         xi = wi - acc.y;
       }

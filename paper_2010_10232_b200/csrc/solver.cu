@@ -945,12 +945,14 @@ static void dense_apply(hd_ctx* c, const ExactSolver& X, const double2* x, doubl
 // Block tridiagonal exact solve (btri.cuh), in/out planar.
 template <class T, int KR>
 static void btri_launch_t(hd_ctx* c, ExactSolver& X) {
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_btri_solve<T, KR>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-    attr = true;
+  const size_t smem = 2 * static_cast<size_t>(X.bt.m) * sizeof(double);
+  static size_t attr = 0;
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_btri_solve<T, KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = smem;
   }
   cudaLaunchConfig_t cfg{};
+  cfg.dynamicSmemBytes = smem;
   cfg.gridDim = dim3(c->n_sms);
   cfg.blockDim = dim3(btri_threads(KR * static_cast<int>(sizeof(T) / 8)));
   cfg.stream = c->st;
@@ -1903,12 +1905,13 @@ static void attach_gen(DevBand& d, const GenHost& h, double2 cA, double2 cM) {
 // for the reference's SparseLU factors (src/precond.cpp:95-99, 133).
 static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int n_sms);
 
-static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl, int n_sms = 148) {
+static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl, int n_sms = 148, bool allow_btri = true) {
   const int n = h.Y[0].n;
   const size_t NN = static_cast<size_t>(n) * n;
   // operators beyond the dense-inverse limit, or HD_BTRI=1: block tridiagonal LU
   const char* fb = std::getenv("HD_BTRI");
-  if ((NN > 20000 || (fb && std::atoi(fb) == 1)) && !(fb && std::atoi(fb) == 0)) return make_btri(st, h, cl, n_sms);
+  if (allow_btri && (NN > 20000 || (fb && std::atoi(fb) == 1)) && !(fb && std::atoi(fb) == 0))
+    return make_btri(st, h, cl, n_sms);
   if (NN > 20000)
     throw Error(HD_ERR_INVALID, "non-separable field: exact solve of " + std::to_string(NN) +
                                     " complex unknowns exceeds the dense-inverse limit (20000)");
@@ -2253,7 +2256,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
         }
     const Band& SL = Ss.back();
     const Band& ML = Ms.back();
-    if (gen) c->coarsest = make_dense(c->st, Hs.back(), cmk(-c->cM.x, -c->cM.y));
+    if (gen) c->coarsest = make_dense(c->st, Hs.back(), cmk(-c->cM.x, -c->cM.y), 148, false);  // <= 32^2 unknowns
     else if (c->dim == 2) c->coarsest = make_fd(c->st, SL, ML, c->cM);
     else c->coarsest = make_bandlu(SL, ML, c->cM, Ss.size() == 1 ? c->corner : cmk(0.0, 0.0));
     for (size_t l = 0; l < c->lev.size(); ++l) {
