@@ -39,10 +39,21 @@ __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* 
   // coarse rows [qb, qe) (a row slab; whole grid: 0, nc), global row addressing
   const int qx0 = blockIdx.x * kRQX, qy0 = qb + blockIdx.y * kRQY;
   const int fx0 = 2 * qx0 + lo, fy0 = 2 * qy0 + lo;
-  for (int e = threadIdx.x; e < RR * RC; e += blockDim.x) {
+  // all loads of the region issued before any is consumed (blockDim == 256)
+  constexpr int NLD = (RR * RC + 255) / 256;
+  double2 v[NLD];
+#pragma unroll
+  for (int k = 0; k < NLD; ++k) {
+    const int e = threadIdx.x + k * 256;
     const int rr = e / RC, cc = e % RC;
     const int fy = fy0 + rr, fx = fx0 + cc;
-    f[rr][cc] = (fy >= 0 && fy < nf && fx >= 0 && fx < nf) ? r[(size_t)fy * nf + fx] : cmk(0.0, 0.0);
+    v[k] = (e < RR * RC && fy >= 0 && fy < nf && fx >= 0 && fx < nf) ? __ldg(r + (size_t)fy * nf + fx)
+                                                                      : cmk(0.0, 0.0);
+  }
+#pragma unroll
+  for (int k = 0; k < NLD; ++k) {
+    const int e = threadIdx.x + k * 256;
+    if (e < RR * RC) f[e / RC][e % RC] = v[k];
   }
   __syncthreads();
   double w[nw];
@@ -155,8 +166,21 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
     ty[r][cc] = t;
   }
   __syncthreads();
-  // x pass + combine with the fine vector, 4 points per thread (coalesced rows)
-  for (int e = threadIdx.x; e < kPFY * kPFX; e += blockDim.x) {
+  // x pass + combine with the fine vector, 4 points per thread (coalesced rows);
+  // the fine-vector loads of all 4 points are issued first (blockDim == 256)
+  constexpr int NPT = kPFY * kPFX / 256;
+  double2 base[NPT];
+#pragma unroll
+  for (int k = 0; k < NPT; ++k) {
+    const int e = threadIdx.x + k * 256;
+    const int fy = fy0 + e / kPFX, fx = fx0 + e % kPFX;
+    const size_t gi = (size_t)fy * nf + fx;
+    base[k] = cmk(0.0, 0.0);
+    if (PMODE != 2 && fy < fe && fx < nf) base[k] = PMODE == 0 ? out[gi] : __ldcs(s + gi);
+  }
+#pragma unroll
+  for (int k = 0; k < NPT; ++k) {
+    const int e = threadIdx.x + k * 256;
     const int r = e / kPFX, cx = e % kPFX;
     const int fy = fy0 + r, fx = fx0 + cx;
     if (fy >= fe || fx >= nf) continue;
@@ -167,8 +191,8 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
     if (fx & 1) acc = cfma_r(w0, ty[r][li - 1], cfma_r(w1, ty[r][li], cscale(w2, ty[r][li + 1])));
     else acc = cfma_r(w0, ty[r][li - 1], cscale(w1, ty[r][li]));
     const size_t gi = (size_t)fy * nf + fx;
-    if (PMODE == 0) out[gi] = cadd(out[gi], acc);
-    else if (PMODE == 1) out[gi] = csub(ld_stream(s + gi), acc);
+    if (PMODE == 0) out[gi] = cadd(base[k], acc);
+    else if (PMODE == 1) out[gi] = csub(base[k], acc);
     else out[gi] = acc;
   }
 }
