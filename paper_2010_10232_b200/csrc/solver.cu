@@ -2431,6 +2431,13 @@ struct hd_slabs {
   std::vector<int> mine;                        // slabs of this process
   std::vector<SlabPost> sends, recvs;           // posted in the current group (vranks)
   double2* red = nullptr;                       // S x nslot per-slab Arnoldi pass-1 sums
+  // graph-resident iteration (HD_GRAPH != 0): one captured body per (maxit),
+  // launched once per iteration with the iteration index in device memory
+  int* dj = nullptr;                            // device iteration index
+  int* hj = nullptr;                            // pinned mirror
+  cudaGraphExec_t body = nullptr;
+  int body_maxit = -1;
+  long body_delta[6] = {0, 0, 0, 0, 0, 0};      // counters one body adds (matvecs .. lib_calls)
   std::vector<SlabLevel> lv;                    // MG levels
   std::vector<std::vector<double2*>> X, Y, B, R;  // [level][slab], levels < g
   std::vector<int> cur;                         // ping-pong state of X/Y per level
@@ -2465,7 +2472,9 @@ __global__ void k_slab_norm(const double* slots, int S, const double* scale_src,
 // Arnoldi pass 1 of one slab: its Gs CTA partials summed per used slot in CTA
 // order (deterministic), so a process contributes one row of kLsaNslot sums
 constexpr int kLsaNslot = 2 * kLsaMaxJ + 2;
-__global__ void k_lsa_slab_reduce(const double2* __restrict__ parts, int Gs, int j, double2* __restrict__ out) {
+__global__ void k_lsa_slab_reduce(const double2* __restrict__ parts, int Gs, int j, const int* dj,
+                                  double2* __restrict__ out) {
+  if (dj) j = *dj;
   for (int q = threadIdx.x; q < kLsaNslot; q += blockDim.x) {
     const bool used = q < j + 1 || (q >= kLsaMaxJ + 1 && q < kLsaMaxJ + 1 + j);
     double2 acc = cmk(0.0, 0.0);
@@ -2826,13 +2835,23 @@ static void s_gather(hd_ctx* c, const std::vector<double2*>& v, double2* full) {
 }
 
 // basis vector u_j of slab s <-> halo'd slab vectors
-static void s_basis_to(hd_ctx* c, int j, std::vector<double2*>& v) {
+__global__ void k_copy_basis(double2* __restrict__ dst, const double2* __restrict__ V, size_t Ns, const int* dj) {
+  const double2* src = V + (size_t)(*dj) * Ns;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < Ns; g += (size_t)gridDim.x * blockDim.x)
+    dst[g] = src[g];
+}
+
+static void s_basis_to(hd_ctx* c, int j, std::vector<double2*>& v, const int* dj = nullptr) {
   hd_slabs* sl = slabs_of(c);
   const SlabLevel& G = sl->lv[0];
   for (int s : sl->mine) {
     const size_t Ns = static_cast<size_t>(own(G, s)) * G.n;
-    CK(cudaMemcpyAsync(v[s] + static_cast<size_t>(G.H) * G.n, sl->V[s] + static_cast<size_t>(j) * Ns,
-                       Ns * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    if (dj)
+      HD_LAUNCH(HD_K_VEC, 32.0 * Ns,
+                k_copy_basis<<<grid_for(Ns), 256, 0, c->st>>>(v[s] + static_cast<size_t>(G.H) * G.n, sl->V[s], Ns, dj));
+    else
+      CK(cudaMemcpyAsync(v[s] + static_cast<size_t>(G.H) * G.n, sl->V[s] + static_cast<size_t>(j) * Ns,
+                         Ns * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
   }
 }
 
@@ -2848,6 +2867,77 @@ static LsaArgs s_lsa(hd_ctx* c, int s, int j, int mode, int maxit) {
   a.part_offset = s * sl->Gs;
   a.partial_only = 1;
   return a;
+}
+
+// Slab Arnoldi iteration, part a: u_j -> w = op(u_j), pass 1 (per-slab partials,
+// per-slab sums, gathered, combined in slab order), pass 2 (u_{j+1} and the
+// lagged x_{j-1}; partials gathered).  dj: device iteration index (graph body).
+static void slab_iteration_a(hd_ctx* c, int j, int maxit, const int* dj) {
+  hd_slabs* sl = slabs_of(c);
+  s_basis_to(c, j, sl->vin, dj);
+  s_op(c, sl->vin, sl->w);
+  for (int s : sl->mine) {
+    LsaArgs a = s_lsa(c, s, j, 0, maxit);
+    a.dj = dj;
+    HD_LAUNCH(HD_K_MGS, (j + 3.0) * 16.0 * a.N, k_lsa_dots<<<sl->Gs, kLsaBD, lsa_dots_smem(), c->st>>>(a));
+  }
+  for (int s : sl->mine)
+    HD_LAUNCH(HD_K_MGS, 0.0, k_lsa_slab_reduce<<<1, kLsaBD, 0, c->st>>>(sl->parts + static_cast<size_t>(s) * sl->Gs * kLsaNslot,
+                                                                     sl->Gs, j, dj, sl->red + static_cast<size_t>(s) * kLsaNslot));
+  slab_allgather(c, reinterpret_cast<double*>(sl->red), 2 * static_cast<size_t>(kLsaNslot));
+  LsaArgs af = s_lsa(c, sl->mine[0], j, 0, maxit);
+  af.dj = dj;
+  af.partials = sl->red;
+  HD_LAUNCH(HD_K_MGS, 0.0, k_lsa_dots_finish<<<1, kLsaBD, 0, c->st>>>(af, sl->S));
+  for (int s : sl->mine) {
+    LsaArgs a = s_lsa(c, s, j, 0, maxit);
+    a.dj = dj;
+    HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 5.0 : 3.0) * 16.0 * a.N, k_lsa_update<<<sl->Gs, kLsaBD, 0, c->st>>>(a));
+  }
+  slab_allgather(c, reinterpret_cast<double*>(sl->parts), 2 * static_cast<size_t>(sl->Gs));
+}
+
+// part b: Givens + back substitution of column j, hnew to the host mirror
+static void slab_iteration_b(hd_ctx* c, int j, int maxit, int nparts, const int* dj) {
+  hd_slabs* sl = slabs_of(c);
+  LsaArgs a0 = s_lsa(c, sl->mine[0], j, 0, maxit);
+  a0.dj = dj;
+  HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a0, nparts));
+  CK(cudaMemcpyAsync(c->hres + 1, c->dres + 1, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+}
+
+// Capture one iteration (parts a and b with the monitor of x_{j-1} between
+// them, the scalars copied to the pinned mirror at the end) as a graph; the
+// counters it adds per launch are recorded.  NCCL calls are captured too.
+static void build_slab_body(hd_ctx* c, int maxit, int nparts) {
+  hd_slabs* sl = slabs_of(c);
+  if (!sl->dj) {
+    sl->dj = dalloc<int>(1);
+    CK(cudaMallocHost(&sl->hj, sizeof(int)));
+  }
+  if (sl->body) {
+    cudaGraphExecDestroy(sl->body);
+    sl->body = nullptr;
+  }
+  const long before[6] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles, c->launches, c->lib_calls};
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
+  slab_iteration_a(c, 0, maxit, sl->dj);
+  s_monitor(c, sl->x);  // x_{j-1} (used by the host for j >= 1)
+  slab_iteration_b(c, 0, maxit, nparts, sl->dj);
+  CK(cudaMemcpyAsync(c->hres, c->dres, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamEndCapture(c->st, &g));
+  CK(cudaGraphInstantiate(&sl->body, g, 0));
+  cudaGraphDestroy(g);
+  const long after[6] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles, c->launches, c->lib_calls};
+  for (int k = 0; k < 6; ++k) sl->body_delta[k] = after[k] - before[k];
+  c->matvecs = before[0];
+  c->coarse_solves = before[1];
+  c->shift_solves = before[2];
+  c->vcycles = before[3];
+  c->launches = static_cast<int>(before[4]);
+  c->lib_calls = static_cast<int>(before[5]);
+  sl->body_maxit = maxit;
 }
 
 static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f_full, double2* xout_full) {
@@ -2920,6 +3010,8 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
   const int nparts = sl->S * sl->Gs;  // pass-2 partials (one per CTA of every slab)
   bool stop = false;
   double hnew_prev = 1.0;
+  const bool graph = c->graph_enabled && !c->prof_on;
+  if (graph && sl->body_maxit != maxit) build_slab_body(c, maxit, nparts);
   for (int j = 0; j < maxit && !stop; ++j) {
     const long snap[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
     auto rollback = [&]() {
@@ -2928,47 +3020,48 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
       c->shift_solves = snap[2];
       c->vcycles = snap[3];
     };
-    s_basis_to(c, j, sl->vin);
-    s_op(c, sl->vin, sl->w);
-    // pass 1 per slab (partials at the slab's offset), then the slab-order combination
-    for (int s : sl->mine) {
-      LsaArgs a = s_lsa(c, s, j, 0, maxit);
-      HD_LAUNCH(HD_K_MGS, (j + 3.0) * 16.0 * a.N, k_lsa_dots<<<sl->Gs, kLsaBD, lsa_dots_smem(), c->st>>>(a));
-    }
-    // per-slab sums of the CTA partials (fixed order), gathered from every slab, combined in slab order
-    for (int s : sl->mine)
-      HD_LAUNCH(HD_K_MGS, 0.0, k_lsa_slab_reduce<<<1, kLsaBD, 0, c->st>>>(sl->parts + static_cast<size_t>(s) * sl->Gs * kLsaNslot,
-                                                                       sl->Gs, j, sl->red + static_cast<size_t>(s) * kLsaNslot));
-    slab_allgather(c, reinterpret_cast<double*>(sl->red), 2 * static_cast<size_t>(kLsaNslot));
-    LsaArgs a0 = s_lsa(c, sl->mine[0], j, 0, maxit);
-    LsaArgs af = a0;
-    af.partials = sl->red;
-    HD_LAUNCH(HD_K_MGS, 0.0, k_lsa_dots_finish<<<1, kLsaBD, 0, c->st>>>(af, sl->S));
-    for (int s : sl->mine) {
-      LsaArgs a = s_lsa(c, s, j, 0, maxit);
-      HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 5.0 : 3.0) * 16.0 * a.N, k_lsa_update<<<sl->Gs, kLsaBD, 0, c->st>>>(a));
-    }
-    slab_allgather(c, reinterpret_cast<double*>(sl->parts), 2 * static_cast<size_t>(sl->Gs));
-    if (j >= 1) {  // x_{j-1} is ready
-      s_monitor(c, sl->x);
-      read_scalars(c);
-      const double rr = c->hres[0];
-      res.iterations = j;
-      res.residuals.push_back(rr);
-      if (rr <= opt.tolerance) {
-        res.converged = true;
-        stop = true;
-        rollback();
-        break;
+    if (graph) {
+      // the whole iteration (pass 1, pass 2, monitor of x_{j-1}, Givens) as one graph launch
+      *sl->hj = j;
+      CK(cudaMemcpyAsync(sl->dj, sl->hj, sizeof(int), cudaMemcpyHostToDevice, c->st));
+      CK(cudaGraphLaunch(sl->body, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      c->matvecs += sl->body_delta[0];
+      c->coarse_solves += sl->body_delta[1];
+      c->shift_solves += sl->body_delta[2];
+      c->vcycles += sl->body_delta[3];
+      c->launches += static_cast<int>(sl->body_delta[4]);
+      c->lib_calls += static_cast<int>(sl->body_delta[5]);
+      if (j >= 1) {
+        const double rr = c->hres[0];
+        res.iterations = j;
+        res.residuals.push_back(rr);
+        if (rr <= opt.tolerance || hnew_prev < 1e-300) {
+          res.converged = rr <= opt.tolerance;
+          rollback();
+          break;
+        }
       }
-      if (hnew_prev < 1e-300) {
-        stop = true;
-        rollback();
-        break;
+    } else {
+      slab_iteration_a(c, j, maxit, nullptr);
+      if (j >= 1) {  // x_{j-1} is ready
+        s_monitor(c, sl->x);
+        read_scalars(c);
+        const double rr = c->hres[0];
+        res.iterations = j;
+        res.residuals.push_back(rr);
+        if (rr <= opt.tolerance) {
+          res.converged = true;
+          rollback();
+          break;
+        }
+        if (hnew_prev < 1e-300) {
+          rollback();
+          break;
+        }
       }
+      slab_iteration_b(c, j, maxit, nparts, nullptr);
     }
-    HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a0, nparts));
-    CK(cudaMemcpyAsync(c->hres + 1, c->dres + 1, sizeof(double), cudaMemcpyDeviceToHost, c->st));
     if (j + 1 == maxit) {  // budget exhausted: x_{maxit-1}, then its monitor
       for (int s : sl->mine) {
         LsaArgs bq = s_lsa(c, s, j, 1, maxit);
@@ -3080,6 +3173,9 @@ static void destroy_slabs(hd_ctx* c) {
   cudaFree(sl->slots);
   cudaFree(sl->parts);
   cudaFree(sl->red);
+  if (sl->body) cudaGraphExecDestroy(sl->body);
+  cudaFree(sl->dj);
+  if (sl->hj) cudaFreeHost(sl->hj);
   if (sl->comm) nccl().CommDestroy(sl->comm);
   delete sl;
   c->slabs = nullptr;

@@ -463,19 +463,23 @@ def test_exact_shifted_inverse_C_ex(problem, p, k, beta2):
 
 
 # ---- row slabs ---------------------------------------------
+@pytest.mark.parametrize("graph", [0, 1])
 @pytest.mark.parametrize("vranks", [0, 1])
 @pytest.mark.parametrize("S,ne,p,k,agg", [(2, 130, 3, 60.0, 40), (3, 200, 2, 100.0, 60), (4, 320, 2, 200.0, 200),
                                           (8, 256, 2, 120.0, 40)])
-def test_row_slabs_match_single_domain(S, ne, p, k, agg, vranks, monkeypatch):
+def test_row_slabs_match_single_domain(S, ne, p, k, agg, vranks, graph, monkeypatch):
     """The slab program (halo'd slab buffers, halo copies, gathered coarse levels
     and E, slab-order reductions) on one device against the single-domain solve:
     components to 1e-10, equal iterations and counts, history 1e-10, solution 1e-8.
     vranks = 1: every slab is its own virtual rank, so each halo transfer goes
     through the posted send/recv records of the multi-process (NCCL) program,
-    matched by (sender, receiver, order) and checked for equal sizes."""
+    matched by (sender, receiver, order) and checked for equal sizes.
+    graph = 1: each iteration is one captured graph launch (device-side
+    iteration index); graph = 0: the host-driven loop."""
     import torch
     monkeypatch.setenv("HD_SLAB_AGGLOMERATE", str(agg))
     monkeypatch.setenv("HD_SLAB_VRANKS", str(vranks))
+    monkeypatch.setenv("HD_GRAPH", str(graph))
     s = hd.assemble(hd.point_source_2d(ne, p, k))
     spec = hd.to_spec("DC_MG", p, k, **BASE)
     rng = np.random.default_rng(5)
@@ -493,6 +497,13 @@ def test_row_slabs_match_single_domain(S, ne, p, k, agg, vranks, monkeypatch):
             assert np.linalg.norm(a - b) <= tol * np.linalg.norm(a), (which, np.linalg.norm(a - b) / np.linalg.norm(a))
         r1 = one.solve(hd.GmresOptions(100, 1e-7))
         r2 = sl.solve(hd.GmresOptions(100, 1e-7))
+        r2b = sl.solve(hd.GmresOptions(100, 1e-7))
+        q1 = one.solve(hd.GmresOptions(4, 1e-7))   # budget exhausted (the loop's tail)
+        q2 = sl.solve(hd.GmresOptions(4, 1e-7))
+    assert np.array_equal(r2.solution, r2b.solution), "slab solve must be deterministic"
+    assert q2.iterations == q1.iterations == 4 and not q2.converged
+    assert np.max(np.abs(np.array(q2.residuals) - np.array(q1.residuals))) <= 1e-10
+    assert (q2.counts.matvecs, q2.counts.coarse_solves) == (q1.counts.matvecs, q1.counts.coarse_solves)
     assert r2.converged == r1.converged and r2.iterations == r1.iterations
     assert (r2.counts.matvecs, r2.counts.coarse_solves, r2.counts.shift_solves, r2.counts.vcycles) == \
         (r1.counts.matvecs, r1.counts.coarse_solves, r1.counts.shift_solves, r1.counts.vcycles)
