@@ -7,26 +7,37 @@
 // Ordering the unknowns lexicographically (x fastest) and grouping q = b grid
 // rows (b = the stencil's half-width in y) into one "super-row" of m = q*n
 // unknowns makes E block tridiagonal with nb = ceil(n/q) diagonal blocks D_i
-// and couplings B_i = E[i, i+1], C_i = E[i, i-1].  Block LU at setup (cuBLAS /
-// cuSOLVER, partial pivoting inside each diagonal block):
+// and couplings B_i = E[i, i+1], C_i = E[i, i-1].  The factorisation is
+// twisted at the middle block k = nb/2 (cuBLAS / cuSOLVER at setup, partial
+// pivoting inside each diagonal block): eliminated from the top for i < k,
 //
 //   S_0 = D_0,  S_i = D_i - G_i B_{i-1},  G_i = C_i S_{i-1}^-1,  H_i = S_i^-1 B_i,
 //
-// and per solve (real operator: the re and im planes are two real right-hand
-// sides; complex operator: one complex right-hand side, planar):
+// from the bottom for i > k,
 //
-//   y_i = r_i - G_i y_{i-1}          (nb sequential steps)
-//   w_i = S_i^-1 y_i                 (all blocks in parallel)
-//   x_i = w_i - H_i x_{i+1}          (nb sequential steps).
+//   T_{nb-1} = D_{nb-1},  T_i = D_i - G'_i C_{i+1},  G'_i = B_i T_{i+1}^-1,  H'_i = T_i^-1 C_i,
+//
+// and M = D_k - G_k B_{k-1} - G'_k C_{k+1} in the middle.  Per solve (real
+// operator: the re and im planes are two real right-hand sides; complex
+// operator: one complex right-hand side, planar), both halves run at once:
+//
+//   y_i = r_i - G_i y_{i-1} (i < k),   z_i = r_i - G'_i z_{i+1} (i > k),
+//   w_i = S_i^-1 y_i,  w'_i = T_i^-1 z_i                     (alongside),
+//   x_k = M^-1 (r_k - G_k y_{k-1} - G'_k z_{k+1}),
+//   x_i = w_i - H_i x_{i+1} (i < k),   x_i = w'_i - H'_i x_{i-1} (i > k),
+//
+// about nb + 2 dependent steps instead of the 2 nb of a one-sided sweep.
 //
 // k_btri_solve runs this in one persistent kernel (one CTA per SM, a grid
-// barrier between dependent steps; w_{i-1} is formed alongside y_i).  A
-// barrier-free variant that ordered the steps by dataflow on self-validating
-// vector slots (sentinel-filled buffers polled by the consumers) was correct
-// but 2x slower: 720 warps polling L2 starve the producers' stores.  Each
-// warp owns matrix rows; the matrices are stored row-major (a warp streams one
-// contiguous row).  Padding rows (n not a multiple of q) carry an identity
-// diagonal and a zero right-hand side.
+// barrier between dependent steps).  A barrier-free variant that ordered the
+// steps by dataflow on self-validating vector slots (sentinel-filled buffers
+// polled by the consumers) was correct but 2x slower: 720 warps polling L2
+// starve the producers' stores.  Each warp owns matrix rows; the matrices are
+// stored row-major (a warp streams one contiguous row) and a warp loads the
+// row of its first task of the next step between arriving at and waiting on
+// the barrier.  Each step's input vectors are staged once per CTA in shared
+// memory.  Padding rows (n not a multiple of q) carry an identity diagonal
+// and a zero right-hand side.
 #pragma once
 
 #include "layered.cuh"
@@ -54,11 +65,12 @@ __device__ __forceinline__ void bt_fma(double2 a, double vr, double vi, double& 
 __host__ __device__ constexpr int btri_threads(int regs) { return regs <= 16 ? 512 : (regs <= 32 ? 384 : 256); }
 
 struct BtriArgs {
-  int n, q, m, nb;     // grid side, rows per block, block size m = q*n, blocks
+  int n, q, m, nb, k;  // grid side, rows per block, block size m = q*n, blocks, middle block
   size_t NN;           // n^2 (unknowns); padded length nb*m
-  const void* GT;      // nb blocks, row-major: G_i (block 0 unused)      [double or double2]
-  const void* SinvT;   // nb blocks, row-major: S_i^-1
-  const void* HT;      // nb blocks, row-major: H_i (block nb-1 unused)
+  const void* GT;      // nb blocks, row-major: G_i (0 < i <= k), G'_i (k < i < nb-1)   [double or double2]
+  const void* G2;      // one block: G'_k (k < nb-1)
+  const void* SinvT;   // nb blocks, row-major: S_i^-1 (i < k), M^-1 (k), T_i^-1 (i > k)
+  const void* HT;      // nb blocks, row-major: H_i (i < k), H'_i (i > k)
   double* y;           // 2 planes x nb*m
   double* w;           // 2 planes x nb*m
   double* x;           // 2 planes x nb*m
@@ -161,95 +173,186 @@ __device__ __forceinline__ double2 btri_row_dot(const T (&r)[KR], const double* 
   return cmk(sr, si);
 }
 
-// Persistent solve.  Sequential steps, one grid barrier each (2 nb in total):
-//   F_i (i = 0..nb-1):  y_i = r_i - G_i y_{i-1}  and  w_{i-1} = S_{i-1}^-1 y_{i-1}
-//                       (2m independent row tasks: both need only y_{i-1})
-//   B_{nb-1}:           x_{nb-1} = S_{nb-1}^-1 y_{nb-1}
-//   B_i (i = nb-2..0):  x_i = w_i - H_i x_{i+1}
-// A warp's first task of the next step has a fixed matrix row, which it loads
-// into registers between arriving at and waiting on the barrier, so the HBM
-// fetch of the step matrices overlaps the barrier (as do its right-hand-side
-// reads); further tasks (2m > warps) load after the wait.
+// One group of m row tasks of a solve step: out row = (rhs) - mat * vec (+ second product).
+struct BtGroup {
+  int kind;       // 0 none, 1 y/z (rhs - A v), 2 w (A v), 3 middle y_k (rhs - A v - A2 v2), 4 x_k (A v), 5 x (w - A v)
+  int blk;        // block of the output rows
+  int vec, vec2;  // staged vector slots (0, 1) read by the products
+  int mat, mat2;  // matrix: 0 none, 1 GT[blk], 2 SinvT[blk'], 3 HT[blk], 4 G2 ; blk' = mblk
+  int mblk;       // block of the (first) matrix
+};
+
+// Step s of the twisted solve: up to 4 groups and the (up to 2) input vectors
+// to stage (block index and buffer: 0 = y, 1 = x; -1 = none).
+struct BtStep {
+  BtGroup g[4];
+  int ng;
+  int sv_blk[2], sv_buf[2];
+};
+
+__device__ __forceinline__ BtStep btri_step(int s, int nb, int k) {
+  BtStep st;
+  st.ng = 0;
+  st.sv_blk[0] = st.sv_blk[1] = -1;
+  st.sv_buf[0] = st.sv_buf[1] = 0;
+  const int F = max(k, nb - 1 - k);  // forward steps
+  auto add = [&](int kind, int blk, int vec, int mat, int mblk, int vec2 = 0, int mat2 = 0) {
+    BtGroup& g = st.g[st.ng++];
+    g.kind = kind;
+    g.blk = blk;
+    g.vec = vec;
+    g.vec2 = vec2;
+    g.mat = mat;
+    g.mat2 = mat2;
+    g.mblk = mblk;
+  };
+  if (s < F) {  // forward: top block i = s (< k), bottom block i = nb-1-s (> k)
+    const int it = s, ib = nb - 1 - s;
+    if (it < k) {
+      if (it > 0) {
+        st.sv_blk[0] = it - 1;
+        add(1, it, 0, 1, it);       // y_it = r - G_it y_{it-1}
+        add(2, it - 1, 0, 2, it - 1);  // w_{it-1} = S^-1 y_{it-1}
+      } else {
+        add(1, it, 0, 0, it);       // y_0 = r_0
+      }
+    }
+    if (ib > k) {
+      if (ib < nb - 1) {
+        st.sv_blk[1] = ib + 1;
+        add(1, ib, 1, 1, ib);       // z_ib = r - G'_ib z_{ib+1}
+        add(2, ib + 1, 1, 2, ib + 1);  // w'_{ib+1} = T^-1 z_{ib+1}
+      } else {
+        add(1, ib, 1, 0, ib);       // z_{nb-1} = r_{nb-1}
+      }
+    }
+    return st;
+  }
+  if (s == F) {  // middle right-hand side and the last w / w'
+    if (k > 0) st.sv_blk[0] = k - 1;
+    if (k < nb - 1) st.sv_blk[1] = k + 1;
+    add(3, k, 0, k > 0 ? 1 : 0, k, 1, k < nb - 1 ? 4 : 0);
+    if (k > 0) add(2, k - 1, 0, 2, k - 1);
+    if (k < nb - 1) add(2, k + 1, 1, 2, k + 1);
+    return st;
+  }
+  if (s == F + 1) {  // x_k = M^-1 y_k
+    st.sv_blk[0] = k;
+    add(4, k, 0, 2, k);
+    return st;
+  }
+  const int t = s - F - 1;  // backward step t >= 1: x_{k-t} (top) and x_{k+t} (bottom)
+  const int it = k - t, ib = k + t;
+  if (it >= 0) {
+    st.sv_blk[0] = it + 1;
+    st.sv_buf[0] = 1;
+    add(5, it, 0, 3, it);
+  }
+  if (ib <= nb - 1) {
+    st.sv_blk[1] = ib - 1;
+    st.sv_buf[1] = 1;
+    add(5, ib, 1, 3, ib);
+  }
+  return st;
+}
+
+template <class T>
+__device__ __forceinline__ const T* bt_mat(const BtriArgs& a, int mat, int blk, int row) {
+  const size_t mm = (size_t)a.m * a.m, off = (size_t)blk * mm + (size_t)row * a.m;
+  switch (mat) {
+    case 1: return static_cast<const T*>(a.GT) + off;
+    case 2: return static_cast<const T*>(a.SinvT) + off;
+    case 3: return static_cast<const T*>(a.HT) + off;
+    case 4: return static_cast<const T*>(a.G2) + (size_t)row * a.m;
+    default: return nullptr;
+  }
+}
+
 template <class T, int KR>
 __global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_btri_solve(BtriArgs a) {
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
   const int W = gridDim.x * wpb;
-  const int m = a.m, nb = a.nb;
-  const size_t mm = (size_t)m * m, P = (size_t)nb * m;
+  const int m = a.m, nb = a.nb, k = a.k;
+  const size_t P = (size_t)nb * m;
   const unsigned G = gridDim.x;
-  const T* GT = static_cast<const T*>(a.GT);
-  const T* SinvT = static_cast<const T*>(a.SinvT);
-  const T* HT = static_cast<const T*>(a.HT);
+  const int F = max(k, nb - 1 - k);
+  const int nsteps = F + 2 + max(k, nb - 1 - k);
   unsigned phase = 0;
   T r[KR];
-  extern __shared__ double vs[];  // 2m: the staged step vector
-  auto frow = [&](int i, int t) -> const T* {
-    return t < m ? GT + i * mm + (size_t)t * m : SinvT + (i - 1) * mm + (size_t)(t - m) * m;
-  };
-  // ---- forward ----
-  for (int i = 0; i < nb; ++i) {
-    const int ntask = i > 0 ? 2 * m : m;
-    if (i > 0 && blockIdx.x * wpb < ntask) btri_stage(a.y + (size_t)(i - 1) * m, P, m, vs);
+  extern __shared__ double vs[];  // two staged vectors, 2m doubles each
+  int pre = -1;                   // task whose matrix row r holds (prefetched), -1: none
+  BtStep st = btri_step(0, nb, k);
+  for (int s = 0; s < nsteps; ++s) {
+    const int ntask = st.ng * m;
+    // stage this step's input vectors (every CTA with tasks)
+    if (blockIdx.x * wpb < ntask) {
+      for (int v = 0; v < 2; ++v) {
+        if (st.sv_blk[v] < 0) continue;
+        const double* src = (st.sv_buf[v] ? a.x : a.y) + (size_t)st.sv_blk[v] * m;
+        for (int c = threadIdx.x; c < m; c += blockDim.x) {
+          vs[v * 2 * m + c] = __ldcg(src + c);
+          vs[v * 2 * m + m + c] = __ldcg(src + P + c);
+        }
+      }
+      __syncthreads();
+    }
     for (int t = gw; t < ntask; t += W) {
-      const bool yrow = t < m;
-      const int row = yrow ? t : t - m;
-      const size_t gi = (size_t)i * m + row;
-      double rr = 0.0, ri = 0.0;
-      if (yrow && lane == 0 && gi < a.NN) {
-        rr = a.io[gi];
-        ri = a.io[a.NN + gi];
+      const BtGroup& g = st.g[t / m];
+      const int row = t % m;
+      const size_t gi = (size_t)g.blk * m + row;
+      double br = 0.0, bi = 0.0;  // rhs (kinds 1, 3) or w (kind 5)
+      if (lane == 0) {
+        if ((g.kind == 1 || g.kind == 3) && gi < a.NN) {
+          br = a.io[gi];
+          bi = a.io[a.NN + gi];
+        } else if (g.kind == 5) {
+          br = __ldcg(a.w + gi);
+          bi = __ldcg(a.w + P + gi);
+        }
       }
       double2 acc = cmk(0.0, 0.0);
-      if (i > 0) {
-        if (t != gw) btri_row_load<T, KR>(frow(i, t), m, r);
-        acc = btri_row_dot<T, KR>(r, vs, m);
+      if (g.mat) {
+        if (t != pre) btri_row_load<T, KR>(bt_mat<T>(a, g.mat, g.mblk, row), m, r);
+        acc = btri_row_dot<T, KR>(r, vs + g.vec * 2 * m, m);
       }
+      if (g.kind == 3 && g.mat2) {
+        btri_row_load<T, KR>(bt_mat<T>(a, g.mat2, g.mblk, row), m, r);
+        const double2 a2 = btri_row_dot<T, KR>(r, vs + g.vec2 * 2 * m, m);
+        acc = cadd(acc, a2);
+      }
+      pre = -1;
       if (lane == 0) {
-        double* dst = yrow ? a.y + gi : a.w + gi - m;
-        dst[0] = yrow ? rr - acc.x : acc.x;
-        dst[P] = yrow ? ri - acc.y : acc.y;
-      }
-    }
-    btri_arrive(a.bar);
-    if (i + 1 < nb) {
-      if (gw < 2 * m) btri_row_load<T, KR>(frow(i + 1, gw), m, r);
-    } else if (gw < m) {
-      btri_row_load<T, KR>(SinvT + (nb - 1) * mm + (size_t)gw * m, m, r);
-    }
-    btri_wait(a.bar, ++phase * G);
-  }
-  // ---- backward (x in its own buffer) ----
-  for (int i = nb - 1; i >= 0; --i) {
-    if (blockIdx.x * wpb < m) btri_stage(i == nb - 1 ? a.y + (size_t)i * m : a.x + (size_t)(i + 1) * m, P, m, vs);
-    for (int row = gw; row < m; row += W) {
-      const size_t gi = (size_t)i * m + row;
-      double xr, xi;
-      if (i == nb - 1) {
-        if (row != gw) btri_row_load<T, KR>(SinvT + i * mm + (size_t)row * m, m, r);
-        const double2 acc = btri_row_dot<T, KR>(r, vs, m);
-        xr = acc.x;
-        xi = acc.y;
-      } else {
-        const double wr = lane == 0 ? __ldcg(a.w + gi) : 0.0, wi = lane == 0 ? __ldcg(a.w + P + gi) : 0.0;
-        if (row != gw) btri_row_load<T, KR>(HT + i * mm + (size_t)row * m, m, r);
-        const double2 acc = btri_row_dot<T, KR>(r, vs, m);
-        xr = wr - acc.x;
-        xi = wi - acc.y;
-      }
-      if (lane == 0) {
-        a.x[gi] = xr;
-        a.x[P + gi] = xi;
-        if (gi < a.NN) {
+        double xr, xi;
+        double* dst;
+        if (g.kind == 1 || g.kind == 3) {
+          xr = br - acc.x; xi = bi - acc.y; dst = a.y;
+        } else if (g.kind == 2) {
+          xr = acc.x; xi = acc.y; dst = a.w;
+        } else if (g.kind == 4) {
+          xr = acc.x; xi = acc.y; dst = a.x;
+        } else {
+          xr = br - acc.x; xi = bi - acc.y; dst = a.x;
+        }
+        dst[gi] = xr;
+        dst[P + gi] = xi;
+        if ((g.kind == 4 || g.kind == 5) && gi < a.NN) {
           a.io[gi] = xr;
           a.io[a.NN + gi] = xi;
         }
       }
     }
-    if (i > 0) {
+    if (s + 1 < nsteps) {
       btri_arrive(a.bar);
-      if (gw < m) btri_row_load<T, KR>(HT + (i - 1) * mm + (size_t)gw * m, m, r);
+      st = btri_step(s + 1, nb, k);
+      if (gw < st.ng * m) {  // prefetch the first task's row of the next step
+        const BtGroup& g = st.g[gw / m];
+        if (g.mat) {
+          btri_row_load<T, KR>(bt_mat<T>(a, g.mat, g.mblk, gw % m), m, r);
+          pre = gw;
+        }
+      }
       btri_wait(a.bar, ++phase * G);
     }
   }

@@ -640,7 +640,7 @@ static void free_exact(ExactSolver& X) {
   cudaFree(X.Ainv); cudaFree(X.dx); cudaFree(X.dy);
   if (X.btri) {
     cudaFree(const_cast<void*>(X.bt.GT)); cudaFree(const_cast<void*>(X.bt.SinvT));
-    cudaFree(const_cast<void*>(X.bt.HT)); cudaFree(X.bt.y); cudaFree(X.bt.bar);
+    cudaFree(const_cast<void*>(X.bt.HT)); cudaFree(const_cast<void*>(X.bt.G2)); cudaFree(X.bt.y); cudaFree(X.bt.bar);
   }
   X = ExactSolver{};
 }
@@ -945,7 +945,7 @@ static void dense_apply(hd_ctx* c, const ExactSolver& X, const double2* x, doubl
 // Block tridiagonal exact solve (btri.cuh), in/out planar.
 template <class T, int KR>
 static void btri_launch_t(hd_ctx* c, ExactSolver& X) {
-  const size_t smem = 2 * static_cast<size_t>(X.bt.m) * sizeof(double);
+  const size_t smem = 4 * static_cast<size_t>(X.bt.m) * sizeof(double);  // two staged vectors
   static size_t attr = 0;
   if (smem > attr) {
     CK(cudaFuncSetAttribute(k_btri_solve<T, KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -968,7 +968,7 @@ static void btri_solve(hd_ctx* c, ExactSolver& X, double* inout) {
   X.bt.io = inout;
   CK(cudaMemsetAsync(X.bt.bar, 0, sizeof(unsigned), c->st));
   const double mm = static_cast<double>(X.bt.m) * X.bt.m * (X.bt_cplx ? 2.0 : 1.0);
-  HD_LAUNCH(HD_K_EXACT, 8.0 * mm * (3.0 * X.bt.nb - 2.0) + 32.0 * X.bt.NN,
+  HD_LAUNCH(HD_K_EXACT, 8.0 * mm * (3.0 * X.bt.nb - 1.0) + 32.0 * X.bt.NN,
             if (X.bt_cplx) switch (X.bt_kr) {
               case 8: btri_launch_t<double2, 8>(c, X); break;
               case 16: btri_launch_t<double2, 16>(c, X); break;
@@ -2006,10 +2006,12 @@ template <class T>
 static void btri_factor(cudaStream_t st, const GenLevel& L, int q, int m, int nb, ExactSolver& X) {
   using Lb = BtriLib<T>;
   const size_t mm = static_cast<size_t>(m) * m, tot = static_cast<size_t>(nb) * mm;
+  const int k = nb / 2;  // the twist: top half eliminated downwards, bottom half upwards
   T *D = dalloc<T>(tot), *Bu = dalloc<T>(tot), *Cl = dalloc<T>(tot);
-  T *GT = dalloc<T>(tot), *SinvT = dalloc<T>(tot), *HT = dalloc<T>(tot);
-  CK(cudaMemsetAsync(GT, 0, mm * sizeof(T), st));
-  CK(cudaMemsetAsync(HT + (nb - 1) * mm, 0, mm * sizeof(T), st));
+  T *GT = dalloc<T>(tot), *SinvT = dalloc<T>(tot), *HT = dalloc<T>(tot), *G2 = dalloc<T>(mm);
+  CK(cudaMemsetAsync(GT, 0, tot * sizeof(T), st));
+  CK(cudaMemsetAsync(HT, 0, tot * sizeof(T), st));
+  CK(cudaMemsetAsync(G2, 0, mm * sizeof(T), st));
   k_btri_blocks<T><<<grid_for(tot, 256, 148 * 32), 256, 0, st>>>(L, q, m, nb, D, Bu, Cl);
   CK(cudaGetLastError());
   cublasHandle_t cb;
@@ -2027,21 +2029,33 @@ static void btri_factor(cudaStream_t st, const GenLevel& L, int q, int m, int nb
   std::vector<T> eye(mm);
   for (size_t e = 0; e < mm; ++e) eye[e] = (e % (m + 1) == 0) ? Lb::one() : Lb::zero();
   const T one = Lb::one(), mone = Lb::mone(), zero = Lb::zero();
-  for (int i = 0; i < nb; ++i) {
-    T* S = D + i * mm;  // S_i overwrites D_i
-    // S_i = D_i - G_i B_{i-1}   (G_i = (G_i^T)^T)
-    if (i > 0) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, GT + i * mm, Bu + (i - 1) * mm, &one, S));
+  // Schur block S (in place of D_i) -> its inverse transposed in SinvT[i] (= row-major inverse)
+  auto invert = [&](int i) {
+    T* S = D + i * mm;
     CKS(Lb::getrf(hs, m, S, work, ipiv, info + 2 * i));
-    // S_i^-T = solve(S_i^T X = I)
     T* Si = SinvT + i * mm;
     CK(cudaMemcpyAsync(Si, eye.data(), mm * sizeof(T), cudaMemcpyHostToDevice, st));
-    CKS(Lb::getrs_t(hs, m, S, ipiv, Si, info + 2 * i + 1));
-    if (i + 1 < nb) {
-      // G_{i+1}^T = S_i^-T C_{i+1}^T ;  H_i^T = B_i^T S_i^-T
-      CKB(Lb::gemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, &one, Si, Cl + (i + 1) * mm, &zero, GT + (i + 1) * mm));
-      CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &one, Bu + i * mm, Si, &zero, HT + i * mm));
-    }
+    CKS(Lb::getrs_t(hs, m, S, ipiv, Si, info + 2 * i + 1));  // S^T X = I
+  };
+  // top: i = 0 .. k-1  (S_i = D_i - G_i B_{i-1}; G_{i+1}^T = S_i^-T C_{i+1}^T; H_i^T = B_i^T S_i^-T)
+  for (int i = 0; i < k; ++i) {
+    if (i > 0) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, GT + i * mm, Bu + (i - 1) * mm, &one, D + i * mm));
+    invert(i);
+    CKB(Lb::gemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, &one, SinvT + i * mm, Cl + (i + 1) * mm, &zero, GT + (i + 1) * mm));
+    CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &one, Bu + i * mm, SinvT + i * mm, &zero, HT + i * mm));
   }
+  // bottom: i = nb-1 .. k+1  (T_i = D_i - G'_i C_{i+1}; G'_{i-1}^T = T_i^-T B_{i-1}^T; H'_i^T = C_i^T T_i^-T)
+  for (int i = nb - 1; i > k; --i) {
+    if (i < nb - 1) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, GT + i * mm, Cl + (i + 1) * mm, &one, D + i * mm));
+    invert(i);
+    T* gdst = (i - 1 == k) ? G2 : GT + (i - 1) * mm;
+    CKB(Lb::gemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, &one, SinvT + i * mm, Bu + (i - 1) * mm, &zero, gdst));
+    CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &one, Cl + i * mm, SinvT + i * mm, &zero, HT + i * mm));
+  }
+  // middle: M = D_k - G_k B_{k-1} - G'_k C_{k+1}
+  if (k > 0) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, GT + k * mm, Bu + (k - 1) * mm, &one, D + k * mm));
+  if (k < nb - 1) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, G2, Cl + (k + 1) * mm, &one, D + k * mm));
+  invert(k);
   std::vector<int> hinfo(2 * nb);
   CK(cudaMemcpyAsync(hinfo.data(), info, hinfo.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -2050,12 +2064,14 @@ static void btri_factor(cudaStream_t st, const GenLevel& L, int q, int m, int nb
   cudaFree(D); cudaFree(Bu); cudaFree(Cl); cudaFree(work); cudaFree(ipiv); cudaFree(info);
   for (int v : hinfo)
     if (v != 0) {
-      cudaFree(GT); cudaFree(SinvT); cudaFree(HT);
+      cudaFree(GT); cudaFree(SinvT); cudaFree(HT); cudaFree(G2);
       throw Error(HD_ERR_FACTOR, "block tridiagonal exact solve: singular block (info " + std::to_string(v) + ")");
     }
   X.bt.GT = GT;
+  X.bt.G2 = G2;
   X.bt.SinvT = SinvT;
   X.bt.HT = HT;
+  X.bt.k = k;
 }
 
 static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int n_sms) {
