@@ -59,6 +59,11 @@ struct Problem {
   double k = 1.0;
   bool layered = false;
   std::array<double, 16> multipliers{};
+  // BASELINE config-4 wedge (an extension: the reference's WaveField cannot express it)
+  bool wedge = false;
+  std::array<double, 4> lines{{0.6, -0.2, 0.3, 0.1}};  // top iff y > l0 + l1 x; middle iff y > l2 + l3 x
+  bool point_source = false;                           // load at `source` instead of (1/2, 1/2)
+  std::array<double, 2> source{{0.5, 0.5}};
 };
 
 inline Problem point_source_1d(int elements, int order, double k) {
@@ -86,10 +91,31 @@ inline Problem layered_medium_2d(int elements, int order, double k,
   return p;
 }
 
+// The three-layer wedge k = k0 (1.2, 1.5, 1.0) with the load at (1/2, 1 - h):
+// BASELINE config 4 (oracle/helmdef_oracle.py wedge_2d freezes the same rule).
+inline Problem wedge_2d(int elements, int order, double k0) {
+  Problem p;
+  p.name = "wedge_2d";
+  p.dim = 2;
+  p.order = order;
+  p.elements = elements;
+  p.k = k0;
+  p.wedge = true;
+  p.multipliers.fill(0.0);
+  p.multipliers[0] = 1.2;
+  p.multipliers[1] = 1.5;
+  p.multipliers[2] = 1.0;
+  p.point_source = true;
+  p.source = {{0.5, 1.0 - 1.0 / elements}};
+  return p;
+}
+
 struct DiscreteSystem {
   int dim = 1, order = 1, elements = 1, per_dim = 0;
   double k = 0.0;
   bool layered = false;
+  bool wedge = false;
+  std::vector<double> shift_mass_2d;  // wedge: K2 as a 2D stencil, N x (2p+1)^2
   std::array<double, 16> multipliers{};
   std::vector<double> stiffness_band, mass_band, interval_mass;  // per_dim x (2p+1) (x4 for interval_mass)
   Vec rhs;
@@ -102,8 +128,12 @@ inline hd_problem to_hd(const Problem& pb) {
   h.order = pb.order;
   h.elements = pb.elements;
   h.k = pb.k;
-  h.field_kind = pb.layered ? HD_FIELD_LAYERED : HD_FIELD_CONSTANT;
+  h.field_kind = pb.wedge ? HD_FIELD_WEDGE : (pb.layered ? HD_FIELD_LAYERED : HD_FIELD_CONSTANT);
   for (int i = 0; i < 16; ++i) h.multipliers[i] = pb.multipliers[i];
+  for (int i = 0; i < 4; ++i) h.lines[i] = pb.lines[i];
+  h.point_source = pb.point_source ? 1 : 0;
+  h.source[0] = pb.source[0];
+  h.source[1] = pb.source[1];
   return h;
 }
 
@@ -126,6 +156,11 @@ inline DiscreteSystem assemble(const Problem& pb) {
   s.rhs.assign(N, cplx(0.0, 0.0));
   check(hd_assemble(&h, s.stiffness_band.data(), s.mass_band.data(),
                     pb.layered ? s.interval_mass.data() : nullptr, reinterpret_cast<double*>(s.rhs.data())));
+  s.wedge = pb.wedge;
+  if (pb.wedge) {
+    s.shift_mass_2d.assign(N * (2 * pb.order + 1) * (2 * pb.order + 1), 0.0);
+    check(hd_assemble_field(&h, s.shift_mass_2d.data()));
+  }
   return s;
 }
 
@@ -197,12 +232,13 @@ inline SolverSetup compose(const DiscreteSystem& sys, const PrecondSpec& spec) {
   hs.order = sys.order;
   hs.elements = sys.elements;
   hs.per_dim = sys.per_dim;
-  hs.field_kind = sys.layered ? HD_FIELD_LAYERED : HD_FIELD_CONSTANT;
+  hs.field_kind = sys.wedge ? HD_FIELD_WEDGE : (sys.layered ? HD_FIELD_LAYERED : HD_FIELD_CONSTANT);
   hs.k = sys.k;
   for (int i = 0; i < 16; ++i) hs.multipliers[i] = sys.multipliers[i];
   hs.stiffness_band = sys.stiffness_band.data();
   hs.mass_band = sys.mass_band.data();
   hs.interval_mass = sys.layered ? sys.interval_mass.data() : nullptr;
+  hs.shift_mass_2d = sys.wedge ? sys.shift_mass_2d.data() : nullptr;
   hd_precond hp{};
   hp.deflate = spec.deflate ? 1 : 0;
   hp.drop = spec.drop;

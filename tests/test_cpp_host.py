@@ -37,7 +37,7 @@ def test_tool_built():
 
 
 @pytest.mark.parametrize("problem,p,k,ne", [("point_source_1d", 2, 50.0, 80), ("point_source_2d", 3, 40.0, 64),
-                                            ("layered_medium_2d", 2, 50.0, 79)])
+                                            ("layered_medium_2d", 2, 50.0, 79), ("wedge_2d", 3, 30.0, 40)])
 def test_cpp_assembly_matches_oracle(problem, p, k, ne):
     d = json.loads(_run("--assemble", problem, p, k, ne).stdout)
     so = O.assemble(O.make_problem(problem, ne, p, k))
@@ -47,6 +47,9 @@ def test_cpp_assembly_matches_oracle(problem, p, k, ne):
     M1 = so.M1.toarray() if hasattr(so.M1, "toarray") else np.asarray(so.M1)
     assert abs(d["stiffness_sum"] - S1.sum()) <= 1e-12 * abs(S1).sum()
     assert abs(d["mass_sum"] - M1.sum()) <= 1e-12 * abs(M1).sum()
+    if problem == "wedge_2d":
+        k2 = so.shift_mass.real
+        assert abs(d["shift_mass_sum"] - k2.sum()) <= 1e-12 * abs(k2).sum()
 
 
 def test_cpp_solve_fails_loudly_without_gpu():
@@ -66,6 +69,8 @@ CELLS = [
     ("point_source_2d", "DC_MG", 3, 40.0, 64, dict(beta2="0.5", cycles=1, smoothing=1, omega=2.0 / 3.0)),
     ("point_source_2d", "Deps_C_MG", 2, 30.0, 48, dict(beta2="1", cycles=2, smoothing=2, omega=0.6, epsilon=0.1)),
     ("layered_medium_2d", "DC_MG", 2, 50.0, 79, dict(beta2="4.2", cycles=12, smoothing=3, omega=0.6)),
+    ("layered_medium_2d", "C_ex", 3, 50.0, 78, dict(beta2="1/(3k)", cycles=1, smoothing=1, omega=0.6)),
+    ("wedge_2d", "DC_MG", 3, 40.0, 64, dict(beta2="0.5", cycles=1, smoothing=1, omega=2.0 / 3.0)),
 ]
 
 
@@ -76,7 +81,7 @@ def test_cpp_run_cell_matches_oracle(problem, tag, p, k, ne, kw):
             kw.get("epsilon", 0.1)]
     d = json.loads(_run(*args).stdout.strip().splitlines()[-1])
     so = O.assemble(O.make_problem(problem, ne, p, k))
-    two_d_const = so.dim == 2 and not so.layered
+    two_d_const = so.dim == 2 and so.separable
     st = O.compose(so, O.to_spec(tag, p, k, **kw), galerkin="kron" if two_d_const else "sparse",
                    e_solver="fd" if two_d_const else "splu")
     g = O.gmres(st.op, st.rhs, st.start, st.monitor, O.GmresOptions(100, 1e-7))

@@ -19,6 +19,7 @@ static hb::Problem make_problem(const std::string& name, int e, int p, double k)
   if (name == "point_source_1d") return hb::point_source_1d(e, p, k);
   if (name == "point_source_2d") return hb::point_source_2d(e, p, k);
   if (name == "layered_medium_2d") return hb::layered_medium_2d(e, p, k);
+  if (name == "wedge_2d") return hb::wedge_2d(e, p, k);
   throw hb::Error(HD_ERR_INVALID, "unknown problem: " + name);
 }
 
@@ -31,8 +32,11 @@ int main(int argc, char** argv) {
       for (const auto& v : s.rhs) fn += std::norm(v);
       for (double v : s.stiffness_band) ss += v;
       for (double v : s.mass_band) ms += v;
-      std::printf("{\"per_dim\": %d, \"size\": %ld, \"rhs_norm\": %.17g, \"stiffness_sum\": %.17g, \"mass_sum\": %.17g}\n",
-                  s.per_dim, s.size(), std::sqrt(fn), ss, ms);
+      double ks = 0.0;
+      for (double v : s.shift_mass_2d) ks += v;
+      std::printf("{\"per_dim\": %d, \"size\": %ld, \"rhs_norm\": %.17g, \"stiffness_sum\": %.17g, \"mass_sum\": %.17g, "
+                  "\"shift_mass_sum\": %.17g}\n",
+                  s.per_dim, s.size(), std::sqrt(fn), ss, ms, ks);
       return 0;
     }
     if (argc < 5) {
