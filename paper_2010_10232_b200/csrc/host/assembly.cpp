@@ -192,15 +192,18 @@ std::vector<double> wedge_mass_stencil(const Knots& kv, double k0, const double*
   const size_t rowsz = static_cast<size_t>(NB) * nb * NB;
   std::vector<double> K(static_cast<size_t>(nb) * rowsz, 0.0);
   std::vector<double> T(static_cast<size_t>(m) * m * m);  // T[qy][lx][mx] of one element
+  std::vector<double> KK(static_cast<size_t>(m) * m);      // k^2 at the element's Gauss points [qy][qx]
   for (int ey = 0; ey < ne; ++ey)
     for (int ex = 0; ex < ne; ++ex) {
+      for (int qy = 0; qy < m; ++qy)
+        for (int qx = 0; qx < m; ++qx) KK[qy * m + qx] = wedge_k2(X[ex * m + qx], X[ey * m + qy], k0, mult, lines);
       // x stage: T[qy][lx][mx] = sum_qx w_qx k^2 B[ex,qx,lx] B[ex,qx,mx]
       for (int qy = 0; qy < m; ++qy)
         for (int lx = 0; lx < m; ++lx)
           for (int mx = 0; mx < m; ++mx) {
             double t = 0.0;
             for (int qx = 0; qx < m; ++qx) {
-              const double kk = wedge_k2(X[ex * m + qx], X[ey * m + qy], k0, mult, lines);
+              const double kk = KK[qy * m + qx];
               t += kk * W[ex * m + qx] * B[(static_cast<size_t>(ex) * m + qx) * m + lx] *
                    B[(static_cast<size_t>(ex) * m + qx) * m + mx];
             }

@@ -1749,12 +1749,48 @@ struct GenHost {
 };
 
 // Galerkin product (z (x) z)^T K (z (x) z) of a 2D stencil (the reference's
-// sparse triple product Z^T M Z, src/precond.cpp:119, in stencil form).
+// sparse triple product Z^T M Z, src/precond.cpp:119, in stencil form), on the
+// device: one thread per coarse entry (I, J - I), gathering over the children
+// of I and J in y and in x.  K and Kc are row-major [point][tap].
+__global__ void k_galerkin_stencil(const double* __restrict__ K, int n, int b, const int* __restrict__ cptr,
+                                   const int* __restrict__ crow, const double* __restrict__ cw, int nc, int bc,
+                                   double* __restrict__ Kc) {
+  const int NB = 2 * b + 1, NBc = 2 * bc + 1;
+  const size_t tot = (size_t)nc * nc * NBc * NBc;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+    const int tap = (int)(e % (NBc * NBc));
+    const size_t I = e / (NBc * NBc);
+    const int Iy = (int)(I / nc), Ix = (int)(I % nc);
+    const int Jy = Iy + tap / NBc - bc, Jx = Ix + tap % NBc - bc;
+    double acc = 0.0;
+    if (Jy >= 0 && Jy < nc && Jx >= 0 && Jx < nc) {
+      for (int pa = cptr[Iy]; pa < cptr[Iy + 1]; ++pa)
+        for (int pc = cptr[Jy]; pc < cptr[Jy + 1]; ++pc) {
+          const int iy = crow[pa], jy = crow[pc], dy = jy - iy;
+          if (dy < -b || dy > b) continue;
+          const double wy = cw[pa] * cw[pc];
+          double sx = 0.0;
+          for (int pb = cptr[Ix]; pb < cptr[Ix + 1]; ++pb)
+            for (int pd = cptr[Jx]; pd < cptr[Jx + 1]; ++pd) {
+              const int ix = crow[pb], jx = crow[pd], dx = jx - ix;
+              if (dx < -b || dx > b) continue;
+              sx += cw[pb] * cw[pd] * K[((size_t)iy * n + ix) * NB * NB + (dy + b) * NB + (dx + b)];
+            }
+          acc += wy * sx;
+        }
+    }
+    Kc[e] = acc;
+  }
+}
+
 static void galerkin_stencil2d(const std::vector<double>& K, int n, int b, const Transfer& z, std::vector<double>& Kc,
                                int& bc) {
   const int nc = z.coarse;
-  std::vector<std::vector<std::pair<int, double>>> par(n);
-  for (size_t t = 0; t < z.w.size(); ++t) par[z.row[t]].push_back({z.col[t], z.w[t]});
+  std::vector<std::vector<std::pair<int, double>>> par(n), ch(nc);
+  for (size_t t = 0; t < z.w.size(); ++t) {
+    par[z.row[t]].push_back({z.col[t], z.w[t]});
+    ch[z.col[t]].push_back({z.row[t], z.w[t]});
+  }
   bc = 0;
   for (int i = 0; i < n; ++i)
     for (int d = -b; d <= b; ++d) {
@@ -1763,29 +1799,36 @@ static void galerkin_stencil2d(const std::vector<double>& K, int n, int b, const
       for (const auto& I : par[i])
         for (const auto& J : par[j]) bc = std::max(bc, std::abs(J.first - I.first));
     }
-  const int NB = 2 * b + 1, NBc = 2 * bc + 1;
-  Kc.assign(static_cast<size_t>(nc) * nc * NBc * NBc, 0.0);
-  for (int iy = 0; iy < n; ++iy)
-    for (int ix = 0; ix < n; ++ix)
-      for (int dy = -b; dy <= b; ++dy) {
-        const int jy = iy + dy;
-        if (jy < 0 || jy >= n) continue;
-        for (int dx = -b; dx <= b; ++dx) {
-          const int jx = ix + dx;
-          if (jx < 0 || jx >= n) continue;
-          const double v = K[(static_cast<size_t>(iy) * n + ix) * NB * NB + (dy + b) * NB + (dx + b)];
-          if (v == 0.0) continue;
-          for (const auto& Iy : par[iy])
-            for (const auto& Jy : par[jy]) {
-              const double vy = Iy.second * v * Jy.second;
-              const int oy = Jy.first - Iy.first + bc;
-              for (const auto& Ix : par[ix])
-                for (const auto& Jx : par[jx])
-                  Kc[(static_cast<size_t>(Iy.first) * nc + Ix.first) * NBc * NBc + oy * NBc +
-                     (Jx.first - Ix.first + bc)] += vy * Ix.second * Jx.second;
-            }
-        }
-      }
+  // children of every coarse index (CSR), fine row order as in z
+  std::vector<int> cptr(nc + 1, 0), crow;
+  std::vector<double> cw;
+  for (int c = 0; c < nc; ++c) {
+    for (const auto& f : ch[c]) {
+      crow.push_back(f.first);
+      cw.push_back(f.second);
+    }
+    cptr[c + 1] = static_cast<int>(crow.size());
+  }
+  const int NBc = 2 * bc + 1;
+  const size_t outn = static_cast<size_t>(nc) * nc * NBc * NBc;
+  double* dK = dalloc<double>(K.size());
+  double* dKc = dalloc<double>(outn);
+  int* dptr = dalloc<int>(cptr.size());
+  int* drow = dalloc<int>(std::max<size_t>(crow.size(), 1));
+  double* dw = dalloc<double>(std::max<size_t>(cw.size(), 1));
+  CK(cudaMemcpy(dK, K.data(), K.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dptr, cptr.data(), cptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(drow, crow.data(), crow.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dw, cw.data(), cw.size() * sizeof(double), cudaMemcpyHostToDevice));
+  k_galerkin_stencil<<<grid_for(outn, 256, 148 * 16), 256>>>(dK, n, b, dptr, drow, dw, nc, bc, dKc);
+  CK(cudaGetLastError());
+  Kc.resize(outn);
+  CK(cudaMemcpy(Kc.data(), dKc, outn * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(dK);
+  cudaFree(dKc);
+  cudaFree(dptr);
+  cudaFree(drow);
+  cudaFree(dw);
 }
 
 // wedge fine level: (M, S), (S, M) and the stored K2 stencil
@@ -2185,6 +2228,16 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   if (wedge && !sys->shift_mass_2d) throw Error(HD_ERR_INVALID, "wedge field needs shift_mass_2d (hd_assemble_field)");
   if (sys->per_dim < 2) throw Error(HD_ERR_INVALID, "per_dim must be >= 2");
   const auto t0 = std::chrono::steady_clock::now();
+  // HD_SETUP_TRACE=1: wall time of the setup phases on stderr
+  const bool trace = std::getenv("HD_SETUP_TRACE") && std::atoi(std::getenv("HD_SETUP_TRACE")) == 1;
+  auto tlast = t0;
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hd setup] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - tlast).count());
+    tlast = now;
+  };
   std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
   c->device = (devices && n_devices == 1) ? devices[0] : 0;
   if (!devices || n_devices == 0) CK(cudaGetDevice(&c->device));
@@ -2210,6 +2263,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   c->cM = cmk(k2, -k2 * c->spec.beta2);
   const Band S1 = band_from_host(sys->stiffness_band, c->n, sys->order);
   const Band M1 = band_from_host(sys->mass_band, c->n, sys->order);
+  mark("context, streams, handles");
   c->fine = upload_pair(S1, M1);
   GenHost fineH;
   if (gen) {
@@ -2232,6 +2286,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
       c->shift_exact = make_bandlu(S1, M1, c->cM, c->corner);
     }
   }
+  mark("fine level (+ C_ex)");
   // multigrid hierarchy of the shifted operator (src/precond.cpp:110-134)
   if (c->spec.shift && c->spec.cycles > 0) {
     std::vector<Band> Ss{S1}, Ms{M1};
@@ -2283,6 +2338,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
       c->mg_r.push_back(dalloc<double2>(NL));
     }
   }
+  mark("multigrid hierarchy");
   // deflation: E = Z^T A Z with the Bezier stencil (src/precond.cpp:93-100, 228-232)
   if (c->spec.deflate) {
     const Transfer z = halving_stencil(c->n, c->spec.drop);
@@ -2320,6 +2376,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
     c->ep = dalloc<double>(2 * NC);
     c->ep2 = dalloc<double>(2 * NC);
   }
+  mark("deflation E and its solver");
   const size_t N = c->N;
   c->f = dalloc<double2>(N);
   c->rhsp = dalloc<double2>(N);
@@ -2344,6 +2401,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   CK(cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, c->device));
   c->cublas_ws = dalloc<char>(32u << 20);
   CKB(cublasSetWorkspace(c->cb, c->cublas_ws, 32u << 20));
+  mark("vectors, workspaces");
   c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = c.release();
 }
