@@ -2505,6 +2505,12 @@ struct hd_slabs {
   std::vector<int> mine;                        // slabs of this process
   std::vector<SlabPost> sends, recvs;           // posted in the current group (vranks)
   double2* red = nullptr;                       // S x nslot per-slab Arnoldi pass-1 sums
+  // distributed E solve (plain fast diagonalisation): per-slab transform
+  // buffers (one shared buffer when all slabs are local and not virtual
+  // ranks) and all-to-all staging (pack -> send/recv -> unpack)
+  bool dist_e = false;
+  std::vector<double*> eT1, eT2;                // [slab] 2 planes x nc^2
+  std::vector<double*> esend, erecv;            // [slab] staging, 2 planes x nc x own columns
   // graph-resident iteration (HD_GRAPH != 0): one captured body per (maxit),
   // launched once per iteration with the iteration index in device memory
   int* dj = nullptr;                            // device iteration index
@@ -2821,6 +2827,125 @@ static void s_mg_solve(hd_ctx* c, std::vector<double2*>& b, std::vector<double2*
                        own(G, s) * row, cudaMemcpyDeviceToDevice, c->st));
 }
 
+// rows [r0, r1) of both planes of a column-major n x n transform buffer scaled by Dinv
+__global__ void k_fd_scale_rows(double* __restrict__ T, const double2* __restrict__ Dinv, int n, int r0, int r1) {
+  const size_t NN = (size_t)n * n;
+  const int h = r1 - r0;
+  const size_t tot = (size_t)h * n;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t g = (e / h) * n + r0 + e % h;
+    const double2 v = cmul(cmk(T[g], T[g + NN]), Dinv[g]);
+    T[g] = v.x;
+    T[g + NN] = v.y;
+  }
+}
+
+// All-to-all of the distributed E solve.  to_rows: block (rows R_t, cols C_s)
+// of slab s's buffer goes to slab t (cols -> rows); else block (rows R_s,
+// cols C_t) of slab s goes to slab t (rows -> cols).  R and C both follow the
+// deflation grid's slab rows.  Pack (2D copies into a contiguous staging
+// block per peer), transfer (NCCL send/recv, or the virtual-rank matcher),
+// unpack; with every slab local and no virtual ranks the buffer is shared and
+// nothing moves.
+static void e_alltoall(hd_ctx* c, bool to_rows) {
+  hd_slabs* sl = slabs_of(c);
+  if (!remote_pairs(sl)) return;
+  const int nc = c->nc;
+  const size_t NN = static_cast<size_t>(nc) * nc;
+  const SlabLevel& Gc = sl->lv[1];
+  auto lo = [&](int t) { return Gc.bounds[t]; };
+  auto cnt = [&](int t) { return Gc.bounds[t + 1] - Gc.bounds[t]; };
+  const size_t dp = sizeof(double);
+  // pack: for each local s and each peer t != s, the block for t, both planes, contiguous
+  for (int s : sl->mine) {
+    size_t off = 0;
+    for (int t = 0; t < sl->S; ++t) {
+      if (t == s) continue;
+      const int rr0 = to_rows ? lo(t) : lo(s), rh = to_rows ? cnt(t) : cnt(s);
+      const int cc0 = to_rows ? lo(s) : lo(t), cw = to_rows ? cnt(s) : cnt(t);
+      for (int pl = 0; pl < 2; ++pl) {
+        CK(cudaMemcpy2DAsync(sl->esend[s] + off, rh * dp, sl->eT1[s] + pl * NN + static_cast<size_t>(cc0) * nc + rr0,
+                             nc * dp, rh * dp, cw, cudaMemcpyDeviceToDevice, c->st));
+        off += static_cast<size_t>(rh) * cw;
+      }
+    }
+  }
+  // transfer
+  std::vector<int> send_from, recv_to;
+  xp_group_start(c);
+  for (int s : sl->mine) {
+    size_t so = 0, ro = 0;
+    for (int t = 0; t < sl->S; ++t) {
+      if (t == s) continue;
+      const size_t ns = 2 * static_cast<size_t>(to_rows ? cnt(t) * cnt(s) : cnt(s) * cnt(t));
+      const size_t nr = ns;  // the block from t has the same shape (|R_s| x |C_t| or |R_t| x |C_s| swapped)
+      // double2 counts for the transport (2 doubles each); blocks have an even double count (2 planes)
+      xp_send(c, reinterpret_cast<const double2*>(sl->esend[s] + so), ns / 2, s, t);
+      send_from.push_back(s);
+      xp_recv(c, reinterpret_cast<double2*>(sl->erecv[s] + ro), nr / 2, t, s);
+      recv_to.push_back(s);
+      so += ns;
+      ro += nr;
+    }
+  }
+  xp_group_end(c, send_from, recv_to);
+  // unpack: the block from t lands at (rows R_s, cols C_t) (to_rows) or (rows R_t, cols C_s)
+  for (int s : sl->mine) {
+    size_t off = 0;
+    for (int t = 0; t < sl->S; ++t) {
+      if (t == s) continue;
+      const int rr0 = to_rows ? lo(s) : lo(t), rh = to_rows ? cnt(s) : cnt(t);
+      const int cc0 = to_rows ? lo(t) : lo(s), cw = to_rows ? cnt(t) : cnt(s);
+      for (int pl = 0; pl < 2; ++pl) {
+        CK(cudaMemcpy2DAsync(sl->eT1[s] + pl * NN + static_cast<size_t>(cc0) * nc + rr0, nc * dp, sl->erecv[s] + off,
+                             rh * dp, rh * dp, cw, cudaMemcpyDeviceToDevice, c->st));
+        off += static_cast<size_t>(rh) * cw;
+      }
+    }
+  }
+}
+
+// E^-1 on the slabs by the fast diagonalisation with the work split by slab:
+// x transforms of the slab's own coarse rows (columns of the column-major
+// planes), all-to-all to kx-row blocks, y transforms and the scaling of the
+// own kx rows, all-to-all back, inverse x transforms of the own rows.  ep
+// holds each slab's restricted rows on entry and its rows of E^-1 r on exit.
+static void s_e_solve_dist(hd_ctx* c) {
+  hd_slabs* sl = slabs_of(c);
+  ExactSolver& X = c->E;
+  const int n = X.n;
+  const long nn = static_cast<long>(n) * n;
+  const double one = 1.0, zero = 0.0;
+  const SlabLevel& Gc = sl->lv[1];
+  auto gemm_b = [&](cublasOperation_t ta, cublasOperation_t tb, int m, int nn_, const double* A, int lda, long sA,
+                    const double* B, int ldb, long sB, double* C2, int ldc, long sC) {
+    const size_t mk = prof_mark(c);
+    CKB(cublasDgemmStridedBatched(c->cb, ta, tb, m, nn_, n, &one, A, lda, sA, B, ldb, sB, &zero, C2, ldc, sC, 2));
+    launched(c, HD_K_LIBGEMM, mk, 16.0 * nn, true);
+  };
+  for (int s : sl->mine) {  // x transforms of the own columns
+    const int q0 = Gc.bounds[s], w = Gc.bounds[s + 1] - q0;
+    gemm_b(CUBLAS_OP_T, CUBLAS_OP_N, n, w, X.V, n, 0, c->ep + static_cast<size_t>(q0) * n, n, nn,
+           sl->eT1[s] + static_cast<size_t>(q0) * n, n, nn);
+  }
+  e_alltoall(c, true);
+  for (int s : sl->mine) {  // y transforms, scaling, inverse y transforms of the own kx rows
+    const int r0 = Gc.bounds[s], h = Gc.bounds[s + 1] - r0;
+    gemm_b(CUBLAS_OP_N, CUBLAS_OP_N, h, n, sl->eT1[s] + r0, n, nn, X.V, n, 0, sl->eT2[s] + r0, n, nn);
+    HD_LAUNCH(HD_K_EXACT, 48.0 * h * n,
+              k_fd_scale_rows<<<grid_for(static_cast<size_t>(h) * n), 256, 0, c->st>>>(sl->eT2[s], X.Dinv, n, r0,
+                                                                                        r0 + h));
+    gemm_b(CUBLAS_OP_N, CUBLAS_OP_T, h, n, sl->eT2[s] + r0, n, nn, X.V, n, 0, sl->eT1[s] + r0, n, nn);
+  }
+  e_alltoall(c, false);
+  for (int s : sl->mine) {  // inverse x transforms of the own columns
+    const int q0 = Gc.bounds[s], w = Gc.bounds[s + 1] - q0;
+    gemm_b(CUBLAS_OP_N, CUBLAS_OP_N, n, w, X.V, n, 0, sl->eT1[s] + static_cast<size_t>(q0) * n, n, nn,
+           c->ep + static_cast<size_t>(q0) * n, n, nn);
+  }
+  slab_share_rows(c, Gc, c->ep, true);  // the prolongation reads coarse rows around the slab
+}
+
 // deflation on the slabs: out = v - Z E^-1 Z^T (A v) (project) or Z E^-1 Z^T v (Q)
 static void s_deflate(hd_ctx* c, std::vector<double2*>& v, std::vector<double2*>& out, bool project) {
   hd_slabs* sl = slabs_of(c);
@@ -2836,8 +2961,12 @@ static void s_deflate(hd_ctx* c, std::vector<double2*>& v, std::vector<double2*>
   for (int s : sl->mine)
     restrict_(c, z, vptr((*src)[s], G.bounds[s], G.H, G.n), c->n, c->nc, nullptr, c->ep, Gc.bounds[s],
               Gc.bounds[s + 1]);
-  slab_share_rows(c, Gc, c->ep, true);  // the deflation coarse vector: allgather (both planes)
-  exact_solve_planar(c, c->E, c->ep);    // redundantly on every process
+  if (sl->dist_e) {
+    s_e_solve_dist(c);                    // the E solve split by slab (two all-to-alls)
+  } else {
+    slab_share_rows(c, Gc, c->ep, true);  // the deflation coarse vector: allgather (both planes)
+    exact_solve_planar(c, c->E, c->ep);    // redundantly on every process
+  }
   for (int s : sl->mine) {
     const int r0 = G.bounds[s], r1 = G.bounds[s + 1];
     if (project)
@@ -3230,6 +3359,34 @@ static void create_slabs(hd_ctx* c, int S, int rank = 0, int nranks = 1, ncclCom
   sl->Gs = std::max(1, std::min(c->lsa_G > 0 ? c->lsa_G : 296, static_cast<int>((Nmax + 1023) / 1024)));
   sl->parts = dalloc<double2>(static_cast<size_t>(S) * sl->Gs * (2 * kLsaMaxJ + 2) + 8);
   sl->red = dalloc<double2>(static_cast<size_t>(S) * kLsaNslot);
+  // distributed E solve when E is the plain fast diagonalisation (HD_DIST_E=0: redundant)
+  {
+    const ExactSolver& X = c->E;
+    const char* de = std::getenv("HD_DIST_E");
+    sl->dist_e = c->spec.deflate && X.dim == 2 && X.V && !X.folded && !X.ypart && !X.dense && !X.btri &&
+                 !(de && std::atoi(de) == 0);
+    if (sl->dist_e) {
+      const int nc = c->nc;
+      const size_t NN = static_cast<size_t>(nc) * nc;
+      const SlabLevel& Gc = sl->lv[1];
+      sl->eT1.assign(S, nullptr);
+      sl->eT2.assign(S, nullptr);
+      sl->esend.assign(S, nullptr);
+      sl->erecv.assign(S, nullptr);
+      for (int s2 : sl->mine) {
+        if (sl->vranks || sl->nranks > 1) {
+          sl->eT1[s2] = dalloc<double>(2 * NN);
+          sl->eT2[s2] = dalloc<double>(2 * NN);
+        } else {
+          sl->eT1[s2] = X.T1;
+          sl->eT2[s2] = X.T2;
+        }
+        const size_t own_c = static_cast<size_t>(Gc.bounds[s2 + 1] - Gc.bounds[s2]);
+        sl->esend[s2] = dalloc<double>(2 * static_cast<size_t>(nc) * own_c);
+        sl->erecv[s2] = dalloc<double>(2 * static_cast<size_t>(nc) * own_c);
+      }
+    }
+  }
   CK(cudaDeviceSynchronize());
 }
 
@@ -3247,6 +3404,15 @@ static void destroy_slabs(hd_ctx* c) {
   cudaFree(sl->slots);
   cudaFree(sl->parts);
   cudaFree(sl->red);
+  if (sl->vranks || sl->nranks > 1)
+    for (int s : sl->mine) {
+      cudaFree(sl->eT1[s]);
+      cudaFree(sl->eT2[s]);
+    }
+  for (int s : sl->mine) {
+    if (!sl->esend.empty()) cudaFree(sl->esend[s]);
+    if (!sl->erecv.empty()) cudaFree(sl->erecv[s]);
+  }
   if (sl->body) cudaGraphExecDestroy(sl->body);
   cudaFree(sl->dj);
   if (sl->hj) cudaFreeHost(sl->hj);

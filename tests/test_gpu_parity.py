@@ -475,11 +475,20 @@ def test_row_slabs_match_single_domain(S, ne, p, k, agg, vranks, graph, monkeypa
     through the posted send/recv records of the multi-process (NCCL) program,
     matched by (sender, receiver, order) and checked for equal sizes.
     graph = 1: each iteration is one captured graph launch (device-side
-    iteration index); graph = 0: the host-driven loop."""
+    iteration index); graph = 0: the host-driven loop.  The E solve runs split
+    by slab (x transforms of own rows, all-to-all, y transforms of own modes)
+    whenever E is the plain fast diagonalisation."""
     import torch
     monkeypatch.setenv("HD_SLAB_AGGLOMERATE", str(agg))
     monkeypatch.setenv("HD_SLAB_VRANKS", str(vranks))
     monkeypatch.setenv("HD_GRAPH", str(graph))
+    # virtual ranks: plain fast diagonalisation of E, so the E solve is split by
+    # slab with packed all-to-alls (even nc would otherwise fold E and solve it
+    # redundantly, as the shared-buffer cases with even nc do)
+    if vranks:
+        monkeypatch.setenv("HD_NOFOLD", "1")
+    else:
+        monkeypatch.delenv("HD_NOFOLD", raising=False)
     s = hd.assemble(hd.point_source_2d(ne, p, k))
     spec = hd.to_spec("DC_MG", p, k, **BASE)
     rng = np.random.default_rng(5)
