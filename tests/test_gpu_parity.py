@@ -543,3 +543,31 @@ def test_row_slabs_reject_unsupported():
     s2 = hd.assemble(hd.point_source_2d(40, 2, 20.0))
     with pytest.raises(hd.HelmdefError):
         hd.Solver(s2, hd.to_spec("DC_MG", 2, 20.0, **BASE), slabs=16)  # slabs thinner than the halo
+
+
+@pytest.mark.parametrize("tag,maxit", [("none", 150), ("D", 140), ("DC_MG", 200)])
+def test_long_budget_and_unpreconditioned(tag, maxit):
+    """Budgets above the one-reduction engine's limit (128 basis vectors) run on
+    the exact-order MGS engine; the unpreconditioned ('none') and deflation-only
+    ('D') chains (src/harness.cpp:175-205).  Against the oracle: iterations +-1,
+    converged flag, solution <= 1e-8, history <= 1e-10 except where two exact CPU
+    implementations (MGS vs its one-reduction form) already differ by more than
+    1e-10 -- long unpreconditioned Helmholtz histories amplify rounding -- where
+    the factor-3 envelope rule of C5 applies."""
+    import sys
+    sys.path.insert(0, str(GOLD))
+    from make_c5_envelope import gmres_icwy
+    ne, p, k = 48, 2, 30.0
+    kw = dict(beta2="0.5", cycles=1, smoothing=1, omega=2.0 / 3.0) if tag == "DC_MG" else {}
+    so, st = _oracle("point_source_2d", p, ne, k, tag, **kw)
+    opt = O.GmresOptions(maxit, 1e-10)
+    g = O.gmres(st.op, st.rhs, st.start, st.monitor, opt)
+    counts = dict(vars(st.counts))  # before the second CPU run adds to them
+    h = gmres_icwy(st.op, st.rhs, st.start, st.monitor, maxit=maxit, tol=1e-10)
+    m = min(len(h), len(g.residuals))
+    env = np.abs(np.array(h[:m]) - np.array(g.residuals[:m]))
+    s = hd.assemble(hd.point_source_2d(ne, p, k))
+    with hd.Solver(s, hd.to_spec(tag, p, k, **kw)) as solver:
+        r = solver.solve(hd.GmresOptions(maxit, 1e-10))
+    meta = dict(iterations=g.iterations, converged=g.converged, residuals=g.residuals, counts=counts)
+    _check(r, meta, g.solution, exact_iters=False, env=env)
