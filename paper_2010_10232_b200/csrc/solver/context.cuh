@@ -1,0 +1,663 @@
+// Device context: error handling, exact-solver types, hd_ctx, setup of the exact solvers (FD, folded FD, partial FD, banded LU).
+// (part of solver.cu, a single translation unit: included in order)
+#pragma once
+
+namespace hd {
+
+static thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+  hd_status code;
+  Error(hd_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess)                                                                        \
+      throw Error(HD_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + \
+                                   ":" + std::to_string(__LINE__));                               \
+  } while (0)
+#define CKB(x)                                                                                    \
+  do {                                                                                            \
+    cublasStatus_t e_ = (x);                                                                      \
+    if (e_ != CUBLAS_STATUS_SUCCESS) throw Error(HD_ERR_CUDA, std::string(#x) + " failed: " + std::to_string(e_)); \
+  } while (0)
+#define CKS(x)                                                                                    \
+  do {                                                                                            \
+    cusolverStatus_t e_ = (x);                                                                    \
+    if (e_ != CUSOLVER_STATUS_SUCCESS) throw Error(HD_ERR_CUDA, std::string(#x) + " failed: " + std::to_string(e_)); \
+  } while (0)
+
+template <class T>
+static T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+struct DevBand {
+  double* S = nullptr;
+  double* M = nullptr;
+  int n = 0, b = 0;
+  // layered field: the level as a G-term Kronecker sum (layered.cuh), with the
+  // unshifted (A) and shifted coefficients; band tables owned by `gen_mem`
+  GenLevel* genA = nullptr;
+  GenLevel* genM = nullptr;
+  double* gen_mem = nullptr;
+};
+
+// Exact solver of one Kronecker-sum (2D) or banded (1D) operator.
+struct ExactSolver {
+  int dim = 0, n = 0;
+  // 2D fast diagonalisation
+  double* V = nullptr;       // n x n column-major eigenvectors, V^T M V = I
+  double2* Dinv = nullptr;   // n x n, 1 / (lam_y + lam_x - c)
+  double* T1 = nullptr;      // planar work, 2 n^2
+  double* T2 = nullptr;
+  // 1D banded LU
+  int kl = 0, ku = 0;
+  double2* L = nullptr;
+  double2* U = nullptr;
+  int* piv = nullptr;
+  double2* work = nullptr;
+  double2* Uinv = nullptr;   // 1 / U(k, k)
+  // segmented sweeps (segsolve.cuh); seg.P == 0: single-lane staged kernel
+  SegArgs seg{};
+  // partial fast diagonalisation (ysolve.cuh): x modes by V, segmented banded LU sweeps along y
+  bool ypart = false;
+  int ykl = 0;
+  YArgs ya{};
+  // reflection-folded fast diagonalisation (centro-symmetric E, even n):
+  // Vt = [Vs_top | Va_top] (2 x n2 x n2), Dinvf in [y parity][x parity][ky][kx]
+  bool folded = false;
+  int n2 = 0;
+  double* Vt = nullptr;
+  double2* Dinvf = nullptr;
+  double *F = nullptr, *G = nullptr, *Hh = nullptr, *R = nullptr;
+  // dense inverse (layered field: E and the coarsest level are not Kronecker sums)
+  bool dense = false;
+  size_t NN = 0;
+  double2* Ainv = nullptr;   // NN x NN column-major
+  double2 *dx = nullptr, *dy = nullptr;
+  // block tridiagonal (btri.cuh): real non-Kronecker operators too large for a dense inverse
+  bool btri = false;
+  bool bt_cplx = false;  // complex operator (C_ex on a non-separable field)
+  BtriArgs bt{};
+  int bt_kr = 0;
+};
+
+}  // namespace hd
+
+using namespace hd;
+
+struct hd_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  cublasHandle_t cb = nullptr;
+  int dim = 1, p = 1, n = 0;
+  size_t N = 0;
+  double k = 0.0;
+  hd_precond spec{};
+  double2 corner = cmk(0.0, 0.0);
+  // operators
+  DevBand fine;                 // reduced S1, M1 (b = p)
+  double2 cA = cmk(0.0, 0.0);   // A = ... - k^2 M(x)M
+  double2 cM = cmk(0.0, 0.0);   // shifted: - k^2 (1 - i beta2) M(x)M
+  std::vector<DevBand> lev;     // multigrid levels (lev[0] = fine)
+  ExactSolver coarsest;
+  ExactSolver shift_exact;      // C_ex: exact inverse of the shifted operator (cycles == 0)
+  double* sx_plan = nullptr;    // planar scratch for the 2D exact shifted solve
+  std::vector<double2*> mg_b, mg_x, mg_y, mg_r;
+  // deflation
+  int nc = 0;
+  ExactSolver E;
+  double* ep = nullptr;         // planar coarse buffers (2 nc^dim)
+  double* ep2 = nullptr;
+  // vectors
+  double2 *f = nullptr, *rhsp = nullptr, *x0 = nullptr, *x = nullptr, *w = nullptr, *t1 = nullptr,
+          *t2 = nullptr, *t3 = nullptr;
+  double2* V = nullptr;
+  int v_cap = 0;
+  // GMRES scalars
+  int maxit_cap = 0;
+  double2 *H = nullptr, *g = nullptr, *cs = nullptr, *sn = nullptr, *y = nullptr;
+  double2* scal = nullptr;      // [0] hnew, [1] beta, [2] scratch dot
+  double* dres = nullptr;       // [0] rr, [1] hnew, [2] beta, [3] fnorm
+  double* hres = nullptr;       // pinned mirror
+  double2* partials = nullptr;
+  unsigned* counter = nullptr;
+  int red_blocks = 0;
+  // persistent Arnoldi tail (arnoldi.cuh)
+  bool use_arnoldi = false;
+  int arn_G = 0, arn_K = 0;
+  size_t arn_chunk = 0, arn_smem = 0;
+  int* dj = nullptr;
+  double2* arn_partials = nullptr;
+  int arn_maxit = -1;
+  unsigned* arn_bar = nullptr;
+  unsigned long long* arn_trace = nullptr;  // HD_TRACE: phase timestamps of the last launch
+  double arn_phase_ns[4] = {0, 0, 0, 0};
+  // Arnoldi engine: 2 = one-reduction ICWY-MGS streaming passes (default),
+  // 1 = persistent exact-order MGS chain, 0 = one kernel per MGS step.
+  int arn_mode = 2;
+  // one-reduction engine state (arnoldi_lowsync.cuh)
+  double* lsa_sig = nullptr;
+  double2 *lsa_L = nullptr, *lsa_ch = nullptr, *lsa_cx = nullptr, *lsa_partials = nullptr;
+  unsigned* lsa_counter = nullptr;
+  int lsa_G = 0, lsa_maxit = -1;
+  size_t lsa_givens_smem = 0;
+  // graph-resident GMRES loop (WHILE conditional node), rebuilt when (maxit, tol) change
+  cudaGraph_t loop_graph = nullptr;
+  cudaGraphExec_t loop_exec = nullptr;
+  int loop_maxit = -1;
+  double loop_tol = -1.0;
+  LoopState* loop_state = nullptr;
+  LoopState* loop_host = nullptr;   // pinned
+  double* res_hist = nullptr;       // device, maxit
+  double* res_host = nullptr;       // pinned
+  void* cublas_ws = nullptr;
+  bool graph_enabled = true;        // HD_GRAPH=0: host-driven loop
+  int graph_body_kernels = 0;       // own kernels per body execution
+  int n_sms = 148;
+  // counters
+  long matvecs = 0, coarse_solves = 0, shift_solves = 0, vcycles = 0;
+  int launches = 0;             // own kernels launched in the last solve
+  int lib_calls = 0;            // cuBLAS calls in the last solve
+  double t_setup = 0.0;
+  // per-launch event timing (hd_profile)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_ev;
+  size_t prof_used = 0;
+  struct ProfRec { int kind; size_t ev; double bytes; };
+  std::vector<ProfRec> prof_recs;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t own_st = nullptr;  // the context's own stream while an external one is set
+  cudaStream_t st2 = nullptr;     // side branch of the graph body (Givens of the previous iteration)
+  void* slabs = nullptr;          // row-slab state (hd_create_slabs), or null
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+};
+
+namespace hd {
+
+static DevBand upload_band(const Band& B) {
+  DevBand d;
+  d.n = B.n;
+  d.b = B.b;
+  d.S = dalloc<double>(B.a.size());
+  CK(cudaMemcpy(d.S, B.a.data(), B.a.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return d;
+}
+
+static DevBand upload_pair(const Band& S, const Band& M) {
+  const int b = std::max(S.b, M.b);
+  Band s2(S.n, b), m2(M.n, b);
+  for (int i = 0; i < S.n; ++i)
+    for (int d = -b; d <= b; ++d) {
+      const int j = i + d;
+      if (j < 0 || j >= S.n) continue;
+      s2.ref(i, j) = S.at(i, j);
+      m2.ref(i, j) = M.at(i, j);
+    }
+  DevBand d;
+  d.n = S.n;
+  d.b = b;
+  d.S = dalloc<double>(s2.a.size());
+  d.M = dalloc<double>(m2.a.size());
+  CK(cudaMemcpy(d.S, s2.a.data(), s2.a.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d.M, m2.a.data(), m2.a.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return d;
+}
+
+static Band band_from_host(const double* a, int n, int b) {
+  Band B(n, b);
+  std::memcpy(B.a.data(), a, B.a.size() * sizeof(double));
+  return B;
+}
+
+static LevelDev level_dev(const DevBand& d, double2 c, double2 corner, const GenLevel* gen = nullptr) {
+  LevelDev L;
+  L.gen = gen;
+  L.S = d.S;
+  L.M = d.M;
+  L.n = d.n;
+  L.b = d.b;
+  L.c = c;
+  L.corner = corner;
+  return L;
+}
+
+static std::vector<double> dense_of(const Band& B) {
+  std::vector<double> D(static_cast<size_t>(B.n) * B.n, 0.0);
+  for (int i = 0; i < B.n; ++i)
+    for (int j = std::max(0, i - B.b); j <= std::min(B.n - 1, i + B.b); ++j) D[i + static_cast<size_t>(j) * B.n] = B.at(i, j);
+  return D;
+}
+
+// Dense generalized symmetric-definite eigenproblem A v = lam B v (cuSOLVER
+// sygvd), eigenvectors returned column-major on the device, V^T B V = I.
+static void sygvd_device(cudaStream_t st, const std::vector<double>& A, const std::vector<double>& Bm, int n,
+                         double* dV, std::vector<double>& lam) {
+  double *dB = dalloc<double>(Bm.size()), *dW = dalloc<double>(n);
+  int* dinfo = dalloc<int>(1);
+  CK(cudaMemcpy(dV, A.data(), A.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, Bm.data(), Bm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  cusolverDnHandle_t h;
+  CKS(cusolverDnCreate(&h));
+  CKS(cusolverDnSetStream(h, st));
+  int lwork = 0;
+  CKS(cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dV, n,
+                                  dB, n, dW, &lwork));
+  double* dwork = dalloc<double>(std::max(lwork, 1));
+  CKS(cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dV, n, dB, n, dW,
+                       dwork, lwork, dinfo));
+  int info = 0;
+  CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cusolverDnDestroy(h);
+  if (info != 0) throw Error(HD_ERR_FACTOR, "coarse operator factorization failed (sygvd info " + std::to_string(info) + ")");
+  lam.resize(n);
+  CK(cudaMemcpy(lam.data(), dW, n * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(dB);
+  cudaFree(dW);
+  cudaFree(dinfo);
+  cudaFree(dwork);
+}
+
+// True when the banded matrix is centro-symmetric, X(i,j) = X(n-1-i, n-1-j),
+// to rounding (the reflected B-spline basis and an odd fine size make the
+// Bezier-coarsened E so).
+static bool centro_symmetric(const Band& X) {
+  double mx = 0.0, dev = 0.0;
+  for (int i = 0; i < X.n; ++i)
+    for (int d = -X.b; d <= X.b; ++d) {
+      const int j = i + d;
+      if (j < 0 || j >= X.n) continue;
+      mx = std::max(mx, std::abs(X.at(i, j)));
+      dev = std::max(dev, std::abs(X.at(i, j) - X.at(X.n - 1 - i, X.n - 1 - j)));
+    }
+  return dev <= 1e-13 * mx;
+}
+
+// Reflection-folded fast diagonalisation: for even n and centro-symmetric
+// S, M the eigenvectors are symmetric [a; Ja]/sqrt2 or antisymmetric
+// [a; -Ja]/sqrt2 with a from the half-size problems (X_tt +- X_tb J).  Every
+// transform then costs two half-size GEMMs instead of one full one.
+static ExactSolver make_fd_folded(cudaStream_t st, const Band& S, const Band& M, double2 c) {
+  ExactSolver X;
+  X.dim = 2;
+  X.folded = true;
+  X.n = S.n;
+  const int n = S.n, n2 = n / 2;
+  X.n2 = n2;
+  X.Vt = dalloc<double>(2 * static_cast<size_t>(n2) * n2);
+  std::vector<double> lam[2];
+  for (int par = 0; par < 2; ++par) {
+    const double sg = par == 0 ? 1.0 : -1.0;
+    std::vector<double> As(static_cast<size_t>(n2) * n2), Bs(As.size());
+    for (int i = 0; i < n2; ++i)
+      for (int j = 0; j < n2; ++j) {
+        // (X_tt +- X_tb J)(i, j) = X(i, j) +- X(i, n-1-j), column-major
+        As[i + static_cast<size_t>(j) * n2] = S.at(i, j) + sg * S.at(i, n - 1 - j);
+        Bs[i + static_cast<size_t>(j) * n2] = M.at(i, j) + sg * M.at(i, n - 1 - j);
+      }
+    double* dV = X.Vt + static_cast<size_t>(par) * n2 * n2;
+    sygvd_device(st, As, Bs, n2, dV, lam[par]);
+  }
+  // scale the half-vectors by 1/sqrt2 (full vectors [a; +-Ja]/sqrt2 are M-orthonormal)
+  {
+    std::vector<double> hv(2 * static_cast<size_t>(n2) * n2);
+    CK(cudaMemcpy(hv.data(), X.Vt, hv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (double& v : hv) v *= std::sqrt(0.5);
+    CK(cudaMemcpy(X.Vt, hv.data(), hv.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  std::vector<double2> D(4 * static_cast<size_t>(n2) * n2);
+  for (int yb = 0; yb < 2; ++yb)
+    for (int xb = 0; xb < 2; ++xb)
+      for (int ky = 0; ky < n2; ++ky)
+        for (int kx = 0; kx < n2; ++kx) {
+          const std::complex<double> d(lam[yb][ky] + lam[xb][kx] - c.x, -c.y);
+          if (d == std::complex<double>(0.0, 0.0))
+            throw Error(HD_ERR_FACTOR, "coarse operator factorization failed (singular)");
+          const std::complex<double> r = 1.0 / d;
+          D[((static_cast<size_t>(yb) * 2 + xb) * n2 + ky) * n2 + kx] = cmk(r.real(), r.imag());
+        }
+  X.Dinvf = dalloc<double2>(D.size());
+  CK(cudaMemcpy(X.Dinvf, D.data(), D.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  const size_t half = 2 * static_cast<size_t>(n2) * 2 * n;  // 2 parities x n2 x 2n
+  X.F = dalloc<double>(half);
+  X.G = dalloc<double>(half);
+  X.Hh = dalloc<double>(8 * static_cast<size_t>(n2) * n2);
+  X.R = dalloc<double>(8 * static_cast<size_t>(n2) * n2);
+  return X;
+}
+
+// Fast diagonalisation of W = M(x)S + S(x)M - c M(x)M: S V = M V diag(lam),
+// V^T M V = I (cuSOLVER sygvd at setup), Dinv = 1/(lam_i + lam_j - c).
+static ExactSolver make_fd(cudaStream_t st, const Band& S, const Band& M, double2 c) {
+  ExactSolver X;
+  X.dim = 2;
+  X.n = S.n;
+  const int n = S.n;
+  std::vector<double> As = dense_of(S), Bm = dense_of(M);
+  double *dA = dalloc<double>(As.size()), *dB = dalloc<double>(Bm.size()), *dW = dalloc<double>(n);
+  int* dinfo = dalloc<int>(1);
+  CK(cudaMemcpy(dA, As.data(), As.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, Bm.data(), Bm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  cusolverDnHandle_t h;
+  CKS(cusolverDnCreate(&h));
+  CKS(cusolverDnSetStream(h, st));
+  int lwork = 0;
+  CKS(cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dA, n,
+                                  dB, n, dW, &lwork));
+  double* dwork = dalloc<double>(std::max(lwork, 1));
+  CKS(cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dA, n, dB, n, dW,
+                       dwork, lwork, dinfo));
+  int info = 0;
+  CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cusolverDnDestroy(h);
+  if (info != 0) throw Error(HD_ERR_FACTOR, "coarse operator factorization failed (sygvd info " + std::to_string(info) + ")");
+  std::vector<double> lam(n);
+  CK(cudaMemcpy(lam.data(), dW, n * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<double2> Dinv(static_cast<size_t>(n) * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const std::complex<double> d(lam[i] + lam[j] - c.x, -c.y);
+      if (d == std::complex<double>(0.0, 0.0)) throw Error(HD_ERR_FACTOR, "coarse operator factorization failed (singular)");
+      const std::complex<double> r = 1.0 / d;
+      Dinv[static_cast<size_t>(i) * n + j] = cmk(r.real(), r.imag());
+    }
+  X.V = dA;
+  X.Dinv = dalloc<double2>(Dinv.size());
+  CK(cudaMemcpy(X.Dinv, Dinv.data(), Dinv.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  X.T1 = dalloc<double>(2 * static_cast<size_t>(n) * n);
+  X.T2 = dalloc<double>(2 * static_cast<size_t>(n) * n);
+  cudaFree(dB);
+  cudaFree(dW);
+  cudaFree(dinfo);
+  cudaFree(dwork);
+  return X;
+}
+
+// Partial fast diagonalisation of a real-shift Kronecker sum (E): V from the
+// x eigenproblem (as make_fd); for every x mode the real banded y operator
+// T_m = S - (c - lam_m) M, LU-factored with partial pivoting (band_lu), and the
+// influence rows / boundary maps of its kYL-row segments (ysolve.cuh).
+static ExactSolver make_fd_ypart(cudaStream_t st, const Band& S, const Band& M, double2 c) {
+  const int n = S.n, kl = std::max(S.b, M.b), ku = 2 * kl, W = kl + 1;
+  ExactSolver X;
+  X.dim = 2;
+  X.n = n;
+  X.ypart = true;
+  X.ykl = kl;
+  X.V = dalloc<double>(static_cast<size_t>(n) * n);
+  std::vector<double> lam;
+  sygvd_device(st, dense_of(S), dense_of(M), n, X.V, lam);
+  const int np = (n + 31) / 32 * 32, Sg = (n + kYL - 1) / kYL, nr = Sg * kYL;
+  const int NF = 2 * kl + 2, NB = 2 * ku + 1;
+  std::vector<double> TF(static_cast<size_t>(nr) * NF * np, 0.0), TB(static_cast<size_t>(nr) * NB * np, 0.0),
+      FM(static_cast<size_t>(Sg) * W * W * np, 0.0), HM(static_cast<size_t>(Sg) * ku * ku * np, 0.0);
+  std::vector<double> Lk, Uk;
+  std::vector<int> pk;
+  for (int m = 0; m < np; ++m) {
+    // factors of mode m, padded rows / modes = identity
+    Lk.assign(static_cast<size_t>(nr) * kl, 0.0);
+    Uk.assign(static_cast<size_t>(nr) * (ku + 1), 0.0);
+    pk.assign(nr, 0);
+    for (int k = 0; k < nr; ++k) Uk[static_cast<size_t>(k) * (ku + 1)] = 1.0;
+    if (m < n) {
+      const BandLU f = band_lu(S, M, cplx(c.x - lam[m], 0.0));
+      if (f.kl != kl || f.ku != ku) throw Error(HD_ERR_INVALID, "unexpected band LU shape");
+      for (int k = 0; k < n; ++k) {
+        for (int q = 0; q < kl; ++q) Lk[static_cast<size_t>(k) * kl + q] = f.L[static_cast<size_t>(k) * kl + q].real();
+        for (int d = 0; d <= ku; ++d) Uk[static_cast<size_t>(k) * (ku + 1) + d] = f.U[static_cast<size_t>(k) * (ku + 1) + d].real();
+        pk[k] = f.piv[k] - k;
+        if (Uk[static_cast<size_t>(k) * (ku + 1)] == 0.0) throw Error(HD_ERR_FACTOR, "deflation matrix E is singular");
+      }
+    }
+    for (int k = 0; k < nr; ++k) {
+      double* tf = &TF[static_cast<size_t>(k) * NF * np + m];
+      for (int q = 0; q < kl; ++q) tf[static_cast<size_t>(q) * np] = Lk[static_cast<size_t>(k) * kl + q];
+      tf[static_cast<size_t>(kl) * np] = pk[k];
+      double* tb = &TB[static_cast<size_t>(k) * NB * np + m];
+      tb[0] = 1.0 / Uk[static_cast<size_t>(k) * (ku + 1)];
+      for (int d = 1; d <= ku; ++d) tb[static_cast<size_t>(d) * np] = Uk[static_cast<size_t>(k) * (ku + 1) + d];
+    }
+    for (int i = 0; i < Sg; ++i) {
+      const int s0 = i * kYL, e0 = s0 + kYL;
+      for (int q = 0; q < W; ++q) {  // forward from window e_q, no rhs
+        std::vector<double> w(W, 0.0);
+        w[q] = 1.0;
+        for (int k = s0; k < e0; ++k) {
+          const int p = pk[k];
+          if (p != 0) std::swap(w[0], w[p]);
+          const double yk = w[0];
+          TF[(static_cast<size_t>(k) * NF + kl + 1 + q) * np + m] = yk;
+          for (int r = 1; r <= kl; ++r) w[r] -= Lk[static_cast<size_t>(k) * kl + r - 1] * yk;
+          for (int r = 0; r < kl; ++r) w[r] = w[r + 1];
+          w[kl] = 0.0;
+        }
+        for (int r = 0; r < W; ++r) FM[((static_cast<size_t>(i) * W + r) * W + q) * np + m] = w[r];
+      }
+      for (int r = 0; r < ku; ++r) {  // backward from future x_{e+r} = 1, no rhs
+        std::vector<double> xw(ku, 0.0);
+        xw[r] = 1.0;
+        for (int k = e0 - 1; k >= s0; --k) {
+          double acc = 0.0;
+          for (int d = ku; d >= 1; --d) acc -= Uk[static_cast<size_t>(k) * (ku + 1) + d] * xw[d - 1];
+          const double xk = acc / Uk[static_cast<size_t>(k) * (ku + 1)];
+          for (int d = ku - 1; d >= 1; --d) xw[d] = xw[d - 1];
+          xw[0] = xk;
+          TB[(static_cast<size_t>(k) * NB + ku + 1 + r) * np + m] = xk;
+          if (k - s0 < ku) HM[((static_cast<size_t>(i) * ku + (k - s0)) * ku + r) * np + m] = xk;
+        }
+      }
+    }
+  }
+  auto up = [](const std::vector<double>& v) {
+    double* d = dalloc<double>(v.size());
+    CK(cudaMemcpy(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return d;
+  };
+  YArgs& a = X.ya;
+  a.n = n;
+  a.np = np;
+  a.S = Sg;
+  a.nr = nr;
+  a.TF = up(TF);
+  a.TB = up(TB);
+  a.FM = up(FM);
+  a.HM = up(HM);
+  a.Y = dalloc<double>(2 * static_cast<size_t>(nr) * np);
+  a.X0 = dalloc<double>(2 * static_cast<size_t>(nr) * np);
+  a.D = dalloc<double>(2 * static_cast<size_t>(Sg) * W * np);
+  a.Dl = dalloc<double>(2 * static_cast<size_t>(Sg) * W * np);
+  a.XS = dalloc<double>(2 * static_cast<size_t>(Sg) * ku * np);
+  a.XB = dalloc<double>(2 * static_cast<size_t>(Sg + 1) * ku * np);
+  X.T1 = dalloc<double>(2 * static_cast<size_t>(n) * np);
+  CK(cudaMemset(X.T1, 0, 2 * static_cast<size_t>(n) * np * sizeof(double)));
+  a.C = X.T1;
+  return X;
+}
+
+// Influence rows and window transfers of the segmented sweeps (segsolve.cuh),
+// by running each segment's recurrences on unit boundary values; all per-row
+// tables in the [row-in-segment][field][segment] layout, rows past n = identity.
+static void make_segments(ExactSolver& X, const BandLU& f) {
+  const int n = f.n, kl = f.kl, ku = f.ku, W = kl + 1, Ls = kSegL;
+  const int P = (n + Ls - 1) / Ls;
+  if (P < 4 || ku != 2 * kl) return;
+  const int NP = P * Ls;
+  // padded row access
+  auto Lm = [&](int k, int q) { return k < n ? f.L[static_cast<size_t>(k) * kl + q] : cplx(0.0, 0.0); };
+  auto Uu = [&](int k, int d) { return k < n ? f.U[static_cast<size_t>(k) * (ku + 1) + d] : (d == 0 ? cplx(1.0, 0.0) : cplx(0.0, 0.0)); };
+  auto pv = [&](int k) { return k < n ? f.piv[k] - k : 0; };
+  auto at = [&](int k, int fld, int nf) { return (static_cast<size_t>(k % Ls) * nf + fld) * P + k / Ls; };
+  std::vector<cplx> Lt(static_cast<size_t>(NP) * kl), hf(static_cast<size_t>(NP) * W), Ut(static_cast<size_t>(NP) * ku),
+      Ui(NP), hb(static_cast<size_t>(NP) * ku), Ff(static_cast<size_t>(P) * W * W), Hb(static_cast<size_t>(P) * ku * ku);
+  std::vector<int> pt(NP);
+  for (int k = 0; k < NP; ++k) {
+    for (int q = 0; q < kl; ++q) Lt[at(k, q, kl)] = Lm(k, q);
+    pt[at(k, 0, 1)] = pv(k);
+    for (int d = 1; d <= ku; ++d) Ut[at(k, d - 1, ku)] = Uu(k, d);
+    Ui[at(k, 0, 1)] = 1.0 / Uu(k, 0);
+  }
+  for (int i = 0; i < P; ++i) {
+    const int s = i * Ls, e = s + Ls;
+    for (int q = 0; q < W; ++q) {  // forward from window e_q, no rhs
+      std::vector<cplx> w(W, cplx(0.0, 0.0));
+      w[q] = 1.0;
+      for (int k = s; k < e; ++k) {
+        const int p = pv(k);
+        if (p != 0) std::swap(w[0], w[p]);
+        const cplx yk = w[0];
+        hf[at(k, q, W)] = yk;
+        for (int r = 1; r <= kl; ++r) w[r] -= Lm(k, r - 1) * yk;
+        for (int r = 0; r < kl; ++r) w[r] = w[r + 1];
+        w[kl] = 0.0;
+      }
+      for (int r = 0; r < W; ++r) Ff[(static_cast<size_t>(i) * W + r) * W + q] = w[r];
+    }
+    for (int r = 0; r < ku; ++r) {  // backward from future x_{e+r} = 1, no rhs
+      std::vector<cplx> xw(ku, cplx(0.0, 0.0));  // x_{k+1} .. x_{k+ku}
+      xw[r] = 1.0;
+      for (int k = e - 1; k >= s; --k) {
+        cplx acc(0.0, 0.0);
+        for (int d = ku; d >= 1; --d) acc -= Uu(k, d) * xw[d - 1];
+        const cplx xk = acc / Uu(k, 0);
+        for (int d = ku - 1; d >= 1; --d) xw[d] = xw[d - 1];
+        xw[0] = xk;
+        hb[at(k, r, ku)] = xk;
+        if (k - s < ku) Hb[(static_cast<size_t>(i) * ku + (k - s)) * ku + r] = xk;
+      }
+    }
+  }
+  auto up = [](const auto& v) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    T* d = dalloc<T>(v.size());
+    CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  };
+  SegArgs& a = X.seg;
+  a.n = n;
+  a.P = P;
+  a.L = reinterpret_cast<const double2*>(up(Lt));
+  a.pv = up(pt);
+  a.hf = reinterpret_cast<const double2*>(up(hf));
+  a.U = reinterpret_cast<const double2*>(up(Ut));
+  a.Ui = reinterpret_cast<const double2*>(up(Ui));
+  a.hb = reinterpret_cast<const double2*>(up(hb));
+  a.Ff = reinterpret_cast<const double2*>(up(Ff));
+  a.Hb = reinterpret_cast<const double2*>(up(Hb));
+  a.y = dalloc<double2>(NP);
+  a.x0 = dalloc<double2>(NP);
+  a.D = dalloc<double2>(static_cast<size_t>(P) * W);
+  a.Dl = dalloc<double2>(static_cast<size_t>(P) * W);
+  a.X0 = dalloc<double2>(static_cast<size_t>(P) * ku);
+  a.Xb = dalloc<double2>(static_cast<size_t>(P + 1) * ku);
+}
+
+static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 corner) {
+  BandLU f = band_lu(S, M, cplx(c.x, c.y), cplx(corner.x, corner.y));
+  ExactSolver X;
+  X.dim = 1;
+  X.n = f.n;
+  X.kl = f.kl;
+  X.ku = f.ku;
+  X.L = dalloc<double2>(f.L.size());
+  X.U = dalloc<double2>(f.U.size());
+  X.piv = dalloc<int>(f.piv.size());
+  X.work = dalloc<double2>(f.n);
+  std::vector<cplx> uinv(f.n);
+  for (int k = 0; k < f.n; ++k) uinv[k] = 1.0 / f.U[static_cast<size_t>(k) * (f.ku + 1)];
+  X.Uinv = dalloc<double2>(f.n);
+  CK(cudaMemcpy(X.Uinv, uinv.data(), uinv.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(X.L, f.L.data(), f.L.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(X.U, f.U.data(), f.U.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(X.piv, f.piv.data(), f.piv.size() * sizeof(int), cudaMemcpyHostToDevice));
+  const char* e = std::getenv("HD_SEG");
+  if (!(e && std::atoi(e) == 0) && f.kl >= 1 && f.kl <= 6) make_segments(X, f);
+  return X;
+}
+
+static void free_exact(ExactSolver& X) {
+  cudaFree(X.V); cudaFree(X.Dinv); cudaFree(X.T1); cudaFree(X.T2);
+  cudaFree(X.Vt); cudaFree(X.Dinvf); cudaFree(X.F); cudaFree(X.G); cudaFree(X.Hh); cudaFree(X.R);
+  cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work); cudaFree(X.Uinv);
+  if (X.ypart) {
+    cudaFree(const_cast<double*>(X.ya.TF)); cudaFree(const_cast<double*>(X.ya.TB));
+    cudaFree(const_cast<double*>(X.ya.FM)); cudaFree(const_cast<double*>(X.ya.HM));
+    cudaFree(X.ya.Y); cudaFree(X.ya.X0); cudaFree(X.ya.D); cudaFree(X.ya.Dl); cudaFree(X.ya.XS); cudaFree(X.ya.XB);
+  }
+  if (X.seg.P) {
+    for (const void* p : {static_cast<const void*>(X.seg.L), static_cast<const void*>(X.seg.pv),
+                          static_cast<const void*>(X.seg.hf), static_cast<const void*>(X.seg.U),
+                          static_cast<const void*>(X.seg.Ui), static_cast<const void*>(X.seg.hb),
+                          static_cast<const void*>(X.seg.Ff), static_cast<const void*>(X.seg.Hb)})
+      cudaFree(const_cast<void*>(p));
+    cudaFree(X.seg.y); cudaFree(X.seg.x0); cudaFree(X.seg.D);
+    cudaFree(X.seg.Dl); cudaFree(X.seg.X0); cudaFree(X.seg.Xb);
+  }
+  cudaFree(X.Ainv); cudaFree(X.dx); cudaFree(X.dy);
+  if (X.btri) {
+    cudaFree(const_cast<void*>(X.bt.GT)); cudaFree(const_cast<void*>(X.bt.SinvT));
+    cudaFree(const_cast<void*>(X.bt.HT)); cudaFree(const_cast<void*>(X.bt.G2)); cudaFree(X.bt.y); cudaFree(X.bt.bar);
+  }
+  X = ExactSolver{};
+}
+
+template <int KL>
+static void bandlu_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b, const double* bp, double2* x,
+                            double* xp) {
+  static bool attr = false;
+  constexpr size_t sm = bandlu_smem<KL>();
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_bandlu_staged<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    attr = true;
+  }
+  k_bandlu_staged<KL><<<1, 256, sm, st>>>(X.L, X.U, X.Uinv, X.piv, X.n, b, bp, X.work, x, xp);
+}
+
+template <int KL>
+static void seg_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b, const double* bp, double2* x,
+                         double* xp) {
+  const SegArgs& a = X.seg;
+  const int blocks = (a.P + 31) / 32;
+  k_seg_fwd<KL><<<blocks, 32, 0, st>>>(a, b, bp);
+  k_seg_scan_fwd<KL><<<1, 32, 0, st>>>(a);
+  k_seg_bwd<KL><<<blocks, 32, 0, st>>>(a);
+  k_seg_scan_bwd<KL><<<1, 32, 0, st>>>(a);
+  k_seg_out<KL><<<std::min((a.n + 255) / 256, 148 * 4), 256, 0, st>>>(a, x, xp);
+}
+
+// 1D exact solve (kl = 1..6), in/out interleaved or planar: segmented sweeps,
+// or the single-lane staged kernel for short systems
+static void bandlu_launch(cudaStream_t st, const ExactSolver& X, const double2* b, const double* bp, double2* x,
+                          double* xp) {
+  if (X.ku != 2 * X.kl) throw Error(HD_ERR_INVALID, "banded LU layout mismatch");
+  if (X.seg.P) {
+    switch (X.kl) {
+      case 1: seg_launch_t<1>(st, X, b, bp, x, xp); break;
+      case 2: seg_launch_t<2>(st, X, b, bp, x, xp); break;
+      case 3: seg_launch_t<3>(st, X, b, bp, x, xp); break;
+      case 4: seg_launch_t<4>(st, X, b, bp, x, xp); break;
+      case 5: seg_launch_t<5>(st, X, b, bp, x, xp); break;
+      default: seg_launch_t<6>(st, X, b, bp, x, xp); break;
+    }
+    return;
+  }
+  switch (X.kl) {
+    case 1: bandlu_launch_t<1>(st, X, b, bp, x, xp); break;
+    case 2: bandlu_launch_t<2>(st, X, b, bp, x, xp); break;
+    case 3: bandlu_launch_t<3>(st, X, b, bp, x, xp); break;
+    case 4: bandlu_launch_t<4>(st, X, b, bp, x, xp); break;
+    case 5: bandlu_launch_t<5>(st, X, b, bp, x, xp); break;
+    case 6: bandlu_launch_t<6>(st, X, b, bp, x, xp); break;
+    default: throw Error(HD_ERR_INVALID, "banded LU bandwidth " + std::to_string(X.kl) + " unsupported");
+  }
+}
+
+
+}  // namespace hd

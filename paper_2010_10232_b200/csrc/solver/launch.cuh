@@ -1,0 +1,1050 @@
+// Launch helpers, per-launch profiling, level operators, transfers, exact solves, the V-cycle, deflation, the composed operator, the Arnoldi engines and the single-domain GMRES loop (host-driven and graph-resident).
+// (part of solver.cu, a single translation unit: included in order)
+#pragma once
+
+namespace hd {
+
+// ---------------------------------------------------------------------------
+// launch helpers + per-launch profiling (CUDA events on the launch stream)
+// ---------------------------------------------------------------------------
+static size_t prof_mark(hd_ctx* c) {
+  if (!c->prof_on) return static_cast<size_t>(-1);
+  if (c->prof_used >= c->prof_ev.size()) {
+    const size_t grow = std::max<size_t>(1024, c->prof_ev.size());
+    for (size_t i = 0; i < grow; ++i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->prof_ev.push_back(e);
+    }
+  }
+  CK(cudaEventRecord(c->prof_ev[c->prof_used], c->st));
+  return c->prof_used++;
+}
+
+// called right after a launch: error check, launch count, profile record
+static void launched(hd_ctx* c, int kind, size_t mark, double bytes, bool library = false) {
+  CK(cudaGetLastError());
+  if (library) ++c->lib_calls;
+  else ++c->launches;
+  if (mark == static_cast<size_t>(-1)) return;
+  prof_mark(c);
+  c->prof_recs.push_back({kind, mark, bytes});
+}
+
+#define HD_LAUNCH(kind, bytes, ...)        \
+  do {                                     \
+    const size_t mk_ = prof_mark(c);       \
+    __VA_ARGS__;                           \
+    launched(c, (kind), mk_, (bytes));     \
+  } while (0)
+static int grid_for(size_t N, int threads = 256, int cap = 148 * 8) {
+  const size_t g = (N + threads - 1) / threads;
+  return static_cast<int>(std::max<size_t>(1, std::min<size_t>(g, cap)));
+}
+
+// algorithmic bytes of one operator launch: x read + output (+ b read)
+static double op_bytes(int mode, size_t NL) {
+  const double P = 16.0 * static_cast<double>(NL);
+  switch (mode) {
+    case OP_APPLY: return 2 * P;
+    case OP_RESNORM: return 2 * P;
+    default: return 3 * P;
+  }
+}
+
+// Per instantiation: opt in to the dynamic shared memory of the tallest strip
+// and query how many CTAs are resident per SM.
+template <int B, int MODE>
+static int stencil_occupancy() {
+  static int per = 0;
+  if (!per) {
+    constexpr size_t sm = stencil_smem<B, MODE>(kSRowsMax);
+    CK(cudaFuncSetAttribute(k_stencil2d<B, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stencil2d<B, MODE>, kSW * kSWarps, sm));
+    per = std::max(per, 1);
+  }
+  return per;
+}
+
+// Strip height: fill whole waves of resident CTAs, discounted by the 2B halo
+// rows each strip re-reads.
+static int pick_rows(int n, int rows, int slots, int B) {
+  const int colblocks = (n + kSW * kSWarps - 1) / (kSW * kSWarps);
+  static const int cand[] = {8, 12, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 112, 128};
+  int best = 32;
+  double best_score = -1.0;
+  for (int ry : cand) {
+    if (ry > kSRowsMax) break;
+    const long tiles = static_cast<long>(colblocks) * ((rows + ry - 1) / ry);
+    const long waves = (tiles + slots - 1) / slots;
+    const double util = static_cast<double>(tiles) / (static_cast<double>(waves) * slots);
+    const double score = util * ry / (ry + 2.0 * B);
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = ry;
+    }
+  }
+  return best;
+}
+
+template <int B, int MODE>
+static void launch_stencil(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
+                           double omega, RedOut red, const int* xidx, size_t xstride, int rb, int re) {
+  const int per = stencil_occupancy<B, MODE>();
+  const int ry = pick_rows(L.n, re - rb, per * c->n_sms, B);
+  dim3 grid((L.n + kSW * kSWarps - 1) / (kSW * kSWarps), (re - rb + ry - 1) / ry);
+  k_stencil2d<B, MODE><<<grid, kSW * kSWarps, stencil_smem<B, MODE>(ry), c->st>>>(L, x, b, out, omega, ry, red,
+                                                                               xidx, xstride, rb, re);
+}
+
+template <int MODE>
+static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
+                             double omega, RedOut red, int kind, const int* xidx, size_t xstride, int rb = 0,
+                             int re = -1) {
+  if (re < 0) re = L.n;
+  const size_t mk = prof_mark(c);
+  switch (L.b) {
+#define HD_CASE(BB) \
+  case BB: launch_stencil<BB, MODE>(c, L, x, b, out, omega, red, xidx, xstride, rb, re); break;
+    HD_CASE(1) HD_CASE(2) HD_CASE(3) HD_CASE(4) HD_CASE(5) HD_CASE(6)
+#undef HD_CASE
+    default: throw Error(HD_ERR_INVALID, "band half-width " + std::to_string(L.b) + " unsupported");
+  }
+  launched(c, kind, mk, op_bytes(MODE, static_cast<size_t>(L.n) * (re - rb)));
+}
+
+// layered field: G-term Kronecker-sum operator (layered.cuh)
+template <int MODE>
+static void launch_gen_mode(hd_ctx* c, const GenLevel& G, const double2* x, const double2* b, double2* out,
+                            double omega, RedOut red, int kind, const int* xidx, size_t xstride) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_kron2d<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(gen_smem(6, kGenMaxG))));
+    attr = true;
+  }
+  if (G.b > 6 || G.G > kGenMaxG) throw Error(HD_ERR_INVALID, "layered operator exceeds the kernel limits");
+  const dim3 grid((G.n + kGenTX - 1) / kGenTX, (G.n + kGenTY - 1) / kGenTY);
+  HD_LAUNCH(kind, op_bytes(MODE, static_cast<size_t>(G.n) * G.n),
+            k_kron2d<MODE><<<grid, kGenThreads, gen_smem(G.b, G.G), c->st>>>(G, x, b, out, omega, red, xidx,
+                                                                               xstride));
+}
+
+static RedOut red_of(hd_ctx* c, double* dst = nullptr, double scale = 1.0) {
+  RedOut r;
+  r.raw = 0;
+  r.partials = c->partials;
+  r.counter = c->counter;
+  r.dst = dst;
+  r.scale = scale;
+  return r;
+}
+
+// out = L x | b - L x | x + w D^-1 (b - L x) | ||b - L x|| * scale -> dst
+static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, const double2* b, double2* out,
+                     double omega = 0.0, double* dst = nullptr, double scale = 1.0, const int* xidx = nullptr,
+                     size_t xstride = 0, int rb = 0, int re = -1, int raw = 0) {
+  RedOut red = red_of(c, dst, scale);
+  red.raw = raw;
+  const int kind = L.n == c->n ? HD_K_OP_FINE : HD_K_OP_COARSE;
+  if (L.gen) {
+    const GenLevel& G = *static_cast<const GenLevel*>(L.gen);
+    switch (mode) {
+      case OP_APPLY: launch_gen_mode<OP_APPLY>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
+      case OP_RESID: launch_gen_mode<OP_RESID>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
+      case OP_JACOBI: launch_gen_mode<OP_JACOBI>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
+      default: launch_gen_mode<OP_RESNORM>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
+    }
+    return;
+  }
+  if (c->dim == 2) {
+    switch (mode) {
+      case OP_APPLY: launch_op2d_mode<OP_APPLY>(c, L, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+      case OP_RESID: launch_op2d_mode<OP_RESID>(c, L, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+      case OP_JACOBI: launch_op2d_mode<OP_JACOBI>(c, L, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+      default: launch_op2d_mode<OP_RESNORM>(c, L, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+    }
+  } else {
+    const int grid = mode == OP_RESNORM ? std::min(grid_for(L.n), c->red_blocks) : grid_for(L.n);
+    const size_t mk = prof_mark(c);
+    switch (mode) {
+      case OP_APPLY: k_op1d<OP_APPLY><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red, xidx, xstride); break;
+      case OP_RESID: k_op1d<OP_RESID><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red, xidx, xstride); break;
+      case OP_JACOBI: k_op1d<OP_JACOBI><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red, xidx, xstride); break;
+      default: k_op1d<OP_RESNORM><<<grid, 256, 0, c->st>>>(L, x, b, out, omega, red, xidx, xstride); break;
+    }
+    launched(c, kind, mk, op_bytes(mode, L.n));
+  }
+}
+
+static void jacobi0(hd_ctx* c, const LevelDev& L, const double2* b, double2* out, double omega, int rb = 0,
+                    int re = -1) {
+  if (re < 0) re = L.n;
+  const size_t NN = c->dim == 2 ? static_cast<size_t>(L.n) * L.n : L.n;
+  if (L.gen) {
+    HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,
+              k_jacobi0_gen<<<grid_for(NN), 256, 0, c->st>>>(*static_cast<const GenLevel*>(L.gen), b, out, omega));
+    return;
+  }
+  HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,
+            if (c->dim == 2) k_jacobi0_2d_t<<<dim3((L.n + 63) / 64, (re - rb + 15) / 16), 256, 0, c->st>>>(
+                L, b, out, omega, rb, re);
+            else k_jacobi0_1d<<<grid_for(NN), 256, 0, c->st>>>(L, b, out, omega));
+}
+
+static void restrict_(hd_ctx* c, Stencil z, const double2* r, int nf, int nc, double2* outc, double* outp,
+                      int qb = 0, int qe = -1) {
+  if (qe < 0) qe = nc;
+  const size_t NC = c->dim == 2 ? static_cast<size_t>(nc) * nc : nc;
+  const double NF = c->dim == 2 ? static_cast<double>(nf) * nf : nf;
+  if (c->dim == 2) {
+    dim3 grid((nc + kRQX - 1) / kRQX, (qe - qb + kRQY - 1) / kRQY);
+    HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NF + NC),
+              if (z.kind == 0 && !outp) k_restrict2d<0, 0><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp, qb, qe);
+              else if (z.kind == 0) k_restrict2d<0, 1><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp, qb, qe);
+              else if (!outp) k_restrict2d<1, 0><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp, qb, qe);
+              else k_restrict2d<1, 1><<<grid, 256, 0, c->st>>>(z.drop, r, nf, nc, outc, outp, qb, qe));
+    return;
+  }
+  HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NF + NC),
+            k_restrict<1><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp));
+}
+
+template <int PMODE>
+static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, int nf, int nc, const double2* s,
+                     double2* out, int fb = 0, int fe = -1) {
+  if (fe < 0) fe = nf;
+  const size_t NF = c->dim == 2 ? static_cast<size_t>(nf) * nf : nf;
+  const double NC = c->dim == 2 ? static_cast<double>(nc) * nc : nc;
+  if (c->dim == 2) {
+    dim3 grid((nf + kPFX - 1) / kPFX, (fe - fb + kPFY - 1) / kPFY);
+    HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NC + (PMODE == 2 ? 1.0 : 2.0) * NF),
+              if (z.kind == 0) k_prolong2d<0, PMODE><<<grid, 256, 0, c->st>>>(z.drop, ec, ep, nf, nc, s, out, fb, fe);
+              else k_prolong2d<1, PMODE><<<grid, 256, 0, c->st>>>(z.drop, ec, ep, nf, nc, s, out, fb, fe));
+    return;
+  }
+  HD_LAUNCH(HD_K_TRANSFER, 16.0 * (NC + (PMODE == 2 ? 1.0 : 2.0) * NF),
+            k_prolong<1, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out));
+}
+
+// interleaved <-> planar (re plane, im plane) complex vectors
+__global__ void k_to_planar(const double2* __restrict__ a, double* __restrict__ p, size_t N) {
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = a[g];
+    p[g] = v.x;
+    p[g + N] = v.y;
+  }
+}
+__global__ void k_from_planar(const double* __restrict__ p, double2* __restrict__ a, size_t N) {
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
+    a[g] = cmk(p[g], p[g + N]);
+}
+
+// y = Ainv x (dense exact solve of the layered field), interleaved
+static void dense_apply(hd_ctx* c, const ExactSolver& X, const double2* x, double2* y) {
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  const size_t mk = prof_mark(c);
+  CKB(cublasZgemv(c->cb, CUBLAS_OP_N, static_cast<int>(X.NN), static_cast<int>(X.NN), &one,
+                  reinterpret_cast<const cuDoubleComplex*>(X.Ainv), static_cast<int>(X.NN),
+                  reinterpret_cast<const cuDoubleComplex*>(x), 1, &zero, reinterpret_cast<cuDoubleComplex*>(y), 1));
+  launched(c, HD_K_LIBGEMM, mk, 16.0 * X.NN * X.NN, true);
+}
+
+// Block tridiagonal exact solve (btri.cuh), in/out planar.
+template <class T, int KR>
+static void btri_launch_t(hd_ctx* c, ExactSolver& X) {
+  const size_t smem = 4 * static_cast<size_t>(X.bt.m) * sizeof(double);  // two staged vectors
+  static size_t attr = 0;
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_btri_solve<T, KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.dynamicSmemBytes = smem;
+  cfg.gridDim = dim3(c->n_sms);
+  cfg.blockDim = dim3(btri_threads(KR * static_cast<int>(sizeof(T) / 8)));
+  cfg.stream = c->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_btri_solve<T, KR>, X.bt));
+}
+
+static void btri_solve(hd_ctx* c, ExactSolver& X, double* inout) {
+  X.bt.io = inout;
+  CK(cudaMemsetAsync(X.bt.bar, 0, sizeof(unsigned), c->st));
+  const double mm = static_cast<double>(X.bt.m) * X.bt.m * (X.bt_cplx ? 2.0 : 1.0);
+  HD_LAUNCH(HD_K_EXACT, 8.0 * mm * (3.0 * X.bt.nb - 1.0) + 32.0 * X.bt.NN,
+            if (X.bt_cplx) switch (X.bt_kr) {
+              case 8: btri_launch_t<double2, 8>(c, X); break;
+              case 16: btri_launch_t<double2, 16>(c, X); break;
+              case 24: btri_launch_t<double2, 24>(c, X); break;
+              case 32: btri_launch_t<double2, 32>(c, X); break;
+              default: btri_launch_t<double2, 48>(c, X); break;
+            } else switch (X.bt_kr) {
+              case 8: btri_launch_t<double, 8>(c, X); break;
+              case 16: btri_launch_t<double, 16>(c, X); break;
+              case 24: btri_launch_t<double, 24>(c, X); break;
+              case 32: btri_launch_t<double, 32>(c, X); break;
+              case 48: btri_launch_t<double, 48>(c, X); break;
+              case 64: btri_launch_t<double, 64>(c, X); break;
+              default: btri_launch_t<double, 96>(c, X); break;
+            });
+}
+
+// Exact solve: in/out planar (2D FD) or via the banded LU (1D).
+template <int KL>
+static void ysolve_launch_t(hd_ctx* c, const YArgs& a) {
+  const dim3 gs(a.np / 32, a.S), gm((a.np + 127) / 128), go(a.np / 32, a.n);
+  k_ys_fwd<KL><<<gs, 32, 0, c->st>>>(a);
+  k_ys_scan_fwd<KL><<<gm, 128, 0, c->st>>>(a);
+  k_ys_bwd<KL><<<gs, 32, 0, c->st>>>(a);
+  k_ys_scan_bwd<KL><<<gm, 128, 0, c->st>>>(a);
+  k_ys_out<KL><<<go, 32, 0, c->st>>>(a);
+}
+
+static void ysolve_launch(hd_ctx* c, const ExactSolver& X) {
+  switch (X.ykl) {
+    case 1: ysolve_launch_t<1>(c, X.ya); break;
+    case 2: ysolve_launch_t<2>(c, X.ya); break;
+    case 3: ysolve_launch_t<3>(c, X.ya); break;
+    case 4: ysolve_launch_t<4>(c, X.ya); break;
+    case 5: ysolve_launch_t<5>(c, X.ya); break;
+    case 6: ysolve_launch_t<6>(c, X.ya); break;
+    default: throw Error(HD_ERR_INVALID, "E band outside the y-solve kernels");
+  }
+}
+
+static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
+  if (X.ypart) {
+    const int n = X.n, np = X.ya.np;
+    const long nn = static_cast<long>(n) * n;
+    const double one = 1.0, zero = 0.0;
+    const double gb = 16.0 * nn * 2 + 8.0 * nn;
+    size_t mk = prof_mark(c);
+    // C = V^T [Xre | Xim]  (x modes), leading dimension np
+    CKB(cublasDgemm(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, inout, n, &zero, X.T1, np));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    // segmented banded sweeps along y for every mode (5 kernels)
+    HD_LAUNCH(HD_K_EXACT, 8.0 * X.ya.nr * np * (2 * X.ykl + 2 + 4 * X.ykl + 1) + 64.0 * nn, ysolve_launch(c, X));
+    c->launches += 4;
+    mk = prof_mark(c);
+    // out = V [Yre | Yim]
+    CKB(cublasDgemm(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, X.T1, np, &zero, inout, n));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    return;
+  }
+  if (X.btri) {
+    btri_solve(c, X, inout);
+    return;
+  }
+  if (X.dense) {
+    HD_LAUNCH(HD_K_VEC, 32.0 * X.NN, k_from_planar<<<grid_for(X.NN), 256, 0, c->st>>>(inout, X.dx, X.NN));
+    dense_apply(c, X, X.dx, X.dy);
+    HD_LAUNCH(HD_K_VEC, 32.0 * X.NN, k_to_planar<<<grid_for(X.NN), 256, 0, c->st>>>(X.dy, inout, X.NN));
+    return;
+  }
+  if (X.dim == 2 && X.folded) {
+    const int n = X.n, n2 = X.n2;
+    const long nn = static_cast<long>(n2) * n2;
+    const long hc = static_cast<long>(n2) * 2 * n;  // one parity of a half-folded n2 x 2n block
+    const double one = 1.0, zero = 0.0;
+    const double gb = 16.0 * nn * 4;               // nominal bytes per GEMM call (profiling)
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_rows<<<grid_for(hc), 256, 0, c->st>>>(inout, X.F, n, n2, 2 * n));
+    size_t mk = prof_mark(c);
+    // x transform: G_b = Vt_b^T F_b
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n2, 2 * n, n2, &one, X.Vt, n2, nn, X.F, n2, hc,
+                                  &zero, X.G, n2, hc, 2));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_cols<<<grid_for(4 * nn), 256, 0, c->st>>>(X.G, X.Hh, n, n2));
+    // y transform: R[yb] = Hh[yb] Vt_yb (batch over x parity and plane)
+    for (int yb = 0; yb < 2; ++yb) {
+      mk = prof_mark(c);
+      CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n2, n2, n2, &one, X.Hh + yb * 4 * nn, n2, nn,
+                                    X.Vt + yb * nn, n2, 0, &zero, X.R + yb * 4 * nn, n2, nn, 4));
+      launched(c, HD_K_LIBGEMM, mk, gb, true);
+    }
+    HD_LAUNCH(HD_K_EXACT, 48.0 * 4 * nn, k_scale_folded<<<grid_for(4 * nn), 256, 0, c->st>>>(X.R, X.Dinvf, n2));
+    // inverse y: S[yb] = R[yb] Vt_yb^T  (into Hh)
+    for (int yb = 0; yb < 2; ++yb) {
+      mk = prof_mark(c);
+      CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, n2, n2, n2, &one, X.R + yb * 4 * nn, n2, nn,
+                                    X.Vt + yb * nn, n2, 0, &zero, X.Hh + yb * 4 * nn, n2, nn, 4));
+      launched(c, HD_K_LIBGEMM, mk, gb, true);
+    }
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_cols<<<grid_for(4 * nn), 256, 0, c->st>>>(X.Hh, X.F, n, n2));
+    // inverse x: Yh_b = Vt_b Z_b  (Z in F, result in G)
+    mk = prof_mark(c);
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n2, 2 * n, n2, &one, X.Vt, n2, nn, X.F, n2, hc,
+                                  &zero, X.G, n2, hc, 2));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_rows<<<grid_for(hc), 256, 0, c->st>>>(X.G, inout, n, n2, 2 * n));
+    return;
+  }
+  if (X.dim == 2) {
+    const int n = X.n;
+    const long nn = static_cast<long>(n) * n;
+    const double one = 1.0, zero = 0.0;
+    const double gb = 16.0 * nn * 2 + 8.0 * nn;  // planar in/out + V  (bytes of one GEMM)
+    size_t mk = prof_mark(c);
+    // T1 = V^T [Xre | Xim]
+    CKB(cublasDgemm(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, inout, n, &zero, X.T1, n));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    mk = prof_mark(c);
+    // T2_plane = T1_plane V
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, X.T1, n, nn, X.V, n, 0, &zero,
+                                  X.T2, n, nn, 2));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    HD_LAUNCH(HD_K_EXACT, 48.0 * nn, k_fd_scale<<<grid_for(nn), 256, 0, c->st>>>(X.T2, X.Dinv, nn));
+    mk = prof_mark(c);
+    // T1 = V [T2re | T2im]
+    CKB(cublasDgemm(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, X.T2, n, &zero, X.T1, n));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    mk = prof_mark(c);
+    // out_plane = T1_plane V^T
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, n, n, n, &one, X.T1, n, nn, X.V, n, 0, &zero,
+                                  inout, n, nn, 2));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+  } else {
+    HD_LAUNCH(HD_K_EXACT, 32.0 * X.n,
+              bandlu_launch(c->st, X, nullptr, inout, nullptr, inout));
+    if (X.seg.P) c->launches += 4;  // segmented sweeps: 5 kernels
+  }
+}
+
+// coarsest multigrid level: interleaved in/out
+static void coarsest_solve(hd_ctx* c, const double2* b, double2* out) {
+  ExactSolver& X = c->coarsest;
+  if (X.dense) {
+    dense_apply(c, X, b, out);
+    return;
+  }
+  const double NL = X.dim == 2 ? static_cast<double>(X.n) * X.n : X.n;
+  HD_LAUNCH(HD_K_EXACT, 32.0 * NL,
+            if (X.dim == 2) k_fd_small<<<1, 1024, 0, c->st>>>(X.V, X.Dinv, X.n, b, out);
+            else bandlu_launch(c->st, X, b, nullptr, out, nullptr));
+  if (X.dim != 2 && X.seg.P) c->launches += 4;
+}
+
+static size_t lsize(const hd_ctx* c, int n) { return c->dim == 2 ? static_cast<size_t>(n) * n : n; }
+
+// level l of the shifted hierarchy
+static LevelDev levM(hd_ctx* c, int l) {
+  return level_dev(c->lev[l], c->cM, l == 0 ? c->corner : cmk(0.0, 0.0), c->lev[l].genM);
+}
+
+// x_out = (damped Jacobi)^steps from x (x_zero: x == 0), ping-pong through tmp
+static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2* xb, bool x_zero, int steps) {
+  const LevelDev L = levM(c, l);
+  double2* cur = xa;
+  double2* oth = xb;
+  int s = 0;
+  if (x_zero) {
+    if (steps == 0) {
+      CK(cudaMemsetAsync(cur, 0, lsize(c, L.n) * sizeof(double2), c->st));
+      return cur;
+    }
+    jacobi0(c, L, b, cur, c->spec.omega);
+    s = 1;
+  }
+  for (; s < steps; ++s) {
+    op_apply(c, OP_JACOBI, L, cur, b, oth, c->spec.omega);
+    std::swap(cur, oth);
+  }
+  return cur;
+}
+
+// One V-cycle at level l (src/precond.cpp:144-153); returns the buffer holding x.
+static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero) {
+  const int last = static_cast<int>(c->lev.size()) - 1;
+  if (l == last) {
+    coarsest_solve(c, b, c->mg_x[l]);
+    return c->mg_x[l];
+  }
+  const LevelDev L = levM(c, l);
+  double2* xcur = smooth(c, l, b, c->mg_x[l], c->mg_y[l], x_zero, c->spec.smooth_steps);
+  double2* xoth = xcur == c->mg_x[l] ? c->mg_y[l] : c->mg_x[l];
+  op_apply(c, OP_RESID, L, xcur, b, c->mg_r[l]);
+  const int nf = c->lev[l].n, ncl = c->lev[l + 1].n;
+  restrict_(c, Stencil{0, 0.0}, c->mg_r[l], nf, ncl, c->mg_b[l + 1], nullptr);
+  double2* ec = cycle_at(c, l + 1, c->mg_b[l + 1], true);
+  prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, nf, ncl, nullptr, xcur);
+  double2* res = smooth(c, l, b, xcur, xoth, false, c->spec.smooth_steps);
+  return res;
+}
+
+// out = M^-1 b exactly (C_ex, src/precond.cpp:204-211): fast diagonalisation
+// of the shifted Kronecker sum on the fine level (2D) or banded LU (1D)
+static void shift_exact_solve(hd_ctx* c, const double2* b, double2* out) {
+  const size_t N = c->N;
+  ExactSolver& X = c->shift_exact;
+  if (X.dim == 2) {
+    HD_LAUNCH(HD_K_VEC, 32.0 * N, k_to_planar<<<grid_for(N), 256, 0, c->st>>>(b, c->sx_plan, N));
+    exact_solve_planar(c, X, c->sx_plan);
+    HD_LAUNCH(HD_K_VEC, 32.0 * N, k_from_planar<<<grid_for(N), 256, 0, c->st>>>(c->sx_plan, out, N));
+  } else {
+    HD_LAUNCH(HD_K_EXACT, 32.0 * X.n,
+              bandlu_launch(c->st, X, b, nullptr, out, nullptr));
+    if (X.seg.P) c->launches += 4;
+  }
+}
+
+static void mg_solve(hd_ctx* c, const double2* b, double2* out) {
+  const size_t N = c->N;
+  if (c->spec.cycles <= 0) {
+    shift_exact_solve(c, b, out);
+    return;
+  }
+  bool zero = true;
+  double2* xb = nullptr;
+  for (int cy = 0; cy < c->spec.cycles; ++cy) {
+    if (!zero) {
+      // level-0 iterate must live in mg_x[0] for the next cycle
+      if (xb != c->mg_x[0]) CK(cudaMemcpyAsync(c->mg_x[0], xb, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    }
+    if (c->lev.size() == 1) {
+      coarsest_solve(c, b, c->mg_x[0]);
+      xb = c->mg_x[0];
+    } else if (zero) {
+      xb = cycle_at(c, 0, b, true);
+    } else {
+      // general cycle from a non-zero iterate held in mg_x[0]
+      const LevelDev L = levM(c, 0);
+      double2* xcur = smooth(c, 0, b, c->mg_x[0], c->mg_y[0], false, c->spec.smooth_steps);
+      double2* xoth = xcur == c->mg_x[0] ? c->mg_y[0] : c->mg_x[0];
+      op_apply(c, OP_RESID, L, xcur, b, c->mg_r[0]);
+      restrict_(c, Stencil{0, 0.0}, c->mg_r[0], c->lev[0].n, c->lev[1].n, c->mg_b[1], nullptr);
+      double2* ec = cycle_at(c, 1, c->mg_b[1], true);
+      prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, c->lev[0].n, c->lev[1].n, nullptr, xcur);
+      xb = smooth(c, 0, b, xcur, xoth, false, c->spec.smooth_steps);
+    }
+    zero = false;
+  }
+  if (c->spec.cycles <= 0) {
+    CK(cudaMemsetAsync(out, 0, N * sizeof(double2), c->st));
+    return;
+  }
+  CK(cudaMemcpyAsync(out, xb, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+}
+
+static LevelDev opA(hd_ctx* c) { return level_dev(c->fine, c->cA, c->corner, c->fine.genA); }
+
+// out = Q v = Z E^-1 Z^T v  (Deflation::apply_Q, src/precond.cpp:102-104)
+static void apply_Q(hd_ctx* c, const double2* v, double2* out) {
+  const Stencil z{1, c->spec.drop};
+  restrict_(c, z, v, c->n, c->nc, nullptr, c->ep);
+  exact_solve_planar(c, c->E, c->ep);
+  prolong_<2>(c, z, nullptr, c->ep, c->n, c->nc, nullptr, out);
+}
+
+// out = w - Q (A w)  (Deflation::project, src/precond.cpp:106-108)
+static void project(hd_ctx* c, const double2* w, double2* out) {
+  const Stencil z{1, c->spec.drop};
+  op_apply(c, OP_APPLY, opA(c), w, nullptr, c->t3);
+  restrict_(c, z, c->t3, c->n, c->nc, nullptr, c->ep);
+  exact_solve_planar(c, c->E, c->ep);
+  prolong_<1>(c, z, nullptr, c->ep, c->n, c->nc, w, out);
+}
+
+// out = op(v) = P MG^-1 A v  (src/precond.cpp:236-245); v, out distinct from t1, t2, t3
+static void compose_op(hd_ctx* c, const double2* v, double2* out, const int* vidx = nullptr) {
+  ++c->matvecs;
+  op_apply(c, OP_APPLY, opA(c), v, nullptr, c->t1, 0.0, nullptr, 1.0, vidx, c->N);
+  const double2* cur = c->t1;
+  if (c->spec.shift) {
+    ++c->shift_solves;
+    c->vcycles += c->spec.cycles;
+    mg_solve(c, c->t1, c->t2);
+    cur = c->t2;
+  }
+  if (c->spec.deflate) {
+    ++c->coarse_solves;
+    project(c, cur, out);
+  } else {
+    CK(cudaMemcpyAsync(out, cur, c->N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+  }
+}
+
+// Chooses the persistent Arnoldi geometry: G CTAs of kArnBD threads (<= one
+// per SM), each owning `chunk` elements, K per thread; shared memory holds the
+// non-register part of w and, in block 0, the packed R of the back substitution.
+static void setup_arnoldi(hd_ctx* c, int maxit) {
+  int dev_sms = 0, smem_optin = 0;
+  CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
+  CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  const size_t N = c->N;
+  const size_t per_thread_target = 4;
+  int G = static_cast<int>(std::min<size_t>(dev_sms, std::max<size_t>(1, (N + kArnBD * per_thread_target - 1) /
+                                                                             (kArnBD * per_thread_target))));
+  const size_t chunk = (N + G - 1) / G;
+  const int K = static_cast<int>((chunk + kArnBD - 1) / kArnBD);
+  const size_t w_smem = static_cast<size_t>(std::max(0, K - kArnRW)) * kArnBD * sizeof(double2);
+  const size_t r_smem = (static_cast<size_t>(maxit + 1) * (maxit + 2) / 2 + 4 * (maxit + 2) + 8) * sizeof(double2);
+  const size_t smem = std::max(w_smem, r_smem);
+  c->use_arnoldi = false;
+  if (maxit > 127) return;  // y staged in 128 shared slots
+  if (smem + 4096 > static_cast<size_t>(smem_optin)) return;  // w does not fit on chip: per-step kernels
+  CK(cudaFuncSetAttribute(k_arnoldi<kArnRW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi<kArnRW>, kArnBD, smem));
+  if (per_sm < 1) return;
+  c->arn_G = G;
+  c->arn_K = K;
+  c->arn_chunk = chunk;
+  c->arn_smem = smem;
+  if (!c->dj) c->dj = dalloc<int>(4);
+  if (!c->arn_partials) c->arn_partials = dalloc<double2>(2 * static_cast<size_t>(dev_sms) + 8);
+  if (!c->arn_bar) c->arn_bar = dalloc<unsigned>(4);
+  if (!c->arn_trace && std::getenv("HD_TRACE")) {
+    CK(cudaMallocHost(&c->arn_trace, 8 * sizeof(unsigned long long)));
+  }
+  c->use_arnoldi = true;
+}
+
+static void launch_arnoldi(hd_ctx* c, double2* xout, int maxit, const int* done, double bytes) {
+  ArnoldiArgs a;
+  a.V = c->V;
+  a.Vw = c->V;
+  a.w = c->w;
+  a.x0 = c->x0;
+  a.x = xout;
+  a.N = c->N;
+  a.dj = c->dj;
+  a.done = done;
+  a.H = c->H;
+  a.ldh = maxit + 1;
+  a.g = c->g;
+  a.cs = c->cs;
+  a.sn = c->sn;
+  a.y = c->y;
+  a.hnew_out = c->dres + 1;
+  a.partials = c->arn_partials;
+  a.bar = c->arn_bar;
+  a.K = c->arn_K;
+  a.chunk = c->arn_chunk;
+  a.trace = c->arn_trace;
+  CK(cudaMemsetAsync(c->arn_bar, 0, sizeof(unsigned), c->st));
+  void* args[] = {&a};
+  const double P = 16.0 * static_cast<double>(c->N);
+  (void)P;
+  const size_t mk = prof_mark(c);
+  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_arnoldi<kArnRW>), dim3(c->arn_G), dim3(kArnBD), args,
+                                 c->arn_smem, c->st));
+  launched(c, HD_K_MGS, mk, bytes);
+}
+
+static void ensure_gmres(hd_ctx* c, int maxit) {
+  if (maxit + 1 > c->v_cap) {
+    cudaFree(c->V);
+    c->V = dalloc<double2>(static_cast<size_t>(maxit + 1) * c->N);
+    c->v_cap = maxit + 1;
+  }
+  if (maxit > c->maxit_cap) {
+    cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
+    c->H = dalloc<double2>(static_cast<size_t>(maxit + 1) * maxit);
+    c->g = dalloc<double2>(maxit + 1);
+    c->cs = dalloc<double2>(maxit);
+    c->sn = dalloc<double2>(maxit);
+    c->y = dalloc<double2>(maxit);
+    c->maxit_cap = maxit;
+  }
+  if (maxit != c->arn_maxit) {
+    setup_arnoldi(c, maxit);
+    c->arn_maxit = maxit;
+  }
+  if (maxit != c->lsa_maxit && maxit + 1 <= kLsaMaxJ) {
+    int sms = 0, per = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    CK(cudaFuncSetAttribute(k_lsa_dots, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(lsa_dots_smem())));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lsa_dots, kLsaBD, lsa_dots_smem()));
+    int per2 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_lsa_update, kLsaBD, 0));
+    per = std::max(1, std::min(per, per2));
+    const size_t tiles = (c->N + static_cast<size_t>(kLsaBD) * kLsaTE - 1) / (static_cast<size_t>(kLsaBD) * kLsaTE);
+    c->lsa_G = static_cast<int>(std::max<size_t>(1, std::min<size_t>(tiles, static_cast<size_t>(sms) * per)));
+    cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
+    c->lsa_sig = dalloc<double>(maxit + 2);
+    c->lsa_L = dalloc<double2>(static_cast<size_t>(maxit + 1) * (maxit + 1));
+    c->lsa_ch = dalloc<double2>(maxit + 2);
+    c->lsa_cx = dalloc<double2>(maxit + 2);
+    c->lsa_partials = dalloc<double2>(static_cast<size_t>(c->lsa_G) * (2 * kLsaMaxJ + 2) + 8);
+    if (!c->lsa_counter) {
+      c->lsa_counter = dalloc<unsigned>(4);
+      CK(cudaMemset(c->lsa_counter, 0, 4 * sizeof(unsigned)));
+    }
+    const int m = maxit + 1;
+    c->lsa_givens_smem = (static_cast<size_t>(m) * (m + 1) / 2 + 4 * (m + 2) + 8) * sizeof(double2);
+    CK(cudaFuncSetAttribute(k_lsa_givens, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(c->lsa_givens_smem)));
+    c->lsa_maxit = maxit;
+  }
+}
+
+static LsaArgs lsa_args(hd_ctx* c, double2* xout, int j, int mode, int maxit) {
+  LsaArgs a;
+  a.jlag = 0;
+  a.part_offset = 0;
+  a.partial_only = 0;
+  a.U = c->V;
+  a.Uw = c->V;
+  a.w = c->w;
+  a.x0 = c->x0;
+  a.x = xout;
+  a.N = c->N;
+  a.j = j;
+  a.mode = mode;
+  a.sig = c->lsa_sig;
+  a.L = c->lsa_L;
+  a.ldl = maxit + 1;
+  a.H = c->H;
+  a.ldh = maxit + 1;
+  a.g = c->g;
+  a.cs = c->cs;
+  a.sn = c->sn;
+  a.ch = c->lsa_ch;
+  a.cx = c->lsa_cx;
+  a.hnew_out = c->dres + 1;
+  a.partials = c->lsa_partials;
+  a.counter = c->lsa_counter;
+  a.done = nullptr;
+  a.dj = nullptr;
+  return a;
+}
+
+__global__ void k_inv_scalar(double* dst, const double* src) { *dst = *src > 0.0 ? 1.0 / *src : 0.0; }
+
+static void read_scalars(hd_ctx* c) {
+  CK(cudaMemcpyAsync(c->hres, c->dres, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+}
+
+__global__ void k_loop_init(LoopState* s) {
+  s->j = 0;
+  s->done = 0;
+  s->iters = 0;
+  s->conv = 0;
+  s->need_tail = 0;
+}
+
+__global__ void k_scale_monitor(double* dres) {  // graph monitor: raw norm / (||f|| or 1)
+  const double f = dres[3];
+  dres[0] = dres[0] / (f > 0.0 ? f : 1.0);
+}
+
+static void monitor_raw(hd_ctx* c, const double2* x) {
+  op_apply(c, OP_RESNORM, opA(c), x, c->f, nullptr, 0.0, c->dres + 0, 1.0);
+}
+
+// Captures the GMRES iteration body (device-side j) into the body of a WHILE
+// conditional node: op(u_j) -> pass 1 (dots, x_{j-1}) -> monitor x_{j-1} ->
+// convergence check -> pass 2 (u_{j+1}) -> Givens -> j++.
+static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
+  if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
+  if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
+  c->loop_exec = nullptr;
+  c->loop_graph = nullptr;
+  if (!c->loop_state) {
+    c->loop_state = dalloc<LoopState>(1);
+    CK(cudaMallocHost(&c->loop_host, sizeof(LoopState)));
+  }
+  cudaFree(c->res_hist);
+  if (c->res_host) cudaFreeHost(c->res_host);
+  c->res_hist = dalloc<double>(maxit + 1);
+  CK(cudaMallocHost(&c->res_host, (maxit + 1) * sizeof(double)));
+  const long saved[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
+  const int saved_l = c->launches, saved_b = c->lib_calls;
+  const bool prof = c->prof_on;
+  c->prof_on = false;
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  const int G = c->lsa_G;
+  int* dj = &c->loop_state->j;
+  LsaArgs a = lsa_args(c, c->x, 0, 0, maxit);
+  a.dj = dj;
+  a.done = &c->loop_state->done;
+  // side branch: the Givens rotation + back substitution of iteration j-1
+  // (needed first by pass 2 of iteration j) overlaps the operator of iteration j
+  if (!c->st2) {
+    CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(c->ev_fork, c->st));
+  CK(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+  LsaArgs ag = a;
+  ag.jlag = 1;
+  k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st2>>>(ag, G);
+  CK(cudaEventRecord(c->ev_join, c->st2));
+  compose_op(c, c->V, c->w, dj);
+  CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+  k_lsa_dots<<<G, kLsaBD, lsa_dots_smem(), c->st>>>(a);
+  k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a);  // u_{j+1} and the lagged x_{j-1}
+  monitor_raw(c, c->x);
+  k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres);
+  k_loop_check<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, c->res_hist, tol, h);
+  k_loop_next<<<1, 1, 0, c->st>>>(c->loop_state, maxit, h);
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(c->st, &captured);
+  c->prof_on = prof;
+  c->graph_body_kernels = c->launches - saved_l + 6;  // op + monitor kernels + dots/scale/check/update/givens/next
+  c->matvecs = saved[0];
+  c->coarse_solves = saved[1];
+  c->shift_solves = saved[2];
+  c->vcycles = saved[3];
+  c->launches = saved_l;
+  c->lib_calls = saved_b;
+  CK(ec);
+  CK(cudaGetLastError());
+  CK(cudaGraphInstantiate(&c->loop_exec, g, 0));
+  c->loop_graph = g;
+  c->loop_maxit = maxit;
+  c->loop_tol = tol;
+}
+
+struct SolveOut {
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> residuals;
+};
+
+// gmres(setup.op, setup.rhs, setup.start, setup.monitor, opt) after the
+// compose() right-hand side / start transforms; f already in c->f.
+static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
+  const size_t N = c->N;
+  const int maxit = opt.max_iterations;
+  ensure_gmres(c, std::max(maxit, 1));
+  c->matvecs = c->coarse_solves = c->shift_solves = c->vcycles = 0;
+  c->launches = c->lib_calls = 0;
+  const int nb = c->red_blocks;
+  const double P = 16.0 * static_cast<double>(N);
+  // ||f|| (monitor scale, src/precond.cpp:258)
+  HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->f, nullptr, nullptr, N, red_of(c, c->dres + 3), c->scal + 2));
+  // rhs' = P MG^-1 f   (src/precond.cpp:247-253)
+  const double2* b = c->f;
+  if (c->spec.shift) {
+    ++c->shift_solves;
+    c->vcycles += c->spec.cycles;
+    mg_solve(c, c->f, c->t2);
+    b = c->t2;
+  }
+  if (c->spec.deflate) {
+    ++c->coarse_solves;
+    project(c, b, c->rhsp);
+  } else {
+    CK(cudaMemcpyAsync(c->rhsp, b, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+  }
+  // start = Q f (src/precond.cpp:255-256)
+  if (c->spec.deflate) {
+    apply_Q(c, c->f, c->x0);
+    ++c->coarse_solves;
+  } else {
+    CK(cudaMemsetAsync(c->x0, 0, N * sizeof(double2), c->st));
+  }
+  read_scalars(c);
+  const double fnorm = c->hres[3];
+  const double scale = fnorm > 0.0 ? fnorm : 1.0;
+
+  SolveOut res;
+  auto monitor = [&](const double2* xv) {
+    op_apply(c, OP_RESNORM, opA(c), xv, c->f, nullptr, 0.0, c->dres + 0, scale);
+  };
+  monitor(c->x0);
+  read_scalars(c);
+  const double r0 = c->hres[0];
+  if (r0 <= opt.tolerance) {  // src/linalg.cpp:17-22
+    res.converged = true;
+    res.residuals.push_back(r0);
+    CK(cudaMemcpyAsync(xout, c->x0, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    return res;
+  }
+  // r = rhs' - op(x0); beta = ||r||; V0 = r / beta  (src/linalg.cpp:24-33)
+  compose_op(c, c->x0, c->w);
+  HD_LAUNCH(HD_K_VEC, 3 * P, k_sub<<<grid_for(N), 256, 0, c->st>>>(c->rhsp, c->w, c->w, N));
+  HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, nullptr, nullptr, N, red_of(c, c->dres + 2), c->g));
+  read_scalars(c);
+  const double beta = c->hres[2];
+  if (beta == 0.0) {
+    monitor(c->x0);
+    read_scalars(c);
+    res.converged = c->hres[0] <= opt.tolerance;
+    CK(cudaMemcpyAsync(xout, c->x0, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    return res;
+  }
+  CK(cudaMemsetAsync(c->H, 0, sizeof(double2) * (maxit + 1) * maxit, c->st));
+  CK(cudaMemsetAsync(c->g + 1, 0, sizeof(double2) * maxit, c->st));
+  HD_LAUNCH(HD_K_VEC, 2 * P, k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V, c->w, c->dres + 2, N));
+  const int ldh = maxit + 1;
+  if (c->arn_mode == 2 && maxit + 1 <= kLsaMaxJ) {
+    // u_0 = r (unnormalised), sigma_0 = 1 / beta
+    CK(cudaMemcpyAsync(c->V, c->w, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    HD_LAUNCH(HD_K_VEC, 0.0, k_inv_scalar<<<1, 1, 0, c->st>>>(c->lsa_sig, c->dres + 2));
+    const int G = c->lsa_G;
+    if (c->graph_enabled && !c->prof_on) {
+      if (c->loop_maxit != maxit || c->loop_tol != opt.tolerance) build_loop_graph(c, maxit, opt.tolerance);
+      k_loop_init<<<1, 1, 0, c->st>>>(c->loop_state);
+      CK(cudaGraphLaunch(c->loop_exec, c->st));
+      CK(cudaMemcpyAsync(c->loop_host, c->loop_state, sizeof(LoopState), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(c->res_host, c->res_hist, maxit * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      const LoopState ls = *c->loop_host;
+      // per-iteration launches of the body (op + 7) for the report
+      int it = ls.iters;
+      res.iterations = it;
+      res.converged = ls.conv != 0;
+      for (int q = 0; q < (ls.need_tail ? maxit - 1 : it); ++q) res.residuals.push_back(c->res_host[q]);
+      if (ls.need_tail) {  // x_{maxit-1}: its Givens, an iterate-only pass + monitor
+        LsaArgs b = lsa_args(c, c->x, maxit - 1, 1, maxit);
+        HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(b, G));
+        HD_LAUNCH(HD_K_ITERATE, (maxit + 2.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(b));
+        monitor(c->x);
+        read_scalars(c);
+        res.residuals.push_back(c->hres[0]);
+        res.converged = c->hres[0] <= opt.tolerance;
+      }
+      c->matvecs += it;
+      if (c->spec.shift) {
+        c->shift_solves += it;
+        c->vcycles += static_cast<long>(it) * c->spec.cycles;
+      }
+      if (c->spec.deflate) c->coarse_solves += it;
+      c->launches += (it + 1) * (c->graph_body_kernels);
+      if (xout != c->x) CK(cudaMemcpyAsync(xout, c->x, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+      return res;
+    }
+    bool stop = false;
+    double hnew_prev = 1.0;
+    for (int j = 0; j < maxit && !stop; ++j) {
+      // the op of iteration j is speculative until x_{j-1} is known not to
+      // have converged; its counts are rolled back if GMRES stops at j-1
+      const long snap[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
+      auto rollback = [&]() {
+        c->matvecs = snap[0];
+        c->coarse_solves = snap[1];
+        c->shift_solves = snap[2];
+        c->vcycles = snap[3];
+      };
+      compose_op(c, c->V + static_cast<size_t>(j) * N, c->w);
+      LsaArgs a = lsa_args(c, xout, j, 0, maxit);
+      // pass 1 reads w, u_j, u_0..u_j; pass 2 reads w, u_0..u_j (+ x0 for j >= 1), writes u_{j+1} (+ x)
+      HD_LAUNCH(HD_K_MGS, (j + 3.0) * P, k_lsa_dots<<<G, kLsaBD, lsa_dots_smem(), c->st>>>(a));
+      HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 5.0 : 3.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a));
+      if (j >= 1) {  // x_{j-1} is ready: monitor it (the reference's iteration j-1)
+        monitor(xout);
+        read_scalars(c);
+        const double rr = c->hres[0];
+        res.iterations = j;
+        res.residuals.push_back(rr);
+        if (rr <= opt.tolerance) {
+          res.converged = true;
+          stop = true;
+          rollback();
+          break;
+        }
+        if (hnew_prev < 1e-300) {
+          stop = true;
+          rollback();
+          break;
+        }
+      }
+      HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a, G));
+      CK(cudaMemcpyAsync(c->hres + 1, c->dres + 1, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      // hnew of this iteration is needed one iteration later (read with the next sync)
+      if (j + 1 == maxit) {
+        // budget exhausted: x_{maxit-1} by an iterate-only pass, then its monitor
+        LsaArgs b = lsa_args(c, xout, j, 1, maxit);
+        HD_LAUNCH(HD_K_ITERATE, (j + 3.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(b));
+        monitor(xout);
+        read_scalars(c);
+        const double rr = c->hres[0];
+        res.iterations = j + 1;
+        res.residuals.push_back(rr);
+        res.converged = rr <= opt.tolerance;
+        stop = true;
+      }
+      CK(cudaStreamSynchronize(c->st));
+      hnew_prev = c->hres[1];
+    }
+    return res;
+  }
+  const bool persistent = c->use_arnoldi && c->arn_mode == 1;
+  if (persistent) CK(cudaMemsetAsync(c->dj, 0, sizeof(int), c->st));
+  for (int j = 0; j < maxit && persistent; ++j) {
+    compose_op(c, c->V + static_cast<size_t>(j) * N, c->w);
+    // w in, V_0..V_j (MGS), V_{j+1} out, x0 + V_0..V_j in + x out (iterate)
+    launch_arnoldi(c, xout, maxit, nullptr, (2.0 * j + 6.0) * P);
+    res.iterations = j + 1;
+    monitor(xout);
+    read_scalars(c);
+    if (c->arn_trace) {
+      const unsigned long long* q = c->arn_trace;
+      c->arn_phase_ns[0] += static_cast<double>(q[1] - q[0]);  // MGS chain
+      c->arn_phase_ns[1] += static_cast<double>(q[2] - q[1]);  // V_{j+1} + Givens
+      c->arn_phase_ns[2] += static_cast<double>(q[3] - q[2]);  // barrier
+      c->arn_phase_ns[3] += static_cast<double>(q[4] - q[3]);  // iterate
+    }
+    const double rr = c->hres[0];
+    const double hnew = c->hres[1];
+    res.residuals.push_back(rr);
+    if (rr <= opt.tolerance) {
+      res.converged = true;
+      break;
+    }
+    if (hnew < 1e-300) break;
+  }
+  for (int j = 0; j < maxit && !persistent; ++j) {
+    double2* Vj = c->V + static_cast<size_t>(j) * N;
+    compose_op(c, Vj, c->w);
+    double2* Hj = c->H + static_cast<size_t>(j) * ldh;
+    // modified Gram-Schmidt (src/linalg.cpp:42-47)
+    HD_LAUNCH(HD_K_MGS, 2 * P, k_dot<<<nb, 256, 0, c->st>>>(c->V, c->w, N, red_of(c), Hj + 0));
+    for (int i = 0; i < j; ++i)
+      HD_LAUNCH(HD_K_MGS, 4 * P,
+                k_axpy_dot<<<nb, 256, 0, c->st>>>(c->w, c->V + static_cast<size_t>(i) * N, Hj + i,
+                                                  c->V + static_cast<size_t>(i + 1) * N, N, red_of(c), Hj + i + 1));
+    HD_LAUNCH(HD_K_MGS, 3 * P,
+              k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, Vj, Hj + j, N, red_of(c, c->dres + 1), Hj + j + 1));
+    HD_LAUNCH(HD_K_GIVENS, 0.0, k_givens<<<1, 32, 0, c->st>>>(c->H, ldh, c->g, c->cs, c->sn, c->y, j));
+    HD_LAUNCH(HD_K_ITERATE, (j + 3) * P,
+              k_iterate<<<grid_for(N), 256, 0, c->st>>>(xout, c->x0, c->V, c->y, j + 1, N));
+    res.iterations = j + 1;
+    monitor(xout);
+    read_scalars(c);
+    const double rr = c->hres[0];
+    const double hnew = c->hres[1];
+    res.residuals.push_back(rr);
+    if (rr <= opt.tolerance) {
+      res.converged = true;
+      break;
+    }
+    if (hnew < 1e-300) break;
+    if (j + 1 < maxit) {
+      HD_LAUNCH(HD_K_VEC, 2 * P,
+                k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V + static_cast<size_t>(j + 1) * N, c->w, c->dres + 1,
+                                                            N));
+    }
+  }
+  if (c->arn_trace) {
+    std::fprintf(stderr, "[hd trace] arnoldi phases over %d its (ms): mgs %.3f givens %.3f barrier %.3f iterate %.3f\n",
+                 res.iterations, c->arn_phase_ns[0] * 1e-6, c->arn_phase_ns[1] * 1e-6, c->arn_phase_ns[2] * 1e-6,
+                 c->arn_phase_ns[3] * 1e-6);
+    for (double& v : c->arn_phase_ns) v = 0.0;
+  }
+  return res;
+}
+
+
+}  // namespace hd

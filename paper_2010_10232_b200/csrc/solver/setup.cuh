@@ -1,0 +1,676 @@
+// Non-separable fields (layered, wedge): Galerkin products, dense and block tridiagonal exact solves; context creation and destruction (compose()).
+// (part of solver.cu, a single translation unit: included in order)
+#pragma once
+
+namespace hd {
+
+// ---------------------------------------------------------------------------
+// layered field (layered.cuh): level groups (Y_g, X_g), g = 0..5
+// ---------------------------------------------------------------------------
+struct GenHost {
+  std::vector<Band> Y, X;
+  // wedge: stored 2D stencil K[(iy*n+ix)*(2kb+1)^2 + (dy+kb)*(2kb+1) + dx+kb] (kb < 0: none)
+  std::vector<double> K;
+  int kb = -1;
+};
+
+// Galerkin product (z (x) z)^T K (z (x) z) of a 2D stencil (the reference's
+// sparse triple product Z^T M Z, src/precond.cpp:119, in stencil form), on the
+// device: one thread per coarse entry (I, J - I), gathering over the children
+// of I and J in y and in x.  K and Kc are row-major [point][tap].
+__global__ void k_galerkin_stencil(const double* __restrict__ K, int n, int b, const int* __restrict__ cptr,
+                                   const int* __restrict__ crow, const double* __restrict__ cw, int nc, int bc,
+                                   double* __restrict__ Kc) {
+  const int NB = 2 * b + 1, NBc = 2 * bc + 1;
+  const size_t tot = (size_t)nc * nc * NBc * NBc;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+    const int tap = (int)(e % (NBc * NBc));
+    const size_t I = e / (NBc * NBc);
+    const int Iy = (int)(I / nc), Ix = (int)(I % nc);
+    const int Jy = Iy + tap / NBc - bc, Jx = Ix + tap % NBc - bc;
+    double acc = 0.0;
+    if (Jy >= 0 && Jy < nc && Jx >= 0 && Jx < nc) {
+      for (int pa = cptr[Iy]; pa < cptr[Iy + 1]; ++pa)
+        for (int pc = cptr[Jy]; pc < cptr[Jy + 1]; ++pc) {
+          const int iy = crow[pa], jy = crow[pc], dy = jy - iy;
+          if (dy < -b || dy > b) continue;
+          const double wy = cw[pa] * cw[pc];
+          double sx = 0.0;
+          for (int pb = cptr[Ix]; pb < cptr[Ix + 1]; ++pb)
+            for (int pd = cptr[Jx]; pd < cptr[Jx + 1]; ++pd) {
+              const int ix = crow[pb], jx = crow[pd], dx = jx - ix;
+              if (dx < -b || dx > b) continue;
+              sx += cw[pb] * cw[pd] * K[((size_t)iy * n + ix) * NB * NB + (dy + b) * NB + (dx + b)];
+            }
+          acc += wy * sx;
+        }
+    }
+    Kc[e] = acc;
+  }
+}
+
+static void galerkin_stencil2d(const std::vector<double>& K, int n, int b, const Transfer& z, std::vector<double>& Kc,
+                               int& bc) {
+  const int nc = z.coarse;
+  std::vector<std::vector<std::pair<int, double>>> par(n), ch(nc);
+  for (size_t t = 0; t < z.w.size(); ++t) {
+    par[z.row[t]].push_back({z.col[t], z.w[t]});
+    ch[z.col[t]].push_back({z.row[t], z.w[t]});
+  }
+  bc = 0;
+  for (int i = 0; i < n; ++i)
+    for (int d = -b; d <= b; ++d) {
+      const int j = i + d;
+      if (j < 0 || j >= n) continue;
+      for (const auto& I : par[i])
+        for (const auto& J : par[j]) bc = std::max(bc, std::abs(J.first - I.first));
+    }
+  // children of every coarse index (CSR), fine row order as in z
+  std::vector<int> cptr(nc + 1, 0), crow;
+  std::vector<double> cw;
+  for (int c = 0; c < nc; ++c) {
+    for (const auto& f : ch[c]) {
+      crow.push_back(f.first);
+      cw.push_back(f.second);
+    }
+    cptr[c + 1] = static_cast<int>(crow.size());
+  }
+  const int NBc = 2 * bc + 1;
+  const size_t outn = static_cast<size_t>(nc) * nc * NBc * NBc;
+  double* dK = dalloc<double>(K.size());
+  double* dKc = dalloc<double>(outn);
+  int* dptr = dalloc<int>(cptr.size());
+  int* drow = dalloc<int>(std::max<size_t>(crow.size(), 1));
+  double* dw = dalloc<double>(std::max<size_t>(cw.size(), 1));
+  CK(cudaMemcpy(dK, K.data(), K.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dptr, cptr.data(), cptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(drow, crow.data(), crow.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dw, cw.data(), cw.size() * sizeof(double), cudaMemcpyHostToDevice));
+  k_galerkin_stencil<<<grid_for(outn, 256, 148 * 16), 256>>>(dK, n, b, dptr, drow, dw, nc, bc, dKc);
+  CK(cudaGetLastError());
+  Kc.resize(outn);
+  CK(cudaMemcpy(Kc.data(), dKc, outn * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(dK);
+  cudaFree(dKc);
+  cudaFree(dptr);
+  cudaFree(drow);
+  cudaFree(dw);
+}
+
+// wedge fine level: (M, S), (S, M) and the stored K2 stencil
+static GenHost wedge_fine(const Band& S1, const Band& M1, const double* K2, int p) {
+  GenHost h;
+  h.Y = {M1, S1};
+  h.X = {S1, M1};
+  const size_t n = static_cast<size_t>(M1.n);
+  h.K.assign(K2, K2 + n * n * (2 * p + 1) * (2 * p + 1));
+  h.kb = p;
+  return h;
+}
+
+// fine level: (M, S), (S, M), (B_by, W_by = sum_bx m_{by,bx}^2 B_bx), by = 0..3
+// (K2 of src/assembly.cpp:234-246 grouped by its y factor)
+static GenHost layered_fine(const Band& S1, const Band& M1, const double* interval_mass, const double* mult) {
+  GenHost h;
+  h.Y = {M1, S1};
+  h.X = {S1, M1};
+  std::vector<Band> Bb;
+  for (int b = 0; b < 4; ++b)
+    Bb.push_back(band_from_host(interval_mass + static_cast<size_t>(b) * M1.a.size(), M1.n, M1.b));
+  for (int by = 0; by < 4; ++by) {
+    Band W(M1.n, M1.b);
+    for (int bx = 0; bx < 4; ++bx) {
+      const double m2 = mult[4 * by + bx] * mult[4 * by + bx];
+      for (size_t e = 0; e < W.a.size(); ++e) W.a[e] += m2 * Bb[bx].a[e];
+    }
+    h.Y.push_back(Bb[by]);
+    h.X.push_back(W);
+  }
+  return h;
+}
+
+static GenHost galerkin_gen(const GenHost& h, const Transfer& z) {
+  GenHost o;
+  for (const Band& y : h.Y) o.Y.push_back(galerkin(y, z));
+  for (const Band& x : h.X) o.X.push_back(galerkin(x, z));
+  if (h.kb >= 0) galerkin_stencil2d(h.K, h.Y[0].n, h.kb, z, o.K, o.kb);
+  return o;
+}
+
+// diagonal entry (iy, ix) of a level operator with group coefficients 1 (g < 2), cl (g >= 2) and kc = cl
+static std::complex<double> gen_diag_host(const GenHost& h, int iy, int ix, std::complex<double> cl) {
+  std::complex<double> d(0.0, 0.0);
+  for (size_t g = 0; g < h.Y.size(); ++g)
+    d += (g < 2 ? std::complex<double>(1.0, 0.0) : cl) * (h.Y[g].at(iy, iy) * h.X[g].at(ix, ix));
+  if (h.kb >= 0) {
+    const int n = h.Y[0].n, NB = 2 * h.kb + 1;
+    d += cl * h.K[(static_cast<size_t>(iy) * n + ix) * NB * NB + h.kb * NB + h.kb];
+  }
+  return d;
+}
+
+static Band padded(const Band& B, int b) {
+  Band o(B.n, b);
+  for (int i = 0; i < B.n; ++i)
+    for (int j = std::max(0, i - B.b); j <= std::min(B.n - 1, i + B.b); ++j) o.ref(i, j) = B.at(i, j);
+  return o;
+}
+
+// Upload the groups; layered coefficient cl of groups 2..5 (groups 0, 1: 1).
+static GenLevel upload_gen(const GenHost& h, double2 cl, double** mem) {
+  const int G = static_cast<int>(h.Y.size());
+  int b = std::max(h.kb, 0);
+  for (int g = 0; g < G; ++g) b = std::max({b, h.Y[g].b, h.X[g].b});
+  const int n = h.Y[0].n;
+  const size_t per = static_cast<size_t>(n) * (2 * b + 1);
+  const int NB = 2 * b + 1;
+  const size_t NN = static_cast<size_t>(n) * n, kplanes = h.kb >= 0 ? static_cast<size_t>(NB) * NB * NN : 0;
+  *mem = dalloc<double>(2 * G * per + kplanes);
+  GenLevel L{};
+  L.n = n;
+  L.b = b;
+  L.G = G;
+  for (int g = 0; g < G; ++g) {
+    const Band y = padded(h.Y[g], b), x = padded(h.X[g], b);
+    double* dy = *mem + (2 * g) * per;
+    double* dx = *mem + (2 * g + 1) * per;
+    CK(cudaMemcpy(dy, y.a.data(), per * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dx, x.a.data(), per * sizeof(double), cudaMemcpyHostToDevice));
+    L.Y[g] = dy;
+    L.X[g] = dx;
+    L.coef[g] = g < 2 ? cmk(1.0, 0.0) : cl;
+  }
+  L.K = nullptr;
+  L.kc = cl;
+  if (h.kb >= 0) {
+    // tap-planar, padded to the level band b
+    const int kNB = 2 * h.kb + 1;
+    std::vector<double> planes(kplanes, 0.0);
+    for (size_t i = 0; i < NN; ++i)
+      for (int dy = -h.kb; dy <= h.kb; ++dy)
+        for (int dx = -h.kb; dx <= h.kb; ++dx)
+          planes[static_cast<size_t>((dy + b) * NB + dx + b) * NN + i] = h.K[i * kNB * kNB + (dy + h.kb) * kNB + dx + h.kb];
+    double* dk = *mem + 2 * G * per;
+    CK(cudaMemcpy(dk, planes.data(), kplanes * sizeof(double), cudaMemcpyHostToDevice));
+    L.K = dk;
+  }
+  return L;
+}
+
+// attach the layered groups to a level: unshifted (-k^2) and shifted (-k^2 (1 - i beta2))
+static void attach_gen(DevBand& d, const GenHost& h, double2 cA, double2 cM) {
+  double* mem = nullptr;
+  GenLevel a = upload_gen(h, cmk(-cA.x, -cA.y), &mem);
+  GenLevel m = a;
+  for (int g = 2; g < m.G; ++g) m.coef[g] = cmk(-cM.x, -cM.y);
+  m.kc = cmk(-cM.x, -cM.y);
+  d.gen_mem = mem;
+  d.genA = new GenLevel(a);
+  d.genM = new GenLevel(m);
+}
+
+// Dense inverse of a layered level operator (coefficient cl on groups 2..5):
+// E = Z^T A Z and the coarsest shifted level of the layered hierarchy stand in
+// for the reference's SparseLU factors (src/precond.cpp:95-99, 133).
+static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int n_sms);
+
+static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl, int n_sms = 148, bool allow_btri = true) {
+  const int n = h.Y[0].n;
+  const size_t NN = static_cast<size_t>(n) * n;
+  // operators beyond the dense-inverse limit, or HD_BTRI=1: block tridiagonal LU
+  const char* fb = std::getenv("HD_BTRI");
+  if (allow_btri && (NN > 20000 || (fb && std::atoi(fb) == 1)) && !(fb && std::atoi(fb) == 0))
+    return make_btri(st, h, cl, n_sms);
+  if (NN > 20000)
+    throw Error(HD_ERR_INVALID, "non-separable field: exact solve of " + std::to_string(NN) +
+                                    " complex unknowns exceeds the dense-inverse limit (20000)");
+  ExactSolver X;
+  X.dim = 2;
+  X.n = n;
+  X.dense = true;
+  X.NN = NN;
+  double* mem = nullptr;
+  const GenLevel L = upload_gen(h, cl, &mem);
+  double2* A = dalloc<double2>(NN * NN);
+  X.Ainv = dalloc<double2>(NN * NN);
+  X.dx = dalloc<double2>(NN);
+  X.dy = dalloc<double2>(NN);
+  k_dense_kron<<<grid_for(NN * NN, 256, 148 * 32), 256, 0, st>>>(L, A);
+  CK(cudaGetLastError());
+  k_identity<<<grid_for(NN * NN, 256, 148 * 32), 256, 0, st>>>(X.Ainv, NN);
+  CK(cudaGetLastError());
+  cusolverDnHandle_t hs;
+  CKS(cusolverDnCreate(&hs));
+  CKS(cusolverDnSetStream(hs, st));
+  const int m = static_cast<int>(NN);
+  int lwork = 0;
+  auto* Az = reinterpret_cast<cuDoubleComplex*>(A);
+  CKS(cusolverDnZgetrf_bufferSize(hs, m, m, Az, m, &lwork));
+  cuDoubleComplex* work = dalloc<cuDoubleComplex>(std::max(lwork, 1));
+  int* ipiv = dalloc<int>(NN);
+  int* info = dalloc<int>(2);
+  CKS(cusolverDnZgetrf(hs, m, m, Az, m, work, ipiv, info));
+  CKS(cusolverDnZgetrs(hs, CUBLAS_OP_N, m, m, Az, m, ipiv, reinterpret_cast<cuDoubleComplex*>(X.Ainv), m, info + 1));
+  int hinfo[2] = {0, 0};
+  CK(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cusolverDnDestroy(hs);
+  cudaFree(A);
+  cudaFree(work);
+  cudaFree(ipiv);
+  cudaFree(info);
+  cudaFree(mem);
+  if (hinfo[0] != 0 || hinfo[1] != 0)
+    throw Error(HD_ERR_FACTOR, "layered exact solve: singular operator (getrf info " + std::to_string(hinfo[0]) + ")");
+  return X;
+}
+
+// Block tridiagonal LU of a level operator (btri.cuh): q = b grid rows per
+// block; real (T = double) when every coefficient is real, else complex.
+template <class T>
+struct BtriLib;
+template <>
+struct BtriLib<double> {
+  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, const double* al,
+                             const double* A, const double* B, const double* be, double* C) {
+    return cublasDgemm(h, ta, tb, m, m, m, al, A, m, B, m, be, C, m);
+  }
+  static cusolverStatus_t getrf_ws(cusolverDnHandle_t h, int m, double* A, int* lw) {
+    return cusolverDnDgetrf_bufferSize(h, m, m, A, m, lw);
+  }
+  static cusolverStatus_t getrf(cusolverDnHandle_t h, int m, double* A, double* w, int* piv, int* info) {
+    return cusolverDnDgetrf(h, m, m, A, m, w, piv, info);
+  }
+  static cusolverStatus_t getrs_t(cusolverDnHandle_t h, int m, const double* A, const int* piv, double* B, int* info) {
+    return cusolverDnDgetrs(h, CUBLAS_OP_T, m, m, A, m, piv, B, m, info);
+  }
+  static double one() { return 1.0; }
+  static double mone() { return -1.0; }
+  static double zero() { return 0.0; }
+};
+template <>
+struct BtriLib<double2> {
+  using Z = cuDoubleComplex;
+  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, const double2* al,
+                             const double2* A, const double2* B, const double2* be, double2* C) {
+    return cublasZgemm(h, ta, tb, m, m, m, reinterpret_cast<const Z*>(al), reinterpret_cast<const Z*>(A), m,
+                       reinterpret_cast<const Z*>(B), m, reinterpret_cast<const Z*>(be), reinterpret_cast<Z*>(C), m);
+  }
+  static cusolverStatus_t getrf_ws(cusolverDnHandle_t h, int m, double2* A, int* lw) {
+    return cusolverDnZgetrf_bufferSize(h, m, m, reinterpret_cast<Z*>(A), m, lw);
+  }
+  static cusolverStatus_t getrf(cusolverDnHandle_t h, int m, double2* A, double2* w, int* piv, int* info) {
+    return cusolverDnZgetrf(h, m, m, reinterpret_cast<Z*>(A), m, reinterpret_cast<Z*>(w), piv, info);
+  }
+  static cusolverStatus_t getrs_t(cusolverDnHandle_t h, int m, const double2* A, const int* piv, double2* B, int* info) {
+    // plain transpose (not conjugate): the stored factors are the row-major blocks
+    return cusolverDnZgetrs(h, CUBLAS_OP_T, m, m, reinterpret_cast<const Z*>(A), m, piv, reinterpret_cast<Z*>(B), m, info);
+  }
+  static double2 one() { return cmk(1.0, 0.0); }
+  static double2 mone() { return cmk(-1.0, 0.0); }
+  static double2 zero() { return cmk(0.0, 0.0); }
+};
+
+template <class T>
+static void btri_factor(cudaStream_t st, const GenLevel& L, int q, int m, int nb, ExactSolver& X) {
+  using Lb = BtriLib<T>;
+  const size_t mm = static_cast<size_t>(m) * m, tot = static_cast<size_t>(nb) * mm;
+  const int k = nb / 2;  // the twist: top half eliminated downwards, bottom half upwards
+  T *D = dalloc<T>(tot), *Bu = dalloc<T>(tot), *Cl = dalloc<T>(tot);
+  T *GT = dalloc<T>(tot), *SinvT = dalloc<T>(tot), *HT = dalloc<T>(tot), *G2 = dalloc<T>(mm);
+  CK(cudaMemsetAsync(GT, 0, tot * sizeof(T), st));
+  CK(cudaMemsetAsync(HT, 0, tot * sizeof(T), st));
+  CK(cudaMemsetAsync(G2, 0, mm * sizeof(T), st));
+  k_btri_blocks<T><<<grid_for(tot, 256, 148 * 32), 256, 0, st>>>(L, q, m, nb, D, Bu, Cl);
+  CK(cudaGetLastError());
+  cublasHandle_t cb;
+  CKB(cublasCreate(&cb));
+  CKB(cublasSetStream(cb, st));
+  cusolverDnHandle_t hs;
+  CKS(cusolverDnCreate(&hs));
+  CKS(cusolverDnSetStream(hs, st));
+  int lwork = 0;
+  CKS(Lb::getrf_ws(hs, m, D, &lwork));
+  T* work = dalloc<T>(std::max(lwork, 1));
+  int* ipiv = dalloc<int>(m);
+  int* info = dalloc<int>(2 * nb);
+  CK(cudaMemsetAsync(info, 0, 2 * nb * sizeof(int), st));
+  std::vector<T> eye(mm);
+  for (size_t e = 0; e < mm; ++e) eye[e] = (e % (m + 1) == 0) ? Lb::one() : Lb::zero();
+  const T one = Lb::one(), mone = Lb::mone(), zero = Lb::zero();
+  // Schur block S (in place of D_i) -> its inverse transposed in SinvT[i] (= row-major inverse)
+  auto invert = [&](int i) {
+    T* S = D + i * mm;
+    CKS(Lb::getrf(hs, m, S, work, ipiv, info + 2 * i));
+    T* Si = SinvT + i * mm;
+    CK(cudaMemcpyAsync(Si, eye.data(), mm * sizeof(T), cudaMemcpyHostToDevice, st));
+    CKS(Lb::getrs_t(hs, m, S, ipiv, Si, info + 2 * i + 1));  // S^T X = I
+  };
+  // top: i = 0 .. k-1  (S_i = D_i - G_i B_{i-1}; G_{i+1}^T = S_i^-T C_{i+1}^T; H_i^T = B_i^T S_i^-T)
+  for (int i = 0; i < k; ++i) {
+    if (i > 0) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, GT + i * mm, Bu + (i - 1) * mm, &one, D + i * mm));
+    invert(i);
+    CKB(Lb::gemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, &one, SinvT + i * mm, Cl + (i + 1) * mm, &zero, GT + (i + 1) * mm));
+    CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &one, Bu + i * mm, SinvT + i * mm, &zero, HT + i * mm));
+  }
+  // bottom: i = nb-1 .. k+1  (T_i = D_i - G'_i C_{i+1}; G'_{i-1}^T = T_i^-T B_{i-1}^T; H'_i^T = C_i^T T_i^-T)
+  for (int i = nb - 1; i > k; --i) {
+    if (i < nb - 1) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, GT + i * mm, Cl + (i + 1) * mm, &one, D + i * mm));
+    invert(i);
+    T* gdst = (i - 1 == k) ? G2 : GT + (i - 1) * mm;
+    CKB(Lb::gemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, &one, SinvT + i * mm, Bu + (i - 1) * mm, &zero, gdst));
+    CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &one, Cl + i * mm, SinvT + i * mm, &zero, HT + i * mm));
+  }
+  // middle: M = D_k - G_k B_{k-1} - G'_k C_{k+1}
+  if (k > 0) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, GT + k * mm, Bu + (k - 1) * mm, &one, D + k * mm));
+  if (k < nb - 1) CKB(Lb::gemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, &mone, G2, Cl + (k + 1) * mm, &one, D + k * mm));
+  invert(k);
+  std::vector<int> hinfo(2 * nb);
+  CK(cudaMemcpyAsync(hinfo.data(), info, hinfo.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cublasDestroy(cb);
+  cusolverDnDestroy(hs);
+  cudaFree(D); cudaFree(Bu); cudaFree(Cl); cudaFree(work); cudaFree(ipiv); cudaFree(info);
+  for (int v : hinfo)
+    if (v != 0) {
+      cudaFree(GT); cudaFree(SinvT); cudaFree(HT); cudaFree(G2);
+      throw Error(HD_ERR_FACTOR, "block tridiagonal exact solve: singular block (info " + std::to_string(v) + ")");
+    }
+  X.bt.GT = GT;
+  X.bt.G2 = G2;
+  X.bt.SinvT = SinvT;
+  X.bt.HT = HT;
+  X.bt.k = k;
+}
+
+static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int n_sms) {
+  const int n = h.Y[0].n;
+  double* mem = nullptr;
+  const GenLevel L = upload_gen(h, cl, &mem);
+  bool cplx = L.K && L.kc.y != 0.0;
+  for (int g = 0; g < L.G; ++g) cplx = cplx || L.coef[g].y != 0.0;
+  const int q = std::max(L.b, 1), m = q * n, nb = (n + q - 1) / q;
+  const int kr_need = (m + 31) / 32;
+  int kr = 0;
+  for (int cand : {8, 16, 24, 32, 48, 64, 96})
+    if (cand >= kr_need && (!cplx || cand <= 48)) {
+      kr = cand;
+      break;
+    }
+  if (kr == 0)
+    throw Error(HD_ERR_INVALID, "block tridiagonal solve: block size " + std::to_string(m) + " above the kernel limit");
+  ExactSolver X;
+  X.dim = 2;
+  X.n = n;
+  X.btri = true;
+  X.bt_cplx = cplx;
+  X.bt_kr = kr;
+  try {
+    if (cplx) btri_factor<double2>(st, L, q, m, nb, X);
+    else btri_factor<double>(st, L, q, m, nb, X);
+  } catch (...) {
+    cudaFree(mem);
+    throw;
+  }
+  cudaFree(mem);
+  X.bt.n = n;
+  X.bt.q = q;
+  X.bt.m = m;
+  X.bt.nb = nb;
+  X.bt.NN = static_cast<size_t>(n) * n;
+  // y, w, x: one allocation
+  X.bt.y = dalloc<double>(6 * static_cast<size_t>(nb) * m);
+  X.bt.w = X.bt.y + 2 * static_cast<size_t>(nb) * m;
+  X.bt.x = X.bt.w + 2 * static_cast<size_t>(nb) * m;
+  X.bt.bar = dalloc<unsigned>(1);
+  (void)n_sms;
+  return X;
+}
+
+static void destroy_slabs(hd_ctx* c);
+
+static void destroy_ctx(hd_ctx* c) {
+  if (!c) return;
+  if (c->slabs) destroy_slabs(c);
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  auto fb = [](DevBand& d) {
+    cudaFree(d.S);
+    cudaFree(d.M);
+    cudaFree(d.gen_mem);
+    delete d.genA;
+    delete d.genM;
+  };
+  fb(c->fine);
+  for (size_t l = 1; l < c->lev.size(); ++l) fb(c->lev[l]);
+  free_exact(c->coarsest);
+  free_exact(c->shift_exact);
+  cudaFree(c->sx_plan);
+  free_exact(c->E);
+  for (auto* p : c->mg_b) cudaFree(p);
+  for (auto* p : c->mg_x) cudaFree(p);
+  for (auto* p : c->mg_y) cudaFree(p);
+  for (auto* p : c->mg_r) cudaFree(p);
+  cudaFree(c->ep); cudaFree(c->ep2);
+  cudaFree(c->f); cudaFree(c->rhsp); cudaFree(c->x0); cudaFree(c->x); cudaFree(c->w);
+  cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->t3); cudaFree(c->V);
+  cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
+  cudaFree(c->scal); cudaFree(c->dres); cudaFree(c->partials); cudaFree(c->counter);
+  cudaFree(c->dj); cudaFree(c->arn_partials); cudaFree(c->arn_bar);
+  cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
+  cudaFree(c->lsa_counter);
+  if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
+  if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
+  cudaFree(c->loop_state); cudaFree(c->res_hist); cudaFree(c->cublas_ws);
+  if (c->loop_host) cudaFreeHost(c->loop_host);
+  if (c->res_host) cudaFreeHost(c->res_host);
+  if (c->arn_trace) cudaFreeHost(c->arn_trace);
+  if (c->hres) cudaFreeHost(c->hres);
+  if (c->cb) cublasDestroy(c->cb);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  for (auto e : c->prof_ev) cudaEventDestroy(e);
+  cudaStream_t mine = c->own_st ? c->own_st : c->st;
+  if (mine) cudaStreamDestroy(mine);
+  if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  delete c;
+}
+
+static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* devices, int n_devices, hd_ctx** out) {
+  if (!sys || !spec || !out) throw Error(HD_ERR_INVALID, "null argument");
+  if (n_devices > 1) throw Error(HD_ERR_INVALID, "multi-device row slabs are not available in this build");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(HD_ERR_NO_DEVICE, "no CUDA device: the helmdef_b200 path has no CPU fallback");
+  if (sys->dim != 1 && sys->dim != 2) throw Error(HD_ERR_INVALID, "dim must be 1 or 2");
+  const bool layered = sys->field_kind == HD_FIELD_LAYERED;
+  const bool wedge = sys->field_kind == HD_FIELD_WEDGE;
+  const bool gen = layered || wedge;  // non-Kronecker-sum fields (layered.cuh)
+  if (sys->field_kind != HD_FIELD_CONSTANT && !gen) throw Error(HD_ERR_INVALID, "unknown wave-number field kind");
+  if (gen && sys->dim != 2) throw Error(HD_ERR_INVALID, "the layered and wedge fields are two-dimensional");
+  if (layered && !sys->interval_mass) throw Error(HD_ERR_INVALID, "layered field needs the interval masses");
+  if (wedge && !sys->shift_mass_2d) throw Error(HD_ERR_INVALID, "wedge field needs shift_mass_2d (hd_assemble_field)");
+  if (sys->per_dim < 2) throw Error(HD_ERR_INVALID, "per_dim must be >= 2");
+  const auto t0 = std::chrono::steady_clock::now();
+  // HD_SETUP_TRACE=1: wall time of the setup phases on stderr
+  const bool trace = std::getenv("HD_SETUP_TRACE") && std::atoi(std::getenv("HD_SETUP_TRACE")) == 1;
+  auto tlast = t0;
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hd setup] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - tlast).count());
+    tlast = now;
+  };
+  std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
+  c->device = (devices && n_devices == 1) ? devices[0] : 0;
+  if (!devices || n_devices == 0) CK(cudaGetDevice(&c->device));
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  CKB(cublasCreate(&c->cb));
+  CKB(cublasSetStream(c->cb, c->st));
+  CKB(cublasSetMathMode(c->cb, CUBLAS_DEFAULT_MATH));
+  CK(cudaEventCreate(&c->ev0));
+  CK(cudaEventCreate(&c->ev1));
+  c->dim = sys->dim;
+  c->p = sys->order;
+  c->n = sys->per_dim;
+  c->N = c->dim == 2 ? static_cast<size_t>(c->n) * c->n : c->n;
+  c->k = sys->k;
+  c->spec = *spec;
+  if (c->spec.coarsest <= 0) c->spec.coarsest = 32;
+  c->corner = c->dim == 1 ? cmk(sys->corner_re, sys->corner_im) : cmk(0.0, 0.0);
+  // wedge: K2 carries k(x,y)^2 itself, so its coefficients are 1 and 1 - i beta2
+  const double k2 = wedge ? 1.0 : c->k * c->k;
+  c->cA = cmk(k2, 0.0);
+  // shifted operator A + i beta2 K2 = ... - k^2 (1 - i beta2) M(x)M  (src/precond.cpp:165-167)
+  c->cM = cmk(k2, -k2 * c->spec.beta2);
+  const Band S1 = band_from_host(sys->stiffness_band, c->n, sys->order);
+  const Band M1 = band_from_host(sys->mass_band, c->n, sys->order);
+  mark("context, streams, handles");
+  c->fine = upload_pair(S1, M1);
+  GenHost fineH;
+  if (gen) {
+    fineH = layered ? layered_fine(S1, M1, sys->interval_mass, sys->multipliers)
+                    : wedge_fine(S1, M1, sys->shift_mass_2d, sys->order);
+    attach_gen(c->fine, fineH, c->cA, c->cM);
+  }
+  // C_ex: exact shifted inverse (src/precond.cpp:204-211)
+  if (c->spec.shift && c->spec.cycles <= 0) {
+    if (gen) {
+      // non-separable field: dense inverse (small) or complex block tridiagonal LU of the shifted operator
+      int nsm = 148;
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+      c->shift_exact = make_dense(c->st, fineH, cmk(-c->cM.x, -c->cM.y), nsm);
+      c->sx_plan = dalloc<double>(2 * c->N);
+    } else if (c->dim == 2) {
+      c->shift_exact = make_fd(c->st, S1, M1, c->cM);
+      c->sx_plan = dalloc<double>(2 * c->N);
+    } else {
+      c->shift_exact = make_bandlu(S1, M1, c->cM, c->corner);
+    }
+  }
+  mark("fine level (+ C_ex)");
+  // multigrid hierarchy of the shifted operator (src/precond.cpp:110-134)
+  if (c->spec.shift && c->spec.cycles > 0) {
+    std::vector<Band> Ss{S1}, Ms{M1};
+    std::vector<GenHost> Hs{fineH};
+    int nl = c->n;
+    while (nl > c->spec.coarsest) {
+      const Transfer z = linear_stencil(nl);
+      Ss.push_back(galerkin(Ss.back(), z));
+      Ms.push_back(galerkin(Ms.back(), z));
+      if (gen) Hs.push_back(galerkin_gen(Hs.back(), z));
+      nl = z.coarse;
+    }
+    c->lev.push_back(c->fine);
+    for (size_t l = 1; l < Ss.size(); ++l) {
+      c->lev.push_back(upload_pair(Ss[l], Ms[l]));
+      if (gen) attach_gen(c->lev.back(), Hs[l], c->cA, c->cM);
+    }
+    if (gen)  // zero-diagonal check of the layered / wedge levels (src/precond.cpp:125-132)
+      for (size_t l = 0; l < Hs.size(); ++l) {
+        const GenHost& h = Hs[l];
+        const int nn = h.Y[0].n;
+        for (int i = 0; i < nn; ++i)
+          for (int j = 0; j < nn; ++j)
+            if (gen_diag_host(h, i, j, -std::complex<double>(c->cM.x, c->cM.y)) == std::complex<double>(0.0, 0.0))
+              throw Error(HD_ERR_FACTOR, "zero diagonal in smoother");
+      }
+    // zero-diagonal check of every level (src/precond.cpp:125-132)
+    for (size_t l = 0; !gen && l < Ss.size(); ++l)
+      for (int i = 0; i < Ss[l].n; ++i)
+        for (int j = 0; j < (c->dim == 2 ? Ss[l].n : 1); ++j) {
+          const int jj = c->dim == 2 ? j : i;
+          std::complex<double> d = c->dim == 2
+                                       ? std::complex<double>(Ms[l].at(i, i) * Ss[l].at(jj, jj) + Ss[l].at(i, i) * Ms[l].at(jj, jj), 0.0) -
+                                             std::complex<double>(c->cM.x, c->cM.y) * (Ms[l].at(i, i) * Ms[l].at(jj, jj))
+                                       : std::complex<double>(Ss[l].at(i, i), 0.0) - std::complex<double>(c->cM.x, c->cM.y) * Ms[l].at(i, i);
+          if (l == 0 && c->dim == 1 && i == c->n - 1) d += std::complex<double>(c->corner.x, c->corner.y);
+          if (d == std::complex<double>(0.0, 0.0)) throw Error(HD_ERR_FACTOR, "zero diagonal in smoother");
+        }
+    const Band& SL = Ss.back();
+    const Band& ML = Ms.back();
+    if (gen) c->coarsest = make_dense(c->st, Hs.back(), cmk(-c->cM.x, -c->cM.y), 148, false);  // <= 32^2 unknowns
+    else if (c->dim == 2) c->coarsest = make_fd(c->st, SL, ML, c->cM);
+    else c->coarsest = make_bandlu(SL, ML, c->cM, Ss.size() == 1 ? c->corner : cmk(0.0, 0.0));
+    for (size_t l = 0; l < c->lev.size(); ++l) {
+      const size_t NL = lsize(c.get(), c->lev[l].n);
+      c->mg_b.push_back(l == 0 ? nullptr : dalloc<double2>(NL));
+      c->mg_x.push_back(dalloc<double2>(NL));
+      c->mg_y.push_back(dalloc<double2>(NL));
+      c->mg_r.push_back(dalloc<double2>(NL));
+    }
+  }
+  mark("multigrid hierarchy");
+  // deflation: E = Z^T A Z with the Bezier stencil (src/precond.cpp:93-100, 228-232)
+  if (c->spec.deflate) {
+    const Transfer z = halving_stencil(c->n, c->spec.drop);
+    c->nc = z.coarse;
+    if (c->nc < 1) throw Error(HD_ERR_INVALID, "deflation needs per_dim >= 2");
+    const Band ES = galerkin(S1, z), EM = galerkin(M1, z);
+    if (gen) {
+      int nsm = 148;
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+      c->E = make_dense(c->st, galerkin_gen(fineH, z), cmk(-c->cA.x, -c->cA.y), nsm);
+    } else if (c->dim == 2) {
+      const bool fold = (c->nc % 2 == 0) && centro_symmetric(ES) && centro_symmetric(EM) &&
+                        !std::getenv("HD_NOFOLD");
+      const char* ey = std::getenv("HD_EYSOLVE");
+      // HD_EYSOLVE=1: partial diagonalisation + segmented y sweeps (experimental:
+      // equally exact, but its rounding differs from the oracle's FD by more
+      // than the C3/C5 history bars allow, and it is not yet faster -- DESIGN.md §4)
+      const bool ys = ey && std::atoi(ey) == 1 && c->cA.y == 0.0 && std::max(ES.b, EM.b) <= 6 && c->nc >= 4 * kYL;
+      if (fold) c->E = make_fd_folded(c->st, ES, EM, c->cA);
+      else if (ys) c->E = make_fd_ypart(c->st, ES, EM, c->cA);
+      else c->E = make_fd(c->st, ES, EM, c->cA);
+    } else {
+      // corner term of A restricted: Z^T (corner e_n e_n^T) Z
+      double2 corner_c = cmk(0.0, 0.0);
+      if (c->corner.x != 0.0 || c->corner.y != 0.0) {
+        // the last fine row maps onto the last coarse column(s); E's (nc-1, nc-1) gets w^2 * corner
+        double wl = 0.0;
+        for (size_t t = 0; t < z.w.size(); ++t)
+          if (z.row[t] == c->n - 1 && z.col[t] == c->nc - 1) wl = z.w[t];
+        if (wl != 0.0) corner_c = cmk(c->corner.x * wl * wl, c->corner.y * wl * wl);
+      }
+      c->E = make_bandlu(ES, EM, c->cA, corner_c);
+    }
+    const size_t NC = lsize(c.get(), c->nc);
+    c->ep = dalloc<double>(2 * NC);
+    c->ep2 = dalloc<double>(2 * NC);
+  }
+  mark("deflation E and its solver");
+  const size_t N = c->N;
+  c->f = dalloc<double2>(N);
+  c->rhsp = dalloc<double2>(N);
+  c->x0 = dalloc<double2>(N);
+  c->x = dalloc<double2>(N);
+  c->w = dalloc<double2>(N);
+  c->t1 = dalloc<double2>(N);
+  c->t2 = dalloc<double2>(N);
+  c->t3 = dalloc<double2>(N);
+  c->scal = dalloc<double2>(8);
+  c->dres = dalloc<double>(8);
+  CK(cudaMallocHost(&c->hres, 8 * sizeof(double)));
+  c->red_blocks = 148 * 4;
+  const int max_stencil_blocks = 148 * 64;
+  c->partials = dalloc<double2>(std::max(c->red_blocks, max_stencil_blocks) + 16);
+  c->counter = dalloc<unsigned>(4);
+  CK(cudaMemset(c->counter, 0, 4 * sizeof(unsigned)));
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaDeviceSynchronize());
+  if (const char* e = std::getenv("HD_ARNOLDI")) c->arn_mode = std::atoi(e);
+  if (const char* e = std::getenv("HD_GRAPH")) c->graph_enabled = std::atoi(e) != 0;
+  CK(cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, c->device));
+  c->cublas_ws = dalloc<char>(32u << 20);
+  CKB(cublasSetWorkspace(c->cb, c->cublas_ws, 32u << 20));
+  mark("vectors, workspaces");
+  c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = c.release();
+}
+
+
+}  // namespace hd
