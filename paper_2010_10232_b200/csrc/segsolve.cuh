@@ -55,31 +55,51 @@ __device__ __forceinline__ double2 seg_rhs(const double2* b, const double* bp, i
   return bp ? cmk(bp[k], bp[k + n]) : b[k];
 }
 
-// local forward sweep of every segment (thread per segment)
+// local forward sweep of every segment (thread per segment).  The tables of
+// row r+1 are loaded while row r is eliminated (the recurrence itself is a
+// short dependent chain; with one thread per segment the loads would
+// otherwise serialise behind it).
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_fwd(SegArgs a, const double2* __restrict__ b,
                                                 const double* __restrict__ bp) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.P) return;
   const int P = a.P, s = i * kSegL;
+  const int* __restrict__ pv = a.pv;
+  const double2* __restrict__ Lt = a.L;
+  double2* __restrict__ y = a.y;
   double2 w[KL + 1];
 #pragma unroll
   for (int q = 0; q <= KL; ++q) w[q] = seg_rhs(b, bp, a.n, s + q);
-#pragma unroll 8
+  int pc = __ldg(pv + i);
+  double2 lc[KL], bc = seg_rhs(b, bp, a.n, s + KL + 1);
+#pragma unroll
+  for (int q = 0; q < KL; ++q) lc[q] = __ldg(Lt + (size_t)q * P + i);
+#pragma unroll 4
   for (int r = 0; r < kSegL; ++r) {
-    const int p = __ldg(a.pv + (size_t)r * P + i);
+    // next row's tables first
+    const int rn = r + 1 < kSegL ? r + 1 : r;
+    const int pn = __ldg(pv + (size_t)rn * P + i);
+    double2 ln[KL];
+#pragma unroll
+    for (int q = 0; q < KL; ++q) ln[q] = __ldg(Lt + ((size_t)rn * KL + q) * P + i);
+    const double2 bn = seg_rhs(b, bp, a.n, s + r + KL + 2);
     double2 yk = w[0];
 #pragma unroll
-    for (int q = 1; q <= KL; ++q) yk = p == q ? w[q] : yk;
+    for (int q = 1; q <= KL; ++q) yk = pc == q ? w[q] : yk;
 #pragma unroll
     for (int q = 1; q <= KL; ++q) {
-      const double2 wq = p == q ? w[0] : w[q];
-      w[q] = csub(wq, cmul(__ldg(a.L + ((size_t)r * KL + q - 1) * P + i), yk));
+      const double2 wq = pc == q ? w[0] : w[q];
+      w[q] = csub(wq, cmul(lc[q - 1], yk));
     }
-    a.y[(size_t)r * P + i] = yk;
+    y[(size_t)r * P + i] = yk;
 #pragma unroll
     for (int q = 0; q < KL; ++q) w[q] = w[q + 1];
-    w[KL] = seg_rhs(b, bp, a.n, s + r + KL + 1);
+    w[KL] = bc;
+    pc = pn;
+    bc = bn;
+#pragma unroll
+    for (int q = 0; q < KL; ++q) lc[q] = ln[q];
   }
   // D_i = end window - raw rhs rows e..e+KL
 #pragma unroll
@@ -129,31 +149,56 @@ __global__ void __launch_bounds__(32) k_seg_scan_fwd(SegArgs a) {
   cp_async_wait<0>();
 }
 
-// forward correction y_k += h_k . Delta_i, then the local backward sweep
+// forward correction y_k += h_k . Delta_i, then the local backward sweep (the
+// tables of row r-1 are loaded while row r is solved, as in k_seg_fwd)
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_bwd(SegArgs a) {
   constexpr int KU = 2 * KL;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.P) return;
   const int P = a.P;
+  const double2* __restrict__ yt = a.y;
+  const double2* __restrict__ hf = a.hf;
+  const double2* __restrict__ Ut = a.U;
+  const double2* __restrict__ Ui = a.Ui;
+  double2* __restrict__ x0 = a.x0;
   double2 dl[KL + 1];
 #pragma unroll
   for (int q = 0; q <= KL; ++q) dl[q] = a.Dl[(size_t)i * (KL + 1) + q];
   double2 xw[KU];  // x_{k+1} .. x_{k+KU}
 #pragma unroll
   for (int d = 0; d < KU; ++d) xw[d] = cmk(0.0, 0.0);
-#pragma unroll 8
+  // tables of one row: y, hf[KL+1], U[KU], 1/u
+  auto load = [&](int r, double2& yv, double2 (&h)[KL + 1], double2 (&u)[KU], double2& ui) {
+    yv = yt[(size_t)r * P + i];
+#pragma unroll
+    for (int q = 0; q <= KL; ++q) h[q] = __ldg(hf + ((size_t)r * (KL + 1) + q) * P + i);
+#pragma unroll
+    for (int d = 0; d < KU; ++d) u[d] = __ldg(Ut + ((size_t)r * KU + d) * P + i);
+    ui = __ldg(Ui + (size_t)r * P + i);
+  };
+  double2 yc, hc[KL + 1], uc[KU], uic;
+  load(kSegL - 1, yc, hc, uc, uic);
+#pragma unroll 2
   for (int r = kSegL - 1; r >= 0; --r) {
-    double2 sacc = a.y[(size_t)r * P + i];
+    double2 yn, hn[KL + 1], un[KU], uin;
+    load(r > 0 ? r - 1 : 0, yn, hn, un, uin);
+    double2 sacc = yc;
 #pragma unroll
-    for (int q = 0; q <= KL; ++q) sacc = cfma(__ldg(a.hf + ((size_t)r * (KL + 1) + q) * P + i), dl[q], sacc);
+    for (int q = 0; q <= KL; ++q) sacc = cfma(hc[q], dl[q], sacc);
 #pragma unroll
-    for (int d = KU; d >= 1; --d) sacc = csub(sacc, cmul(__ldg(a.U + ((size_t)r * KU + d - 1) * P + i), xw[d - 1]));
-    const double2 xk = cmul(sacc, __ldg(a.Ui + (size_t)r * P + i));
+    for (int d = KU; d >= 1; --d) sacc = csub(sacc, cmul(uc[d - 1], xw[d - 1]));
+    const double2 xk = cmul(sacc, uic);
 #pragma unroll
     for (int d = KU - 1; d >= 1; --d) xw[d] = xw[d - 1];
     xw[0] = xk;
-    a.x0[(size_t)r * P + i] = xk;
+    x0[(size_t)r * P + i] = xk;
+    yc = yn;
+    uic = uin;
+#pragma unroll
+    for (int q = 0; q <= KL; ++q) hc[q] = hn[q];
+#pragma unroll
+    for (int d = 0; d < KU; ++d) uc[d] = un[d];
   }
 #pragma unroll
   for (int d = 0; d < KU; ++d) a.X0[(size_t)i * KU + d] = xw[d];  // xw[d] = x_{s+d}
