@@ -38,6 +38,7 @@
 #include "btri.cuh"
 #include "segsolve.cuh"
 #include "ysolve.cuh"
+#include "tail1d.cuh"
 
 
 #include "solver/context.cuh"

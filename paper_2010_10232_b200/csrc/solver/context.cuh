@@ -110,6 +110,9 @@ struct hd_ctx {
   ExactSolver shift_exact;      // C_ex: exact inverse of the shifted operator (cycles == 0)
   double* sx_plan = nullptr;    // planar scratch for the 2D exact shifted solve
   std::vector<double2*> mg_b, mg_x, mg_y, mg_r;
+  int tail_l = -1;              // 1D: first level of the single-CTA tail V-cycle (tail1d.cuh), -1: none
+  TailArgs tail{};
+  size_t tail_smem_bytes = 0;
   // deflation
   int nc = 0;
   ExactSolver E;

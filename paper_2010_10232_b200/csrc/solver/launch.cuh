@@ -459,6 +459,13 @@ static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2*
 // One V-cycle at level l (src/precond.cpp:144-153); returns the buffer holding x.
 static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero) {
   const int last = static_cast<int>(c->lev.size()) - 1;
+  if (l == c->tail_l && x_zero) {  // 1D: the remaining levels in one single-CTA kernel
+    double nb = 0.0;
+    for (int t = 0; t < c->tail.nl; ++t) nb += 64.0 * c->tail.n[t];
+    HD_LAUNCH(HD_K_OP_COARSE, nb,
+              k_tail1d<<<1, kTailThreads, c->tail_smem_bytes, c->st>>>(c->tail, b, c->mg_x[l]));
+    return c->mg_x[l];
+  }
   if (l == last) {
     coarsest_solve(c, b, c->mg_x[l]);
     return c->mg_x[l];

@@ -596,6 +596,43 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
     if (gen) c->coarsest = make_dense(c->st, Hs.back(), cmk(-c->cM.x, -c->cM.y), 148, false);  // <= 32^2 unknowns
     else if (c->dim == 2) c->coarsest = make_fd(c->st, SL, ML, c->cM);
     else c->coarsest = make_bandlu(SL, ML, c->cM, Ss.size() == 1 ? c->corner : cmk(0.0, 0.0));
+    // 1D tail: the levels from the first one with <= kTailMax rows down to the coarsest
+    // in one single-CTA kernel (tail1d.cuh); HD_TAIL=0 keeps the per-level kernels
+    const char* te = std::getenv("HD_TAIL");
+    if (c->dim == 1 && !(te && std::atoi(te) == 0) && c->lev.size() >= 2 && c->coarsest.L && !c->coarsest.dense) {
+      const int last = static_cast<int>(c->lev.size()) - 1;
+      int t = 0;
+      while (t < last && c->lev[t].n > kTailMax) ++t;
+      if (t < last && last - t + 1 <= kTailLevels) {
+        TailArgs& A = c->tail;
+        A.nl = last - t + 1;
+        int off = 0;
+        for (int l = 0; l < A.nl; ++l) {
+          const DevBand& d = c->lev[t + l];
+          A.n[l] = d.n;
+          A.b[l] = d.b;
+          A.S[l] = d.S;
+          A.M[l] = d.M;
+          A.off[l] = off;
+          off += 4 * d.n;
+        }
+        A.c = c->cM;
+        A.corner = t == 0 ? c->corner : cmk(0.0, 0.0);
+        A.omega = c->spec.omega;
+        A.nu = c->spec.smooth_steps;
+        A.Lf = c->coarsest.L;
+        A.Uf = c->coarsest.U;
+        A.piv = c->coarsest.piv;
+        A.kl = c->coarsest.kl;
+        A.ku = c->coarsest.ku;
+        const size_t smem = tail_smem(A);
+        if (smem <= 200u * 1024u) {
+          CK(cudaFuncSetAttribute(k_tail1d, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+          c->tail_smem_bytes = smem;
+          c->tail_l = t;
+        }
+      }
+    }
     for (size_t l = 0; l < c->lev.size(); ++l) {
       const size_t NL = lsize(c.get(), c->lev[l].n);
       c->mg_b.push_back(l == 0 ? nullptr : dalloc<double2>(NL));
