@@ -39,6 +39,7 @@
 #include "segsolve.cuh"
 #include "ysolve.cuh"
 #include "tail1d.cuh"
+#include "small1d.cuh"
 
 
 #include "solver/context.cuh"

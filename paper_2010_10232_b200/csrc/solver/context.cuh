@@ -113,6 +113,10 @@ struct hd_ctx {
   int tail_l = -1;              // 1D: first level of the single-CTA tail V-cycle (tail1d.cuh), -1: none
   TailArgs tail{};
   size_t tail_smem_bytes = 0;
+  bool small_ok = false;        // 1D, N <= kSmallMax: the whole solve in one single-CTA kernel (small1d.cuh)
+  SmallArgs small{};
+  double* small_res = nullptr;  // device residual history
+  int* small_state = nullptr;
   // deflation
   int nc = 0;
   ExactSolver E;

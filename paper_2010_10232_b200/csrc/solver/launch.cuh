@@ -830,7 +830,74 @@ struct SolveOut {
 
 // gmres(setup.op, setup.rhs, setup.start, setup.monitor, opt) after the
 // compose() right-hand side / start transforms; f already in c->f.
+// small 1D systems: the whole solve in one single-CTA kernel (small1d.cuh);
+// the counters follow the reference's call pattern (compose: rhs and start,
+// then one op per GMRES step plus the initial residual's)
+static SolveOut run_solve_small1d(hd_ctx* c, const hd_gmres& opt, double2* xout) {
+  const int maxit = opt.max_iterations;
+  ensure_gmres(c, std::max(maxit, 1));
+  c->matvecs = c->coarse_solves = c->shift_solves = c->vcycles = 0;
+  c->launches = c->lib_calls = 0;
+  SmallArgs a = c->small;
+  a.maxit = maxit;
+  a.tol = opt.tolerance;
+  a.f = c->f;
+  a.x = xout;
+  a.V = c->V;
+  a.H = c->H;
+  a.res = c->small_res;
+  a.state = c->small_state;
+  const size_t smem = small_smem(a);
+  static size_t attr = 0;
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_solve1d_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = smem;
+  }
+  // one warp per 32 unknowns (64..512 threads): fewer warps make the block barriers cheaper
+  const int threads = static_cast<int>(std::min<size_t>(kSmallThreads, std::max<size_t>(64, (c->N + 31) / 32 * 32)));
+  HD_LAUNCH(HD_K_OP_FINE, 16.0 * c->N * 10.0, k_solve1d_small<<<1, threads, smem, c->st>>>(a));
+  int st[4] = {0, 0, 0, 0};
+  std::vector<double> res(static_cast<size_t>(maxit) + 1, 0.0);
+  CK(cudaMemcpyAsync(st, c->small_state, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(res.data(), c->small_res, res.size() * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const long cyc = c->spec.shift && c->spec.cycles > 0 ? c->spec.cycles : 0;
+  auto one_op = [&]() {  // compose_op's counters
+    ++c->matvecs;
+    if (c->spec.shift) {
+      ++c->shift_solves;
+      c->vcycles += cyc;
+    }
+    if (c->spec.deflate) ++c->coarse_solves;
+  };
+  if (c->spec.shift) {  // rhs' = P MG^-1 f
+    ++c->shift_solves;
+    c->vcycles += cyc;
+  }
+  if (c->spec.deflate) c->coarse_solves += 2;  // project(rhs'), start = Q f
+  SolveOut r;
+  if (st[2] == 1) {  // monitor(x0) <= tol
+    r.converged = true;
+    r.residuals.push_back(res[0]);
+    return r;
+  }
+  one_op();  // r = rhs' - op(x0)
+  if (st[2] == 2) {  // beta == 0
+    r.converged = st[1] != 0;
+    return r;
+  }
+  r.iterations = st[0];
+  r.converged = st[1] != 0;
+  for (int j = 0; j < r.iterations; ++j) {
+    r.residuals.push_back(res[j]);
+    one_op();
+  }
+  return r;
+}
+
 static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
+  if (c->small_ok && opt.max_iterations >= 1 && opt.max_iterations + 1 <= kLsaMaxJ && !c->prof_on)
+    return run_solve_small1d(c, opt, xout);
   const size_t N = c->N;
   const int maxit = opt.max_iterations;
   ensure_gmres(c, std::max(maxit, 1));

@@ -452,6 +452,7 @@ static void destroy_ctx(hd_ctx* c) {
   for (auto* p : c->mg_y) cudaFree(p);
   for (auto* p : c->mg_r) cudaFree(p);
   cudaFree(c->ep); cudaFree(c->ep2);
+  cudaFree(c->small_res); cudaFree(c->small_state);
   cudaFree(c->f); cudaFree(c->rhsp); cudaFree(c->x0); cudaFree(c->x); cudaFree(c->w);
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->t3); cudaFree(c->V);
   cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
@@ -680,6 +681,69 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
     c->ep2 = dalloc<double>(2 * NC);
   }
   mark("deflation E and its solver");
+  // small 1D systems: the whole solve as one single-CTA kernel (small1d.cuh); HD_SMALL=0: per-kernel path
+  {
+    const char* se = std::getenv("HD_SMALL");
+    const bool mg_ok = c->spec.shift && c->spec.cycles > 0 && c->lev.size() >= 1 &&
+                       static_cast<int>(c->lev.size()) <= kTailLevels && c->coarsest.L;
+    const bool cex_ok = c->spec.shift && c->spec.cycles <= 0 && c->shift_exact.L;
+    if (c->dim == 1 && c->n <= kSmallMax && !(se && std::atoi(se) == 0) && (!c->spec.shift || mg_ok || cex_ok) &&
+        (!c->spec.deflate || c->E.L)) {
+      SmallArgs& A = c->small;
+      A.shift = !c->spec.shift ? 0 : (c->spec.cycles > 0 ? 1 : 2);
+      A.cycles = c->spec.cycles;
+      int off = 0;
+      if (A.shift == 1) {
+        TailArgs& T = A.mg;
+        T.nl = static_cast<int>(c->lev.size());
+        for (int l = 0; l < T.nl; ++l) {
+          T.n[l] = c->lev[l].n;
+          T.b[l] = c->lev[l].b;
+          T.S[l] = c->lev[l].S;
+          T.M[l] = c->lev[l].M;
+          T.off[l] = off;
+          off += 4 * c->lev[l].n;
+        }
+        T.c = c->cM;
+        T.corner = c->corner;
+        T.omega = c->spec.omega;
+        T.nu = c->spec.smooth_steps;
+        T.Lf = c->coarsest.L;
+        T.Uf = c->coarsest.U;
+        T.piv = c->coarsest.piv;
+        T.kl = c->coarsest.kl;
+        T.ku = c->coarsest.ku;
+      }
+      if (A.shift == 2) {
+        A.sLf = c->shift_exact.L;
+        A.sUf = c->shift_exact.U;
+        A.spiv = c->shift_exact.piv;
+        A.skl = c->shift_exact.kl;
+        A.sku = c->shift_exact.ku;
+      }
+      A.AS = c->fine.S;
+      A.AM = c->fine.M;
+      A.Ab = c->fine.b;
+      A.cA = c->cA;
+      A.corner = c->corner;
+      A.deflate = c->spec.deflate;
+      A.nc = c->spec.deflate ? c->nc : 0;
+      A.drop = c->spec.drop;
+      if (c->spec.deflate) {
+        A.eLf = c->E.L;
+        A.eUf = c->E.U;
+        A.epiv = c->E.piv;
+        A.ekl = c->E.kl;
+        A.eku = c->E.ku;
+      }
+      A.N = c->n;
+      A.mg_off = 0;
+      A.vec_off = off;
+      c->small_res = dalloc<double>(kLsaMaxJ + 8);
+      c->small_state = dalloc<int>(4);
+      c->small_ok = true;
+    }
+  }
   const size_t N = c->N;
   c->f = dalloc<double2>(N);
   c->rhsp = dalloc<double2>(N);
