@@ -108,29 +108,6 @@ __device__ __forceinline__ double small_norm(const double2* a, int n, double* re
   return sqrt(small_bsum(s, red));
 }
 
-// banded LU solve in place (one thread), k_bandlu_solve's arithmetic
-__device__ __forceinline__ void small_lu(double2* w, int n, const double2* Lf, const double2* Uf, const int* piv, int kl,
-                                         int ku) {
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < n; ++k) {
-      const int p = piv[k];
-      if (p != k) {
-        const double2 tmp = w[k];
-        w[k] = w[p];
-        w[p] = tmp;
-      }
-      const double2 wk = w[k];
-      for (int r = 1; r <= kl && k + r < n; ++r) w[k + r] = csub(w[k + r], cmul(Lf[(size_t)k * kl + r - 1], wk));
-    }
-    for (int k = n - 1; k >= 0; --k) {
-      double2 s = w[k];
-      for (int d = 1; d <= ku && k + d < n; ++d) s = csub(s, cmul(Uf[(size_t)k * (ku + 1) + d], w[k + d]));
-      w[k] = cdiv(s, Uf[(size_t)k * (ku + 1)]);
-    }
-  }
-  __syncthreads();
-}
-
 // out = L x for a level of the hierarchy (l) or A (l < 0)
 __device__ __forceinline__ void small_apply(const SmallArgs& a, const double2* x, double2* out) {
   const int n = a.N, b = a.Ab, NB = 2 * b + 1;
@@ -150,98 +127,6 @@ __device__ __forceinline__ void small_apply(const SmallArgs& a, const double2* x
   __syncthreads();
 }
 
-// One V-cycle of the shifted hierarchy on the shared-memory levels (tail
-// layout: per level x, y, b, r).  The fine right-hand side is in level 0's b;
-// x_zero: the fine iterate starts from zero (else from level 0's current x,
-// *cur0 says which buffer).  Returns the fine iterate's buffer index in *cur0.
-__device__ void small_vcycle(const TailArgs& a, double2* tsm, bool x_zero, int* cur0) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  auto X = [&](int l, int k) { return tsm + a.off[l] + k * a.n[l]; };
-  int cur[kTailLevels];
-  const int last = a.nl - 1;
-  for (int l = 0; l < last; ++l) {
-    const double2 corner = l == 0 ? a.corner : cmk(0.0, 0.0);
-    const int n = a.n[l];
-    double2* b = X(l, 2);
-    double2* r = X(l, 3);
-    int s0 = 0;
-    if (l == 0 && !x_zero) {
-      cur[l] = *cur0;
-    } else {
-      cur[l] = 0;
-      if (a.nu == 0) {
-        for (int i = tid; i < n; i += nt) X(l, 0)[i] = cmk(0.0, 0.0);
-      } else {
-        for (int i = tid; i < n; i += nt) X(l, 0)[i] = cscale(a.omega, cmul(cinv(tail_diag(a, l, i, corner)), b[i]));
-        s0 = 1;
-      }
-      __syncthreads();
-    }
-    for (int s = s0; s < a.nu; ++s) {
-      const double2* x = X(l, cur[l]);
-      double2* y = X(l, cur[l] ^ 1);
-      for (int i = tid; i < n; i += nt) {
-        const double2 yv = tail_apply(a, l, x, i, corner);
-        y[i] = cadd(x[i], cscale(a.omega, cmul(cinv(tail_diag(a, l, i, corner)), csub(b[i], yv))));
-      }
-      cur[l] ^= 1;
-      __syncthreads();
-    }
-    const double2* x = X(l, cur[l]);
-    for (int i = tid; i < n; i += nt) r[i] = csub(b[i], tail_apply(a, l, x, i, corner));
-    __syncthreads();
-    const int nc = a.n[l + 1];
-    double2* bc = X(l + 1, 2);
-    for (int q = tid; q < nc; q += nt) {
-      double2 acc = cmk(0.0, 0.0);
-      for (int o = 0; o < 3; ++o) {
-        const int i = 2 * q + o;
-        if (i < n) acc = cfma_r(o == 1 ? 1.0 : 0.5, r[i], acc);
-      }
-      bc[q] = acc;
-    }
-    __syncthreads();
-  }
-  {  // coarsest: banded LU
-    const int n = a.n[last];
-    double2* w = X(last, 0);
-    cur[last] = 0;
-    for (int i = tid; i < n; i += nt) w[i] = X(last, 2)[i];
-    __syncthreads();
-    small_lu(w, n, a.Lf, a.Uf, a.piv, a.kl, a.ku);
-  }
-  for (int l = last - 1; l >= 0; --l) {
-    const double2 corner = l == 0 ? a.corner : cmk(0.0, 0.0);
-    const int n = a.n[l], nc = a.n[l + 1];
-    double2* x = X(l, cur[l]);
-    const double2* e = X(l + 1, cur[l + 1]);
-    for (int i = tid; i < n; i += nt) {
-      double2 acc = cmk(0.0, 0.0);
-      if (i & 1) {
-        const int q = (i - 1) / 2;
-        if (q < nc) acc = cfma_r(1.0, e[q], acc);
-      } else {
-        if (i / 2 - 1 >= 0 && i / 2 - 1 < nc) acc = cfma_r(0.5, e[i / 2 - 1], acc);
-        if (i / 2 < nc) acc = cfma_r(0.5, e[i / 2], acc);
-      }
-      x[i] = cadd(x[i], acc);
-    }
-    __syncthreads();
-    const double2* b = X(l, 2);
-    for (int s = 0; s < a.nu; ++s) {
-      const double2* xs = X(l, cur[l]);
-      double2* y = X(l, cur[l] ^ 1);
-      for (int i = tid; i < n; i += nt) {
-        const double2 yv = tail_apply(a, l, xs, i, corner);
-        y[i] = cadd(xs[i], cscale(a.omega, cmul(cinv(tail_diag(a, l, i, corner)), csub(b[i], yv))));
-      }
-      cur[l] ^= 1;
-      __syncthreads();
-    }
-  }
-  *cur0 = cur[0];
-}
-
 // Bezier restriction of the fine vector r into ec, E^-1 in place, then
 // mode 1: out = s - Z ec;  mode 2: out = Z ec
 __device__ void small_deflate(const SmallArgs& a, const double2* r, double2* ec, const double2* s, double2* out,
@@ -257,7 +142,7 @@ __device__ void small_deflate(const SmallArgs& a, const double2* r, double2* ec,
     ec[q] = acc;
   }
   __syncthreads();
-  small_lu(ec, nc, a.eLf, a.eUf, a.epiv, a.ekl, a.eku);
+  tail_lu(ec, nc, a.eLf, a.eUf, a.epiv, a.ekl, a.eku);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double2 acc = cmk(0.0, 0.0);
     auto add = [&](int q, double w) {
@@ -313,13 +198,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve1d_small(SmallArgs a) {
     if (a.shift == 2) {
       for (int i = tid; i < N; i += nt) out[i] = v[i];
       __syncthreads();
-      small_lu(out, N, a.sLf, a.sUf, a.spiv, a.skl, a.sku);
+      tail_lu(out, N, a.sLf, a.sUf, a.spiv, a.skl, a.sku);
       return;
     }
     for (int i = tid; i < N; i += nt) mg_b0[i] = v[i];
     __syncthreads();
     int cur0 = 0;
-    for (int cy = 0; cy < a.cycles; ++cy) small_vcycle(mg, tsm, cy == 0, &cur0);
+    for (int cy = 0; cy < a.cycles; ++cy) tail_vcycle(mg, tsm, cy == 0, &cur0);
     const double2* xs = tsm + a.mg.off[0] + cur0 * a.mg.n[0];
     for (int i = tid; i < N; i += nt) out[i] = xs[i];
     __syncthreads();

@@ -5,7 +5,8 @@
 // prolongation, post-smoothing; the coarsest level by its banded LU).  On the
 // 1D configs these levels are a few thousand rows at most, so a per-level
 // kernel chain (five launches per level) is launch-latency bound; here the
-// phases are separated by __syncthreads only.  Same formulas and summation
+// phases are separated by __syncthreads only.  tail_vcycle is shared with the
+// whole-solve kernel of small1d.cuh.  Same formulas and summation
 // order as k_op1d / k_jacobi0_1d / k_restrict<1> / k_prolong<1,0> /
 // k_bandlu_solve.
 #pragma once
@@ -63,30 +64,57 @@ __device__ __forceinline__ double2 tail_diag(const TailArgs& a, int l, int i, do
   return D;
 }
 
-__global__ void __launch_bounds__(kTailThreads) k_tail1d(TailArgs a, const double2* __restrict__ bin,
-                                                         double2* __restrict__ xout) {
-  extern __shared__ __align__(16) double2 tsm[];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  // per level: x (current), y (ping-pong), b, r
-  auto X = [&](int l, int k) { return tsm + a.off[l] + k * a.n[l]; };
-  int cur[kTailLevels];  // which of X(l, 0) / X(l, 1) holds the iterate
-  const int last = a.nl - 1;
-  for (int i = tid; i < a.n[0]; i += nt) X(0, 2)[i] = bin[i];
+// banded LU solve in place (one thread), k_bandlu_solve's arithmetic
+__device__ __forceinline__ void tail_lu(double2* w, int n, const double2* Lf, const double2* Uf, const int* piv, int kl,
+                                         int ku) {
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < n; ++k) {
+      const int p = piv[k];
+      if (p != k) {
+        const double2 tmp = w[k];
+        w[k] = w[p];
+        w[p] = tmp;
+      }
+      const double2 wk = w[k];
+      for (int r = 1; r <= kl && k + r < n; ++r) w[k + r] = csub(w[k + r], cmul(Lf[(size_t)k * kl + r - 1], wk));
+    }
+    for (int k = n - 1; k >= 0; --k) {
+      double2 s = w[k];
+      for (int d = 1; d <= ku && k + d < n; ++d) s = csub(s, cmul(Uf[(size_t)k * (ku + 1) + d], w[k + d]));
+      w[k] = cdiv(s, Uf[(size_t)k * (ku + 1)]);
+    }
+  }
   __syncthreads();
-  // ---- down: smooth from zero, residual, restriction ----
+}
+
+// One V-cycle of the shifted hierarchy on the shared-memory levels (tail
+// layout: per level x, y, b, r).  The fine right-hand side is in level 0's b;
+// x_zero: the fine iterate starts from zero (else from level 0's current x,
+// *cur0 says which buffer).  Returns the fine iterate's buffer index in *cur0.
+__device__ void tail_vcycle(const TailArgs& a, double2* tsm, bool x_zero, int* cur0) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  auto X = [&](int l, int k) { return tsm + a.off[l] + k * a.n[l]; };
+  int cur[kTailLevels];
+  const int last = a.nl - 1;
   for (int l = 0; l < last; ++l) {
     const double2 corner = l == 0 ? a.corner : cmk(0.0, 0.0);
     const int n = a.n[l];
     double2* b = X(l, 2);
     double2* r = X(l, 3);
-    cur[l] = 0;
-    if (a.nu == 0) {
-      for (int i = tid; i < n; i += nt) X(l, 0)[i] = cmk(0.0, 0.0);
+    int s0 = 0;
+    if (l == 0 && !x_zero) {
+      cur[l] = *cur0;
     } else {
-      for (int i = tid; i < n; i += nt) X(l, 0)[i] = cscale(a.omega, cmul(cinv(tail_diag(a, l, i, corner)), b[i]));
+      cur[l] = 0;
+      if (a.nu == 0) {
+        for (int i = tid; i < n; i += nt) X(l, 0)[i] = cmk(0.0, 0.0);
+      } else {
+        for (int i = tid; i < n; i += nt) X(l, 0)[i] = cscale(a.omega, cmul(cinv(tail_diag(a, l, i, corner)), b[i]));
+        s0 = 1;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    for (int s = 1; s < a.nu; ++s) {
+    for (int s = s0; s < a.nu; ++s) {
       const double2* x = X(l, cur[l]);
       double2* y = X(l, cur[l] ^ 1);
       for (int i = tid; i < n; i += nt) {
@@ -101,7 +129,7 @@ __global__ void __launch_bounds__(kTailThreads) k_tail1d(TailArgs a, const doubl
     __syncthreads();
     const int nc = a.n[l + 1];
     double2* bc = X(l + 1, 2);
-    for (int q = tid; q < nc; q += nt) {  // linear restriction (1/2, 1, 1/2), out-of-range rows dropped
+    for (int q = tid; q < nc; q += nt) {
       double2 acc = cmk(0.0, 0.0);
       for (int o = 0; o < 3; ++o) {
         const int i = 2 * q + o;
@@ -111,39 +139,20 @@ __global__ void __launch_bounds__(kTailThreads) k_tail1d(TailArgs a, const doubl
     }
     __syncthreads();
   }
-  // ---- coarsest: banded LU with partial pivoting (one thread, as k_bandlu_solve) ----
-  {
+  {  // coarsest: banded LU
     const int n = a.n[last];
     double2* w = X(last, 0);
     cur[last] = 0;
-    if (tid == 0) {
-      const double2* bl = X(last, 2);
-      for (int i = 0; i < n; ++i) w[i] = bl[i];
-      for (int k = 0; k < n; ++k) {
-        const int p = a.piv[k];
-        if (p != k) {
-          const double2 tmp = w[k];
-          w[k] = w[p];
-          w[p] = tmp;
-        }
-        const double2 wk = w[k];
-        for (int r = 1; r <= a.kl && k + r < n; ++r) w[k + r] = csub(w[k + r], cmul(a.Lf[(size_t)k * a.kl + r - 1], wk));
-      }
-      for (int k = n - 1; k >= 0; --k) {
-        double2 s = w[k];
-        for (int d = 1; d <= a.ku && k + d < n; ++d) s = csub(s, cmul(a.Uf[(size_t)k * (a.ku + 1) + d], w[k + d]));
-        w[k] = cdiv(s, a.Uf[(size_t)k * (a.ku + 1)]);
-      }
-    }
+    for (int i = tid; i < n; i += nt) w[i] = X(last, 2)[i];
     __syncthreads();
+    tail_lu(w, n, a.Lf, a.Uf, a.piv, a.kl, a.ku);
   }
-  // ---- up: prolongation, post-smoothing ----
   for (int l = last - 1; l >= 0; --l) {
     const double2 corner = l == 0 ? a.corner : cmk(0.0, 0.0);
     const int n = a.n[l], nc = a.n[l + 1];
     double2* x = X(l, cur[l]);
     const double2* e = X(l + 1, cur[l + 1]);
-    for (int i = tid; i < n; i += nt) {  // x += Z e (odd i: e[(i-1)/2]; even: (e[i/2-1] + e[i/2]) / 2)
+    for (int i = tid; i < n; i += nt) {
       double2 acc = cmk(0.0, 0.0);
       if (i & 1) {
         const int q = (i - 1) / 2;
@@ -167,8 +176,19 @@ __global__ void __launch_bounds__(kTailThreads) k_tail1d(TailArgs a, const doubl
       __syncthreads();
     }
   }
-  const double2* x0 = X(0, cur[0]);
-  for (int i = tid; i < a.n[0]; i += nt) xout[i] = x0[i];
+  *cur0 = cur[0];
+}
+
+__global__ void __launch_bounds__(kTailThreads) k_tail1d(TailArgs a, const double2* __restrict__ bin,
+                                                         double2* __restrict__ xout) {
+  extern __shared__ __align__(16) double2 tsm[];
+  double2* b0 = tsm + a.off[0] + 2 * a.n[0];
+  for (int i = threadIdx.x; i < a.n[0]; i += blockDim.x) b0[i] = bin[i];
+  __syncthreads();
+  int cur0 = 0;
+  tail_vcycle(a, tsm, true, &cur0);
+  const double2* x0 = tsm + a.off[0] + cur0 * a.n[0];
+  for (int i = threadIdx.x; i < a.n[0]; i += blockDim.x) xout[i] = x0[i];
 }
 
 }  // namespace hd
