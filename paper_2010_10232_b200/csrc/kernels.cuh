@@ -537,47 +537,57 @@ __global__ void k_fold_rows(const double* __restrict__ X, double* __restrict__ F
   }
 }
 
-// Hh[yb][xb][p](kx, j) = G_xb(kx, p n + j) +- G_xb(kx, p n + n-1-j)
+// Hh[yb] is col-major (4 n2) x n2, ld 4 n2: row q n2 + kx (q = 2 xb + p), column j,
+// so each y transform is one (4 n2) x n2 x n2 GEMM per y parity.
+__device__ __forceinline__ size_t fold_idx(int yb, int xb, int p, int kx, int j, int n2) {
+  const size_t nn = (size_t)n2 * n2;
+  return (size_t)yb * 4 * nn + (size_t)j * 4 * n2 + (size_t)(2 * xb + p) * n2 + kx;
+}
+
+// Hh[yb](q n2 + kx, j) = G_xb(kx, p n + j) +- G_xb(kx, p n + n-1-j)
 __global__ void k_fold_cols(const double* __restrict__ G, double* __restrict__ Hh, int n, int n2) {
   const size_t nn = (size_t)n2 * n2;
   const size_t tot = 4 * nn;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
     const int kx = (int)(g % n2);
-    const int j = (int)((g / n2) % n2);
-    const int p = (int)((g / nn) % 2);
-    const int xb = (int)(g / (2 * nn));
+    const int q = (int)((g / n2) % 4);
+    const int j = (int)(g / (4 * (size_t)n2));
+    const int xb = q >> 1, p = q & 1;
     const double* Gx = G + (size_t)xb * n2 * 2 * n;
     const double a = Gx[((size_t)p * n + j) * n2 + kx], b = Gx[((size_t)p * n + (n - 1 - j)) * n2 + kx];
-    Hh[((size_t)(0 * 2 + xb) * 2 + p) * nn + (size_t)j * n2 + kx] = a + b;
-    Hh[((size_t)(1 * 2 + xb) * 2 + p) * nn + (size_t)j * n2 + kx] = a - b;
+    Hh[fold_idx(0, xb, p, kx, j, n2)] = a + b;
+    Hh[fold_idx(1, xb, p, kx, j, n2)] = a - b;
   }
 }
 
-// R[yb][xb][p](kx, ky): (R_p0 + i R_p1) *= D[yb][xb][ky][kx]
+// R[yb](q n2 + kx, ky), q = 2 xb + p: (R_p0 + i R_p1) *= D[yb][xb][ky][kx]
 __global__ void k_scale_folded(double* __restrict__ R, const double2* __restrict__ D, int n2) {
   const size_t nn = (size_t)n2 * n2;
   const size_t tot = 4 * nn;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
-    const size_t blk = g / nn, e = g % nn;  // e = ky * n2 + kx (col-major (kx, ky))
-    double* r0 = R + (blk * 2 + 0) * nn + e;
-    double* r1 = R + (blk * 2 + 1) * nn + e;
-    const double2 v = cmul(cmk(*r0, *r1), D[g]);
+    const int kx = (int)(g % n2);
+    const int xb = (int)((g / n2) % 2);
+    const int ky = (int)((g / (2 * (size_t)n2)) % n2);
+    const int yb = (int)(g / (2 * nn));
+    double* r0 = R + fold_idx(yb, xb, 0, kx, ky, n2);
+    double* r1 = R + fold_idx(yb, xb, 1, kx, ky, n2);
+    const double2 v = cmul(cmk(*r0, *r1), D[(((size_t)yb * 2 + xb) * n2 + ky) * n2 + kx]);
     *r0 = v.x;
     *r1 = v.y;
   }
 }
 
-// S[yb][xb][p](kx, j) -> Z_xb(kx, p n + j) = S_s + S_a, Z_xb(kx, p n + n-1-j) = S_s - S_a
+// S[yb](q n2 + kx, j) -> Z_xb(kx, p n + j) = S_s + S_a, Z_xb(kx, p n + n-1-j) = S_s - S_a
 __global__ void k_unfold_cols(const double* __restrict__ S, double* __restrict__ Z, int n, int n2) {
   const size_t nn = (size_t)n2 * n2;
   const size_t tot = 4 * nn;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
     const int kx = (int)(g % n2);
-    const int j = (int)((g / n2) % n2);
-    const int p = (int)((g / nn) % 2);
-    const int xb = (int)(g / (2 * nn));
-    const double ss = S[((size_t)(0 * 2 + xb) * 2 + p) * nn + (size_t)j * n2 + kx];
-    const double sa = S[((size_t)(1 * 2 + xb) * 2 + p) * nn + (size_t)j * n2 + kx];
+    const int q = (int)((g / n2) % 4);
+    const int j = (int)(g / (4 * (size_t)n2));
+    const int xb = q >> 1, p = q & 1;
+    const double ss = S[fold_idx(0, xb, p, kx, j, n2)];
+    const double sa = S[fold_idx(1, xb, p, kx, j, n2)];
     double* Zx = Z + (size_t)xb * n2 * 2 * n;
     Zx[((size_t)p * n + j) * n2 + kx] = ss + sa;
     Zx[((size_t)p * n + (n - 1 - j)) * n2 + kx] = ss - sa;

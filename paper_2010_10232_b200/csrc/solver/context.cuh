@@ -284,7 +284,8 @@ static bool centro_symmetric(const Band& X) {
       mx = std::max(mx, std::abs(X.at(i, j)));
       dev = std::max(dev, std::abs(X.at(i, j) - X.at(X.n - 1 - i, X.n - 1 - j)));
     }
-  return dev <= 1e-13 * mx;
+  static const double tol = std::getenv("HD_CENTRO_TOL") ? std::atof(std::getenv("HD_CENTRO_TOL")) : 1e-12;
+  return dev <= tol * mx;
 }
 
 // Reflection-folded fast diagonalisation: for even n and centro-symmetric

@@ -359,21 +359,17 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
                                   &zero, X.G, n2, hc, 2));
     launched(c, HD_K_LIBGEMM, mk, gb, true);
     HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_cols<<<grid_for(4 * nn), 256, 0, c->st>>>(X.G, X.Hh, n, n2));
-    // y transform: R[yb] = Hh[yb] Vt_yb (batch over x parity and plane)
-    for (int yb = 0; yb < 2; ++yb) {
-      mk = prof_mark(c);
-      CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n2, n2, n2, &one, X.Hh + yb * 4 * nn, n2, nn,
-                                    X.Vt + yb * nn, n2, 0, &zero, X.R + yb * 4 * nn, n2, nn, 4));
-      launched(c, HD_K_LIBGEMM, mk, gb, true);
-    }
+    // y transform: R[yb] = Hh[yb] Vt_yb, Hh[yb] (4 n2) x n2 (x parity and plane stacked), batch over yb
+    mk = prof_mark(c);
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, 4 * n2, n2, n2, &one, X.Hh, 4 * n2, 4 * nn, X.Vt,
+                                  n2, nn, &zero, X.R, 4 * n2, 4 * nn, 2));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
     HD_LAUNCH(HD_K_EXACT, 48.0 * 4 * nn, k_scale_folded<<<grid_for(4 * nn), 256, 0, c->st>>>(X.R, X.Dinvf, n2));
     // inverse y: S[yb] = R[yb] Vt_yb^T  (into Hh)
-    for (int yb = 0; yb < 2; ++yb) {
-      mk = prof_mark(c);
-      CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, n2, n2, n2, &one, X.R + yb * 4 * nn, n2, nn,
-                                    X.Vt + yb * nn, n2, 0, &zero, X.Hh + yb * 4 * nn, n2, nn, 4));
-      launched(c, HD_K_LIBGEMM, mk, gb, true);
-    }
+    mk = prof_mark(c);
+    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, 4 * n2, n2, n2, &one, X.R, 4 * n2, 4 * nn, X.Vt,
+                                  n2, nn, &zero, X.Hh, 4 * n2, 4 * nn, 2));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
     HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_cols<<<grid_for(4 * nn), 256, 0, c->st>>>(X.Hh, X.F, n, n2));
     // inverse x: Yh_b = Vt_b Z_b  (Z in F, result in G)
     mk = prof_mark(c);
@@ -498,11 +494,14 @@ static void shift_exact_solve(hd_ctx* c, const double2* b, double2* out) {
   }
 }
 
-static void mg_solve(hd_ctx* c, const double2* b, double2* out) {
+// MG^-1 b (Multigrid::solve, src/precond.cpp:159-163).  Returns the buffer that
+// holds the result: `out` for C_ex, else the level-0 iterate buffer (mg_x[0] or
+// mg_y[0]), valid until the next multigrid application.
+static const double2* mg_solve_ptr(hd_ctx* c, const double2* b, double2* out) {
   const size_t N = c->N;
   if (c->spec.cycles <= 0) {
     shift_exact_solve(c, b, out);
-    return;
+    return out;
   }
   bool zero = true;
   double2* xb = nullptr;
@@ -529,12 +528,14 @@ static void mg_solve(hd_ctx* c, const double2* b, double2* out) {
     }
     zero = false;
   }
-  if (c->spec.cycles <= 0) {
-    CK(cudaMemsetAsync(out, 0, N * sizeof(double2), c->st));
-    return;
-  }
-  CK(cudaMemcpyAsync(out, xb, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+  return xb;
 }
+
+static void mg_solve(hd_ctx* c, const double2* b, double2* out) {
+  const double2* r = mg_solve_ptr(c, b, out);
+  if (r != out) CK(cudaMemcpyAsync(out, r, c->N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+}
+
 
 static LevelDev opA(hd_ctx* c) { return level_dev(c->fine, c->cA, c->corner, c->fine.genA); }
 
@@ -563,8 +564,7 @@ static void compose_op(hd_ctx* c, const double2* v, double2* out, const int* vid
   if (c->spec.shift) {
     ++c->shift_solves;
     c->vcycles += c->spec.cycles;
-    mg_solve(c, c->t1, c->t2);
-    cur = c->t2;
+    cur = mg_solve_ptr(c, c->t1, c->t2);  // no copy: project reads it before the next V-cycle
   }
   if (c->spec.deflate) {
     ++c->coarse_solves;
