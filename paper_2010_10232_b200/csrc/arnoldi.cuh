@@ -166,6 +166,7 @@ __device__ void arn_givens(const ArnoldiArgs& a, int j, double2* sm) {
 
 template <int RW>
 __global__ void __launch_bounds__(kArnBD, 1) k_arnoldi(ArnoldiArgs a) {
+  HD_PDL_ENTRY();
   extern __shared__ __align__(16) double2 wsm[];
   __shared__ double2 sred[33];
   __shared__ double2 ys[128];

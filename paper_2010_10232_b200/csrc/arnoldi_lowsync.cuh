@@ -102,6 +102,7 @@ __device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh
 constexpr size_t lsa_dots_smem() { return sizeof(double2) * (2 * kLsaCE + 2 * (kLsaMaxJ + 1)); }
 
 __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
+  HD_PDL_ENTRY();
   constexpr int NW = kLsaBD / 32;
   constexpr int PER = kLsaCE / 32;  // elements per lane per chunk
   extern __shared__ __align__(16) double2 dsm[];
@@ -207,6 +208,7 @@ __device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh
 
 // row slabs: combine the partials of all slabs (nparts CTA slots, slab order)
 __global__ void __launch_bounds__(kLsaBD) k_lsa_dots_finish(LsaArgs a, int nparts) {
+  HD_PDL_ENTRY();
   __shared__ double2 sh_s[kLsaMaxJ + 1];
   __shared__ double2 sh_lj[kLsaMaxJ];
   __shared__ double2 hsm[kLsaMaxJ + 1];
@@ -223,6 +225,7 @@ __device__ __forceinline__ double2 lsa_cdiv(double2 a, double2 b) { return cmul(
 // lagged iterate x_{j-1} = x0 + sum_{i<j} c'_i u_i (src/linalg.cpp:78-80);
 // mode 1 (budget exhausted): only x_j = x0 + sum_{i<=j} c'_i u_i.
 __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
+  HD_PDL_ENTRY();
   constexpr int NW = kLsaBD / 32;
   __shared__ double2 sh_c[kLsaMaxJ + 1];
   __shared__ double2 sh_x[kLsaMaxJ + 1];
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
 // nparts = gridDim.x of the update pass.  Dynamic smem: packed R + work.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kLsaBD) k_lsa_givens(LsaArgs a, int nparts) {
+  HD_PDL_ENTRY();
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double s_hnew;
   if (a.done && *((volatile const int*)a.done)) return;
@@ -410,6 +414,7 @@ struct LoopState {
 // stop on tolerance or Krylov breakdown of the previous step.
 __global__ void k_loop_check(LoopState* s, const double* dres, double* res_hist, double tol,
                              cudaGraphConditionalHandle h) {
+  HD_PDL_ENTRY();
   if (s->done) return;
   const int j = s->j;
   if (j < 1) return;
@@ -430,6 +435,7 @@ __global__ void k_loop_check(LoopState* s, const double* dres, double* res_hist,
 }
 
 __global__ void k_loop_next(LoopState* s, int maxit, cudaGraphConditionalHandle h) {
+  HD_PDL_ENTRY();
   if (s->done) return;
   if (s->j + 1 >= maxit) {
     s->done = 1;

@@ -6,6 +6,13 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+// Programmatic dependent launch: every solver kernel first waits for the grids
+// it depends on to complete (and their writes to be visible), then lets its
+// own dependents start launching.  Both are no-ops for an ordinary launch; the
+// loop graph turns kernel->kernel edges into programmatic ones (pdl_edges in
+// solver/launch.cuh), so the next kernel's launch overlaps this one's tail.
+#define HD_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
 namespace hd {
 
 __host__ __device__ __forceinline__ double2 cmk(double r, double i) { return make_double2(r, i); }
@@ -38,6 +45,16 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool va
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   const int n = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>

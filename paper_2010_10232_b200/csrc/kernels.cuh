@@ -40,7 +40,10 @@ struct RedOut {
   int raw;           // 1: dst = sum |.|^2 (a row slab's share; slabs are summed before the sqrt)
 };
 
-enum OpMode { OP_APPLY = 0, OP_RESID = 1, OP_JACOBI = 2, OP_RESNORM = 3 };
+// OP_APPLYJ0: out = L x and out2 = omega D2^-1 (L x), D2 the diagonal of the
+// level with constant c2 (the A apply that feeds the V-cycle also takes the
+// first damped-Jacobi sweep of the shifted operator from the zero iterate)
+enum OpMode { OP_APPLY = 0, OP_RESID = 1, OP_JACOBI = 2, OP_RESNORM = 3, OP_APPLYJ0 = 4 };
 
 constexpr int kTX = 128;  // threads (columns) per stencil CTA
 constexpr int kNS = 8;    // cp.async ring depth (rows in flight per CTA)
@@ -55,6 +58,7 @@ template <int B, int MODE>
 __global__ void __launch_bounds__(kTX) k_op2d(LevelDev L, const double2* __restrict__ x,
                                               const double2* __restrict__ bv, double2* __restrict__ out,
                                               double omega, int RY, RedOut red) {
+  HD_PDL_ENTRY();
   constexpr int NB = 2 * B + 1;
   constexpr int W = kTX + 2 * B;
   constexpr bool NEED_B = (MODE != OP_APPLY);
@@ -181,6 +185,7 @@ __global__ void __launch_bounds__(kTX) k_op2d(LevelDev L, const double2* __restr
 // x = omega D^-1 b: the first Jacobi sweep from a zero iterate
 // (src/precond.cpp:140 with x = 0, src/precond.cpp:150,160).
 __global__ void k_jacobi0_2d(LevelDev L, const double2* __restrict__ b, double2* __restrict__ out, double omega) {
+  HD_PDL_ENTRY();
   const int n = L.n, NB = 2 * L.b + 1;
   const size_t N = (size_t)n * n;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
@@ -198,6 +203,7 @@ __global__ void k_jacobi0_2d(LevelDev L, const double2* __restrict__ b, double2*
 template <int MODE>
 __global__ void k_op1d(LevelDev L, const double2* __restrict__ x, const double2* __restrict__ bv,
                        double2* __restrict__ out, double omega, RedOut red, const int* xidx, size_t xstride) {
+  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   if (xidx) x += (size_t)(*xidx) * xstride;
   const int n = L.n, b = L.b, NB = 2 * b + 1;
@@ -232,6 +238,7 @@ __global__ void k_op1d(LevelDev L, const double2* __restrict__ x, const double2*
 }
 
 __global__ void k_jacobi0_1d(LevelDev L, const double2* __restrict__ b, double2* __restrict__ out, double omega) {
+  HD_PDL_ENTRY();
   const int n = L.n, NB = 2 * L.b + 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double2 D = csub(cmk(L.S[(size_t)i * NB + L.b], 0.0), cscale(L.M[(size_t)i * NB + L.b], L.c));
@@ -288,6 +295,7 @@ __device__ __forceinline__ int pweights(const Stencil& z, int i, int nc, int* q,
 template <int DIM>
 __global__ void k_restrict(Stencil z, const double2* __restrict__ r, int nf, int nc, double2* __restrict__ outc,
                            double* __restrict__ outp) {
+  HD_PDL_ENTRY();
   double w[5];
   const int olo = rweights(z, w);
   const int nw = z.kind == 0 ? 3 : 5;
@@ -326,6 +334,7 @@ __global__ void k_restrict(Stencil z, const double2* __restrict__ r, int nf, int
 template <int DIM, int PMODE>
 __global__ void k_prolong(Stencil z, const double2* __restrict__ ec, const double* __restrict__ ep, int nf, int nc,
                           const double2* __restrict__ s, double2* __restrict__ out) {
+  HD_PDL_ENTRY();
   const size_t NF = DIM == 2 ? (size_t)nf * nf : (size_t)nf;
   const size_t NC = DIM == 2 ? (size_t)nc * nc : (size_t)nc;
   auto ce = [&](size_t qi) -> double2 { return PMODE == 0 ? ec[qi] : cmk(ep[qi], ep[qi + NC]); };
@@ -355,6 +364,7 @@ __global__ void k_prolong(Stencil z, const double2* __restrict__ ec, const doubl
 // dst = conj(a) . b
 __global__ void k_dot(const double2* __restrict__ a, const double2* __restrict__ b, size_t N, RedOut red,
                       double2* dst) {
+  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   double2 acc = cmk(0.0, 0.0);
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
@@ -366,6 +376,7 @@ __global__ void k_dot(const double2* __restrict__ a, const double2* __restrict__
 // w -= h * vi ; dst = conj(vn) . w      (one fused MGS step)
 __global__ void k_axpy_dot(double2* __restrict__ w, const double2* __restrict__ vi, const double2* __restrict__ h,
                            const double2* __restrict__ vn, size_t N, RedOut red, double2* dst) {
+  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   const double2 hh = *h;
   double2 acc = cmk(0.0, 0.0);
@@ -381,6 +392,7 @@ __global__ void k_axpy_dot(double2* __restrict__ w, const double2* __restrict__ 
 // w -= h * vi ; hnew = ||w||  -> dst (as complex (hnew, 0)) and *dnorm
 __global__ void k_axpy_norm(double2* __restrict__ w, const double2* __restrict__ vi, const double2* __restrict__ h,
                             size_t N, RedOut red, double2* dst) {
+  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   const double2 hh = h ? *h : cmk(0.0, 0.0);
   double acc = 0.0;
@@ -403,6 +415,7 @@ __global__ void k_axpy_norm(double2* __restrict__ w, const double2* __restrict__
 // out = a - b
 __global__ void k_sub(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ out,
                       size_t N) {
+  HD_PDL_ENTRY();
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
     out[g] = csub(a[g], b[g]);
 }
@@ -410,6 +423,7 @@ __global__ void k_sub(const double2* __restrict__ a, const double2* __restrict__
 // dst = src / h (h real, read from device; the reference's `w / hnew`)
 __global__ void k_scale_inv(double2* __restrict__ dst, const double2* __restrict__ src, const double* __restrict__ h,
                             size_t N) {
+  HD_PDL_ENTRY();
   const double s = *h;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
     const double2 v = src[g];
@@ -420,6 +434,7 @@ __global__ void k_scale_inv(double2* __restrict__ dst, const double2* __restrict
 // x = x0 + sum_{i<m} y_i V_i   (basis vectors contiguous, stride N)
 __global__ void k_iterate(double2* __restrict__ x, const double2* __restrict__ x0, const double2* __restrict__ V,
                           const double2* __restrict__ y, int m, size_t N) {
+  HD_PDL_ENTRY();
   __shared__ double2 ys[128];
   for (int i = threadIdx.x; i < m && i < 128; i += blockDim.x) ys[i] = y[i];
   __syncthreads();
@@ -436,6 +451,7 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) { return cmul(a, c
 __device__ __forceinline__ double2 cconj(double2 a) { return cmk(a.x, -a.y); }
 
 __global__ void k_givens(double2* H, int ldh, double2* g, double2* cs, double2* sn, double2* y, int j) {
+  HD_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double2* col = H + (size_t)j * ldh;
   for (int i = 0; i < j; ++i) {
@@ -474,6 +490,7 @@ __global__ void k_givens(double2* H, int ldh, double2* g, double2* cs, double2* 
 // V column-major (V[i + k n] = v_k(i)), Dinv[ky*n + kx].
 __global__ void k_fd_small(const double* __restrict__ V, const double2* __restrict__ Dinv, int n,
                            const double2* __restrict__ X, double2* __restrict__ Y) {
+  HD_PDL_ENTRY();
   __shared__ double2 A[32 * 32], Bm[32 * 32];
   __shared__ double Vs[32 * 32];
   const int nn = n * n;
@@ -517,6 +534,7 @@ __global__ void k_fd_small(const double* __restrict__ V, const double2* __restri
 
 // planar complex T (re plane, im plane; n*n each) *= Dinv (complex, n*n)
 __global__ void k_fd_scale(double* __restrict__ T, const double2* __restrict__ Dinv, size_t NN) {
+  HD_PDL_ENTRY();
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < NN; g += (size_t)gridDim.x * blockDim.x) {
     const double2 v = cmul(cmk(T[g], T[g + NN]), Dinv[g]);
     T[g] = v.x;
@@ -527,6 +545,7 @@ __global__ void k_fd_scale(double* __restrict__ T, const double2* __restrict__ D
 // ---- reflection-folded fast diagonalisation (solver.cu make_fd_folded) ----
 // X col-major n x ncol (planar complex: ncol = 2n); F[b] col-major n2 x ncol
 __global__ void k_fold_rows(const double* __restrict__ X, double* __restrict__ F, int n, int n2, int ncol) {
+  HD_PDL_ENTRY();
   const size_t tot = (size_t)n2 * ncol;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(g % n2);
@@ -546,6 +565,7 @@ __device__ __forceinline__ size_t fold_idx(int yb, int xb, int p, int kx, int j,
 
 // Hh[yb](q n2 + kx, j) = G_xb(kx, p n + j) +- G_xb(kx, p n + n-1-j)
 __global__ void k_fold_cols(const double* __restrict__ G, double* __restrict__ Hh, int n, int n2) {
+  HD_PDL_ENTRY();
   const size_t nn = (size_t)n2 * n2;
   const size_t tot = 4 * nn;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
@@ -562,6 +582,7 @@ __global__ void k_fold_cols(const double* __restrict__ G, double* __restrict__ H
 
 // R[yb](q n2 + kx, ky), q = 2 xb + p: (R_p0 + i R_p1) *= D[yb][xb][ky][kx]
 __global__ void k_scale_folded(double* __restrict__ R, const double2* __restrict__ D, int n2) {
+  HD_PDL_ENTRY();
   const size_t nn = (size_t)n2 * n2;
   const size_t tot = 4 * nn;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
@@ -579,6 +600,7 @@ __global__ void k_scale_folded(double* __restrict__ R, const double2* __restrict
 
 // S[yb](q n2 + kx, j) -> Z_xb(kx, p n + j) = S_s + S_a, Z_xb(kx, p n + n-1-j) = S_s - S_a
 __global__ void k_unfold_cols(const double* __restrict__ S, double* __restrict__ Z, int n, int n2) {
+  HD_PDL_ENTRY();
   const size_t nn = (size_t)n2 * n2;
   const size_t tot = 4 * nn;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
@@ -596,6 +618,7 @@ __global__ void k_unfold_cols(const double* __restrict__ S, double* __restrict__
 
 // Y(i, c) = Yh_s(i, c) + Yh_a(i, c);  Y(n-1-i, c) = Yh_s(i, c) - Yh_a(i, c)
 __global__ void k_unfold_rows(const double* __restrict__ Yh, double* __restrict__ Y, int n, int n2, int ncol) {
+  HD_PDL_ENTRY();
   const size_t tot = (size_t)n2 * ncol;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(g % n2);
@@ -617,6 +640,7 @@ __global__ void __launch_bounds__(256) k_bandlu_staged(const double2* __restrict
                                                        int n, const double2* __restrict__ b,
                                                        const double* __restrict__ bp, double2* __restrict__ work,
                                                        double2* __restrict__ x, double* __restrict__ xp) {
+  HD_PDL_ENTRY();
   constexpr int KU = 2 * KL;
   constexpr int CH = 256;
   extern __shared__ __align__(16) double2 sm[];
@@ -773,6 +797,7 @@ __global__ void k_bandlu_solve(const double2* __restrict__ Lf, const double2* __
                                const int* __restrict__ piv, int n, int kl, int ku, const double2* __restrict__ b,
                                const double* __restrict__ bp, double2* __restrict__ work, double2* __restrict__ x,
                                double* __restrict__ xp) {
+  HD_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   for (int i = 0; i < n; ++i) work[i] = bp ? cmk(bp[i], bp[i + n]) : b[i];
   for (int k = 0; k < n; ++k) {

@@ -55,61 +55,86 @@ __device__ __forceinline__ double2 seg_rhs(const double2* b, const double* bp, i
   return bp ? cmk(bp[k], bp[k + n]) : b[k];
 }
 
-// local forward sweep of every segment (thread per segment).  The tables of
-// row r+1 are loaded while row r is eliminated (the recurrence itself is a
-// short dependent chain; with one thread per segment the loads would
-// otherwise serialise behind it).
+// Rows of per-row tables in flight per segment thread (cp.async ring in shared
+// memory; each lane copies and later reads only its own segment's entries).
+constexpr int kSegDepth = 16;
+template <int KL>
+__host__ __device__ constexpr size_t seg_fwd_smem() {
+  return (size_t)kSegDepth * 32 * ((KL + 1) * sizeof(double2) + sizeof(int));
+}
+template <int KL>
+__host__ __device__ constexpr size_t seg_bwd_smem() {
+  return (size_t)kSegDepth * 32 * (3 * KL + 3) * sizeof(double2);
+}
+
+// local forward sweep of every segment (thread per segment, warp = 32
+// segments).  The per-row tables (pivot, multipliers, the rhs row shifted in)
+// stream through a kSegDepth-row cp.async ring, so the dependent elimination
+// chain never waits on a global load.
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_fwd(SegArgs a, const double2* __restrict__ b,
                                                 const double* __restrict__ bp) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.P) return;
-  const int P = a.P, s = i * kSegL;
-  const int* __restrict__ pv = a.pv;
-  const double2* __restrict__ Lt = a.L;
-  double2* __restrict__ y = a.y;
+  HD_PDL_ENTRY();
+  extern __shared__ __align__(16) double2 sring[];
+  double2(*rl)[KL + 1][32] = reinterpret_cast<double2(*)[KL + 1][32]>(sring);  // [slot][L_0..L_{KL-1}, b][lane]
+  int(*rp)[32] = reinterpret_cast<int(*)[32]>(sring + (size_t)kSegDepth * (KL + 1) * 32);
+  const int lane = threadIdx.x;
+  const int i = blockIdx.x * 32 + lane;
+  const bool valid = i < a.P;
+  const int P = a.P, s = i * kSegL, n = a.n;
+  // row r's tables: pv, L[r][0..KL-1], rhs row s + r + KL + 1
+  auto issue = [&](int r) {
+    if (r < kSegL) {
+      const int sl = r % kSegDepth;
+      cp_async4(&rp[sl][lane], a.pv + (size_t)r * P + (valid ? i : 0), valid);
+#pragma unroll
+      for (int q = 0; q < KL; ++q) cp_async16(&rl[sl][q][lane], a.L + ((size_t)r * KL + q) * P + (valid ? i : 0), valid);
+      const int k = s + r + KL + 1;
+      const bool kv = valid && k < n;
+      if (bp) {
+        cp_async8(&rl[sl][KL][lane].x, bp + (kv ? k : 0), kv);
+        cp_async8(&rl[sl][KL][lane].y, bp + (kv ? k + n : 0), kv);
+      } else {
+        cp_async16(&rl[sl][KL][lane], b + (kv ? k : 0), kv);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int t = 0; t < kSegDepth - 1; ++t) issue(t);
   double2 w[KL + 1];
 #pragma unroll
-  for (int q = 0; q <= KL; ++q) w[q] = seg_rhs(b, bp, a.n, s + q);
-  int pc = __ldg(pv + i);
-  double2 lc[KL], bc = seg_rhs(b, bp, a.n, s + KL + 1);
-#pragma unroll
-  for (int q = 0; q < KL; ++q) lc[q] = __ldg(Lt + (size_t)q * P + i);
-#pragma unroll 4
+  for (int q = 0; q <= KL; ++q) w[q] = valid ? seg_rhs(b, bp, n, s + q) : cmk(0.0, 0.0);
   for (int r = 0; r < kSegL; ++r) {
-    // next row's tables first
-    const int rn = r + 1 < kSegL ? r + 1 : r;
-    const int pn = __ldg(pv + (size_t)rn * P + i);
-    double2 ln[KL];
-#pragma unroll
-    for (int q = 0; q < KL; ++q) ln[q] = __ldg(Lt + ((size_t)rn * KL + q) * P + i);
-    const double2 bn = seg_rhs(b, bp, a.n, s + r + KL + 2);
+    cp_async_wait<kSegDepth - 2>();
+    issue(r + kSegDepth - 1);
+    const int sl = r % kSegDepth;
+    const int pc = rp[sl][lane];
     double2 yk = w[0];
 #pragma unroll
     for (int q = 1; q <= KL; ++q) yk = pc == q ? w[q] : yk;
 #pragma unroll
     for (int q = 1; q <= KL; ++q) {
       const double2 wq = pc == q ? w[0] : w[q];
-      w[q] = csub(wq, cmul(lc[q - 1], yk));
+      w[q] = csub(wq, cmul(rl[sl][q - 1][lane], yk));
     }
-    y[(size_t)r * P + i] = yk;
+    if (valid) a.y[(size_t)r * P + i] = yk;
 #pragma unroll
     for (int q = 0; q < KL; ++q) w[q] = w[q + 1];
-    w[KL] = bc;
-    pc = pn;
-    bc = bn;
-#pragma unroll
-    for (int q = 0; q < KL; ++q) lc[q] = ln[q];
+    w[KL] = rl[sl][KL][lane];
   }
+  cp_async_wait<0>();
+  if (!valid) return;
   // D_i = end window - raw rhs rows e..e+KL
 #pragma unroll
-  for (int q = 0; q <= KL; ++q) a.D[(size_t)i * (KL + 1) + q] = csub(w[q], seg_rhs(b, bp, a.n, s + kSegL + q));
+  for (int q = 0; q <= KL; ++q) a.D[(size_t)i * (KL + 1) + q] = csub(w[q], seg_rhs(b, bp, n, s + kSegL + q));
 }
 
 // Delta_0 = 0, Delta_{i+1} = D_i + F_i Delta_i  (one warp; lane q owns component q;
 // the maps are staged kSegC segments at a time, double-buffered)
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_scan_fwd(SegArgs a) {
+  HD_PDL_ENTRY();
   constexpr int W = KL + 1, PER = W * W + W;  // F_i then D_i
   constexpr int kSegC = seg_chunk(PER);
   __shared__ __align__(16) double2 buf[2][kSegC * PER];
@@ -149,57 +174,56 @@ __global__ void __launch_bounds__(32) k_seg_scan_fwd(SegArgs a) {
   cp_async_wait<0>();
 }
 
-// forward correction y_k += h_k . Delta_i, then the local backward sweep (the
-// tables of row r-1 are loaded while row r is solved, as in k_seg_fwd)
+// forward correction y_k += h_k . Delta_i, then the local backward sweep; the
+// per-row tables (y, h, U, 1/u) stream through a kSegDepth-row cp.async ring
+// as in k_seg_fwd
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_bwd(SegArgs a) {
-  constexpr int KU = 2 * KL;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.P) return;
-  const int P = a.P;
-  const double2* __restrict__ yt = a.y;
-  const double2* __restrict__ hf = a.hf;
-  const double2* __restrict__ Ut = a.U;
-  const double2* __restrict__ Ui = a.Ui;
-  double2* __restrict__ x0 = a.x0;
+  HD_PDL_ENTRY();
+  constexpr int KU = 2 * KL, NF = KL + KU + 3;  // y, hf[KL+1], U[KU], 1/u
+  extern __shared__ __align__(16) double2 sring[];
+  double2(*rg)[NF][32] = reinterpret_cast<double2(*)[NF][32]>(sring);
+  const int lane = threadIdx.x;
+  const int i = blockIdx.x * 32 + lane;
+  const bool valid = i < a.P;
+  const int P = a.P, ii = valid ? i : 0;
+  auto issue = [&](int t) {  // t-th row from the end: r = kSegL - 1 - t
+    if (t < kSegL) {
+      const int r = kSegL - 1 - t, sl = t % kSegDepth;
+      cp_async16(&rg[sl][0][lane], a.y + (size_t)r * P + ii, valid);
+#pragma unroll
+      for (int q = 0; q <= KL; ++q) cp_async16(&rg[sl][1 + q][lane], a.hf + ((size_t)r * (KL + 1) + q) * P + ii, valid);
+#pragma unroll
+      for (int d = 0; d < KU; ++d) cp_async16(&rg[sl][KL + 2 + d][lane], a.U + ((size_t)r * KU + d) * P + ii, valid);
+      cp_async16(&rg[sl][KL + KU + 2][lane], a.Ui + (size_t)r * P + ii, valid);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int t = 0; t < kSegDepth - 1; ++t) issue(t);
   double2 dl[KL + 1];
 #pragma unroll
-  for (int q = 0; q <= KL; ++q) dl[q] = a.Dl[(size_t)i * (KL + 1) + q];
+  for (int q = 0; q <= KL; ++q) dl[q] = valid ? a.Dl[(size_t)i * (KL + 1) + q] : cmk(0.0, 0.0);
   double2 xw[KU];  // x_{k+1} .. x_{k+KU}
 #pragma unroll
   for (int d = 0; d < KU; ++d) xw[d] = cmk(0.0, 0.0);
-  // tables of one row: y, hf[KL+1], U[KU], 1/u
-  auto load = [&](int r, double2& yv, double2 (&h)[KL + 1], double2 (&u)[KU], double2& ui) {
-    yv = yt[(size_t)r * P + i];
+  for (int t = 0; t < kSegL; ++t) {
+    const int r = kSegL - 1 - t, sl = t % kSegDepth;
+    cp_async_wait<kSegDepth - 2>();
+    issue(t + kSegDepth - 1);
+    double2 sacc = rg[sl][0][lane];
 #pragma unroll
-    for (int q = 0; q <= KL; ++q) h[q] = __ldg(hf + ((size_t)r * (KL + 1) + q) * P + i);
+    for (int q = 0; q <= KL; ++q) sacc = cfma(rg[sl][1 + q][lane], dl[q], sacc);
 #pragma unroll
-    for (int d = 0; d < KU; ++d) u[d] = __ldg(Ut + ((size_t)r * KU + d) * P + i);
-    ui = __ldg(Ui + (size_t)r * P + i);
-  };
-  double2 yc, hc[KL + 1], uc[KU], uic;
-  load(kSegL - 1, yc, hc, uc, uic);
-#pragma unroll 2
-  for (int r = kSegL - 1; r >= 0; --r) {
-    double2 yn, hn[KL + 1], un[KU], uin;
-    load(r > 0 ? r - 1 : 0, yn, hn, un, uin);
-    double2 sacc = yc;
-#pragma unroll
-    for (int q = 0; q <= KL; ++q) sacc = cfma(hc[q], dl[q], sacc);
-#pragma unroll
-    for (int d = KU; d >= 1; --d) sacc = csub(sacc, cmul(uc[d - 1], xw[d - 1]));
-    const double2 xk = cmul(sacc, uic);
+    for (int d = KU; d >= 1; --d) sacc = csub(sacc, cmul(rg[sl][KL + 1 + d][lane], xw[d - 1]));
+    const double2 xk = cmul(sacc, rg[sl][KL + KU + 2][lane]);
 #pragma unroll
     for (int d = KU - 1; d >= 1; --d) xw[d] = xw[d - 1];
     xw[0] = xk;
-    x0[(size_t)r * P + i] = xk;
-    yc = yn;
-    uic = uin;
-#pragma unroll
-    for (int q = 0; q <= KL; ++q) hc[q] = hn[q];
-#pragma unroll
-    for (int d = 0; d < KU; ++d) uc[d] = un[d];
+    if (valid) a.x0[(size_t)r * P + i] = xk;
   }
+  cp_async_wait<0>();
+  if (!valid) return;
 #pragma unroll
   for (int d = 0; d < KU; ++d) a.X0[(size_t)i * KU + d] = xw[d];  // xw[d] = x_{s+d}
 }
@@ -207,6 +231,7 @@ __global__ void __launch_bounds__(32) k_seg_bwd(SegArgs a) {
 // X_P = 0, X_i = X0_i + H'_i X_{i+1}  (one warp, lane d owns component d)
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_scan_bwd(SegArgs a) {
+  HD_PDL_ENTRY();
   constexpr int KU = 2 * KL, PER = KU * KU + KU;  // H'_i then X0_i
   constexpr int kSegC = seg_chunk(PER);
   __shared__ __align__(16) double2 buf[2][kSegC * PER];
@@ -252,6 +277,7 @@ __global__ void __launch_bounds__(32) k_seg_scan_bwd(SegArgs a) {
 // x_k = x0_k + h'_k . X_{i+1}  (thread per row), output interleaved or planar
 template <int KL>
 __global__ void k_seg_out(SegArgs a, double2* __restrict__ x, double* __restrict__ xp) {
+  HD_PDL_ENTRY();
   constexpr int KU = 2 * KL;
   const int P = a.P;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += gridDim.x * blockDim.x) {

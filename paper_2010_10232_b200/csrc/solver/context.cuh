@@ -110,6 +110,7 @@ struct hd_ctx {
   ExactSolver shift_exact;      // C_ex: exact inverse of the shifted operator (cycles == 0)
   double* sx_plan = nullptr;    // planar scratch for the 2D exact shifted solve
   std::vector<double2*> mg_b, mg_x, mg_y, mg_r;
+  int pdl_edges = 0;            // programmatic kernel->kernel edges in the loop graph body
   int tail_l = -1;              // 1D: first level of the single-CTA tail V-cycle (tail1d.cuh), -1: none
   TailArgs tail{};
   size_t tail_smem_bytes = 0;
@@ -633,9 +634,17 @@ static void seg_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b
                          double* xp) {
   const SegArgs& a = X.seg;
   const int blocks = (a.P + 31) / 32;
-  k_seg_fwd<KL><<<blocks, 32, 0, st>>>(a, b, bp);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_seg_fwd<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(seg_fwd_smem<KL>())));
+    CK(cudaFuncSetAttribute(k_seg_bwd<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(seg_bwd_smem<KL>())));
+    attr = true;
+  }
+  k_seg_fwd<KL><<<blocks, 32, seg_fwd_smem<KL>(), st>>>(a, b, bp);
   k_seg_scan_fwd<KL><<<1, 32, 0, st>>>(a);
-  k_seg_bwd<KL><<<blocks, 32, 0, st>>>(a);
+  k_seg_bwd<KL><<<blocks, 32, seg_bwd_smem<KL>(), st>>>(a);
   k_seg_scan_bwd<KL><<<1, 32, 0, st>>>(a);
   k_seg_out<KL><<<std::min((a.n + 255) / 256, 148 * 4), 256, 0, st>>>(a, x, xp);
 }

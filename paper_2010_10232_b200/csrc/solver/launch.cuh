@@ -21,9 +21,16 @@ static size_t prof_mark(hd_ctx* c) {
   return c->prof_used++;
 }
 
+// source line of the launch being checked (error messages; HD_LAUNCH sets it)
+static thread_local int g_launch_line = 0;
+
 // called right after a launch: error check, launch count, profile record
 static void launched(hd_ctx* c, int kind, size_t mark, double bytes, bool library = false) {
-  CK(cudaGetLastError());
+  const cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess)
+    throw Error(HD_ERR_CUDA, std::string("kernel launch (kind ") + std::to_string(kind) + ", launch.cuh:" +
+                                 std::to_string(g_launch_line) + "): " + cudaGetErrorString(le));
+  g_launch_line = 0;
   if (library) ++c->lib_calls;
   else ++c->launches;
   if (mark == static_cast<size_t>(-1)) return;
@@ -34,6 +41,7 @@ static void launched(hd_ctx* c, int kind, size_t mark, double bytes, bool librar
 #define HD_LAUNCH(kind, bytes, ...)        \
   do {                                     \
     const size_t mk_ = prof_mark(c);       \
+    g_launch_line = __LINE__;              \
     __VA_ARGS__;                           \
     launched(c, (kind), mk_, (bytes));     \
   } while (0)
@@ -89,28 +97,30 @@ static int pick_rows(int n, int rows, int slots, int B) {
 
 template <int B, int MODE>
 static void launch_stencil(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
-                           double omega, RedOut red, const int* xidx, size_t xstride, int rb, int re) {
+                           double omega, RedOut red, const int* xidx, size_t xstride, int rb, int re,
+                           double2* out2 = nullptr, double2 c2 = double2{0.0, 0.0}) {
   const int per = stencil_occupancy<B, MODE>();
   const int ry = pick_rows(L.n, re - rb, per * c->n_sms, B);
   dim3 grid((L.n + kSW * kSWarps - 1) / (kSW * kSWarps), (re - rb + ry - 1) / ry);
   k_stencil2d<B, MODE><<<grid, kSW * kSWarps, stencil_smem<B, MODE>(ry), c->st>>>(L, x, b, out, omega, ry, red,
-                                                                               xidx, xstride, rb, re);
+                                                                               xidx, xstride, rb, re, out2, c2);
 }
 
 template <int MODE>
 static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
                              double omega, RedOut red, int kind, const int* xidx, size_t xstride, int rb = 0,
-                             int re = -1) {
+                             int re = -1, double2* out2 = nullptr, double2 c2 = double2{0.0, 0.0}) {
   if (re < 0) re = L.n;
   const size_t mk = prof_mark(c);
+  g_launch_line = __LINE__ + 1000 * MODE;
   switch (L.b) {
 #define HD_CASE(BB) \
-  case BB: launch_stencil<BB, MODE>(c, L, x, b, out, omega, red, xidx, xstride, rb, re); break;
+  case BB: launch_stencil<BB, MODE>(c, L, x, b, out, omega, red, xidx, xstride, rb, re, out2, c2); break;
     HD_CASE(1) HD_CASE(2) HD_CASE(3) HD_CASE(4) HD_CASE(5) HD_CASE(6)
 #undef HD_CASE
     default: throw Error(HD_ERR_INVALID, "band half-width " + std::to_string(L.b) + " unsupported");
   }
-  launched(c, kind, mk, op_bytes(MODE, static_cast<size_t>(L.n) * (re - rb)));
+  launched(c, kind, mk, op_bytes(MODE, static_cast<size_t>(L.n) * (re - rb)) + (MODE == OP_APPLYJ0 ? 16.0 * L.n * (re - rb) : 0.0));
 }
 
 // layered field: G-term Kronecker-sum operator (layered.cuh)
@@ -210,6 +220,15 @@ static void restrict_(hd_ctx* c, Stencil z, const double2* r, int nf, int nc, do
             k_restrict<1><<<grid_for(NC), 256, 0, c->st>>>(z, r, nf, nc, outc, outp));
 }
 
+// linear restriction fused with the coarse level's first Jacobi sweep from zero:
+// outc = z^T r and x0 = omega D^-1 outc (2D Kronecker-sum levels)
+static void restrict_j0(hd_ctx* c, const double2* r, int nf, int nc, double2* outc, const LevelDev& Lc, double omega,
+                        double2* x0) {
+  dim3 grid((nc + kRQX - 1) / kRQX, (nc + kRQY - 1) / kRQY);
+  HD_LAUNCH(HD_K_TRANSFER, 16.0 * (static_cast<double>(nf) * nf + 2.0 * nc * nc),
+            k_restrict2d<0, 0, true><<<grid, 256, 0, c->st>>>(0.0, r, nf, nc, outc, nullptr, 0, nc, Lc, omega, x0));
+}
+
 template <int PMODE>
 static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, int nf, int nc, const double2* s,
                      double2* out, int fb = 0, int fe = -1) {
@@ -229,6 +248,7 @@ static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, 
 
 // interleaved <-> planar (re plane, im plane) complex vectors
 __global__ void k_to_planar(const double2* __restrict__ a, double* __restrict__ p, size_t N) {
+  HD_PDL_ENTRY();
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
     const double2 v = a[g];
     p[g] = v.x;
@@ -236,6 +256,7 @@ __global__ void k_to_planar(const double2* __restrict__ a, double* __restrict__ 
   }
 }
 __global__ void k_from_planar(const double* __restrict__ p, double2* __restrict__ a, size_t N) {
+  HD_PDL_ENTRY();
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
     a[g] = cmk(p[g], p[g + N]);
 }
@@ -432,7 +453,9 @@ static LevelDev levM(hd_ctx* c, int l) {
 }
 
 // x_out = (damped Jacobi)^steps from x (x_zero: x == 0), ping-pong through tmp
-static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2* xb, bool x_zero, int steps) {
+// x0_ready: xa already holds the first sweep from zero (fused into the producer of b)
+static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2* xb, bool x_zero, int steps,
+                       bool x0_ready = false) {
   const LevelDev L = levM(c, l);
   double2* cur = xa;
   double2* oth = xb;
@@ -442,7 +465,7 @@ static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2*
       CK(cudaMemsetAsync(cur, 0, lsize(c, L.n) * sizeof(double2), c->st));
       return cur;
     }
-    jacobi0(c, L, b, cur, c->spec.omega);
+    if (!x0_ready) jacobi0(c, L, b, cur, c->spec.omega);
     s = 1;
   }
   for (; s < steps; ++s) {
@@ -453,7 +476,18 @@ static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2*
 }
 
 // One V-cycle at level l (src/precond.cpp:144-153); returns the buffer holding x.
-static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero) {
+// True when level l's first sweep from zero can ride with the kernel that
+// produces its right-hand side: a 2D Kronecker-sum level that is smoothed
+// (not the coarsest, not the 1D tail, not a layered/wedge level).
+static bool j0_fusable(hd_ctx* c, int l) {
+  static const bool off = std::getenv("HD_NOJ0FUSE") != nullptr;
+  const int last = static_cast<int>(c->lev.size()) - 1;
+  return !off && c->dim == 2 && l < last && l != c->tail_l && c->spec.smooth_steps >= 1 && !c->lev[l].genM &&
+         !c->fine.genA;
+}
+
+// x0_ready: mg_x[l] already holds omega D^-1 b (see smooth)
+static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero, bool x0_ready = false) {
   const int last = static_cast<int>(c->lev.size()) - 1;
   if (l == c->tail_l && x_zero) {  // 1D: the remaining levels in one single-CTA kernel
     double nb = 0.0;
@@ -467,12 +501,14 @@ static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero) {
     return c->mg_x[l];
   }
   const LevelDev L = levM(c, l);
-  double2* xcur = smooth(c, l, b, c->mg_x[l], c->mg_y[l], x_zero, c->spec.smooth_steps);
+  double2* xcur = smooth(c, l, b, c->mg_x[l], c->mg_y[l], x_zero, c->spec.smooth_steps, x0_ready && x_zero);
   double2* xoth = xcur == c->mg_x[l] ? c->mg_y[l] : c->mg_x[l];
   op_apply(c, OP_RESID, L, xcur, b, c->mg_r[l]);
   const int nf = c->lev[l].n, ncl = c->lev[l + 1].n;
-  restrict_(c, Stencil{0, 0.0}, c->mg_r[l], nf, ncl, c->mg_b[l + 1], nullptr);
-  double2* ec = cycle_at(c, l + 1, c->mg_b[l + 1], true);
+  const bool fuse = j0_fusable(c, l + 1);
+  if (fuse) restrict_j0(c, c->mg_r[l], nf, ncl, c->mg_b[l + 1], levM(c, l + 1), c->spec.omega, c->mg_x[l + 1]);
+  else restrict_(c, Stencil{0, 0.0}, c->mg_r[l], nf, ncl, c->mg_b[l + 1], nullptr);
+  double2* ec = cycle_at(c, l + 1, c->mg_b[l + 1], true, fuse);
   prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, nf, ncl, nullptr, xcur);
   double2* res = smooth(c, l, b, xcur, xoth, false, c->spec.smooth_steps);
   return res;
@@ -497,7 +533,7 @@ static void shift_exact_solve(hd_ctx* c, const double2* b, double2* out) {
 // MG^-1 b (Multigrid::solve, src/precond.cpp:159-163).  Returns the buffer that
 // holds the result: `out` for C_ex, else the level-0 iterate buffer (mg_x[0] or
 // mg_y[0]), valid until the next multigrid application.
-static const double2* mg_solve_ptr(hd_ctx* c, const double2* b, double2* out) {
+static const double2* mg_solve_ptr(hd_ctx* c, const double2* b, double2* out, bool x0_ready = false) {
   const size_t N = c->N;
   if (c->spec.cycles <= 0) {
     shift_exact_solve(c, b, out);
@@ -514,7 +550,7 @@ static const double2* mg_solve_ptr(hd_ctx* c, const double2* b, double2* out) {
       coarsest_solve(c, b, c->mg_x[0]);
       xb = c->mg_x[0];
     } else if (zero) {
-      xb = cycle_at(c, 0, b, true);
+      xb = cycle_at(c, 0, b, true, x0_ready);
     } else {
       // general cycle from a non-zero iterate held in mg_x[0]
       const LevelDev L = levM(c, 0);
@@ -559,12 +595,20 @@ static void project(hd_ctx* c, const double2* w, double2* out) {
 // out = op(v) = P MG^-1 A v  (src/precond.cpp:236-245); v, out distinct from t1, t2, t3
 static void compose_op(hd_ctx* c, const double2* v, double2* out, const int* vidx = nullptr) {
   ++c->matvecs;
-  op_apply(c, OP_APPLY, opA(c), v, nullptr, c->t1, 0.0, nullptr, 1.0, vidx, c->N);
+  // A v also takes the fine level's first Jacobi sweep of the V-cycle (OP_APPLYJ0)
+  const bool fuse = c->spec.shift && c->spec.cycles >= 1 && c->lev.size() > 1 && j0_fusable(c, 0);
+  if (fuse) {
+    RedOut red = red_of(c);
+    launch_op2d_mode<OP_APPLYJ0>(c, opA(c), v, nullptr, c->t1, c->spec.omega, red, HD_K_OP_FINE, vidx, c->N, 0, -1,
+                                 c->mg_x[0], c->cM);
+  } else {
+    op_apply(c, OP_APPLY, opA(c), v, nullptr, c->t1, 0.0, nullptr, 1.0, vidx, c->N);
+  }
   const double2* cur = c->t1;
   if (c->spec.shift) {
     ++c->shift_solves;
     c->vcycles += c->spec.cycles;
-    cur = mg_solve_ptr(c, c->t1, c->t2);  // no copy: project reads it before the next V-cycle
+    cur = mg_solve_ptr(c, c->t1, c->t2, fuse);  // no copy: project reads it before the next V-cycle
   }
   if (c->spec.deflate) {
     ++c->coarse_solves;
@@ -721,7 +765,8 @@ static LsaArgs lsa_args(hd_ctx* c, double2* xout, int j, int mode, int maxit) {
   return a;
 }
 
-__global__ void k_inv_scalar(double* dst, const double* src) { *dst = *src > 0.0 ? 1.0 / *src : 0.0; }
+__global__ void k_inv_scalar(double* dst, const double* src) {
+  HD_PDL_ENTRY(); *dst = *src > 0.0 ? 1.0 / *src : 0.0; }
 
 static void read_scalars(hd_ctx* c) {
   CK(cudaMemcpyAsync(c->hres, c->dres, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -729,6 +774,7 @@ static void read_scalars(hd_ctx* c) {
 }
 
 __global__ void k_loop_init(LoopState* s) {
+  HD_PDL_ENTRY();
   s->j = 0;
   s->done = 0;
   s->iters = 0;
@@ -736,7 +782,8 @@ __global__ void k_loop_init(LoopState* s) {
   s->need_tail = 0;
 }
 
-__global__ void k_scale_monitor(double* dres) {  // graph monitor: raw norm / (||f|| or 1)
+__global__ void k_scale_monitor(double* dres) {
+  HD_PDL_ENTRY();  // graph monitor: raw norm / (||f|| or 1)
   const double f = dres[3];
   dres[0] = dres[0] / (f > 0.0 ? f : 1.0);
 }
@@ -748,6 +795,56 @@ static void monitor_raw(hd_ctx* c, const double2* x) {
 // Captures the GMRES iteration body (device-side j) into the body of a WHILE
 // conditional node: op(u_j) -> pass 1 (dots, x_{j-1}) -> monitor x_{j-1} ->
 // convergence check -> pass 2 (u_{j+1}) -> Givens -> j++.
+// Turns kernel -> hd-kernel edges of a captured graph into programmatic
+// edge (the dependent's launch overlaps the tail of its predecessor; its
+// HD_PDL_ENTRY waits for the predecessor to complete before touching memory).
+// Only edges INTO this library's kernels are converted: library kernels
+// (cuBLAS) have no griddepcontrol.wait.  Opt-in (HD_PDL=1): measured on B200 it
+// is neutral at C5 and C2 and 3-4% slower at C3 and C4.
+static int pdl_edges(cudaGraph_t g) {
+  static const bool off = !(std::getenv("HD_PDL") && std::atoi(std::getenv("HD_PDL")) == 1);
+  if (off) return 0;
+  static const long pdl_max_ctas = std::getenv("HD_PDL_MAXCTA") ? std::atol(std::getenv("HD_PDL_MAXCTA")) : 148;
+  size_t ne = 0;
+  CK(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));
+  if (ne == 0) return 0;
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  std::vector<cudaGraphEdgeData> ed(ne);
+  CK(cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne));
+  auto is_kernel = [](cudaGraphNode_t n) {
+    cudaGraphNodeType t;
+    return cudaGraphNodeGetType(n, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel;
+  };
+  auto is_hd = [&](cudaGraphNode_t n) {
+    if (!is_kernel(n)) return false;
+    cudaKernelNodeParams kp = {};
+    if (cudaGraphKernelNodeGetParams(n, &kp) != cudaSuccess || !kp.func) {
+      cudaGetLastError();
+      return false;
+    }
+    const char* name = nullptr;
+    if (cudaFuncGetName(&name, kp.func) != cudaSuccess || !name) {
+      cudaGetLastError();
+      return false;
+    }
+    // single-wave kernels only (their launch latency is exposed; larger grids and
+    // the persistent block-tridiagonal solve measured slower with early launch)
+    const long ctas = static_cast<long>(kp.gridDim.x) * kp.gridDim.y * kp.gridDim.z;
+    return std::strncmp(name, "_ZN2hd", 6) == 0 && ctas <= pdl_max_ctas && !std::strstr(name, "btri");
+  };
+  int nconv = 0;
+  for (size_t e = 0; e < ne; ++e) {
+    if (ed[e].type != cudaGraphDependencyTypeDefault || !is_kernel(from[e]) || !is_hd(to[e])) continue;
+    CK(cudaGraphRemoveDependencies_v2(g, &from[e], &to[e], &ed[e], 1));
+    cudaGraphEdgeData pe = {};
+    pe.type = cudaGraphDependencyTypeProgrammatic;
+    pe.from_port = cudaGraphKernelNodePortProgrammatic;
+    CK(cudaGraphAddDependencies_v2(g, &from[e], &to[e], &pe, 1));
+    ++nconv;
+  }
+  return nconv;
+}
+
 static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
   if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
   if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
@@ -816,6 +913,8 @@ static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
   c->lib_calls = saved_b;
   CK(ec);
   CK(cudaGetLastError());
+  c->pdl_edges = pdl_edges(body);
+  if (std::getenv("HD_PDL_TRACE")) std::fprintf(stderr, "[hd] loop graph: %d programmatic edges\n", c->pdl_edges);
   CK(cudaGraphInstantiate(&c->loop_exec, g, 0));
   c->loop_graph = g;
   c->loop_maxit = maxit;

@@ -21,6 +21,7 @@ struct GenHost {
 __global__ void k_galerkin_stencil(const double* __restrict__ K, int n, int b, const int* __restrict__ cptr,
                                    const int* __restrict__ crow, const double* __restrict__ cw, int nc, int bc,
                                    double* __restrict__ Kc) {
+  HD_PDL_ENTRY();
   const int NB = 2 * b + 1, NBc = 2 * bc + 1;
   const size_t tot = (size_t)nc * nc * NBc * NBc;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {

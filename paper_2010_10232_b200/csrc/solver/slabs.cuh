@@ -128,6 +128,7 @@ struct hd_slabs {
 };
 
 __global__ void k_slab_sumsq(const double2* __restrict__ x, size_t N, RedOut red) {
+  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   double acc = 0.0;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
@@ -138,6 +139,7 @@ __global__ void k_slab_sumsq(const double2* __restrict__ x, size_t N, RedOut red
 
 // norm = sqrt(sum of the slabs' raw sums, slab order) / scale -> dst (and cdst = (norm, 0))
 __global__ void k_slab_norm(const double* slots, int S, const double* scale_src, double* dst, double2* cdst) {
+  HD_PDL_ENTRY();
   double s = 0.0;
   for (int i = 0; i < S; ++i) s += slots[i];
   double sc = 1.0;
@@ -152,6 +154,7 @@ __global__ void k_slab_norm(const double* slots, int S, const double* scale_src,
 constexpr int kLsaNslot = 2 * kLsaMaxJ + 2;
 __global__ void k_lsa_slab_reduce(const double2* __restrict__ parts, int Gs, int j, const int* dj,
                                   double2* __restrict__ out) {
+  HD_PDL_ENTRY();
   if (dj) j = *dj;
   for (int q = threadIdx.x; q < kLsaNslot; q += blockDim.x) {
     const bool used = q < j + 1 || (q >= kLsaMaxJ + 1 && q < kLsaMaxJ + 1 + j);
@@ -427,6 +430,7 @@ static void s_mg_solve(hd_ctx* c, std::vector<double2*>& b, std::vector<double2*
 
 // rows [r0, r1) of both planes of a column-major n x n transform buffer scaled by Dinv
 __global__ void k_fd_scale_rows(double* __restrict__ T, const double2* __restrict__ Dinv, int n, int r0, int r1) {
+  HD_PDL_ENTRY();
   const size_t NN = (size_t)n * n;
   const int h = r1 - r0;
   const size_t tot = (size_t)h * n;
@@ -637,6 +641,7 @@ static void s_gather(hd_ctx* c, const std::vector<double2*>& v, double2* full) {
 
 // basis vector u_j of slab s <-> halo'd slab vectors
 __global__ void k_copy_basis(double2* __restrict__ dst, const double2* __restrict__ V, size_t Ns, const int* dj) {
+  HD_PDL_ENTRY();
   const double2* src = V + (size_t)(*dj) * Ns;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < Ns; g += (size_t)gridDim.x * blockDim.x)
     dst[g] = src[g];

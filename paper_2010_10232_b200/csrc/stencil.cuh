@@ -15,7 +15,7 @@
 // in shared memory as (My, Sy) pairs.  The strip height RY is chosen by the
 // host so that the tile count fills whole waves of resident CTAs.
 //
-// Modes: APPLY y; RESID b - y; JACOBI x + omega D^-1 (b - y); RESNORM
+// Modes: APPLY y; APPLYJ0 y and omega D2^-1 y; RESID b - y; JACOBI x + omega D^-1 (b - y); RESNORM
 // ||b - y||^2 (deterministic grid reduction, no write).
 #pragma once
 
@@ -37,7 +37,7 @@ __host__ __device__ constexpr int stencil_ring() {
 
 template <int B, int MODE>
 __host__ __device__ constexpr size_t stencil_smem(int ry) {
-  return sizeof(double2) * ((size_t)kSWarps * stencil_ring<B>() * ((kSW + 2 * B) + (MODE != OP_APPLY ? kSW : 0)) +
+  return sizeof(double2) * ((size_t)kSWarps * stencil_ring<B>() * ((kSW + 2 * B) + (MODE != OP_APPLY && MODE != OP_APPLYJ0 ? kSW : 0)) +
                             (size_t)(ry + 4 * B + 1) * (2 * B + 1));
 }
 
@@ -46,11 +46,12 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
                                                             const double2* __restrict__ bv,
                                                             double2* __restrict__ out, double omega, int RY,
                                                             RedOut red, const int* xidx, size_t xstride, int rb,
-                                                            int re) {
+                                                            int re, double2* __restrict__ out2, double2 c2) {
+  HD_PDL_ENTRY();
   constexpr int NB = 2 * B + 1;
   constexpr int W = kSW + 2 * B;
   constexpr int kSRing = stencil_ring<B>();
-  constexpr bool NEED_B = MODE != OP_APPLY;
+  constexpr bool NEED_B = MODE != OP_APPLY && MODE != OP_APPLYJ0;
   if (xidx) x += (size_t)(*xidx) * xstride;  // graph mode: x = V + j N
   extern __shared__ __align__(16) double2 dsm[];
   double2(*ring)[kSRing][W] = reinterpret_cast<double2(*)[kSRing][W]>(dsm);
@@ -164,6 +165,11 @@ __global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const d
             if (colv) {
               if (MODE == OP_APPLY) {
                 *outp = yo;
+              } else if (MODE == OP_APPLYJ0) {
+                *outp = yo;
+                const double2 cyc = cyk[B];
+                const double2 D = csub(cmk(cyc.x * sx[B] + cyc.y * mx[B], 0.0), cscale(cyc.x * mx[B], c2));
+                out2[outp - out] = cscale(omega, cmul(cinv(D), yo));
               } else if (MODE == OP_RESID) {
                 *outp = csub(bring[warp][s][lane], yo);
               } else if (MODE == OP_RESNORM) {

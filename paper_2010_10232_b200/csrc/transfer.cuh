@@ -26,11 +26,15 @@ struct ZW {
   }
 };
 
-// PLANAR: 0 interleaved output (outc), 1 planar (outp: re plane then im plane)
-template <int KIND, int PLANAR>
+// PLANAR: 0 interleaved output (outc), 1 planar (outp: re plane then im plane).
+// J0 (interleaved only): also x0 = omega D^-1 rc, the first damped-Jacobi sweep
+// of the coarse level Lc from the zero iterate (k_jacobi0_2d_t's arithmetic).
+template <int KIND, int PLANAR, bool J0 = false>
 __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* __restrict__ r, int nf, int nc,
                                                     double2* __restrict__ outc, double* __restrict__ outp, int qb,
-                                                    int qe) {
+                                                    int qe, LevelDev Lc = LevelDev{}, double omega = 0.0,
+                                                    double2* __restrict__ x0 = nullptr) {
+  HD_PDL_ENTRY();
   constexpr int lo = ZW<KIND>::lo, nw = ZW<KIND>::nw;
   constexpr int RR = 2 * kRQY + nw - 1;  // fine rows of the region
   constexpr int RC = 2 * kRQX + nw - 1;  // fine cols
@@ -39,6 +43,7 @@ __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* 
   // coarse rows [qb, qe) (a row slab; whole grid: 0, nc), global row addressing
   const int qx0 = blockIdx.x * kRQX, qy0 = qb + blockIdx.y * kRQY;
   const int fx0 = 2 * qx0 + lo, fy0 = 2 * qy0 + lo;
+  const int fymax = 2 * (min(qy0 + kRQY, qe) - 1) + lo + nw - 1;
   // all loads of the region issued before any is consumed (blockDim == 256)
   constexpr int NLD = (RR * RC + 255) / 256;
   double2 v[NLD];
@@ -47,8 +52,10 @@ __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* 
     const int e = threadIdx.x + k * 256;
     const int rr = e / RC, cc = e % RC;
     const int fy = fy0 + rr, fx = fx0 + cc;
-    v[k] = (e < RR * RC && fy >= 0 && fy < nf && fx >= 0 && fx < nf) ? __ldg(r + (size_t)fy * nf + fx)
-                                                                      : cmk(0.0, 0.0);
+    // only the fine rows the tile's coarse rows [qy0, min(qy0 + kRQY, qe)) use: a row slab's
+    // buffer ends a halo below its last row, so a partial tile must not read past it
+    v[k] = (e < RR * RC && fy >= 0 && fy < nf && fy <= fymax && fx >= 0 && fx < nf) ? __ldg(r + (size_t)fy * nf + fx)
+                                                                                     : cmk(0.0, 0.0);
   }
 #pragma unroll
   for (int k = 0; k < NLD; ++k) {
@@ -81,6 +88,13 @@ __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* 
       outp[gi + NC] = s.y;
     } else {
       outc[gi] = s;
+      if (J0) {
+        const int NB = 2 * Lc.b + 1;
+        const double my = Lc.M[(size_t)gy * NB + Lc.b], sy = Lc.S[(size_t)gy * NB + Lc.b];
+        const double mxx = Lc.M[(size_t)gx * NB + Lc.b], sxx = Lc.S[(size_t)gx * NB + Lc.b];
+        const double2 D = csub(cmk(my * sxx + sy * mxx, 0.0), cscale(my * mxx, Lc.c));
+        x0[gi] = cscale(omega, cmul(cinv(D), s));
+      }
     }
   }
 }
@@ -135,18 +149,22 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
                                                    const double* __restrict__ ep, int nf, int nc,
                                                    const double2* __restrict__ s, double2* __restrict__ out, int fb,
                                                    int fe) {
+  HD_PDL_ENTRY();
   constexpr int CR = kPFY / 2 + 3, CC = kPFX / 2 + 3;
   __shared__ double2 cs[CR][CC];
   __shared__ double2 ty[kPFY][CC];  // y-interpolated coarse columns for every fine row of the tile
   // fine rows [fb, fe) (a row slab, fb even; whole grid: 0, nf), global row addressing
   const int fx0 = blockIdx.x * kPFX, fy0 = fb + blockIdx.y * kPFY;
   const int qx0 = fx0 / 2 - 1, qy0 = fy0 / 2 - 1;  // region origin (may be -1)
+  const int qymax = min(fy0 + kPFY, fe) / 2;        // largest coarse row a fine row < fe uses
   const size_t NC = (size_t)nc * nc;
   for (int e = threadIdx.x; e < CR * CC; e += blockDim.x) {
     const int rr = e / CC, cc = e % CC;
     const int qy = qy0 + rr, qx = qx0 + cc;
     double2 v = cmk(0.0, 0.0);
-    if (qy >= 0 && qy < nc && qx >= 0 && qx < nc) {
+    // coarse rows past qymax feed no fine row of the tile below fe (and a row
+    // slab's coarse buffer may end right after its halo)
+    if (qy >= 0 && qy < nc && qy <= qymax && qx >= 0 && qx < nc) {
       const size_t qi = (size_t)qy * nc + qx;
       v = PMODE == 0 ? ec[qi] : cmk(ep[qi], ep[qi + NC]);
     }
@@ -200,10 +218,17 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
 // x = omega D^-1 b on a 2D level, 2D grid (no 64-bit div/mod per element)
 __global__ void __launch_bounds__(256) k_jacobi0_2d_t(LevelDev L, const double2* __restrict__ b,
                                                       double2* __restrict__ out, double omega, int rb, int re) {
+  HD_PDL_ENTRY();
   const int n = L.n, NB = 2 * L.b + 1;
   const int ix = blockIdx.x * 64 + (threadIdx.x & 63);
   const int iy0 = rb + blockIdx.y * 16 + (threadIdx.x >> 6) * 4;
   if (ix >= n) return;
+  double2 bv[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {  // all loads in flight before the divisions
+    const int iy = iy0 + r;
+    bv[r] = iy < re ? ld_stream(b + (size_t)iy * n + ix) : cmk(0.0, 0.0);
+  }
   const double mxx = L.M[(size_t)ix * NB + L.b], sxx = L.S[(size_t)ix * NB + L.b];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -211,8 +236,7 @@ __global__ void __launch_bounds__(256) k_jacobi0_2d_t(LevelDev L, const double2*
     if (iy >= re) break;
     const double my = L.M[(size_t)iy * NB + L.b], sy = L.S[(size_t)iy * NB + L.b];
     const double2 D = csub(cmk(my * sxx + sy * mxx, 0.0), cscale(my * mxx, L.c));
-    const size_t g = (size_t)iy * n + ix;
-    out[g] = cscale(omega, cmul(cinv(D), ld_stream(b + g)));
+    out[(size_t)iy * n + ix] = cscale(omega, cmul(cinv(D), bv[r]));
   }
 }
 

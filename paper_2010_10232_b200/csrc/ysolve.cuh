@@ -44,6 +44,7 @@ struct YArgs {
 
 template <int KL>
 __global__ void __launch_bounds__(128) k_ys_fwd(YArgs a) {
+  HD_PDL_ENTRY();
   constexpr int W = KL + 1, NF = 2 * KL + 2;
   const int m = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
   if (m >= a.np) return;
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(128) k_ys_fwd(YArgs a) {
 // Delta_0 = 0, Delta_{i+1} = D_i + F_i Delta_i  (thread per mode)
 template <int KL>
 __global__ void k_ys_scan_fwd(YArgs a) {
+  HD_PDL_ENTRY();
   constexpr int W = KL + 1;
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= a.np) return;
@@ -132,6 +134,7 @@ __global__ void k_ys_scan_fwd(YArgs a) {
 // y_k += h_k . Delta_i, then the local backward sweep
 template <int KL>
 __global__ void __launch_bounds__(128) k_ys_bwd(YArgs a) {
+  HD_PDL_ENTRY();
   constexpr int W = KL + 1, KU = 2 * KL, NF = 2 * KL + 2, NB = 2 * KU + 1;
   const int m = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
   if (m >= a.np) return;
@@ -190,6 +193,7 @@ __global__ void __launch_bounds__(128) k_ys_bwd(YArgs a) {
 // X_S = 0, X_i = XS_i + H_i X_{i+1}  (thread per mode)
 template <int KL>
 __global__ void k_ys_scan_bwd(YArgs a) {
+  HD_PDL_ENTRY();
   constexpr int KU = 2 * KL;
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= a.np) return;
@@ -230,6 +234,7 @@ __global__ void k_ys_scan_bwd(YArgs a) {
 // x_k = x0_k + h'_k . X_{i+1}  -> C  (thread per (row, mode))
 template <int KL>
 __global__ void k_ys_out(YArgs a) {
+  HD_PDL_ENTRY();
   constexpr int KU = 2 * KL, NB = 2 * KU + 1;
   const int m = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
   if (m >= a.np) return;

@@ -12,8 +12,11 @@ import paper_2010_10232_b200 as hd  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 dim, p, ne, k = {"C5": (2, 3, 1600, 1000.0), "C3": (2, 2, 320, 200.0), "C2": (1, 4, 31623, 1000.0),
-                 "C1": (1, 2, 80, 50.0)}[cfg]
-s = hd.assemble(hd.point_source_2d(ne, p, k) if dim == 2 else hd.point_source_1d(ne, p, k))
+                 "C1": (1, 2, 80, 50.0), "C4": (2, 3, 480, 150.0)}[cfg]
+if cfg == "C4":
+    s = hd.assemble(hd.wedge_2d(ne, p, k))
+else:
+    s = hd.assemble(hd.point_source_2d(ne, p, k) if dim == 2 else hd.point_source_1d(ne, p, k))
 solver = hd.Solver(s, hd.to_spec("DC_MG", p, k, beta2="0.5", omega=2 / 3))
 st = torch.cuda.current_stream()
 solver.set_stream(st.cuda_stream)
