@@ -274,6 +274,123 @@ __global__ void __launch_bounds__(32) k_seg_scan_bwd(SegArgs a) {
   cp_async_wait<0>();
 }
 
+// ---- two-level scan over the segments (replaces the P-step sequential scans) ----
+// The boundary recurrences are affine maps applied in step order t = 0..P-1:
+//   forward  (BWD = 0): map i = t,       s <- D_i + F_i s,  out[i] = s before the map (Delta_i)
+//   backward (BWD = 1): map i = P-1-t,   s <- X0_i + H'_i s, out[i] = s after the map (X_i), out[P] = 0
+// Phase 1: warp g composes the maps of its group of m consecutive steps into one
+// affine map (A_g, b_g).  Phase 2: one warp runs the G group maps in order and
+// records every group's incoming state.  Phase 3: warp g replays its group's m
+// maps from that state, in the sequential kernels' arithmetic, writing the
+// outputs.  3 x m + G dependent steps instead of P; the incoming states differ
+// from the sequential scan's only by the rounding of the compositions.
+constexpr int kScanWarps = 16, kScanRing = 4;
+
+template <int DM>
+__host__ __device__ constexpr size_t seg_scan2_smem() {
+  return sizeof(double2) * ((size_t)kScanWarps * kScanRing * (DM * DM + DM) +  // map ring per warp
+                            (size_t)kScanWarps * 2 * (DM * DM + DM) +           // A, b double-buffered per warp
+                            (size_t)kScanWarps * (DM * DM + DM) +               // group maps (A_g, b_g)
+                            (size_t)kScanWarps * DM);                           // group incoming states
+}
+
+template <int DM, int BWD>
+__global__ void __launch_bounds__(kScanWarps * 32) k_seg_scan2(const double2* __restrict__ Mt,
+                                                               const double2* __restrict__ ct, double2* __restrict__ out,
+                                                               int P) {
+  HD_PDL_ENTRY();
+  constexpr int DD = DM * DM, PER = DD + DM;
+  extern __shared__ __align__(16) double2 ssm[];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  double2* ring = ssm + (size_t)g * kScanRing * PER;
+  double2* ab = ssm + (size_t)kScanWarps * kScanRing * PER + (size_t)g * 2 * PER;  // [2][A | b]
+  double2* agg = ssm + (size_t)kScanWarps * (kScanRing + 2) * PER;                // [G][A_g | b_g]
+  double2* sin = agg + (size_t)kScanWarps * PER;                                   // [G][DM]
+  const int m = (P + kScanWarps - 1) / kScanWarps;
+  const int t0 = min(P, g * m), t1 = min(P, t0 + m);
+  auto mapidx = [&](int t) { return BWD ? P - 1 - t : t; };
+  auto issue = [&](int t) {
+    if (t < t1) {
+      const int i = mapidx(t);
+      double2* d = ring + (size_t)((t - t0) % kScanRing) * PER;
+      for (int e = lane; e < DD; e += 32) cp_async16(d + e, Mt + (size_t)i * DD + e, true);
+      for (int e = lane; e < DM; e += 32) cp_async16(d + DD + e, ct + (size_t)i * DM + e, true);
+    }
+    cp_async_commit();
+  };
+  // phase 1: (A, b) <- (M A, M b + c) over the group's steps
+  for (int t = t0; t < t0 + kScanRing - 1; ++t) issue(t);
+  for (int e = lane; e < PER; e += 32) ab[e] = cmk(e < DD && e / DM == e % DM ? 1.0 : 0.0, 0.0);
+  __syncwarp();
+  int cur = 0;
+  for (int t = t0; t < t1; ++t) {
+    cp_async_wait<kScanRing - 2>();
+    __syncwarp();
+    issue(t + kScanRing - 1);
+    const double2* M = ring + (size_t)((t - t0) % kScanRing) * PER;
+    const double2* A = ab + cur * PER;
+    double2* An = ab + (cur ^ 1) * PER;
+    for (int e = lane; e < PER; e += 32) {
+      double2 v;
+      if (e < DD) {  // (M A)(r, c)
+        const int r = e / DM, c = e % DM;
+        v = cmk(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < DM; ++k) v = cfma(M[r * DM + k], A[k * DM + c], v);
+      } else {  // (M b + c)(r)
+        const int r = e - DD;
+        v = M[DD + r];
+#pragma unroll
+        for (int k = 0; k < DM; ++k) v = cfma(M[r * DM + k], A[DD + k], v);
+      }
+      An[e] = v;
+    }
+    cur ^= 1;
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  for (int e = lane; e < PER; e += 32) agg[(size_t)g * PER + e] = ab[cur * PER + e];
+  __syncthreads();
+  // phase 2: group maps in order, lane q owns component q
+  if (g == 0) {
+    double2 sv = cmk(0.0, 0.0);
+    for (int gg = 0; gg < kScanWarps; ++gg) {
+      if (lane < DM) sin[gg * DM + lane] = sv;
+      const double2* Ag = agg + (size_t)gg * PER;
+      double2 nx = lane < DM ? Ag[DD + lane] : cmk(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < DM; ++r) {
+        const double2 sr = cmk(__shfl_sync(0xffffffffu, sv.x, r), __shfl_sync(0xffffffffu, sv.y, r));
+        if (lane < DM) nx = cfma(Ag[lane * DM + r], sr, nx);
+      }
+      sv = nx;
+    }
+    if (BWD && lane < DM) out[(size_t)P * DM + lane] = cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  // phase 3: replay the group's steps from its incoming state
+  for (int t = t0; t < t0 + kScanRing - 1; ++t) issue(t);
+  double2 sv = lane < DM ? sin[g * DM + lane] : cmk(0.0, 0.0);
+  for (int t = t0; t < t1; ++t) {
+    cp_async_wait<kScanRing - 2>();
+    __syncwarp();
+    issue(t + kScanRing - 1);
+    const int i = mapidx(t);
+    if (!BWD && lane < DM) out[(size_t)i * DM + lane] = sv;
+    const double2* M = ring + (size_t)((t - t0) % kScanRing) * PER;
+    double2 nx = lane < DM ? M[DD + lane] : cmk(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < DM; ++r) {
+      const double2 sr = cmk(__shfl_sync(0xffffffffu, sv.x, r), __shfl_sync(0xffffffffu, sv.y, r));
+      if (lane < DM) nx = cfma(M[lane * DM + r], sr, nx);
+    }
+    sv = nx;
+    if (BWD && lane < DM) out[(size_t)i * DM + lane] = sv;
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+}
+
 // x_k = x0_k + h'_k . X_{i+1}  (thread per row), output interleaved or planar
 template <int KL>
 __global__ void k_seg_out(SegArgs a, double2* __restrict__ x, double* __restrict__ xp) {

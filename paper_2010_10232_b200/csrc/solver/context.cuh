@@ -642,10 +642,23 @@ static void seg_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b
                             static_cast<int>(seg_bwd_smem<KL>())));
     attr = true;
   }
+  constexpr int W = KL + 1, KU = 2 * KL;
+  // the P-step single-warp scans: HD_SEG_SEQSCAN, or maps too large for the staged two-level scan (KL = 6)
+  static const bool seq = std::getenv("HD_SEG_SEQSCAN") != nullptr || seg_scan2_smem<KU>() > 227u * 1024u;
+  static bool attr2 = false;
+  if (!attr2 && !seq) {
+    CK(cudaFuncSetAttribute(k_seg_scan2<W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(seg_scan2_smem<W>())));
+    CK(cudaFuncSetAttribute(k_seg_scan2<KU, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(seg_scan2_smem<KU>())));
+    attr2 = true;
+  }
   k_seg_fwd<KL><<<blocks, 32, seg_fwd_smem<KL>(), st>>>(a, b, bp);
-  k_seg_scan_fwd<KL><<<1, 32, 0, st>>>(a);
+  if (seq) k_seg_scan_fwd<KL><<<1, 32, 0, st>>>(a);
+  else k_seg_scan2<W, 0><<<1, kScanWarps * 32, seg_scan2_smem<W>(), st>>>(a.Ff, a.D, a.Dl, a.P);
   k_seg_bwd<KL><<<blocks, 32, seg_bwd_smem<KL>(), st>>>(a);
-  k_seg_scan_bwd<KL><<<1, 32, 0, st>>>(a);
+  if (seq) k_seg_scan_bwd<KL><<<1, 32, 0, st>>>(a);
+  else k_seg_scan2<KU, 1><<<1, kScanWarps * 32, seg_scan2_smem<KU>(), st>>>(a.Hb, a.X0, a.Xb, a.P);
   k_seg_out<KL><<<std::min((a.n + 255) / 256, 148 * 4), 256, 0, st>>>(a, x, xp);
 }
 

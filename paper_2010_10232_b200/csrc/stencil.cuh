@@ -41,8 +41,12 @@ __host__ __device__ constexpr size_t stencil_smem(int ry) {
                             (size_t)(ry + 4 * B + 1) * (2 * B + 1));
 }
 
+#ifndef HD_STENCIL_MINB
+#define HD_STENCIL_MINB 1
+#endif
+
 template <int B, int MODE>
-__global__ void __launch_bounds__(kSW * kSWarps) k_stencil2d(LevelDev L, const double2* __restrict__ x,
+__global__ void __launch_bounds__(kSW * kSWarps, HD_STENCIL_MINB) k_stencil2d(LevelDev L, const double2* __restrict__ x,
                                                             const double2* __restrict__ bv,
                                                             double2* __restrict__ out, double omega, int RY,
                                                             RedOut red, const int* xidx, size_t xstride, int rb,
