@@ -65,6 +65,7 @@ struct ExactSolver {
   double2* Uinv = nullptr;   // 1 / U(k, k)
   // segmented sweeps (segsolve.cuh); seg.P == 0: single-lane staged kernel
   SegArgs seg{};
+  bool seg_seqscan = false;  // P-step single-warp boundary scans instead of k_seg_scan2 (HD_SEG_SEQSCAN at setup)
   // partial fast diagonalisation (ysolve.cuh): x modes by V, segmented banded LU sweeps along y
   bool ypart = false;
   int ykl = 0;
@@ -110,6 +111,7 @@ struct hd_ctx {
   ExactSolver shift_exact;      // C_ex: exact inverse of the shifted operator (cycles == 0)
   double* sx_plan = nullptr;    // planar scratch for the 2D exact shifted solve
   std::vector<double2*> mg_b, mg_x, mg_y, mg_r;
+  bool j0_fuse = true;          // first Jacobi sweeps ride with their producers (HD_NOJ0FUSE=1 at create: off)
   int pdl_edges = 0;            // programmatic kernel->kernel edges in the loop graph body
   int tail_l = -1;              // 1D: first level of the single-CTA tail V-cycle (tail1d.cuh), -1: none
   TailArgs tail{};
@@ -285,7 +287,7 @@ static bool centro_symmetric(const Band& X) {
       mx = std::max(mx, std::abs(X.at(i, j)));
       dev = std::max(dev, std::abs(X.at(i, j) - X.at(X.n - 1 - i, X.n - 1 - j)));
     }
-  static const double tol = std::getenv("HD_CENTRO_TOL") ? std::atof(std::getenv("HD_CENTRO_TOL")) : 1e-12;
+  const double tol = std::getenv("HD_CENTRO_TOL") ? std::atof(std::getenv("HD_CENTRO_TOL")) : 1e-12;
   return dev <= tol * mx;
 }
 
@@ -549,6 +551,7 @@ static void make_segments(ExactSolver& X, const BandLU& f) {
     CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
     return d;
   };
+  X.seg_seqscan = std::getenv("HD_SEG_SEQSCAN") != nullptr;
   SegArgs& a = X.seg;
   a.n = n;
   a.P = P;
@@ -644,7 +647,7 @@ static void seg_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b
   }
   constexpr int W = KL + 1, KU = 2 * KL;
   // the P-step single-warp scans: HD_SEG_SEQSCAN, or maps too large for the staged two-level scan (KL = 6)
-  static const bool seq = std::getenv("HD_SEG_SEQSCAN") != nullptr || seg_scan2_smem<KU>() > 227u * 1024u;
+  const bool seq = X.seg_seqscan || seg_scan2_smem<KU>() > 227u * 1024u;
   static bool attr2 = false;
   if (!attr2 && !seq) {
     CK(cudaFuncSetAttribute(k_seg_scan2<W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,

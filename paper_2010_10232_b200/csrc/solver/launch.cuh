@@ -480,7 +480,7 @@ static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2*
 // produces its right-hand side: a 2D Kronecker-sum level that is smoothed
 // (not the coarsest, not the 1D tail, not a layered/wedge level).
 static bool j0_fusable(hd_ctx* c, int l) {
-  static const bool off = std::getenv("HD_NOJ0FUSE") != nullptr;
+  const bool off = !c->j0_fuse;
   const int last = static_cast<int>(c->lev.size()) - 1;
   return !off && c->dim == 2 && l < last && l != c->tail_l && c->spec.smooth_steps >= 1 && !c->lev[l].genM &&
          !c->fine.genA;
