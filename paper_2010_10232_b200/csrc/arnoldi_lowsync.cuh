@@ -99,16 +99,18 @@ constexpr int kLsaCE = 1024;  // chunk elements
 struct LsaArgs;
 __device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh_s, double2* sh_lj, double2* hsm);
 
-constexpr size_t lsa_dots_smem() { return sizeof(double2) * (2 * kLsaCE + 2 * (kLsaMaxJ + 1)); }
+constexpr size_t lsa_dots_smem() { return sizeof(double2) * (4 * kLsaCE + 2 * (kLsaMaxJ + 1)); }
 
 __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   HD_PDL_ENTRY();
   constexpr int NW = kLsaBD / 32;
   constexpr int PER = kLsaCE / 32;  // elements per lane per chunk
   extern __shared__ __align__(16) double2 dsm[];
-  double2* ws = dsm;                    // w chunk
-  double2* us = dsm + kLsaCE;           // u_j chunk
-  double2* acc = dsm + 2 * kLsaCE;      // [0..j]: s_i ; [kLsaMaxJ+1 ..]: G_ji
+  // w and u_j chunks, double-buffered: the next chunk's pair is copied (cp.async)
+  // while the warps stream the basis vectors against the current one
+  double2* wsb = dsm;                   // [2][kLsaCE] w chunks
+  double2* usb = dsm + 2 * kLsaCE;      // [2][kLsaCE] u_j chunks
+  double2* acc = dsm + 4 * kLsaCE;      // [0..j]: s_i ; [kLsaMaxJ+1 ..]: G_ji
   __shared__ double2 sh_s[kLsaMaxJ + 1];
   __shared__ double2 sh_lj[kLsaMaxJ];
   __shared__ double2 hsm[kLsaMaxJ + 1];
@@ -121,15 +123,28 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   const size_t N = a.N;
   const double2* uj = a.U + (size_t)j * N;
   const size_t nchunks = (N + kLsaCE - 1) / kLsaCE;
-  for (size_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+  auto stage = [&](size_t ch, int buf) {
+    if (ch < nchunks) {
+      const size_t c0 = ch * kLsaCE;
+      const int len = (int)min((size_t)kLsaCE, N - c0);
+      for (int e = threadIdx.x; e < kLsaCE; e += kLsaBD) {
+        const bool v = e < len;
+        cp_async16(wsb + buf * kLsaCE + e, v ? a.w + c0 + e : a.w, v);
+        cp_async16(usb + buf * kLsaCE + e, v && j > 0 ? uj + c0 + e : a.w, v && j > 0);
+      }
+    }
+    cp_async_commit();
+  };
+  stage(blockIdx.x, 0);
+  int buf = 0;
+  for (size_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, buf ^= 1) {
     const size_t c0 = ch * kLsaCE;
     const int len = (int)min((size_t)kLsaCE, N - c0);
-    __syncthreads();  // previous chunk fully consumed
-    for (int e = threadIdx.x; e < kLsaCE; e += kLsaBD) {
-      ws[e] = e < len ? ld_stream(a.w + c0 + e) : cmk(0.0, 0.0);
-      us[e] = (e < len && j > 0) ? uj[c0 + e] : cmk(0.0, 0.0);
-    }
-    __syncthreads();
+    stage(ch + gridDim.x, buf ^ 1);  // its buffer was last read before the previous chunk's closing barrier
+    cp_async_wait<1>();
+    __syncthreads();  // this chunk's w and u_j visible to every warp
+    const double2* ws = wsb + buf * kLsaCE;
+    const double2* us = usb + buf * kLsaCE;
     for (int i = warp; i < nd; i += NW) {
       const double2* ui = a.U + (size_t)i * N + c0;
       double2 sa = cmk(0.0, 0.0), sb = cmk(0.0, 0.0), ga = cmk(0.0, 0.0), gb = cmk(0.0, 0.0);
@@ -152,7 +167,9 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
         if (i < j) acc[kLsaMaxJ + 1 + i] = cadd(acc[kLsaMaxJ + 1 + i], g_);
       }
     }
+    __syncthreads();  // every warp done with this chunk's buffers before they are refilled
   }
+  cp_async_wait<0>();
   __syncthreads();
   for (int q = threadIdx.x; q < nslot; q += kLsaBD) {
     const bool used = q < nd || (q >= kLsaMaxJ + 1 && q < kLsaMaxJ + 1 + j);

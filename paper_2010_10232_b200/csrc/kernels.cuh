@@ -543,41 +543,11 @@ __global__ void k_fd_scale(double* __restrict__ T, const double2* __restrict__ D
 }
 
 // ---- reflection-folded fast diagonalisation (solver.cu make_fd_folded) ----
-// X col-major n x ncol (planar complex: ncol = 2n); F[b] col-major n2 x ncol
-__global__ void k_fold_rows(const double* __restrict__ X, double* __restrict__ F, int n, int n2, int ncol) {
-  HD_PDL_ENTRY();
-  const size_t tot = (size_t)n2 * ncol;
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
-    const int i = (int)(g % n2);
-    const size_t col = g / n2;
-    const double a = X[col * n + i], b = X[col * n + (n - 1 - i)];
-    F[col * n2 + i] = a + b;
-    F[tot + col * n2 + i] = a - b;
-  }
-}
-
 // Hh[yb] is col-major (4 n2) x n2, ld 4 n2: row q n2 + kx (q = 2 xb + p), column j,
 // so each y transform is one (4 n2) x n2 x n2 GEMM per y parity.
 __device__ __forceinline__ size_t fold_idx(int yb, int xb, int p, int kx, int j, int n2) {
   const size_t nn = (size_t)n2 * n2;
   return (size_t)yb * 4 * nn + (size_t)j * 4 * n2 + (size_t)(2 * xb + p) * n2 + kx;
-}
-
-// Hh[yb](q n2 + kx, j) = G_xb(kx, p n + j) +- G_xb(kx, p n + n-1-j)
-__global__ void k_fold_cols(const double* __restrict__ G, double* __restrict__ Hh, int n, int n2) {
-  HD_PDL_ENTRY();
-  const size_t nn = (size_t)n2 * n2;
-  const size_t tot = 4 * nn;
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
-    const int kx = (int)(g % n2);
-    const int q = (int)((g / n2) % 4);
-    const int j = (int)(g / (4 * (size_t)n2));
-    const int xb = q >> 1, p = q & 1;
-    const double* Gx = G + (size_t)xb * n2 * 2 * n;
-    const double a = Gx[((size_t)p * n + j) * n2 + kx], b = Gx[((size_t)p * n + (n - 1 - j)) * n2 + kx];
-    Hh[fold_idx(0, xb, p, kx, j, n2)] = a + b;
-    Hh[fold_idx(1, xb, p, kx, j, n2)] = a - b;
-  }
 }
 
 // R[yb](q n2 + kx, ky), q = 2 xb + p: (R_p0 + i R_p1) *= D[yb][xb][ky][kx]
@@ -598,34 +568,46 @@ __global__ void k_scale_folded(double* __restrict__ R, const double2* __restrict
   }
 }
 
-// S[yb](q n2 + kx, j) -> Z_xb(kx, p n + j) = S_s + S_a, Z_xb(kx, p n + n-1-j) = S_s - S_a
-__global__ void k_unfold_cols(const double* __restrict__ S, double* __restrict__ Z, int n, int n2) {
+// Both reflections at once (x rows and y columns of the planar n x n input X):
+// Q[xb][yb][p](i, j), i, j < n2: x rows folded first (a +- b), then y columns.
+// Q blocks n2 x n2 column-major, block (2 xb + yb) 2 + p.
+__global__ void k_fold_both(const double* __restrict__ X, double* __restrict__ Q, int n, int n2) {
   HD_PDL_ENTRY();
-  const size_t nn = (size_t)n2 * n2;
-  const size_t tot = 4 * nn;
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
-    const int kx = (int)(g % n2);
-    const int q = (int)((g / n2) % 4);
-    const int j = (int)(g / (4 * (size_t)n2));
-    const int xb = q >> 1, p = q & 1;
-    const double ss = S[fold_idx(0, xb, p, kx, j, n2)];
-    const double sa = S[fold_idx(1, xb, p, kx, j, n2)];
-    double* Zx = Z + (size_t)xb * n2 * 2 * n;
-    Zx[((size_t)p * n + j) * n2 + kx] = ss + sa;
-    Zx[((size_t)p * n + (n - 1 - j)) * n2 + kx] = ss - sa;
+  const size_t nn = (size_t)n2 * n2, N2 = (size_t)n * n;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < 2 * nn; g += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(g % n2);
+    const int j = (int)((g / n2) % n2);
+    const int p = (int)(g / nn);
+    const double* Xp = X + p * N2;
+    const double a = Xp[(size_t)j * n + i], b = Xp[(size_t)j * n + (n - 1 - i)];
+    const double c = Xp[(size_t)(n - 1 - j) * n + i], d = Xp[(size_t)(n - 1 - j) * n + (n - 1 - i)];
+    const double f0 = a + b, f1 = a - b, g0 = c + d, g1 = c - d;  // x parity 0 / 1 at columns j, n-1-j
+    const size_t o = (size_t)j * n2 + i;
+    Q[(size_t)((0 * 2 + 0) * 2 + p) * nn + o] = f0 + g0;
+    Q[(size_t)((0 * 2 + 1) * 2 + p) * nn + o] = f0 - g0;
+    Q[(size_t)((1 * 2 + 0) * 2 + p) * nn + o] = f1 + g1;
+    Q[(size_t)((1 * 2 + 1) * 2 + p) * nn + o] = f1 - g1;
   }
 }
 
-// Y(i, c) = Yh_s(i, c) + Yh_a(i, c);  Y(n-1-i, c) = Yh_s(i, c) - Yh_a(i, c)
-__global__ void k_unfold_rows(const double* __restrict__ Yh, double* __restrict__ Y, int n, int n2, int ncol) {
+// Inverse of k_fold_both: P[xb][yb][p] blocks -> planar n x n Y (y columns
+// unfolded first, then x rows).
+__global__ void k_unfold_both(const double* __restrict__ Pb, double* __restrict__ Y, int n, int n2) {
   HD_PDL_ENTRY();
-  const size_t tot = (size_t)n2 * ncol;
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
+  const size_t nn = (size_t)n2 * n2, N2 = (size_t)n * n;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < 2 * nn; g += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(g % n2);
-    const size_t col = g / n2;
-    const double a = Yh[col * n2 + i], b = Yh[tot + col * n2 + i];
-    Y[col * n + i] = a + b;
-    Y[col * n + (n - 1 - i)] = a - b;
+    const int j = (int)((g / n2) % n2);
+    const int p = (int)(g / nn);
+    const size_t o = (size_t)j * n2 + i;
+    const double p00 = Pb[(size_t)((0 * 2 + 0) * 2 + p) * nn + o], p01 = Pb[(size_t)((0 * 2 + 1) * 2 + p) * nn + o];
+    const double p10 = Pb[(size_t)((1 * 2 + 0) * 2 + p) * nn + o], p11 = Pb[(size_t)((1 * 2 + 1) * 2 + p) * nn + o];
+    const double z0j = p00 + p01, z0m = p00 - p01, z1j = p10 + p11, z1m = p10 - p11;
+    double* Yp = Y + p * N2;
+    Yp[(size_t)j * n + i] = z0j + z1j;
+    Yp[(size_t)j * n + (n - 1 - i)] = z0j - z1j;
+    Yp[(size_t)(n - 1 - j) * n + i] = z0m + z1m;
+    Yp[(size_t)(n - 1 - j) * n + (n - 1 - i)] = z0m - z1m;
   }
 }
 

@@ -76,7 +76,11 @@ struct ExactSolver {
   int n2 = 0;
   double* Vt = nullptr;
   double2* Dinvf = nullptr;
-  double *F = nullptr, *G = nullptr, *Hh = nullptr, *R = nullptr;
+  double *F = nullptr, *Hh = nullptr, *R = nullptr;  // folded blocks (8 n2^2 each)
+  // pointer arrays of the two 8-entry batched x transforms (device): A, B, C of
+  // the forward (Vt_xb^T Q -> Hh blocks) and of the inverse (Vt_xb S -> F blocks)
+  const double** xf_ptr = nullptr;
+  const double** xi_ptr = nullptr;
   // dense inverse (layered field: E and the coarsest level are not Kronecker sums)
   bool dense = false;
   size_t NN = 0;
@@ -338,9 +342,29 @@ static ExactSolver make_fd_folded(cudaStream_t st, const Band& S, const Band& M,
   CK(cudaMemcpy(X.Dinvf, D.data(), D.size() * sizeof(double2), cudaMemcpyHostToDevice));
   const size_t half = 2 * static_cast<size_t>(n2) * 2 * n;  // 2 parities x n2 x 2n
   X.F = dalloc<double>(half);
-  X.G = dalloc<double>(half);
   X.Hh = dalloc<double>(8 * static_cast<size_t>(n2) * n2);
   X.R = dalloc<double>(8 * static_cast<size_t>(n2) * n2);
+  // x transforms as 8-entry pointer-batched GEMMs over (x parity, y parity, plane):
+  // forward Vt_xb^T Q[xb][yb][p] (Q blocks n2 x n2 in F) into Hh[yb] rows (2 xb + p) n2,
+  // inverse Vt_xb Hh[yb] rows (2 xb + p) n2 into F blocks
+  {
+    const size_t nn = static_cast<size_t>(n2) * n2;
+    std::vector<const double*> hp(48);
+    for (int xb = 0; xb < 2; ++xb)
+      for (int yb = 0; yb < 2; ++yb)
+        for (int p = 0; p < 2; ++p) {
+          const int e = (xb * 2 + yb) * 2 + p;
+          const double* vt = X.Vt + xb * nn;
+          const double* fb = X.F + e * nn;
+          const double* hb = X.Hh + yb * 4 * nn + (2 * xb + p) * n2;
+          hp[e] = vt; hp[8 + e] = fb; hp[16 + e] = hb;        // forward: A, B, C
+          hp[24 + e] = vt; hp[32 + e] = hb; hp[40 + e] = fb;  // inverse: A, B, C
+        }
+    const double** d = dalloc<const double*>(48);
+    CK(cudaMemcpy(d, hp.data(), 48 * sizeof(const double*), cudaMemcpyHostToDevice));
+    X.xf_ptr = d;
+    X.xi_ptr = d + 24;
+  }
   return X;
 }
 
@@ -596,7 +620,8 @@ static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 
 
 static void free_exact(ExactSolver& X) {
   cudaFree(X.V); cudaFree(X.Dinv); cudaFree(X.T1); cudaFree(X.T2);
-  cudaFree(X.Vt); cudaFree(X.Dinvf); cudaFree(X.F); cudaFree(X.G); cudaFree(X.Hh); cudaFree(X.R);
+  cudaFree(X.Vt); cudaFree(X.Dinvf); cudaFree(X.F); cudaFree(X.Hh); cudaFree(X.R);
+    cudaFree(const_cast<double**>(X.xf_ptr));
   cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work); cudaFree(X.Uinv);
   if (X.ypart) {
     cudaFree(const_cast<double*>(X.ya.TF)); cudaFree(const_cast<double*>(X.ya.TB));

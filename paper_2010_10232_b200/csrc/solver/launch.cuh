@@ -370,16 +370,14 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
   if (X.dim == 2 && X.folded) {
     const int n = X.n, n2 = X.n2;
     const long nn = static_cast<long>(n2) * n2;
-    const long hc = static_cast<long>(n2) * 2 * n;  // one parity of a half-folded n2 x 2n block
     const double one = 1.0, zero = 0.0;
     const double gb = 16.0 * nn * 4;               // nominal bytes per GEMM call (profiling)
-    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_rows<<<grid_for(hc), 256, 0, c->st>>>(inout, X.F, n, n2, 2 * n));
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_both<<<grid_for(2 * nn), 256, 0, c->st>>>(inout, X.F, n, n2));
     size_t mk = prof_mark(c);
-    // x transform: G_b = Vt_b^T F_b
-    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n2, 2 * n, n2, &one, X.Vt, n2, nn, X.F, n2, hc,
-                                  &zero, X.G, n2, hc, 2));
+    // x transform: Hh[yb] rows (2 xb + p) n2 = Vt_xb^T Q[xb][yb][p]  (8 pointer-batched n2^3 GEMMs)
+    CKB(cublasDgemmBatched(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n2, n2, n2, &one, X.xf_ptr, n2, X.xf_ptr + 8, n2, &zero,
+                           const_cast<double**>(X.xf_ptr + 16), 4 * n2, 8));
     launched(c, HD_K_LIBGEMM, mk, gb, true);
-    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_cols<<<grid_for(4 * nn), 256, 0, c->st>>>(X.G, X.Hh, n, n2));
     // y transform: R[yb] = Hh[yb] Vt_yb, Hh[yb] (4 n2) x n2 (x parity and plane stacked), batch over yb
     mk = prof_mark(c);
     CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, 4 * n2, n2, n2, &one, X.Hh, 4 * n2, 4 * nn, X.Vt,
@@ -391,13 +389,12 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
     CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, 4 * n2, n2, n2, &one, X.R, 4 * n2, 4 * nn, X.Vt,
                                   n2, nn, &zero, X.Hh, 4 * n2, 4 * nn, 2));
     launched(c, HD_K_LIBGEMM, mk, gb, true);
-    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_cols<<<grid_for(4 * nn), 256, 0, c->st>>>(X.Hh, X.F, n, n2));
-    // inverse x: Yh_b = Vt_b Z_b  (Z in F, result in G)
+    // inverse x: F blocks = Vt_xb Hh[yb] rows (2 xb + p) n2, then both reflections undone
     mk = prof_mark(c);
-    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n2, 2 * n, n2, &one, X.Vt, n2, nn, X.F, n2, hc,
-                                  &zero, X.G, n2, hc, 2));
+    CKB(cublasDgemmBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n2, n2, n2, &one, X.xi_ptr, n2, X.xi_ptr + 8, 4 * n2,
+                           &zero, const_cast<double**>(X.xi_ptr + 16), n2, 8));
     launched(c, HD_K_LIBGEMM, mk, gb, true);
-    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_rows<<<grid_for(hc), 256, 0, c->st>>>(X.G, inout, n, n2, 2 * n));
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_both<<<grid_for(2 * nn), 256, 0, c->st>>>(X.F, inout, n, n2));
     return;
   }
   if (X.dim == 2) {
