@@ -99,6 +99,14 @@ constexpr int kLsaCE = 1024;  // chunk elements
 struct LsaArgs;
 __device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh_s, double2* sh_lj, double2* hsm);
 
+// basis loads in flight per lane in pass 1 (16: C5 90.0 -> 89.3 ms against 8, with the
+// double-buffered w / u_j chunks; a split of each vector chunk over two warps needs
+// per-item partial slots and was not pursued)
+#ifndef HD_LSA_UNROLL
+#define HD_LSA_UNROLL 16
+#endif
+constexpr int kLsaUnroll = HD_LSA_UNROLL;
+
 constexpr size_t lsa_dots_smem() { return sizeof(double2) * (4 * kLsaCE + 2 * (kLsaMaxJ + 1)); }
 
 __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
@@ -148,7 +156,7 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
     for (int i = warp; i < nd; i += NW) {
       const double2* ui = a.U + (size_t)i * N + c0;
       double2 sa = cmk(0.0, 0.0), sb = cmk(0.0, 0.0), ga = cmk(0.0, 0.0), gb = cmk(0.0, 0.0);
-#pragma unroll 8
+#pragma unroll kLsaUnroll
       for (int q = 0; q < PER; ++q) {
         const int e = q * 32 + lane;
         const double2 v = e < len ? __ldg(ui + e) : cmk(0.0, 0.0);
