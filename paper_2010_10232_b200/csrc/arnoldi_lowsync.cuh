@@ -24,6 +24,10 @@ namespace hd {
 
 constexpr int kLsaBD = 256;  // threads per CTA
 constexpr int kLsaTE = 4;    // elements per thread per tile
+#ifndef HD_LSA_VPS
+#define HD_LSA_VPS 2
+#endif
+constexpr int kLsaVPS = HD_LSA_VPS;  // basis vectors per step of pass 2
 constexpr int kLsaMaxJ = 128;
 
 struct LsaArgs {
@@ -280,29 +284,27 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
       wv[u] = (upd && e < N) ? cscale(sj, ld_stream(a.w + e)) : cmk(0.0, 0.0);
       xv[u] = (iter && e < N) ? ld_stream(a.x0 + e) : cmk(0.0, 0.0);
     }
-    // two vectors per step: 8 outstanding 16-B loads per thread
-    for (int i = 0; i < nv; i += 2) {
-      const bool two = i + 1 < nv;
-      const double2* u0 = a.U + (size_t)i * N;
-      const double2* u1 = a.U + (size_t)(i + 1) * N;
-      double2 v0[kLsaTE], v1[kLsaTE];
+    // kLsaVPS vectors per step: 4 kLsaVPS outstanding 16-B loads per thread; the
+    // products are accumulated in vector order (as two per step did)
+    for (int i = 0; i < nv; i += kLsaVPS) {
+      double2 v[kLsaVPS][kLsaTE];
 #pragma unroll
-      for (int u = 0; u < kLsaTE; ++u) {
-        const size_t e = t0 + (size_t)u * kLsaBD + threadIdx.x;
-        v0[u] = e < N ? __ldg(u0 + e) : cmk(0.0, 0.0);
-        v1[u] = (two && e < N) ? __ldg(u1 + e) : cmk(0.0, 0.0);
-      }
-      const double2 c0 = sh_c[i], c1 = two ? sh_c[i + 1] : cmk(0.0, 0.0);
-      const double2 d0 = sh_x[i], d1 = two ? sh_x[i + 1] : cmk(0.0, 0.0);
+      for (int b = 0; b < kLsaVPS; ++b) {
+        const double2* ub = a.U + (size_t)(i + b) * N;
 #pragma unroll
-      for (int u = 0; u < kLsaTE; ++u) {
-        if (upd) {
-          wv[u] = csub(wv[u], cmul(c0, v0[u]));
-          if (two) wv[u] = csub(wv[u], cmul(c1, v1[u]));
+        for (int u = 0; u < kLsaTE; ++u) {
+          const size_t e = t0 + (size_t)u * kLsaBD + threadIdx.x;
+          v[b][u] = (i + b < nv && e < N) ? __ldg(ub + e) : cmk(0.0, 0.0);
         }
-        if (iter) {
-          xv[u] = cfma(d0, v0[u], xv[u]);
-          if (two) xv[u] = cfma(d1, v1[u], xv[u]);
+      }
+#pragma unroll
+      for (int b = 0; b < kLsaVPS; ++b) {
+        if (i + b >= nv) break;
+        const double2 cb = sh_c[i + b], db = sh_x[i + b];
+#pragma unroll
+        for (int u = 0; u < kLsaTE; ++u) {
+          if (upd) wv[u] = csub(wv[u], cmul(cb, v[b][u]));
+          if (iter) xv[u] = cfma(db, v[b][u], xv[u]);
         }
       }
     }
