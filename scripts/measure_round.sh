@@ -3,4 +3,4 @@ for c in C5 C1 C2 C3 C4; do timeout 400 python bench.py --config $c > gpurun_out
 timeout 300 python bench.py --impl reference > gpurun_out/m_ref_C5.log 2>&1
 export HD_GRAPH=0
 python scripts/profile_c5.py 100 C5 > gpurun_out/m_plain.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__grid_size --clock-control none --csv --log-file gpurun_out/m_launches_C5.csv python scripts/profile_c5.py 100 C5 > gpurun_out/m_ncu1.log 2>&1
-python scripts/profile_c5.py 40 C5 > gpurun_out/m_plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_lsa_dots|k_lsa_update|k_stencil2d" -s 60 -c 6 -o gpurun_out/m_full python scripts/profile_c5.py 40 C5 > gpurun_out/m_ncu2.log 2>&1
+python scripts/profile_c5.py 40 C5 > gpurun_out/m_plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_lsa_dots|k_lsa_update" -s 50 -c 4 -o gpurun_out/m_full python scripts/profile_c5.py 40 C5 > gpurun_out/m_ncu2.log 2>&1
