@@ -435,6 +435,7 @@ struct LoopState {
   int iters;      // GmresResult::iterations when done
   int conv;       // converged flag
   int need_tail;  // budget exhausted: the host forms x_{maxit-1} and its monitor
+  int breakdown;  // side-branch monitor: Krylov breakdown, the host monitors x_{iters-1}
 };
 
 // After the monitor of x_{j-1} (src/linalg.cpp:82-88): record the residual,
@@ -456,6 +457,39 @@ __global__ void k_loop_check(LoopState* s, const double* dres, double* res_hist,
   }
   if (dres[1] < 1e-300) {  // hnew of iteration j-1
     s->done = 1;
+    s->iters = j;
+    cudaGraphSetConditional(h, 0);
+  }
+}
+
+// Side-branch monitor (HD_MON_SIDE): body j monitors x_{j-2} concurrently with
+// op(u_j); x_{j-2} is still in place because pass 2 of body j (which writes
+// x_{j-1}) runs after the branch joins, and exits early once done is set.
+__global__ void k_loop_check_lag2(LoopState* s, const double* dres, double* res_hist, double tol,
+                                  cudaGraphConditionalHandle h) {
+  HD_PDL_ENTRY();
+  if (s->done) return;
+  const int j = s->j;
+  if (j < 2) return;
+  const double rr = dres[0];
+  res_hist[j - 2] = rr;
+  if (rr <= tol) {
+    s->conv = 1;
+    s->done = 1;
+    s->iters = j - 1;
+    cudaGraphSetConditional(h, 0);
+  }
+}
+
+// Side-branch monitor: breakdown of iteration j-1 (hnew from its Givens) stops
+// the loop with x_{j-1} formed but not yet monitored (the host does that).
+__global__ void k_loop_breakdown(LoopState* s, const double* dres, cudaGraphConditionalHandle h) {
+  HD_PDL_ENTRY();
+  if (s->done) return;
+  const int j = s->j;
+  if (j >= 1 && dres[1] < 1e-300) {
+    s->done = 1;
+    s->breakdown = 1;
     s->iters = j;
     cudaGraphSetConditional(h, 0);
   }

@@ -173,6 +173,9 @@ struct hd_ctx {
   double* res_host = nullptr;       // pinned
   void* cublas_ws = nullptr;
   bool graph_enabled = true;        // HD_GRAPH=0: host-driven loop
+  bool mon_side = false;            // HD_MON_SIDE=1: monitor of x_{j-2} on the graph body's side branch (measured neutral, opt-in)
+  double2* mon_partials = nullptr;  // side-branch monitor's own grid-reduction scratch
+  unsigned* mon_counter = nullptr;
   int graph_body_kernels = 0;       // own kernels per body execution
   int n_sms = 148;
   // counters

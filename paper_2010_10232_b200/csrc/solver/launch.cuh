@@ -777,6 +777,7 @@ __global__ void k_loop_init(LoopState* s) {
   s->iters = 0;
   s->conv = 0;
   s->need_tail = 0;
+  s->breakdown = 0;
 }
 
 __global__ void k_scale_monitor(double* dres) {
@@ -889,19 +890,37 @@ static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
   LsaArgs ag = a;
   ag.jlag = 1;
   k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st2>>>(ag, G);
+  if (c->mon_side) {
+    // side branch, after the Givens: monitor x_{j-2} (written by pass 2 of the
+    // previous body) with its own reduction scratch, record it, stop on tolerance
+    std::swap(c->st, c->st2);
+    std::swap(c->partials, c->mon_partials);
+    std::swap(c->counter, c->mon_counter);
+    monitor_raw(c, c->x);
+    std::swap(c->st, c->st2);
+    std::swap(c->partials, c->mon_partials);
+    std::swap(c->counter, c->mon_counter);
+    k_scale_monitor<<<1, 1, 0, c->st2>>>(c->dres);
+    k_loop_check_lag2<<<1, 1, 0, c->st2>>>(c->loop_state, c->dres, c->res_hist, tol, h);
+  }
   CK(cudaEventRecord(c->ev_join, c->st2));
   compose_op(c, c->V, c->w, dj);
   CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
   k_lsa_dots<<<G, kLsaBD, lsa_dots_smem(), c->st>>>(a);
   k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a);  // u_{j+1} and the lagged x_{j-1}
-  monitor_raw(c, c->x);
-  k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres);
-  k_loop_check<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, c->res_hist, tol, h);
+  if (c->mon_side) {
+    k_loop_breakdown<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, h);
+  } else {
+    monitor_raw(c, c->x);
+    k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres);
+    k_loop_check<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, c->res_hist, tol, h);
+  }
   k_loop_next<<<1, 1, 0, c->st>>>(c->loop_state, maxit, h);
   cudaGraph_t captured = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(c->st, &captured);
   c->prof_on = prof;
-  c->graph_body_kernels = c->launches - saved_l + 6;  // op + monitor kernels + dots/scale/check/update/givens/next
+  // op + monitor kernels + dots/update/givens/scale/check/next (+ breakdown check when the monitor is on the side)
+  c->graph_body_kernels = c->launches - saved_l + (c->mon_side ? 7 : 6);
   c->matvecs = saved[0];
   c->coarse_solves = saved[1];
   c->shift_solves = saved[2];
@@ -1075,8 +1094,22 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
       int it = ls.iters;
       res.iterations = it;
       res.converged = ls.conv != 0;
-      for (int q = 0; q < (ls.need_tail ? maxit - 1 : it); ++q) res.residuals.push_back(c->res_host[q]);
-      if (ls.need_tail) {  // x_{maxit-1}: its Givens, an iterate-only pass + monitor
+      const int lag = c->mon_side ? 2 : 1;  // monitors recorded by the graph trail the iterate by lag - 1
+      const int recorded = ls.conv ? it : ls.need_tail ? std::max(0, maxit - lag) : it - (lag - 1);
+      for (int q = 0; q < recorded; ++q) res.residuals.push_back(c->res_host[q]);
+      bool tail = ls.need_tail != 0;
+      if (c->mon_side && ((ls.need_tail && maxit >= 2) || ls.breakdown)) {
+        // x_{it-1} (breakdown) or x_{maxit-2} (budget) is formed but its monitor is not recorded yet
+        monitor(c->x);
+        read_scalars(c);
+        res.residuals.push_back(c->hres[0]);
+        if (c->hres[0] <= opt.tolerance) {
+          res.converged = true;
+          if (tail) it = res.iterations = maxit - 1;
+          tail = false;
+        }
+      }
+      if (tail) {  // x_{maxit-1}: its Givens, an iterate-only pass + monitor
         LsaArgs b = lsa_args(c, c->x, maxit - 1, 1, maxit);
         HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(b, G));
         HD_LAUNCH(HD_K_ITERATE, (maxit + 2.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(b));

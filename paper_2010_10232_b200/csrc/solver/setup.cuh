@@ -458,6 +458,7 @@ static void destroy_ctx(hd_ctx* c) {
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->t3); cudaFree(c->V);
   cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
   cudaFree(c->scal); cudaFree(c->dres); cudaFree(c->partials); cudaFree(c->counter);
+  cudaFree(c->mon_partials); cudaFree(c->mon_counter);
   cudaFree(c->dj); cudaFree(c->arn_partials); cudaFree(c->arn_bar);
   cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
   cudaFree(c->lsa_counter);
@@ -763,10 +764,14 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   c->partials = dalloc<double2>(std::max(c->red_blocks, max_stencil_blocks) + 16);
   c->counter = dalloc<unsigned>(4);
   CK(cudaMemset(c->counter, 0, 4 * sizeof(unsigned)));
+  c->mon_partials = dalloc<double2>(std::max(c->red_blocks, max_stencil_blocks) + 16);
+  c->mon_counter = dalloc<unsigned>(4);
+  CK(cudaMemset(c->mon_counter, 0, 4 * sizeof(unsigned)));
   CK(cudaStreamSynchronize(c->st));
   CK(cudaDeviceSynchronize());
   if (const char* e = std::getenv("HD_ARNOLDI")) c->arn_mode = std::atoi(e);
   if (const char* e = std::getenv("HD_GRAPH")) c->graph_enabled = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HD_MON_SIDE")) c->mon_side = std::atoi(e) != 0;
   CK(cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, c->device));
   c->cublas_ws = dalloc<char>(32u << 20);
   CKB(cublasSetWorkspace(c->cb, c->cublas_ws, 32u << 20));

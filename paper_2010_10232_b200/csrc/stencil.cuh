@@ -30,9 +30,13 @@ constexpr int kSRowsMax = 128;
 // ring depth (rows in flight per warp): the band height 2B+1 if that is >= 7,
 // else its smallest multiple >= 8, so that the row loop unrolled over one ring period addresses
 // both the ring slots and the rotating accumulators statically
+// HD_SRING_MULT scales the depth by a whole number of band periods (A/B builds).
+#ifndef HD_SRING_MULT
+#define HD_SRING_MULT 1
+#endif
 template <int B>
 __host__ __device__ constexpr int stencil_ring() {
-  return 2 * B + 1 >= 7 ? 2 * B + 1 : (2 * B + 1) * ((8 + 2 * B) / (2 * B + 1));
+  return HD_SRING_MULT * (2 * B + 1 >= 7 ? 2 * B + 1 : (2 * B + 1) * ((8 + 2 * B) / (2 * B + 1)));
 }
 
 template <int B, int MODE>

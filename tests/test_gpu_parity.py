@@ -571,3 +571,29 @@ def test_long_budget_and_unpreconditioned(tag, maxit):
         r = solver.solve(hd.GmresOptions(maxit, 1e-10))
     meta = dict(iterations=g.iterations, converged=g.converged, residuals=g.residuals, counts=counts)
     _check(r, meta, g.solution, exact_iters=False, env=env)
+
+
+@pytest.mark.parametrize("budget", ["K-2", "K-1", "K", "K+1", 1, 2, 3, 100])
+def test_side_branch_monitor_matches_main_chain(budget, monkeypatch):
+    """The graph body's monitor of x_{j-2} on the side branch (HD_MON_SIDE=1,
+    opt-in) gives the same GmresResult, bit for bit, as the monitor of x_{j-1}
+    on the main chain (HD_MON_SIDE=0), for budgets around the converged count K
+    (K+1: x_{maxit-2} converges in the host's budget tail) and tiny budgets."""
+    s = hd.assemble(hd.point_source_2d(64, 3, 40.0))
+    spec = hd.to_spec("DC_MG", 3, 40.0, **BASE)
+    out = {}
+    for side in (0, 1):
+        monkeypatch.setenv("HD_MON_SIDE", str(side))
+        with hd.Solver(s, spec) as solver:
+            K = solver.solve(hd.GmresOptions(100, 1e-7)).iterations
+            m = budget if isinstance(budget, int) else K + int(budget[1:]) if "+" in budget else K - int(budget[2:])
+            out[side] = (solver.solve(hd.GmresOptions(m, 1e-7)), solver.solve(hd.GmresOptions(m, 1e-7)), m, K)
+    (a, a2, m, K), (b, b2, _, _) = out[0], out[1]
+    assert K > 3
+    for x, y in ((a, b), (a2, b2), (b, b2)):
+        assert (x.iterations, x.converged) == (y.iterations, y.converged)
+        assert x.residuals == y.residuals
+        assert np.array_equal(x.solution, y.solution)
+        assert (x.counts.matvecs, x.counts.coarse_solves, x.counts.shift_solves) == \
+            (y.counts.matvecs, y.counts.coarse_solves, y.counts.shift_solves)
+    assert len(b.residuals) == b.iterations and b.converged == (m >= K)
