@@ -586,7 +586,7 @@ def test_side_branch_monitor_matches_main_chain(budget, monkeypatch):
         monkeypatch.setenv("HD_MON_SIDE", str(side))
         with hd.Solver(s, spec) as solver:
             K = solver.solve(hd.GmresOptions(100, 1e-7)).iterations
-            m = budget if isinstance(budget, int) else K + int(budget[1:]) if "+" in budget else K - int(budget[2:])
+            m = budget if isinstance(budget, int) else K + int(budget[1:] or 0)
             out[side] = (solver.solve(hd.GmresOptions(m, 1e-7)), solver.solve(hd.GmresOptions(m, 1e-7)), m, K)
     (a, a2, m, K), (b, b2, _, _) = out[0], out[1]
     assert K > 3
