@@ -111,12 +111,21 @@ __device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh
 #endif
 constexpr int kLsaUnroll = HD_LSA_UNROLL;
 
-constexpr size_t lsa_dots_smem() { return sizeof(double2) * (4 * kLsaCE + 2 * (kLsaMaxJ + 1)); }
+// Items per chunk and vector: each staged chunk's vector products are split into
+// kLsaSplit sub-chunk items so that the j+1 vectors spread evenly over the warps
+// between the chunk barriers; every split has its own accumulator slots, summed
+// in split order at the end (deterministic).
+#ifndef HD_LSA_SPLIT
+#define HD_LSA_SPLIT 1
+#endif
+constexpr int kLsaSplit = HD_LSA_SPLIT;
+
+constexpr size_t lsa_dots_smem() { return sizeof(double2) * (4 * kLsaCE + kLsaSplit * 2 * (kLsaMaxJ + 1)); }
 
 __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   HD_PDL_ENTRY();
   constexpr int NW = kLsaBD / 32;
-  constexpr int PER = kLsaCE / 32;  // elements per lane per chunk
+  constexpr int PER = kLsaCE / 32 / kLsaSplit;  // elements per lane per item
   extern __shared__ __align__(16) double2 dsm[];
   // w and u_j chunks, double-buffered: the next chunk's pair is copied (cp.async)
   // while the warps stream the basis vectors against the current one
@@ -131,7 +140,7 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   const int nd = j + 1;
   const int nslot = 2 * kLsaMaxJ + 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int q = threadIdx.x; q < nslot; q += kLsaBD) acc[q] = cmk(0.0, 0.0);
+  for (int q = threadIdx.x; q < kLsaSplit * nslot; q += kLsaBD) acc[q] = cmk(0.0, 0.0);
   const size_t N = a.N;
   const double2* uj = a.U + (size_t)j * N;
   const size_t nchunks = (N + kLsaCE - 1) / kLsaCE;
@@ -157,12 +166,14 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
     __syncthreads();  // this chunk's w and u_j visible to every warp
     const double2* ws = wsb + buf * kLsaCE;
     const double2* us = usb + buf * kLsaCE;
-    for (int i = warp; i < nd; i += NW) {
+    for (int t = warp; t < nd * kLsaSplit; t += NW) {
+      const int i = t / kLsaSplit, hs = t % kLsaSplit;
       const double2* ui = a.U + (size_t)i * N + c0;
+      double2* acch = acc + hs * nslot;
       double2 sa = cmk(0.0, 0.0), sb = cmk(0.0, 0.0), ga = cmk(0.0, 0.0), gb = cmk(0.0, 0.0);
 #pragma unroll kLsaUnroll
       for (int q = 0; q < PER; ++q) {
-        const int e = q * 32 + lane;
+        const int e = (hs * PER + q) * 32 + lane;
         const double2 v = e < len ? __ldg(ui + e) : cmk(0.0, 0.0);
         if (q & 1) {
           sb = cadd(sb, cconjmul(v, ws[e]));
@@ -175,8 +186,8 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
       double2 s_ = lsa_warp_sum(cadd(sa, sb));
       double2 g_ = (i < j) ? lsa_warp_sum(cadd(ga, gb)) : cmk(0.0, 0.0);
       if (lane == 0) {
-        acc[i] = cadd(acc[i], s_);
-        if (i < j) acc[kLsaMaxJ + 1 + i] = cadd(acc[kLsaMaxJ + 1 + i], g_);
+        acch[i] = cadd(acch[i], s_);
+        if (i < j) acch[kLsaMaxJ + 1 + i] = cadd(acch[kLsaMaxJ + 1 + i], g_);
       }
     }
     __syncthreads();  // every warp done with this chunk's buffers before they are refilled
@@ -185,7 +196,12 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   __syncthreads();
   for (int q = threadIdx.x; q < nslot; q += kLsaBD) {
     const bool used = q < nd || (q >= kLsaMaxJ + 1 && q < kLsaMaxJ + 1 + j);
-    if (used) a.partials[(size_t)(a.part_offset + blockIdx.x) * nslot + q] = acc[q];
+    if (used) {
+      double2 v = acc[q];
+#pragma unroll
+      for (int h = 1; h < kLsaSplit; ++h) v = cadd(v, acc[h * nslot + q]);
+      a.partials[(size_t)(a.part_offset + blockIdx.x) * nslot + q] = v;
+    }
   }
   if (a.partial_only) return;
   if (!lsa_last_block(a.counter)) return;
