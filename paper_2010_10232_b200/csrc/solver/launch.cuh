@@ -1043,6 +1043,16 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   } else {
     CK(cudaMemsetAsync(c->x0, 0, N * sizeof(double2), c->st));
   }
+  // One host synchronisation before the loop: ||f||, monitor(x0) (scaled on the
+  // device, as in the graph body) and beta are read together.  The operator of
+  // x0 is speculative until monitor(x0) > tol is known; its counts are rolled back.
+  monitor_raw(c, c->x0);
+  HD_LAUNCH(HD_K_VEC, 0.0, k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres));
+  const long snap0[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
+  // r = rhs' - op(x0); beta = ||r||; V0 = r / beta  (src/linalg.cpp:24-33)
+  compose_op(c, c->x0, c->w);
+  HD_LAUNCH(HD_K_VEC, 3 * P, k_sub<<<grid_for(N), 256, 0, c->st>>>(c->rhsp, c->w, c->w, N));
+  HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, nullptr, nullptr, N, red_of(c, c->dres + 2), c->g));
   read_scalars(c);
   const double fnorm = c->hres[3];
   const double scale = fnorm > 0.0 ? fnorm : 1.0;
@@ -1051,25 +1061,20 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   auto monitor = [&](const double2* xv) {
     op_apply(c, OP_RESNORM, opA(c), xv, c->f, nullptr, 0.0, c->dres + 0, scale);
   };
-  monitor(c->x0);
-  read_scalars(c);
   const double r0 = c->hres[0];
   if (r0 <= opt.tolerance) {  // src/linalg.cpp:17-22
+    c->matvecs = snap0[0];
+    c->coarse_solves = snap0[1];
+    c->shift_solves = snap0[2];
+    c->vcycles = snap0[3];
     res.converged = true;
     res.residuals.push_back(r0);
     CK(cudaMemcpyAsync(xout, c->x0, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
     return res;
   }
-  // r = rhs' - op(x0); beta = ||r||; V0 = r / beta  (src/linalg.cpp:24-33)
-  compose_op(c, c->x0, c->w);
-  HD_LAUNCH(HD_K_VEC, 3 * P, k_sub<<<grid_for(N), 256, 0, c->st>>>(c->rhsp, c->w, c->w, N));
-  HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, nullptr, nullptr, N, red_of(c, c->dres + 2), c->g));
-  read_scalars(c);
   const double beta = c->hres[2];
-  if (beta == 0.0) {
-    monitor(c->x0);
-    read_scalars(c);
-    res.converged = c->hres[0] <= opt.tolerance;
+  if (beta == 0.0) {  // the reference monitors x0 again: the same r0 > tol
+    res.converged = false;
     CK(cudaMemcpyAsync(xout, c->x0, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
     return res;
   }
