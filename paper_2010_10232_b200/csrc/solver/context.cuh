@@ -165,6 +165,11 @@ struct hd_ctx {
   // graph-resident GMRES loop (WHILE conditional node), rebuilt when (maxit, tol) change
   cudaGraph_t loop_graph = nullptr;
   cudaGraphExec_t loop_exec = nullptr;
+  bool pre_graph = true;               // HD_PRE_GRAPH=0: eager prelude launches
+  cudaGraphExec_t pre_exec = nullptr;  // GMRES prelude (rhs', start, monitor(x0), op(x0), beta)
+  const void* pre_g = nullptr;          // c->g the prelude was captured with (ensure_gmres may move it)
+  long pre_dcnt[4] = {0, 0, 0, 0}, pre_dsnap[4] = {0, 0, 0, 0};
+  int pre_dl = 0, pre_db = 0;
   int loop_maxit = -1;
   double loop_tol = -1.0;
   LoopState* loop_state = nullptr;

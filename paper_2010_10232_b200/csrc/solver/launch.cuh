@@ -1020,39 +1020,80 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   c->launches = c->lib_calls = 0;
   const int nb = c->red_blocks;
   const double P = 16.0 * static_cast<double>(N);
-  // ||f|| (monitor scale, src/precond.cpp:258)
-  HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->f, nullptr, nullptr, N, red_of(c, c->dres + 3), c->scal + 2));
-  // rhs' = P MG^-1 f   (src/precond.cpp:247-253)
-  const double2* b = c->f;
-  if (c->spec.shift) {
-    ++c->shift_solves;
-    c->vcycles += c->spec.cycles;
-    mg_solve(c, c->f, c->t2);
-    b = c->t2;
-  }
-  if (c->spec.deflate) {
-    ++c->coarse_solves;
-    project(c, b, c->rhsp);
+  // The prelude up to the one host synchronisation (no host decisions inside) is
+  // captured once per context as a graph and replayed: small systems are
+  // launch-bound there.  Counter and launch deltas of the capture are replayed too.
+  long* cnt[4] = {&c->matvecs, &c->coarse_solves, &c->shift_solves, &c->vcycles};
+  long snap0[4] = {0, 0, 0, 0};  // counters before the speculative op(x0)
+  auto prelude = [&]() {
+    // ||f|| (monitor scale, src/precond.cpp:258)
+    HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->f, nullptr, nullptr, N, red_of(c, c->dres + 3), c->scal + 2));
+    // rhs' = P MG^-1 f   (src/precond.cpp:247-253)
+    const double2* b = c->f;
+    if (c->spec.shift) {
+      ++c->shift_solves;
+      c->vcycles += c->spec.cycles;
+      mg_solve(c, c->f, c->t2);
+      b = c->t2;
+    }
+    if (c->spec.deflate) {
+      ++c->coarse_solves;
+      project(c, b, c->rhsp);
+    } else {
+      CK(cudaMemcpyAsync(c->rhsp, b, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    }
+    // start = Q f (src/precond.cpp:255-256)
+    if (c->spec.deflate) {
+      apply_Q(c, c->f, c->x0);
+      ++c->coarse_solves;
+    } else {
+      CK(cudaMemsetAsync(c->x0, 0, N * sizeof(double2), c->st));
+    }
+    // ||f||, monitor(x0) (scaled on the device, as in the graph body) and beta are
+    // read with one host synchronisation after the prelude.  The operator of x0 is
+    // speculative until monitor(x0) > tol is known; its counts are rolled back.
+    monitor_raw(c, c->x0);
+    HD_LAUNCH(HD_K_VEC, 0.0, k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres));
+    for (int q = 0; q < 4; ++q) snap0[q] = *cnt[q];
+    // r = rhs' - op(x0); beta = ||r||; V0 = r / beta  (src/linalg.cpp:24-33)
+    compose_op(c, c->x0, c->w);
+    HD_LAUNCH(HD_K_VEC, 3 * P, k_sub<<<grid_for(N), 256, 0, c->st>>>(c->rhsp, c->w, c->w, N));
+    HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, nullptr, nullptr, N, red_of(c, c->dres + 2), c->g));
+  };
+  if (c->graph_enabled && !c->prof_on && c->pre_graph) {
+    if (!c->pre_exec || c->pre_g != c->g) {
+      if (c->pre_exec) cudaGraphExecDestroy(c->pre_exec);
+      c->pre_exec = nullptr;
+      const long c0[4] = {*cnt[0], *cnt[1], *cnt[2], *cnt[3]};
+      const int l0 = c->launches, b0 = c->lib_calls;
+      cudaGraph_t pg = nullptr;
+      CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
+      prelude();
+      const cudaError_t ec = cudaStreamEndCapture(c->st, &pg);
+      CK(ec);
+      CK(cudaGraphInstantiate(&c->pre_exec, pg, 0));
+      CK(cudaGraphDestroy(pg));
+      for (int q = 0; q < 4; ++q) {
+        c->pre_dcnt[q] = *cnt[q] - c0[q];
+        c->pre_dsnap[q] = snap0[q] - c0[q];
+        *cnt[q] = c0[q];
+      }
+      c->pre_dl = c->launches - l0;
+      c->pre_db = c->lib_calls - b0;
+      c->launches = l0;
+      c->lib_calls = b0;
+      c->pre_g = c->g;
+    }
+    for (int q = 0; q < 4; ++q) {
+      snap0[q] = *cnt[q] + c->pre_dsnap[q];
+      *cnt[q] += c->pre_dcnt[q];
+    }
+    c->launches += c->pre_dl;
+    c->lib_calls += c->pre_db;
+    CK(cudaGraphLaunch(c->pre_exec, c->st));
   } else {
-    CK(cudaMemcpyAsync(c->rhsp, b, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
+    prelude();
   }
-  // start = Q f (src/precond.cpp:255-256)
-  if (c->spec.deflate) {
-    apply_Q(c, c->f, c->x0);
-    ++c->coarse_solves;
-  } else {
-    CK(cudaMemsetAsync(c->x0, 0, N * sizeof(double2), c->st));
-  }
-  // One host synchronisation before the loop: ||f||, monitor(x0) (scaled on the
-  // device, as in the graph body) and beta are read together.  The operator of
-  // x0 is speculative until monitor(x0) > tol is known; its counts are rolled back.
-  monitor_raw(c, c->x0);
-  HD_LAUNCH(HD_K_VEC, 0.0, k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres));
-  const long snap0[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
-  // r = rhs' - op(x0); beta = ||r||; V0 = r / beta  (src/linalg.cpp:24-33)
-  compose_op(c, c->x0, c->w);
-  HD_LAUNCH(HD_K_VEC, 3 * P, k_sub<<<grid_for(N), 256, 0, c->st>>>(c->rhsp, c->w, c->w, N));
-  HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, nullptr, nullptr, N, red_of(c, c->dres + 2), c->g));
   read_scalars(c);
   const double fnorm = c->hres[3];
   const double scale = fnorm > 0.0 ? fnorm : 1.0;

@@ -463,6 +463,7 @@ static void destroy_ctx(hd_ctx* c) {
   cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
   cudaFree(c->lsa_counter);
   if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
+  if (c->pre_exec) cudaGraphExecDestroy(c->pre_exec);
   if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
   cudaFree(c->loop_state); cudaFree(c->res_hist); cudaFree(c->cublas_ws);
   if (c->loop_host) cudaFreeHost(c->loop_host);
@@ -772,6 +773,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   if (const char* e = std::getenv("HD_ARNOLDI")) c->arn_mode = std::atoi(e);
   if (const char* e = std::getenv("HD_GRAPH")) c->graph_enabled = std::atoi(e) != 0;
   if (const char* e = std::getenv("HD_MON_SIDE")) c->mon_side = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HD_PRE_GRAPH")) c->pre_graph = std::atoi(e) != 0;
   CK(cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, c->device));
   c->cublas_ws = dalloc<char>(32u << 20);
   CKB(cublasSetWorkspace(c->cb, c->cublas_ws, 32u << 20));

@@ -597,3 +597,21 @@ def test_side_branch_monitor_matches_main_chain(budget, monkeypatch):
         assert (x.counts.matvecs, x.counts.coarse_solves, x.counts.shift_solves) == \
             (y.counts.matvecs, y.counts.coarse_solves, y.counts.shift_solves)
     assert len(b.residuals) == b.iterations and b.converged == (m >= K)
+
+
+def test_prelude_graph_matches_eager(monkeypatch):
+    """The GMRES prelude (rhs', start, monitor(x0), op(x0), beta) replayed as a
+    cached graph (default) equals the eager launches (HD_PRE_GRAPH=0) bit for bit,
+    also after a budget change that reallocates the Hessenberg buffers."""
+    s = hd.assemble(hd.point_source_2d(64, 3, 40.0))
+    spec = hd.to_spec("DC_MG", 3, 40.0, **BASE)
+    with hd.Solver(s, spec) as solver:
+        a = [solver.solve(hd.GmresOptions(m, 1e-7)) for m in (5, 100, 5)]
+    monkeypatch.setenv("HD_PRE_GRAPH", "0")
+    with hd.Solver(s, spec) as solver:
+        b = [solver.solve(hd.GmresOptions(m, 1e-7)) for m in (5, 100, 5)]
+    for x, y in zip(a, b):
+        assert (x.iterations, x.converged, x.residuals) == (y.iterations, y.converged, y.residuals)
+        assert np.array_equal(x.solution, y.solution)
+        assert (x.counts.matvecs, x.counts.coarse_solves, x.counts.shift_solves) == \
+            (y.counts.matvecs, y.counts.coarse_solves, y.counts.shift_solves)
