@@ -456,9 +456,8 @@ struct LoopState {
 
 // After the monitor of x_{j-1} (src/linalg.cpp:82-88): record the residual,
 // stop on tolerance or Krylov breakdown of the previous step.
-__global__ void k_loop_check(LoopState* s, const double* dres, double* res_hist, double tol,
-                             cudaGraphConditionalHandle h) {
-  HD_PDL_ENTRY();
+__device__ __forceinline__ void loop_check(LoopState* s, const double* dres, double* res_hist, double tol,
+                                           cudaGraphConditionalHandle h) {
   if (s->done) return;
   const int j = s->j;
   if (j < 1) return;
@@ -476,6 +475,12 @@ __global__ void k_loop_check(LoopState* s, const double* dres, double* res_hist,
     s->iters = j;
     cudaGraphSetConditional(h, 0);
   }
+}
+
+__global__ void k_loop_check(LoopState* s, const double* dres, double* res_hist, double tol,
+                             cudaGraphConditionalHandle h) {
+  HD_PDL_ENTRY();
+  loop_check(s, dres, res_hist, tol, h);
 }
 
 // Side-branch monitor (HD_MON_SIDE): body j monitors x_{j-2} concurrently with
@@ -511,8 +516,7 @@ __global__ void k_loop_breakdown(LoopState* s, const double* dres, cudaGraphCond
   }
 }
 
-__global__ void k_loop_next(LoopState* s, int maxit, cudaGraphConditionalHandle h) {
-  HD_PDL_ENTRY();
+__device__ __forceinline__ void loop_next(LoopState* s, int maxit, cudaGraphConditionalHandle h) {
   if (s->done) return;
   if (s->j + 1 >= maxit) {
     s->done = 1;
@@ -522,6 +526,22 @@ __global__ void k_loop_next(LoopState* s, int maxit, cudaGraphConditionalHandle 
     return;
   }
   s->j += 1;
+}
+
+__global__ void k_loop_next(LoopState* s, int maxit, cudaGraphConditionalHandle h) {
+  HD_PDL_ENTRY();
+  loop_next(s, maxit, h);
+}
+
+// The graph body's tail in one launch: monitor scaling (raw norm / ||f||),
+// convergence / breakdown check of x_{j-1}, and the step to j+1.
+__global__ void k_loop_step(LoopState* s, double* dres, double* res_hist, double tol, int maxit,
+                            cudaGraphConditionalHandle h) {
+  HD_PDL_ENTRY();
+  const double f = dres[3];
+  dres[0] = dres[0] / (f > 0.0 ? f : 1.0);
+  loop_check(s, dres, res_hist, tol, h);
+  loop_next(s, maxit, h);
 }
 
 }  // namespace hd

@@ -910,17 +910,16 @@ static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
   k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a);  // u_{j+1} and the lagged x_{j-1}
   if (c->mon_side) {
     k_loop_breakdown<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, h);
+    k_loop_next<<<1, 1, 0, c->st>>>(c->loop_state, maxit, h);
   } else {
     monitor_raw(c, c->x);
-    k_scale_monitor<<<1, 1, 0, c->st>>>(c->dres);
-    k_loop_check<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, c->res_hist, tol, h);
+    k_loop_step<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, c->res_hist, tol, maxit, h);  // scale, check, next
   }
-  k_loop_next<<<1, 1, 0, c->st>>>(c->loop_state, maxit, h);
   cudaGraph_t captured = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(c->st, &captured);
   c->prof_on = prof;
-  // op + monitor kernels + dots/update/givens/scale/check/next (+ breakdown check when the monitor is on the side)
-  c->graph_body_kernels = c->launches - saved_l + (c->mon_side ? 7 : 6);
+  // op + monitor kernels + givens/dots/update/step (side monitor: scale/check/breakdown/next instead of step)
+  c->graph_body_kernels = c->launches - saved_l + (c->mon_side ? 7 : 4);
   c->matvecs = saved[0];
   c->coarse_solves = saved[1];
   c->shift_solves = saved[2];

@@ -1,7 +1,7 @@
-# A/B of the pre-loop: sync1 = one host synchronisation, eager launches; pre = the same captured as a cached graph
+# A/B: pre_keep = prelude graph; step = plus one fused scale/check/next kernel in the graph body
 set -x
 for r in 1 2; do
-for v in sync1 pre; do
+for v in pre_keep step; do
   for c in C2 C3 C4 C5; do HD_LIBRARY=_ab/libhelmdef_$v.so timeout 300 python scripts/ab_time.py $c 11; done
 done
 done
