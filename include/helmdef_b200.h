@@ -40,7 +40,9 @@ typedef enum {
   HD_ERR_INVALID = 1,     /* bad argument / unsupported combination        */
   HD_ERR_CUDA = 2,        /* CUDA runtime / cuBLAS / cuSOLVER failure       */
   HD_ERR_FACTOR = 3,      /* singular coarse operator or zero diagonal      */
-  HD_ERR_NO_DEVICE = 4    /* no CUDA device: there is no CPU fallback       */
+  HD_ERR_NO_DEVICE = 4,   /* no CUDA device: there is no CPU fallback       */
+  HD_ERR_NONFINITE = 5    /* NaN/Inf residual or Arnoldi norm: the solve
+                             stopped (the reference would run on to maxit) */
 } hd_status;
 
 /* Wave-number field kinds (WaveField, inc/problems.hpp:18-29), plus the
@@ -102,7 +104,10 @@ typedef struct {
   double drop;
   int shift;
   double beta2;
-  int cycles;          /* >= 1: multigrid V-cycles; 0: exact shifted inverse (unsupported here) */
+  int cycles;          /* >= 1: multigrid V-cycles; <= 0: exact shifted inverse
+                          (C_ex, src/precond.cpp:203-211): fast diagonalisation
+                          (2D constant k), banded LU (1D), dense or block
+                          tridiagonal LU (layered / wedge fields)             */
   int smooth_steps;
   double omega;
   int coarsest;        /* per-dimension size solved directly (reference: 32) */
@@ -149,9 +154,10 @@ hd_status hd_assemble_field(const hd_problem* pb, double* shift_mass_2d);
 
 /* ---- the drop-in solver ------------------------------------------------ */
 
-/* compose(): build the preconditioner on device(s).  devices/n_devices: the
- * CUDA devices to use (NULL/0 = current device); n_devices > 1 is reserved
- * for the row-slab decomposition and is rejected in this build. */
+/* compose() (inc/precond.hpp:149, src/precond.cpp:196-265): build the
+ * preconditioner on one device.  devices/n_devices: the CUDA device to use
+ * (NULL/0 = current device).  n_devices > 1 is rejected: the multi-GPU
+ * program is one process per GPU, each calling hd_create_dist for its slab. */
 hd_status hd_create(const hd_system* sys, const hd_precond* spec, const int* devices,
                     int n_devices, hd_ctx** out);
 

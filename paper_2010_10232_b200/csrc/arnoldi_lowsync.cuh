@@ -123,7 +123,6 @@ constexpr int kLsaSplit = HD_LSA_SPLIT;
 constexpr size_t lsa_dots_smem() { return sizeof(double2) * (4 * kLsaCE + kLsaSplit * 2 * (kLsaMaxJ + 1)); }
 
 __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
-  HD_PDL_ENTRY();
   constexpr int NW = kLsaBD / 32;
   constexpr int PER = kLsaCE / 32 / kLsaSplit;  // elements per lane per item
   extern __shared__ __align__(16) double2 dsm[];
@@ -253,7 +252,6 @@ __device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh
 
 // row slabs: combine the partials of all slabs (nparts CTA slots, slab order)
 __global__ void __launch_bounds__(kLsaBD) k_lsa_dots_finish(LsaArgs a, int nparts) {
-  HD_PDL_ENTRY();
   __shared__ double2 sh_s[kLsaMaxJ + 1];
   __shared__ double2 sh_lj[kLsaMaxJ];
   __shared__ double2 hsm[kLsaMaxJ + 1];
@@ -270,7 +268,6 @@ __device__ __forceinline__ double2 lsa_cdiv(double2 a, double2 b) { return cmul(
 // lagged iterate x_{j-1} = x0 + sum_{i<j} c'_i u_i (src/linalg.cpp:78-80);
 // mode 1 (budget exhausted): only x_j = x0 + sum_{i<=j} c'_i u_i.
 __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
-  HD_PDL_ENTRY();
   constexpr int NW = kLsaBD / 32;
   __shared__ double2 sh_c[kLsaMaxJ + 1];
   __shared__ double2 sh_x[kLsaMaxJ + 1];
@@ -355,7 +352,6 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
 // nparts = gridDim.x of the update pass.  Dynamic smem: packed R + work.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kLsaBD) k_lsa_givens(LsaArgs a, int nparts) {
-  HD_PDL_ENTRY();
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double s_hnew;
   if (a.done && *((volatile const int*)a.done)) return;
@@ -452,6 +448,7 @@ struct LoopState {
   int conv;       // converged flag
   int need_tail;  // budget exhausted: the host forms x_{maxit-1} and its monitor
   int breakdown;  // side-branch monitor: Krylov breakdown, the host monitors x_{iters-1}
+  int nonfinite;  // NaN/Inf residual or hnew: stopped, the host reports an error
 };
 
 // After the monitor of x_{j-1} (src/linalg.cpp:82-88): record the residual,
@@ -463,6 +460,13 @@ __device__ __forceinline__ void loop_check(LoopState* s, const double* dres, dou
   if (j < 1) return;
   const double rr = dres[0];
   res_hist[j - 1] = rr;
+  if (!isfinite(rr) || !isfinite(dres[1])) {  // poisoned solve: stop instead of running to maxit
+    s->nonfinite = 1;
+    s->done = 1;
+    s->iters = j;
+    cudaGraphSetConditional(h, 0);
+    return;
+  }
   if (rr <= tol) {
     s->conv = 1;
     s->done = 1;
@@ -479,7 +483,6 @@ __device__ __forceinline__ void loop_check(LoopState* s, const double* dres, dou
 
 __global__ void k_loop_check(LoopState* s, const double* dres, double* res_hist, double tol,
                              cudaGraphConditionalHandle h) {
-  HD_PDL_ENTRY();
   loop_check(s, dres, res_hist, tol, h);
 }
 
@@ -488,7 +491,6 @@ __global__ void k_loop_check(LoopState* s, const double* dres, double* res_hist,
 // x_{j-1}) runs after the branch joins, and exits early once done is set.
 __global__ void k_loop_check_lag2(LoopState* s, const double* dres, double* res_hist, double tol,
                                   cudaGraphConditionalHandle h) {
-  HD_PDL_ENTRY();
   if (s->done) return;
   const int j = s->j;
   if (j < 2) return;
@@ -505,7 +507,6 @@ __global__ void k_loop_check_lag2(LoopState* s, const double* dres, double* res_
 // Side-branch monitor: breakdown of iteration j-1 (hnew from its Givens) stops
 // the loop with x_{j-1} formed but not yet monitored (the host does that).
 __global__ void k_loop_breakdown(LoopState* s, const double* dres, cudaGraphConditionalHandle h) {
-  HD_PDL_ENTRY();
   if (s->done) return;
   const int j = s->j;
   if (j >= 1 && dres[1] < 1e-300) {
@@ -529,7 +530,6 @@ __device__ __forceinline__ void loop_next(LoopState* s, int maxit, cudaGraphCond
 }
 
 __global__ void k_loop_next(LoopState* s, int maxit, cudaGraphConditionalHandle h) {
-  HD_PDL_ENTRY();
   loop_next(s, maxit, h);
 }
 
@@ -537,7 +537,6 @@ __global__ void k_loop_next(LoopState* s, int maxit, cudaGraphConditionalHandle 
 // convergence / breakdown check of x_{j-1}, and the step to j+1.
 __global__ void k_loop_step(LoopState* s, double* dres, double* res_hist, double tol, int maxit,
                             cudaGraphConditionalHandle h) {
-  HD_PDL_ENTRY();
   const double f = dres[3];
   dres[0] = dres[0] / (f > 0.0 ? f : 1.0);
   loop_check(s, dres, res_hist, tol, h);

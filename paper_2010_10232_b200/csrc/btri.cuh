@@ -83,7 +83,6 @@ struct BtriArgs {
 template <class T>
 __global__ void k_btri_blocks(GenLevel L, int q, int m, int nb, T* __restrict__ D, T* __restrict__ Bu,
                               T* __restrict__ Cl) {
-  HD_PDL_ENTRY();
   const int n = L.n;
   const size_t mm = (size_t)m * m, tot = (size_t)nb * mm;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
@@ -295,7 +294,6 @@ __device__ __forceinline__ void btri_prefetch_step(const BtriArgs& a, int s, int
 
 template <class T, int KR>
 __global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_btri_solve(BtriArgs a) {
-  HD_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);

@@ -6,13 +6,6 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
-// Programmatic dependent launch: every solver kernel first waits for the grids
-// it depends on to complete (and their writes to be visible), then lets its
-// own dependents start launching.  Both are no-ops for an ordinary launch; the
-// loop graph turns kernel->kernel edges into programmatic ones (pdl_edges in
-// solver/launch.cuh), so the next kernel's launch overlaps this one's tail.
-#define HD_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
-
 namespace hd {
 
 __host__ __device__ __forceinline__ double2 cmk(double r, double i) { return make_double2(r, i); }

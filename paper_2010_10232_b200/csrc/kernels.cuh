@@ -49,161 +49,11 @@ constexpr int kTX = 128;  // threads (columns) per stencil CTA
 constexpr int kNS = 8;    // cp.async ring depth (rows in flight per CTA)
 
 // ---------------------------------------------------------------------------
-// 2D stencil: one thread per column, the CTA streams a strip of rows through a
-// cp.async ring in shared memory; the x pass produces P = Sx x - c Mx x and
-// Q = Mx x per row into register queues of depth 2B+1; the y pass combines
-// y = sum_d My(iy,d) P(iy+d) + Sy(iy,d) Q(iy+d).
-// ---------------------------------------------------------------------------
-template <int B, int MODE>
-__global__ void __launch_bounds__(kTX) k_op2d(LevelDev L, const double2* __restrict__ x,
-                                              const double2* __restrict__ bv, double2* __restrict__ out,
-                                              double omega, int RY, RedOut red) {
-  HD_PDL_ENTRY();
-  constexpr int NB = 2 * B + 1;
-  constexpr int W = kTX + 2 * B;
-  constexpr bool NEED_B = (MODE != OP_APPLY);
-  __shared__ __align__(16) double2 xs[kNS][W];
-  __shared__ __align__(16) double2 bs[NEED_B ? kNS : 1][kTX];
-  __shared__ double cy[2][64][NB];  // (My, Sy) rows of this strip (RY <= 64)
-  __shared__ double2 scratch[32];
-
-  const int n = L.n;
-  const int t = threadIdx.x;
-  const int x0 = blockIdx.x * kTX;
-  const int y0 = blockIdx.y * RY;
-  const int yend = min(y0 + RY, n);
-  const int nout = yend - y0;
-  const int nin = nout + 2 * B;
-  const int ix = x0 + t;
-  const bool colv = ix < n;
-
-  for (int e = t; e < nout * NB; e += kTX) {
-    const int r = e / NB, d = e % NB;
-    cy[0][r][d] = L.M[(size_t)(y0 + r) * NB + d];
-    cy[1][r][d] = L.S[(size_t)(y0 + r) * NB + d];
-  }
-  double sx[NB], mx[NB];
-#pragma unroll
-  for (int j = 0; j < NB; ++j) {
-    sx[j] = colv ? L.S[(size_t)ix * NB + j] : 0.0;
-    mx[j] = colv ? L.M[(size_t)ix * NB + j] : 0.0;
-  }
-
-  auto load = [&](int k) {
-    const int r = y0 - B + k;
-    const int s = k % kNS;
-    const bool rv = (r >= 0) && (r < n);
-    const double2* rowp = x + (size_t)(rv ? r : 0) * n;
-    int col = x0 - B + t;
-    bool v = rv && col >= 0 && col < n;
-    cp_async16(&xs[s][t], rowp + (v ? col : 0), v);
-    if (t < 2 * B) {
-      col = x0 - B + kTX + t;
-      v = rv && col >= 0 && col < n;
-      cp_async16(&xs[s][kTX + t], rowp + (v ? col : 0), v);
-    }
-    if (NEED_B) {
-      const int rb = r - B;  // output row consumed at the same step
-      v = (rb >= y0) && (rb < yend) && colv;
-      cp_async16(&bs[s][t], bv + (v ? (size_t)rb * n + ix : 0), v);
-    }
-  };
-
-#pragma unroll
-  for (int k = 0; k < kNS - 1; ++k) {
-    if (k < nin) load(k);
-    cp_async_commit();
-  }
-  double2 P[NB], Q[NB];
-  double2 XC[B + 1];  // this column's x on the last B+1 input rows (Jacobi centre)
-#pragma unroll
-  for (int j = 0; j < NB; ++j) P[j] = Q[j] = cmk(0.0, 0.0);
-#pragma unroll
-  for (int j = 0; j <= B; ++j) XC[j] = cmk(0.0, 0.0);
-  double acc = 0.0;
-  const double2 c = L.c;
-
-  for (int k = 0; k < nin; ++k) {
-    cp_async_wait<kNS - 2>();
-    __syncthreads();
-    if (k + kNS - 1 < nin) load(k + kNS - 1);
-    cp_async_commit();
-    const int s = k % kNS;
-    double2 u = cmk(0.0, 0.0), v = cmk(0.0, 0.0);
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      const double2 xv = xs[s][t + j];
-      u = cfma_r(sx[j], xv, u);
-      v = cfma_r(mx[j], xv, v);
-    }
-#pragma unroll
-    for (int j = 0; j < NB - 1; ++j) {
-      P[j] = P[j + 1];
-      Q[j] = Q[j + 1];
-    }
-    P[NB - 1] = csub(u, cmul(c, v));
-    Q[NB - 1] = v;
-    if (MODE == OP_JACOBI) {
-#pragma unroll
-      for (int j = 0; j < B; ++j) XC[j] = XC[j + 1];
-      XC[B] = xs[s][t + B];
-    }
-    if (k >= 2 * B) {
-      const int ro = k - 2 * B;  // output row offset within the strip
-      const int iy = y0 + ro;
-      double2 y = cmk(0.0, 0.0);
-#pragma unroll
-      for (int d = 0; d < NB; ++d) {
-        y = cfma_r(cy[0][ro][d], P[d], y);
-        y = cfma_r(cy[1][ro][d], Q[d], y);
-      }
-      if (colv) {
-        const size_t gi = (size_t)iy * n + ix;
-        if (MODE == OP_APPLY) {
-          out[gi] = y;
-        } else if (MODE == OP_RESID) {
-          out[gi] = csub(bs[s][t], y);
-        } else if (MODE == OP_RESNORM) {
-          acc += cnorm2(csub(bs[s][t], y));
-        } else {  // damped Jacobi: x + omega D^-1 (b - L x)
-          const double myc = cy[0][ro][B], syc = cy[1][ro][B];
-          const double2 D = csub(cmk(myc * sx[B] + syc * mx[B], 0.0), cscale(myc * mx[B], c));
-          const double2 xc = XC[0];
-          const double2 r = csub(bs[s][t], y);
-          out[gi] = cadd(xc, cscale(omega, cmul(cinv(D), r)));
-        }
-      }
-    }
-  }
-  cp_async_wait<0>();
-  if (MODE == OP_RESNORM) {
-    double2 total;
-    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) / red.scale;
-  }
-}
-
-// x = omega D^-1 b: the first Jacobi sweep from a zero iterate
-// (src/precond.cpp:140 with x = 0, src/precond.cpp:150,160).
-__global__ void k_jacobi0_2d(LevelDev L, const double2* __restrict__ b, double2* __restrict__ out, double omega) {
-  HD_PDL_ENTRY();
-  const int n = L.n, NB = 2 * L.b + 1;
-  const size_t N = (size_t)n * n;
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
-    const int iy = (int)(g / n), ix = (int)(g % n);
-    const double my = L.M[(size_t)iy * NB + L.b], sy = L.S[(size_t)iy * NB + L.b];
-    const double mxx = L.M[(size_t)ix * NB + L.b], sxx = L.S[(size_t)ix * NB + L.b];
-    const double2 D = csub(cmk(my * sxx + sy * mxx, 0.0), cscale(my * mxx, L.c));
-    out[g] = cscale(omega, cmul(cinv(D), b[g]));
-  }
-}
-
-// ---------------------------------------------------------------------------
 // 1D banded operator L = S - c M (+ corner), one thread per row.
 // ---------------------------------------------------------------------------
 template <int MODE>
 __global__ void k_op1d(LevelDev L, const double2* __restrict__ x, const double2* __restrict__ bv,
                        double2* __restrict__ out, double omega, RedOut red, const int* xidx, size_t xstride) {
-  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   if (xidx) x += (size_t)(*xidx) * xstride;
   const int n = L.n, b = L.b, NB = 2 * b + 1;
@@ -238,7 +88,6 @@ __global__ void k_op1d(LevelDev L, const double2* __restrict__ x, const double2*
 }
 
 __global__ void k_jacobi0_1d(LevelDev L, const double2* __restrict__ b, double2* __restrict__ out, double omega) {
-  HD_PDL_ENTRY();
   const int n = L.n, NB = 2 * L.b + 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double2 D = csub(cmk(L.S[(size_t)i * NB + L.b], 0.0), cscale(L.M[(size_t)i * NB + L.b], L.c));
@@ -295,7 +144,6 @@ __device__ __forceinline__ int pweights(const Stencil& z, int i, int nc, int* q,
 template <int DIM>
 __global__ void k_restrict(Stencil z, const double2* __restrict__ r, int nf, int nc, double2* __restrict__ outc,
                            double* __restrict__ outp) {
-  HD_PDL_ENTRY();
   double w[5];
   const int olo = rweights(z, w);
   const int nw = z.kind == 0 ? 3 : 5;
@@ -334,7 +182,6 @@ __global__ void k_restrict(Stencil z, const double2* __restrict__ r, int nf, int
 template <int DIM, int PMODE>
 __global__ void k_prolong(Stencil z, const double2* __restrict__ ec, const double* __restrict__ ep, int nf, int nc,
                           const double2* __restrict__ s, double2* __restrict__ out) {
-  HD_PDL_ENTRY();
   const size_t NF = DIM == 2 ? (size_t)nf * nf : (size_t)nf;
   const size_t NC = DIM == 2 ? (size_t)nc * nc : (size_t)nc;
   auto ce = [&](size_t qi) -> double2 { return PMODE == 0 ? ec[qi] : cmk(ep[qi], ep[qi + NC]); };
@@ -364,7 +211,6 @@ __global__ void k_prolong(Stencil z, const double2* __restrict__ ec, const doubl
 // dst = conj(a) . b
 __global__ void k_dot(const double2* __restrict__ a, const double2* __restrict__ b, size_t N, RedOut red,
                       double2* dst) {
-  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   double2 acc = cmk(0.0, 0.0);
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
@@ -376,7 +222,6 @@ __global__ void k_dot(const double2* __restrict__ a, const double2* __restrict__
 // w -= h * vi ; dst = conj(vn) . w      (one fused MGS step)
 __global__ void k_axpy_dot(double2* __restrict__ w, const double2* __restrict__ vi, const double2* __restrict__ h,
                            const double2* __restrict__ vn, size_t N, RedOut red, double2* dst) {
-  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   const double2 hh = *h;
   double2 acc = cmk(0.0, 0.0);
@@ -392,7 +237,6 @@ __global__ void k_axpy_dot(double2* __restrict__ w, const double2* __restrict__ 
 // w -= h * vi ; hnew = ||w||  -> dst (as complex (hnew, 0)) and *dnorm
 __global__ void k_axpy_norm(double2* __restrict__ w, const double2* __restrict__ vi, const double2* __restrict__ h,
                             size_t N, RedOut red, double2* dst) {
-  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   const double2 hh = h ? *h : cmk(0.0, 0.0);
   double acc = 0.0;
@@ -415,7 +259,6 @@ __global__ void k_axpy_norm(double2* __restrict__ w, const double2* __restrict__
 // out = a - b
 __global__ void k_sub(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ out,
                       size_t N) {
-  HD_PDL_ENTRY();
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
     out[g] = csub(a[g], b[g]);
 }
@@ -423,7 +266,6 @@ __global__ void k_sub(const double2* __restrict__ a, const double2* __restrict__
 // dst = src / h (h real, read from device; the reference's `w / hnew`)
 __global__ void k_scale_inv(double2* __restrict__ dst, const double2* __restrict__ src, const double* __restrict__ h,
                             size_t N) {
-  HD_PDL_ENTRY();
   const double s = *h;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
     const double2 v = src[g];
@@ -434,7 +276,6 @@ __global__ void k_scale_inv(double2* __restrict__ dst, const double2* __restrict
 // x = x0 + sum_{i<m} y_i V_i   (basis vectors contiguous, stride N)
 __global__ void k_iterate(double2* __restrict__ x, const double2* __restrict__ x0, const double2* __restrict__ V,
                           const double2* __restrict__ y, int m, size_t N) {
-  HD_PDL_ENTRY();
   __shared__ double2 ys[128];
   for (int i = threadIdx.x; i < m && i < 128; i += blockDim.x) ys[i] = y[i];
   __syncthreads();
@@ -451,7 +292,6 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) { return cmul(a, c
 __device__ __forceinline__ double2 cconj(double2 a) { return cmk(a.x, -a.y); }
 
 __global__ void k_givens(double2* H, int ldh, double2* g, double2* cs, double2* sn, double2* y, int j) {
-  HD_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double2* col = H + (size_t)j * ldh;
   for (int i = 0; i < j; ++i) {
@@ -490,7 +330,6 @@ __global__ void k_givens(double2* H, int ldh, double2* g, double2* cs, double2* 
 // V column-major (V[i + k n] = v_k(i)), Dinv[ky*n + kx].
 __global__ void k_fd_small(const double* __restrict__ V, const double2* __restrict__ Dinv, int n,
                            const double2* __restrict__ X, double2* __restrict__ Y) {
-  HD_PDL_ENTRY();
   __shared__ double2 A[32 * 32], Bm[32 * 32];
   __shared__ double Vs[32 * 32];
   const int nn = n * n;
@@ -534,7 +373,6 @@ __global__ void k_fd_small(const double* __restrict__ V, const double2* __restri
 
 // planar complex T (re plane, im plane; n*n each) *= Dinv (complex, n*n)
 __global__ void k_fd_scale(double* __restrict__ T, const double2* __restrict__ Dinv, size_t NN) {
-  HD_PDL_ENTRY();
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < NN; g += (size_t)gridDim.x * blockDim.x) {
     const double2 v = cmul(cmk(T[g], T[g + NN]), Dinv[g]);
     T[g] = v.x;
@@ -552,7 +390,6 @@ __device__ __forceinline__ size_t fold_idx(int yb, int xb, int p, int kx, int j,
 
 // R[yb](q n2 + kx, ky), q = 2 xb + p: (R_p0 + i R_p1) *= D[yb][xb][ky][kx]
 __global__ void k_scale_folded(double* __restrict__ R, const double2* __restrict__ D, int n2) {
-  HD_PDL_ENTRY();
   const size_t nn = (size_t)n2 * n2;
   const size_t tot = 4 * nn;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
@@ -572,7 +409,6 @@ __global__ void k_scale_folded(double* __restrict__ R, const double2* __restrict
 // Q[xb][yb][p](i, j), i, j < n2: x rows folded first (a +- b), then y columns.
 // Q blocks n2 x n2 column-major, block (2 xb + yb) 2 + p.
 __global__ void k_fold_both(const double* __restrict__ X, double* __restrict__ Q, int n, int n2) {
-  HD_PDL_ENTRY();
   const size_t nn = (size_t)n2 * n2, N2 = (size_t)n * n;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < 2 * nn; g += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(g % n2);
@@ -593,7 +429,6 @@ __global__ void k_fold_both(const double* __restrict__ X, double* __restrict__ Q
 // Inverse of k_fold_both: P[xb][yb][p] blocks -> planar n x n Y (y columns
 // unfolded first, then x rows).
 __global__ void k_unfold_both(const double* __restrict__ Pb, double* __restrict__ Y, int n, int n2) {
-  HD_PDL_ENTRY();
   const size_t nn = (size_t)n2 * n2, N2 = (size_t)n * n;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < 2 * nn; g += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(g % n2);
@@ -622,7 +457,6 @@ __global__ void __launch_bounds__(256) k_bandlu_staged(const double2* __restrict
                                                        int n, const double2* __restrict__ b,
                                                        const double* __restrict__ bp, double2* __restrict__ work,
                                                        double2* __restrict__ x, double* __restrict__ xp) {
-  HD_PDL_ENTRY();
   constexpr int KU = 2 * KL;
   constexpr int CH = 256;
   extern __shared__ __align__(16) double2 sm[];
@@ -771,40 +605,6 @@ constexpr size_t bandlu_smem() {
   const size_t f = sizeof(double2) * (2 * CH * KL + 2 * (CH + KL)) + sizeof(int) * 2 * CH;
   const size_t b = sizeof(double2) * (2 * CH * 2 * KL + 4 * CH);
   return f > b ? f : b;
-}
-
-// Banded LU solve with the host-computed factors (one thread; 1D only).
-// in/out interleaved (planar == nullptr) or planar (n re, n im).
-__global__ void k_bandlu_solve(const double2* __restrict__ Lf, const double2* __restrict__ Uf,
-                               const int* __restrict__ piv, int n, int kl, int ku, const double2* __restrict__ b,
-                               const double* __restrict__ bp, double2* __restrict__ work, double2* __restrict__ x,
-                               double* __restrict__ xp) {
-  HD_PDL_ENTRY();
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int i = 0; i < n; ++i) work[i] = bp ? cmk(bp[i], bp[i + n]) : b[i];
-  for (int k = 0; k < n; ++k) {
-    const int p = piv[k];
-    if (p != k) {
-      const double2 tmp = work[k];
-      work[k] = work[p];
-      work[p] = tmp;
-    }
-    const double2 wk = work[k];
-    for (int r = 1; r <= kl && k + r < n; ++r) work[k + r] = csub(work[k + r], cmul(Lf[(size_t)k * kl + r - 1], wk));
-  }
-  for (int k = n - 1; k >= 0; --k) {
-    double2 s = work[k];
-    for (int d = 1; d <= ku && k + d < n; ++d) s = csub(s, cmul(Uf[(size_t)k * (ku + 1) + d], work[k + d]));
-    work[k] = cdiv(s, Uf[(size_t)k * (ku + 1)]);
-  }
-  for (int i = 0; i < n; ++i) {
-    if (xp) {
-      xp[i] = work[i].x;
-      xp[i + n] = work[i].y;
-    } else {
-      x[i] = work[i];
-    }
-  }
 }
 
 }  // namespace hd

@@ -64,7 +64,6 @@ template <int MODE>
 __global__ void __launch_bounds__(kGenThreads) k_kron2d(GenLevel L, const double2* __restrict__ x,
                                                         const double2* __restrict__ bv, double2* __restrict__ out,
                                                         double omega, RedOut red, const int* xidx, size_t xstride) {
-  HD_PDL_ENTRY();
   if (xidx) x += (size_t)(*xidx) * xstride;
   extern __shared__ __align__(16) double2 gsm[];
   __shared__ double2 scratch[32];
@@ -140,7 +139,6 @@ __global__ void __launch_bounds__(kGenThreads) k_kron2d(GenLevel L, const double
 // x = omega D^-1 b (Jacobi sweep from a zero iterate)
 __global__ void __launch_bounds__(256) k_jacobi0_gen(GenLevel L, const double2* __restrict__ bv,
                                                      double2* __restrict__ out, double omega) {
-  HD_PDL_ENTRY();
   const int n = L.n, NB = 2 * L.b + 1;
   const size_t NN = (size_t)n * n;
   for (size_t gi = blockIdx.x * (size_t)blockDim.x + threadIdx.x; gi < NN; gi += (size_t)gridDim.x * blockDim.x) {
@@ -153,7 +151,6 @@ __global__ void __launch_bounds__(256) k_jacobi0_gen(GenLevel L, const double2* 
 // Dense column-major n^2 x n^2 matrix of the Kronecker sum (row = iy*n+ix,
 // col = jy*n+jx), for the dense exact solves.
 __global__ void k_dense_kron(GenLevel L, double2* __restrict__ A) {
-  HD_PDL_ENTRY();
   const int n = L.n, b = L.b, NB = 2 * b + 1;
   const size_t NN = (size_t)n * n, tot = NN * NN;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
@@ -165,7 +162,6 @@ __global__ void k_dense_kron(GenLevel L, double2* __restrict__ A) {
 }
 
 __global__ void k_identity(double2* __restrict__ B, size_t NN) {
-  HD_PDL_ENTRY();
   const size_t tot = NN * NN;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x)
     B[e] = cmk((e % NN) == (e / NN) ? 1.0 : 0.0, 0.0);

@@ -74,7 +74,6 @@ __host__ __device__ constexpr size_t seg_bwd_smem() {
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_fwd(SegArgs a, const double2* __restrict__ b,
                                                 const double* __restrict__ bp) {
-  HD_PDL_ENTRY();
   extern __shared__ __align__(16) double2 sring[];
   double2(*rl)[KL + 1][32] = reinterpret_cast<double2(*)[KL + 1][32]>(sring);  // [slot][L_0..L_{KL-1}, b][lane]
   int(*rp)[32] = reinterpret_cast<int(*)[32]>(sring + (size_t)kSegDepth * (KL + 1) * 32);
@@ -134,7 +133,6 @@ __global__ void __launch_bounds__(32) k_seg_fwd(SegArgs a, const double2* __rest
 // the maps are staged kSegC segments at a time, double-buffered)
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_scan_fwd(SegArgs a) {
-  HD_PDL_ENTRY();
   constexpr int W = KL + 1, PER = W * W + W;  // F_i then D_i
   constexpr int kSegC = seg_chunk(PER);
   __shared__ __align__(16) double2 buf[2][kSegC * PER];
@@ -179,7 +177,6 @@ __global__ void __launch_bounds__(32) k_seg_scan_fwd(SegArgs a) {
 // as in k_seg_fwd
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_bwd(SegArgs a) {
-  HD_PDL_ENTRY();
   constexpr int KU = 2 * KL, NF = KL + KU + 3;  // y, hf[KL+1], U[KU], 1/u
   extern __shared__ __align__(16) double2 sring[];
   double2(*rg)[NF][32] = reinterpret_cast<double2(*)[NF][32]>(sring);
@@ -231,7 +228,6 @@ __global__ void __launch_bounds__(32) k_seg_bwd(SegArgs a) {
 // X_P = 0, X_i = X0_i + H'_i X_{i+1}  (one warp, lane d owns component d)
 template <int KL>
 __global__ void __launch_bounds__(32) k_seg_scan_bwd(SegArgs a) {
-  HD_PDL_ENTRY();
   constexpr int KU = 2 * KL, PER = KU * KU + KU;  // H'_i then X0_i
   constexpr int kSegC = seg_chunk(PER);
   __shared__ __align__(16) double2 buf[2][kSegC * PER];
@@ -298,7 +294,6 @@ template <int DM, int BWD>
 __global__ void __launch_bounds__(kScanWarps * 32) k_seg_scan2(const double2* __restrict__ Mt,
                                                                const double2* __restrict__ ct, double2* __restrict__ out,
                                                                int P) {
-  HD_PDL_ENTRY();
   constexpr int DD = DM * DM, PER = DD + DM;
   extern __shared__ __align__(16) double2 ssm[];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
@@ -394,7 +389,6 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_seg_scan2(const double2* __
 // x_k = x0_k + h'_k . X_{i+1}  (thread per row), output interleaved or planar
 template <int KL>
 __global__ void k_seg_out(SegArgs a, double2* __restrict__ x, double* __restrict__ xp) {
-  HD_PDL_ENTRY();
   constexpr int KU = 2 * KL;
   const int P = a.P;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += gridDim.x * blockDim.x) {

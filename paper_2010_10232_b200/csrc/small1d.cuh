@@ -162,7 +162,6 @@ __device__ void small_deflate(const SmallArgs& a, const double2* r, double2* ec,
 }
 
 __global__ void __launch_bounds__(kSmallThreads) k_solve1d_small(SmallArgs a) {
-  HD_PDL_ENTRY();
   extern __shared__ __align__(16) double2 ssm[];
   __shared__ double red[32];
   const int tid = threadIdx.x, nt = blockDim.x, N = a.N;

@@ -21,7 +21,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <cstring>
+#include <map>
+#include <mutex>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -33,12 +34,10 @@
 #include "kernels.cuh"
 #include "stencil.cuh"
 #include "transfer.cuh"
-#include "arnoldi.cuh"
 #include "arnoldi_lowsync.cuh"
 #include "layered.cuh"
 #include "btri.cuh"
 #include "segsolve.cuh"
-#include "ysolve.cuh"
 #include "tail1d.cuh"
 #include "small1d.cuh"
 
@@ -216,6 +215,9 @@ static hd_status solve_impl(hd_ctx* c, const hd_gmres* opt, const double* rhs, b
     ensure_gmres(c, 1);
   }
   r = c->slabs ? run_solve_slabs(c, *opt, c->f, xd) : run_solve(c, *opt, xd);
+  for (size_t i = 0; i < r.residuals.size(); ++i)
+    if (!std::isfinite(r.residuals[i]))
+      throw Error(HD_ERR_NONFINITE, "non-finite residual at GMRES iteration " + std::to_string(i + 1));
   if (!x_dev) CK(cudaMemcpyAsync(x_out, xd, N * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
   CK(cudaEventRecord(c->ev1, c->st));
   CK(cudaEventSynchronize(c->ev1));

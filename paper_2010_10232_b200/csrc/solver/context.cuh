@@ -37,6 +37,22 @@ static T* dalloc(size_t n) {
   return static_cast<T*>(p);
 }
 
+// Opt-in to `bytes` of dynamic shared memory for kernel `f` on the CURRENT
+// device.  cudaFuncSetAttribute applies per device, so the cache is keyed by
+// (device, function) and guarded: contexts on other GPUs or other host
+// threads each get their own opt-in.
+static void smem_optin(const void* f, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{dev, f}];
+  if (bytes <= have) return;
+  CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  have = bytes;
+}
+
 struct DevBand {
   double* S = nullptr;
   double* M = nullptr;
@@ -66,10 +82,6 @@ struct ExactSolver {
   // segmented sweeps (segsolve.cuh); seg.P == 0: single-lane staged kernel
   SegArgs seg{};
   bool seg_seqscan = false;  // P-step single-warp boundary scans instead of k_seg_scan2 (HD_SEG_SEQSCAN at setup)
-  // partial fast diagonalisation (ysolve.cuh): x modes by V, segmented banded LU sweeps along y
-  bool ypart = false;
-  int ykl = 0;
-  YArgs ya{};
   // reflection-folded fast diagonalisation (centro-symmetric E, even n):
   // Vt = [Vs_top | Va_top] (2 x n2 x n2), Dinvf in [y parity][x parity][ky][kx]
   bool folded = false;
@@ -116,7 +128,6 @@ struct hd_ctx {
   double* sx_plan = nullptr;    // planar scratch for the 2D exact shifted solve
   std::vector<double2*> mg_b, mg_x, mg_y, mg_r;
   bool j0_fuse = true;          // first Jacobi sweeps ride with their producers (HD_NOJ0FUSE=1 at create: off)
-  int pdl_edges = 0;            // programmatic kernel->kernel edges in the loop graph body
   int tail_l = -1;              // 1D: first level of the single-CTA tail V-cycle (tail1d.cuh), -1: none
   TailArgs tail{};
   size_t tail_smem_bytes = 0;
@@ -143,19 +154,10 @@ struct hd_ctx {
   double2* partials = nullptr;
   unsigned* counter = nullptr;
   int red_blocks = 0;
-  // persistent Arnoldi tail (arnoldi.cuh)
-  bool use_arnoldi = false;
-  int arn_G = 0, arn_K = 0;
-  size_t arn_chunk = 0, arn_smem = 0;
   int* dj = nullptr;
-  double2* arn_partials = nullptr;
-  int arn_maxit = -1;
-  unsigned* arn_bar = nullptr;
-  unsigned long long* arn_trace = nullptr;  // HD_TRACE: phase timestamps of the last launch
-  double arn_phase_ns[4] = {0, 0, 0, 0};
-  // Arnoldi engine: 2 = one-reduction ICWY-MGS streaming passes (default),
-  // 1 = persistent exact-order MGS chain, 0 = one kernel per MGS step.
-  int arn_mode = 2;
+  // Arnoldi engine: 1 = one-reduction ICWY-MGS streaming passes (default),
+  // 0 = exact-order MGS, one kernel per MGS step (budgets above kLsaMaxJ, HD_ARNOLDI=0)
+  int arn_mode = 1;
   // one-reduction engine state (arnoldi_lowsync.cuh)
   double* lsa_sig = nullptr;
   double2 *lsa_L = nullptr, *lsa_ch = nullptr, *lsa_cx = nullptr, *lsa_partials = nullptr;
@@ -167,11 +169,14 @@ struct hd_ctx {
   cudaGraphExec_t loop_exec = nullptr;
   bool pre_graph = true;               // HD_PRE_GRAPH=0: eager prelude launches
   cudaGraphExec_t pre_exec = nullptr;  // GMRES prelude (rhs', start, monitor(x0), op(x0), beta)
-  const void* pre_g = nullptr;          // c->g the prelude was captured with (ensure_gmres may move it)
   long pre_dcnt[4] = {0, 0, 0, 0}, pre_dsnap[4] = {0, 0, 0, 0};
   int pre_dl = 0, pre_db = 0;
   int loop_maxit = -1;
   double loop_tol = -1.0;
+  // bumped whenever a buffer a captured graph points at is reallocated
+  // (ensure_gmres, the slab basis); graphs record the epoch they captured
+  unsigned buf_epoch = 0;
+  unsigned loop_epoch = ~0u, pre_epoch = ~0u;
   LoopState* loop_state = nullptr;
   LoopState* loop_host = nullptr;   // pinned
   double* res_hist = nullptr;       // device, maxit
@@ -424,107 +429,6 @@ static ExactSolver make_fd(cudaStream_t st, const Band& S, const Band& M, double
   return X;
 }
 
-// Partial fast diagonalisation of a real-shift Kronecker sum (E): V from the
-// x eigenproblem (as make_fd); for every x mode the real banded y operator
-// T_m = S - (c - lam_m) M, LU-factored with partial pivoting (band_lu), and the
-// influence rows / boundary maps of its kYL-row segments (ysolve.cuh).
-static ExactSolver make_fd_ypart(cudaStream_t st, const Band& S, const Band& M, double2 c) {
-  const int n = S.n, kl = std::max(S.b, M.b), ku = 2 * kl, W = kl + 1;
-  ExactSolver X;
-  X.dim = 2;
-  X.n = n;
-  X.ypart = true;
-  X.ykl = kl;
-  X.V = dalloc<double>(static_cast<size_t>(n) * n);
-  std::vector<double> lam;
-  sygvd_device(st, dense_of(S), dense_of(M), n, X.V, lam);
-  const int np = (n + 31) / 32 * 32, Sg = (n + kYL - 1) / kYL, nr = Sg * kYL;
-  const int NF = 2 * kl + 2, NB = 2 * ku + 1;
-  std::vector<double> TF(static_cast<size_t>(nr) * NF * np, 0.0), TB(static_cast<size_t>(nr) * NB * np, 0.0),
-      FM(static_cast<size_t>(Sg) * W * W * np, 0.0), HM(static_cast<size_t>(Sg) * ku * ku * np, 0.0);
-  std::vector<double> Lk, Uk;
-  std::vector<int> pk;
-  for (int m = 0; m < np; ++m) {
-    // factors of mode m, padded rows / modes = identity
-    Lk.assign(static_cast<size_t>(nr) * kl, 0.0);
-    Uk.assign(static_cast<size_t>(nr) * (ku + 1), 0.0);
-    pk.assign(nr, 0);
-    for (int k = 0; k < nr; ++k) Uk[static_cast<size_t>(k) * (ku + 1)] = 1.0;
-    if (m < n) {
-      const BandLU f = band_lu(S, M, cplx(c.x - lam[m], 0.0));
-      if (f.kl != kl || f.ku != ku) throw Error(HD_ERR_INVALID, "unexpected band LU shape");
-      for (int k = 0; k < n; ++k) {
-        for (int q = 0; q < kl; ++q) Lk[static_cast<size_t>(k) * kl + q] = f.L[static_cast<size_t>(k) * kl + q].real();
-        for (int d = 0; d <= ku; ++d) Uk[static_cast<size_t>(k) * (ku + 1) + d] = f.U[static_cast<size_t>(k) * (ku + 1) + d].real();
-        pk[k] = f.piv[k] - k;
-        if (Uk[static_cast<size_t>(k) * (ku + 1)] == 0.0) throw Error(HD_ERR_FACTOR, "deflation matrix E is singular");
-      }
-    }
-    for (int k = 0; k < nr; ++k) {
-      double* tf = &TF[static_cast<size_t>(k) * NF * np + m];
-      for (int q = 0; q < kl; ++q) tf[static_cast<size_t>(q) * np] = Lk[static_cast<size_t>(k) * kl + q];
-      tf[static_cast<size_t>(kl) * np] = pk[k];
-      double* tb = &TB[static_cast<size_t>(k) * NB * np + m];
-      tb[0] = 1.0 / Uk[static_cast<size_t>(k) * (ku + 1)];
-      for (int d = 1; d <= ku; ++d) tb[static_cast<size_t>(d) * np] = Uk[static_cast<size_t>(k) * (ku + 1) + d];
-    }
-    for (int i = 0; i < Sg; ++i) {
-      const int s0 = i * kYL, e0 = s0 + kYL;
-      for (int q = 0; q < W; ++q) {  // forward from window e_q, no rhs
-        std::vector<double> w(W, 0.0);
-        w[q] = 1.0;
-        for (int k = s0; k < e0; ++k) {
-          const int p = pk[k];
-          if (p != 0) std::swap(w[0], w[p]);
-          const double yk = w[0];
-          TF[(static_cast<size_t>(k) * NF + kl + 1 + q) * np + m] = yk;
-          for (int r = 1; r <= kl; ++r) w[r] -= Lk[static_cast<size_t>(k) * kl + r - 1] * yk;
-          for (int r = 0; r < kl; ++r) w[r] = w[r + 1];
-          w[kl] = 0.0;
-        }
-        for (int r = 0; r < W; ++r) FM[((static_cast<size_t>(i) * W + r) * W + q) * np + m] = w[r];
-      }
-      for (int r = 0; r < ku; ++r) {  // backward from future x_{e+r} = 1, no rhs
-        std::vector<double> xw(ku, 0.0);
-        xw[r] = 1.0;
-        for (int k = e0 - 1; k >= s0; --k) {
-          double acc = 0.0;
-          for (int d = ku; d >= 1; --d) acc -= Uk[static_cast<size_t>(k) * (ku + 1) + d] * xw[d - 1];
-          const double xk = acc / Uk[static_cast<size_t>(k) * (ku + 1)];
-          for (int d = ku - 1; d >= 1; --d) xw[d] = xw[d - 1];
-          xw[0] = xk;
-          TB[(static_cast<size_t>(k) * NB + ku + 1 + r) * np + m] = xk;
-          if (k - s0 < ku) HM[((static_cast<size_t>(i) * ku + (k - s0)) * ku + r) * np + m] = xk;
-        }
-      }
-    }
-  }
-  auto up = [](const std::vector<double>& v) {
-    double* d = dalloc<double>(v.size());
-    CK(cudaMemcpy(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
-    return d;
-  };
-  YArgs& a = X.ya;
-  a.n = n;
-  a.np = np;
-  a.S = Sg;
-  a.nr = nr;
-  a.TF = up(TF);
-  a.TB = up(TB);
-  a.FM = up(FM);
-  a.HM = up(HM);
-  a.Y = dalloc<double>(2 * static_cast<size_t>(nr) * np);
-  a.X0 = dalloc<double>(2 * static_cast<size_t>(nr) * np);
-  a.D = dalloc<double>(2 * static_cast<size_t>(Sg) * W * np);
-  a.Dl = dalloc<double>(2 * static_cast<size_t>(Sg) * W * np);
-  a.XS = dalloc<double>(2 * static_cast<size_t>(Sg) * ku * np);
-  a.XB = dalloc<double>(2 * static_cast<size_t>(Sg + 1) * ku * np);
-  X.T1 = dalloc<double>(2 * static_cast<size_t>(n) * np);
-  CK(cudaMemset(X.T1, 0, 2 * static_cast<size_t>(n) * np * sizeof(double)));
-  a.C = X.T1;
-  return X;
-}
-
 // Influence rows and window transfers of the segmented sweeps (segsolve.cuh),
 // by running each segment's recurrences on unit boundary values; all per-row
 // tables in the [row-in-segment][field][segment] layout, rows past n = identity.
@@ -631,11 +535,6 @@ static void free_exact(ExactSolver& X) {
   cudaFree(X.Vt); cudaFree(X.Dinvf); cudaFree(X.F); cudaFree(X.Hh); cudaFree(X.R);
     cudaFree(const_cast<double**>(X.xf_ptr));
   cudaFree(X.L); cudaFree(X.U); cudaFree(X.piv); cudaFree(X.work); cudaFree(X.Uinv);
-  if (X.ypart) {
-    cudaFree(const_cast<double*>(X.ya.TF)); cudaFree(const_cast<double*>(X.ya.TB));
-    cudaFree(const_cast<double*>(X.ya.FM)); cudaFree(const_cast<double*>(X.ya.HM));
-    cudaFree(X.ya.Y); cudaFree(X.ya.X0); cudaFree(X.ya.D); cudaFree(X.ya.Dl); cudaFree(X.ya.XS); cudaFree(X.ya.XB);
-  }
   if (X.seg.P) {
     for (const void* p : {static_cast<const void*>(X.seg.L), static_cast<const void*>(X.seg.pv),
                           static_cast<const void*>(X.seg.hf), static_cast<const void*>(X.seg.U),
@@ -656,12 +555,8 @@ static void free_exact(ExactSolver& X) {
 template <int KL>
 static void bandlu_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b, const double* bp, double2* x,
                             double* xp) {
-  static bool attr = false;
   constexpr size_t sm = bandlu_smem<KL>();
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_bandlu_staged<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_bandlu_staged<KL>), sm);
   k_bandlu_staged<KL><<<1, 256, sm, st>>>(X.L, X.U, X.Uinv, X.piv, X.n, b, bp, X.work, x, xp);
 }
 
@@ -670,24 +565,14 @@ static void seg_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b
                          double* xp) {
   const SegArgs& a = X.seg;
   const int blocks = (a.P + 31) / 32;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_seg_fwd<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(seg_fwd_smem<KL>())));
-    CK(cudaFuncSetAttribute(k_seg_bwd<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(seg_bwd_smem<KL>())));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_seg_fwd<KL>), seg_fwd_smem<KL>());
+  smem_optin(reinterpret_cast<const void*>(k_seg_bwd<KL>), seg_bwd_smem<KL>());
   constexpr int W = KL + 1, KU = 2 * KL;
   // the P-step single-warp scans: HD_SEG_SEQSCAN, or maps too large for the staged two-level scan (KL = 6)
   const bool seq = X.seg_seqscan || seg_scan2_smem<KU>() > 227u * 1024u;
-  static bool attr2 = false;
-  if (!attr2 && !seq) {
-    CK(cudaFuncSetAttribute(k_seg_scan2<W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(seg_scan2_smem<W>())));
-    CK(cudaFuncSetAttribute(k_seg_scan2<KU, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(seg_scan2_smem<KU>())));
-    attr2 = true;
+  if (!seq) {
+    smem_optin(reinterpret_cast<const void*>(k_seg_scan2<W, 0>), seg_scan2_smem<W>());
+    smem_optin(reinterpret_cast<const void*>(k_seg_scan2<KU, 1>), seg_scan2_smem<KU>());
   }
   k_seg_fwd<KL><<<blocks, 32, seg_fwd_smem<KL>(), st>>>(a, b, bp);
   if (seq) k_seg_scan_fwd<KL><<<1, 32, 0, st>>>(a);

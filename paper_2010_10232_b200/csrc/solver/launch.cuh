@@ -64,13 +64,23 @@ static double op_bytes(int mode, size_t NL) {
 // and query how many CTAs are resident per SM.
 template <int B, int MODE>
 static int stencil_occupancy() {
-  static int per = 0;
-  if (!per) {
-    constexpr size_t sm = stencil_smem<B, MODE>(kSRowsMax);
-    CK(cudaFuncSetAttribute(k_stencil2d<B, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stencil2d<B, MODE>, kSW * kSWarps, sm));
-    per = std::max(per, 1);
+  // per device: the opt-in and the resident-CTA count (cached per (device, kernel))
+  static std::mutex mu;
+  static std::map<int, int> per_dev;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = per_dev.find(dev);
+    if (it != per_dev.end()) return it->second;
   }
+  constexpr size_t sm = stencil_smem<B, MODE>(kSRowsMax);
+  smem_optin(reinterpret_cast<const void*>(k_stencil2d<B, MODE>), sm);
+  int per = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stencil2d<B, MODE>, kSW * kSWarps, sm));
+  per = std::max(per, 1);
+  std::lock_guard<std::mutex> lk(mu);
+  per_dev[dev] = per;
   return per;
 }
 
@@ -127,12 +137,7 @@ static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, con
 template <int MODE>
 static void launch_gen_mode(hd_ctx* c, const GenLevel& G, const double2* x, const double2* b, double2* out,
                             double omega, RedOut red, int kind, const int* xidx, size_t xstride) {
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_kron2d<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(gen_smem(6, kGenMaxG))));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_kron2d<MODE>), gen_smem(6, kGenMaxG));
   if (G.b > 6 || G.G > kGenMaxG) throw Error(HD_ERR_INVALID, "layered operator exceeds the kernel limits");
   const dim3 grid((G.n + kGenTX - 1) / kGenTX, (G.n + kGenTY - 1) / kGenTY);
   HD_LAUNCH(kind, op_bytes(MODE, static_cast<size_t>(G.n) * G.n),
@@ -248,7 +253,6 @@ static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, 
 
 // interleaved <-> planar (re plane, im plane) complex vectors
 __global__ void k_to_planar(const double2* __restrict__ a, double* __restrict__ p, size_t N) {
-  HD_PDL_ENTRY();
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
     const double2 v = a[g];
     p[g] = v.x;
@@ -256,7 +260,6 @@ __global__ void k_to_planar(const double2* __restrict__ a, double* __restrict__ 
   }
 }
 __global__ void k_from_planar(const double* __restrict__ p, double2* __restrict__ a, size_t N) {
-  HD_PDL_ENTRY();
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
     a[g] = cmk(p[g], p[g + N]);
 }
@@ -275,11 +278,7 @@ static void dense_apply(hd_ctx* c, const ExactSolver& X, const double2* x, doubl
 template <class T, int KR>
 static void btri_launch_t(hd_ctx* c, ExactSolver& X) {
   const size_t smem = 4 * static_cast<size_t>(X.bt.m) * sizeof(double);  // two staged vectors
-  static size_t attr = 0;
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_btri_solve<T, KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = smem;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_btri_solve<T, KR>), smem);
   cudaLaunchConfig_t cfg{};
   cfg.dynamicSmemBytes = smem;
   cfg.gridDim = dim3(c->n_sms);
@@ -315,48 +314,7 @@ static void btri_solve(hd_ctx* c, ExactSolver& X, double* inout) {
             });
 }
 
-// Exact solve: in/out planar (2D FD) or via the banded LU (1D).
-template <int KL>
-static void ysolve_launch_t(hd_ctx* c, const YArgs& a) {
-  const dim3 gs(a.np / 32, a.S), gm((a.np + 127) / 128), go(a.np / 32, a.n);
-  k_ys_fwd<KL><<<gs, 32, 0, c->st>>>(a);
-  k_ys_scan_fwd<KL><<<gm, 128, 0, c->st>>>(a);
-  k_ys_bwd<KL><<<gs, 32, 0, c->st>>>(a);
-  k_ys_scan_bwd<KL><<<gm, 128, 0, c->st>>>(a);
-  k_ys_out<KL><<<go, 32, 0, c->st>>>(a);
-}
-
-static void ysolve_launch(hd_ctx* c, const ExactSolver& X) {
-  switch (X.ykl) {
-    case 1: ysolve_launch_t<1>(c, X.ya); break;
-    case 2: ysolve_launch_t<2>(c, X.ya); break;
-    case 3: ysolve_launch_t<3>(c, X.ya); break;
-    case 4: ysolve_launch_t<4>(c, X.ya); break;
-    case 5: ysolve_launch_t<5>(c, X.ya); break;
-    case 6: ysolve_launch_t<6>(c, X.ya); break;
-    default: throw Error(HD_ERR_INVALID, "E band outside the y-solve kernels");
-  }
-}
-
 static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
-  if (X.ypart) {
-    const int n = X.n, np = X.ya.np;
-    const long nn = static_cast<long>(n) * n;
-    const double one = 1.0, zero = 0.0;
-    const double gb = 16.0 * nn * 2 + 8.0 * nn;
-    size_t mk = prof_mark(c);
-    // C = V^T [Xre | Xim]  (x modes), leading dimension np
-    CKB(cublasDgemm(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, inout, n, &zero, X.T1, np));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
-    // segmented banded sweeps along y for every mode (5 kernels)
-    HD_LAUNCH(HD_K_EXACT, 8.0 * X.ya.nr * np * (2 * X.ykl + 2 + 4 * X.ykl + 1) + 64.0 * nn, ysolve_launch(c, X));
-    c->launches += 4;
-    mk = prof_mark(c);
-    // out = V [Yre | Yim]
-    CKB(cublasDgemm(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, X.T1, np, &zero, inout, n));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
-    return;
-  }
   if (X.btri) {
     btri_solve(c, X, inout);
     return;
@@ -615,81 +573,16 @@ static void compose_op(hd_ctx* c, const double2* v, double2* out, const int* vid
   }
 }
 
-// Chooses the persistent Arnoldi geometry: G CTAs of kArnBD threads (<= one
-// per SM), each owning `chunk` elements, K per thread; shared memory holds the
-// non-register part of w and, in block 0, the packed R of the back substitution.
-static void setup_arnoldi(hd_ctx* c, int maxit) {
-  int dev_sms = 0, smem_optin = 0;
-  CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
-  CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-  const size_t N = c->N;
-  const size_t per_thread_target = 4;
-  int G = static_cast<int>(std::min<size_t>(dev_sms, std::max<size_t>(1, (N + kArnBD * per_thread_target - 1) /
-                                                                             (kArnBD * per_thread_target))));
-  const size_t chunk = (N + G - 1) / G;
-  const int K = static_cast<int>((chunk + kArnBD - 1) / kArnBD);
-  const size_t w_smem = static_cast<size_t>(std::max(0, K - kArnRW)) * kArnBD * sizeof(double2);
-  const size_t r_smem = (static_cast<size_t>(maxit + 1) * (maxit + 2) / 2 + 4 * (maxit + 2) + 8) * sizeof(double2);
-  const size_t smem = std::max(w_smem, r_smem);
-  c->use_arnoldi = false;
-  if (maxit > 127) return;  // y staged in 128 shared slots
-  if (smem + 4096 > static_cast<size_t>(smem_optin)) return;  // w does not fit on chip: per-step kernels
-  CK(cudaFuncSetAttribute(k_arnoldi<kArnRW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi<kArnRW>, kArnBD, smem));
-  if (per_sm < 1) return;
-  c->arn_G = G;
-  c->arn_K = K;
-  c->arn_chunk = chunk;
-  c->arn_smem = smem;
-  if (!c->dj) c->dj = dalloc<int>(4);
-  if (!c->arn_partials) c->arn_partials = dalloc<double2>(2 * static_cast<size_t>(dev_sms) + 8);
-  if (!c->arn_bar) c->arn_bar = dalloc<unsigned>(4);
-  if (!c->arn_trace && std::getenv("HD_TRACE")) {
-    CK(cudaMallocHost(&c->arn_trace, 8 * sizeof(unsigned long long)));
-  }
-  c->use_arnoldi = true;
-}
-
-static void launch_arnoldi(hd_ctx* c, double2* xout, int maxit, const int* done, double bytes) {
-  ArnoldiArgs a;
-  a.V = c->V;
-  a.Vw = c->V;
-  a.w = c->w;
-  a.x0 = c->x0;
-  a.x = xout;
-  a.N = c->N;
-  a.dj = c->dj;
-  a.done = done;
-  a.H = c->H;
-  a.ldh = maxit + 1;
-  a.g = c->g;
-  a.cs = c->cs;
-  a.sn = c->sn;
-  a.y = c->y;
-  a.hnew_out = c->dres + 1;
-  a.partials = c->arn_partials;
-  a.bar = c->arn_bar;
-  a.K = c->arn_K;
-  a.chunk = c->arn_chunk;
-  a.trace = c->arn_trace;
-  CK(cudaMemsetAsync(c->arn_bar, 0, sizeof(unsigned), c->st));
-  void* args[] = {&a};
-  const double P = 16.0 * static_cast<double>(c->N);
-  (void)P;
-  const size_t mk = prof_mark(c);
-  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_arnoldi<kArnRW>), dim3(c->arn_G), dim3(kArnBD), args,
-                                 c->arn_smem, c->st));
-  launched(c, HD_K_MGS, mk, bytes);
-}
-
 static void ensure_gmres(hd_ctx* c, int maxit) {
+  // every branch below that reallocates moves pointers the loop / prelude graphs captured
   if (maxit + 1 > c->v_cap) {
+    ++c->buf_epoch;
     cudaFree(c->V);
     c->V = dalloc<double2>(static_cast<size_t>(maxit + 1) * c->N);
     c->v_cap = maxit + 1;
   }
   if (maxit > c->maxit_cap) {
+    ++c->buf_epoch;
     cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
     c->H = dalloc<double2>(static_cast<size_t>(maxit + 1) * maxit);
     c->g = dalloc<double2>(maxit + 1);
@@ -698,15 +591,11 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
     c->y = dalloc<double2>(maxit);
     c->maxit_cap = maxit;
   }
-  if (maxit != c->arn_maxit) {
-    setup_arnoldi(c, maxit);
-    c->arn_maxit = maxit;
-  }
   if (maxit != c->lsa_maxit && maxit + 1 <= kLsaMaxJ) {
+    ++c->buf_epoch;
     int sms = 0, per = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-    CK(cudaFuncSetAttribute(k_lsa_dots, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(lsa_dots_smem())));
+    smem_optin(reinterpret_cast<const void*>(k_lsa_dots), lsa_dots_smem());
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lsa_dots, kLsaBD, lsa_dots_smem()));
     int per2 = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_lsa_update, kLsaBD, 0));
@@ -725,8 +614,7 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
     }
     const int m = maxit + 1;
     c->lsa_givens_smem = (static_cast<size_t>(m) * (m + 1) / 2 + 4 * (m + 2) + 8) * sizeof(double2);
-    CK(cudaFuncSetAttribute(k_lsa_givens, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(c->lsa_givens_smem)));
+    smem_optin(reinterpret_cast<const void*>(k_lsa_givens), c->lsa_givens_smem);
     c->lsa_maxit = maxit;
   }
 }
@@ -762,8 +650,7 @@ static LsaArgs lsa_args(hd_ctx* c, double2* xout, int j, int mode, int maxit) {
   return a;
 }
 
-__global__ void k_inv_scalar(double* dst, const double* src) {
-  HD_PDL_ENTRY(); *dst = *src > 0.0 ? 1.0 / *src : 0.0; }
+__global__ void k_inv_scalar(double* dst, const double* src) { *dst = *src > 0.0 ? 1.0 / *src : 0.0; }
 
 static void read_scalars(hd_ctx* c) {
   CK(cudaMemcpyAsync(c->hres, c->dres, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -771,17 +658,17 @@ static void read_scalars(hd_ctx* c) {
 }
 
 __global__ void k_loop_init(LoopState* s) {
-  HD_PDL_ENTRY();
   s->j = 0;
   s->done = 0;
   s->iters = 0;
   s->conv = 0;
   s->need_tail = 0;
   s->breakdown = 0;
+  s->nonfinite = 0;
 }
 
 __global__ void k_scale_monitor(double* dres) {
-  HD_PDL_ENTRY();  // graph monitor: raw norm / (||f|| or 1)
+  // graph monitor: raw norm / (||f|| or 1)
   const double f = dres[3];
   dres[0] = dres[0] / (f > 0.0 ? f : 1.0);
 }
@@ -793,56 +680,6 @@ static void monitor_raw(hd_ctx* c, const double2* x) {
 // Captures the GMRES iteration body (device-side j) into the body of a WHILE
 // conditional node: op(u_j) -> pass 1 (dots, x_{j-1}) -> monitor x_{j-1} ->
 // convergence check -> pass 2 (u_{j+1}) -> Givens -> j++.
-// Turns kernel -> hd-kernel edges of a captured graph into programmatic
-// edge (the dependent's launch overlaps the tail of its predecessor; its
-// HD_PDL_ENTRY waits for the predecessor to complete before touching memory).
-// Only edges INTO this library's kernels are converted: library kernels
-// (cuBLAS) have no griddepcontrol.wait.  Opt-in (HD_PDL=1): measured on B200 it
-// is neutral at C5 and C2 and 3-4% slower at C3 and C4.
-static int pdl_edges(cudaGraph_t g) {
-  static const bool off = !(std::getenv("HD_PDL") && std::atoi(std::getenv("HD_PDL")) == 1);
-  if (off) return 0;
-  static const long pdl_max_ctas = std::getenv("HD_PDL_MAXCTA") ? std::atol(std::getenv("HD_PDL_MAXCTA")) : 148;
-  size_t ne = 0;
-  CK(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));
-  if (ne == 0) return 0;
-  std::vector<cudaGraphNode_t> from(ne), to(ne);
-  std::vector<cudaGraphEdgeData> ed(ne);
-  CK(cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne));
-  auto is_kernel = [](cudaGraphNode_t n) {
-    cudaGraphNodeType t;
-    return cudaGraphNodeGetType(n, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel;
-  };
-  auto is_hd = [&](cudaGraphNode_t n) {
-    if (!is_kernel(n)) return false;
-    cudaKernelNodeParams kp = {};
-    if (cudaGraphKernelNodeGetParams(n, &kp) != cudaSuccess || !kp.func) {
-      cudaGetLastError();
-      return false;
-    }
-    const char* name = nullptr;
-    if (cudaFuncGetName(&name, kp.func) != cudaSuccess || !name) {
-      cudaGetLastError();
-      return false;
-    }
-    // single-wave kernels only (their launch latency is exposed; larger grids and
-    // the persistent block-tridiagonal solve measured slower with early launch)
-    const long ctas = static_cast<long>(kp.gridDim.x) * kp.gridDim.y * kp.gridDim.z;
-    return std::strncmp(name, "_ZN2hd", 6) == 0 && ctas <= pdl_max_ctas && !std::strstr(name, "btri");
-  };
-  int nconv = 0;
-  for (size_t e = 0; e < ne; ++e) {
-    if (ed[e].type != cudaGraphDependencyTypeDefault || !is_kernel(from[e]) || !is_hd(to[e])) continue;
-    CK(cudaGraphRemoveDependencies_v2(g, &from[e], &to[e], &ed[e], 1));
-    cudaGraphEdgeData pe = {};
-    pe.type = cudaGraphDependencyTypeProgrammatic;
-    pe.from_port = cudaGraphKernelNodePortProgrammatic;
-    CK(cudaGraphAddDependencies_v2(g, &from[e], &to[e], &pe, 1));
-    ++nconv;
-  }
-  return nconv;
-}
-
 static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
   if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
   if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
@@ -928,12 +765,11 @@ static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
   c->lib_calls = saved_b;
   CK(ec);
   CK(cudaGetLastError());
-  c->pdl_edges = pdl_edges(body);
-  if (std::getenv("HD_PDL_TRACE")) std::fprintf(stderr, "[hd] loop graph: %d programmatic edges\n", c->pdl_edges);
   CK(cudaGraphInstantiate(&c->loop_exec, g, 0));
   c->loop_graph = g;
   c->loop_maxit = maxit;
   c->loop_tol = tol;
+  c->loop_epoch = c->buf_epoch;
 }
 
 struct SolveOut {
@@ -962,11 +798,7 @@ static SolveOut run_solve_small1d(hd_ctx* c, const hd_gmres& opt, double2* xout)
   a.res = c->small_res;
   a.state = c->small_state;
   const size_t smem = small_smem(a);
-  static size_t attr = 0;
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_solve1d_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = smem;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_solve1d_small), smem);
   // one warp per 32 unknowns (64..512 threads): fewer warps make the block barriers cheaper
   const int threads = static_cast<int>(std::min<size_t>(kSmallThreads, std::max<size_t>(64, (c->N + 31) / 32 * 32)));
   HD_LAUNCH(HD_K_OP_FINE, 16.0 * c->N * 10.0, k_solve1d_small<<<1, threads, smem, c->st>>>(a));
@@ -1060,7 +892,7 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
     HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->w, nullptr, nullptr, N, red_of(c, c->dres + 2), c->g));
   };
   if (c->graph_enabled && !c->prof_on && c->pre_graph) {
-    if (!c->pre_exec || c->pre_g != c->g) {
+    if (!c->pre_exec || c->pre_epoch != c->buf_epoch) {
       if (c->pre_exec) cudaGraphExecDestroy(c->pre_exec);
       c->pre_exec = nullptr;
       const long c0[4] = {*cnt[0], *cnt[1], *cnt[2], *cnt[3]};
@@ -1081,7 +913,7 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
       c->pre_db = c->lib_calls - b0;
       c->launches = l0;
       c->lib_calls = b0;
-      c->pre_g = c->g;
+      c->pre_epoch = c->buf_epoch;
     }
     for (int q = 0; q < 4; ++q) {
       snap0[q] = *cnt[q] + c->pre_dsnap[q];
@@ -1122,19 +954,22 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   CK(cudaMemsetAsync(c->g + 1, 0, sizeof(double2) * maxit, c->st));
   HD_LAUNCH(HD_K_VEC, 2 * P, k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V, c->w, c->dres + 2, N));
   const int ldh = maxit + 1;
-  if (c->arn_mode == 2 && maxit + 1 <= kLsaMaxJ) {
+  if (c->arn_mode == 1 && maxit + 1 <= kLsaMaxJ) {
     // u_0 = r (unnormalised), sigma_0 = 1 / beta
     CK(cudaMemcpyAsync(c->V, c->w, N * sizeof(double2), cudaMemcpyDeviceToDevice, c->st));
     HD_LAUNCH(HD_K_VEC, 0.0, k_inv_scalar<<<1, 1, 0, c->st>>>(c->lsa_sig, c->dres + 2));
     const int G = c->lsa_G;
     if (c->graph_enabled && !c->prof_on) {
-      if (c->loop_maxit != maxit || c->loop_tol != opt.tolerance) build_loop_graph(c, maxit, opt.tolerance);
+      if (c->loop_maxit != maxit || c->loop_tol != opt.tolerance || c->loop_epoch != c->buf_epoch)
+        build_loop_graph(c, maxit, opt.tolerance);
       k_loop_init<<<1, 1, 0, c->st>>>(c->loop_state);
       CK(cudaGraphLaunch(c->loop_exec, c->st));
       CK(cudaMemcpyAsync(c->loop_host, c->loop_state, sizeof(LoopState), cudaMemcpyDeviceToHost, c->st));
       CK(cudaMemcpyAsync(c->res_host, c->res_hist, maxit * sizeof(double), cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
       const LoopState ls = *c->loop_host;
+      if (ls.nonfinite)
+        throw Error(HD_ERR_NONFINITE, "non-finite residual or Arnoldi norm at GMRES iteration " + std::to_string(ls.iters));
       // per-iteration launches of the body (op + 7) for the report
       int it = ls.iters;
       res.iterations = it;
@@ -1228,32 +1063,7 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
     }
     return res;
   }
-  const bool persistent = c->use_arnoldi && c->arn_mode == 1;
-  if (persistent) CK(cudaMemsetAsync(c->dj, 0, sizeof(int), c->st));
-  for (int j = 0; j < maxit && persistent; ++j) {
-    compose_op(c, c->V + static_cast<size_t>(j) * N, c->w);
-    // w in, V_0..V_j (MGS), V_{j+1} out, x0 + V_0..V_j in + x out (iterate)
-    launch_arnoldi(c, xout, maxit, nullptr, (2.0 * j + 6.0) * P);
-    res.iterations = j + 1;
-    monitor(xout);
-    read_scalars(c);
-    if (c->arn_trace) {
-      const unsigned long long* q = c->arn_trace;
-      c->arn_phase_ns[0] += static_cast<double>(q[1] - q[0]);  // MGS chain
-      c->arn_phase_ns[1] += static_cast<double>(q[2] - q[1]);  // V_{j+1} + Givens
-      c->arn_phase_ns[2] += static_cast<double>(q[3] - q[2]);  // barrier
-      c->arn_phase_ns[3] += static_cast<double>(q[4] - q[3]);  // iterate
-    }
-    const double rr = c->hres[0];
-    const double hnew = c->hres[1];
-    res.residuals.push_back(rr);
-    if (rr <= opt.tolerance) {
-      res.converged = true;
-      break;
-    }
-    if (hnew < 1e-300) break;
-  }
-  for (int j = 0; j < maxit && !persistent; ++j) {
+  for (int j = 0; j < maxit; ++j) {
     double2* Vj = c->V + static_cast<size_t>(j) * N;
     compose_op(c, Vj, c->w);
     double2* Hj = c->H + static_cast<size_t>(j) * ldh;
@@ -1284,12 +1094,6 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
                 k_scale_inv<<<grid_for(N), 256, 0, c->st>>>(c->V + static_cast<size_t>(j + 1) * N, c->w, c->dres + 1,
                                                             N));
     }
-  }
-  if (c->arn_trace) {
-    std::fprintf(stderr, "[hd trace] arnoldi phases over %d its (ms): mgs %.3f givens %.3f barrier %.3f iterate %.3f\n",
-                 res.iterations, c->arn_phase_ns[0] * 1e-6, c->arn_phase_ns[1] * 1e-6, c->arn_phase_ns[2] * 1e-6,
-                 c->arn_phase_ns[3] * 1e-6);
-    for (double& v : c->arn_phase_ns) v = 0.0;
   }
   return res;
 }

@@ -21,7 +21,6 @@ struct GenHost {
 __global__ void k_galerkin_stencil(const double* __restrict__ K, int n, int b, const int* __restrict__ cptr,
                                    const int* __restrict__ crow, const double* __restrict__ cw, int nc, int bc,
                                    double* __restrict__ Kc) {
-  HD_PDL_ENTRY();
   const int NB = 2 * b + 1, NBc = 2 * bc + 1;
   const size_t tot = (size_t)nc * nc * NBc * NBc;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
@@ -459,7 +458,7 @@ static void destroy_ctx(hd_ctx* c) {
   cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
   cudaFree(c->scal); cudaFree(c->dres); cudaFree(c->partials); cudaFree(c->counter);
   cudaFree(c->mon_partials); cudaFree(c->mon_counter);
-  cudaFree(c->dj); cudaFree(c->arn_partials); cudaFree(c->arn_bar);
+  cudaFree(c->dj);
   cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
   cudaFree(c->lsa_counter);
   if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
@@ -468,7 +467,6 @@ static void destroy_ctx(hd_ctx* c) {
   cudaFree(c->loop_state); cudaFree(c->res_hist); cudaFree(c->cublas_ws);
   if (c->loop_host) cudaFreeHost(c->loop_host);
   if (c->res_host) cudaFreeHost(c->res_host);
-  if (c->arn_trace) cudaFreeHost(c->arn_trace);
   if (c->hres) cudaFreeHost(c->hres);
   if (c->cb) cublasDestroy(c->cb);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -525,6 +523,8 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   c->N = c->dim == 2 ? static_cast<size_t>(c->n) * c->n : c->n;
   c->k = sys->k;
   c->spec = *spec;
+  // any cycles <= 0 is the exact shifted inverse with no V-cycles (src/precond.cpp:203-209)
+  if (c->spec.cycles < 0) c->spec.cycles = 0;
   if (c->spec.coarsest <= 0) c->spec.coarsest = 32;
   c->corner = c->dim == 1 ? cmk(sys->corner_re, sys->corner_im) : cmk(0.0, 0.0);
   // wedge: K2 carries k(x,y)^2 itself, so its coefficients are 1 and 1 - i beta2
@@ -632,7 +632,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
         A.ku = c->coarsest.ku;
         const size_t smem = tail_smem(A);
         if (smem <= 200u * 1024u) {
-          CK(cudaFuncSetAttribute(k_tail1d, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+          smem_optin(reinterpret_cast<const void*>(k_tail1d), smem);
           c->tail_smem_bytes = smem;
           c->tail_l = t;
         }
@@ -660,13 +660,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
     } else if (c->dim == 2) {
       const bool fold = (c->nc % 2 == 0) && centro_symmetric(ES) && centro_symmetric(EM) &&
                         !std::getenv("HD_NOFOLD");
-      const char* ey = std::getenv("HD_EYSOLVE");
-      // HD_EYSOLVE=1: partial diagonalisation + segmented y sweeps (experimental:
-      // equally exact, but its rounding differs from the oracle's FD by more
-      // than the C3/C5 history bars allow, and it is not yet faster -- DESIGN.md §4)
-      const bool ys = ey && std::atoi(ey) == 1 && c->cA.y == 0.0 && std::max(ES.b, EM.b) <= 6 && c->nc >= 4 * kYL;
       if (fold) c->E = make_fd_folded(c->st, ES, EM, c->cA);
-      else if (ys) c->E = make_fd_ypart(c->st, ES, EM, c->cA);
       else c->E = make_fd(c->st, ES, EM, c->cA);
     } else {
       // corner term of A restricted: Z^T (corner e_n e_n^T) Z
@@ -770,7 +764,8 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   CK(cudaMemset(c->mon_counter, 0, 4 * sizeof(unsigned)));
   CK(cudaStreamSynchronize(c->st));
   CK(cudaDeviceSynchronize());
-  if (const char* e = std::getenv("HD_ARNOLDI")) c->arn_mode = std::atoi(e);
+  // HD_ARNOLDI=0: exact-order MGS engine (one kernel per MGS step) for every budget
+  if (const char* e = std::getenv("HD_ARNOLDI")) c->arn_mode = std::atoi(e) == 0 ? 0 : 1;
   if (const char* e = std::getenv("HD_GRAPH")) c->graph_enabled = std::atoi(e) != 0;
   if (const char* e = std::getenv("HD_MON_SIDE")) c->mon_side = std::atoi(e) != 0;
   if (const char* e = std::getenv("HD_PRE_GRAPH")) c->pre_graph = std::atoi(e) != 0;

@@ -115,6 +115,7 @@ struct hd_slabs {
   int* hj = nullptr;                            // pinned mirror
   cudaGraphExec_t body = nullptr;
   int body_maxit = -1;
+  unsigned body_epoch = ~0u;  // hd_ctx::buf_epoch the body graph captured
   long body_delta[6] = {0, 0, 0, 0, 0, 0};      // counters one body adds (matvecs .. lib_calls)
   std::vector<SlabLevel> lv;                    // MG levels
   std::vector<std::vector<double2*>> X, Y, B, R;  // [level][slab], levels < g
@@ -128,7 +129,6 @@ struct hd_slabs {
 };
 
 __global__ void k_slab_sumsq(const double2* __restrict__ x, size_t N, RedOut red) {
-  HD_PDL_ENTRY();
   __shared__ double2 scratch[32];
   double acc = 0.0;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x)
@@ -139,7 +139,6 @@ __global__ void k_slab_sumsq(const double2* __restrict__ x, size_t N, RedOut red
 
 // norm = sqrt(sum of the slabs' raw sums, slab order) / scale -> dst (and cdst = (norm, 0))
 __global__ void k_slab_norm(const double* slots, int S, const double* scale_src, double* dst, double2* cdst) {
-  HD_PDL_ENTRY();
   double s = 0.0;
   for (int i = 0; i < S; ++i) s += slots[i];
   double sc = 1.0;
@@ -154,7 +153,6 @@ __global__ void k_slab_norm(const double* slots, int S, const double* scale_src,
 constexpr int kLsaNslot = 2 * kLsaMaxJ + 2;
 __global__ void k_lsa_slab_reduce(const double2* __restrict__ parts, int Gs, int j, const int* dj,
                                   double2* __restrict__ out) {
-  HD_PDL_ENTRY();
   if (dj) j = *dj;
   for (int q = threadIdx.x; q < kLsaNslot; q += blockDim.x) {
     const bool used = q < j + 1 || (q >= kLsaMaxJ + 1 && q < kLsaMaxJ + 1 + j);
@@ -430,7 +428,6 @@ static void s_mg_solve(hd_ctx* c, std::vector<double2*>& b, std::vector<double2*
 
 // rows [r0, r1) of both planes of a column-major n x n transform buffer scaled by Dinv
 __global__ void k_fd_scale_rows(double* __restrict__ T, const double2* __restrict__ Dinv, int n, int r0, int r1) {
-  HD_PDL_ENTRY();
   const size_t NN = (size_t)n * n;
   const int h = r1 - r0;
   const size_t tot = (size_t)h * n;
@@ -641,7 +638,6 @@ static void s_gather(hd_ctx* c, const std::vector<double2*>& v, double2* full) {
 
 // basis vector u_j of slab s <-> halo'd slab vectors
 __global__ void k_copy_basis(double2* __restrict__ dst, const double2* __restrict__ V, size_t Ns, const int* dj) {
-  HD_PDL_ENTRY();
   const double2* src = V + (size_t)(*dj) * Ns;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < Ns; g += (size_t)gridDim.x * blockDim.x)
     dst[g] = src[g];
@@ -744,6 +740,7 @@ static void build_slab_body(hd_ctx* c, int maxit, int nparts) {
   c->launches = static_cast<int>(before[4]);
   c->lib_calls = static_cast<int>(before[5]);
   sl->body_maxit = maxit;
+  sl->body_epoch = c->buf_epoch;
 }
 
 static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f_full, double2* xout_full) {
@@ -753,6 +750,7 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
   ensure_gmres(c, maxit);
   const SlabLevel& G = sl->lv[0];
   if (sl->maxit < maxit) {
+    ++c->buf_epoch;
     for (auto* p : sl->V) cudaFree(p);
     for (int s : sl->mine) sl->V[s] = dalloc<double2>(static_cast<size_t>(maxit + 1) * own(G, s) * G.n);
     sl->maxit = maxit;
@@ -817,7 +815,7 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
   bool stop = false;
   double hnew_prev = 1.0;
   const bool graph = c->graph_enabled && !c->prof_on;
-  if (graph && sl->body_maxit != maxit) build_slab_body(c, maxit, nparts);
+  if (graph && (sl->body_maxit != maxit || sl->body_epoch != c->buf_epoch)) build_slab_body(c, maxit, nparts);
   for (int j = 0; j < maxit && !stop; ++j) {
     const long snap[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
     auto rollback = [&]() {
@@ -966,7 +964,7 @@ static void create_slabs(hd_ctx* c, int S, int rank = 0, int nranks = 1, ncclCom
   {
     const ExactSolver& X = c->E;
     const char* de = std::getenv("HD_DIST_E");
-    sl->dist_e = c->spec.deflate && X.dim == 2 && X.V && !X.folded && !X.ypart && !X.dense && !X.btri &&
+    sl->dist_e = c->spec.deflate && X.dim == 2 && X.V && !X.folded && !X.dense && !X.btri &&
                  !(de && std::atoi(de) == 0);
     if (sl->dist_e) {
       const int nc = c->nc;

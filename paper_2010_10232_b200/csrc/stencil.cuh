@@ -55,7 +55,6 @@ __global__ void __launch_bounds__(kSW * kSWarps, HD_STENCIL_MINB) k_stencil2d(Le
                                                             double2* __restrict__ out, double omega, int RY,
                                                             RedOut red, const int* xidx, size_t xstride, int rb,
                                                             int re, double2* __restrict__ out2, double2 c2) {
-  HD_PDL_ENTRY();
   constexpr int NB = 2 * B + 1;
   constexpr int W = kSW + 2 * B;
   constexpr int kSRing = stencil_ring<B>();

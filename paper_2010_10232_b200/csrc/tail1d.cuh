@@ -181,7 +181,6 @@ __device__ void tail_vcycle(const TailArgs& a, double2* tsm, bool x_zero, int* c
 
 __global__ void __launch_bounds__(kTailThreads) k_tail1d(TailArgs a, const double2* __restrict__ bin,
                                                          double2* __restrict__ xout) {
-  HD_PDL_ENTRY();
   extern __shared__ __align__(16) double2 tsm[];
   double2* b0 = tsm + a.off[0] + 2 * a.n[0];
   for (int i = threadIdx.x; i < a.n[0]; i += blockDim.x) b0[i] = bin[i];

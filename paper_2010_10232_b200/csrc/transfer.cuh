@@ -34,7 +34,6 @@ __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* 
                                                     double2* __restrict__ outc, double* __restrict__ outp, int qb,
                                                     int qe, LevelDev Lc = LevelDev{}, double omega = 0.0,
                                                     double2* __restrict__ x0 = nullptr) {
-  HD_PDL_ENTRY();
   constexpr int lo = ZW<KIND>::lo, nw = ZW<KIND>::nw;
   constexpr int RR = 2 * kRQY + nw - 1;  // fine rows of the region
   constexpr int RC = 2 * kRQX + nw - 1;  // fine cols
@@ -149,7 +148,6 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
                                                    const double* __restrict__ ep, int nf, int nc,
                                                    const double2* __restrict__ s, double2* __restrict__ out, int fb,
                                                    int fe) {
-  HD_PDL_ENTRY();
   constexpr int CR = kPFY / 2 + 3, CC = kPFX / 2 + 3;
   __shared__ double2 cs[CR][CC];
   __shared__ double2 ty[kPFY][CC];  // y-interpolated coarse columns for every fine row of the tile
@@ -218,7 +216,6 @@ __global__ void __launch_bounds__(256) k_prolong2d(double drop, const double2* _
 // x = omega D^-1 b on a 2D level, 2D grid (no 64-bit div/mod per element)
 __global__ void __launch_bounds__(256) k_jacobi0_2d_t(LevelDev L, const double2* __restrict__ b,
                                                       double2* __restrict__ out, double omega, int rb, int re) {
-  HD_PDL_ENTRY();
   const int n = L.n, NB = 2 * L.b + 1;
   const int ix = blockIdx.x * 64 + (threadIdx.x & 63);
   const int iy0 = rb + blockIdx.y * 16 + (threadIdx.x >> 6) * 4;
