@@ -3,20 +3,24 @@
 preconditioned GMRES iterations/s & time-to-solution; achieved HBM GB/s).
 
 One "step" = one complete solve (hd_solve_device: transformed rhs, start
-vector, GMRES to tol 1e-7) of the workload on every rank.  Default workload:
-C5 = 2D point source, k = 1000, p = 3, 1600 x 1600 elements (N = 2,563,201
-complex doubles), DC_MG^1 with beta2 = 0.5, omega = 2/3, nu = 1 -- the largest
-BASELINE config and the one its roofline target names.
+vector, GMRES to tol 1e-7) of the workload.  Default workload: C5 = 2D point
+source, k = 1000, p = 3, 1600 x 1600 elements (N = 2,563,201 complex
+doubles), DC_MG^1 with beta2 = 0.5, omega = 2/3, nu = 1 -- the largest
+BASELINE config and the one its roofline and scaling targets name.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5]
-  python bench.py --impl reference ...   # the reference algorithm on the host CPU
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--replicas]
+  python bench.py --impl reference ...   # the reference algorithm on the host CPU (1 thread)
 
-N > 1 (torchrun): every rank solves its own replica (weak scaling, no
-data-path collective); with --slabs the ranks share one
-solve as row slabs over NCCL (hd_create_dist, strong scaling).  Timing: CUDA events on the
-library's stream (set to torch's current stream), barrier + synchronize on
-both sides, max over ranks; the L2 is flushed (256 MiB write) between steps
-outside the timed events.
+N > 1: one process per GPU.  Launched by torchrun (RANK / WORLD_SIZE set), or
+by this script itself when --gpus N > 1 and WORLD_SIZE is unset (it re-runs
+itself under torch.distributed.run on 127.0.0.1 and relays rank 0's line).
+2D configs then run ONE solve as N row slabs over NCCL (hd_create_dist,
+strong scaling); --replicas (and every 1D config) runs N
+independent replicas instead (weak scaling).  NCCL_DEBUG=INFO is set for
+N > 1 so the communicator lines show the rank count.
+Timing: CUDA events on a dedicated torch stream that the library, the L2
+flush and the events share; barrier + synchronize on both sides, max over
+ranks; the L2 is flushed (256 MiB write) between steps, outside the events.
 """
 from __future__ import annotations
 
@@ -86,36 +90,46 @@ def workload_name(cfg):
 # ---------------------------------------------------------------------------
 # CPU legs: the oracle restatement of the reference (test infrastructure)
 # ---------------------------------------------------------------------------
-def oracle_sample(cfg, iters, warm=0):
+def oracle_sample(cfg, iters, warm=0, threads=1):
     """Time `iters` GMRES iterations (after `warm` untimed ones) of the oracle
-    on the host; returns (iterations/s, seconds, note)."""
+    on `threads` host threads (1: the reference is single-threaded per solve,
+    README:262-263); returns (iterations/s, seconds, note, t_setup)."""
+    from threadpoolctl import threadpool_limits
     from oracle import helmdef_oracle as O
     dim, p, ne, k = CONFIGS[cfg]
-    pb = make_problem(O, cfg)
-    spec = O.to_spec(SPEC["tag"], p, k, beta2=SPEC["beta2"], cycles=SPEC["cycles"],
-                     smoothing=SPEC["smoothing"], omega=SPEC["omega"])
-    t0 = time.perf_counter()
-    s = O.assemble(pb)
-    big = dim == 2 and s.A.shape[0] > 300_000 and s.separable
-    setup = O.compose(s, spec, galerkin="kron" if dim == 2 and s.separable else "sparse",
-                      e_solver="fd" if big else "splu")
-    t_setup = time.perf_counter() - t0
-    gen = O.gmres_steps(setup.op, setup.rhs, setup.start, setup.monitor, O.GmresOptions(MAXIT, TOL))
-    done = 0
-    t_start = None
-    res = None
-    tic = time.perf_counter()
-    for res in gen:
-        done += 1
-        if done == warm:
-            tic = time.perf_counter()
-        if done >= warm + iters or res.converged:
-            break
-    el = time.perf_counter() - tic
+    with threadpool_limits(limits=threads):
+        pb = make_problem(O, cfg)
+        spec = O.to_spec(SPEC["tag"], p, k, beta2=SPEC["beta2"], cycles=SPEC["cycles"],
+                         smoothing=SPEC["smoothing"], omega=SPEC["omega"])
+        t0 = time.perf_counter()
+        s = O.assemble(pb)
+        big = dim == 2 and s.A.shape[0] > 300_000 and s.separable
+        setup = O.compose(s, spec, galerkin="kron" if dim == 2 and s.separable else "sparse",
+                          e_solver="fd" if big else "splu")
+        t_setup = time.perf_counter() - t0
+        gen = O.gmres_steps(setup.op, setup.rhs, setup.start, setup.monitor, O.GmresOptions(MAXIT, TOL))
+        done = 0
+        tic = time.perf_counter()
+        for res in gen:
+            done += 1
+            if done == warm:
+                tic = time.perf_counter()
+            if done >= warm + iters or res.converged:
+                break
+        el = time.perf_counter() - tic
     n = max(done - warm, 1)
-    note = (f"oracle port (scipy CSR SpMV + SuperLU/FD), first {warm}+{n} GMRES iterations of {cfg} "
-            f"after {t_setup:.1f}s untimed setup; E solve by {'fast diagonalisation' if big else 'SuperLU'}")
+    note = (f"oracle port (scipy CSR SpMV + {'fast diagonalisation' if big else 'SuperLU'} E solve), "
+            f"GMRES iterations {warm}..{warm + n - 1} of {cfg} on {threads} host thread(s), after "
+            f"{t_setup:.1f}s untimed assembly + setup")
     return n / el, el, note, t_setup
+
+
+def cpu_full_reference(cfg):
+    """A committed full CPU time-to-solution of the config (profiles/r2_cpu_full_<cfg>.json), if any."""
+    try:
+        return json.loads((ROOT / "profiles" / f"r2_cpu_full_{cfg}.json").read_text())
+    except Exception:
+        return None
 
 
 def cpu_threads():
@@ -131,16 +145,16 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    rate, el, note, t_setup = oracle_sample(args.config, args.steps, warm=args.warmup)
-    cores = cpu_threads()
+    rate, el, note, t_setup = oracle_sample(args.config, args.steps, warm=args.warmup, threads=1)
     line = {"metric": "preconditioned GMRES iterations/s", "value": rate, "unit": "iterations/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * el / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * el / max(args.steps, 1), "higher_is_better": True,
+            "scaling": "strong" if (args.gpus > 1 and CONFIGS[args.config][0] == 2 and not args.replicas) else "weak",
             "vs_baseline": None, "dtype": "c128 (f64 complex)", "data": "synthetic (deterministic point source)",
             "config": {"workload": workload_name(args.config), "step": "one GMRES iteration (CPU sample)"},
             "impl": "reference",
-            "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": cores, "kind": "port",
-                             "sample": note + "; SpMV single-threaded, BLAS threads=%d" % cores},
+            "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": 1, "kind": "port",
+                             "sample": note, "full_solve": cpu_full_reference(args.config)},
             "e2e": {"value": rate, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -210,13 +224,16 @@ def run_gpu(args):
     import paper_2010_10232_b200 as hd
 
     ws, rank, local = dist_env()
+    dim, p, ne, k = CONFIGS[args.config]
+    slabs = ws > 1 and dim == 2 and not args.replicas
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    dim, p, ne, k = CONFIGS[args.config]
     t_asm0 = time.perf_counter()
     sys_ = hd.assemble(make_problem(hd, args.config))
     t_assemble = time.perf_counter() - t_asm0
@@ -224,7 +241,7 @@ def run_gpu(args):
                       omega=SPEC["omega"])
     opt = hd.GmresOptions(MAXIT, TOL)
     N = sys_.size
-    if args.slabs:
+    if slabs:
         # row slabs, one per process, NCCL transport (hd_create_dist): strong scaling of one solve
         uid = [hd.nccl_unique_id() if rank == 0 else None]
         if dist:
@@ -235,11 +252,13 @@ def run_gpu(args):
     # setup of a second context in this process: hd_create without the one-time
     # CUDA / cuBLAS / cuSOLVER initialisation the first context pays
     t_setup_warm = None
-    if not args.slabs:
+    if not slabs:
         t_w0 = time.perf_counter()
         with hd.Solver(sys_, spec, devices=[local]):
             t_setup_warm = time.perf_counter() - t_w0
-    stream = torch.cuda.current_stream(dev)
+    # one dedicated stream for the library, the L2 flush and the timing events
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     solver.set_stream(stream.cuda_stream)
     rhs_d = torch.from_numpy(sys_.rhs.view(np.float64)).to(dev)
     x_d = torch.zeros(2 * N, dtype=torch.float64, device=dev)
@@ -283,7 +302,7 @@ def run_gpu(args):
     prof = solver.profile_read()
     solver.profile(False)
     t_max, iters_all = rank_reduce(dist, t_ms, iters, dev)
-    if args.slabs:
+    if slabs:
         iters_all /= ws  # one distributed solve: every rank reports the same iterations
     value = iters_all / (t_max * 1e-3)
 
@@ -310,7 +329,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     e_ms = float(sum(a.elapsed_time(b) for a, b in e_evs))
     e_ms, e_iters = rank_reduce(dist, e_ms, e_iters, dev)
-    if args.slabs:
+    if slabs:
         e_iters /= ws
     e2e = {"value": e_iters / (e_ms * 1e-3), "unit": "iterations/s", "h2d_bytes_per_step": 16 * N,
            "d2h_bytes_per_step": 16 * N + 8 * (r.iterations), "ms_per_step": e_ms / args.steps}
@@ -343,31 +362,27 @@ def run_gpu(args):
         roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "traffic_source": traffic_src, "launches": n,
                 "bytes_per_launch": b / n, "us_per_launch": 1e3 * ms / n, "peak_source": peak_src}
-    # whole-solve effective bandwidth on the algorithmic bytes of all own kernels
+    # whole path: the algorithmic bytes of every own kernel of one solve (each
+    # launch's compulsory vector passes: (2j+8) P for the Arnoldi passes of
+    # iteration j, the fine / multigrid / projection passes, the monitor) over
+    # the timed solve time.  Coarse multigrid levels are counted as HBM bytes
+    # although they are L2-resident, so this is an upper bound on the DRAM
+    # traffic the solve needs; the deflation GEMMs (compute) add none.
     all_b = sum(v[2] for k_, v in prof.items() if k_ != "lib_gemm")
-    # SURVEY.md 8(d) path roofline: compulsory bytes B_min(j) of the reference's
-    # formulation (MGS + per-step iterate), summed over this solve's iterations
-    L = solver.levels
-    if L > 1:
-        nl = [solver.level_size(l) ** dim for l in range(L)]
-        mg = sum((6 * SPEC["smoothing"] + 2) * nl[l] / N + 2 * nl[l + 1] / N for l in range(L - 1))
-    else:
-        mg = 0.0
-    base = (18.0 if dim == 2 else 19.0) + SPEC["cycles"] * mg
-    bmin = sum(16.0 * N * (base + 5 * j) for j in range(r.iterations))
-    path_bmin = {"bytes_per_solve": bmin, "GBps": round(bmin / (t_max / args.steps * 1e-3) / 1e9, 1),
-                 "frac": round(bmin / (t_max / args.steps * 1e-3) / 1e9 / peak, 4),
-                 "note": "SURVEY.md 8(d) B_min(j) = 16N[18 + 5j + c*MG] (2D): the reference's MGS formulation; "
-                         "this path's one-reduction Arnoldi streams ~2j vector passes per iteration, not 5j"}
+    t_solve_s = t_max / args.steps * 1e-3
+    path = {"bytes_per_solve": all_b, "GBps": round(all_b / t_solve_s / 1e9, 1),
+            "frac": round(all_b / t_solve_s / 1e9 / peak, 4),
+            "note": "sum of the per-launch algorithmic bytes of one profiled solve (own kernels) over the "
+                    "timed solve time; coarse levels counted as HBM bytes"}
 
     line = {"metric": "preconditioned GMRES iterations/s", "value": value, "unit": "iterations/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-            "higher_is_better": True, "scaling": "strong" if args.slabs else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if slabs else "weak", "vs_baseline": None,
             "dtype": "c128 (f64 complex)",
             "data": "synthetic (deterministic point source, as the reference)",
             "config": {"workload": workload_name(args.config), "N": N, "iterations_per_solve": r.iterations,
                        "step": "one full solve (hd_solve_device)",
-                       "parallelism": (f"row slabs x{ws} (NCCL)" if args.slabs else
+                       "parallelism": (f"row slabs x{ws} (NCCL)" if slabs else
                                        (f"replicas x{ws}" if ws > 1 else "single GPU")),
                        "l2": "flushed (256 MiB write) between steps, outside the timed events"},
             "time_to_solution_ms": t_max / args.steps, "t_setup_s": r.t_setup,
@@ -378,13 +393,12 @@ def run_gpu(args):
             "roofline": roof, "kernel_breakdown": breakdown,
             "roofline_note": "per-kernel CUDA events of one extra profiled solve (host-driven launch loop) "
                              "after the timed region; achieved = algorithmic bytes / event time",
-            "solve_effective_GBps": round(all_b / (tot_prof_ms * 1e-3) / 1e9, 1) if prof else None,
-            "path_roofline_Bmin": path_bmin,
+            "path_roofline": path,
             "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, el, note, _ = oracle_sample(args.config, args.cpu_iters)
-        line["cpu_baseline"] = {"value": rate, "unit": "iterations/s", "cores": cpu_threads(), "kind": "port",
-                                "sample": note}
+        rate, el, note, _ = oracle_sample(args.config, args.cpu_iters, warm=args.cpu_warm, threads=1)
+        line["cpu_baseline"] = {"value": rate, "unit": "iterations/s", "cores": 1, "kind": "port",
+                                "sample": note, "full_solve": cpu_full_reference(args.config)}
     solver.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -400,15 +414,32 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C5")
-    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--cpu-iters", type=int, default=6, help="GMRES iterations timed by the cpu_baseline leg")
+    ap.add_argument("--cpu-warm", type=int, default=2, help="untimed GMRES iterations before them")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--slabs", action="store_true",
-                    help="N > 1: one row slab per rank over NCCL (hd_create_dist), strong scaling of one solve; "
-                         "default: N independent replicas")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent replicas (weak scaling) instead of one solve as N row slabs")
     args = ap.parse_args()
+    ws, _, _ = dist_env()
+    if args.gpus > 1 and ws == 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)
+
+
+def spawn_ranks(args):
+    """--gpus N without a launcher: re-run this script as N ranks under
+    torch.distributed.run on 127.0.0.1 (one process per GPU); every rank's
+    output is relayed, rank 0 prints the JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

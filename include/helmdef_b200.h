@@ -199,6 +199,14 @@ hd_status hd_solve(hd_ctx* ctx, const hd_gmres* opt, const double* rhs, double* 
 hd_status hd_solve_device(hd_ctx* ctx, const hd_gmres* opt, const double* d_rhs,
                           double* d_x, double* residuals_out, hd_report* report);
 
+/* Exact direct solve x = A^-1 rhs of the unshifted operator on the current
+ * device -- the reference's DirectSolver(sys.A).solve(sys.rhs) behind
+ * RunRecord::direct_gap (src/harness.cpp:234-238, src/linalg.cpp:94-102):
+ * fast diagonalisation (2D constant k), banded LU (1D), dense or block
+ * tridiagonal LU (layered / wedge).  Host buffers of 2N doubles; builds and
+ * frees a transient context. */
+hd_status hd_direct_solve(const hd_system* sys, const double* rhs, double* x_out);
+
 /* Vector length N (= per_dim^dim) and multigrid level count of a context. */
 long hd_size(const hd_ctx* ctx);
 int hd_levels(const hd_ctx* ctx);
@@ -229,6 +237,14 @@ enum { HD_K_OP_FINE = 0, HD_K_OP_COARSE = 1, HD_K_JACOBI0 = 2, HD_K_TRANSFER = 3
        HD_K_MGS = 5, HD_K_ITERATE = 6, HD_K_VEC = 7, HD_K_GIVENS = 8, HD_K_LIBGEMM = 9, HD_K_COUNT = 10 };
 hd_status hd_profile(hd_ctx* ctx, int enable);
 hd_status hd_profile_read(hd_ctx* ctx, int kind, long* launches, double* ms, double* bytes);
+
+/* Memory checking without compute-sanitizer (not available on the GPU pool):
+ * with HD_POISON=1 in the environment every device allocation of the library
+ * is filled with 0xFF bytes (NaN in every double) and framed by poisoned guard
+ * zones, so reads of never-written memory poison the result and out-of-bounds
+ * stores change a guard.  Returns the number of changed guards over all live
+ * allocations of the process (0 when HD_POISON is unset), -1 on a CUDA error. */
+long hd_debug_check_guards(void);
 
 void hd_destroy(hd_ctx* ctx);
 const char* hd_last_error(void);

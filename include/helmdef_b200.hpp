@@ -22,6 +22,8 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <limits>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -226,7 +228,8 @@ class SolverSetup {
   hd_ctx* ctx_ = nullptr;
 };
 
-inline SolverSetup compose(const DiscreteSystem& sys, const PrecondSpec& spec) {
+// the device's view of a DiscreteSystem (plain pointers into sys; sys must outlive the call)
+inline hd_system to_hd_system(const DiscreteSystem& sys) {
   hd_system hs{};
   hs.dim = sys.dim;
   hs.order = sys.order;
@@ -239,6 +242,11 @@ inline SolverSetup compose(const DiscreteSystem& sys, const PrecondSpec& spec) {
   hs.mass_band = sys.mass_band.data();
   hs.interval_mass = sys.layered ? sys.interval_mass.data() : nullptr;
   hs.shift_mass_2d = sys.wedge ? sys.shift_mass_2d.data() : nullptr;
+  return hs;
+}
+
+inline SolverSetup compose(const DiscreteSystem& sys, const PrecondSpec& spec) {
+  const hd_system hs = to_hd_system(sys);
   hd_precond hp{};
   hp.deflate = spec.deflate ? 1 : 0;
   hp.drop = spec.drop;
@@ -291,10 +299,12 @@ inline double resolve_beta2(const std::string& expr, double k) {  // src/harness
   if (expr == "1/(3k)") return 1.0 / (3.0 * k);
   return std::stod(expr);
 }
+// src/harness.cpp:175-205, including the per-degree overrides of :200-203
 inline PrecondSpec to_spec(const std::string& tag, int order, double k, double epsilon = 0.1,
-                           const std::string& beta2 = "1", int cycles = 1, int smoothing = 1, double omega = 0.6) {
-  (void)order;
-  PrecondSpec s;  // src/harness.cpp:175-205
+                           const std::string& beta2 = "1", int cycles = 1, int smoothing = 1, double omega = 0.6,
+                           const std::map<int, int>& smoothing_by_p = {},
+                           const std::map<int, double>& omega_by_p = {}) {
+  PrecondSpec s;
   if (tag == "D") {
     s.deflate = true;
   } else if (tag == "D_eps") {
@@ -314,15 +324,17 @@ inline PrecondSpec to_spec(const std::string& tag, int order, double k, double e
     throw Error(HD_ERR_INVALID, "unknown preconditioner tag: " + tag);
   }
   if (s.shift) s.beta2 = resolve_beta2(beta2, k);
-  s.smooth_steps = smoothing;
-  s.omega = omega;
+  const auto is = smoothing_by_p.find(order);
+  s.smooth_steps = is != smoothing_by_p.end() ? is->second : smoothing;
+  const auto io = omega_by_p.find(order);
+  s.omega = io != omega_by_p.end() ? io->second : omega;
   return s;
 }
 inline std::string label(const std::string& tag, int cycles) {  // src/harness.cpp:77-82
   return (tag == "DC_MG" || tag == "Deps_C_MG") ? tag + "^" + std::to_string(cycles) : tag;
 }
 
-struct RunRecord {  // include/helmdef/harness.hpp:81-98 (direct_gap and config_hash not produced)
+struct RunRecord {  // include/helmdef/harness.hpp:81-98
   std::string problem, tag;
   double k = 0.0;
   int order = 0, elements = 0;
@@ -330,8 +342,10 @@ struct RunRecord {  // include/helmdef/harness.hpp:81-98 (direct_gap and config_
   int iterations = 0;
   bool converged = false;
   double residual = 0.0;
+  double direct_gap = std::numeric_limits<double>::quiet_NaN();  // ||x - A^-1 f|| / ||A^-1 f|| (check_direct)
   long matvecs = 0, shift_solves = 0, vcycles = 0, coarse_solves = 0;
   double seconds = 0.0;
+  std::string config_hash;  // FNV-1a of the sweep config (helmdef_b200_harness.hpp)
 };
 
 inline RunRecord run_cell(const Problem& pb, const PrecondSpec& spec, const std::string& tag,

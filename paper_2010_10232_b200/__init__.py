@@ -43,7 +43,7 @@ HD_APPLY_A, HD_APPLY_SHIFTED, HD_APPLY_MG, HD_APPLY_PROJECT, HD_APPLY_OP, HD_APP
 EXPORTS = ["hd_problem_per_dim", "hd_assemble", "hd_assemble_field", "hd_create", "hd_solve", "hd_solve_device", "hd_size",
            "hd_levels", "hd_apply", "hd_debug_level", "hd_level_size", "hd_set_stream", "hd_profile",
            "hd_profile_read", "hd_destroy", "hd_last_error", "hd_create_slabs", "hd_slab_info",
-           "hd_nccl_unique_id", "hd_create_dist"]
+           "hd_nccl_unique_id", "hd_create_dist", "hd_direct_solve", "hd_debug_check_guards"]
 KERNEL_KINDS = ["op_fine", "op_coarse", "jacobi0", "transfer", "exact", "mgs", "iterate", "vec", "givens",
                 "lib_gemm"]
 
@@ -131,6 +131,10 @@ def load_library() -> C.CDLL:
     lib.hd_profile_read.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_long), C.POINTER(C.c_double),
                                     C.POINTER(C.c_double)]
     lib.hd_profile_read.restype = C.c_int
+    lib.hd_direct_solve.argtypes = [C.POINTER(HdSystem), dp, dp]
+    lib.hd_direct_solve.restype = C.c_int
+    lib.hd_debug_check_guards.argtypes = []
+    lib.hd_debug_check_guards.restype = C.c_long
     lib.hd_destroy.argtypes = [C.c_void_p]
     lib.hd_destroy.restype = None
     lib.hd_last_error.argtypes = []
@@ -355,6 +359,48 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def _hd_system(sys_: DiscreteSystem):
+    """hd_system view of a DiscreteSystem (+ the arrays it points into, to keep alive)."""
+    pb = sys_.problem
+    h = HdSystem()
+    h.dim, h.order, h.elements, h.per_dim = pb.dim, pb.order, pb.elements, sys_.per_dim
+    h.field_kind = HD_FIELD_WEDGE if pb.wedge else (HD_FIELD_LAYERED if pb.layered else HD_FIELD_CONSTANT)
+    h.k = pb.k
+    for i, m in enumerate(pb.multipliers):
+        h.multipliers[i] = m
+    keep = [np.ascontiguousarray(sys_.stiffness_band), np.ascontiguousarray(sys_.mass_band)]
+    h.stiffness_band = _dp(keep[0])
+    h.mass_band = _dp(keep[1])
+    if sys_.interval_mass is not None:
+        keep.append(np.ascontiguousarray(sys_.interval_mass))
+        h.interval_mass = _dp(keep[-1])
+    if sys_.shift_mass_2d is not None:
+        keep.append(np.ascontiguousarray(sys_.shift_mass_2d))
+        h.shift_mass_2d = _dp(keep[-1])
+    return h, keep
+
+
+def direct_solve(sys_: DiscreteSystem, rhs: Optional[np.ndarray] = None) -> np.ndarray:
+    """x = A^-1 f by an exact device solve (hd_direct_solve): the reference's
+    DirectSolver(sys.A).solve(sys.rhs) behind RunRecord::direct_gap
+    (src/harness.cpp:234-238)."""
+    lib = load_library()
+    h, keep = _hd_system(sys_)
+    b = np.ascontiguousarray(sys_.rhs if rhs is None else rhs, dtype=np.complex128)
+    x = np.zeros_like(b)
+    _check(lib.hd_direct_solve(C.byref(h), _dp(b.view(np.float64)), _dp(x.view(np.float64))))
+    return x
+
+
+def check_guards() -> int:
+    """Changed guard zones over the live device allocations (HD_POISON=1 runs;
+    the pool has no compute-sanitizer, see include/helmdef_b200.h)."""
+    n = load_library().hd_debug_check_guards()
+    if n < 0:
+        raise HelmdefError(2, load_library().hd_last_error().decode())
+    return int(n)
+
+
 class Solver:
     """compose(sys, spec) on the device; .solve() is gmres(op, rhs, start, monitor)."""
 
@@ -365,23 +411,7 @@ class Solver:
         self._lib = lib
         self.sys = sys_
         self.spec = spec
-        pb = sys_.problem
-        h = HdSystem()
-        h.dim, h.order, h.elements, h.per_dim = pb.dim, pb.order, pb.elements, sys_.per_dim
-        h.field_kind = HD_FIELD_WEDGE if pb.wedge else (HD_FIELD_LAYERED if pb.layered else HD_FIELD_CONSTANT)
-        h.k = pb.k
-        for i, m in enumerate(pb.multipliers):
-            h.multipliers[i] = m
-        self._S = np.ascontiguousarray(sys_.stiffness_band)
-        self._M = np.ascontiguousarray(sys_.mass_band)
-        h.stiffness_band = _dp(self._S)
-        h.mass_band = _dp(self._M)
-        if sys_.interval_mass is not None:
-            self._IM = np.ascontiguousarray(sys_.interval_mass)
-            h.interval_mass = _dp(self._IM)
-        if sys_.shift_mass_2d is not None:
-            self._K2 = np.ascontiguousarray(sys_.shift_mass_2d)
-            h.shift_mass_2d = _dp(self._K2)
+        h, self._keep = _hd_system(sys_)
         p = HdPrecond(int(spec.deflate), spec.drop, int(spec.shift), spec.beta2, spec.cycles,
                       spec.smooth_steps, spec.omega, spec.coarsest)
         ctx = C.c_void_p()

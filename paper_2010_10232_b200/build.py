@@ -24,6 +24,22 @@ COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include"
 
 TOOL_SRC = ROOT / "tools" / "hd_cell.cpp"
 TOOL = ROOT / "tools" / "hd_cell"
+BENCH_SRC = ROOT / "tools" / "hd_bench.cpp"
+BENCH = ROOT / "tools" / "hd_bench"
+
+
+def nlohmann_include():
+    """Directory holding nlohmann/json.hpp (the reference's JSON library; this
+    image ships it inside site-packages, e.g. cudnn_frontend's thirdparty)."""
+    env = os.environ.get("HD_NLOHMANN_INCLUDE")
+    if env:
+        return Path(env)
+    import site
+    roots = [Path(p) for p in site.getsitepackages()] + [Path("/usr/include"), Path("/usr/local/include")]
+    for r in roots:
+        for hit in sorted(r.glob("**/nlohmann/json.hpp")) if r.is_dir() else []:
+            return hit.parent.parent
+    return None
 CU_SOURCES = ["solver.cu"]
 CPP_SOURCES = ["host/banded.cpp", "host/assembly.cpp"]
 
@@ -72,6 +88,13 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
     if TOOL_SRC.exists() and _stale(TOOL, [TOOL_SRC, OUT, ROOT / "include" / "helmdef_b200.hpp"]):
         _run(["g++", "-O2", "-std=c++17", "-Wall", "-I", str(ROOT / "include"), str(TOOL_SRC), "-o", str(TOOL),
               "-L", str(PKG), "-lhelmdef_b200", "-Wl,-rpath,$ORIGIN/../paper_2010_10232_b200"])
+    # the helmbench CLI mirror (table / compare / solve) with the JSON harness
+    inc = nlohmann_include()
+    hdrs = [ROOT / "include" / "helmdef_b200.hpp", ROOT / "include" / "helmdef_b200_harness.hpp"]
+    if inc is not None and BENCH_SRC.exists() and _stale(BENCH, [BENCH_SRC, OUT, *hdrs]):
+        _run(["g++", "-O2", "-std=c++17", "-Wall", "-I", str(ROOT / "include"), "-I", str(inc), str(BENCH_SRC),
+              "-o", str(BENCH), "-L", str(PKG), "-lhelmdef_b200", "-pthread",
+              "-Wl,-rpath,$ORIGIN/../paper_2010_10232_b200"])
     return OUT
 
 

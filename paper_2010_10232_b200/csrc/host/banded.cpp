@@ -88,26 +88,31 @@ Band galerkin(const Band& A, const Transfer& z) {
   return C.trimmed();
 }
 
-BandLU band_lu(const Band& S, const Band& M, cplx c, cplx corner) {
+namespace {
+
+// Banded LU with partial pivoting of S - c M (+ corner), scalar type T
+// (complex for the 1D operators, real for the per-mode systems of the
+// partially diagonalised E); the same elimination order for both.
+template <class T, class F>
+void band_lu_t(const Band& S, const Band& M, T c, T corner, F& f) {
   const int n = S.n;
   const int kl = std::max(S.b, M.b);
   const int ku = kl;
   const int w = 2 * kl + ku + 1;  // window columns [i-kl, i+kl+ku]
-  std::vector<cplx> W(static_cast<size_t>(n) * w, cplx(0.0, 0.0));
-  auto el = [&](int i, int j) -> cplx& { return W[static_cast<size_t>(i) * w + (j - i + kl)]; };
+  std::vector<T> W(static_cast<size_t>(n) * w, T(0.0));
+  auto el = [&](int i, int j) -> T& { return W[static_cast<size_t>(i) * w + (j - i + kl)]; };
   for (int i = 0; i < n; ++i)
     for (int d = -kl; d <= ku; ++d) {
       const int j = i + d;
       if (j < 0 || j >= n) continue;
-      el(i, j) = cplx(S.at(i, j), 0.0) - c * M.at(i, j);
+      el(i, j) = T(S.at(i, j)) - c * M.at(i, j);
     }
   el(n - 1, n - 1) += corner;
-  BandLU f;
   f.n = n;
   f.kl = kl;
   f.ku = kl + ku;
-  f.L.assign(static_cast<size_t>(n) * std::max(kl, 1), cplx(0.0, 0.0));
-  f.U.assign(static_cast<size_t>(n) * (f.ku + 1), cplx(0.0, 0.0));
+  f.L.assign(static_cast<size_t>(n) * std::max(kl, 1), T(0.0));
+  f.U.assign(static_cast<size_t>(n) * (f.ku + 1), T(0.0));
   f.piv.assign(n, 0);
   for (int k = 0; k < n; ++k) {
     const int last = std::min(n - 1, k + kl);
@@ -123,18 +128,31 @@ BandLU band_lu(const Band& S, const Band& M, cplx c, cplx corner) {
     const int jend = std::min(n - 1, k + kl + ku);
     if (p != k)
       for (int j = k; j <= jend; ++j) std::swap(el(k, j), el(p, j));
-    const cplx piv = el(k, k);
+    const T piv = el(k, k);
     for (int i = k + 1; i <= last; ++i) {
-      const cplx l = el(i, k) / piv;
+      const T l = el(i, k) / piv;
       f.L[static_cast<size_t>(k) * kl + (i - k - 1)] = l;
-      if (l == cplx(0.0, 0.0)) continue;
+      if (l == T(0.0)) continue;
       for (int j = k + 1; j <= jend; ++j) el(i, j) -= l * el(k, j);
     }
     for (int d = 0; d <= f.ku; ++d) {
       const int j = k + d;
-      f.U[static_cast<size_t>(k) * (f.ku + 1) + d] = j < n ? el(k, j) : cplx(0.0, 0.0);
+      f.U[static_cast<size_t>(k) * (f.ku + 1) + d] = j < n ? el(k, j) : T(0.0);
     }
   }
+}
+
+}  // namespace
+
+BandLU band_lu(const Band& S, const Band& M, cplx c, cplx corner) {
+  BandLU f;
+  band_lu_t<cplx>(S, M, c, corner, f);
+  return f;
+}
+
+BandLUr band_lu_real(const Band& S, const Band& M, double c) {
+  BandLUr f;
+  band_lu_t<double>(S, M, c, 0.0, f);
   return f;
 }
 

@@ -67,6 +67,14 @@ struct BandLU {
 /// Factor the complex banded matrix (S - c M) (+ corner at (n-1,n-1)).
 BandLU band_lu(const Band& S, const Band& M, cplx c, cplx corner = cplx(0.0, 0.0));
 
+/// The same factorisation in real arithmetic (real S - c M).
+struct BandLUr {
+  int n = 0, kl = 0, ku = 0;
+  std::vector<double> L, U;
+  std::vector<int> piv;
+};
+BandLUr band_lu_real(const Band& S, const Band& M, double c);
+
 /// Reference host solve (used by the unit test of the factorisation only).
 std::vector<cplx> band_lu_solve(const BandLU& f, std::vector<cplx> b);
 

@@ -37,6 +37,7 @@
 #include "arnoldi_lowsync.cuh"
 #include "layered.cuh"
 #include "btri.cuh"
+#include "pfd.cuh"
 #include "segsolve.cuh"
 #include "tail1d.cuh"
 #include "small1d.cuh"
@@ -250,6 +251,28 @@ hd_status hd_solve_device(hd_ctx* c, const hd_gmres* opt, const double* d_rhs, d
   return solve_impl(c, opt, d_rhs, true, d_x, true, residuals_out, report);
 }
 
+hd_status hd_direct_solve(const hd_system* sys, const double* rhs, double* x_out) {
+  HD_GUARD_BEGIN
+  if (!sys || !rhs || !x_out) throw Error(HD_ERR_INVALID, "null argument");
+  // A itself is the "shifted" operator with beta2 = 0; cycles = 0 selects its exact inverse
+  hd_precond p{};
+  p.shift = 1;
+  p.beta2 = 0.0;
+  p.cycles = 0;
+  p.smooth_steps = 1;
+  p.omega = 0.6;
+  p.coarsest = 32;
+  hd_ctx* c = nullptr;
+  create_ctx(sys, &p, nullptr, 0, &c);
+  std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> guard(c, destroy_ctx);
+  const size_t N = c->N;
+  CK(cudaMemcpyAsync(c->f, rhs, N * sizeof(double2), cudaMemcpyHostToDevice, c->st));
+  shift_exact_solve(c, c->f, c->x);
+  CK(cudaMemcpyAsync(x_out, c->x, N * sizeof(double2), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  HD_GUARD_END
+}
+
 long hd_size(const hd_ctx* c) { return c ? static_cast<long>(c->N) : -1; }
 int hd_levels(const hd_ctx* c) { return c ? static_cast<int>(c->lev.size()) : -1; }
 
@@ -372,6 +395,15 @@ hd_status hd_debug_level(hd_ctx* c, int which, int level, const double* d_x, dou
   }
   CK(cudaStreamSynchronize(c->st));
   HD_GUARD_END
+}
+
+long hd_debug_check_guards(void) {
+  try {
+    return check_guards();
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return -1;
+  }
 }
 
 void hd_destroy(hd_ctx* c) { destroy_ctx(c); }

@@ -315,6 +315,33 @@ static void btri_solve(hd_ctx* c, ExactSolver& X, double* inout) {
 }
 
 static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
+  if (X.pfd) {
+    const int n = X.n, np = X.np;
+    const double one = 1.0, zero = 0.0;
+    const double gb = 16.0 * n * n * 2 + 8.0 * n * n;  // planar in/out + V (bytes of one GEMM)
+    size_t mk = prof_mark(c);
+    // T = V^T [Bre | Bim]  (x modes; leading dimension np)
+    CKB(cublasDgemm(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, inout, n, &zero, X.T1, np));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    PfdArgs a{X.T1, X.pfdF, X.pfdB, n, np};
+    const int ng = np / kPG;
+    const double tb = 8.0 * n * static_cast<double>(np) * ((X.pfd_kl + 1) + (2 * X.pfd_kl + 1)) + 64.0 * n * np;
+    switch (X.pfd_kl) {
+#define HD_PFD(KL)                                                                                   \
+  case KL:                                                                                         \
+    smem_optin(reinterpret_cast<const void*>(k_pfd_ysolve<KL>), pfd_smem<KL>());                    \
+    HD_LAUNCH(HD_K_EXACT, tb, k_pfd_ysolve<KL><<<ng, 32, pfd_smem<KL>(), c->st>>>(a));             \
+    break;
+      HD_PFD(1) HD_PFD(2) HD_PFD(3) HD_PFD(4)
+#undef HD_PFD
+      default: throw Error(HD_ERR_INVALID, "partial diagonalisation: band half-width");
+    }
+    mk = prof_mark(c);
+    // X = V [Yre | Yim]
+    CKB(cublasDgemm(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, X.T1, np, &zero, inout, n));
+    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    return;
+  }
   if (X.btri) {
     btri_solve(c, X, inout);
     return;
@@ -577,13 +604,13 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
   // every branch below that reallocates moves pointers the loop / prelude graphs captured
   if (maxit + 1 > c->v_cap) {
     ++c->buf_epoch;
-    cudaFree(c->V);
+    dfree(c->V);
     c->V = dalloc<double2>(static_cast<size_t>(maxit + 1) * c->N);
     c->v_cap = maxit + 1;
   }
   if (maxit > c->maxit_cap) {
     ++c->buf_epoch;
-    cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
+    dfree(c->H); dfree(c->g); dfree(c->cs); dfree(c->sn); dfree(c->y);
     c->H = dalloc<double2>(static_cast<size_t>(maxit + 1) * maxit);
     c->g = dalloc<double2>(maxit + 1);
     c->cs = dalloc<double2>(maxit);
@@ -602,7 +629,7 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
     per = std::max(1, std::min(per, per2));
     const size_t tiles = (c->N + static_cast<size_t>(kLsaBD) * kLsaTE - 1) / (static_cast<size_t>(kLsaBD) * kLsaTE);
     c->lsa_G = static_cast<int>(std::max<size_t>(1, std::min<size_t>(tiles, static_cast<size_t>(sms) * per)));
-    cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
+    dfree(c->lsa_sig); dfree(c->lsa_L); dfree(c->lsa_ch); dfree(c->lsa_cx); dfree(c->lsa_partials);
     c->lsa_sig = dalloc<double>(maxit + 2);
     c->lsa_L = dalloc<double2>(static_cast<size_t>(maxit + 1) * (maxit + 1));
     c->lsa_ch = dalloc<double2>(maxit + 2);
@@ -689,7 +716,7 @@ static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
     c->loop_state = dalloc<LoopState>(1);
     CK(cudaMallocHost(&c->loop_host, sizeof(LoopState)));
   }
-  cudaFree(c->res_hist);
+  dfree(c->res_hist);
   if (c->res_host) cudaFreeHost(c->res_host);
   c->res_hist = dalloc<double>(maxit + 1);
   CK(cudaMallocHost(&c->res_host, (maxit + 1) * sizeof(double)));

@@ -90,11 +90,11 @@ static void galerkin_stencil2d(const std::vector<double>& K, int n, int b, const
   CK(cudaGetLastError());
   Kc.resize(outn);
   CK(cudaMemcpy(Kc.data(), dKc, outn * sizeof(double), cudaMemcpyDeviceToHost));
-  cudaFree(dK);
-  cudaFree(dKc);
-  cudaFree(dptr);
-  cudaFree(drow);
-  cudaFree(dw);
+  dfree(dK);
+  dfree(dKc);
+  dfree(dptr);
+  dfree(drow);
+  dfree(dw);
 }
 
 // wedge fine level: (M, S), (S, M) and the stored K2 stencil
@@ -255,11 +255,11 @@ static ExactSolver make_dense(cudaStream_t st, const GenHost& h, double2 cl, int
   CK(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   cusolverDnDestroy(hs);
-  cudaFree(A);
-  cudaFree(work);
-  cudaFree(ipiv);
-  cudaFree(info);
-  cudaFree(mem);
+  dfree(A);
+  dfree(work);
+  dfree(ipiv);
+  dfree(info);
+  dfree(mem);
   if (hinfo[0] != 0 || hinfo[1] != 0)
     throw Error(HD_ERR_FACTOR, "layered exact solve: singular operator (getrf info " + std::to_string(hinfo[0]) + ")");
   return X;
@@ -370,10 +370,10 @@ static void btri_factor(cudaStream_t st, const GenLevel& L, int q, int m, int nb
   CK(cudaStreamSynchronize(st));
   cublasDestroy(cb);
   cusolverDnDestroy(hs);
-  cudaFree(D); cudaFree(Bu); cudaFree(Cl); cudaFree(work); cudaFree(ipiv); cudaFree(info);
+  dfree(D); dfree(Bu); dfree(Cl); dfree(work); dfree(ipiv); dfree(info);
   for (int v : hinfo)
     if (v != 0) {
-      cudaFree(GT); cudaFree(SinvT); cudaFree(HT); cudaFree(G2);
+      dfree(GT); dfree(SinvT); dfree(HT); dfree(G2);
       throw Error(HD_ERR_FACTOR, "block tridiagonal exact solve: singular block (info " + std::to_string(v) + ")");
     }
   X.bt.GT = GT;
@@ -409,10 +409,10 @@ static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int 
     if (cplx) btri_factor<double2>(st, L, q, m, nb, X);
     else btri_factor<double>(st, L, q, m, nb, X);
   } catch (...) {
-    cudaFree(mem);
+    dfree(mem);
     throw;
   }
-  cudaFree(mem);
+  dfree(mem);
   X.bt.n = n;
   X.bt.q = q;
   X.bt.m = m;
@@ -435,9 +435,9 @@ static void destroy_ctx(hd_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   auto fb = [](DevBand& d) {
-    cudaFree(d.S);
-    cudaFree(d.M);
-    cudaFree(d.gen_mem);
+    dfree(d.S);
+    dfree(d.M);
+    dfree(d.gen_mem);
     delete d.genA;
     delete d.genM;
   };
@@ -445,26 +445,26 @@ static void destroy_ctx(hd_ctx* c) {
   for (size_t l = 1; l < c->lev.size(); ++l) fb(c->lev[l]);
   free_exact(c->coarsest);
   free_exact(c->shift_exact);
-  cudaFree(c->sx_plan);
+  dfree(c->sx_plan);
   free_exact(c->E);
-  for (auto* p : c->mg_b) cudaFree(p);
-  for (auto* p : c->mg_x) cudaFree(p);
-  for (auto* p : c->mg_y) cudaFree(p);
-  for (auto* p : c->mg_r) cudaFree(p);
-  cudaFree(c->ep); cudaFree(c->ep2);
-  cudaFree(c->small_res); cudaFree(c->small_state);
-  cudaFree(c->f); cudaFree(c->rhsp); cudaFree(c->x0); cudaFree(c->x); cudaFree(c->w);
-  cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->t3); cudaFree(c->V);
-  cudaFree(c->H); cudaFree(c->g); cudaFree(c->cs); cudaFree(c->sn); cudaFree(c->y);
-  cudaFree(c->scal); cudaFree(c->dres); cudaFree(c->partials); cudaFree(c->counter);
-  cudaFree(c->mon_partials); cudaFree(c->mon_counter);
-  cudaFree(c->dj);
-  cudaFree(c->lsa_sig); cudaFree(c->lsa_L); cudaFree(c->lsa_ch); cudaFree(c->lsa_cx); cudaFree(c->lsa_partials);
-  cudaFree(c->lsa_counter);
+  for (auto* p : c->mg_b) dfree(p);
+  for (auto* p : c->mg_x) dfree(p);
+  for (auto* p : c->mg_y) dfree(p);
+  for (auto* p : c->mg_r) dfree(p);
+  dfree(c->ep); dfree(c->ep2);
+  dfree(c->small_res); dfree(c->small_state);
+  dfree(c->f); dfree(c->rhsp); dfree(c->x0); dfree(c->x); dfree(c->w);
+  dfree(c->t1); dfree(c->t2); dfree(c->t3); dfree(c->V);
+  dfree(c->H); dfree(c->g); dfree(c->cs); dfree(c->sn); dfree(c->y);
+  dfree(c->scal); dfree(c->dres); dfree(c->partials); dfree(c->counter);
+  dfree(c->mon_partials); dfree(c->mon_counter);
+  dfree(c->dj);
+  dfree(c->lsa_sig); dfree(c->lsa_L); dfree(c->lsa_ch); dfree(c->lsa_cx); dfree(c->lsa_partials);
+  dfree(c->lsa_counter);
   if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
   if (c->pre_exec) cudaGraphExecDestroy(c->pre_exec);
   if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
-  cudaFree(c->loop_state); cudaFree(c->res_hist); cudaFree(c->cublas_ws);
+  dfree(c->loop_state); dfree(c->res_hist); dfree(c->cublas_ws);
   if (c->loop_host) cudaFreeHost(c->loop_host);
   if (c->res_host) cudaFreeHost(c->res_host);
   if (c->hres) cudaFreeHost(c->hres);
@@ -658,9 +658,16 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
       CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
       c->E = make_dense(c->st, galerkin_gen(fineH, z), cmk(-c->cA.x, -c->cA.y), nsm);
     } else if (c->dim == 2) {
-      const bool fold = (c->nc % 2 == 0) && centro_symmetric(ES) && centro_symmetric(EM) &&
-                        !std::getenv("HD_NOFOLD");
-      if (fold) c->E = make_fd_folded(c->st, ES, EM, c->cA);
+      // exact E solver (HD_ESOLVE=fd|pfd|fold overrides the choice):
+      //   fd   full fast diagonalisation, 4 GEMMs (the oracle's own method)
+      //   pfd  partial diagonalisation, 2 GEMMs + per-mode banded LU (pfd.cuh)
+      //   fold reflection-folded FD -- only where E is exactly centro-symmetric
+      const char* es = std::getenv("HD_ESOLVE");
+      const std::string esel = es ? es : "";
+      const int eb = std::max(ES.b, EM.b);
+      const bool exact_centro = (c->nc % 2 == 0) && centro_symmetric(ES) && centro_symmetric(EM);
+      if (esel == "fold" || (esel.empty() && exact_centro)) c->E = make_fd_folded(c->st, ES, EM, c->cA);
+      else if (esel == "pfd" || (esel.empty() && c->nc >= kPfdMinN && eb <= 4)) c->E = make_pfd(c->st, ES, EM, c->cA.x);
       else c->E = make_fd(c->st, ES, EM, c->cA);
     } else {
       // corner term of A restricted: Z^T (corner e_n e_n^T) Z

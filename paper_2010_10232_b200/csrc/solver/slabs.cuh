@@ -751,7 +751,7 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
   const SlabLevel& G = sl->lv[0];
   if (sl->maxit < maxit) {
     ++c->buf_epoch;
-    for (auto* p : sl->V) cudaFree(p);
+    for (auto* p : sl->V) dfree(p);
     for (int s : sl->mine) sl->V[s] = dalloc<double2>(static_cast<size_t>(maxit + 1) * own(G, s) * G.n);
     sl->maxit = maxit;
   }
@@ -964,7 +964,7 @@ static void create_slabs(hd_ctx* c, int S, int rank = 0, int nranks = 1, ncclCom
   {
     const ExactSolver& X = c->E;
     const char* de = std::getenv("HD_DIST_E");
-    sl->dist_e = c->spec.deflate && X.dim == 2 && X.V && !X.folded && !X.dense && !X.btri &&
+    sl->dist_e = c->spec.deflate && X.dim == 2 && X.V && !X.folded && !X.pfd && !X.dense && !X.btri &&
                  !(de && std::atoi(de) == 0);
     if (sl->dist_e) {
       const int nc = c->nc;
@@ -995,27 +995,27 @@ static void destroy_slabs(hd_ctx* c) {
   hd_slabs* sl = slabs_of(c);
   if (!sl) return;
   auto fr = [](std::vector<double2*>& v) {
-    for (auto* p : v) cudaFree(p);
+    for (auto* p : v) dfree(p);
   };
   for (auto& v : sl->X) fr(v);
   for (auto& v : sl->Y) fr(v);
   for (auto& v : sl->B) fr(v);
   for (auto& v : sl->R) fr(v);
   for (auto* v : {&sl->f, &sl->w, &sl->t1, &sl->t2, &sl->t3, &sl->x, &sl->x0, &sl->rhsp, &sl->vin, &sl->V}) fr(*v);
-  cudaFree(sl->slots);
-  cudaFree(sl->parts);
-  cudaFree(sl->red);
+  dfree(sl->slots);
+  dfree(sl->parts);
+  dfree(sl->red);
   if (sl->vranks || sl->nranks > 1)
     for (int s : sl->mine) {
-      cudaFree(sl->eT1[s]);
-      cudaFree(sl->eT2[s]);
+      dfree(sl->eT1[s]);
+      dfree(sl->eT2[s]);
     }
   for (int s : sl->mine) {
-    if (!sl->esend.empty()) cudaFree(sl->esend[s]);
-    if (!sl->erecv.empty()) cudaFree(sl->erecv[s]);
+    if (!sl->esend.empty()) dfree(sl->esend[s]);
+    if (!sl->erecv.empty()) dfree(sl->erecv[s]);
   }
   if (sl->body) cudaGraphExecDestroy(sl->body);
-  cudaFree(sl->dj);
+  dfree(sl->dj);
   if (sl->hj) cudaFreeHost(sl->hj);
   if (sl->comm) nccl().CommDestroy(sl->comm);
   delete sl;

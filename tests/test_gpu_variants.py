@@ -13,6 +13,8 @@ move results beyond rounding:
 Each pair is also tied to the oracle by tests/test_gpu_parity.py (the default
 paths) -- these tests bound the distance between the two device paths.
 """
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -90,17 +92,69 @@ def test_two_level_scan_matches_sequential_scan(monkeypatch, ne, p, k):
     _same_solve(ra, rb, 1e-9)
 
 
-def test_folded_E_at_C5_matches_unfolded(monkeypatch):
-    """C5's E factors are centro-symmetric to ~3e-13 relative, inside the 1e-12
-    tolerance: the folded solve applies the inverse of the symmetrised E.  Its
-    distance to the unfolded fast diagonalisation is held to 1e-8 per deflation
-    application (the solution bar); measured 9e-12 on B200, below the unfolded
-    FD's own distance to SuperLU at cond(E) ~ 5e5."""
-    s = hd.assemble(hd.point_source_2d(1600, 3, 1000.0))
-    a, b = _pair(monkeypatch, "HD_NOFOLD", s, hd.to_spec("DC_MG", 3, 1000.0, **BASE))
-    with a, b:
-        for seed in (13, 14):
-            x = _rand(s.size, seed)
-            d = _rel(_apply(a, hd.HD_APPLY_Q, x), _apply(b, hd.HD_APPLY_Q, x))
-            print(f"folded vs unfolded Q at C5: {d:.2e}")
-            assert d <= 1e-8
+def _pair_env(monkeypatch, var, va, vb, s, spec):
+    """(solver created with var=va, solver created with var=vb)"""
+    monkeypatch.setenv(var, va)
+    a = hd.Solver(s, spec)
+    monkeypatch.setenv(var, vb)
+    b = hd.Solver(s, spec)
+    monkeypatch.delenv(var, raising=False)
+    return a, b
+
+
+@pytest.mark.parametrize("ne,p,k", [(200, 2, 100.0), (161, 3, 90.0), (120, 4, 60.0), (101, 5, 50.0)])
+def test_partial_diagonalisation_E_matches_oracle(monkeypatch, ne, p, k):
+    """The partially diagonalised E solve (pfd.cuh: V^T, per-mode banded LU with
+    partial pivoting along y, V) is an exact direct method: the deflation
+    operators Q and P agree with the oracle's SuperLU of E (the reference's
+    kind of solver, src/precond.cpp:95-104) to the bars of
+    tests/test_gpu_parity.py, for E half-bandwidths 3 and 4 and odd and even
+    coarse sizes."""
+    from oracle import helmdef_oracle as O
+    so = O.assemble(O.point_source_2d(ne, p, k))
+    st = O.compose(so, O.to_spec("DC_MG", p, k, **BASE), galerkin="kron", e_solver="splu")
+    s = hd.assemble(hd.point_source_2d(ne, p, k))
+    monkeypatch.setenv("HD_ESOLVE", "pfd")
+    solver = hd.Solver(s, hd.to_spec("DC_MG", p, k, **BASE))
+    monkeypatch.delenv("HD_ESOLVE", raising=False)
+    with solver:
+        x = _rand(s.size, 21)
+        assert _rel(_apply(solver, hd.HD_APPLY_Q, x), st.deflation.apply_Q(x)) <= 1e-10
+        assert _rel(_apply(solver, hd.HD_APPLY_PROJECT, x), st.deflation.project(x)) <= 1e-10
+        r = solver.solve(hd.GmresOptions(100, 1e-7))
+    g = O.gmres(st.op, st.rhs, st.start, st.monitor, O.GmresOptions(100, 1e-7))
+    assert r.converged and abs(r.iterations - g.iterations) <= 1
+    assert _rel(r.solution, g.solution) <= 1e-8
+
+
+def test_E_solvers_at_C5_agree():
+    """C5's three exact E solvers on the device -- full fast diagonalisation
+    (HD_ESOLVE=fd), partial diagonalisation + banded LU (pfd, the default at
+    this size) -- and the reflection-folded FD, which at C5 solves the
+    symmetrised E' (||E - E'|| ~ 3e-13 ||E||, hence no longer the default):
+    per deflation application Q, within the solution bar of each other."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, torch, paper_2010_10232_b200 as hd\n"
+            "s = hd.assemble(hd.point_source_2d(1600, 3, 1000.0))\n"
+            "sp = hd.to_spec('DC_MG', 3, 1000.0, beta2='0.5', cycles=1, smoothing=1, omega=2.0/3.0)\n"
+            "rng = np.random.default_rng(13)\n"
+            "x = rng.uniform(-1, 1, s.size) + 1j * rng.uniform(-1, 1, s.size)\n"
+            "with hd.Solver(s, sp) as solver:\n"
+            "    xd = torch.from_numpy(x).cuda(); yd = torch.zeros_like(xd)\n"
+            "    solver.apply(hd.HD_APPLY_Q, xd.data_ptr(), yd.data_ptr()); torch.cuda.synchronize()\n"
+            "    np.save(__import__('sys').argv[1], yd.cpu().numpy())\n")
+    import os
+    import tempfile
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        for mode in ("fd", "pfd", "fold"):
+            env = dict(os.environ, HD_ESOLVE=mode)
+            f = os.path.join(d, mode + ".npy")
+            r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True,
+                               cwd=str(Path(__file__).resolve().parents[1]), timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            out[mode] = np.load(f)
+    d_pfd, d_fold = _rel(out["pfd"], out["fd"]), _rel(out["fold"], out["fd"])
+    print(f"C5 Q: pfd vs fd {d_pfd:.2e}, fold vs fd {d_fold:.2e}")
+    assert d_pfd <= 1e-8 and d_fold <= 1e-8
