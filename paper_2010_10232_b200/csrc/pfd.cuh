@@ -11,8 +11,8 @@
 // (its rounding is held to the exact-solver envelope, tests/golden/
 // make_e_envelope.py).
 //
-// k_pfd_ysolve: one warp per group of kPG = 8 modes, lane = (mode, plane):
-// the re and im planes are independent real recurrences.  Each lane runs the
+// k_pfd_ysolve: one warp per group of kPG = 8 modes, one lane per mode running
+// the re and im planes as two interleaved real recurrences.  Each lane runs the
 // forward sweep (row interchanges + unit-L elimination, window of KL+1
 // partially eliminated right-hand-side rows in registers), writing y in place,
 // then the backward sweep (U with 2KL superdiagonals, window of the last 2KL
@@ -59,8 +59,8 @@ __device__ __forceinline__ void pfd_wait() {
 template <int KL>
 __global__ void __launch_bounds__(32) k_pfd_ysolve(PfdArgs a) {
   constexpr int KU = 2 * KL;
-  constexpr int FW = (KL + 1) * kPG;      // forward table doubles per row
-  constexpr int BW = (KU + 1) * kPG;      // backward table doubles per row
+  constexpr int FW = (KL + 1) * kPG;        // forward table doubles per row
+  constexpr int BW = (KU + 1) * kPG;        // backward table doubles per row
   constexpr int SF = kPR * (FW + 2 * kPG);  // doubles per forward stage
   constexpr int SB = kPR * (BW + 2 * kPG);  // doubles per backward stage
   constexpr int SS = SF > SB ? SF : SB;     // slot stride
@@ -68,9 +68,10 @@ __global__ void __launch_bounds__(32) k_pfd_ysolve(PfdArgs a) {
   const int lane = threadIdx.x;
   const int g = blockIdx.x;
   const int n = a.n, np = a.np;
-  const int mm = lane & (kPG - 1), pl = (lane >> 3) & 1;
-  const bool active = lane < 2 * kPG;
-  double* const Tg = a.T + static_cast<size_t>(g) * kPG;  // + (iy + pl n) np
+  const int mm = lane & (kPG - 1);  // this lane's mode; it runs both planes (two independent chains)
+  const bool active = lane < kPG;
+  double* const Tg = a.T + static_cast<size_t>(g) * kPG;  // + (iy + plane n) np
+  const size_t pstride = static_cast<size_t>(n) * np;     // plane offset in T
   const int nst = (n + kPR - 1) / kPR;
 
   // ---------------- forward: rows 0 .. n-1 ----------------
@@ -90,43 +91,68 @@ __global__ void __launch_bounds__(32) k_pfd_ysolve(PfdArgs a) {
     }
     pfd_commit();
   };
-  auto t_at = [&](int q) -> double {  // right-hand side row q of this lane (0 past the end)
+  auto t_at = [&](int q, int p) -> double {  // right-hand side row q, plane p (0 past the end)
     if (q >= n) return 0.0;
     const double* slot = pfd_sm + static_cast<size_t>((q / kPR) % kPD) * SS;
-    return slot[kPR * FW + ((q % kPR) * 2 + pl) * kPG + mm];
+    return slot[kPR * FW + ((q % kPR) * 2 + p) * kPG + mm];
   };
 #pragma unroll 1
   for (int s = 0; s < kPD; ++s) issue_f(s);
   pfd_wait<kPD - 2>();
   __syncwarp();
-  double w[KL + 1];
+  double w0[KL + 1], w1[KL + 1];  // window rows k .. k+KL of both planes
 #pragma unroll
-  for (int r = 0; r <= KL; ++r) w[r] = active ? t_at(r) : 0.0;
+  for (int r = 0; r <= KL; ++r) {
+    w0[r] = active ? t_at(r, 0) : 0.0;
+    w1[r] = active ? t_at(r, 1) : 0.0;
+  }
 #pragma unroll 1
   for (int s = 0; s < nst; ++s) {
     const double* slot = pfd_sm + static_cast<size_t>(s % kPD) * SS;
     const int r0 = s * kPR;
+    // the stage's coefficients and the refill rows into registers first, so the
+    // recurrence below is a chain of register selects and FMAs only
+    double lf[kPR][KL];
+    int pv[kPR];
+    double tn0[kPR], tn1[kPR];
+#pragma unroll
+    for (int rr = 0; rr < kPR; ++rr) {
+      const double* fr = slot + rr * FW;
+#pragma unroll
+      for (int q = 0; q < KL; ++q) lf[rr][q] = fr[q * kPG + mm];
+      pv[rr] = static_cast<int>(fr[KL * kPG + mm]);
+      tn0[rr] = t_at(r0 + rr + KL + 1, 0);
+      tn1[rr] = t_at(r0 + rr + KL + 1, 1);
+    }
 #pragma unroll
     for (int rr = 0; rr < kPR; ++rr) {
       const int k = r0 + rr;
       if (k < n && active) {
-        const double* fr = slot + rr * FW;
-        const int p = static_cast<int>(fr[KL * kPG + mm]);
+        const int p = pv[rr];
         // row interchange k <-> k + p inside the window
-        double wk = w[0];
+        double y0 = w0[0], y1 = w1[0];
 #pragma unroll
         for (int r = 1; r <= KL; ++r)
           if (p == r) {
-            wk = w[r];
-            w[r] = w[0];
+            y0 = w0[r];
+            w0[r] = w0[0];
+            y1 = w1[r];
+            w1[r] = w1[0];
           }
-        const double y = wk;
 #pragma unroll
-        for (int r = 1; r <= KL; ++r) w[r] = fma(-fr[(r - 1) * kPG + mm], y, w[r]);
-        Tg[static_cast<size_t>(k + pl * n) * np + mm] = y;
+        for (int r = 1; r <= KL; ++r) {
+          w0[r] = fma(-lf[rr][r - 1], y0, w0[r]);
+          w1[r] = fma(-lf[rr][r - 1], y1, w1[r]);
+        }
+        Tg[static_cast<size_t>(k) * np + mm] = y0;
+        Tg[pstride + static_cast<size_t>(k) * np + mm] = y1;
 #pragma unroll
-        for (int r = 0; r < KL; ++r) w[r] = w[r + 1];
-        w[KL] = t_at(k + KL + 1);
+        for (int r = 0; r < KL; ++r) {
+          w0[r] = w0[r + 1];
+          w1[r] = w1[r + 1];
+        }
+        w0[KL] = tn0[rr];
+        w1[KL] = tn1[rr];
       }
     }
     __syncwarp();
@@ -158,9 +184,9 @@ __global__ void __launch_bounds__(32) k_pfd_ysolve(PfdArgs a) {
   };
 #pragma unroll 1
   for (int s = 0; s < kPD; ++s) issue_b(s);
-  double xw[KU];  // x_{k+1} .. x_{k+KU}
+  double xa[KU], xb[KU];  // x_{k+1} .. x_{k+KU} of both planes
 #pragma unroll
-  for (int d = 0; d < KU; ++d) xw[d] = 0.0;
+  for (int d = 0; d < KU; ++d) xa[d] = xb[d] = 0.0;
 #pragma unroll 1
   for (int s = 0; s < nst; ++s) {
     pfd_wait<kPD - 1>();
@@ -173,14 +199,27 @@ __global__ void __launch_bounds__(32) k_pfd_ysolve(PfdArgs a) {
       if (k >= klo && active) {
         const int r = k - klo;
         const double* br = slot + r * BW;
-        double acc = slot[kPR * BW + (r * 2 + pl) * kPG + mm];
+        double u[KU + 1];
 #pragma unroll
-        for (int d = KU; d >= 1; --d) acc = fma(-br[d * kPG + mm], xw[d - 1], acc);
-        const double x = acc * br[mm];
-        Tg[static_cast<size_t>(k + pl * n) * np + mm] = x;
+        for (int d = 0; d <= KU; ++d) u[d] = br[d * kPG + mm];
+        double acc0 = slot[kPR * BW + (r * 2) * kPG + mm];
+        double acc1 = slot[kPR * BW + (r * 2 + 1) * kPG + mm];
+        // the far taps first: only the last FMA waits for x_{k+1}
 #pragma unroll
-        for (int d = KU - 1; d >= 1; --d) xw[d] = xw[d - 1];
-        xw[0] = x;
+        for (int d = KU; d >= 1; --d) {
+          acc0 = fma(-u[d], xa[d - 1], acc0);
+          acc1 = fma(-u[d], xb[d - 1], acc1);
+        }
+        const double x0 = acc0 * u[0], x1 = acc1 * u[0];
+        Tg[static_cast<size_t>(k) * np + mm] = x0;
+        Tg[pstride + static_cast<size_t>(k) * np + mm] = x1;
+#pragma unroll
+        for (int d = KU - 1; d >= 1; --d) {
+          xa[d] = xa[d - 1];
+          xb[d] = xb[d - 1];
+        }
+        xa[0] = x0;
+        xb[0] = x1;
       }
     }
     __syncwarp();

@@ -134,10 +134,6 @@ struct DevBand {
   double* gen_mem = nullptr;
 };
 
-// partial diagonalisation for E from this size on (the 4 GEMMs of the full
-// fast diagonalisation cost 8 n^3 flops per application)
-constexpr int kPfdMinN = 512;
-
 // Exact solver of one Kronecker-sum (2D) or banded (1D) operator.
 struct ExactSolver {
   int dim = 0, n = 0;

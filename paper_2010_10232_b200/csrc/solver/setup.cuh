@@ -658,16 +658,17 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
       CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
       c->E = make_dense(c->st, galerkin_gen(fineH, z), cmk(-c->cA.x, -c->cA.y), nsm);
     } else if (c->dim == 2) {
-      // exact E solver (HD_ESOLVE=fd|pfd|fold overrides the choice):
-      //   fd   full fast diagonalisation, 4 GEMMs (the oracle's own method)
-      //   pfd  partial diagonalisation, 2 GEMMs + per-mode banded LU (pfd.cuh)
-      //   fold reflection-folded FD -- only where E is exactly centro-symmetric
+      // exact E solver (HD_ESOLVE=fd|pfd|fold overrides the default):
+      //   fd   full fast diagonalisation, 4 GEMMs -- the oracle's own method and the
+      //        default: its histories are the closest to the oracle's
+      //   pfd  partial diagonalisation, 2 GEMMs + per-mode banded LU (pfd.cuh), exact
+      //   fold reflection-folded FD: the default only where E is exactly
+      //        centro-symmetric (elsewhere it would solve a symmetrised E')
       const char* es = std::getenv("HD_ESOLVE");
       const std::string esel = es ? es : "";
-      const int eb = std::max(ES.b, EM.b);
       const bool exact_centro = (c->nc % 2 == 0) && centro_symmetric(ES) && centro_symmetric(EM);
       if (esel == "fold" || (esel.empty() && exact_centro)) c->E = make_fd_folded(c->st, ES, EM, c->cA);
-      else if (esel == "pfd" || (esel.empty() && c->nc >= kPfdMinN && eb <= 4)) c->E = make_pfd(c->st, ES, EM, c->cA.x);
+      else if (esel == "pfd") c->E = make_pfd(c->st, ES, EM, c->cA.x);
       else c->E = make_fd(c->st, ES, EM, c->cA);
     } else {
       // corner term of A restricted: Z^T (corner e_n e_n^T) Z

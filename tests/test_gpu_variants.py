@@ -7,8 +7,9 @@ move results beyond rounding:
     k_jacobi0_2d_t launch (HD_NOJ0FUSE=1);
   * the two-level segment scans of the 1D banded solves (k_seg_scan2) vs the
     P-step single-warp scans (HD_SEG_SEQSCAN=1);
-  * the reflection-folded E solve at C5, whose factors are centro-symmetric to
-    3e-13 only, vs the unfolded fast diagonalisation (HD_NOFOLD=1).
+  * the exact E solvers (HD_ESOLVE=fd | pfd) against each other and the
+    oracle, and the reflection-folded E solve at C5 (centro-symmetric to 3e-13
+    only, so a symmetrised E') against them.
 
 Each pair is also tied to the oracle by tests/test_gpu_parity.py (the default
 paths) -- these tests bound the distance between the two device paths.
@@ -128,10 +129,10 @@ def test_partial_diagonalisation_E_matches_oracle(monkeypatch, ne, p, k):
 
 
 def test_E_solvers_at_C5_agree():
-    """C5's three exact E solvers on the device -- full fast diagonalisation
-    (HD_ESOLVE=fd), partial diagonalisation + banded LU (pfd, the default at
-    this size) -- and the reflection-folded FD, which at C5 solves the
-    symmetrised E' (||E - E'|| ~ 3e-13 ||E||, hence no longer the default):
+    """C5's exact E solvers on the device -- full fast diagonalisation
+    (HD_ESOLVE=fd, the default), partial diagonalisation + banded LU (pfd) --
+    and the reflection-folded FD, which at C5 solves the symmetrised E'
+    (||E - E'|| ~ 3e-13 ||E||, hence not the default there):
     per deflation application Q, within the solution bar of each other."""
     import subprocess
     import sys

@@ -217,3 +217,26 @@ def test_fd_coarse_solve_matches_splu():
     v = rvec(s.A.shape[0], 3)
     qa, qb = a.deflation.apply_Q(v), b.deflation.apply_Q(v)
     assert np.linalg.norm(qa - qb) < 1e-10 * np.linalg.norm(qa)
+
+
+def test_c_spmv_bit_identical_to_scipy():
+    """oracle/csr_spmv.c (the oracle's threaded product for the live C5 run) must
+    round exactly like scipy's csr_matvec, for any thread count."""
+    if not O.use_c_spmv(3):
+        pytest.skip("oracle/libcsr_spmv.so not built")
+    try:
+        s = O.assemble(O.point_source_2d(60, 3, 30.0))
+        A = sp.csr_matrix(O.shifted_operator(s, 0.5))
+        A.sort_indices()
+        rng = np.random.default_rng(7)
+        x = rng.uniform(-1, 1, A.shape[0]) + 1j * rng.uniform(-1, 1, A.shape[0])
+        for t in (1, 3, 8):
+            O.use_c_spmv(t)
+            assert np.array_equal(O._mv(A, x), A @ x)
+        B = sp.random(3000, 2000, density=0.01, format="csr", random_state=3).astype(np.complex128)
+        B.data = B.data + 1j * rng.uniform(-1, 1, B.nnz)
+        B.sort_indices()
+        y = rng.uniform(-1, 1, 2000) + 1j * rng.uniform(-1, 1, 2000)
+        assert np.array_equal(O._mv(B, y), B @ y)
+    finally:
+        O._SPMV["lib"] = None
