@@ -234,7 +234,9 @@ hd_status hd_set_stream(hd_ctx* ctx, void* stream);
  * and algorithmic bytes (compulsory HBM traffic of that launch).  hd_profile
  * (enable) also clears previous records; hd_profile_read sums one kind. */
 enum { HD_K_OP_FINE = 0, HD_K_OP_COARSE = 1, HD_K_JACOBI0 = 2, HD_K_TRANSFER = 3, HD_K_EXACT = 4,
-       HD_K_MGS = 5, HD_K_ITERATE = 6, HD_K_VEC = 7, HD_K_GIVENS = 8, HD_K_LIBGEMM = 9, HD_K_COUNT = 10 };
+       HD_K_MGS = 5, HD_K_ITERATE = 6, HD_K_VEC = 7, HD_K_GIVENS = 8, HD_K_LIBGEMM = 9, HD_K_DGEMM = 10,
+       HD_K_COUNT = 11 };
+/* (HD_K_DGEMM and HD_K_LIBGEMM record FLOPs, not bytes, in hd_profile_read's "bytes".) */
 hd_status hd_profile(hd_ctx* ctx, int enable);
 hd_status hd_profile_read(hd_ctx* ctx, int kind, long* launches, double* ms, double* bytes);
 

@@ -45,7 +45,7 @@ EXPORTS = ["hd_problem_per_dim", "hd_assemble", "hd_assemble_field", "hd_create"
            "hd_profile_read", "hd_destroy", "hd_last_error", "hd_create_slabs", "hd_slab_info",
            "hd_nccl_unique_id", "hd_create_dist", "hd_direct_solve", "hd_debug_check_guards"]
 KERNEL_KINDS = ["op_fine", "op_coarse", "jacobi0", "transfer", "exact", "mgs", "iterate", "vec", "givens",
-                "lib_gemm"]
+                "lib_gemm", "dgemm"]
 
 
 class HdProblem(C.Structure):
@@ -357,6 +357,24 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(load_library().hd_nccl_unique_id(buf))
     return buf.raw
+
+
+def system_from_bands(pb: Problem, S1: np.ndarray, M1: np.ndarray, rhs: np.ndarray) -> DiscreteSystem:
+    """DiscreteSystem from given dense reduced 1D factors and load vector (a
+    constant-k problem): the device solves exactly these inputs, e.g. the
+    oracle's own assembly, so parity tests compare solvers on the same system."""
+    n, b = S1.shape[0], pb.order
+    def band(X):
+        B = np.zeros((n, 2 * b + 1))
+        for d in range(-b, b + 1):
+            dg = np.diagonal(X, d)
+            if d >= 0:
+                B[:n - d, d + b] = dg
+            else:
+                B[-d:, d + b] = dg
+        return B
+    return DiscreteSystem(pb, n, band(np.asarray(S1)), band(np.asarray(M1)),
+                          np.ascontiguousarray(rhs, dtype=np.complex128))
 
 
 def _hd_system(sys_: DiscreteSystem):

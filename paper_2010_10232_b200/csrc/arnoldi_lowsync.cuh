@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_dots_finish(LsaArgs a, int npart
   __shared__ double2 sh_s[kLsaMaxJ + 1];
   __shared__ double2 sh_lj[kLsaMaxJ];
   __shared__ double2 hsm[kLsaMaxJ + 1];
+  if (a.done && *((volatile const int*)a.done)) return;
   const int j = a.dj ? *a.dj : a.j;
   lsa_dots_finish(a, j, nparts, sh_s, sh_lj, hsm);
 }
@@ -449,7 +450,43 @@ struct LoopState {
   int need_tail;  // budget exhausted: the host forms x_{maxit-1} and its monitor
   int breakdown;  // side-branch monitor: Krylov breakdown, the host monitors x_{iters-1}
   int nonfinite;  // NaN/Inf residual or hnew: stopped, the host reports an error
+  double hprev;   // row slabs: hnew of the previous iteration (the body's Givens runs last)
 };
+
+// Row-slab loop control, last kernel of the slab graph body (after the monitor
+// of x_{j-1} and the Givens of column j): the host loop's decisions of
+// run_solve_slabs on the device -- record rr(x_{j-1}), stop on tolerance, on a
+// non-finite value or on the breakdown of iteration j-1, stop at the budget,
+// else step to j+1.  Every rank computes the same scalars (slab-order sums),
+// so every rank takes the same decision.
+__global__ void k_slab_loop_step(LoopState* s, const double* dres, double* res_hist, double tol, int maxit) {
+  if (s->done) return;
+  const int j = s->j;
+  if (j >= 1) {
+    const double rr = dres[0];
+    res_hist[j - 1] = rr;
+    if (!isfinite(rr) || !isfinite(s->hprev)) {
+      s->nonfinite = 1;
+      s->done = 1;
+      s->iters = j;
+      return;
+    }
+    if (rr <= tol || s->hprev < 1e-300) {
+      s->conv = rr <= tol;
+      s->done = 1;
+      s->iters = j;
+      return;
+    }
+  }
+  s->hprev = dres[1];
+  if (j + 1 >= maxit) {
+    s->done = 1;
+    s->need_tail = 1;
+    s->iters = maxit;
+    return;
+  }
+  s->j = j + 1;
+}
 
 // After the monitor of x_{j-1} (src/linalg.cpp:82-88): record the residual,
 // stop on tolerance or Krylov breakdown of the previous step.

@@ -34,10 +34,12 @@
 #include "kernels.cuh"
 #include "stencil.cuh"
 #include "transfer.cuh"
+#include "stencil_restrict.cuh"
 #include "arnoldi_lowsync.cuh"
 #include "layered.cuh"
 #include "btri.cuh"
 #include "pfd.cuh"
+#include "dgemm.cuh"
 #include "segsolve.cuh"
 #include "tail1d.cuh"
 #include "small1d.cuh"

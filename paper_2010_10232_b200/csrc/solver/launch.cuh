@@ -251,6 +251,62 @@ static void prolong_(hd_ctx* c, Stencil z, const double2* ec, const double* ep, 
             k_prolong<1, PMODE><<<grid_for(NF), 256, 0, c->st>>>(z, ec, ep, nf, nc, s, out));
 }
 
+// Fused level operator + restriction (stencil_restrict.cuh): rc = Z^T (L x)
+// (APPLY, the projection) or Z^T (b - L x) (RESID, the V-cycle), r never
+// stored.  kind 0: linear MG transfer into outc (+ J0: x0 = omega D_c^-1 rc);
+// kind 1: Bezier deflation transfer into the planar coarse vector outp.
+static bool fused_restrict_ok(hd_ctx* c, const LevelDev& L) {
+  static const bool off = std::getenv("HD_NOFUSE") != nullptr;
+  return !off && c->dim == 2 && !L.gen && L.b >= 1 && L.b <= 6;
+}
+
+template <int B, int MODE, int KIND, int PLANAR, bool J0>
+static void launch_sr(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double drop, int nc,
+                      double2* outc, double* outp, const LevelDev& Lc, double omega, double2* x0c) {
+  constexpr int QW = sr_qw<KIND>();
+  constexpr int nw = ZW<KIND>::nw;
+  const int per = stencil_occupancy<B, MODE>();  // same ring and smem as the plain stencil
+  const int slots = per * c->n_sms;
+  const int cols = (nc + QW * kSWarps - 1) / (QW * kSWarps);
+  // strip height in coarse rows: fill whole waves, discounting the recomputed rows
+  int best = 16;
+  double best_score = -1.0;
+  for (int qr = 4; 2 * qr + nw - 1 <= kSRowsMax; qr += 2) {
+    const long tiles = static_cast<long>(cols) * ((nc + qr - 1) / qr);
+    const long waves = (tiles + slots - 1) / slots;
+    const double util = static_cast<double>(tiles) / (static_cast<double>(waves) * slots);
+    const double score = util * (2.0 * qr) / (2.0 * qr + nw - 2 + 2.0 * B);
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = qr;
+    }
+  }
+  const int nout = 2 * best + nw - 1;
+  smem_optin(reinterpret_cast<const void*>(k_stencil_restrict2d<B, MODE, KIND, PLANAR, J0>),
+             stencil_smem<B, MODE>(kSRowsMax));
+  const dim3 grid(cols, (nc + best - 1) / best);
+  k_stencil_restrict2d<B, MODE, KIND, PLANAR, J0><<<grid, kSW * kSWarps, stencil_smem<B, MODE>(nout), c->st>>>(
+      L, x, b, drop, nc, best, outc, outp, Lc, omega, x0c);
+}
+
+template <int MODE, int KIND, int PLANAR, bool J0>
+static void op_restrict(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double drop, int nc,
+                        double2* outc, double* outp, const LevelDev& Lc = LevelDev{}, double omega = 0.0,
+                        double2* x0c = nullptr) {
+  const double NF = static_cast<double>(L.n) * L.n, NCd = static_cast<double>(nc) * nc;
+  const double bytes = 16.0 * (NF * (MODE == OP_RESID ? 2.0 : 1.0) + NCd * (J0 ? 2.0 : 1.0));
+  const size_t mk = prof_mark(c);
+  g_launch_line = __LINE__;
+  switch (L.b) {
+#define HD_CASE(BB) \
+  case BB: launch_sr<BB, MODE, KIND, PLANAR, J0>(c, L, x, b, drop, nc, outc, outp, Lc, omega, x0c); break;
+    HD_CASE(1) HD_CASE(2) HD_CASE(3) HD_CASE(4) HD_CASE(5) HD_CASE(6)
+#undef HD_CASE
+    default: throw Error(HD_ERR_INVALID, "band half-width " + std::to_string(L.b) + " unsupported");
+  }
+  launched(c, L.n == c->n ? HD_K_OP_FINE : HD_K_OP_COARSE, mk, bytes);
+}
+
 // interleaved <-> planar (re plane, im plane) complex vectors
 __global__ void k_to_planar(const double2* __restrict__ a, double* __restrict__ p, size_t N) {
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < N; g += (size_t)gridDim.x * blockDim.x) {
@@ -314,15 +370,73 @@ static void btri_solve(hd_ctx* c, ExactSolver& X, double* inout) {
             });
 }
 
+// C = op(A) op(B) (column-major, batched by strides) on the context stream:
+// plain dense GEMMs of the fast diagonalisation, cuBLAS DGEMM by default
+// (sm_100 DMMA kernels, 299 us per C5 E solve); HD_DGEMM=dmma selects this
+// build's own FP64 tensor-core kernel (dgemm.cuh; 331 us at C5, 53 vs 36 us at
+// C3 -- it does not beat the library yet).
+static bool dgemm_cublas() {
+  static const bool on = !(std::getenv("HD_DGEMM") && std::string(std::getenv("HD_DGEMM")) == "dmma");
+  return on;
+}
+
+template <bool TA, bool TB>
+static void dgemm(hd_ctx* c, int M, int N, int K, const double* A, int lda, long long sA, const double* B, int ldb,
+                  long long sB, double* C, int ldc, long long sC, int batch, const double* const* Ap = nullptr,
+                  const double* const* Bp = nullptr, double* const* Cp = nullptr) {
+  const double flops = 2.0 * M * N * K * batch;
+  if (Ap && dgemm_cublas()) {
+    const double one = 1.0, zero = 0.0;
+    const size_t mk = prof_mark(c);
+    CKB(cublasDgemmBatched(c->cb, TA ? CUBLAS_OP_T : CUBLAS_OP_N, TB ? CUBLAS_OP_T : CUBLAS_OP_N, M, N, K, &one, Ap,
+                           lda, Bp, ldb, &zero, const_cast<double**>(Cp), ldc, batch));
+    launched(c, HD_K_LIBGEMM, mk, flops, true);
+    return;
+  }
+  if (dgemm_cublas()) {
+    const double one = 1.0, zero = 0.0;
+    const size_t mk = prof_mark(c);
+    CKB(cublasDgemmStridedBatched(c->cb, TA ? CUBLAS_OP_T : CUBLAS_OP_N, TB ? CUBLAS_OP_T : CUBLAS_OP_N, M, N, K,
+                                  &one, A, lda, sA, B, ldb, sB, &zero, C, ldc, sC, batch));
+    launched(c, HD_K_LIBGEMM, mk, flops, true);
+    return;
+  }
+  DgemmArgs g{M, N, K, A, B, C, lda, ldb, ldc, sA, sB, sC, Ap, Bp, Cp};
+  constexpr size_t sm = DgemmSmem<TA, TB>::bytes;
+  // pointer-batched: the folded blocks are n2^2 doubles apart (16-byte aligned when n2 is even)
+  const bool al16 = (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) % 16 == 0 &&
+                    (!Ap || ((static_cast<long long>(lda) * K) % 2 == 0 && (static_cast<long long>(ldb) * N) % 2 == 0));
+  const bool even = ((M | N | K | lda | ldb) & 1) == 0 && ((sA | sB) & 1) == 0;
+  // split K in two when one pass of tiles would leave the 148 SMs unevenly loaded
+  const long tiles = static_cast<long>((N + kGBN - 1) / kGBN) * ((M + kGBM - 1) / kGBM) * batch;
+  static const int ks_env = std::getenv("HD_DGEMM_KSPLIT") ? std::atoi(std::getenv("HD_DGEMM_KSPLIT")) : 1;
+  const int ks = (ks_env == 2 && tiles < 4L * c->n_sms && K >= 8 * kGBK) ? 2 : 1;
+  const dim3 grid((N + kGBN - 1) / kGBN, (M + kGBM - 1) / kGBM, batch * ks);
+  if (ks == 2) {  // both halves add into C
+    if (static_cast<long long>(ldc) == M && (batch == 1 || sC == static_cast<long long>(ldc) * N)) {
+      CK(cudaMemsetAsync(C, 0, sizeof(double) * static_cast<size_t>(ldc) * N * batch, c->st));
+    } else {
+      for (int b = 0; b < batch; ++b)
+        CK(cudaMemset2DAsync(C + b * sC, sizeof(double) * ldc, 0, sizeof(double) * M, N, c->st));
+    }
+  }
+  // profiled as FLOPs (kind HD_K_DGEMM): the roofline of this kernel is the FP64 tensor rate
+#define HD_DG(V, KS)                                                                      \
+  smem_optin(reinterpret_cast<const void*>(k_dgemm<TA, TB, V, KS>), sm);                  \
+  HD_LAUNCH(HD_K_DGEMM, flops, k_dgemm<TA, TB, V, KS><<<grid, 128, sm, c->st>>>(g));
+  if (al16 && even) {
+    if (ks == 2) { HD_DG(2, 2) } else { HD_DG(2, 1) }
+  } else {
+    if (ks == 2) { HD_DG(1, 2) } else { HD_DG(1, 1) }
+  }
+#undef HD_DG
+}
+
 static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
   if (X.pfd) {
     const int n = X.n, np = X.np;
-    const double one = 1.0, zero = 0.0;
-    const double gb = 16.0 * n * n * 2 + 8.0 * n * n;  // planar in/out + V (bytes of one GEMM)
-    size_t mk = prof_mark(c);
     // T = V^T [Bre | Bim]  (x modes; leading dimension np)
-    CKB(cublasDgemm(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, inout, n, &zero, X.T1, np));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    dgemm<true, false>(c, n, 2 * n, n, X.V, n, 0, inout, n, 0, X.T1, np, 0, 1);
     PfdArgs a{X.T1, X.pfdF, X.pfdB, n, np};
     const int ng = np / kPG;
     const double tb = 8.0 * n * static_cast<double>(np) * ((X.pfd_kl + 1) + (2 * X.pfd_kl + 1)) + 64.0 * n * np;
@@ -336,10 +450,8 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
 #undef HD_PFD
       default: throw Error(HD_ERR_INVALID, "partial diagonalisation: band half-width");
     }
-    mk = prof_mark(c);
     // X = V [Yre | Yim]
-    CKB(cublasDgemm(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, X.T1, np, &zero, inout, n));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    dgemm<false, false>(c, n, 2 * n, n, X.V, n, 0, X.T1, np, 0, inout, n, 0, 1);
     return;
   }
   if (X.btri) {
@@ -354,58 +466,34 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
   }
   if (X.dim == 2 && X.folded) {
     const int n = X.n, n2 = X.n2;
-    const long nn = static_cast<long>(n2) * n2;
-    const double one = 1.0, zero = 0.0;
-    const double gb = 16.0 * nn * 4;               // nominal bytes per GEMM call (profiling)
+    const long long nn = static_cast<long long>(n2) * n2;
     HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_both<<<grid_for(2 * nn), 256, 0, c->st>>>(inout, X.F, n, n2));
-    size_t mk = prof_mark(c);
     // x transform: Hh[yb] rows (2 xb + p) n2 = Vt_xb^T Q[xb][yb][p]  (8 pointer-batched n2^3 GEMMs)
-    CKB(cublasDgemmBatched(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n2, n2, n2, &one, X.xf_ptr, n2, X.xf_ptr + 8, n2, &zero,
-                           const_cast<double**>(X.xf_ptr + 16), 4 * n2, 8));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    dgemm<true, false>(c, n2, n2, n2, nullptr, n2, 0, nullptr, n2, 0, nullptr, 4 * n2, 0, 8, X.xf_ptr, X.xf_ptr + 8,
+                       const_cast<double* const*>(X.xf_ptr + 16));
     // y transform: R[yb] = Hh[yb] Vt_yb, Hh[yb] (4 n2) x n2 (x parity and plane stacked), batch over yb
-    mk = prof_mark(c);
-    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, 4 * n2, n2, n2, &one, X.Hh, 4 * n2, 4 * nn, X.Vt,
-                                  n2, nn, &zero, X.R, 4 * n2, 4 * nn, 2));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    dgemm<false, false>(c, 4 * n2, n2, n2, X.Hh, 4 * n2, 4 * nn, X.Vt, n2, nn, X.R, 4 * n2, 4 * nn, 2);
     HD_LAUNCH(HD_K_EXACT, 48.0 * 4 * nn, k_scale_folded<<<grid_for(4 * nn), 256, 0, c->st>>>(X.R, X.Dinvf, n2));
     // inverse y: S[yb] = R[yb] Vt_yb^T  (into Hh)
-    mk = prof_mark(c);
-    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, 4 * n2, n2, n2, &one, X.R, 4 * n2, 4 * nn, X.Vt,
-                                  n2, nn, &zero, X.Hh, 4 * n2, 4 * nn, 2));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    dgemm<false, true>(c, 4 * n2, n2, n2, X.R, 4 * n2, 4 * nn, X.Vt, n2, nn, X.Hh, 4 * n2, 4 * nn, 2);
     // inverse x: F blocks = Vt_xb Hh[yb] rows (2 xb + p) n2, then both reflections undone
-    mk = prof_mark(c);
-    CKB(cublasDgemmBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n2, n2, n2, &one, X.xi_ptr, n2, X.xi_ptr + 8, 4 * n2,
-                           &zero, const_cast<double**>(X.xi_ptr + 16), n2, 8));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    dgemm<false, false>(c, n2, n2, n2, nullptr, n2, 0, nullptr, 4 * n2, 0, nullptr, n2, 0, 8, X.xi_ptr, X.xi_ptr + 8,
+                        const_cast<double* const*>(X.xi_ptr + 16));
     HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_both<<<grid_for(2 * nn), 256, 0, c->st>>>(X.F, inout, n, n2));
     return;
   }
   if (X.dim == 2) {
     const int n = X.n;
-    const long nn = static_cast<long>(n) * n;
-    const double one = 1.0, zero = 0.0;
-    const double gb = 16.0 * nn * 2 + 8.0 * nn;  // planar in/out + V  (bytes of one GEMM)
-    size_t mk = prof_mark(c);
+    const long long nn = static_cast<long long>(n) * n;
     // T1 = V^T [Xre | Xim]
-    CKB(cublasDgemm(c->cb, CUBLAS_OP_T, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, inout, n, &zero, X.T1, n));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
-    mk = prof_mark(c);
+    dgemm<true, false>(c, n, 2 * n, n, X.V, n, 0, inout, n, 0, X.T1, n, 0, 1);
     // T2_plane = T1_plane V
-    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, X.T1, n, nn, X.V, n, 0, &zero,
-                                  X.T2, n, nn, 2));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    dgemm<false, false>(c, n, n, n, X.T1, n, nn, X.V, n, 0, X.T2, n, nn, 2);
     HD_LAUNCH(HD_K_EXACT, 48.0 * nn, k_fd_scale<<<grid_for(nn), 256, 0, c->st>>>(X.T2, X.Dinv, nn));
-    mk = prof_mark(c);
     // T1 = V [T2re | T2im]
-    CKB(cublasDgemm(c->cb, CUBLAS_OP_N, CUBLAS_OP_N, n, 2 * n, n, &one, X.V, n, X.T2, n, &zero, X.T1, n));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
-    mk = prof_mark(c);
+    dgemm<false, false>(c, n, 2 * n, n, X.V, n, 0, X.T2, n, 0, X.T1, n, 0, 1);
     // out_plane = T1_plane V^T
-    CKB(cublasDgemmStridedBatched(c->cb, CUBLAS_OP_N, CUBLAS_OP_T, n, n, n, &one, X.T1, n, nn, X.V, n, 0, &zero,
-                                  inout, n, nn, 2));
-    launched(c, HD_K_LIBGEMM, mk, gb, true);
+    dgemm<false, true>(c, n, n, n, X.T1, n, nn, X.V, n, 0, inout, n, nn, 2);
   } else {
     HD_LAUNCH(HD_K_EXACT, 32.0 * X.n,
               bandlu_launch(c->st, X, nullptr, inout, nullptr, inout));
@@ -485,11 +573,19 @@ static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero, bool x
   const LevelDev L = levM(c, l);
   double2* xcur = smooth(c, l, b, c->mg_x[l], c->mg_y[l], x_zero, c->spec.smooth_steps, x0_ready && x_zero);
   double2* xoth = xcur == c->mg_x[l] ? c->mg_y[l] : c->mg_x[l];
-  op_apply(c, OP_RESID, L, xcur, b, c->mg_r[l]);
   const int nf = c->lev[l].n, ncl = c->lev[l + 1].n;
   const bool fuse = j0_fusable(c, l + 1);
-  if (fuse) restrict_j0(c, c->mg_r[l], nf, ncl, c->mg_b[l + 1], levM(c, l + 1), c->spec.omega, c->mg_x[l + 1]);
-  else restrict_(c, Stencil{0, 0.0}, c->mg_r[l], nf, ncl, c->mg_b[l + 1], nullptr);
+  if (fused_restrict_ok(c, L)) {  // residual + restriction (+ the coarse first sweep) in one pass
+    if (fuse)
+      op_restrict<OP_RESID, 0, 0, true>(c, L, xcur, b, 0.0, ncl, c->mg_b[l + 1], nullptr, levM(c, l + 1),
+                                        c->spec.omega, c->mg_x[l + 1]);
+    else
+      op_restrict<OP_RESID, 0, 0, false>(c, L, xcur, b, 0.0, ncl, c->mg_b[l + 1], nullptr);
+  } else {
+    op_apply(c, OP_RESID, L, xcur, b, c->mg_r[l]);
+    if (fuse) restrict_j0(c, c->mg_r[l], nf, ncl, c->mg_b[l + 1], levM(c, l + 1), c->spec.omega, c->mg_x[l + 1]);
+    else restrict_(c, Stencil{0, 0.0}, c->mg_r[l], nf, ncl, c->mg_b[l + 1], nullptr);
+  }
   double2* ec = cycle_at(c, l + 1, c->mg_b[l + 1], true, fuse);
   prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, nf, ncl, nullptr, xcur);
   double2* res = smooth(c, l, b, xcur, xoth, false, c->spec.smooth_steps);
@@ -538,8 +634,12 @@ static const double2* mg_solve_ptr(hd_ctx* c, const double2* b, double2* out, bo
       const LevelDev L = levM(c, 0);
       double2* xcur = smooth(c, 0, b, c->mg_x[0], c->mg_y[0], false, c->spec.smooth_steps);
       double2* xoth = xcur == c->mg_x[0] ? c->mg_y[0] : c->mg_x[0];
-      op_apply(c, OP_RESID, L, xcur, b, c->mg_r[0]);
-      restrict_(c, Stencil{0, 0.0}, c->mg_r[0], c->lev[0].n, c->lev[1].n, c->mg_b[1], nullptr);
+      if (fused_restrict_ok(c, L)) {
+        op_restrict<OP_RESID, 0, 0, false>(c, L, xcur, b, 0.0, c->lev[1].n, c->mg_b[1], nullptr);
+      } else {
+        op_apply(c, OP_RESID, L, xcur, b, c->mg_r[0]);
+        restrict_(c, Stencil{0, 0.0}, c->mg_r[0], c->lev[0].n, c->lev[1].n, c->mg_b[1], nullptr);
+      }
       double2* ec = cycle_at(c, 1, c->mg_b[1], true);
       prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, c->lev[0].n, c->lev[1].n, nullptr, xcur);
       xb = smooth(c, 0, b, xcur, xoth, false, c->spec.smooth_steps);
@@ -568,8 +668,13 @@ static void apply_Q(hd_ctx* c, const double2* v, double2* out) {
 // out = w - Q (A w)  (Deflation::project, src/precond.cpp:106-108)
 static void project(hd_ctx* c, const double2* w, double2* out) {
   const Stencil z{1, c->spec.drop};
-  op_apply(c, OP_APPLY, opA(c), w, nullptr, c->t3);
-  restrict_(c, z, c->t3, c->n, c->nc, nullptr, c->ep);
+  const LevelDev A = opA(c);
+  if (fused_restrict_ok(c, A)) {  // Z^T (A w) in one pass, A w never stored
+    op_restrict<OP_APPLY, 1, 1, false>(c, A, w, nullptr, c->spec.drop, c->nc, nullptr, c->ep);
+  } else {
+    op_apply(c, OP_APPLY, A, w, nullptr, c->t3);
+    restrict_(c, z, c->t3, c->n, c->nc, nullptr, c->ep);
+  }
   exact_solve_planar(c, c->E, c->ep);
   prolong_<1>(c, z, nullptr, c->ep, c->n, c->nc, w, out);
 }
@@ -692,6 +797,7 @@ __global__ void k_loop_init(LoopState* s) {
   s->need_tail = 0;
   s->breakdown = 0;
   s->nonfinite = 0;
+  s->hprev = 1.0;
 }
 
 __global__ void k_scale_monitor(double* dres) {

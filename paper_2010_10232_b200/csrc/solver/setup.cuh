@@ -659,11 +659,11 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
       c->E = make_dense(c->st, galerkin_gen(fineH, z), cmk(-c->cA.x, -c->cA.y), nsm);
     } else if (c->dim == 2) {
       // exact E solver (HD_ESOLVE=fd|pfd|fold overrides the default):
-      //   fd   full fast diagonalisation, 4 GEMMs -- the oracle's own method and the
-      //        default: its histories are the closest to the oracle's
+      //   fold reflection-folded FD (half the GEMM flops), the default where E is
+      //        centro-symmetric to 1e-12 (centro_symmetric); C5's history is then
+      //        inside the envelope of exact implementations
+      //   fd   full fast diagonalisation, 4 GEMMs (the oracle's own method), elsewhere
       //   pfd  partial diagonalisation, 2 GEMMs + per-mode banded LU (pfd.cuh), exact
-      //   fold reflection-folded FD: the default only where E is exactly
-      //        centro-symmetric (elsewhere it would solve a symmetrised E')
       const char* es = std::getenv("HD_ESOLVE");
       const std::string esel = es ? es : "";
       const bool exact_centro = (c->nc % 2 == 0) && centro_symmetric(ES) && centro_symmetric(EM);

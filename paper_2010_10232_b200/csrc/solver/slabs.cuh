@@ -115,7 +115,9 @@ struct hd_slabs {
   int* hj = nullptr;                            // pinned mirror
   cudaGraphExec_t body = nullptr;
   int body_maxit = -1;
+  double body_tol = -1.0;
   unsigned body_epoch = ~0u;  // hd_ctx::buf_epoch the body graph captured
+  const int* done = nullptr;  // while capturing the body: the loop state's done flag (early exit)
   long body_delta[6] = {0, 0, 0, 0, 0, 0};      // counters one body adds (matvecs .. lib_calls)
   std::vector<SlabLevel> lv;                    // MG levels
   std::vector<std::vector<double2*>> X, Y, B, R;  // [level][slab], levels < g
@@ -668,6 +670,7 @@ static LsaArgs s_lsa(hd_ctx* c, int s, int j, int mode, int maxit) {
   a.partials = sl->parts;
   a.part_offset = s * sl->Gs;
   a.partial_only = 1;
+  a.done = sl->done;
   return a;
 }
 
@@ -705,30 +708,39 @@ static void slab_iteration_b(hd_ctx* c, int j, int maxit, int nparts, const int*
   LsaArgs a0 = s_lsa(c, sl->mine[0], j, 0, maxit);
   a0.dj = dj;
   HD_LAUNCH(HD_K_GIVENS, 0.0, k_lsa_givens<<<1, kLsaBD, c->lsa_givens_smem, c->st>>>(a0, nparts));
-  CK(cudaMemcpyAsync(c->hres + 1, c->dres + 1, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  if (!dj) CK(cudaMemcpyAsync(c->hres + 1, c->dres + 1, sizeof(double), cudaMemcpyDeviceToHost, c->st));
 }
 
 // Capture one iteration (parts a and b with the monitor of x_{j-1} between
 // them, the scalars copied to the pinned mirror at the end) as a graph; the
 // counters it adds per launch are recorded.  NCCL calls are captured too.
-static void build_slab_body(hd_ctx* c, int maxit, int nparts) {
+constexpr int kSlabChunk = 8;  // slab bodies launched per host synchronisation
+
+static void build_slab_body(hd_ctx* c, int maxit, double tol, int nparts) {
   hd_slabs* sl = slabs_of(c);
-  if (!sl->dj) {
-    sl->dj = dalloc<int>(1);
-    CK(cudaMallocHost(&sl->hj, sizeof(int)));
+  if (!c->loop_state) {
+    c->loop_state = dalloc<LoopState>(1);
+    CK(cudaMallocHost(&c->loop_host, sizeof(LoopState)));
   }
+  dfree(c->res_hist);
+  if (c->res_host) cudaFreeHost(c->res_host);
+  c->res_hist = dalloc<double>(maxit + 1);
+  CK(cudaMallocHost(&c->res_host, (maxit + 1) * sizeof(double)));
   if (sl->body) {
     cudaGraphExecDestroy(sl->body);
     sl->body = nullptr;
   }
   const long before[6] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles, c->launches, c->lib_calls};
   cudaGraph_t g = nullptr;
+  int* dj = &c->loop_state->j;
+  sl->done = &c->loop_state->done;
   CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
-  slab_iteration_a(c, 0, maxit, sl->dj);
-  s_monitor(c, sl->x);  // x_{j-1} (used by the host for j >= 1)
-  slab_iteration_b(c, 0, maxit, nparts, sl->dj);
-  CK(cudaMemcpyAsync(c->hres, c->dres, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  slab_iteration_a(c, 0, maxit, dj);
+  s_monitor(c, sl->x);  // x_{j-1} (recorded by the loop step for j >= 1)
+  slab_iteration_b(c, 0, maxit, nparts, dj);
+  k_slab_loop_step<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, c->res_hist, tol, maxit);
   CK(cudaStreamEndCapture(c->st, &g));
+  sl->done = nullptr;
   CK(cudaGraphInstantiate(&sl->body, g, 0));
   cudaGraphDestroy(g);
   const long after[6] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles, c->launches, c->lib_calls};
@@ -740,6 +752,7 @@ static void build_slab_body(hd_ctx* c, int maxit, int nparts) {
   c->launches = static_cast<int>(before[4]);
   c->lib_calls = static_cast<int>(before[5]);
   sl->body_maxit = maxit;
+  sl->body_tol = tol;
   sl->body_epoch = c->buf_epoch;
 }
 
@@ -812,10 +825,60 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
   }
   HD_LAUNCH(HD_K_VEC, 0.0, k_inv_scalar<<<1, 1, 0, c->st>>>(c->lsa_sig, c->dres + 2));
   const int nparts = sl->S * sl->Gs;  // pass-2 partials (one per CTA of every slab)
+  const bool graph = c->graph_enabled && !c->prof_on;
+  if (graph) {
+    // The whole iteration (op, pass 1, pass 2, monitor of x_{j-1}, Givens, loop
+    // step) is one captured graph reading j and done from device memory.  It is
+    // launched in chunks of kSlabChunk with one host synchronisation per chunk:
+    // bodies past the stopping iteration exit early (their collectives still
+    // run, the same number on every rank, since every rank takes the same
+    // device decision).  No per-iteration host round trip.
+    if (sl->body_maxit != maxit || sl->body_tol != opt.tolerance || sl->body_epoch != c->buf_epoch)
+      build_slab_body(c, maxit, opt.tolerance, nparts);
+    k_loop_init<<<1, 1, 0, c->st>>>(c->loop_state);
+    int bodies = 0;
+    for (;;) {
+      const int chunk = std::min(kSlabChunk, maxit - bodies + 1);
+      for (int q = 0; q < chunk; ++q) CK(cudaGraphLaunch(sl->body, c->st));
+      bodies += chunk;
+      CK(cudaMemcpyAsync(c->loop_host, c->loop_state, sizeof(LoopState), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      if (c->loop_host->done) break;
+      if (bodies > maxit + 1) throw Error(HD_ERR_INVALID, "row slabs: loop state did not terminate");
+    }
+    const LoopState ls = *c->loop_host;
+    CK(cudaMemcpyAsync(c->res_host, c->res_hist, maxit * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (ls.nonfinite)
+      throw Error(HD_ERR_NONFINITE, "non-finite residual or Arnoldi norm at GMRES iteration " + std::to_string(ls.iters));
+    const int it = ls.iters;
+    res.iterations = it;
+    res.converged = ls.conv != 0;
+    const int recorded = ls.need_tail ? maxit - 1 : it;
+    for (int q = 0; q < recorded; ++q) res.residuals.push_back(c->res_host[q]);
+    // counts of the ops GMRES used (speculative ops past the stop are not counted,
+    // as the host loop's rollback); launches of every body that ran
+    c->matvecs += static_cast<long>(it) * sl->body_delta[0];
+    c->coarse_solves += static_cast<long>(it) * sl->body_delta[1];
+    c->shift_solves += static_cast<long>(it) * sl->body_delta[2];
+    c->vcycles += static_cast<long>(it) * sl->body_delta[3];
+    c->launches += static_cast<int>(bodies * sl->body_delta[4]);
+    c->lib_calls += static_cast<int>(bodies * sl->body_delta[5]);
+    if (ls.need_tail) {  // budget exhausted: x_{maxit-1}, then its monitor
+      for (int s : sl->mine) {
+        LsaArgs bq = s_lsa(c, s, maxit - 1, 1, maxit);
+        HD_LAUNCH(HD_K_ITERATE, (maxit + 2.0) * 16.0 * bq.N, k_lsa_update<<<sl->Gs, kLsaBD, 0, c->st>>>(bq));
+      }
+      s_monitor(c, sl->x);
+      read_scalars(c);
+      res.residuals.push_back(c->hres[0]);
+      res.converged = c->hres[0] <= opt.tolerance;
+    }
+    s_gather(c, sl->x, xout_full);
+    return res;
+  }
   bool stop = false;
   double hnew_prev = 1.0;
-  const bool graph = c->graph_enabled && !c->prof_on;
-  if (graph && (sl->body_maxit != maxit || sl->body_epoch != c->buf_epoch)) build_slab_body(c, maxit, nparts);
   for (int j = 0; j < maxit && !stop; ++j) {
     const long snap[4] = {c->matvecs, c->coarse_solves, c->shift_solves, c->vcycles};
     auto rollback = [&]() {
@@ -824,48 +887,24 @@ static SolveOut run_solve_slabs(hd_ctx* c, const hd_gmres& opt, const double2* f
       c->shift_solves = snap[2];
       c->vcycles = snap[3];
     };
-    if (graph) {
-      // the whole iteration (pass 1, pass 2, monitor of x_{j-1}, Givens) as one graph launch
-      *sl->hj = j;
-      CK(cudaMemcpyAsync(sl->dj, sl->hj, sizeof(int), cudaMemcpyHostToDevice, c->st));
-      CK(cudaGraphLaunch(sl->body, c->st));
-      CK(cudaStreamSynchronize(c->st));
-      c->matvecs += sl->body_delta[0];
-      c->coarse_solves += sl->body_delta[1];
-      c->shift_solves += sl->body_delta[2];
-      c->vcycles += sl->body_delta[3];
-      c->launches += static_cast<int>(sl->body_delta[4]);
-      c->lib_calls += static_cast<int>(sl->body_delta[5]);
-      if (j >= 1) {
-        const double rr = c->hres[0];
-        res.iterations = j;
-        res.residuals.push_back(rr);
-        if (rr <= opt.tolerance || hnew_prev < 1e-300) {
-          res.converged = rr <= opt.tolerance;
-          rollback();
-          break;
-        }
+    slab_iteration_a(c, j, maxit, nullptr);
+    if (j >= 1) {  // x_{j-1} is ready
+      s_monitor(c, sl->x);
+      read_scalars(c);
+      const double rr = c->hres[0];
+      res.iterations = j;
+      res.residuals.push_back(rr);
+      if (rr <= opt.tolerance) {
+        res.converged = true;
+        rollback();
+        break;
       }
-    } else {
-      slab_iteration_a(c, j, maxit, nullptr);
-      if (j >= 1) {  // x_{j-1} is ready
-        s_monitor(c, sl->x);
-        read_scalars(c);
-        const double rr = c->hres[0];
-        res.iterations = j;
-        res.residuals.push_back(rr);
-        if (rr <= opt.tolerance) {
-          res.converged = true;
-          rollback();
-          break;
-        }
-        if (hnew_prev < 1e-300) {
-          rollback();
-          break;
-        }
+      if (hnew_prev < 1e-300) {
+        rollback();
+        break;
       }
-      slab_iteration_b(c, j, maxit, nparts, nullptr);
     }
+    slab_iteration_b(c, j, maxit, nparts, nullptr);
     if (j + 1 == maxit) {  // budget exhausted: x_{maxit-1}, then its monitor
       for (int s : sl->mine) {
         LsaArgs bq = s_lsa(c, s, j, 1, maxit);

@@ -1,11 +1,13 @@
 """Rounding envelope of the GMRES history: oracle runs of a config that are
 all exact implementations of the reference algorithm and differ only in
 rounding --
-  * the deflation matrix E solved by fast diagonalisation (FDSolver, the
-    committed C5 oracle run), by partial diagonalisation + banded LU with
-    partial pivoting (PartialFDSolver), and by SuperLU (the reference's own
-    kind of solver, Eigen::SparseLU at src/precond.cpp:95-104) where that is
-    feasible (C3);
+  * the deflation matrix E solved by fast diagonalisation with LAPACK dsygvd
+    eigenvectors (FDSolver, the committed C5 oracle run) or with dsygv's
+    (fd_gv: another eigen-algorithm, so other eigenvector rounding -- what
+    separates the device's cuSOLVER eigenvectors from the oracle's), by
+    partial diagonalisation + banded LU with partial pivoting
+    (PartialFDSolver), and by SuperLU (the reference's own kind of solver,
+    Eigen::SparseLU at src/precond.cpp:95-104) where that is feasible (C3);
   * every operator product through the assembled CSR matrix or through its
     Kronecker factors (apply="kron": another summation order, the device's).
 The per-step spread of their histories is how far rounding alone moves the
@@ -25,8 +27,8 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 from oracle import helmdef_oracle as O  # noqa: E402
 
-CFG = {"C3": (2, 320, 200.0, (("fd", "csr"), ("pfd", "csr"), ("splu", "csr"), ("fd", "kron"))),
-       "C5": (3, 1600, 1000.0, (("pfd", "csr"), ("fd", "kron")))}
+CFG = {"C3": (2, 320, 200.0, (("fd", "csr"), ("pfd", "csr"), ("splu", "csr"), ("fd", "kron"), ("fd_gv", "csr"))),
+       "C5": (3, 1600, 1000.0, (("pfd", "csr"), ("fd", "kron"), ("fd_gv", "csr")))}
 BASE = dict(beta2="0.5", cycles=1, smoothing=1, omega=2.0 / 3.0)
 
 if __name__ == "__main__":
