@@ -60,10 +60,15 @@ __host__ __device__ constexpr size_t gen_smem(int b, int G) {
   return sizeof(double2) * ((size_t)(kGenTY + 2 * b) * (kGenTX + 2 * b) + (size_t)G * (kGenTY + 2 * b) * kGenTX);
 }
 
+// Output rows [rb, re) (a row slab; the whole grid: 0, n), addressed with
+// global rows: a slab's pointers are shifted by its origin and its b halo rows
+// above and below hold the neighbours' rows, so loads stay inside
+// [rb - b, re + b).
 template <int MODE>
 __global__ void __launch_bounds__(kGenThreads) k_kron2d(GenLevel L, const double2* __restrict__ x,
                                                         const double2* __restrict__ bv, double2* __restrict__ out,
-                                                        double omega, RedOut red, const int* xidx, size_t xstride) {
+                                                        double omega, RedOut red, const int* xidx, size_t xstride,
+                                                        int rb, int re) {
   if (xidx) x += (size_t)(*xidx) * xstride;
   extern __shared__ __align__(16) double2 gsm[];
   __shared__ double2 scratch[32];
@@ -71,11 +76,12 @@ __global__ void __launch_bounds__(kGenThreads) k_kron2d(GenLevel L, const double
   const int RW = kGenTX + 2 * b, RH = kGenTY + 2 * b;
   double2* xs = gsm;             // RH x RW
   double2* px = gsm + RH * RW;   // G x RH x kGenTX
-  const int x0 = blockIdx.x * kGenTX, y0 = blockIdx.y * kGenTY;
+  const int x0 = blockIdx.x * kGenTX, y0 = rb + blockIdx.y * kGenTY;
   for (int e = threadIdx.x; e < RH * RW; e += blockDim.x) {
     const int rr = e / RW, cc = e % RW;
     const int gy = y0 - b + rr, gx = x0 - b + cc;
-    xs[e] = (gy >= 0 && gy < n && gx >= 0 && gx < n) ? x[(size_t)gy * n + gx] : cmk(0.0, 0.0);
+    xs[e] = (gy >= 0 && gy < n && gy >= rb - b && gy < re + b && gx >= 0 && gx < n) ? x[(size_t)gy * n + gx]
+                                                                                       : cmk(0.0, 0.0);
   }
   __syncthreads();
   // x pass: px[g][rr][c] = sum_j X_g(ix, j) x(row rr, ix + j - b)
@@ -96,7 +102,7 @@ __global__ void __launch_bounds__(kGenThreads) k_kron2d(GenLevel L, const double
   for (int e = threadIdx.x; e < kGenTY * kGenTX; e += blockDim.x) {
     const int r = e / kGenTX, c = e % kGenTX;
     const int iy = y0 + r, ix = x0 + c;
-    if (iy >= n || ix >= n) continue;
+    if (iy >= re || iy >= n || ix >= n) continue;
     double2 y = cmk(0.0, 0.0);
     for (int g = 0; g < G; ++g) {
       const double* Yr = L.Y[g] + (size_t)iy * NB;
@@ -132,16 +138,17 @@ __global__ void __launch_bounds__(kGenThreads) k_kron2d(GenLevel L, const double
   }
   if (MODE == OP_RESNORM) {
     double2 total;
-    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total)) *red.dst = sqrt(total.x) / red.scale;
+    if (grid_sum2(cmk(acc, 0.0), red.partials, red.counter, scratch, &total))
+      *red.dst = red.raw ? total.x : sqrt(total.x) / red.scale;
   }
 }
 
-// x = omega D^-1 b (Jacobi sweep from a zero iterate)
+// x = omega D^-1 b (Jacobi sweep from a zero iterate), rows [rb, re)
 __global__ void __launch_bounds__(256) k_jacobi0_gen(GenLevel L, const double2* __restrict__ bv,
-                                                     double2* __restrict__ out, double omega) {
-  const int n = L.n, NB = 2 * L.b + 1;
-  const size_t NN = (size_t)n * n;
-  for (size_t gi = blockIdx.x * (size_t)blockDim.x + threadIdx.x; gi < NN; gi += (size_t)gridDim.x * blockDim.x) {
+                                                     double2* __restrict__ out, double omega, int rb, int re) {
+  const int n = L.n;
+  const size_t g0 = (size_t)rb * n, g1 = (size_t)re * n;
+  for (size_t gi = g0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; gi < g1; gi += (size_t)gridDim.x * blockDim.x) {
     const int iy = (int)(gi / n), ix = (int)(gi % n);
     const double2 D = gen_entry(L, iy, ix, 0, 0);
     out[gi] = cscale(omega, cmul(cinv(D), bv[gi]));

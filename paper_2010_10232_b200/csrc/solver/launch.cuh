@@ -136,13 +136,14 @@ static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, con
 // layered field: G-term Kronecker-sum operator (layered.cuh)
 template <int MODE>
 static void launch_gen_mode(hd_ctx* c, const GenLevel& G, const double2* x, const double2* b, double2* out,
-                            double omega, RedOut red, int kind, const int* xidx, size_t xstride) {
+                            double omega, RedOut red, int kind, const int* xidx, size_t xstride, int rb, int re) {
   smem_optin(reinterpret_cast<const void*>(k_kron2d<MODE>), gen_smem(6, kGenMaxG));
   if (G.b > 6 || G.G > kGenMaxG) throw Error(HD_ERR_INVALID, "layered operator exceeds the kernel limits");
-  const dim3 grid((G.n + kGenTX - 1) / kGenTX, (G.n + kGenTY - 1) / kGenTY);
-  HD_LAUNCH(kind, op_bytes(MODE, static_cast<size_t>(G.n) * G.n),
+  if (re < 0) re = G.n;
+  const dim3 grid((G.n + kGenTX - 1) / kGenTX, (re - rb + kGenTY - 1) / kGenTY);
+  HD_LAUNCH(kind, op_bytes(MODE, static_cast<size_t>(G.n) * (re - rb)),
             k_kron2d<MODE><<<grid, kGenThreads, gen_smem(G.b, G.G), c->st>>>(G, x, b, out, omega, red, xidx,
-                                                                               xstride));
+                                                                               xstride, rb, re));
 }
 
 static RedOut red_of(hd_ctx* c, double* dst = nullptr, double scale = 1.0) {
@@ -165,10 +166,10 @@ static void op_apply(hd_ctx* c, int mode, const LevelDev& L, const double2* x, c
   if (L.gen) {
     const GenLevel& G = *static_cast<const GenLevel*>(L.gen);
     switch (mode) {
-      case OP_APPLY: launch_gen_mode<OP_APPLY>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
-      case OP_RESID: launch_gen_mode<OP_RESID>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
-      case OP_JACOBI: launch_gen_mode<OP_JACOBI>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
-      default: launch_gen_mode<OP_RESNORM>(c, G, x, b, out, omega, red, kind, xidx, xstride); break;
+      case OP_APPLY: launch_gen_mode<OP_APPLY>(c, G, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+      case OP_RESID: launch_gen_mode<OP_RESID>(c, G, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+      case OP_JACOBI: launch_gen_mode<OP_JACOBI>(c, G, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
+      default: launch_gen_mode<OP_RESNORM>(c, G, x, b, out, omega, red, kind, xidx, xstride, rb, re); break;
     }
     return;
   }
@@ -197,8 +198,10 @@ static void jacobi0(hd_ctx* c, const LevelDev& L, const double2* b, double2* out
   if (re < 0) re = L.n;
   const size_t NN = c->dim == 2 ? static_cast<size_t>(L.n) * L.n : L.n;
   if (L.gen) {
-    HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,
-              k_jacobi0_gen<<<grid_for(NN), 256, 0, c->st>>>(*static_cast<const GenLevel*>(L.gen), b, out, omega));
+    const size_t NR = static_cast<size_t>(re - rb) * L.n;
+    HD_LAUNCH(HD_K_JACOBI0, 32.0 * NR,
+              k_jacobi0_gen<<<grid_for(NR), 256, 0, c->st>>>(*static_cast<const GenLevel*>(L.gen), b, out, omega, rb,
+                                                             re));
     return;
   }
   HD_LAUNCH(HD_K_JACOBI0, 32.0 * NN,

@@ -930,7 +930,9 @@ static void create_slabs(hd_ctx* c, int S, int rank = 0, int nranks = 1, ncclCom
   if (c->dim != 2) throw Error(HD_ERR_INVALID, "row slabs: 2D only (1D configs run as replicas)");
   if (c->lev.size() < 2 || !c->spec.shift || c->spec.cycles < 1)
     throw Error(HD_ERR_INVALID, "row slabs: needs the multigrid-CSLP preconditioner (shift, cycles >= 1)");
-  if (c->fine.genA) throw Error(HD_ERR_INVALID, "row slabs: constant wave-number field only");
+  // layered and wedge fields: the G-term / stored-stencil level operators take
+  // row ranges like the Kronecker-sum stencil; their exact E solves (dense or
+  // block tridiagonal) run redundantly on the gathered coarse vector
   const int L = static_cast<int>(c->lev.size());
   const char* e = std::getenv("HD_SLAB_AGGLOMERATE");
   const int agg = e ? std::atoi(e) : 200;

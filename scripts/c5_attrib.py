@@ -1,7 +1,7 @@
 """C5 pre-stagnation history deviation vs the committed oracle run, per solver
 variant (run one variant per process: the env switches are read at create).
 
-  python scripts/c5_attrib.py LABEL   (env: HD_NOFOLD / HD_ARNOLDI / ...)
+  python scripts/c5_attrib.py LABEL   (env: HD_ESOLVE / HD_ARNOLDI / ...)
 prints max |dres| over steps 0..19 and per-step diffs, and writes
 gpurun_out/c5_attrib_LABEL.json with the full history and projections."""
 import json

@@ -332,12 +332,40 @@ def test_arbitrary_rhs_linearity():
     assert abs(true - r1.residuals[-1]) <= 1e-12
 
 
-def test_unsupported_specs_fail_loudly():
-    """Row slabs are built for the constant field only; the build refuses the
-    layered field there instead of approximating."""
-    s = hd.assemble(hd.layered_medium_2d(40, 2, 20.0))
-    with pytest.raises(hd.HelmdefError):
-        hd.Solver(s, hd.to_spec("DC_MG", 2, 20.0, **BASE), slabs=2)
+@pytest.mark.parametrize("graph", [0, 1])
+@pytest.mark.parametrize("field,S,ne,p,k,agg", [("wedge", 2, 120, 3, 40.0, 40), ("wedge", 4, 240, 3, 80.0, 60),
+                                                 ("layered", 3, 96, 2, 30.0, 30)])
+def test_row_slabs_non_separable_fields(field, S, ne, p, k, agg, graph, monkeypatch):
+    """Row slabs on the non-separable fields (north_star: "2D problems are
+    partitioned ... as row slabs", config 4 is the wedge): the G-term /
+    stored-stencil level operators take the slabs' row ranges and halo rows,
+    E (block tridiagonal or dense) is solved on the gathered coarse vector.
+    Against the single-domain solve: components to 1e-10, equal iterations and
+    counts, history 1e-10, solution 1e-8."""
+    import torch
+    monkeypatch.setenv("HD_SLAB_AGGLOMERATE", str(agg))
+    monkeypatch.setenv("HD_GRAPH", str(graph))
+    s = hd.assemble(hd.wedge_2d(ne, p, k) if field == "wedge" else hd.layered_medium_2d(ne, p, k))
+    spec = hd.to_spec("DC_MG", p, k, **BASE)
+    rng = np.random.default_rng(6)
+    v = rng.uniform(-1, 1, s.size) + 1j * rng.uniform(-1, 1, s.size)
+    xd = torch.from_numpy(v).cuda()
+    with hd.Solver(s, spec) as one, hd.Solver(s, spec, slabs=S) as sl:
+        assert sl.slabs == S
+        for which, tol in ((hd.HD_APPLY_A, 1e-13), (hd.HD_APPLY_MG, 1e-12), (hd.HD_APPLY_Q, 1e-10),
+                           (hd.HD_APPLY_OP, 1e-10)):
+            y1, y2 = torch.zeros_like(xd), torch.zeros_like(xd)
+            one.apply(which, xd.data_ptr(), y1.data_ptr())
+            sl.apply(which, xd.data_ptr(), y2.data_ptr())
+            a, b = y1.cpu().numpy(), y2.cpu().numpy()
+            assert np.linalg.norm(a - b) <= tol * np.linalg.norm(a), (which, np.linalg.norm(a - b) / np.linalg.norm(a))
+        r1 = one.solve(hd.GmresOptions(100, 1e-7))
+        r2 = sl.solve(hd.GmresOptions(100, 1e-7))
+    assert r2.converged == r1.converged and r2.iterations == r1.iterations
+    assert (r2.counts.matvecs, r2.counts.coarse_solves, r2.counts.shift_solves, r2.counts.vcycles) == \
+        (r1.counts.matvecs, r1.counts.coarse_solves, r1.counts.shift_solves, r1.counts.vcycles)
+    assert np.max(np.abs(np.array(r2.residuals) - np.array(r1.residuals))) <= 1e-10
+    assert np.linalg.norm(r2.solution - r1.solution) <= 1e-8 * np.linalg.norm(r1.solution)
 
 
 # ---- layered 4x4 medium (table6, SURVEY.md §8(f)) -----------------------------
@@ -535,9 +563,9 @@ def test_row_slabs_match_single_domain(S, ne, p, k, agg, vranks, graph, monkeypa
     # slab with packed all-to-alls (even nc would otherwise fold E and solve it
     # redundantly, as the shared-buffer cases with even nc do)
     if vranks:
-        monkeypatch.setenv("HD_NOFOLD", "1")
+        monkeypatch.setenv("HD_ESOLVE", "fd")
     else:
-        monkeypatch.delenv("HD_NOFOLD", raising=False)
+        monkeypatch.delenv("HD_ESOLVE", raising=False)
     s = hd.assemble(hd.point_source_2d(ne, p, k))
     spec = hd.to_spec("DC_MG", p, k, **BASE)
     rng = np.random.default_rng(5)
