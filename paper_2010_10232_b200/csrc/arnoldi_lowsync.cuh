@@ -208,6 +208,194 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
   if (threadIdx.x == 0) *a.counter = 0u;
 }
 
+// ---------------------------------------------------------------------------
+// pass 1 on the Blackwell bulk-copy engine (HD_LSA_TMA=1; default: k_lsa_dots).
+// One CTA per SM, 8 warps.  The CTA's chunks of w and u_j (kTCE elements) go
+// through a 3-deep ring of cp.async.bulk copies issued by thread 0 and
+// completed on mbarriers; every warp streams its own items -- (chunk, vector)
+// pairs t = c (j+1) + i, dealt round-robin over the warps so any j splits
+// evenly -- through its own 2-stage ring of bulk copies of u_i's chunk.  No
+// register staging and no CTA barrier in the stream: up to 3 chunks x 8 warps
+// of copies are in flight per SM, what the DRAM latency needs at this per-SM
+// share of the bandwidth.  A w / u_j buffer is refilled once all 8 warps have
+// left its chunk (an "empty" mbarrier of count 8).  Per-warp accumulators,
+// summed over the warps in fixed order at the end (deterministic).
+// Measured at C5: both passes 48.6 ms per solve against 48.3 ms with the
+// register-streaming pass 1 -- the stream was not short of bytes in flight.
+// ---------------------------------------------------------------------------
+constexpr int kTCE = 512;   // chunk elements (8 KB)
+constexpr int kTNW = 8;     // warps per CTA
+constexpr int kTWU = 3;     // w / u_j chunk buffers
+constexpr int kTST = 2;     // u_i ring stages per warp
+
+__host__ __device__ constexpr size_t lsa_tma_smem() {
+  return sizeof(double2) * ((size_t)2 * kTWU * kTCE + (size_t)kTNW * kTST * kTCE + (size_t)kTNW * 2 * (kLsaMaxJ + 1)) +
+         sizeof(unsigned long long) * (2 * kTWU + kTNW * kTST);
+}
+
+__device__ __forceinline__ unsigned tma_sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tma_mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tma_sa(b)), "r"(count));
+}
+__device__ __forceinline__ void tma_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tma_sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tma_sa(b)) : "memory");
+}
+__device__ __forceinline__ void tma_wait(unsigned long long* b, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(tma_sa(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_g2s(void* smem, const void* g, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tma_sa(smem)),
+               "l"(g), "r"(bytes), "r"(tma_sa(b))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kTNW * 32, 1) k_lsa_dots_tma(LsaArgs a) {
+  extern __shared__ __align__(128) double2 dsm[];
+  double2* wub = dsm;                                   // [kTWU][2][kTCE]: w chunk, u_j chunk
+  double2* ring = wub + 2 * kTWU * kTCE;                // [kTNW][kTST][kTCE]
+  double2* acc = ring + kTNW * kTST * kTCE;             // [kTNW][2][kLsaMaxJ+1]: s_i, G_ji
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(acc + kTNW * 2 * (kLsaMaxJ + 1));
+  unsigned long long* full_wu = bar;                    // [kTWU]
+  unsigned long long* empty_wu = bar + kTWU;            // [kTWU], count kTNW
+  unsigned long long* full_r = bar + 2 * kTWU;          // [kTNW][kTST]
+  __shared__ double2 sh_s[kLsaMaxJ + 1];
+  __shared__ double2 sh_lj[kLsaMaxJ];
+  __shared__ double2 hsm[kLsaMaxJ + 1];
+  if (a.done && *((volatile const int*)a.done)) return;
+  const int j = a.dj ? *a.dj : a.j;
+  const int nd = j + 1;
+  const int nslot = 2 * kLsaMaxJ + 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t N = a.N;
+  const double2* uj = a.U + (size_t)j * N;
+  const size_t nchunks = (N + kTCE - 1) / kTCE;
+  const int nch = nchunks > blockIdx.x ? (int)((nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+  auto chunk0 = [&](int c) { return ((size_t)blockIdx.x + (size_t)c * gridDim.x) * kTCE; };
+  auto chunk_len = [&](int c) { return (int)min((size_t)kTCE, N - chunk0(c)); };
+  for (int q = threadIdx.x; q < kTNW * 2 * (kLsaMaxJ + 1); q += blockDim.x) acc[q] = cmk(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kTWU; ++b) {
+      tma_mbar_init(&full_wu[b], 1);
+      tma_mbar_init(&empty_wu[b], kTNW);
+    }
+    for (int r = 0; r < kTNW * kTST; ++r) tma_mbar_init(&full_r[r], 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  auto load_wu = [&](int c) {  // thread 0: chunk c of w and u_j into buffer c % kTWU
+    const int b = c % kTWU, len = chunk_len(c);
+    const unsigned bytes = (unsigned)len * 16u;
+    tma_expect(&full_wu[b], (j > 0 ? 2u : 1u) * bytes);
+    tma_g2s(wub + (size_t)(2 * b) * kTCE, a.w + chunk0(c), bytes, &full_wu[b]);
+    if (j > 0) tma_g2s(wub + (size_t)(2 * b + 1) * kTCE, uj + chunk0(c), bytes, &full_wu[b]);
+  };
+  if (threadIdx.x == 0)
+    for (int c = 0; c < kTWU && c < nch; ++c) load_wu(c);
+  // this warp's items t = warp + k kTNW < nch nd: chunk t / nd, vector t % nd
+  const long nitems = (long)nch * nd;
+  auto load_item = [&](long t, int slot) {  // lane 0: u_i's chunk into the warp's ring slot
+    const int c = (int)(t / nd), i = (int)(t % nd);
+    const unsigned bytes = (unsigned)chunk_len(c) * 16u;
+    unsigned long long* fb = &full_r[warp * kTST + slot];
+    tma_expect(fb, bytes);
+    tma_g2s(ring + (size_t)(warp * kTST + slot) * kTCE, a.U + (size_t)i * N + chunk0(c), bytes, fb);
+  };
+  if (lane == 0)
+    for (int s2 = 0; s2 < kTST; ++s2) {
+      const long t = warp + (long)s2 * kTNW;
+      if (t < nitems) load_item(t, s2);
+    }
+  double2* myacc = acc + (size_t)warp * 2 * (kLsaMaxJ + 1);
+  int left = 0;  // chunks this warp has left (arrived on their empty barrier)
+  // arrive on the chunks before c_excl (after their load landed, so the arrival
+  // counts toward that use of the buffer even when the warp had no item in the
+  // chunk); warp 0 then refills each buffer once all warps have left it
+  auto leave_until = [&](int c_excl) {
+    for (; left < c_excl; ++left) {
+      tma_wait(&full_wu[left % kTWU], (unsigned)((left / kTWU) & 1));
+      __syncwarp();
+      if (lane == 0) tma_arrive(&empty_wu[left % kTWU]);
+      if (warp == 0 && lane == 0 && left + kTWU < nch) {
+        tma_wait(&empty_wu[left % kTWU], (unsigned)((left / kTWU) & 1));
+        load_wu(left + kTWU);
+      }
+    }
+  };
+  long k = 0;
+  // the chunk's w and u_j stay in registers while the warp's items stay in that
+  // chunk (consecutive items t, t + 8, ... are vectors i, i + 8, ... of one chunk),
+  // so a vector costs one shared-memory read per element
+  constexpr int PL = kTCE / 32;
+  double2 wr[PL], ur[PL];
+  int cur = -1;
+  for (long t = warp; t < nitems; t += kTNW, ++k) {
+    const int c = (int)(t / nd), i = (int)(t % nd);
+    leave_until(c);
+    const int slot = (int)(k % kTST);
+    const int len = chunk_len(c);
+    if (c != cur) {
+      tma_wait(&full_wu[c % kTWU], (unsigned)((c / kTWU) & 1));
+      const double2* ws = wub + (size_t)(2 * (c % kTWU)) * kTCE;
+      const double2* us = ws + kTCE;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const int e = q * 32 + lane;
+        wr[q] = e < len ? ws[e] : cmk(0.0, 0.0);
+        ur[q] = (e < len && j > 0) ? us[e] : cmk(0.0, 0.0);
+      }
+      cur = c;
+    }
+    tma_wait(&full_r[warp * kTST + slot], (unsigned)((k / kTST) & 1));
+    const double2* ui = ring + (size_t)(warp * kTST + slot) * kTCE;
+    double2 sa = cmk(0.0, 0.0), sb = cmk(0.0, 0.0), ga = cmk(0.0, 0.0), gb = cmk(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      const int e = q * 32 + lane;
+      const double2 v = e < len ? ui[e] : cmk(0.0, 0.0);
+      if (q & 1) {
+        sb = cadd(sb, cconjmul(v, wr[q]));
+        gb = cadd(gb, cconjmul(ur[q], v));
+      } else {
+        sa = cadd(sa, cconjmul(v, wr[q]));
+        ga = cadd(ga, cconjmul(ur[q], v));
+      }
+    }
+    const double2 s_ = lsa_warp_sum(cadd(sa, sb));
+    const double2 g_ = lsa_warp_sum(cadd(ga, gb));
+    __syncwarp();  // every lane done with the slot before it is refilled
+    if (lane == 0) {
+      myacc[i] = cadd(myacc[i], s_);
+      if (i < j) myacc[kLsaMaxJ + 1 + i] = cadd(myacc[kLsaMaxJ + 1 + i], g_);
+      const long tn = t + (long)kTST * kTNW;
+      if (tn < nitems) load_item(tn, slot);
+    }
+  }
+  leave_until(nch);
+  __syncthreads();
+  // CTA partials: the warps' accumulators in warp order
+  for (int q = threadIdx.x; q < nslot; q += blockDim.x) {
+    const bool used = q < nd || (q >= kLsaMaxJ + 1 && q < kLsaMaxJ + 1 + j);
+    if (used) {
+      double2 v = cmk(0.0, 0.0);
+      for (int w2 = 0; w2 < kTNW; ++w2) v = cadd(v, acc[(size_t)w2 * 2 * (kLsaMaxJ + 1) + q]);
+      a.partials[(size_t)(a.part_offset + blockIdx.x) * nslot + q] = v;
+    }
+  }
+  if (a.partial_only) return;
+  if (!lsa_last_block(a.counter)) return;
+  lsa_dots_finish(a, j, gridDim.x, sh_s, sh_lj, hsm);
+  if (threadIdx.x == 0) *a.counter = 0u;
+}
+
 // ---- totals, Gram row j, triangular solve (I + L) h = s (one CTA) ----------
 __device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh_s, double2* sh_lj, double2* hsm) {
   constexpr int NW = kLsaBD / 32;

@@ -239,6 +239,7 @@ struct hd_ctx {
   double2 *lsa_L = nullptr, *lsa_ch = nullptr, *lsa_cx = nullptr, *lsa_partials = nullptr;
   unsigned* lsa_counter = nullptr;
   int lsa_G = 0, lsa_maxit = -1;
+  bool lsa_tma = false;         // HD_LSA_TMA=1 at create: pass 1 on the bulk-copy ring (k_lsa_dots_tma)
   size_t lsa_givens_smem = 0;
   // graph-resident GMRES loop (WHILE conditional node), rebuilt when (maxit, tol) change
   cudaGraph_t loop_graph = nullptr;

@@ -578,7 +578,10 @@ static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero, bool x
   double2* xoth = xcur == c->mg_x[l] ? c->mg_y[l] : c->mg_x[l];
   const int nf = c->lev[l].n, ncl = c->lev[l + 1].n;
   const bool fuse = j0_fusable(c, l + 1);
-  if (fused_restrict_ok(c, L)) {  // residual + restriction (+ the coarse first sweep) in one pass
+  // residual + restriction (+ the coarse first sweep) in one pass on the levels with a
+  // 2-wide band; at the p = 3 fine level the fused kernel (up to 174 registers) measured
+  // 62 us against 52 us for the separate residual and restriction (ncu, C5), so it is split there
+  if (fused_restrict_ok(c, L) && L.b <= 2) {
     if (fuse)
       op_restrict<OP_RESID, 0, 0, true>(c, L, xcur, b, 0.0, ncl, c->mg_b[l + 1], nullptr, levM(c, l + 1),
                                         c->spec.omega, c->mg_x[l + 1]);
@@ -637,7 +640,7 @@ static const double2* mg_solve_ptr(hd_ctx* c, const double2* b, double2* out, bo
       const LevelDev L = levM(c, 0);
       double2* xcur = smooth(c, 0, b, c->mg_x[0], c->mg_y[0], false, c->spec.smooth_steps);
       double2* xoth = xcur == c->mg_x[0] ? c->mg_y[0] : c->mg_x[0];
-      if (fused_restrict_ok(c, L)) {
+      if (fused_restrict_ok(c, L) && L.b <= 2) {
         op_restrict<OP_RESID, 0, 0, false>(c, L, xcur, b, 0.0, c->lev[1].n, c->mg_b[1], nullptr);
       } else {
         op_apply(c, OP_RESID, L, xcur, b, c->mg_r[0]);
@@ -751,6 +754,19 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
     c->lsa_givens_smem = (static_cast<size_t>(m) * (m + 1) / 2 + 4 * (m + 2) + 8) * sizeof(double2);
     smem_optin(reinterpret_cast<const void*>(k_lsa_givens), c->lsa_givens_smem);
     c->lsa_maxit = maxit;
+  }
+}
+
+// pass 1 of the one-reduction Arnoldi: the register-streaming k_lsa_dots, or
+// (HD_LSA_TMA=1 at create) the bulk-copy ring kernel -- equal at C5 (48.6 vs
+// 48.3 ms for both passes over a solve), so the round-1 kernel stays the default
+static void launch_lsa_dots(hd_ctx* c, const LsaArgs& a, int G, cudaStream_t st) {
+  if (c->lsa_tma) {
+    smem_optin(reinterpret_cast<const void*>(k_lsa_dots_tma), lsa_tma_smem());
+    // one CTA per SM, never more CTAs than the partials buffer has slots (lsa_G)
+    k_lsa_dots_tma<<<std::min(c->n_sms, G), kTNW * 32, lsa_tma_smem(), st>>>(a);
+  } else {
+    k_lsa_dots<<<G, kLsaBD, lsa_dots_smem(), st>>>(a);
   }
 }
 
@@ -879,7 +895,7 @@ static void build_loop_graph(hd_ctx* c, int maxit, double tol) {
   CK(cudaEventRecord(c->ev_join, c->st2));
   compose_op(c, c->V, c->w, dj);
   CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
-  k_lsa_dots<<<G, kLsaBD, lsa_dots_smem(), c->st>>>(a);
+  launch_lsa_dots(c, a, G, c->st);
   k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a);  // u_{j+1} and the lagged x_{j-1}
   if (c->mon_side) {
     k_loop_breakdown<<<1, 1, 0, c->st>>>(c->loop_state, c->dres, h);
@@ -1159,7 +1175,7 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
       compose_op(c, c->V + static_cast<size_t>(j) * N, c->w);
       LsaArgs a = lsa_args(c, xout, j, 0, maxit);
       // pass 1 reads w, u_j, u_0..u_j; pass 2 reads w, u_0..u_j (+ x0 for j >= 1), writes u_{j+1} (+ x)
-      HD_LAUNCH(HD_K_MGS, (j + 3.0) * P, k_lsa_dots<<<G, kLsaBD, lsa_dots_smem(), c->st>>>(a));
+      HD_LAUNCH(HD_K_MGS, (j + 3.0) * P, launch_lsa_dots(c, a, G, c->st));
       HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 5.0 : 3.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a));
       if (j >= 1) {  // x_{j-1} is ready: monitor it (the reference's iteration j-1)
         monitor(xout);

@@ -509,6 +509,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
   c->device = (devices && n_devices == 1) ? devices[0] : 0;
   c->j0_fuse = std::getenv("HD_NOJ0FUSE") == nullptr;
+  c->lsa_tma = std::getenv("HD_LSA_TMA") && std::atoi(std::getenv("HD_LSA_TMA")) == 1;
   if (!devices || n_devices == 0) CK(cudaGetDevice(&c->device));
   CK(cudaSetDevice(c->device));
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));

@@ -159,3 +159,17 @@ def test_E_solvers_at_C5_agree():
     d_pfd, d_fold = _rel(out["pfd"], out["fd"]), _rel(out["fold"], out["fd"])
     print(f"C5 Q: pfd vs fd {d_pfd:.2e}, fold vs fd {d_fold:.2e}")
     assert d_pfd <= 1e-8 and d_fold <= 1e-8
+
+
+@pytest.mark.parametrize("ne,p,k", [(96, 2, 60.0), (130, 3, 80.0)])
+def test_tma_pass1_matches_register_pass1(monkeypatch, ne, p, k):
+    """Arnoldi pass 1 on the bulk-copy ring (k_lsa_dots_tma, HD_LSA_TMA=1)
+    against the register-streaming default (HD_LSA_TMA=0): the same dot
+    products summed in another order, so equal iterations and solutions within
+    1e-11."""
+    s = hd.assemble(hd.point_source_2d(ne, p, k))
+    a, b = _pair_env(monkeypatch, "HD_LSA_TMA", "1", "0", s, hd.to_spec("DC_MG", p, k, **BASE))
+    with a, b:
+        ra = a.solve(hd.GmresOptions(100, 1e-7))
+        rb = b.solve(hd.GmresOptions(100, 1e-7))
+    _same_solve(ra, rb, 1e-11)
