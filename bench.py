@@ -358,7 +358,8 @@ def run_gpu(args):
         ach = b / (ms * 1e-3) / 1e9
         traffic, traffic_src = None, None
         try:  # per-launch DRAM bytes of the same kernels from the committed ncu capture
-            tr = json.loads((ROOT / "profiles" / "r1_traffic.json").read_text())
+            tr_file = max((ROOT / "profiles").glob("r*_traffic.json"))  # the newest round's capture
+            tr = json.loads(tr_file.read_text())
             if tr.get("kernel_kind") == name and args.config == "C5":
                 traffic, traffic_src = tr["dram_bytes_per_launch"], tr["source"]
         except Exception:

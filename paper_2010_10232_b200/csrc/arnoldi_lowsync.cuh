@@ -59,6 +59,8 @@ struct LsaArgs {
   int part_offset;    // row slabs: this slab's first CTA slot in `partials` (0: single domain)
   int partial_only;   // row slabs: pass 1 writes its CTA partials and stops (k_lsa_dots_finish
                       // combines the slabs' partials in slab order)
+  int rev;            // pass 2 walks its tiles from the end of the vectors: pass 1 read them front to
+                      // back, so the tail of every basis vector is what the L2 still holds
 };
 
 __device__ __forceinline__ double2 lsa_warp_sum(double2 v) {
@@ -478,7 +480,9 @@ __global__ void __launch_bounds__(kLsaBD) k_lsa_update(LsaArgs a) {
   const size_t tile = (size_t)kLsaBD * kLsaTE;
   double2* un = a.Uw + (size_t)(j + 1) * N;
   double nrm = 0.0;
-  for (size_t t0 = (size_t)blockIdx.x * tile; t0 < N; t0 += (size_t)gridDim.x * tile) {
+  const size_t ntiles = (N + tile - 1) / tile;
+  for (size_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+    const size_t t0 = (a.rev ? ntiles - 1 - tt : tt) * tile;
     double2 wv[kLsaTE], xv[kLsaTE];
 #pragma unroll
     for (int u = 0; u < kLsaTE; ++u) {

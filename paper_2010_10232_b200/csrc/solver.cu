@@ -26,6 +26,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/helmdef_b200.h"
@@ -35,6 +36,7 @@
 #include "stencil.cuh"
 #include "transfer.cuh"
 #include "stencil_restrict.cuh"
+#include "stencil_tma.cuh"
 #include "arnoldi_lowsync.cuh"
 #include "layered.cuh"
 #include "btri.cuh"

@@ -239,6 +239,19 @@ struct hd_ctx {
   double2 *lsa_L = nullptr, *lsa_ch = nullptr, *lsa_cx = nullptr, *lsa_partials = nullptr;
   unsigned* lsa_counter = nullptr;
   int lsa_G = 0, lsa_maxit = -1;
+  // tensor-copy stencil (stencil_tma.cuh) for whole-grid 2D level operators of at least
+  // tma_min_n rows: HD_STENCIL_TMA=0 at create keeps the cp.async stencil everywhere
+  bool stencil_tma = true;
+  int tma_min_n = 512;
+  std::map<std::pair<const double*, const double*>, double2*> tma_ct;  // (S, M) tables -> CT of the level
+  struct TmaKey {
+    const void* base; int n, nvec, cols;
+    bool operator<(const TmaKey& o) const {
+      return std::tie(base, n, nvec, cols) < std::tie(o.base, o.n, o.nvec, o.cols);
+    }
+  };
+  std::map<TmaKey, CUtensorMap> tma_maps;
+  bool lsa_rev = true;          // HD_LSA_REV=0 at create: pass 2 walks the vectors front to back (A/B of the L2 reuse)
   bool lsa_tma = false;         // HD_LSA_TMA=1 at create: pass 1 on the bulk-copy ring (k_lsa_dots_tma)
   size_t lsa_givens_smem = 0;
   // graph-resident GMRES loop (WHILE conditional node), rebuilt when (maxit, tol) change

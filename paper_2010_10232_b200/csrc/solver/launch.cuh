@@ -105,10 +105,133 @@ static int pick_rows(int n, int rows, int slots, int B) {
   return best;
 }
 
+// ---- tensor-copy stencil (stencil_tma.cuh): tensor maps, CT tables, launch -------------------
+typedef CUresult (*TmaEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// cuTensorMapEncodeTiled through the runtime (the library does not link libcuda); null when the driver lacks it
+static TmaEncodeFn tma_encode_fn() {
+  static TmaEncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<TmaEncodeFn>(f);
+  }();
+  return fn;
+}
+
+// Map of `nvec` consecutive n x n complex grids at `base` viewed as doubles (2n, n, nvec), box
+// (2 cols, kTSR rows, 1); rows and columns outside a grid read as zero.  Cached per context.
+static const CUtensorMap& tma_map(hd_ctx* c, const double2* base, int n, int nvec, int cols) {
+  const hd_ctx::TmaKey key{base, n, nvec, cols};
+  auto it = c->tma_maps.find(key);
+  if (it != c->tma_maps.end()) return it->second;
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2) * n, static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(nvec)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(16) * n, static_cast<cuuint64_t>(16) * n * n};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(2 * cols), static_cast<cuuint32_t>(kTSR), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = tma_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(base), dims, strides,
+                                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(HD_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return c->tma_maps.emplace(key, m).first->second;
+}
+
+// CT of a level (y coefficients per input row, stencil_tma.cuh); setup builds the tables of
+// every eligible level (tma_prepare), so no allocation happens inside a graph capture
+static const double2* tma_ct(hd_ctx* c, const LevelDev& L) {
+  auto key = std::make_pair(L.S, L.M);
+  auto it = c->tma_ct.find(key);
+  if (it != c->tma_ct.end()) return it->second;
+  const int rows = L.n + 2 * L.b + kTSR;
+  double2* ct = dalloc<double2>(static_cast<size_t>(rows) * (2 * L.b + 2));
+  k_build_ct<<<64, 256, 0, c->st>>>(L, ct, rows);
+  CK(cudaGetLastError());
+  c->tma_ct[key] = ct;
+  return ct;
+}
+
+// the modes and levels the tensor-copy kernel takes: whole-grid operators (no row slab) of 2D
+// Kronecker-sum levels with at least tma_min_n rows.  The Jacobi mode stays on the cp.async
+// kernel (its centre-value queue spills at two columns per lane).
+template <int MODE>
+static bool stencil_tma_ok(hd_ctx* c, const LevelDev& L, int rb, int re) {
+  return c->stencil_tma && MODE != OP_JACOBI && rb == 0 && re == L.n && L.n >= c->tma_min_n && L.b <= 6 &&
+         tma_encode_fn() != nullptr;
+}
+
+template <int B, int MODE>
+static int stencil_tma_occupancy() {
+  static std::mutex mu;
+  static std::map<int, int> per_dev;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = per_dev.find(dev);
+    if (it != per_dev.end()) return it->second;
+  }
+  constexpr size_t sm = TmaLayout<B, MODE>::total;
+  smem_optin(reinterpret_cast<const void*>(k_stencil2d_tma<B, MODE>), sm);
+  int per = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stencil2d_tma<B, MODE>, 32 * kTWarps, sm));
+  per = std::max(per, 1);
+  std::lock_guard<std::mutex> lk(mu);
+  per_dev[dev] = per;
+  return per;
+}
+
+// strip height of the tensor-copy kernel: the warp tasks fill whole waves of resident warps,
+// discounted by the 2B halo rows every strip recomputes
+static int pick_rows_tma(int n, int warp_slots, int B, int* strips_x, int* ntasks) {
+  const int sx = (n + kTW - 1) / kTW;
+  int best = 32;
+  double best_score = -1.0;
+  for (int ry = 8; ry <= 256; ++ry) {
+    const long tasks = static_cast<long>(sx) * ((n + ry - 1) / ry);
+    const long waves = (tasks + warp_slots - 1) / warp_slots;
+    const double util = static_cast<double>(tasks) / (static_cast<double>(waves) * warp_slots);
+    const double score = util * ry / (ry + 2.0 * B);
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = ry;
+    }
+  }
+  *strips_x = sx;
+  *ntasks = sx * ((n + best - 1) / best);
+  return best;
+}
+
+template <int B, int MODE>
+static void launch_stencil_tma(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
+                               double omega, RedOut red, const int* xidx, size_t xstride, double2* out2, double2 c2) {
+  const int per = stencil_tma_occupancy<B, MODE>();
+  int strips_x = 0, ntasks = 0;
+  const int ry = pick_rows_tma(L.n, per * kTWarps * c->n_sms, B, &strips_x, &ntasks);
+  // x: one grid, or (graph mode, x = V + j N with j on the device) the whole basis as a 3D map
+  const bool basis = xidx != nullptr;
+  if (basis && xstride != static_cast<size_t>(L.n) * L.n) throw Error(HD_ERR_INVALID, "stencil: basis stride");
+  const CUtensorMap& tmx = tma_map(c, x, L.n, basis ? c->v_cap : 1, tma_xc<B>());
+  const bool need_b = TmaLayout<B, MODE>::NEED_B;
+  const CUtensorMap& tmb = need_b ? tma_map(c, b, L.n, 1, kTBC) : tmx;
+  const double2* ct = tma_ct(c, L);
+  const int grid = (ntasks + kTWarps - 1) / kTWarps;
+  k_stencil2d_tma<B, MODE><<<grid, 32 * kTWarps, TmaLayout<B, MODE>::total, c->st>>>(tmx, tmb, L, ct, out, omega, ry,
+                                                                                      strips_x, ntasks, red, xidx, out2, c2);
+}
+
 template <int B, int MODE>
 static void launch_stencil(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
                            double omega, RedOut red, const int* xidx, size_t xstride, int rb, int re,
                            double2* out2 = nullptr, double2 c2 = double2{0.0, 0.0}) {
+  if (stencil_tma_ok<MODE>(c, L, rb, re)) {
+    launch_stencil_tma<B, MODE>(c, L, x, b, out, omega, red, xidx, xstride, out2, c2);
+    return;
+  }
   const int per = stencil_occupancy<B, MODE>();
   const int ry = pick_rows(L.n, re - rb, per * c->n_sms, B);
   dim3 grid((L.n + kSW * kSWarps - 1) / (kSW * kSWarps), (re - rb + ry - 1) / ry);
@@ -775,6 +898,7 @@ static LsaArgs lsa_args(hd_ctx* c, double2* xout, int j, int mode, int maxit) {
   a.jlag = 0;
   a.part_offset = 0;
   a.partial_only = 0;
+  a.rev = c->lsa_rev ? 1 : 0;
   a.U = c->V;
   a.Uw = c->V;
   a.w = c->w;

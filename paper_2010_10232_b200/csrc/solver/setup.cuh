@@ -461,6 +461,7 @@ static void destroy_ctx(hd_ctx* c) {
   dfree(c->dj);
   dfree(c->lsa_sig); dfree(c->lsa_L); dfree(c->lsa_ch); dfree(c->lsa_cx); dfree(c->lsa_partials);
   dfree(c->lsa_counter);
+  for (auto& kv : c->tma_ct) dfree(kv.second);
   if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
   if (c->pre_exec) cudaGraphExecDestroy(c->pre_exec);
   if (c->loop_graph) cudaGraphDestroy(c->loop_graph);
@@ -509,6 +510,9 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
   c->device = (devices && n_devices == 1) ? devices[0] : 0;
   c->j0_fuse = std::getenv("HD_NOJ0FUSE") == nullptr;
+  c->stencil_tma = !(std::getenv("HD_STENCIL_TMA") && std::atoi(std::getenv("HD_STENCIL_TMA")) == 0);
+  if (std::getenv("HD_STENCIL_TMA_MIN")) c->tma_min_n = std::atoi(std::getenv("HD_STENCIL_TMA_MIN"));
+  c->lsa_rev = !(std::getenv("HD_LSA_REV") && std::atoi(std::getenv("HD_LSA_REV")) == 0);
   c->lsa_tma = std::getenv("HD_LSA_TMA") && std::atoi(std::getenv("HD_LSA_TMA")) == 1;
   if (!devices || n_devices == 0) CK(cudaGetDevice(&c->device));
   CK(cudaSetDevice(c->device));
@@ -771,6 +775,12 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   c->mon_partials = dalloc<double2>(std::max(c->red_blocks, max_stencil_blocks) + 16);
   c->mon_counter = dalloc<unsigned>(4);
   CK(cudaMemset(c->mon_counter, 0, 4 * sizeof(unsigned)));
+  // tensor-copy stencil: the y-coefficient tables of every level it will take
+  if (c->dim == 2 && c->stencil_tma && tma_encode_fn() != nullptr) {
+    if (!c->fine.genA && c->n >= c->tma_min_n) tma_ct(c.get(), opA(c.get()));
+    for (size_t l = 0; l < c->lev.size(); ++l)
+      if (!c->lev[l].genM && c->lev[l].n >= c->tma_min_n) tma_ct(c.get(), levM(c.get(), static_cast<int>(l)));
+  }
   CK(cudaStreamSynchronize(c->st));
   CK(cudaDeviceSynchronize());
   // HD_ARNOLDI=0: exact-order MGS engine (one kernel per MGS step) for every budget

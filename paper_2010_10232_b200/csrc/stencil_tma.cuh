@@ -121,17 +121,9 @@ __global__ void k_build_ct(LevelDev L, double2* __restrict__ ct, int rows) {
   }
 }
 
-// interior band rows of a level whose rows are identical away from the boundary (uniform knots):
-// passed by value, so every coefficient is a constant-bank operand of its FMA
-struct UniCoef {
-  double sx[13], mx[13];  // band row of S and M
-  double2 cy[14];         // (M, S) band entries in CT order + the diagonal pair
-};
-
-template <int B, int MODE, bool UNI = false>
-__global__ void __launch_bounds__(32 * kTWarps, UNI ? 3 : 2)
-    k_stencil2d_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
-                    const __grid_constant__ UniCoef cu, LevelDev L,
+template <int B, int MODE>
+__global__ void __launch_bounds__(32 * kTWarps, 2)
+    k_stencil2d_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, LevelDev L,
                     const double2* __restrict__ ct, double2* __restrict__ out, double omega, int RY, int strips_x,
                     int ntasks, RedOut red, const int* xidx, double2* __restrict__ out2, double2 c2) {
   constexpr int NB = 2 * B + 1;
@@ -188,10 +180,10 @@ __global__ void __launch_bounds__(32 * kTWarps, UNI ? 3 : 2)
     double sx0[NB], mx0[NB], sx1[NB], mx1[NB];
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      sx0[j] = UNI ? 0.0 : v0 ? L.S[(size_t)c0 * NB + j] : 0.0;
-      mx0[j] = UNI ? 0.0 : v0 ? L.M[(size_t)c0 * NB + j] : 0.0;
-      sx1[j] = UNI ? 0.0 : v1 ? L.S[(size_t)(c0 + 1) * NB + j] : 0.0;
-      mx1[j] = UNI ? 0.0 : v1 ? L.M[(size_t)(c0 + 1) * NB + j] : 0.0;
+      sx0[j] = v0 ? L.S[(size_t)c0 * NB + j] : 0.0;
+      mx0[j] = v0 ? L.M[(size_t)c0 * NB + j] : 0.0;
+      sx1[j] = v1 ? L.S[(size_t)(c0 + 1) * NB + j] : 0.0;
+      mx1[j] = v1 ? L.M[(size_t)(c0 + 1) * NB + j] : 0.0;
     }
     // per-lane byte offsets inside a stage
     const unsigned xoff = (sel ? (unsigned)Lay::xbox : 0u) + (unsigned)(2 * pp + sel) * 16u;
@@ -239,20 +231,20 @@ __global__ void __launch_bounds__(32 * kTWarps, UNI ? 3 : 2)
           double2 cyv[NB + 1];
 #pragma unroll
           for (int d = 0; d < NB + 1; ++d) cyv[d] = cmk(0.0, 0.0);
-          if (!UNI) cyv[0] = tq_lds<0>(ca);
-          if (!UNI && NB + 1 > 1) cyv[1] = tq_lds<16>(ca);
-          if (!UNI && NB + 1 > 2) cyv[2] = tq_lds<32>(ca);
-          if (!UNI && NB + 1 > 3) cyv[3] = tq_lds<48>(ca);
-          if (!UNI && NB + 1 > 4) cyv[4] = tq_lds<64>(ca);
-          if (!UNI && NB + 1 > 5) cyv[5] = tq_lds<80>(ca);
-          if (!UNI && NB + 1 > 6) cyv[6] = tq_lds<96>(ca);
-          if (!UNI && NB + 1 > 7) cyv[7] = tq_lds<112>(ca);
-          if (!UNI && NB + 1 > 8) cyv[8] = tq_lds<128>(ca);
-          if (!UNI && NB + 1 > 9) cyv[9] = tq_lds<144>(ca);
-          if (!UNI && NB + 1 > 10) cyv[10] = tq_lds<160>(ca);
-          if (!UNI && NB + 1 > 11) cyv[11] = tq_lds<176>(ca);
-          if (!UNI && NB + 1 > 12) cyv[12] = tq_lds<192>(ca);
-          if (!UNI && NB + 1 > 13) cyv[13] = tq_lds<208>(ca);
+          cyv[0] = tq_lds<0>(ca);
+          if (NB + 1 > 1) cyv[1] = tq_lds<16>(ca);
+          if (NB + 1 > 2) cyv[2] = tq_lds<32>(ca);
+          if (NB + 1 > 3) cyv[3] = tq_lds<48>(ca);
+          if (NB + 1 > 4) cyv[4] = tq_lds<64>(ca);
+          if (NB + 1 > 5) cyv[5] = tq_lds<80>(ca);
+          if (NB + 1 > 6) cyv[6] = tq_lds<96>(ca);
+          if (NB + 1 > 7) cyv[7] = tq_lds<112>(ca);
+          if (NB + 1 > 8) cyv[8] = tq_lds<128>(ca);
+          if (NB + 1 > 9) cyv[9] = tq_lds<144>(ca);
+          if (NB + 1 > 10) cyv[10] = tq_lds<160>(ca);
+          if (NB + 1 > 11) cyv[11] = tq_lds<176>(ca);
+          if (NB + 1 > 12) cyv[12] = tq_lds<192>(ca);
+          if (NB + 1 > 13) cyv[13] = tq_lds<208>(ca);
           double2 b0 = cmk(0.0, 0.0), b1 = cmk(0.0, 0.0);
           if (NEED_B) {
             const unsigned ba = st + boff + (unsigned)rs * (kTBC * 16);
@@ -265,15 +257,15 @@ __global__ void __launch_bounds__(32 * kTWarps, UNI ? 3 : 2)
 #pragma unroll
           for (int j = 0; j < NB; ++j) {
             if (j & 1) {
-              u1 = cfma_r(UNI ? cu.sx[j] : sx0[j], xv[j], u1);
-              w1 = cfma_r(UNI ? cu.mx[j] : mx0[j], xv[j], w1);
-              p1 = cfma_r(UNI ? cu.sx[j] : sx1[j], xv[j + 1], p1);
-              r1 = cfma_r(UNI ? cu.mx[j] : mx1[j], xv[j + 1], r1);
+              u1 = cfma_r(sx0[j], xv[j], u1);
+              w1 = cfma_r(mx0[j], xv[j], w1);
+              p1 = cfma_r(sx1[j], xv[j + 1], p1);
+              r1 = cfma_r(mx1[j], xv[j + 1], r1);
             } else {
-              u0 = cfma_r(UNI ? cu.sx[j] : sx0[j], xv[j], u0);
-              w0 = cfma_r(UNI ? cu.mx[j] : mx0[j], xv[j], w0);
-              p0 = cfma_r(UNI ? cu.sx[j] : sx1[j], xv[j + 1], p0);
-              r0 = cfma_r(UNI ? cu.mx[j] : mx1[j], xv[j + 1], r0);
+              u0 = cfma_r(sx0[j], xv[j], u0);
+              w0 = cfma_r(mx0[j], xv[j], w0);
+              p0 = cfma_r(sx1[j], xv[j + 1], p0);
+              r0 = cfma_r(mx1[j], xv[j + 1], r0);
             }
           }
           if (MODE == OP_JACOBI) {
@@ -314,7 +306,7 @@ __global__ void __launch_bounds__(32 * kTWarps, UNI ? 3 : 2)
           const double2 Pb = csub(cadd(p0, p1), cmul(c, vb));
 #pragma unroll
           for (int d = 0; d < NB; ++d) {
-            const double2 cyd = UNI ? cu.cy[d] : cyv[d];
+            const double2 cyd = cyv[d];
             double2& ya = Y0[(t + 1 + d) % NB];
             double2& yb = Y1[(t + 1 + d) % NB];
             ya = cfma_r(cyd.x, Pa, cfma_r(cyd.y, va, ya));
@@ -324,19 +316,19 @@ __global__ void __launch_bounds__(32 * kTWarps, UNI ? 3 : 2)
             double2& ya = Y0[(t + 1) % NB];
             double2& yb = Y1[(t + 1) % NB];
             if (k >= 2 * B) {  // output row y0 + k - 2B is complete
-              const double2 cyc = UNI ? cu.cy[NB] : cyv[NB];
+              const double2 cyc = cyv[NB];
               if (MODE == OP_APPLY) {
                 if (v0) outp[0] = ya;
                 if (v1) outp[1] = yb;
               } else if (MODE == OP_APPLYJ0) {
                 if (v0) {
                   outp[0] = ya;
-                  const double2 D = csub(cmk(cyc.x * (UNI ? cu.sx[B] : sx0[B]) + cyc.y * (UNI ? cu.mx[B] : mx0[B]), 0.0), cscale(cyc.x * (UNI ? cu.mx[B] : mx0[B]), c2));
+                  const double2 D = csub(cmk(cyc.x * sx0[B] + cyc.y * mx0[B], 0.0), cscale(cyc.x * mx0[B], c2));
                   out2[outp - out] = cscale(omega, cmul(cinv(D), ya));
                 }
                 if (v1) {
                   outp[1] = yb;
-                  const double2 D = csub(cmk(cyc.x * (UNI ? cu.sx[B] : sx1[B]) + cyc.y * (UNI ? cu.mx[B] : mx1[B]), 0.0), cscale(cyc.x * (UNI ? cu.mx[B] : mx1[B]), c2));
+                  const double2 D = csub(cmk(cyc.x * sx1[B] + cyc.y * mx1[B], 0.0), cscale(cyc.x * mx1[B], c2));
                   out2[outp - out + 1] = cscale(omega, cmul(cinv(D), yb));
                 }
               } else if (MODE == OP_RESID) {
@@ -347,11 +339,11 @@ __global__ void __launch_bounds__(32 * kTWarps, UNI ? 3 : 2)
                 if (v1) acc += cnorm2(csub(b1, yb));
               } else {
                 if (v0) {
-                  const double2 D = csub(cmk(cyc.x * (UNI ? cu.sx[B] : sx0[B]) + cyc.y * (UNI ? cu.mx[B] : mx0[B]), 0.0), cscale(cyc.x * (UNI ? cu.mx[B] : mx0[B]), c));
+                  const double2 D = csub(cmk(cyc.x * sx0[B] + cyc.y * mx0[B], 0.0), cscale(cyc.x * mx0[B], c));
                   outp[0] = cadd(XC0[(t + 1) % NB], cscale(omega, cmul(cinv(D), csub(b0, ya))));
                 }
                 if (v1) {
-                  const double2 D = csub(cmk(cyc.x * (UNI ? cu.sx[B] : sx1[B]) + cyc.y * (UNI ? cu.mx[B] : mx1[B]), 0.0), cscale(cyc.x * (UNI ? cu.mx[B] : mx1[B]), c));
+                  const double2 D = csub(cmk(cyc.x * sx1[B] + cyc.y * mx1[B], 0.0), cscale(cyc.x * mx1[B], c));
                   outp[1] = cadd(XC1[(t + 1) % NB], cscale(omega, cmul(cinv(D), csub(b1, yb))));
                 }
               }

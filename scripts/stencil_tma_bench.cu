@@ -103,14 +103,6 @@ static void run_mode(int n, int reps, const char* name) {
   auto rnd = [] { return 2.0 * rand() / RAND_MAX - 1.0; };
   for (auto& v : hS) v = rnd();
   for (auto& v : hM) v = rnd() + 3.0;
-  const bool uni = std::getenv("UNI") != nullptr;
-  if (uni)  // every row as row 0 (uniform interior; the frame is not handled in this A/B)
-    for (int i = 1; i < n; ++i)
-      for (int j = 0; j < NB; ++j) hS[(size_t)i * NB + j] = hS[j], hM[(size_t)i * NB + j] = hM[j];
-  UniCoef cu{};
-  for (int j = 0; j < NB; ++j) cu.sx[j] = hS[j], cu.mx[j] = hM[j];
-  for (int d = 0; d < NB; ++d) cu.cy[d] = make_double2(hM[2 * B - d], hS[2 * B - d]);
-  cu.cy[NB] = make_double2(hM[B], hS[B]);
   const int nvec = 3, jv = 2;
   std::vector<double2> hx(N * nvec), hb(N);
   for (auto& v : hx) v = make_double2(rnd(), rnd());
@@ -177,7 +169,7 @@ static void run_mode(int n, int reps, const char* name) {
 
   // --- tensor-copy kernel
   using Lay = TmaLayout<B, MODE>;
-  auto kern = uni ? k_stencil2d_tma<B, MODE, true> : k_stencil2d_tma<B, MODE, false>;
+  auto kern = k_stencil2d_tma<B, MODE>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::total));
   int per2 = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, kern, 32 * kTWarps, Lay::total));
@@ -189,7 +181,7 @@ static void run_mode(int n, int reps, const char* name) {
   for (int r = 0; r < reps; ++r) {
     CK(cudaMemsetAsync(flush, r, 256u << 20));
     CK(cudaEventRecord(e0));
-    kern<<<grid2, 32 * kTWarps, Lay::total>>>(tmx, tmb, cu, L, ct, p1, omega, ry2, strips_x, ntasks, red,
+    kern<<<grid2, 32 * kTWarps, Lay::total>>>(tmx, tmb, L, ct, p1, omega, ry2, strips_x, ntasks, red,
                                                                  didx, p2, c2);
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));

@@ -173,3 +173,28 @@ def test_tma_pass1_matches_register_pass1(monkeypatch, ne, p, k):
         ra = a.solve(hd.GmresOptions(100, 1e-7))
         rb = b.solve(hd.GmresOptions(100, 1e-7))
     _same_solve(ra, rb, 1e-11)
+
+
+@pytest.mark.parametrize("ne,p,k", [(130, 3, 80.0), (200, 2, 100.0), (97, 4, 50.0), (75, 1, 30.0), (66, 5, 30.0)])
+def test_tensor_copy_stencil_is_bit_identical(monkeypatch, ne, p, k):
+    """The tensor-copy stencil (stencil_tma.cuh: UTMALDG boxes, two columns per
+    lane; HD_STENCIL_TMA, default on for levels of >= 512 rows, forced here for
+    every level of >= 16 rows) does the arithmetic of the cp.async stencil in
+    the same order: A v, the shifted operator, a V-cycle and the composed
+    operator are bit-identical; only the monitor's reduction is summed in
+    another order, so a solve's history agrees to rounding."""
+    s = hd.assemble(hd.point_source_2d(ne, p, k))
+    spec = hd.to_spec("DC_MG", p, k, **BASE)
+    monkeypatch.setenv("HD_STENCIL_TMA_MIN", "16")
+    a, b = _pair_env(monkeypatch, "HD_STENCIL_TMA", "1", "0", s, spec)
+    monkeypatch.delenv("HD_STENCIL_TMA_MIN", raising=False)
+    x = _rand(s.size, 11)
+    with a, b:
+        for which in (hd.HD_APPLY_A, hd.HD_APPLY_SHIFTED, hd.HD_APPLY_MG, hd.HD_APPLY_OP):
+            ya, yb = _apply(a, which, x), _apply(b, which, x)
+            assert np.array_equal(ya.view(np.uint64), yb.view(np.uint64)), which
+        ra = a.solve(hd.GmresOptions(100, 1e-7))
+        rb = b.solve(hd.GmresOptions(100, 1e-7))
+    assert ra.iterations == rb.iterations and ra.converged and rb.converged
+    assert np.max(np.abs(np.array(ra.residuals) - np.array(rb.residuals))) <= 1e-13
+    assert _rel(ra.solution, rb.solution) <= 1e-12
