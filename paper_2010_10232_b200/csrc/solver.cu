@@ -14,6 +14,7 @@
 #include <cusolverDn.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges cost nothing unless a profiler is attached
 
 #include <algorithm>
 #include <chrono>
@@ -207,6 +208,7 @@ static hd_status solve_impl(hd_ctx* c, const hd_gmres* opt, const double* rhs, b
   if (!c || !opt || !rhs || !x_out) throw Error(HD_ERR_INVALID, "null argument");
   if (opt->max_iterations < 0) throw Error(HD_ERR_INVALID, "max_iterations < 0");
   CK(cudaSetDevice(c->device));
+  NvtxRange nvtx_solve("hd_solve");
   const size_t N = c->N;
   CK(cudaEventRecord(c->ev0, c->st));
   CK(cudaMemcpyAsync(c->f, rhs, N * sizeof(double2), rhs_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,

@@ -107,6 +107,15 @@ static long check_guards() {
   return bad;
 }
 
+// NVTX range of a host-side phase (setup phases, the prelude, the GMRES loop and, in the
+// host-driven loop, the operator's parts and the Arnoldi passes): visible in nsys / ncu timelines.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Opt-in to `bytes` of dynamic shared memory for kernel `f` on the CURRENT
 // device.  cudaFuncSetAttribute applies per device, so the cache is keyed by
 // (device, function) and guarded: contexts on other GPUs or other host

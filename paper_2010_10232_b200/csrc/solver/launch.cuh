@@ -810,6 +810,7 @@ static void project(hd_ctx* c, const double2* w, double2* out) {
 
 // out = op(v) = P MG^-1 A v  (src/precond.cpp:236-245); v, out distinct from t1, t2, t3
 static void compose_op(hd_ctx* c, const double2* v, double2* out, const int* vidx = nullptr) {
+  NvtxRange nvtx_op("op = P MG^-1 A");
   ++c->matvecs;
   // A v also takes the fine level's first Jacobi sweep of the V-cycle (OP_APPLYJ0)
   const bool fuse = c->spec.shift && c->spec.cycles >= 1 && c->lev.size() > 1 && j0_fusable(c, 0);
@@ -822,11 +823,13 @@ static void compose_op(hd_ctx* c, const double2* v, double2* out, const int* vid
   }
   const double2* cur = c->t1;
   if (c->spec.shift) {
+    NvtxRange nvtx_mg("MG^-1 (V-cycles / C_ex)");
     ++c->shift_solves;
     c->vcycles += c->spec.cycles;
     cur = mg_solve_ptr(c, c->t1, c->t2, fuse);  // no copy: project reads it before the next V-cycle
   }
   if (c->spec.deflate) {
+    NvtxRange nvtx_p("project (Z^T A, E^-1, Z)");
     ++c->coarse_solves;
     project(c, cur, out);
   } else {
@@ -1133,6 +1136,7 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
   long* cnt[4] = {&c->matvecs, &c->coarse_solves, &c->shift_solves, &c->vcycles};
   long snap0[4] = {0, 0, 0, 0};  // counters before the speculative op(x0)
   auto prelude = [&]() {
+    NvtxRange nvtx_pre("GMRES prelude (rhs', x0, monitor, op(x0), beta)");
     // ||f|| (monitor scale, src/precond.cpp:258)
     HD_LAUNCH(HD_K_VEC, P, k_axpy_norm<<<nb, 256, 0, c->st>>>(c->f, nullptr, nullptr, N, red_of(c, c->dres + 3), c->scal + 2));
     // rhs' = P MG^-1 f   (src/precond.cpp:247-253)
@@ -1238,6 +1242,7 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
     if (c->graph_enabled && !c->prof_on) {
       if (c->loop_maxit != maxit || c->loop_tol != opt.tolerance || c->loop_epoch != c->buf_epoch)
         build_loop_graph(c, maxit, opt.tolerance);
+      NvtxRange nvtx_loop("GMRES loop (device-resident graph)");
       k_loop_init<<<1, 1, 0, c->st>>>(c->loop_state);
       CK(cudaGraphLaunch(c->loop_exec, c->st));
       CK(cudaMemcpyAsync(c->loop_host, c->loop_state, sizeof(LoopState), cudaMemcpyDeviceToHost, c->st));
@@ -1299,8 +1304,11 @@ static SolveOut run_solve(hd_ctx* c, const hd_gmres& opt, double2* xout) {
       compose_op(c, c->V + static_cast<size_t>(j) * N, c->w);
       LsaArgs a = lsa_args(c, xout, j, 0, maxit);
       // pass 1 reads w, u_j, u_0..u_j; pass 2 reads w, u_0..u_j (+ x0 for j >= 1), writes u_{j+1} (+ x)
-      HD_LAUNCH(HD_K_MGS, (j + 3.0) * P, launch_lsa_dots(c, a, G, c->st));
-      HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 5.0 : 3.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a));
+      {
+        NvtxRange nvtx_a("Arnoldi passes");
+        HD_LAUNCH(HD_K_MGS, (j + 3.0) * P, launch_lsa_dots(c, a, G, c->st));
+        HD_LAUNCH(HD_K_MGS, (j >= 1 ? j + 5.0 : 3.0) * P, k_lsa_update<<<G, kLsaBD, 0, c->st>>>(a));
+      }
       if (j >= 1) {  // x_{j-1} is ready: monitor it (the reference's iteration j-1)
         monitor(xout);
         read_scalars(c);

@@ -500,7 +500,9 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   // HD_SETUP_TRACE=1: wall time of the setup phases on stderr
   const bool trace = std::getenv("HD_SETUP_TRACE") && std::atoi(std::getenv("HD_SETUP_TRACE")) == 1;
   auto tlast = t0;
+  NvtxRange nvtx_create("hd_create");
   auto mark = [&](const char* what) {
+    nvtxMarkA(what);  // end of the setup phase `what`
     if (!trace) return;
     cudaDeviceSynchronize();
     const auto now = std::chrono::steady_clock::now();
