@@ -62,7 +62,10 @@ __device__ __forceinline__ void bt_fma(double2 a, double vr, double vi, double& 
 }
 
 // warps per CTA by the registers a row needs per lane (doubles per lane)
-__host__ __device__ constexpr int btri_threads(int regs) { return regs <= 16 ? 512 : (regs <= 32 ? 384 : 256); }
+#ifndef HD_BTRI_T32
+#define HD_BTRI_T32 384
+#endif
+__host__ __device__ constexpr int btri_threads(int regs) { return regs <= 16 ? 512 : (regs <= 32 ? HD_BTRI_T32 : 256); }
 
 struct BtriArgs {
   int n, q, m, nb, k;  // grid side, rows per block, block size m = q*n, blocks, middle block
