@@ -62,6 +62,9 @@ __device__ __forceinline__ void bt_fma(double2 a, double vr, double vi, double& 
 }
 
 // warps per CTA by the registers a row needs per lane (doubles per lane)
+// (round 2, C4, 24 doubles per lane: 256 / 320 / 384 / 512 / 640 / 768 threads give 27.6 / 26.3 / 25.9 / 28.3 /
+// 28.5 / 31.8 ms per solve; prefetching the rows of a warp's first TWO tasks across the barrier: 26.3 ms -- the
+// step time is the barrier and the dependent vector hand-over, not the rows' DRAM latency)
 #ifndef HD_BTRI_T32
 #define HD_BTRI_T32 384
 #endif
