@@ -43,7 +43,9 @@ struct RedOut {
 // OP_APPLYJ0: out = L x and out2 = omega D2^-1 (L x), D2 the diagonal of the
 // level with constant c2 (the A apply that feeds the V-cycle also takes the
 // first damped-Jacobi sweep of the shifted operator from the zero iterate)
-enum OpMode { OP_APPLY = 0, OP_RESID = 1, OP_JACOBI = 2, OP_RESNORM = 3, OP_APPLYJ0 = 4 };
+// OP_JACOBIP: the Jacobi sweep of x + Z e, e the coarse correction (linear prolongation applied on the
+// fly to the staged rows: the V-cycle's prolongation and its first post-smoothing sweep in one pass)
+enum OpMode { OP_APPLY = 0, OP_RESID = 1, OP_JACOBI = 2, OP_RESNORM = 3, OP_APPLYJ0 = 4, OP_JACOBIP = 5 };
 
 constexpr int kTX = 128;  // threads (columns) per stencil CTA
 constexpr int kNS = 8;    // cp.async ring depth (rows in flight per CTA)

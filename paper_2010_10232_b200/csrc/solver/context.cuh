@@ -212,6 +212,11 @@ struct hd_ctx {
   ExactSolver shift_exact;      // C_ex: exact inverse of the shifted operator (cycles == 0)
   double* sx_plan = nullptr;    // planar scratch for the 2D exact shifted solve
   std::vector<double2*> mg_b, mg_x, mg_y, mg_r;
+  // prolongation inside the first post-smoothing sweep (K4, OP_JACOBIP; HD_K4FUSE=1 at create).  Off by
+  // default: equal results, but the sweep's extra registers (170 at B = 3: two CTAs per SM instead of
+  // three) and per-row interpolation cost more than the saved launch and fine-vector round trip
+  // (C5 89.9 vs 88.6 ms, C3 2.58 vs 2.49 ms)
+  bool k4_fuse = false;
   bool j0_fuse = true;          // first Jacobi sweeps ride with their producers (HD_NOJ0FUSE=1 at create: off)
   int tail_l = -1;              // 1D: first level of the single-CTA tail V-cycle (tail1d.cuh), -1: none
   TailArgs tail{};

@@ -56,6 +56,7 @@ static double op_bytes(int mode, size_t NL) {
   switch (mode) {
     case OP_APPLY: return 2 * P;
     case OP_RESNORM: return 2 * P;
+    case OP_JACOBIP: return 3.25 * P;  // + the coarse correction, a quarter of a fine pass
     default: return 3 * P;
   }
 }
@@ -160,7 +161,7 @@ static const double2* tma_ct(hd_ctx* c, const LevelDev& L) {
 // kernel (its centre-value queue spills at two columns per lane).
 template <int MODE>
 static bool stencil_tma_ok(hd_ctx* c, const LevelDev& L, int rb, int re) {
-  return c->stencil_tma && MODE != OP_JACOBI && rb == 0 && re == L.n && L.n >= c->tma_min_n && L.b <= 6 &&
+  return c->stencil_tma && MODE != OP_JACOBI && MODE != OP_JACOBIP && rb == 0 && re == L.n && L.n >= c->tma_min_n && L.b <= 6 &&
          tma_encode_fn() != nullptr;
 }
 
@@ -227,7 +228,8 @@ static void launch_stencil_tma(hd_ctx* c, const LevelDev& L, const double2* x, c
 template <int B, int MODE>
 static void launch_stencil(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
                            double omega, RedOut red, const int* xidx, size_t xstride, int rb, int re,
-                           double2* out2 = nullptr, double2 c2 = double2{0.0, 0.0}) {
+                           double2* out2 = nullptr, double2 c2 = double2{0.0, 0.0}, const double2* ec = nullptr,
+                           int nc = 0) {
   if (stencil_tma_ok<MODE>(c, L, rb, re)) {
     launch_stencil_tma<B, MODE>(c, L, x, b, out, omega, red, xidx, xstride, out2, c2);
     return;
@@ -236,19 +238,20 @@ static void launch_stencil(hd_ctx* c, const LevelDev& L, const double2* x, const
   const int ry = pick_rows(L.n, re - rb, per * c->n_sms, B);
   dim3 grid((L.n + kSW * kSWarps - 1) / (kSW * kSWarps), (re - rb + ry - 1) / ry);
   k_stencil2d<B, MODE><<<grid, kSW * kSWarps, stencil_smem<B, MODE>(ry), c->st>>>(L, x, b, out, omega, ry, red,
-                                                                               xidx, xstride, rb, re, out2, c2);
+                                                                               xidx, xstride, rb, re, out2, c2, ec, nc);
 }
 
 template <int MODE>
 static void launch_op2d_mode(hd_ctx* c, const LevelDev& L, const double2* x, const double2* b, double2* out,
                              double omega, RedOut red, int kind, const int* xidx, size_t xstride, int rb = 0,
-                             int re = -1, double2* out2 = nullptr, double2 c2 = double2{0.0, 0.0}) {
+                             int re = -1, double2* out2 = nullptr, double2 c2 = double2{0.0, 0.0},
+                             const double2* ec = nullptr, int nc = 0) {
   if (re < 0) re = L.n;
   const size_t mk = prof_mark(c);
   g_launch_line = __LINE__ + 1000 * MODE;
   switch (L.b) {
 #define HD_CASE(BB) \
-  case BB: launch_stencil<BB, MODE>(c, L, x, b, out, omega, red, xidx, xstride, rb, re, out2, c2); break;
+  case BB: launch_stencil<BB, MODE>(c, L, x, b, out, omega, red, xidx, xstride, rb, re, out2, c2, ec, nc); break;
     HD_CASE(1) HD_CASE(2) HD_CASE(3) HD_CASE(4) HD_CASE(5) HD_CASE(6)
 #undef HD_CASE
     default: throw Error(HD_ERR_INVALID, "band half-width " + std::to_string(L.b) + " unsupported");
@@ -650,12 +653,20 @@ static LevelDev levM(hd_ctx* c, int l) {
 
 // x_out = (damped Jacobi)^steps from x (x_zero: x == 0), ping-pong through tmp
 // x0_ready: xa already holds the first sweep from zero (fused into the producer of b)
+// ec (with its grid side nc): the coarse correction still to be prolonged onto x; the first sweep
+// then runs on x + Z ec without storing it (OP_JACOBIP)
 static double2* smooth(hd_ctx* c, int l, const double2* b, double2* xa, double2* xb, bool x_zero, int steps,
-                       bool x0_ready = false) {
+                       bool x0_ready = false, const double2* ec = nullptr, int nc = 0) {
   const LevelDev L = levM(c, l);
   double2* cur = xa;
   double2* oth = xb;
   int s = 0;
+  if (ec) {  // caller guarantees steps >= 1 and a 2D Kronecker-sum level
+    launch_op2d_mode<OP_JACOBIP>(c, L, cur, b, oth, c->spec.omega, red_of(c), L.n == c->n ? HD_K_OP_FINE : HD_K_OP_COARSE,
+                                 nullptr, 0, 0, -1, nullptr, double2{0.0, 0.0}, ec, nc);
+    std::swap(cur, oth);
+    s = 1;
+  }
   if (x_zero) {
     if (steps == 0) {
       CK(cudaMemsetAsync(cur, 0, lsize(c, L.n) * sizeof(double2), c->st));
@@ -716,6 +727,9 @@ static double2* cycle_at(hd_ctx* c, int l, const double2* b, bool x_zero, bool x
     else restrict_(c, Stencil{0, 0.0}, c->mg_r[l], nf, ncl, c->mg_b[l + 1], nullptr);
   }
   double2* ec = cycle_at(c, l + 1, c->mg_b[l + 1], true, fuse);
+  // prolongation + first post-smoothing sweep in one pass (K4) on 2D Kronecker-sum levels
+  if (c->k4_fuse && c->dim == 2 && !L.gen && c->spec.smooth_steps >= 1 && L.b <= 6)
+    return smooth(c, l, b, xcur, xoth, false, c->spec.smooth_steps, false, ec, ncl);
   prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, nf, ncl, nullptr, xcur);
   double2* res = smooth(c, l, b, xcur, xoth, false, c->spec.smooth_steps);
   return res;
@@ -770,8 +784,12 @@ static const double2* mg_solve_ptr(hd_ctx* c, const double2* b, double2* out, bo
         restrict_(c, Stencil{0, 0.0}, c->mg_r[0], c->lev[0].n, c->lev[1].n, c->mg_b[1], nullptr);
       }
       double2* ec = cycle_at(c, 1, c->mg_b[1], true);
-      prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, c->lev[0].n, c->lev[1].n, nullptr, xcur);
-      xb = smooth(c, 0, b, xcur, xoth, false, c->spec.smooth_steps);
+      if (c->k4_fuse && c->dim == 2 && !L.gen && c->spec.smooth_steps >= 1 && L.b <= 6) {
+        xb = smooth(c, 0, b, xcur, xoth, false, c->spec.smooth_steps, false, ec, c->lev[1].n);
+      } else {
+        prolong_<0>(c, Stencil{0, 0.0}, ec, nullptr, c->lev[0].n, c->lev[1].n, nullptr, xcur);
+        xb = smooth(c, 0, b, xcur, xoth, false, c->spec.smooth_steps);
+      }
     }
     zero = false;
   }

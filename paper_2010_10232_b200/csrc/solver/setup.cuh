@@ -512,6 +512,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   std::unique_ptr<hd_ctx, void (*)(hd_ctx*)> c(new hd_ctx(), destroy_ctx);
   c->device = (devices && n_devices == 1) ? devices[0] : 0;
   c->j0_fuse = std::getenv("HD_NOJ0FUSE") == nullptr;
+  c->k4_fuse = std::getenv("HD_K4FUSE") && std::atoi(std::getenv("HD_K4FUSE")) == 1;
   c->stencil_tma = !(std::getenv("HD_STENCIL_TMA") && std::atoi(std::getenv("HD_STENCIL_TMA")) == 0);
   if (std::getenv("HD_STENCIL_TMA_MIN")) c->tma_min_n = std::atoi(std::getenv("HD_STENCIL_TMA_MIN"));
   c->lsa_rev = !(std::getenv("HD_LSA_REV") && std::atoi(std::getenv("HD_LSA_REV")) == 0);

@@ -16,7 +16,10 @@
 // host so that the tile count fills whole waves of resident CTAs.
 //
 // Modes: APPLY y; APPLYJ0 y and omega D2^-1 y; RESID b - y; JACOBI x + omega D^-1 (b - y); RESNORM
-// ||b - y||^2 (deterministic grid reduction, no write).
+// ||b - y||^2 (deterministic grid reduction, no write); JACOBIP: JACOBI of x + Z e (src/precond.cpp:151-152
+// in one pass): the warp also stages the rows of the coarse correction e that its fine rows interpolate
+// from and adds the linear prolongation (k_prolong2d's arithmetic: y then x, weights 1/2, 1/2 | 1) to
+// every staged row before its x pass, so x + Z e is never stored.
 #pragma once
 
 #include "kernels.cuh"
@@ -26,6 +29,8 @@ namespace hd {
 constexpr int kSW = 32;      // columns per warp
 constexpr int kSWarps = 4;   // warps per CTA
 constexpr int kSRowsMax = 128;
+constexpr int kSCR = 16;     // JACOBIP: coarse rows in a warp's ring (>= (ring depth)/2 + 2)
+constexpr int kSCW = 24;     // JACOBIP: coarse columns a warp's 32 + 2B fine columns interpolate from (B <= 6)
 
 // ring depth (rows in flight per warp): the band height 2B+1 if that is >= 7,
 // else its smallest multiple >= 8, so that the row loop unrolled over one ring period addresses
@@ -42,7 +47,8 @@ __host__ __device__ constexpr int stencil_ring() {
 template <int B, int MODE>
 __host__ __device__ constexpr size_t stencil_smem(int ry) {
   return sizeof(double2) * ((size_t)kSWarps * stencil_ring<B>() * ((kSW + 2 * B) + (MODE != OP_APPLY && MODE != OP_APPLYJ0 ? kSW : 0)) +
-                            (size_t)(ry + 4 * B + 1) * (2 * B + 1));
+                            (size_t)(ry + 4 * B + 1) * (2 * B + 1) +
+                            (MODE == OP_JACOBIP ? (size_t)kSWarps * (kSCR + 1) * kSCW : 0));
 }
 
 #ifndef HD_STENCIL_MINB
@@ -54,11 +60,13 @@ __global__ void __launch_bounds__(kSW * kSWarps, HD_STENCIL_MINB) k_stencil2d(Le
                                                             const double2* __restrict__ bv,
                                                             double2* __restrict__ out, double omega, int RY,
                                                             RedOut red, const int* xidx, size_t xstride, int rb,
-                                                            int re, double2* __restrict__ out2, double2 c2) {
+                                                            int re, double2* __restrict__ out2, double2 c2,
+                                                            const double2* __restrict__ ec = nullptr, int nc = 0) {
   constexpr int NB = 2 * B + 1;
   constexpr int W = kSW + 2 * B;
   constexpr int kSRing = stencil_ring<B>();
   constexpr bool NEED_B = MODE != OP_APPLY && MODE != OP_APPLYJ0;
+  constexpr bool JAC = MODE == OP_JACOBI || MODE == OP_JACOBIP;
   if (xidx) x += (size_t)(*xidx) * xstride;  // graph mode: x = V + j N
   extern __shared__ __align__(16) double2 dsm[];
   double2(*ring)[kSRing][W] = reinterpret_cast<double2(*)[kSRing][W]>(dsm);
@@ -78,6 +86,16 @@ __global__ void __launch_bounds__(kSW * kSWarps, HD_STENCIL_MINB) k_stencil2d(Le
   const int nin = nout + 2 * B;
   const int ix = x0 + lane;
   const bool colv = ix < n;
+  // JACOBIP: this warp's ring of coarse rows (slot q & (kSCR-1), columns cq0 .. cq0 + kSCW - 1) and one
+  // row of y-interpolated coarse values; they sit behind the (My, Sy) table of the tallest strip
+  double2(*cr)[kSCW] = nullptr;
+  double2* tyr = nullptr;
+  const int cq0 = (x0 >> 1) + ((-B - 1) >> 1);  // floor((x0 - B - 1) / 2): x0 is a multiple of 32
+  if (MODE == OP_JACOBIP) {
+    double2* cbase = cy + (size_t)(RY + 4 * B + 1) * NB + (size_t)warp * (kSCR + 1) * kSCW;
+    cr = reinterpret_cast<double2(*)[kSCW]>(cbase);
+    tyr = cbase + kSCR * kSCW;
+  }
 
   // (My, Sy) band rows of output rows o = -2B .. nout+2B-1 of the strip,
   // zero outside [0, nout): accumulation into out-of-strip rows is a no-op
@@ -117,6 +135,18 @@ __global__ void __launch_bounds__(kSW * kSWarps, HD_STENCIL_MINB) k_stencil2d(Le
         cp_async16(&bring[warp][sl][lane], v ? pb : bv, v);
         pb += n;
       }
+      if (MODE == OP_JACOBIP && lane < kSCW) {
+        // fine row rl interpolates from the coarse rows (rl-1)>>1 and rl>>1: a new one appears at even rl
+        // (the strip's first row brings both); rows and columns outside the coarse grid are zero
+        const int qc = cq0 + lane;
+        const bool cv = qc >= 0 && qc < nc;
+        auto cload = [&](int q) {
+          const bool v = cv && q >= 0 && q < nc;
+          cp_async16(&cr[q & (kSCR - 1)][lane], v ? ec + (size_t)q * nc + qc : ec, v);
+        };
+        if (rl == y0 - B && (rl & 1) == 0) cload((rl - 1) >> 1);
+        if (rl == y0 - B || (rl & 1) == 0) cload(rl >> 1);
+      }
       pA += n;
       pB += n;
       ++rl;
@@ -145,6 +175,27 @@ __global__ void __launch_bounds__(kSW * kSWarps, HD_STENCIL_MINB) k_stencil2d(Le
           __syncwarp();
           if (k + kSRing - 1 < nin) load((t + kSRing - 1) % kSRing);
           cp_async_commit();
+          if (MODE == OP_JACOBIP) {  // rg[s] += (Z e)(row, .): y interpolation into tyr, then x
+            const int rk = y0 - B + k;
+            if (rk >= 0 && rk < n) {  // warp-uniform
+              if (lane < kSCW) {
+                const double2 cb = cr[(rk >> 1) & (kSCR - 1)][lane];
+                tyr[lane] = (rk & 1) ? cb : cfma_r(0.5, cr[((rk - 1) >> 1) & (kSCR - 1)][lane], cscale(0.5, cb));
+              }
+              __syncwarp();
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int e = h * kSW + lane;
+                const int fx = x0 - B + e;
+                if ((h == 0 || lane < 2 * B) && fx >= 0 && fx < n) {
+                  const int li = (fx >> 1) - cq0;
+                  const double2 pz = (fx & 1) ? tyr[li] : cfma_r(0.5, tyr[li - 1], cscale(0.5, tyr[li]));
+                  rg[s][e] = cadd(rg[s][e], pz);
+                }
+              }
+            }
+            __syncwarp();
+          }
           double2 u0 = cmk(0.0, 0.0), u1 = cmk(0.0, 0.0), v0 = cmk(0.0, 0.0), v1 = cmk(0.0, 0.0);
 #pragma unroll
           for (int j = 0; j < NB; ++j) {
@@ -159,7 +210,7 @@ __global__ void __launch_bounds__(kSW * kSWarps, HD_STENCIL_MINB) k_stencil2d(Le
           }
           const double2 v = cadd(v0, v1);
           const double2 Pk = csub(cadd(u0, u1), cmul(c, v));
-          if (MODE == OP_JACOBI) XC[(t + 1 + B) % NB] = rg[s][lane + B];  // centre of output k - B
+          if (JAC) XC[(t + 1 + B) % NB] = rg[s][lane + B];  // centre of output k - B
 #pragma unroll
           for (int d = 0; d < NB; ++d) {
             // output o = k - 2B + d takes row k with its band offset 2B - d

@@ -198,3 +198,31 @@ def test_tensor_copy_stencil_is_bit_identical(monkeypatch, ne, p, k):
     assert ra.iterations == rb.iterations and ra.converged and rb.converged
     assert np.max(np.abs(np.array(ra.residuals) - np.array(rb.residuals))) <= 1e-13
     assert _rel(ra.solution, rb.solution) <= 1e-12
+
+
+@pytest.mark.parametrize("ne,p,k,kw", [(130, 3, 80.0, {}), (200, 2, 100.0, {}), (97, 4, 50.0, {}), (75, 1, 30.0, {}),
+                                       (66, 5, 30.0, {}), (96, 3, 50.0, dict(cycles=2, smoothing=2)),
+                                       (80, 2, 40.0, dict(tag="Deps_C_MG", beta2="4.2", cycles=3, smoothing=3, omega=0.6))])
+def test_prolongation_in_post_smoothing_matches_separate_launches(monkeypatch, ne, p, k, kw):
+    """K4: the V-cycle's prolongation x += Z e rides inside the
+    first post-smoothing sweep (OP_JACOBIP: the staged rows of x get the linear
+    interpolation of e added before the x pass, k_prolong2d's arithmetic), so
+    x + Z e is never stored.  Against the separate prolongation + Jacobi
+    launches (the default; the fused sweep is opt-in, HD_K4FUSE=1, because it
+    measured slower: DESIGN.md §6): V-cycle, composed operator and whole solves
+    equal (numerically identical arithmetic; only signed zeros may differ)."""
+    s = hd.assemble(hd.point_source_2d(ne, p, k))
+    args = dict(BASE)
+    tag = kw.pop("tag", "DC_MG") if "tag" in kw else "DC_MG"
+    args.update(kw)
+    spec = hd.to_spec(tag, p, k, **args)
+    b, a = _pair(monkeypatch, "HD_K4FUSE", s, spec)
+    x = _rand(s.size, 13)
+    with a, b:
+        for which in (hd.HD_APPLY_MG, hd.HD_APPLY_OP):
+            assert np.array_equal(_apply(a, which, x), _apply(b, which, x)), which
+        ra = a.solve(hd.GmresOptions(100, 1e-7))
+        rb = b.solve(hd.GmresOptions(100, 1e-7))
+    assert (ra.iterations, ra.converged) == (rb.iterations, rb.converged)
+    assert ra.residuals == rb.residuals
+    assert np.array_equal(ra.solution, rb.solution)
