@@ -230,9 +230,11 @@ static void launch_stencil(hd_ctx* c, const LevelDev& L, const double2* x, const
                            double omega, RedOut red, const int* xidx, size_t xstride, int rb, int re,
                            double2* out2 = nullptr, double2 c2 = double2{0.0, 0.0}, const double2* ec = nullptr,
                            int nc = 0) {
-  if (stencil_tma_ok<MODE>(c, L, rb, re)) {
-    launch_stencil_tma<B, MODE>(c, L, x, b, out, omega, red, xidx, xstride, out2, c2);
-    return;
+  if constexpr (MODE != OP_JACOBI && MODE != OP_JACOBIP) {  // (the Jacobi modes have no tensor-copy instantiation)
+    if (stencil_tma_ok<MODE>(c, L, rb, re)) {
+      launch_stencil_tma<B, MODE>(c, L, x, b, out, omega, red, xidx, xstride, out2, c2);
+      return;
+    }
   }
   const int per = stencil_occupancy<B, MODE>();
   const int ry = pick_rows(L.n, re - rb, per * c->n_sms, B);
