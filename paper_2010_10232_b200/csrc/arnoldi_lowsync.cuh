@@ -211,6 +211,130 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// pass 1 as a tall-skinny FP64 tensor-core GEMM (HD_LSA_MMA=1).  All dots of
+// an iteration are one contraction over the N elements,
+//
+//   [ s_i , G_ji ] = sum_e  conj(u_i[e]) w[e] ,  conj(u_j[e]) u_i[e]      (i = 0 .. j),
+//
+// i.e. C = A B with A the basis as a real (j+1) x 2N matrix (re, im interleaved,
+// exactly its memory layout) and B a 2N x 4 matrix built from w and u_j:
+//   col 0 (Re s): [wr, wi]   col 1 (Im s): [wi, -wr]   col 2 (Re G): [ur, ui]   col 3 (Im G): [-ui, ur]
+// mma.sync.m8n8k4.f64 (DMMA) takes 8 basis vectors x 4 values of K per
+// instruction: lane (r = lane/4, q = lane%4) feeds A[r][q] and B[q][r]; the 8 x 8
+// accumulator (2 doubles per lane per group of 8 vectors) stays in registers
+// over the warp's whole share of N, so there is NO per-chunk reduction, no
+// shared-memory staging of w / u_j and no block barrier in the loop: the warp
+// loads, the tensor core multiplies and sums.  A warp walks tiles of kMmaTE
+// elements; per tile it builds its B fragments once and streams the groups of
+// 8 vectors against them.  The per-CTA and grid reductions at the end are the
+// fixed-order ones of k_lsa_dots (same partial slots, same finishing step).
+//
+// Measured at C5 (round 2): correct (tests/test_gpu_switches.py) and SLOWER --
+// both passes 52 ms per solve against 24.8 ms for k_lsa_dots' pass 1 (the
+// solve 114.6 vs 88.7 ms).  The 72 accumulator registers of up to 18 vector
+// groups leave one CTA of 8 warps per SM (238-252 registers), and each warp
+// alternates a load phase (8 KB in flight) with a DMMA phase; 8-byte loads
+// (106 ms), 16-byte loads with the permuted K index (114.6 ms) and eight short
+// DMMA chains instead of two long ones (116 ms) all land there: what is
+// missing is bytes in flight, which registers cannot buy here.  Opt-in.
+// ---------------------------------------------------------------------------
+constexpr int kMmaTE = 32;                       // complex elements per warp tile (16 k4 steps)
+constexpr int kMmaKS = kMmaTE / 2;               // DMMA steps per tile
+constexpr int kMmaNG = ((kLsaMaxJ + 1 + 7) / 8 + 1) / 2 * 2;  // groups of 8 basis vectors (even: streamed in pairs)
+
+__device__ __forceinline__ void lsa_dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kLsaBD, 1) k_lsa_dots_mma(LsaArgs a) {
+  constexpr int NW = kLsaBD / 32;
+  __shared__ double2 acc[2 * kLsaMaxJ + 2];  // [0..j]: s_i ; [kLsaMaxJ+1 ..]: G_ji  (k_lsa_dots' slots)
+  __shared__ double2 sh_s[kLsaMaxJ + 1];
+  __shared__ double2 sh_lj[kLsaMaxJ];
+  __shared__ double2 hsm[kLsaMaxJ + 1];
+  if (a.done && *((volatile const int*)a.done)) return;
+  const int j = a.dj ? *a.dj : a.j;
+  const int nd = j + 1, ng = (nd + 7) >> 3;
+  const int nslot = 2 * kLsaMaxJ + 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  for (int t = threadIdx.x; t < nslot; t += kLsaBD) acc[t] = cmk(0.0, 0.0);
+  const size_t N = a.N;
+  // The contraction index may be permuted freely as long as A and B agree: a lane loads one whole complex
+  // element (16 bytes; the four lanes of a vector read 64 contiguous bytes) and feeds its real part to one
+  // DMMA step and its imaginary part to the next.  B operand of this lane (K row q -> element e0 + 4 t + q,
+  // column r): from w (r = 0, 1) or u_j (r = 2, 3), columns 4..7 are zero:
+  //   "re" step: wr, wi, ur, -ui      "im" step: wi, -wr, ui, ur
+  const double2* bsrc = r < 2 ? a.w : a.U + (size_t)j * N;
+  const bool buse = r < 4;
+  double C[kMmaNG][2];
+#pragma unroll
+  for (int g = 0; g < kMmaNG; ++g) C[g][0] = C[g][1] = 0.0;
+  constexpr int NT = kMmaTE / 4;  // element quads per tile
+  const size_t ntiles = (N + kMmaTE - 1) / kMmaTE;
+  for (size_t tile = (size_t)blockIdx.x * NW + warp; tile < ntiles; tile += (size_t)gridDim.x * NW) {
+    const size_t e0 = tile * kMmaTE + q;  // this lane's element of quad 0
+    double bre[NT], bim[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const size_t e = e0 + 4 * t;
+      const double2 v = (buse && e < N) ? __ldg(bsrc + e) : cmk(0.0, 0.0);
+      bre[t] = r == 0 ? v.x : (r == 1 ? v.y : (r == 2 ? v.x : -v.y));
+      bim[t] = r == 0 ? v.y : (r == 1 ? -v.x : (r == 2 ? v.y : v.x));
+    }
+    // two groups of 8 vectors per step: 2 NT 16-byte loads in flight per lane, two independent DMMA chains
+#pragma unroll
+    for (int g = 0; g < kMmaNG; g += 2) {
+      if (g < ng) {  // warp-uniform
+        const int i0 = 8 * g + r, i1 = i0 + 8;
+        const bool v0 = i0 <= j, v1 = i1 <= j;
+        const double2* up0 = a.U + (size_t)(v0 ? i0 : 0) * N + e0;
+        const double2* up1 = a.U + (size_t)(v1 ? i1 : 0) * N + e0;
+        double2 a0[NT], a1[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const bool in = e0 + 4 * t < N;
+          a0[t] = (v0 && in) ? __ldg(up0 + 4 * t) : cmk(0.0, 0.0);
+          a1[t] = (v1 && in) ? __ldg(up1 + 4 * t) : cmk(0.0, 0.0);
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          lsa_dmma(C[g], a0[t].x, bre[t]);
+          lsa_dmma(C[g + 1], a1[t].x, bre[t]);
+          lsa_dmma(C[g], a0[t].y, bim[t]);
+          lsa_dmma(C[g + 1], a1[t].y, bim[t]);
+        }
+      }
+    }
+  }
+  // CTA sums in warp order (fixed => deterministic): C[g] of lane (r, q): q = 0 -> s_i, q = 1 -> G_ji, i = 8 g + r
+  __syncthreads();
+  for (int wq = 0; wq < NW; ++wq) {
+    if (warp == wq && q < 2) {
+#pragma unroll
+      for (int g = 0; g < kMmaNG; ++g) {
+        const int i = 8 * g + r;
+        if (g < ng && i <= j) {
+          if (q == 0) acc[i] = cadd(acc[i], cmk(C[g][0], C[g][1]));
+          else if (i < j) acc[kLsaMaxJ + 1 + i] = cadd(acc[kLsaMaxJ + 1 + i], cmk(C[g][0], C[g][1]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < nslot; t += kLsaBD) {
+    const bool used = t < nd || (t >= kLsaMaxJ + 1 && t < kLsaMaxJ + 1 + j);
+    if (used) a.partials[(size_t)(a.part_offset + blockIdx.x) * nslot + t] = acc[t];
+  }
+  if (a.partial_only) return;
+  if (!lsa_last_block(a.counter)) return;
+  lsa_dots_finish(a, j, gridDim.x, sh_s, sh_lj, hsm);
+  if (threadIdx.x == 0) *a.counter = 0u;
+}
+
+// ---------------------------------------------------------------------------
 // pass 1 on the Blackwell bulk-copy engine (HD_LSA_TMA=1; default: k_lsa_dots).
 // One CTA per SM, 8 warps.  The CTA's chunks of w and u_j (kTCE elements) go
 // through a 3-deep ring of cp.async.bulk copies issued by thread 0 and

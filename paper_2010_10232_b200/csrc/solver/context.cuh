@@ -266,6 +266,7 @@ struct hd_ctx {
   };
   std::map<TmaKey, CUtensorMap> tma_maps;
   bool lsa_rev = true;          // HD_LSA_REV=0 at create: pass 2 walks the vectors front to back (A/B of the L2 reuse)
+  bool lsa_mma = false;         // HD_LSA_MMA=1 at create: pass 1 as an FP64 tensor-core GEMM (k_lsa_dots_mma)
   bool lsa_tma = false;         // HD_LSA_TMA=1 at create: pass 1 on the bulk-copy ring (k_lsa_dots_tma)
   size_t lsa_givens_smem = 0;
   // graph-resident GMRES loop (WHILE conditional node), rebuilt when (maxit, tol) change

@@ -907,7 +907,9 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
 // (HD_LSA_TMA=1 at create) the bulk-copy ring kernel -- equal at C5 (48.6 vs
 // 48.3 ms for both passes over a solve), so the round-1 kernel stays the default
 static void launch_lsa_dots(hd_ctx* c, const LsaArgs& a, int G, cudaStream_t st) {
-  if (c->lsa_tma) {
+  if (c->lsa_mma) {  // one CTA per SM (never more CTAs than the partials buffer has slots)
+    k_lsa_dots_mma<<<std::min(c->n_sms, G), kLsaBD, 0, st>>>(a);
+  } else if (c->lsa_tma) {
     smem_optin(reinterpret_cast<const void*>(k_lsa_dots_tma), lsa_tma_smem());
     // one CTA per SM, never more CTAs than the partials buffer has slots (lsa_G)
     k_lsa_dots_tma<<<std::min(c->n_sms, G), kTNW * 32, lsa_tma_smem(), st>>>(a);

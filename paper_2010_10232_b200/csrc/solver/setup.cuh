@@ -516,6 +516,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   c->stencil_tma = !(std::getenv("HD_STENCIL_TMA") && std::atoi(std::getenv("HD_STENCIL_TMA")) == 0);
   if (std::getenv("HD_STENCIL_TMA_MIN")) c->tma_min_n = std::atoi(std::getenv("HD_STENCIL_TMA_MIN"));
   c->lsa_rev = !(std::getenv("HD_LSA_REV") && std::atoi(std::getenv("HD_LSA_REV")) == 0);
+  c->lsa_mma = std::getenv("HD_LSA_MMA") && std::atoi(std::getenv("HD_LSA_MMA")) == 1;
   c->lsa_tma = std::getenv("HD_LSA_TMA") && std::atoi(std::getenv("HD_LSA_TMA")) == 1;
   if (!devices || n_devices == 0) CK(cudaGetDevice(&c->device));
   CK(cudaSetDevice(c->device));

@@ -22,6 +22,8 @@ SWITCHES = [
     ("2d_p2", "HD_DGEMM", "dmma"),
     ("2d_p3", "HD_NOFUSE", "1"),        # separate operator and restriction launches vs the fused K3/K6 kernels
     ("2d_p2", "HD_NOFUSE", "1"),
+    ("2d_p3", "HD_LSA_MMA", "1"),       # Arnoldi pass 1 as an FP64 tensor-core GEMM (k_lsa_dots_mma)
+    ("2d_p2", "HD_LSA_MMA", "1"),
     ("2d_p3", "HD_LSA_REV", "0"),       # pass 2 front to back
     ("2d_p3", "HD_ARNOLDI", "0"),       # exact-order MGS engine vs the one-reduction form
     ("2d_p3", "HD_ESOLVE", "fd"),       # unfolded fast diagonalisation of E
