@@ -18,6 +18,8 @@
 // last CTA to finish sums the per-CTA partials in index order.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (type only)
+
 #include "device_common.cuh"
 
 namespace hd {
@@ -203,130 +205,6 @@ __global__ void __launch_bounds__(kLsaBD, 2) k_lsa_dots(LsaArgs a) {
       for (int h = 1; h < kLsaSplit; ++h) v = cadd(v, acc[h * nslot + q]);
       a.partials[(size_t)(a.part_offset + blockIdx.x) * nslot + q] = v;
     }
-  }
-  if (a.partial_only) return;
-  if (!lsa_last_block(a.counter)) return;
-  lsa_dots_finish(a, j, gridDim.x, sh_s, sh_lj, hsm);
-  if (threadIdx.x == 0) *a.counter = 0u;
-}
-
-// ---------------------------------------------------------------------------
-// pass 1 as a tall-skinny FP64 tensor-core GEMM (HD_LSA_MMA=1).  All dots of
-// an iteration are one contraction over the N elements,
-//
-//   [ s_i , G_ji ] = sum_e  conj(u_i[e]) w[e] ,  conj(u_j[e]) u_i[e]      (i = 0 .. j),
-//
-// i.e. C = A B with A the basis as a real (j+1) x 2N matrix (re, im interleaved,
-// exactly its memory layout) and B a 2N x 4 matrix built from w and u_j:
-//   col 0 (Re s): [wr, wi]   col 1 (Im s): [wi, -wr]   col 2 (Re G): [ur, ui]   col 3 (Im G): [-ui, ur]
-// mma.sync.m8n8k4.f64 (DMMA) takes 8 basis vectors x 4 values of K per
-// instruction: lane (r = lane/4, q = lane%4) feeds A[r][q] and B[q][r]; the 8 x 8
-// accumulator (2 doubles per lane per group of 8 vectors) stays in registers
-// over the warp's whole share of N, so there is NO per-chunk reduction, no
-// shared-memory staging of w / u_j and no block barrier in the loop: the warp
-// loads, the tensor core multiplies and sums.  A warp walks tiles of kMmaTE
-// elements; per tile it builds its B fragments once and streams the groups of
-// 8 vectors against them.  The per-CTA and grid reductions at the end are the
-// fixed-order ones of k_lsa_dots (same partial slots, same finishing step).
-//
-// Measured at C5 (round 2): correct (tests/test_gpu_switches.py) and SLOWER --
-// both passes 52 ms per solve against 24.8 ms for k_lsa_dots' pass 1 (the
-// solve 114.6 vs 88.7 ms).  The 72 accumulator registers of up to 18 vector
-// groups leave one CTA of 8 warps per SM (238-252 registers), and each warp
-// alternates a load phase (8 KB in flight) with a DMMA phase; 8-byte loads
-// (106 ms), 16-byte loads with the permuted K index (114.6 ms) and eight short
-// DMMA chains instead of two long ones (116 ms) all land there: what is
-// missing is bytes in flight, which registers cannot buy here.  Opt-in.
-// ---------------------------------------------------------------------------
-constexpr int kMmaTE = 32;                       // complex elements per warp tile (16 k4 steps)
-constexpr int kMmaKS = kMmaTE / 2;               // DMMA steps per tile
-constexpr int kMmaNG = ((kLsaMaxJ + 1 + 7) / 8 + 1) / 2 * 2;  // groups of 8 basis vectors (even: streamed in pairs)
-
-__device__ __forceinline__ void lsa_dmma(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
-}
-
-__global__ void __launch_bounds__(kLsaBD, 1) k_lsa_dots_mma(LsaArgs a) {
-  constexpr int NW = kLsaBD / 32;
-  __shared__ double2 acc[2 * kLsaMaxJ + 2];  // [0..j]: s_i ; [kLsaMaxJ+1 ..]: G_ji  (k_lsa_dots' slots)
-  __shared__ double2 sh_s[kLsaMaxJ + 1];
-  __shared__ double2 sh_lj[kLsaMaxJ];
-  __shared__ double2 hsm[kLsaMaxJ + 1];
-  if (a.done && *((volatile const int*)a.done)) return;
-  const int j = a.dj ? *a.dj : a.j;
-  const int nd = j + 1, ng = (nd + 7) >> 3;
-  const int nslot = 2 * kLsaMaxJ + 2;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = lane >> 2, q = lane & 3;
-  for (int t = threadIdx.x; t < nslot; t += kLsaBD) acc[t] = cmk(0.0, 0.0);
-  const size_t N = a.N;
-  // The contraction index may be permuted freely as long as A and B agree: a lane loads one whole complex
-  // element (16 bytes; the four lanes of a vector read 64 contiguous bytes) and feeds its real part to one
-  // DMMA step and its imaginary part to the next.  B operand of this lane (K row q -> element e0 + 4 t + q,
-  // column r): from w (r = 0, 1) or u_j (r = 2, 3), columns 4..7 are zero:
-  //   "re" step: wr, wi, ur, -ui      "im" step: wi, -wr, ui, ur
-  const double2* bsrc = r < 2 ? a.w : a.U + (size_t)j * N;
-  const bool buse = r < 4;
-  double C[kMmaNG][2];
-#pragma unroll
-  for (int g = 0; g < kMmaNG; ++g) C[g][0] = C[g][1] = 0.0;
-  constexpr int NT = kMmaTE / 4;  // element quads per tile
-  const size_t ntiles = (N + kMmaTE - 1) / kMmaTE;
-  for (size_t tile = (size_t)blockIdx.x * NW + warp; tile < ntiles; tile += (size_t)gridDim.x * NW) {
-    const size_t e0 = tile * kMmaTE + q;  // this lane's element of quad 0
-    double bre[NT], bim[NT];
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const size_t e = e0 + 4 * t;
-      const double2 v = (buse && e < N) ? __ldg(bsrc + e) : cmk(0.0, 0.0);
-      bre[t] = r == 0 ? v.x : (r == 1 ? v.y : (r == 2 ? v.x : -v.y));
-      bim[t] = r == 0 ? v.y : (r == 1 ? -v.x : (r == 2 ? v.y : v.x));
-    }
-    // two groups of 8 vectors per step: 2 NT 16-byte loads in flight per lane, two independent DMMA chains
-#pragma unroll
-    for (int g = 0; g < kMmaNG; g += 2) {
-      if (g < ng) {  // warp-uniform
-        const int i0 = 8 * g + r, i1 = i0 + 8;
-        const bool v0 = i0 <= j, v1 = i1 <= j;
-        const double2* up0 = a.U + (size_t)(v0 ? i0 : 0) * N + e0;
-        const double2* up1 = a.U + (size_t)(v1 ? i1 : 0) * N + e0;
-        double2 a0[NT], a1[NT];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const bool in = e0 + 4 * t < N;
-          a0[t] = (v0 && in) ? __ldg(up0 + 4 * t) : cmk(0.0, 0.0);
-          a1[t] = (v1 && in) ? __ldg(up1 + 4 * t) : cmk(0.0, 0.0);
-        }
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          lsa_dmma(C[g], a0[t].x, bre[t]);
-          lsa_dmma(C[g + 1], a1[t].x, bre[t]);
-          lsa_dmma(C[g], a0[t].y, bim[t]);
-          lsa_dmma(C[g + 1], a1[t].y, bim[t]);
-        }
-      }
-    }
-  }
-  // CTA sums in warp order (fixed => deterministic): C[g] of lane (r, q): q = 0 -> s_i, q = 1 -> G_ji, i = 8 g + r
-  __syncthreads();
-  for (int wq = 0; wq < NW; ++wq) {
-    if (warp == wq && q < 2) {
-#pragma unroll
-      for (int g = 0; g < kMmaNG; ++g) {
-        const int i = 8 * g + r;
-        if (g < ng && i <= j) {
-          if (q == 0) acc[i] = cadd(acc[i], cmk(C[g][0], C[g][1]));
-          else if (i < j) acc[kLsaMaxJ + 1 + i] = cadd(acc[kLsaMaxJ + 1 + i], cmk(C[g][0], C[g][1]));
-        }
-      }
-    }
-    __syncthreads();
-  }
-  for (int t = threadIdx.x; t < nslot; t += kLsaBD) {
-    const bool used = t < nd || (t >= kLsaMaxJ + 1 && t < kLsaMaxJ + 1 + j);
-    if (used) a.partials[(size_t)(a.part_offset + blockIdx.x) * nslot + t] = acc[t];
   }
   if (a.partial_only) return;
   if (!lsa_last_block(a.counter)) return;
@@ -562,6 +440,208 @@ __device__ void lsa_dots_finish(const LsaArgs& a, int j, int nparts, double2* sh
       __syncwarp();
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// pass 1 as a tall-skinny FP64 tensor-core GEMM fed by the bulk-copy engine
+// (HD_LSA_MMA=1).  All dots of an iteration are one contraction over the N
+// elements,
+//
+//   [ s_i , G_ji ] = sum_e  conj(u_i[e]) w[e] ,  conj(u_j[e]) u_i[e]      (i = 0 .. j),
+//
+// i.e. C = A B with A the basis as a real (j+1) x 2N matrix (exactly its memory
+// layout) and B a 2N x 4 matrix built from w and u_j.  mma.sync.m8n8k4.f64
+// (DMMA) takes 8 basis vectors x 4 values of K per instruction: lane
+// (r = lane/4, q = lane%4) feeds A[r][q] and B[q][r], and the 8 x 8 accumulator
+// (2 doubles per lane per group of 8 vectors) stays in registers over the
+// warp's whole share of N: no per-chunk reduction and no block barrier in the
+// loop.  The contraction index may be permuted freely as long as A and B
+// agree, so a lane takes one whole complex element (16 bytes) of its vector
+// and feeds its real part to one DMMA step and its imaginary part to the next:
+//   "re" step B column r: wr, wi, ur, -ui      "im" step: wi, -wr, ui, ur     (r = 0..3; 4..7 zero).
+// Every warp is its own pipeline: a unit is (tile of kMmaTE elements, group of
+// 8 vectors) = an 8-row box of the basis seen as a 2D tensor (2N doubles x
+// vectors), fetched by ONE cp.async.bulk.tensor (UTMALDG) into a kMmaST-deep
+// ring completed on mbarriers; elements past N and vectors past the allocation
+// are zero-filled.  The data in flight lives in shared memory (kMmaST x 8 KB
+// per warp), not in registers.
+// The (w, u_j) tile arrives by two cp.async.bulk copies; its fragments go to
+// registers at once, so one buffer suffices.  The per-CTA and grid reductions
+// at the end are the fixed-order ones of k_lsa_dots (same partial slots, same
+// finishing step).
+//
+// Measured at C5 (round 2): correct (tests/test_gpu_switches.py) and SLOWER:
+// pass 1 takes 32.5 ms per solve against 24.8 ms for k_lsa_dots (the solve
+// 94.6 vs 88.7 ms).  History: fragments loaded straight into registers (one
+// 8-warp CTA per SM at 240+ registers, 8 KB in flight per warp): 106-116 ms;
+// this ring with eight 512-byte cp.async.bulk rows per unit: 106.7 ms; one
+// 4 KB tensor box per unit: 97.6 ms; 8 KB boxes (kMmaTE = 64): 94.6 ms.  With
+// the DMMAs replaced by two FMAs the pipeline alone streams at 4.6 TB/s for
+// 4 KB and 8 KB boxes alike, below k_lsa_dots' 5.5 TB/s: boxes of eight rows
+// from eight vectors (eight DRAM pages) are what the copy engine is slow on,
+// and that shape is what the DMMA operand layout asks for.  Opt-in.
+// ---------------------------------------------------------------------------
+#ifndef HD_MMA_TE
+#define HD_MMA_TE 64
+#endif
+#ifndef HD_MMA_ST
+#define HD_MMA_ST 3
+#endif
+constexpr int kMmaTE = HD_MMA_TE;               // complex elements per tile (1 KB per vector)
+constexpr int kMmaNG = (kLsaMaxJ + 1 + 7) / 8;  // groups of 8 basis vectors
+constexpr int kMmaST = HD_MMA_ST;               // ring stages per warp
+constexpr int kMmaRS = kMmaTE * 16;             // row pitch in shared memory (bytes): a dense tensor-copy box
+constexpr int kMmaWarp = kMmaST * 8 * kMmaRS + 2 * kMmaTE * 16 + 128;  // ring + the (w, u_j) tile + barriers
+constexpr size_t lsa_mma_smem() { return (size_t)(kLsaBD / 32) * kMmaWarp + 128; }
+
+__device__ __forceinline__ void lsa_dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double2 lsa_lds16(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kLsaBD, 1) k_lsa_dots_mma(LsaArgs a, const __grid_constant__ CUtensorMap tmU) {
+  constexpr int NW = kLsaBD / 32;
+  constexpr int NT = kMmaTE / 4;  // element quads per tile
+  extern __shared__ __align__(128) unsigned char msm_raw[];
+  __shared__ double2 acc[2 * kLsaMaxJ + 2];  // [0..j]: s_i ; [kLsaMaxJ+1 ..]: G_ji  (k_lsa_dots' slots)
+  __shared__ double2 sh_s[kLsaMaxJ + 1];
+  __shared__ double2 sh_lj[kLsaMaxJ];
+  __shared__ double2 hsm[kLsaMaxJ + 1];
+  if (a.done && *((volatile const int*)a.done)) return;
+  const int j = a.dj ? *a.dj : a.j;
+  const int nd = j + 1, ng = (nd + 7) >> 3;
+  const int nslot = 2 * kLsaMaxJ + 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  for (int t = threadIdx.x; t < nslot; t += kLsaBD) acc[t] = cmk(0.0, 0.0);
+  const size_t N = a.N;
+  const double2* uj = a.U + (size_t)j * N;
+  unsigned char* wbase = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(msm_raw) + 127) & ~uintptr_t(127)) +
+                         (size_t)warp * kMmaWarp;
+  unsigned char* bbuf = wbase + kMmaST * 8 * kMmaRS;                             // [w tile | u_j tile]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(bbuf + 2 * kMmaTE * 16);  // [kMmaST]
+  unsigned long long* bfull = full + kMmaST;                                     // the (w, u_j) tile's barrier
+  if (lane == 0) {
+    for (int s = 0; s < kMmaST; ++s) tma_mbar_init(&full[s], 1);
+    tma_mbar_init(&bfull[0], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  const size_t ntiles = (N + kMmaTE - 1) / kMmaTE;
+  const size_t gw = (size_t)blockIdx.x * NW + warp, W = (size_t)gridDim.x * NW;
+  const int nt = gw < ntiles ? (int)((ntiles - gw + W - 1) / W) : 0;  // this warp's tiles gw, gw + W, ...
+  const int nunits = nt * ng;
+  auto tile_bytes = [&](int k) {  // bytes of tile k of a vector (the last tile of the grid may be short)
+    const size_t e0 = (gw + (size_t)k * W) * kMmaTE;
+    return (unsigned)(min((size_t)kMmaTE, N - e0) * 16);
+  };
+  auto issue_unit = [&](int u) {  // lane 0: unit u = (tile u / ng, group u % ng) as one 8-row tensor-copy box
+    const int k = u / ng, g = u - k * ng, slot = u % kMmaST;
+    const size_t e0 = (gw + (size_t)k * W) * kMmaTE;
+    if (lane == 0) {
+      tma_expect(&full[slot], 8 * kMmaRS);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              tma_sa(wbase + (size_t)slot * 8 * kMmaRS)),
+          "l"(&tmU), "r"((int)(2 * e0)), "r"(8 * g), "r"(tma_sa(&full[slot]))
+          : "memory");
+    }
+  };
+  auto issue_b = [&](int k) {  // lanes 0, 1: the w and u_j tiles of tile k (its fragments go to registers at once)
+    const size_t e0 = (gw + (size_t)k * W) * kMmaTE;
+    const unsigned bytes = tile_bytes(k);
+    if (lane == 0) tma_expect(&bfull[0], 2 * bytes);
+    if (lane == 0) tma_g2s(bbuf, a.w + e0, bytes, &bfull[0]);
+    if (lane == 1) tma_g2s(bbuf + kMmaTE * 16, uj + e0, bytes, &bfull[0]);
+  };
+  if (lane == 0)
+    for (int u = 0; u < kMmaST && u < nunits; ++u) issue_unit(u);
+  if (lane < 2 && nt > 0) issue_b(0);
+  double C[kMmaNG][2];
+#pragma unroll
+  for (int g = 0; g < kMmaNG; ++g) C[g][0] = C[g][1] = 0.0;
+  const bool buse = r < 4;
+  const unsigned boff = (unsigned)((buse ? (r >> 1) : 0) * kMmaTE * 16 + q * 16);  // this lane's element of quad 0 in a (w | u_j) tile
+  const unsigned aoff = (unsigned)(r * kMmaRS + q * 16);              // ... in a ring stage
+  int uc = 0, slot = 0;
+  unsigned ph = 0;
+  for (int k = 0; k < nt; ++k) {
+    const size_t e0 = (gw + (size_t)k * W) * kMmaTE + q;
+    tma_wait(&bfull[0], (unsigned)(k & 1));
+    double bre[NT], bim[NT];
+    const unsigned bb = tma_sa(bbuf) + boff;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      double2 v = lsa_lds16(bb + t * 64);
+      if (!buse || e0 + 4 * t >= N) v = cmk(0.0, 0.0);  // columns 4..7 and the tail of the last tile
+      bre[t] = r == 0 ? v.x : (r == 1 ? v.y : (r == 2 ? v.x : -v.y));
+      bim[t] = r == 0 ? v.y : (r == 1 ? -v.x : (r == 2 ? v.y : v.x));
+    }
+    __syncwarp();
+    if (lane < 2 && k + 1 < nt) issue_b(k + 1);
+#pragma unroll
+    for (int g = 0; g < kMmaNG; ++g) {
+      if (g < ng) {  // warp-uniform
+        tma_wait(&full[slot], ph);
+        const unsigned ab = tma_sa(wbase) + (unsigned)slot * 8 * kMmaRS + aoff;
+        double T[2] = {0.0, 0.0};  // second chain: halves the dependent DMMA chain on C[g]
+        const bool row_ok = 8 * g + r <= j;  // rows beyond the basis hold other memory: mask them
+#pragma unroll
+        for (int h = 0; h < NT; h += 8) {
+          double2 av[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            av[t] = lsa_lds16(ab + (h + t) * 64);
+            if (!row_ok) av[t] = cmk(0.0, 0.0);
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            lsa_dmma(C[g], av[t].x, bre[h + t]);
+            lsa_dmma(T, av[t].y, bim[h + t]);
+          }
+        }
+        C[g][0] += T[0];
+        C[g][1] += T[1];
+        __syncwarp();  // every lane has read the stage before it is refilled
+        if (lane == 0 && uc + kMmaST < nunits) issue_unit(uc + kMmaST);
+        ++uc;
+        if (++slot == kMmaST) {
+          slot = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  }
+  // CTA sums in warp order (fixed => deterministic): C[g] of lane (r, q): q = 0 -> s_i, q = 1 -> G_ji, i = 8 g + r
+  __syncthreads();
+  for (int wq = 0; wq < NW; ++wq) {
+    if (warp == wq && q < 2) {
+#pragma unroll
+      for (int g = 0; g < kMmaNG; ++g) {
+        const int i = 8 * g + r;
+        if (g < ng && i <= j) {
+          if (q == 0) acc[i] = cadd(acc[i], cmk(C[g][0], C[g][1]));
+          else if (i < j) acc[kLsaMaxJ + 1 + i] = cadd(acc[kLsaMaxJ + 1 + i], cmk(C[g][0], C[g][1]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < nslot; t += kLsaBD) {
+    const bool used = t < nd || (t >= kLsaMaxJ + 1 && t < kLsaMaxJ + 1 + j);
+    if (used) a.partials[(size_t)(a.part_offset + blockIdx.x) * nslot + t] = acc[t];
+  }
+  if (a.partial_only) return;
+  if (!lsa_last_block(a.counter)) return;
+  lsa_dots_finish(a, j, gridDim.x, sh_s, sh_lj, hsm);
+  if (threadIdx.x == 0) *a.counter = 0u;
 }
 
 // row slabs: combine the partials of all slabs (nparts CTA slots, slab order)

@@ -908,7 +908,23 @@ static void ensure_gmres(hd_ctx* c, int maxit) {
 // 48.3 ms for both passes over a solve), so the round-1 kernel stays the default
 static void launch_lsa_dots(hd_ctx* c, const LsaArgs& a, int G, cudaStream_t st) {
   if (c->lsa_mma) {  // one CTA per SM (never more CTAs than the partials buffer has slots)
-    k_lsa_dots_mma<<<std::min(c->n_sms, G), kLsaBD, 0, st>>>(a);
+    smem_optin(reinterpret_cast<const void*>(k_lsa_dots_mma), lsa_mma_smem());
+    // the basis as a 2D tensor (2N doubles x v_cap vectors), box = kMmaTE elements x 8 vectors
+    const hd_ctx::TmaKey key{a.U, static_cast<int>(a.N), c->v_cap, -kMmaTE};
+    auto it = c->tma_maps.find(key);
+    if (it == c->tma_maps.end()) {
+      CUtensorMap m;
+      const cuuint64_t dims[2] = {static_cast<cuuint64_t>(2) * a.N, static_cast<cuuint64_t>(c->v_cap)};
+      const cuuint64_t strides[1] = {static_cast<cuuint64_t>(16) * a.N};
+      const cuuint32_t box[2] = {2 * kMmaTE, 8};
+      const cuuint32_t es[2] = {1, 1};
+      const CUresult r = tma_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(a.U), dims, strides, box,
+                                         es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(HD_ERR_CUDA, "cuTensorMapEncodeTiled (basis) failed: " + std::to_string(static_cast<int>(r)));
+      it = c->tma_maps.emplace(key, m).first;
+    }
+    k_lsa_dots_mma<<<std::min(c->n_sms, G), kLsaBD, lsa_mma_smem(), st>>>(a, it->second);
   } else if (c->lsa_tma) {
     smem_optin(reinterpret_cast<const void*>(k_lsa_dots_tma), lsa_tma_smem());
     // one CTA per SM, never more CTAs than the partials buffer has slots (lsa_G)
