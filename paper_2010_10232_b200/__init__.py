@@ -38,6 +38,8 @@ HD_FIELD_CONSTANT = 0
 HD_FIELD_LAYERED = 1
 HD_FIELD_WEDGE = 2
 HD_APPLY_A, HD_APPLY_SHIFTED, HD_APPLY_MG, HD_APPLY_PROJECT, HD_APPLY_OP, HD_APPLY_Q = range(6)
+# hd_status (include/helmdef_b200.h); HelmdefError.status carries one of these
+HD_OK, HD_ERR_INVALID, HD_ERR_CUDA, HD_ERR_FACTOR, HD_ERR_NO_DEVICE, HD_ERR_NONFINITE = range(6)
 
 # Every symbol include/helmdef_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = ["hd_problem_per_dim", "hd_assemble", "hd_assemble_field", "hd_create", "hd_solve", "hd_solve_device", "hd_size",
