@@ -64,7 +64,8 @@ __device__ __forceinline__ void bt_fma(double2 a, double vr, double vi, double& 
 // warps per CTA by the registers a row needs per lane (doubles per lane)
 // (round 2, C4, 24 doubles per lane: 256 / 320 / 384 / 512 / 640 / 768 threads give 27.6 / 26.3 / 25.9 / 28.3 /
 // 28.5 / 31.8 ms per solve; prefetching the rows of a warp's first TWO tasks across the barrier: 26.3 ms -- the
-// step time is the barrier and the dependent vector hand-over, not the rows' DRAM latency)
+// step time is the barrier and the dependent vector hand-over, not the rows' DRAM latency; blocks of 2b grid
+// rows (m = 1440, 40 blocks, dense factors): 28.2 ms -- half the steps, twice the bytes, 15 us per step)
 #ifndef HD_BTRI_T32
 #define HD_BTRI_T32 384
 #endif
