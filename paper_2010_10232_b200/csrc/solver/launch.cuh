@@ -269,7 +269,10 @@ static void launch_gen_mode(hd_ctx* c, const GenLevel& G, const double2* x, cons
   if (G.b > 6 || G.G > kGenMaxG) throw Error(HD_ERR_INVALID, "layered operator exceeds the kernel limits");
   if (re < 0) re = G.n;
   const dim3 grid((G.n + kGenTX - 1) / kGenTX, (re - rb + kGenTY - 1) / kGenTY);
-  HD_LAUNCH(kind, op_bytes(MODE, static_cast<size_t>(G.n) * (re - rb)),
+  // algorithmic bytes: the vector passes plus, for a stored stencil, its (2b+1)^2 coefficient planes
+  const double bytes = op_bytes(MODE, static_cast<size_t>(G.n) * (re - rb)) +
+                       (G.K ? 8.0 * (2 * G.b + 1) * (2 * G.b + 1) * G.n * (re - rb) : 0.0);
+  HD_LAUNCH(kind, bytes,
             k_kron2d<MODE><<<grid, kGenThreads, gen_smem(G.b, G.G), c->st>>>(G, x, b, out, omega, red, xidx,
                                                                                xstride, rb, re));
 }
