@@ -83,6 +83,8 @@ struct BtriArgs {
   double* x;           // 2 planes x nb*m
   double* io;          // in/out planar (re plane NN, im plane NN)
   unsigned* bar;       // grid barrier counter, zeroed before the launch
+  const void* steps;   // the solve's step table (BtStep per step), built on the host at setup
+  int nsteps;
 };
 
 // Column-major m x m blocks D_i, B_i (= E[i, i+1]), C_i (= E[i, i-1]) of the
@@ -197,12 +199,18 @@ struct BtStep {
   int sv_blk[2], sv_buf[2];
 };
 
-__device__ __forceinline__ BtStep btri_step(int s, int nb, int k) {
+// word offsets inside the step table (BtStep as ints), used where a single field is read from global memory
+constexpr int kGroupWords = (int)(sizeof(BtGroup) / sizeof(int));
+constexpr int kGroupMatWord = 4, kGroupMblkWord = 6;  // BtGroup::mat, BtGroup::mblk
+constexpr int kStepNgWord = 4 * kGroupWords;          // BtStep::ng
+static_assert(sizeof(BtGroup) == 7 * sizeof(int) && sizeof(BtStep) == (4 * 7 + 5) * sizeof(int), "step table layout");
+
+__host__ __device__ inline BtStep btri_step(int s, int nb, int k) {
   BtStep st;
   st.ng = 0;
   st.sv_blk[0] = st.sv_blk[1] = -1;
   st.sv_buf[0] = st.sv_buf[1] = 0;
-  const int F = max(k, nb - 1 - k);  // forward steps
+  const int F = k > nb - 1 - k ? k : nb - 1 - k;  // forward steps
   auto add = [&](int kind, int blk, int vec, int mat, int mblk, int vec2 = 0, int mat2 = 0) {
     BtGroup& g = st.g[st.ng++];
     g.kind = kind;
@@ -275,30 +283,6 @@ __device__ __forceinline__ const T* bt_mat(const BtriArgs& a, int mat, int blk, 
   }
 }
 
-// L2 prefetch of every matrix row this warp reads in step s (one bulk prefetch
-// per row by lane 0): the rows do not depend on the solve's data, so they are
-// pulled into L2 a few steps ahead of the barrier-separated dependent steps.
-template <class T>
-__device__ __forceinline__ void btri_prefetch_step(const BtriArgs& a, int s, int nsteps, int gw, int W) {
-  if (s >= nsteps || (threadIdx.x & 31) != 0) return;
-  const unsigned bytes = (unsigned)(a.m * sizeof(T));
-  if (bytes % 16u) return;
-  const BtStep st = btri_step(s, a.nb, a.k);
-  for (int t = gw; t < st.ng * a.m; t += W) {
-    const BtGroup& g = st.g[t / a.m];
-    for (int q = 0; q < 2; ++q) {
-      const int mat = q == 0 ? g.mat : (g.kind == 3 ? g.mat2 : 0);
-      if (!mat) continue;
-      const T* p = bt_mat<T>(a, mat, g.mblk, t % a.m);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-    }
-  }
-}
-
-#ifndef HD_BTRI_PREFETCH
-#define HD_BTRI_PREFETCH 0  // measured slower at C4 with 2, 3, 5 steps ahead (30.3 vs 26.8 ms)
-#endif
-
 template <class T, int KR>
 __global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_btri_solve(BtriArgs a) {
   const int lane = threadIdx.x & 31;
@@ -308,17 +292,24 @@ __global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_
   const int m = a.m, nb = a.nb, k = a.k;
   const size_t P = (size_t)nb * m;
   const unsigned G = gridDim.x;
-  const int F = max(k, nb - 1 - k);
-  const int nsteps = F + 2 + max(k, nb - 1 - k);
+  const int nsteps = a.nsteps;
   unsigned phase = 0;
   T r[KR];
   extern __shared__ double vs[];  // two staged vectors, 2m doubles each
+  // The step table was built on the host (btri_step): the descriptor of the current step and, loaded between
+  // arriving at and waiting on the barrier, of the next one live in shared memory -- no per-thread recomputation
+  // of the schedule and no local-memory copy of it (round 2: 16% of the kernel's instructions were the
+  // schedule's integer arithmetic and 8% its local-memory traffic).
+  __shared__ BtStep sst[2];
+  constexpr int kStepWords = (int)(sizeof(BtStep) / sizeof(int));
+  const int* steps_w = static_cast<const int*>(a.steps);
+  if (threadIdx.x < kStepWords) reinterpret_cast<int*>(&sst[0])[threadIdx.x] = __ldg(steps_w + threadIdx.x);
+  __syncthreads();
   int pre = -1;                   // task whose matrix row r holds (prefetched), -1: none
-  BtStep st = btri_step(0, nb, k);
-  for (int s = 1; s <= HD_BTRI_PREFETCH; ++s) btri_prefetch_step<T>(a, s, nsteps, gw, W);
+  const int gw0 = gw / m, gr0 = gw % m;  // group and row of this warp's first task of any step
   for (int s = 0; s < nsteps; ++s) {
+    const BtStep& st = sst[s & 1];
     const int ntask = st.ng * m;
-    if (HD_BTRI_PREFETCH > 0) btri_prefetch_step<T>(a, s + HD_BTRI_PREFETCH + 1, nsteps, gw, W);
     // stage this step's input vectors (every CTA with tasks)
     if (blockIdx.x * wpb < ntask) {
       for (int v = 0; v < 2; ++v) {
@@ -331,9 +322,10 @@ __global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_
       }
       __syncthreads();
     }
+    // tasks t = gw, gw + W, ...: group t / m and row t % m advanced without divisions
+    int grp = gw0, row = gr0;
     for (int t = gw; t < ntask; t += W) {
-      const BtGroup& g = st.g[t / m];
-      const int row = t % m;
+      const BtGroup& g = st.g[grp];
       const size_t gi = (size_t)g.blk * m + row;
       double br = 0.0, bi = 0.0;  // rhs (kinds 1, 3) or w (kind 5)
       if (lane == 0) {
@@ -375,15 +367,26 @@ __global__ void __launch_bounds__(btri_threads(KR * (int)(sizeof(T) / 8)), 1) k_
           a.io[a.NN + gi] = xi;
         }
       }
+      row += W;
+      while (row >= m) {
+        row -= m;
+        ++grp;
+      }
     }
     if (s + 1 < nsteps) {
       btri_arrive(a.bar);
-      st = btri_step(s + 1, nb, k);
-      if (gw < st.ng * m) {  // prefetch the first task's row of the next step
-        const BtGroup& g = st.g[gw / m];
-        if (g.mat) {
-          btri_row_load<T, KR>(bt_mat<T>(a, g.mat, g.mblk, gw % m), m, r);
-          pre = gw;
+      // the next step's descriptor (read by this CTA only after the barrier's closing __syncthreads)
+      if (threadIdx.x < kStepWords)
+        reinterpret_cast<int*>(&sst[(s + 1) & 1])[threadIdx.x] = __ldg(steps_w + (size_t)(s + 1) * kStepWords + threadIdx.x);
+      {  // prefetch the first task's row of the next step (its group comes straight from the table)
+        const int ng1 = __ldg(steps_w + (size_t)(s + 1) * kStepWords + kStepNgWord);
+        if (gw < ng1 * m) {
+          const int* gwd = steps_w + (size_t)(s + 1) * kStepWords + gw0 * kGroupWords;
+          const int mat = __ldg(gwd + kGroupMatWord), mblk = __ldg(gwd + kGroupMblkWord);
+          if (mat) {
+            btri_row_load<T, KR>(bt_mat<T>(a, mat, mblk, gr0), m, r);
+            pre = gw;
+          }
         }
       }
       btri_wait(a.bar, ++phase * G);

@@ -724,7 +724,7 @@ static void free_exact(ExactSolver& X) {
   dfree(X.pfdF); dfree(X.pfdB);
   if (X.btri) {
     dfree(const_cast<void*>(X.bt.GT)); dfree(const_cast<void*>(X.bt.SinvT));
-    dfree(const_cast<void*>(X.bt.HT)); dfree(const_cast<void*>(X.bt.G2)); dfree(X.bt.y); dfree(X.bt.bar);
+    dfree(const_cast<void*>(X.bt.HT)); dfree(const_cast<void*>(X.bt.G2)); dfree(X.bt.y); dfree(X.bt.bar); dfree(const_cast<void*>(X.bt.steps));
   }
   X = ExactSolver{};
 }

@@ -423,6 +423,15 @@ static ExactSolver make_btri(cudaStream_t st, const GenHost& h, double2 cl, int 
   X.bt.w = X.bt.y + 2 * static_cast<size_t>(nb) * m;
   X.bt.x = X.bt.w + 2 * static_cast<size_t>(nb) * m;
   X.bt.bar = dalloc<unsigned>(1);
+  {  // the solve's schedule, one BtStep per barrier-separated step
+    const int F = std::max(X.bt.k, nb - 1 - X.bt.k);
+    X.bt.nsteps = 2 * F + 2;
+    std::vector<BtStep> steps(X.bt.nsteps);
+    for (int s = 0; s < X.bt.nsteps; ++s) steps[s] = btri_step(s, nb, X.bt.k);
+    BtStep* d = dalloc<BtStep>(steps.size());
+    CK(cudaMemcpy(d, steps.data(), steps.size() * sizeof(BtStep), cudaMemcpyHostToDevice));
+    X.bt.steps = d;
+  }
   (void)n_sms;
   return X;
 }
