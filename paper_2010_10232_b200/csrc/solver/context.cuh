@@ -256,6 +256,7 @@ struct hd_ctx {
   // tensor-copy stencil (stencil_tma.cuh) for whole-grid 2D level operators of at least
   // tma_min_n rows: HD_STENCIL_TMA=0 at create keeps the cp.async stencil everywhere
   bool stencil_tma = true;
+  bool restrict_stream = true;  // streaming linear restriction on levels of >= tma_min_n rows (HD_RESTRICT_STREAM=0: tiled)
   int tma_min_n = 512;
   std::map<std::pair<const double*, const double*>, double2*> tma_ct;  // (S, M) tables -> CT of the level
   struct TmaKey {

@@ -361,8 +361,38 @@ static void restrict_(hd_ctx* c, Stencil z, const double2* r, int nf, int nc, do
 
 // linear restriction fused with the coarse level's first Jacobi sweep from zero:
 // outc = z^T r and x0 = omega D^-1 outc (2D Kronecker-sum levels)
+// strip height of the streaming linear restriction: the warp tasks fill the resident warps in whole waves
+static int restrict_stream_rows(hd_ctx* c, int nc, int* strips_x, int* ntasks) {
+  static int per_sm = 0;  // resident warps per SM of the kernel (same for both J0 variants)
+  if (!per_sm) {
+    int ctas = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, k_restrict_lin_stream<true>, 32 * kRSWarps, 0));
+    per_sm = std::max(1, ctas) * kRSWarps;
+  }
+  const int sx = (nc + 31) / 32, slots = c->n_sms * per_sm;
+  int best = 16;
+  double best_score = -1.0;
+  for (int qr = 4; qr <= 64; ++qr) {
+    const long tasks = static_cast<long>(sx) * ((nc + qr - 1) / qr);
+    const long waves = (tasks + slots - 1) / slots;
+    const double score = static_cast<double>(tasks) / (static_cast<double>(waves) * slots) * (2.0 * qr) / (2.0 * qr + 1.0);
+    if (score > best_score + 1e-9) best_score = score, best = qr;
+  }
+  *strips_x = sx;
+  *ntasks = sx * ((nc + best - 1) / best);
+  return best;
+}
+
 static void restrict_j0(hd_ctx* c, const double2* r, int nf, int nc, double2* outc, const LevelDev& Lc, double omega,
                         double2* x0) {
+  if (c->restrict_stream && nf >= c->tma_min_n) {  // fine levels: the streaming kernel (same arithmetic)
+    int sx = 0, nt = 0;
+    const int qr = restrict_stream_rows(c, nc, &sx, &nt);
+    HD_LAUNCH(HD_K_TRANSFER, 16.0 * (static_cast<double>(nf) * nf + 2.0 * nc * nc),
+              k_restrict_lin_stream<true><<<(nt + kRSWarps - 1) / kRSWarps, 32 * kRSWarps, 0, c->st>>>(
+                  r, nf, nc, qr, sx, nt, outc, Lc, omega, x0));
+    return;
+  }
   dim3 grid((nc + kRQX - 1) / kRQX, (nc + kRQY - 1) / kRQY);
   HD_LAUNCH(HD_K_TRANSFER, 16.0 * (static_cast<double>(nf) * nf + 2.0 * nc * nc),
             k_restrict2d<0, 0, true><<<grid, 256, 0, c->st>>>(0.0, r, nf, nc, outc, nullptr, 0, nc, Lc, omega, x0));

@@ -524,6 +524,7 @@ static void create_ctx(const hd_system* sys, const hd_precond* spec, const int* 
   c->k4_fuse = std::getenv("HD_K4FUSE") && std::atoi(std::getenv("HD_K4FUSE")) == 1;
   c->stencil_tma = !(std::getenv("HD_STENCIL_TMA") && std::atoi(std::getenv("HD_STENCIL_TMA")) == 0);
   if (std::getenv("HD_STENCIL_TMA_MIN")) c->tma_min_n = std::atoi(std::getenv("HD_STENCIL_TMA_MIN"));
+  c->restrict_stream = !(std::getenv("HD_RESTRICT_STREAM") && std::atoi(std::getenv("HD_RESTRICT_STREAM")) == 0);
   c->lsa_rev = !(std::getenv("HD_LSA_REV") && std::atoi(std::getenv("HD_LSA_REV")) == 0);
   c->lsa_mma = std::getenv("HD_LSA_MMA") && std::atoi(std::getenv("HD_LSA_MMA")) == 1;
   c->lsa_tma = std::getenv("HD_LSA_TMA") && std::atoi(std::getenv("HD_LSA_TMA")) == 1;

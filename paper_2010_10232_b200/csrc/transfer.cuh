@@ -98,6 +98,83 @@ __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* 
   }
 }
 
+// Linear restriction rc = (z (x) z)^T r as a warp-streaming kernel (fine levels; k_restrict2d<0,0,J0>'s
+// arithmetic in the same order, so the same bits): a warp owns 32 coarse columns of a strip of QR coarse
+// rows and walks the 2 QR + 1 fine rows that feed them.  Per fine row a lane loads its two fine columns
+// 2q, 2q+1 (32 contiguous bytes; the third tap 2q+2 is the next lane's first value, lane 31 loads its own),
+// restricts in x in registers and adds the row into the (at most two) coarse rows it feeds; a coarse row is
+// written when its third fine row has passed.  No shared memory, no block barrier, ~10 instructions per fine
+// point (the tiled kernel: ~200, a quarter of them index arithmetic); kRSU fine rows are loaded ahead.
+constexpr int kRSU = 4;      // fine rows in flight per warp
+constexpr int kRSWarps = 4;  // warps per CTA (independent)
+
+template <bool J0>
+__global__ void __launch_bounds__(32 * kRSWarps) k_restrict_lin_stream(const double2* __restrict__ r, int nf, int nc,
+                                                                        int QR, int strips_x, int ntasks,
+                                                                        double2* __restrict__ outc, LevelDev Lc,
+                                                                        double omega, double2* __restrict__ x0) {
+  const int lane = threadIdx.x & 31;
+  const int task = blockIdx.x * kRSWarps + (threadIdx.x >> 5);
+  if (task >= ntasks) return;
+  const int q0 = (task % strips_x) * 32, qy0 = (task / strips_x) * QR;
+  const int qy1 = min(qy0 + QR, nc);
+  const int qx = q0 + lane;             // this lane's coarse column
+  const int c0 = 2 * qx;                // its first fine column
+  const bool v0 = c0 < nf, v1 = c0 + 1 < nf, v2 = lane == 31 && c0 + 2 < nf;
+  const int fy0 = 2 * qy0, nrows = 2 * (qy1 - qy0) + 1;  // fine rows fy0 .. fy0 + nrows - 1
+  auto load_row = [&](int k, double2& a, double2& b, double2& e) {  // fine row fy0 + k (zero past the grid)
+    const int fy = fy0 + k;
+    const bool rv = k < nrows && fy < nf;
+    const double2* p = r + (size_t)(rv ? fy : 0) * nf + c0;
+    a = rv && v0 ? __ldg(p) : cmk(0.0, 0.0);
+    b = rv && v1 ? __ldg(p + 1) : cmk(0.0, 0.0);
+    e = rv && v2 ? __ldg(p + 2) : cmk(0.0, 0.0);
+  };
+  double2 fa[kRSU], fb[kRSU], fe[kRSU];
+#pragma unroll
+  for (int u = 0; u < kRSU; ++u) load_row(u, fa[u], fb[u], fe[u]);
+  double2 acur = cmk(0.0, 0.0), aprev = cmk(0.0, 0.0);  // coarse rows q (started) and q - 1 (finishing)
+  int q = qy0;
+  const int NBc = J0 ? 2 * Lc.b + 1 : 1;
+  for (int kb = 0; kb < nrows; kb += kRSU) {
+#pragma unroll
+    for (int u = 0; u < kRSU; ++u) {
+      const int k = kb + u;
+      if (k < nrows) {  // warp-uniform
+        const double2 a = fa[u], b = fb[u];
+        // third tap: the next lane's first value (lane 31: its own extra load)
+        double2 cN = cmk(__shfl_down_sync(0xffffffffu, a.x, 1), __shfl_down_sync(0xffffffffu, a.y, 1));
+        if (lane == 31) cN = fe[u];
+        load_row(k + kRSU, fa[u], fb[u], fe[u]);  // refill the slot kRSU rows ahead
+        // x restriction (weights 1/2, 1, 1/2 in tap order, k_restrict2d's chain from zero)
+        const double2 tx = cfma_r(0.5, cN, cfma_r(1.0, b, cfma_r(0.5, a, cmk(0.0, 0.0))));
+        if ((k & 1) == 0) {
+          // even fine row 2 q: third tap of coarse row q - 1 (complete -> store), first tap of coarse row q
+          if (k > 0) {
+            const double2 sres = cfma_r(0.5, tx, aprev);
+            const int gy = q - 1;
+            if (qx < nc) {
+              const size_t gi = (size_t)gy * nc + qx;
+              outc[gi] = sres;
+              if (J0) {
+                const double my = Lc.M[(size_t)gy * NBc + Lc.b], sy = Lc.S[(size_t)gy * NBc + Lc.b];
+                const double mxx = Lc.M[(size_t)qx * NBc + Lc.b], sxx = Lc.S[(size_t)qx * NBc + Lc.b];
+                const double2 D = csub(cmk(my * sxx + sy * mxx, 0.0), cscale(my * mxx, Lc.c));
+                x0[gi] = cscale(omega, cmul(cinv(D), sres));
+              }
+            }
+          }
+          acur = cfma_r(0.5, tx, cmk(0.0, 0.0));
+        } else {
+          // odd fine row 2 q + 1: middle tap of coarse row q, which then waits for its third tap
+          aprev = cfma_r(1.0, tx, acur);
+          ++q;
+        }
+      }
+    }
+  }
+}
+
 // fine index i -> coarse neighbours as offsets into a staged region starting at
 // coarse index qbase; returns count.  Same stencil as pweights() in kernels.cuh.
 template <int KIND>
