@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(256) k_restrict2d(double drop, const double2* 
 // restricts in x in registers and adds the row into the (at most two) coarse rows it feeds; a coarse row is
 // written when its third fine row has passed.  No shared memory, no block barrier, ~10 instructions per fine
 // point (the tiled kernel: ~200, a quarter of them index arithmetic); kRSU fine rows are loaded ahead.
+// C5 fine level: 19.1 -> 14.1 us per launch.  (The same treatment of the linear prolongation x += Z e gave
+// 18.2 -> 17.3 us: that kernel already moves its 92 MB at 5.1 TB/s, so the tiled form stays.)
 constexpr int kRSU = 4;      // fine rows in flight per warp
 constexpr int kRSWarps = 4;  // warps per CTA (independent)
 
