@@ -390,62 +390,55 @@ __device__ __forceinline__ size_t fold_idx(int yb, int xb, int p, int kx, int j,
   return (size_t)yb * 4 * nn + (size_t)j * 4 * n2 + (size_t)(2 * xb + p) * n2 + kx;
 }
 
-// R[yb](q n2 + kx, ky), q = 2 xb + p: (R_p0 + i R_p1) *= D[yb][xb][ky][kx]
-__global__ void k_scale_folded(double* __restrict__ R, const double2* __restrict__ D, int n2) {
-  const size_t nn = (size_t)n2 * n2;
-  const size_t tot = 4 * nn;
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
-    const int kx = (int)(g % n2);
-    const int xb = (int)((g / n2) % 2);
-    const int ky = (int)((g / (2 * (size_t)n2)) % n2);
-    const int yb = (int)(g / (2 * nn));
-    double* r0 = R + fold_idx(yb, xb, 0, kx, ky, n2);
-    double* r1 = R + fold_idx(yb, xb, 1, kx, ky, n2);
-    const double2 v = cmul(cmk(*r0, *r1), D[(((size_t)yb * 2 + xb) * n2 + ky) * n2 + kx]);
-    *r0 = v.x;
-    *r1 = v.y;
-  }
+// The three kernels below index with a 3D grid (x: the contiguous index, y: the row / column, z: the block), so
+// no thread does 64-bit divisions (the grid-stride forms spent most of their instructions on them: 7-10 us each
+// for 10-30 MB at C5).
+//
+// R[yb](q n2 + kx, ky), q = 2 xb + p: (R_p0 + i R_p1) *= D[yb][xb][ky][kx]     grid (ceil(n2 / 256), n2, 4)
+__global__ void __launch_bounds__(256) k_scale_folded(double* __restrict__ R, const double2* __restrict__ D, int n2) {
+  const int kx = blockIdx.x * 256 + threadIdx.x, ky = blockIdx.y;
+  const int xb = blockIdx.z & 1, yb = blockIdx.z >> 1;
+  if (kx >= n2) return;
+  double* r0 = R + fold_idx(yb, xb, 0, kx, ky, n2);
+  double* r1 = R + fold_idx(yb, xb, 1, kx, ky, n2);
+  const double2 v = cmul(cmk(*r0, *r1), D[(((size_t)yb * 2 + xb) * n2 + ky) * n2 + kx]);
+  *r0 = v.x;
+  *r1 = v.y;
 }
 
 // Both reflections at once (x rows and y columns of the planar n x n input X):
 // Q[xb][yb][p](i, j), i, j < n2: x rows folded first (a +- b), then y columns.
-// Q blocks n2 x n2 column-major, block (2 xb + yb) 2 + p.
-__global__ void k_fold_both(const double* __restrict__ X, double* __restrict__ Q, int n, int n2) {
+// Q blocks n2 x n2 column-major, block (2 xb + yb) 2 + p.                     grid (ceil(n2 / 256), n2, 2)
+__global__ void __launch_bounds__(256) k_fold_both(const double* __restrict__ X, double* __restrict__ Q, int n, int n2) {
   const size_t nn = (size_t)n2 * n2, N2 = (size_t)n * n;
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < 2 * nn; g += (size_t)gridDim.x * blockDim.x) {
-    const int i = (int)(g % n2);
-    const int j = (int)((g / n2) % n2);
-    const int p = (int)(g / nn);
-    const double* Xp = X + p * N2;
-    const double a = Xp[(size_t)j * n + i], b = Xp[(size_t)j * n + (n - 1 - i)];
-    const double c = Xp[(size_t)(n - 1 - j) * n + i], d = Xp[(size_t)(n - 1 - j) * n + (n - 1 - i)];
-    const double f0 = a + b, f1 = a - b, g0 = c + d, g1 = c - d;  // x parity 0 / 1 at columns j, n-1-j
-    const size_t o = (size_t)j * n2 + i;
-    Q[(size_t)((0 * 2 + 0) * 2 + p) * nn + o] = f0 + g0;
-    Q[(size_t)((0 * 2 + 1) * 2 + p) * nn + o] = f0 - g0;
-    Q[(size_t)((1 * 2 + 0) * 2 + p) * nn + o] = f1 + g1;
-    Q[(size_t)((1 * 2 + 1) * 2 + p) * nn + o] = f1 - g1;
-  }
+  const int i = blockIdx.x * 256 + threadIdx.x, j = blockIdx.y, p = blockIdx.z;
+  if (i >= n2) return;
+  const double* Xp = X + p * N2;
+  const double a = Xp[(size_t)j * n + i], b = Xp[(size_t)j * n + (n - 1 - i)];
+  const double c = Xp[(size_t)(n - 1 - j) * n + i], d = Xp[(size_t)(n - 1 - j) * n + (n - 1 - i)];
+  const double f0 = a + b, f1 = a - b, g0 = c + d, g1 = c - d;  // x parity 0 / 1 at columns j, n-1-j
+  const size_t o = (size_t)j * n2 + i;
+  Q[(size_t)((0 * 2 + 0) * 2 + p) * nn + o] = f0 + g0;
+  Q[(size_t)((0 * 2 + 1) * 2 + p) * nn + o] = f0 - g0;
+  Q[(size_t)((1 * 2 + 0) * 2 + p) * nn + o] = f1 + g1;
+  Q[(size_t)((1 * 2 + 1) * 2 + p) * nn + o] = f1 - g1;
 }
 
 // Inverse of k_fold_both: P[xb][yb][p] blocks -> planar n x n Y (y columns
-// unfolded first, then x rows).
-__global__ void k_unfold_both(const double* __restrict__ Pb, double* __restrict__ Y, int n, int n2) {
+// unfolded first, then x rows).                                                grid (ceil(n2 / 256), n2, 2)
+__global__ void __launch_bounds__(256) k_unfold_both(const double* __restrict__ Pb, double* __restrict__ Y, int n, int n2) {
   const size_t nn = (size_t)n2 * n2, N2 = (size_t)n * n;
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < 2 * nn; g += (size_t)gridDim.x * blockDim.x) {
-    const int i = (int)(g % n2);
-    const int j = (int)((g / n2) % n2);
-    const int p = (int)(g / nn);
-    const size_t o = (size_t)j * n2 + i;
-    const double p00 = Pb[(size_t)((0 * 2 + 0) * 2 + p) * nn + o], p01 = Pb[(size_t)((0 * 2 + 1) * 2 + p) * nn + o];
-    const double p10 = Pb[(size_t)((1 * 2 + 0) * 2 + p) * nn + o], p11 = Pb[(size_t)((1 * 2 + 1) * 2 + p) * nn + o];
-    const double z0j = p00 + p01, z0m = p00 - p01, z1j = p10 + p11, z1m = p10 - p11;
-    double* Yp = Y + p * N2;
-    Yp[(size_t)j * n + i] = z0j + z1j;
-    Yp[(size_t)j * n + (n - 1 - i)] = z0j - z1j;
-    Yp[(size_t)(n - 1 - j) * n + i] = z0m + z1m;
-    Yp[(size_t)(n - 1 - j) * n + (n - 1 - i)] = z0m - z1m;
-  }
+  const int i = blockIdx.x * 256 + threadIdx.x, j = blockIdx.y, p = blockIdx.z;
+  if (i >= n2) return;
+  const size_t o = (size_t)j * n2 + i;
+  const double p00 = Pb[(size_t)((0 * 2 + 0) * 2 + p) * nn + o], p01 = Pb[(size_t)((0 * 2 + 1) * 2 + p) * nn + o];
+  const double p10 = Pb[(size_t)((1 * 2 + 0) * 2 + p) * nn + o], p11 = Pb[(size_t)((1 * 2 + 1) * 2 + p) * nn + o];
+  const double z0j = p00 + p01, z0m = p00 - p01, z1j = p10 + p11, z1m = p10 - p11;
+  double* Yp = Y + p * N2;
+  Yp[(size_t)j * n + i] = z0j + z1j;
+  Yp[(size_t)j * n + (n - 1 - i)] = z0j - z1j;
+  Yp[(size_t)(n - 1 - j) * n + i] = z0m + z1m;
+  Yp[(size_t)(n - 1 - j) * n + (n - 1 - i)] = z0m - z1m;
 }
 
 // Banded LU solve, sequential in one thread, with the factors streamed into

@@ -631,19 +631,19 @@ static void exact_solve_planar(hd_ctx* c, ExactSolver& X, double* inout) {
   if (X.dim == 2 && X.folded) {
     const int n = X.n, n2 = X.n2;
     const long long nn = static_cast<long long>(n2) * n2;
-    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_both<<<grid_for(2 * nn), 256, 0, c->st>>>(inout, X.F, n, n2));
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_fold_both<<<dim3((n2 + 255) / 256, n2, 2), 256, 0, c->st>>>(inout, X.F, n, n2));
     // x transform: Hh[yb] rows (2 xb + p) n2 = Vt_xb^T Q[xb][yb][p]  (8 pointer-batched n2^3 GEMMs)
     dgemm<true, false>(c, n2, n2, n2, nullptr, n2, 0, nullptr, n2, 0, nullptr, 4 * n2, 0, 8, X.xf_ptr, X.xf_ptr + 8,
                        const_cast<double* const*>(X.xf_ptr + 16));
     // y transform: R[yb] = Hh[yb] Vt_yb, Hh[yb] (4 n2) x n2 (x parity and plane stacked), batch over yb
     dgemm<false, false>(c, 4 * n2, n2, n2, X.Hh, 4 * n2, 4 * nn, X.Vt, n2, nn, X.R, 4 * n2, 4 * nn, 2);
-    HD_LAUNCH(HD_K_EXACT, 48.0 * 4 * nn, k_scale_folded<<<grid_for(4 * nn), 256, 0, c->st>>>(X.R, X.Dinvf, n2));
+    HD_LAUNCH(HD_K_EXACT, 48.0 * 4 * nn, k_scale_folded<<<dim3((n2 + 255) / 256, n2, 4), 256, 0, c->st>>>(X.R, X.Dinvf, n2));
     // inverse y: S[yb] = R[yb] Vt_yb^T  (into Hh)
     dgemm<false, true>(c, 4 * n2, n2, n2, X.R, 4 * n2, 4 * nn, X.Vt, n2, nn, X.Hh, 4 * n2, 4 * nn, 2);
     // inverse x: F blocks = Vt_xb Hh[yb] rows (2 xb + p) n2, then both reflections undone
     dgemm<false, false>(c, n2, n2, n2, nullptr, n2, 0, nullptr, 4 * n2, 0, nullptr, n2, 0, 8, X.xi_ptr, X.xi_ptr + 8,
                         const_cast<double* const*>(X.xi_ptr + 16));
-    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_both<<<grid_for(2 * nn), 256, 0, c->st>>>(X.F, inout, n, n2));
+    HD_LAUNCH(HD_K_EXACT, 32.0 * n * n, k_unfold_both<<<dim3((n2 + 255) / 256, n2, 2), 256, 0, c->st>>>(X.F, inout, n, n2));
     return;
   }
   if (X.dim == 2) {
