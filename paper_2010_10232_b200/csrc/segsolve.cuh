@@ -48,6 +48,8 @@ struct SegArgs {
   double2* Dl;           // [P][KL+1] Delta_i
   double2* X0;           // [P][KU]   local x of the first KU rows
   double2* Xb;           // [P+1][KU] true x of the first KU rows
+  double2* AgF;          // [kScanWarps][(KL+1)^2] matrix parts of the forward scan's group maps (setup)
+  double2* AgB;          // [kScanWarps][KU^2]     ... of the backward scan's
 };
 
 __device__ __forceinline__ double2 seg_rhs(const double2* b, const double* bp, int n, int k) {
@@ -290,10 +292,14 @@ __host__ __device__ constexpr size_t seg_scan2_smem() {
                             (size_t)kScanWarps * DM);                           // group incoming states
 }
 
-template <int DM, int BWD>
+// AG, PRE: the matrix part A_g of every group map depends only on the factorisation, not on the right-hand
+// side.  PRE = 1 (once at setup, ct = zeros): phase 1 composes (A, b) as matrix products and stores A_g to AG.
+// PRE = 0 (every solve): phase 1 runs only the vector recurrence b <- M b + c (the same arithmetic as the b part
+// of the composition, so the same bits) and reads A_g from AG: DM-fold less work in the kernel's longest phase.
+template <int DM, int BWD, int PRE = 0>
 __global__ void __launch_bounds__(kScanWarps * 32) k_seg_scan2(const double2* __restrict__ Mt,
                                                                const double2* __restrict__ ct, double2* __restrict__ out,
-                                                               int P) {
+                                                               int P, double2* __restrict__ AG) {
   constexpr int DD = DM * DM, PER = DD + DM;
   extern __shared__ __align__(16) double2 ssm[];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
@@ -315,37 +321,61 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_seg_scan2(const double2* __
   };
   // phase 1: (A, b) <- (M A, M b + c) over the group's steps
   for (int t = t0; t < t0 + kScanRing - 1; ++t) issue(t);
-  for (int e = lane; e < PER; e += 32) ab[e] = cmk(e < DD && e / DM == e % DM ? 1.0 : 0.0, 0.0);
-  __syncwarp();
-  int cur = 0;
-  for (int t = t0; t < t1; ++t) {
-    cp_async_wait<kScanRing - 2>();
+  if (PRE) {
+    for (int e = lane; e < PER; e += 32) ab[e] = cmk(e < DD && e / DM == e % DM ? 1.0 : 0.0, 0.0);
     __syncwarp();
-    issue(t + kScanRing - 1);
-    const double2* M = ring + (size_t)((t - t0) % kScanRing) * PER;
-    const double2* A = ab + cur * PER;
-    double2* An = ab + (cur ^ 1) * PER;
-    for (int e = lane; e < PER; e += 32) {
-      double2 v;
-      if (e < DD) {  // (M A)(r, c)
-        const int r = e / DM, c = e % DM;
-        v = cmk(0.0, 0.0);
+    int cur = 0;
+    for (int t = t0; t < t1; ++t) {
+      cp_async_wait<kScanRing - 2>();
+      __syncwarp();
+      issue(t + kScanRing - 1);
+      const double2* M = ring + (size_t)((t - t0) % kScanRing) * PER;
+      const double2* A = ab + cur * PER;
+      double2* An = ab + (cur ^ 1) * PER;
+      for (int e = lane; e < PER; e += 32) {
+        double2 v;
+        if (e < DD) {  // (M A)(r, c)
+          const int r = e / DM, c = e % DM;
+          v = cmk(0.0, 0.0);
 #pragma unroll
-        for (int k = 0; k < DM; ++k) v = cfma(M[r * DM + k], A[k * DM + c], v);
-      } else {  // (M b + c)(r)
-        const int r = e - DD;
-        v = M[DD + r];
+          for (int k = 0; k < DM; ++k) v = cfma(M[r * DM + k], A[k * DM + c], v);
+        } else {  // (M b + c)(r)
+          const int r = e - DD;
+          v = M[DD + r];
 #pragma unroll
-        for (int k = 0; k < DM; ++k) v = cfma(M[r * DM + k], A[DD + k], v);
+          for (int k = 0; k < DM; ++k) v = cfma(M[r * DM + k], A[DD + k], v);
+        }
+        An[e] = v;
       }
-      An[e] = v;
+      cur ^= 1;
+      __syncwarp();
     }
-    cur ^= 1;
-    __syncwarp();
+    cp_async_wait<0>();
+    for (int e = lane; e < PER; e += 32) agg[(size_t)g * PER + e] = ab[cur * PER + e];
+    for (int e = lane; e < DD; e += 32) AG[(size_t)g * DD + e] = ab[cur * PER + e];
+  } else {
+    // b <- M b + c, lane r owns component r (M's vector part is c); A_g comes from the setup pass
+    double2 bv = cmk(0.0, 0.0);
+    for (int t = t0; t < t1; ++t) {
+      cp_async_wait<kScanRing - 2>();
+      __syncwarp();
+      issue(t + kScanRing - 1);
+      const double2* M = ring + (size_t)((t - t0) % kScanRing) * PER;
+      double2 nx = lane < DM ? M[DD + lane] : cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < DM; ++k) {
+        const double2 bk = cmk(__shfl_sync(0xffffffffu, bv.x, k), __shfl_sync(0xffffffffu, bv.y, k));
+        if (lane < DM) nx = cfma(M[lane * DM + k], bk, nx);
+      }
+      bv = nx;
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+    for (int e = lane; e < DD; e += 32) agg[(size_t)g * PER + e] = __ldg(AG + (size_t)g * DD + e);
+    if (lane < DM) agg[(size_t)g * PER + DD + lane] = bv;
   }
-  cp_async_wait<0>();
-  for (int e = lane; e < PER; e += 32) agg[(size_t)g * PER + e] = ab[cur * PER + e];
   __syncthreads();
+  if (PRE) return;  // the setup pass only wanted the A_g
   // phase 2: group maps in order, lane q owns component q
   if (g == 0) {
     double2 sv = cmk(0.0, 0.0);

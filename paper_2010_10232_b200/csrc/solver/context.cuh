@@ -682,6 +682,35 @@ static void make_segments(ExactSolver& X, const BandLU& f) {
   a.Dl = dalloc<double2>(static_cast<size_t>(P) * W);
   a.X0 = dalloc<double2>(static_cast<size_t>(P) * ku);
   a.Xb = dalloc<double2>(static_cast<size_t>(P + 1) * ku);
+  a.AgF = dalloc<double2>(static_cast<size_t>(kScanWarps) * W * W);
+  a.AgB = dalloc<double2>(static_cast<size_t>(kScanWarps) * ku * ku);
+}
+
+// Setup pass of the two-level scans: the matrix parts of their group maps (k_seg_scan2 PRE = 1)
+template <int KL>
+static void seg_precompute_t(ExactSolver& X) {
+  constexpr int W = KL + 1, KU = 2 * KL;
+  if (seg_scan2_smem<KU>() > 227u * 1024u) return;  // that size uses the sequential scans
+  SegArgs& a = X.seg;
+  smem_optin(reinterpret_cast<const void*>(k_seg_scan2<W, 0, 1>), seg_scan2_smem<W>());
+  smem_optin(reinterpret_cast<const void*>(k_seg_scan2<KU, 1, 1>), seg_scan2_smem<KU>());
+  CK(cudaMemset(a.D, 0, static_cast<size_t>(a.P) * W * sizeof(double2)));
+  CK(cudaMemset(a.X0, 0, static_cast<size_t>(a.P) * KU * sizeof(double2)));
+  k_seg_scan2<W, 0, 1><<<1, kScanWarps * 32, seg_scan2_smem<W>()>>>(a.Ff, a.D, nullptr, a.P, a.AgF);
+  k_seg_scan2<KU, 1, 1><<<1, kScanWarps * 32, seg_scan2_smem<KU>()>>>(a.Hb, a.X0, nullptr, a.P, a.AgB);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+}
+
+static void seg_precompute(ExactSolver& X) {
+  switch (X.kl) {
+    case 1: seg_precompute_t<1>(X); break;
+    case 2: seg_precompute_t<2>(X); break;
+    case 3: seg_precompute_t<3>(X); break;
+    case 4: seg_precompute_t<4>(X); break;
+    case 5: seg_precompute_t<5>(X); break;
+    default: seg_precompute_t<6>(X); break;
+  }
 }
 
 static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 corner) {
@@ -704,6 +733,7 @@ static ExactSolver make_bandlu(const Band& S, const Band& M, double2 c, double2 
   CK(cudaMemcpy(X.piv, f.piv.data(), f.piv.size() * sizeof(int), cudaMemcpyHostToDevice));
   const char* e = std::getenv("HD_SEG");
   if (!(e && std::atoi(e) == 0) && f.kl >= 1 && f.kl <= 6) make_segments(X, f);
+  if (X.seg.P && !X.seg_seqscan) seg_precompute(X);
   return X;
 }
 
@@ -719,7 +749,7 @@ static void free_exact(ExactSolver& X) {
                           static_cast<const void*>(X.seg.Ff), static_cast<const void*>(X.seg.Hb)})
       dfree(const_cast<void*>(p));
     dfree(X.seg.y); dfree(X.seg.x0); dfree(X.seg.D);
-    dfree(X.seg.Dl); dfree(X.seg.X0); dfree(X.seg.Xb);
+    dfree(X.seg.Dl); dfree(X.seg.X0); dfree(X.seg.Xb); dfree(X.seg.AgF); dfree(X.seg.AgB);
   }
   dfree(X.Ainv); dfree(X.dx); dfree(X.dy);
   dfree(X.pfdF); dfree(X.pfdB);
@@ -754,10 +784,10 @@ static void seg_launch_t(cudaStream_t st, const ExactSolver& X, const double2* b
   }
   k_seg_fwd<KL><<<blocks, 32, seg_fwd_smem<KL>(), st>>>(a, b, bp);
   if (seq) k_seg_scan_fwd<KL><<<1, 32, 0, st>>>(a);
-  else k_seg_scan2<W, 0><<<1, kScanWarps * 32, seg_scan2_smem<W>(), st>>>(a.Ff, a.D, a.Dl, a.P);
+  else k_seg_scan2<W, 0><<<1, kScanWarps * 32, seg_scan2_smem<W>(), st>>>(a.Ff, a.D, a.Dl, a.P, a.AgF);
   k_seg_bwd<KL><<<blocks, 32, seg_bwd_smem<KL>(), st>>>(a);
   if (seq) k_seg_scan_bwd<KL><<<1, 32, 0, st>>>(a);
-  else k_seg_scan2<KU, 1><<<1, kScanWarps * 32, seg_scan2_smem<KU>(), st>>>(a.Hb, a.X0, a.Xb, a.P);
+  else k_seg_scan2<KU, 1><<<1, kScanWarps * 32, seg_scan2_smem<KU>(), st>>>(a.Hb, a.X0, a.Xb, a.P, a.AgB);
   k_seg_out<KL><<<std::min((a.n + 255) / 256, 148 * 4), 256, 0, st>>>(a, x, xp);
 }
 
